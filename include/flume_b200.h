@@ -1,0 +1,227 @@
+/* flume_b200.h -- C ABI of the B200-native differentiable MLS-MPM substep.
+ *
+ * This is the drop-in boundary for the reference engine's hot path
+ * (proj/include/flume, header-only C++20).  The reference has no FFI; its
+ * "API" is the set of templated C++ calls below, and each entry point here
+ * replaces one of them for D = 3 (the C++ adapter include/flume/gpu.hpp
+ * re-exposes the reference signatures on top of this ABI):
+ *
+ *   flume_ctx_create / flume_state_upload / flume_state_download
+ *       Scene<3> + SimState<3> hand-off        types.hpp:179-235, scene.hpp:161
+ *   flume_substep                               mpm_substep      mpm.hpp:455-473
+ *   flume_stage_grid                            p2g + grid_update mpm.hpp:249-320
+ *   flume_adjoint_substep                       adjoint_substep  adjoint.hpp:476-548
+ *   flume_rollout_loss                          rollout_loss     grad.hpp:15-41
+ *   flume_grad_trajectory                       grad_trajectory  grad.hpp:61-134
+ *                                               (+ CheckpointStore checkpoint.hpp:11-50)
+ *   flume_set_mode                              SimConfig::hard_contact types.hpp:65
+ *   flume_last_error                            EngineError hierarchy core.hpp:18-48
+ *   flume_scene_build_json (+ accessors)        build_scene<3>   scene.hpp:161-408
+ *
+ * Conventions: plain pointers and sizes, no C++ or torch types; particle
+ * arrays are in the reference's particle index order ("id"), row-major per
+ * particle (x,v: n*3; F,C: n*9).  Every call returns a flume_status; on
+ * failure flume_last_error() carries the reference exception's context.
+ * A context is single-threaded; distinct contexts are
+ * independent.  Execution is always deterministic: reruns are bit-identical.
+ */
+#ifndef FLUME_B200_H
+#define FLUME_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLUME_B200_ABI_VERSION 1
+
+typedef enum {
+    FLUME_OK = 0,
+    FLUME_E_ENGINE = 1,      /* EngineError        core.hpp:18 */
+    FLUME_E_SCENE = 2,       /* SceneError         core.hpp:22 */
+    FLUME_E_DEGENERATE = 3,  /* DegenerateDeformation core.hpp:26 (particle_id) */
+    FLUME_E_RIGIDITY = 4,    /* RigidityError      core.hpp:32 (body_id) */
+    FLUME_E_ADJOINT = 5,     /* AdjointError       core.hpp:44 (substep) */
+    FLUME_E_SOLVER = 6,      /* SolverError        core.hpp:38 */
+    FLUME_E_CUDA = 7,        /* device / driver failure */
+    FLUME_E_ARG = 8,         /* invalid argument */
+    FLUME_E_OTHER = 9
+} flume_status;
+
+typedef struct flume_ctx flume_ctx;
+typedef struct flume_scene flume_scene;
+
+/* SimConfig<3> (types.hpp:53-95) */
+typedef struct {
+    int grid_resolution;
+    double domain[3];
+    double dt_substep;
+    int substeps_per_step;
+    double gravity[3];
+    int boundary_width;
+    double contact_eps_cells;
+    double cfl_fraction;
+    double mass_epsilon;
+    int hard_contact;
+} flume_config;
+
+/* MaterialParams (types.hpp:32-51); kind numbering = MaterialKind */
+typedef struct {
+    int kind;
+    double mu, lambda, rho;
+    double theta_c, theta_s, sigma_y;
+} flume_material;
+
+/* static part of Effector<3> (types.hpp:114-125, sdf.hpp:37-73);
+ * shape_kind numbering = ShapeKind; friction_mu = +inf means sticky */
+typedef struct {
+    int shape_kind;
+    double radius;
+    double half_extents[3];
+    double seg_a[3], seg_b[3];
+    double plane_normal[3];
+    double plane_offset;
+    double half_height;
+    double shape_t[3];
+    double shape_R[9];
+    double friction_mu;
+    int action_mask[6];
+} flume_effector_shape;
+
+/* dynamic part of Effector<3> */
+typedef struct {
+    double pose_t[3];
+    double pose_R[9];
+    double linear_velocity[3];
+    double angular_velocity[3];
+} flume_effector_state;
+
+/* RigidBodyRef<3> (types.hpp:218-224) */
+typedef struct {
+    int body_id;
+    long n_members;
+    const long* members;
+    const double* rest_offsets; /* n_members*3 */
+    double total_mass;
+} flume_rigid_body;
+
+/* EmitterSpawn<3> (types.hpp:209-215) */
+typedef struct {
+    long particle;
+    int effector;
+    double local_pos[3];
+    double local_vel[3];
+} flume_emitter;
+
+/* Scene<3> plus the immutable per-particle fields of SimState<3> */
+typedef struct {
+    flume_config config;
+    int n_materials;
+    const flume_material* materials;
+    int n_effectors;
+    const flume_effector_shape* effectors;
+    int n_rigid;
+    const flume_rigid_body* rigid;
+    long n_emitters;
+    const flume_emitter* emitters;
+    long n_particles;
+    const int* material_id;
+    const int* body_id;
+    const double* mass;
+    const double* volume0;
+    const long* activation_substep;
+} flume_scene_desc;
+
+/* mutable part of SimState<3> */
+typedef struct {
+    double time;
+    long substep_index;
+    double* x; /* n*3 */
+    double* v; /* n*3 */
+    double* F; /* n*9 */
+    double* C; /* n*9 */
+    flume_effector_state* effectors; /* n_effectors */
+} flume_state_view;
+
+/* LossEvaluator terms supported on device (losses.hpp:474-551) */
+typedef enum { FLUME_LOSS_TARGET_POINT = 0, FLUME_LOSS_HOLD_INITIAL = 1 } flume_loss_kind;
+typedef struct {
+    int kind;
+    int body;
+    double weight;
+    int squared;
+    int final_only;
+    double goal[3];
+} flume_loss_term;
+typedef struct {
+    int n_terms;
+    const flume_loss_term* terms;
+} flume_loss_desc;
+
+/* ActionTrajectory (actions.hpp:13-39): values = n_segments*6 */
+typedef struct {
+    int n_segments;
+    int segment_length;
+    const double* values;
+} flume_actions;
+
+typedef struct {
+    int code;
+    long particle_id;
+    int body_id;
+    long substep;
+    char message[256];
+} flume_error_info;
+
+/* per-call timing breakdown (device ms, CUDA events on the context stream) */
+typedef struct {
+    double forward_ms;
+    double backward_ms;
+    long substeps;
+    long particle_substeps;
+    long launches;
+} flume_timing;
+
+int flume_abi_version(void);
+
+/* ---- scene construction (build_scene<3>, scene.hpp:161-408) ---- */
+int flume_scene_build_json(const char* json_text, flume_scene** out);
+int flume_scene_free(flume_scene* s);
+int flume_scene_desc_get(const flume_scene* s, flume_scene_desc* out); /* pointers owned by s */
+int flume_scene_state_get(const flume_scene* s, flume_state_view* out); /* initial state, owned by s */
+int flume_scene_loss_get(const flume_scene* s, flume_loss_desc* out);
+int flume_scene_optimizer_get(const flume_scene* s, int* n_segments, int* segment_length, double* init6);
+
+/* ---- context ---- */
+int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out);
+int flume_ctx_destroy(flume_ctx* ctx);
+int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact);
+int flume_last_error(const flume_ctx* ctx, flume_error_info* info);
+int flume_get_stream(flume_ctx* ctx, void** cuda_stream);
+int flume_sync(flume_ctx* ctx);
+int flume_last_timing(const flume_ctx* ctx, flume_timing* out);
+
+/* ---- state hand-off ---- */
+int flume_state_upload(flume_ctx* ctx, const flume_state_view* view);
+int flume_state_download(flume_ctx* ctx, flume_state_view* view);
+/* canonical store order: cell keys, particle ids and active count (n entries each) */
+int flume_store_order(flume_ctx* ctx, unsigned* keys, unsigned* ids, long* n_active);
+/* fp32 positions in store order (for the bit-exact key/order check) */
+int flume_store_positions(flume_ctx* ctx, float* x);
+
+/* ---- hot path ---- */
+int flume_substep(flume_ctx* ctx, const double action[6], int count);
+int flume_stage_grid(flume_ctx* ctx, double* mass, double* vel); /* dense (i*ny+j)*nz+k order */
+int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long window,
+                       double* loss_out, double* per_segment);
+int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long stride,
+                          long window, double* action_grad, double* loss_out, double* full_loss,
+                          double* per_segment, long* snapshots);
+int flume_adjoint_substep(flume_ctx* ctx, const double action[6], double* x_bar, double* v_bar, double* F_bar,
+                          double* C_bar, double* eff_bars /* n_eff*12: t_bar[3], R_bar[9] */,
+                          double* action_bar);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLUME_B200_H */

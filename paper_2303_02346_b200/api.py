@@ -1,0 +1,566 @@
+"""Host-side mirror of the reference's scene / step / grad API (D = 3).
+
+Names, argument meaning and error behaviour follow proj/include/flume:
+
+    build_scene(spec)                               scene.hpp:161   -> World
+    mpm_substep(scene, state, action, ws)           mpm.hpp:455
+    p2g_grid(scene, state, ws)                      mpm.hpp:249 + :301 (p2g then grid_update)
+    adjoint_substep(scene, rec, adj, action_bar, ws) adjoint.hpp:476
+    rollout_loss(scene, state0, actions, loss, window, per_segment)   grad.hpp:15
+    grad_trajectory(scene, state0, actions, loss, stride, window)     grad.hpp:61
+    ActionTrajectory, LossEvaluator, TrajectoryGrad, AdjointState, SubstepRecord
+
+`ws` is a GpuWorkspace (the MpmWorkspace analogue): it owns the device
+context, and the SimState stays resident in HBM between calls -- host arrays
+are only copied back when read.  Errors raise the reference's exception
+types (core.hpp:18-48).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json as _json
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import load
+
+# ---------------------------------------------------------------------------
+# exceptions (core.hpp:18-48)
+# ---------------------------------------------------------------------------
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+class SceneError(EngineError):
+    pass
+
+
+class DegenerateDeformation(EngineError):
+    def __init__(self, msg, particle_id=-1):
+        super().__init__(msg)
+        self.particle_id = particle_id
+
+
+class RigidityError(EngineError):
+    def __init__(self, msg, body_id=-1):
+        super().__init__(msg)
+        self.body_id = body_id
+
+
+class AdjointError(EngineError):
+    def __init__(self, msg, substep=-1):
+        super().__init__(msg)
+        self.substep = substep
+
+
+class SolverError(EngineError):
+    pass
+
+
+class DeviceError(EngineError):
+    pass
+
+
+def _raise(lib, ctx, rc):
+    if rc == _abi.FLUME_OK:
+        return
+    info = _abi.ErrorInfo()
+    lib.flume_last_error(ctx, C.byref(info))
+    msg = info.message.decode(errors="replace")
+    if rc == _abi.FLUME_E_SCENE:
+        raise SceneError(msg)
+    if rc == _abi.FLUME_E_DEGENERATE:
+        raise DegenerateDeformation(msg, info.particle_id)
+    if rc == _abi.FLUME_E_RIGIDITY:
+        raise RigidityError(msg, info.body_id)
+    if rc == _abi.FLUME_E_ADJOINT:
+        raise AdjointError(msg, info.substep)
+    if rc == _abi.FLUME_E_SOLVER:
+        raise SolverError(msg)
+    if rc == _abi.FLUME_E_CUDA:
+        raise DeviceError(msg)
+    if rc == _abi.FLUME_E_ARG:
+        raise ValueError(msg)
+    raise EngineError(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ---------------------------------------------------------------------------
+# data model
+# ---------------------------------------------------------------------------
+
+MATERIAL_KINDS = ["elastic", "plastic", "liquid", "viscous_liquid", "non_newtonian", "rigid"]
+SHAPE_KINDS = ["sphere", "box", "capsule", "cylinder", "halfspace"]
+
+
+class Scene:
+    """Immutable scene data (types.hpp:227-235) as a flume_scene_desc.
+
+    Owns the ctypes arrays the descriptor points to."""
+
+    def __init__(self, desc: _abi.SceneDesc, keepalive):
+        self.desc = desc
+        self._keep = keepalive
+        c = desc.config
+        self.grid_resolution = c.grid_resolution
+        self.domain = tuple(c.domain)
+        self.dt_substep = c.dt_substep
+        self.gravity = tuple(c.gravity)
+        self.dx = c.domain[0] / c.grid_resolution
+        self.n_particles = desc.n_particles
+        n = desc.n_particles
+        self.material_id = np.ctypeslib.as_array(desc.material_id, (n,)).copy()
+        self.body_id = np.ctypeslib.as_array(desc.body_id, (n,)).copy()
+        self.mass = np.ctypeslib.as_array(desc.mass, (n,)).copy()
+        self.volume0 = np.ctypeslib.as_array(desc.volume0, (n,)).copy()
+        self.activation_substep = np.ctypeslib.as_array(desc.activation_substep, (n,)).copy()
+        self.materials = [desc.materials[i] for i in range(desc.n_materials)]
+        self.n_effectors = desc.n_effectors
+
+    @property
+    def node_dims(self):
+        return tuple(int(round(self.domain[a] / self.dx)) + 1 for a in range(3))
+
+
+class SimState:
+    """SimState<3> (types.hpp:179-205) with lazy host/device synchronisation."""
+
+    def __init__(self, x, v, F, C_, effectors, time=0.0, substep_index=0):
+        self._x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 3)
+        self._v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1, 3)
+        self._F = np.ascontiguousarray(F, dtype=np.float64).reshape(-1, 3, 3)
+        self._C = np.ascontiguousarray(C_, dtype=np.float64).reshape(-1, 3, 3)
+        self._eff = np.ascontiguousarray(effectors, dtype=np.float64).reshape(-1, 18)
+        self._time = float(time)
+        self._substep = int(substep_index)
+        self._ws: Optional["GpuWorkspace"] = None  # workspace holding the newer copy
+
+    # host views pull the device copy first and make the host authoritative
+    def _pull(self):
+        if self._ws is not None:
+            self._ws._download(self)
+            self._ws._resident = None
+            self._ws = None
+
+    def copy(self) -> "SimState":
+        self._pull()
+        return SimState(self._x.copy(), self._v.copy(), self._F.copy(), self._C.copy(), self._eff.copy(),
+                        self._time, self._substep)
+
+    @property
+    def n_particles(self):
+        return self._x.shape[0]
+
+    def _prop(name):  # noqa: N805
+        def get(self):
+            self._pull()
+            return getattr(self, name)
+
+        def set_(self, val):
+            self._pull()
+            getattr(self, name)[...] = val
+
+        return property(get, set_)
+
+    x = _prop("_x")
+    v = _prop("_v")
+    F = _prop("_F")
+    C = _prop("_C")
+    effectors = _prop("_eff")
+
+    @property
+    def time(self):
+        return self._time
+
+    @property
+    def substep_index(self):
+        return self._substep
+
+    @substep_index.setter
+    def substep_index(self, v):
+        self._pull()
+        self._substep = int(v)
+
+    def active_particle_count(self, scene: Scene) -> int:
+        return int(np.sum(scene.activation_substep <= self.substep_index))
+
+
+@dataclass
+class World:
+    scene: Scene
+    state: SimState
+    loss_spec: list
+    n_segments: int
+    segment_length: int
+    init_action: np.ndarray
+    spec: dict
+
+
+def build_scene(spec) -> World:
+    """build_scene<3> (scene.hpp:161) through the library's JSON builder."""
+    lib = load()
+    text = spec if isinstance(spec, str) else _json.dumps(spec)
+    h = C.c_void_p()
+    rc = lib.flume_scene_build_json(text.encode(), C.byref(h))
+    if rc != _abi.FLUME_OK:
+        msg = lib.flume_scene_error(h).decode() if h else "scene error"
+        lib.flume_scene_free(h)
+        raise SceneError(msg)
+    try:
+        desc = _abi.SceneDesc()
+        lib.flume_scene_desc_get(h, C.byref(desc))
+        keep = _copy_desc(desc)
+        view = _abi.StateView()
+        lib.flume_scene_state_get(h, C.byref(view))
+        n = desc.n_particles
+        x = np.ctypeslib.as_array(view.x, (n, 3)).copy()
+        v = np.ctypeslib.as_array(view.v, (n, 3)).copy()
+        F = np.ctypeslib.as_array(view.F, (n, 9)).copy()
+        Cm = np.ctypeslib.as_array(view.C, (n, 9)).copy()
+        eff = np.zeros((desc.n_effectors, 18))
+        for i in range(desc.n_effectors):
+            e = view.effectors[i]
+            eff[i] = list(e.pose_t) + list(e.pose_R) + list(e.linear_velocity) + list(e.angular_velocity)
+        ld = _abi.LossDesc()
+        lib.flume_scene_loss_get(h, C.byref(ld))
+        terms = [_term_dict(ld.terms[i]) for i in range(ld.n_terms)]
+        ns, sl = C.c_int(), C.c_int()
+        init = np.zeros(6)
+        lib.flume_scene_optimizer_get(h, C.byref(ns), C.byref(sl), _dp(init))
+    finally:
+        lib.flume_scene_free(h)
+    scene = Scene(keep[0], keep)
+    state = SimState(x, v, F, Cm, eff)
+    return World(scene, state, terms, ns.value, sl.value, init,
+                 spec if isinstance(spec, dict) else _json.loads(text))
+
+
+def _term_dict(t: _abi.LossTerm) -> dict:
+    return {"kind": ["target_point", "hold_initial"][t.kind], "body": t.body, "weight": t.weight,
+            "squared": bool(t.squared), "final_only": bool(t.final_only), "goal": list(t.goal)}
+
+
+def _copy_desc(d: _abi.SceneDesc):
+    """Deep-copy a descriptor into Python-owned ctypes arrays."""
+    keep = []
+
+    def arr(ctype, src, n):
+        a = (ctype * max(n, 1))()
+        if n:
+            C.memmove(a, src, C.sizeof(ctype) * n)
+        keep.append(a)
+        return C.cast(a, C.POINTER(ctype))
+
+    out = _abi.SceneDesc()
+    out.config = d.config
+    out.n_materials = d.n_materials
+    out.materials = arr(_abi.Material, d.materials, d.n_materials)
+    out.n_effectors = d.n_effectors
+    out.effectors = arr(_abi.EffectorShape, d.effectors, d.n_effectors)
+    out.n_rigid = d.n_rigid
+    rbs = (_abi.RigidBody * max(d.n_rigid, 1))()
+    for i in range(d.n_rigid):
+        r = d.rigid[i]
+        rbs[i].body_id = r.body_id
+        rbs[i].n_members = r.n_members
+        rbs[i].members = arr(C.c_long, r.members, r.n_members)
+        rbs[i].rest_offsets = arr(C.c_double, r.rest_offsets, 3 * r.n_members)
+        rbs[i].total_mass = r.total_mass
+    keep.append(rbs)
+    out.rigid = C.cast(rbs, C.POINTER(_abi.RigidBody))
+    out.n_emitters = d.n_emitters
+    out.emitters = arr(_abi.Emitter, d.emitters, d.n_emitters)
+    n = d.n_particles
+    out.n_particles = n
+    out.material_id = arr(C.c_int, d.material_id, n)
+    out.body_id = arr(C.c_int, d.body_id, n)
+    out.mass = arr(C.c_double, d.mass, n)
+    out.volume0 = arr(C.c_double, d.volume0, n)
+    out.activation_substep = arr(C.c_long, d.activation_substep, n)
+    return [out] + keep
+
+
+@dataclass
+class ActionTrajectory:
+    """actions.hpp:13-39: one Action6 per segment."""
+    n_segments: int = 1
+    segment_length: int = 1
+    values: np.ndarray = None
+
+    def __post_init__(self):
+        if self.values is None:
+            self.values = np.zeros((self.n_segments, 6))
+        self.values = np.ascontiguousarray(self.values, dtype=np.float64).reshape(self.n_segments, 6)
+
+    def horizon(self) -> int:
+        return self.n_segments * self.segment_length
+
+    def segment_of(self, t: int) -> int:
+        return t // self.segment_length
+
+    def at_substep(self, t: int):
+        return self.values[self.segment_of(t)]
+
+    def _c(self):
+        a = _abi.Actions()
+        a.n_segments = self.n_segments
+        a.segment_length = self.segment_length
+        a.values = _dp(self.values)
+        return a
+
+
+class LossEvaluator:
+    """Device-evaluable LossEvaluator (losses.hpp:306): target_point and
+    hold_initial terms, optionally composite."""
+
+    def __init__(self, scene: Optional[Scene] = None, spec=None, state0: Optional[SimState] = None):
+        terms = spec if isinstance(spec, list) else ([] if spec is None else self._parse(spec))
+        if not terms:
+            raise SceneError("scene has no loss specification")
+        self.terms = terms
+        self._arr = (_abi.LossTerm * len(terms))()
+        for i, t in enumerate(terms):
+            k = {"target_point": 0, "hold_initial": 1}[t["kind"]]
+            self._arr[i].kind = k
+            self._arr[i].body = int(t["body"])
+            self._arr[i].weight = float(t.get("weight", 1.0))
+            self._arr[i].squared = int(bool(t.get("squared", False)))
+            self._arr[i].final_only = int(bool(t.get("final_only", False)))
+            g = t.get("goal", [0, 0, 0])
+            for a in range(3):
+                self._arr[i].goal[a] = float(g[a])
+        self.desc = _abi.LossDesc(len(terms), C.cast(self._arr, C.POINTER(_abi.LossTerm)))
+
+    @staticmethod
+    def _parse(spec: dict):
+        def one(t):
+            return {"kind": t.get("kind", "target_point"), "body": t["body"], "weight": t.get("weight", 1.0),
+                    "squared": t.get("squared", False), "final_only": t.get("eval", "per_step") == "final",
+                    "goal": t.get("goal", [0, 0, 0])}
+        if spec.get("kind") == "composite":
+            return [one(t) for t in spec["terms"]]
+        return [one(spec)]
+
+
+@dataclass
+class TrajectoryGrad:
+    loss: float = 0.0
+    full_loss: float = 0.0
+    per_segment: List[float] = field(default_factory=list)
+    action_grad: np.ndarray = None
+    snapshots: int = 0
+    forward_ms: float = 0.0
+    backward_ms: float = 0.0
+
+    def flatten(self):
+        return self.action_grad.reshape(-1).tolist()
+
+
+@dataclass
+class AdjointState:
+    """Cotangents of a SimState (adjoint.hpp:9-46), reference particle order."""
+    x_bar: np.ndarray
+    v_bar: np.ndarray
+    F_bar: np.ndarray
+    C_bar: np.ndarray
+    eff_bars: np.ndarray  # n_eff x 12: t_bar[3], R_bar[9]
+
+    @staticmethod
+    def init(state: SimState) -> "AdjointState":
+        n = state.n_particles
+        return AdjointState(np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 3, 3)), np.zeros((n, 3, 3)),
+                            np.zeros((state._eff.shape[0], 12)))
+
+
+@dataclass
+class SubstepRecord:
+    index: int
+    action: Sequence[float]
+    pre_state: SimState
+
+
+# ---------------------------------------------------------------------------
+# workspace = device context
+# ---------------------------------------------------------------------------
+
+
+class GpuWorkspace:
+    """Device context for one scene (MpmWorkspace analogue, mpm.hpp:223-238)."""
+
+    def __init__(self, scene: Scene, device: int = 0):
+        self.lib = load()
+        self.scene = scene
+        self.ctx = C.c_void_p()
+        rc = self.lib.flume_ctx_create(C.byref(scene.desc), device, C.byref(self.ctx))
+        if rc != _abi.FLUME_OK:
+            _raise(self.lib, None, rc)
+        self._resident: Optional[SimState] = None
+        self._ctx_time = 0.0
+        self._ctx_substep = 0
+
+    def close(self):
+        if self.ctx:
+            if self._resident is not None:
+                self._resident._pull()
+            self.lib.flume_ctx_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        _raise(self.lib, self.ctx, rc)
+
+    def _view(self, st: SimState, effs):
+        v = _abi.StateView()
+        v.time = st._time
+        v.substep_index = st._substep
+        v.x, v.v, v.F, v.C = _dp(st._x), _dp(st._v), _dp(st._F), _dp(st._C)
+        v.effectors = effs
+        return v
+
+    @staticmethod
+    def _eff_to_c(eff):
+        arr = (_abi.EffectorState * max(len(eff), 1))()
+        for i, e in enumerate(eff):
+            arr[i].pose_t[:] = list(e[0:3])
+            arr[i].pose_R[:] = list(e[3:12])
+            arr[i].linear_velocity[:] = list(e[12:15])
+            arr[i].angular_velocity[:] = list(e[15:18])
+        return arr
+
+    def _upload(self, st: SimState):
+        if self._resident is st:
+            return
+        if self._resident is not None:
+            self._resident._pull()
+        st._pull()
+        effs = self._eff_to_c(st._eff)
+        self._check(self.lib.flume_state_upload(self.ctx, C.byref(self._view(st, effs))))
+        self._resident = st
+        self._ctx_time = st._time
+        self._ctx_substep = st._substep
+
+    def _download(self, st: SimState):
+        effs = (_abi.EffectorState * max(len(st._eff), 1))()
+        v = self._view(st, effs)
+        self._check(self.lib.flume_state_download(self.ctx, C.byref(v)))
+        for i in range(len(st._eff)):
+            e = effs[i]
+            st._eff[i] = list(e.pose_t) + list(e.pose_R) + list(e.linear_velocity) + list(e.angular_velocity)
+        st._time = v.time
+        st._substep = v.substep_index
+
+    def _mark_device_newer(self, st: SimState):
+        st._ws = self
+        self._resident = st
+
+    def store_order(self, st: SimState):
+        """Canonical store order (cell keys, particle ids, active count) + fp32 positions."""
+        self._upload(st)
+        n = self.scene.n_particles
+        keys = np.zeros(n, np.uint32)
+        ids = np.zeros(n, np.uint32)
+        na = C.c_long()
+        self._check(self.lib.flume_store_order(self.ctx, keys.ctypes.data_as(C.POINTER(C.c_uint)),
+                                               ids.ctypes.data_as(C.POINTER(C.c_uint)), C.byref(na)))
+        xs = np.zeros(3 * n, np.float32)
+        self._check(self.lib.flume_store_positions(self.ctx, xs.ctypes.data_as(C.POINTER(C.c_float))))
+        return keys, ids, na.value, xs.reshape(3, n)
+
+    def last_timing(self):
+        t = _abi.Timing()
+        self.lib.flume_last_timing(self.ctx, C.byref(t))
+        return t
+
+
+def _ws_for(scene: Scene, ws: Optional[GpuWorkspace]) -> GpuWorkspace:
+    if ws is None:
+        raise ValueError("a GpuWorkspace is required (MpmWorkspace analogue)")
+    if ws.scene is not scene:
+        raise ValueError("workspace belongs to a different scene")
+    return ws
+
+
+# ---------------------------------------------------------------------------
+# API
+# ---------------------------------------------------------------------------
+
+
+def mpm_substep(scene: Scene, state: SimState, action, ws: GpuWorkspace, count: int = 1) -> None:
+    """mpm.hpp:455-473 (count > 1 chains substeps without host round trips)."""
+    ws = _ws_for(scene, ws)
+    ws._upload(state)
+    a = np.ascontiguousarray(action, dtype=np.float64)
+    ws._check(ws.lib.flume_substep(ws.ctx, _dp(a), int(count)))
+    ws._ctx_time = state._time + count * scene.dt_substep
+    ws._ctx_substep = state._substep + count
+    state._time, state._substep = ws._ctx_time, ws._ctx_substep
+    ws._mark_device_newer(state)
+
+
+def p2g_grid(scene: Scene, state: SimState, ws: GpuWorkspace):
+    """p2g + grid_update on a state (mpm.hpp:249, :301); dense mass and velocity grids."""
+    ws = _ws_for(scene, ws)
+    ws._upload(state)
+    nd = scene.node_dims
+    mass = np.zeros(nd)
+    vel = np.zeros(nd + (3,))
+    ws._check(ws.lib.flume_stage_grid(ws.ctx, _dp(mass), _dp(vel)))
+    return mass, vel
+
+
+def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss: LossEvaluator,
+                 window: int = 0, per_segment: Optional[list] = None, ws: Optional[GpuWorkspace] = None) -> float:
+    """grad.hpp:15-41."""
+    ws = _ws_for(scene, ws)
+    ws._upload(state0)
+    out = C.c_double()
+    per = np.zeros(actions.n_segments)
+    a = actions._c()
+    ws._check(ws.lib.flume_rollout_loss(ws.ctx, C.byref(a), C.byref(loss.desc), int(window), C.byref(out),
+                                        _dp(per)))
+    if per_segment is not None:
+        per_segment[:] = per.tolist()
+    return out.value
+
+
+def grad_trajectory(scene: Scene, state0: SimState, actions: ActionTrajectory, loss: LossEvaluator,
+                    stride: int = 0, window: int = 0, ws: Optional[GpuWorkspace] = None) -> TrajectoryGrad:
+    """grad.hpp:61-134 (checkpoint stride semantics of checkpoint.hpp:11-50)."""
+    ws = _ws_for(scene, ws)
+    ws._upload(state0)
+    g = np.zeros((actions.n_segments, 6))
+    lo, fl, snaps = C.c_double(), C.c_double(), C.c_long()
+    per = np.zeros(actions.n_segments)
+    a = actions._c()
+    ws._check(ws.lib.flume_grad_trajectory(ws.ctx, C.byref(a), C.byref(loss.desc), int(stride), int(window), _dp(g),
+                                           C.byref(lo), C.byref(fl), _dp(per), C.byref(snaps)))
+    t = ws.last_timing()
+    return TrajectoryGrad(lo.value, fl.value, per.tolist(), g, snaps.value, t.forward_ms, t.backward_ms)
+
+
+def adjoint_substep(scene: Scene, rec: SubstepRecord, adj: AdjointState, action_bar: np.ndarray,
+                    ws: GpuWorkspace) -> None:
+    """adjoint.hpp:476-548: bars of the post-state -> bars of rec.pre_state (in place)."""
+    ws = _ws_for(scene, ws)
+    ws._upload(rec.pre_state)
+    act = np.ascontiguousarray(rec.action, dtype=np.float64)
+    for name in ("x_bar", "v_bar", "F_bar", "C_bar", "eff_bars"):
+        setattr(adj, name, np.ascontiguousarray(getattr(adj, name), dtype=np.float64))
+    ab = np.ascontiguousarray(action_bar, dtype=np.float64)
+    eb = adj.eff_bars if adj.eff_bars.size else np.zeros((1, 12))
+    ws._check(ws.lib.flume_adjoint_substep(ws.ctx, _dp(act), _dp(adj.x_bar), _dp(adj.v_bar), _dp(adj.F_bar),
+                                           _dp(adj.C_bar), _dp(eb), _dp(ab)))
+    action_bar[...] = ab

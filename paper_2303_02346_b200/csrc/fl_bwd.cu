@@ -1,0 +1,649 @@
+// fl_bwd.cu -- reverse-mode MLS-MPM substep kernels for sm_100a.
+//
+// Mirrors adjoint_substep (proj/include/flume/adjoint.hpp:476-548) without the
+// reference's capture_forward re-run: the pre-state of the substep is read from
+// the trajectory store, the forward grid is rebuilt by one P2G + grid update,
+// and then
+//   adjoint_rigid_pass   (adjoint.hpp:210-279)   k_adj_rigid_*
+//   adjoint_g2p          (adjoint.hpp:281-365)   k_adj_g2p   (gather + scatter of grid v_bar)
+//   adjoint_grid_update  (adjoint.hpp:367-412)   k_adj_grid  (+ deterministic effector-bar reduction)
+//   adjoint_p2g          (adjoint.hpp:414-470)   k_adj_p2g
+//   emitter adjoint      (adjoint.hpp:503-520)   k_adj_emit
+// Bars of state[t+1] are indexed by sorted position j (= storage slot of
+// state[t+1]); bars of state[t] are written at the storage slot perm[j].
+#include <cuda_runtime.h>
+
+#include "fl_kernels.h"
+#include "fl_scatter.cuh"
+
+namespace fl {
+
+// ---------------------------------------------------------------------------
+// loss cotangent injection at segment boundaries (losses.hpp:506-525)
+// ---------------------------------------------------------------------------
+__global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, LossSet ls, uint32_t mask,
+                            uint32_t key_inactive, BarBuf bars) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int body = cls[st.meta[i]].body;
+    const bool active = st.key[i] != key_inactive;
+    double g[3] = {0.0, 0.0, 0.0};
+    bool any = false;
+    for (int k = 0; k < ls.n; k++) {
+        if (!((mask >> k) & 1u) || ls.t[k].body != body) continue;
+        const LossTermDev& t = ls.t[k];
+        double d[3];
+        if (t.kind == LK_TARGET) {
+            if (!active) continue;
+            for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - t.goal[a];
+        } else {
+            const uint32_t id = st.id[i];
+            for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - double(t.init[3 * size_t(id) + a]);
+        }
+        const double nn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        if (t.kind == LK_TARGET && t.squared) {
+            for (int a = 0; a < 3; a++) g[a] += d[a] * (2.0 * t.weight);
+            any = true;
+        } else if (nn > 1e-300) {
+            for (int a = 0; a < 3; a++) g[a] += d[a] * (t.weight / nn);
+            any = true;
+        }
+    }
+    if (any)
+        for (int a = 0; a < 3; a++) bars.x(a)[i] += float(g[a]);
+}
+
+void launch_loss_grad(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, BarBuf bars,
+                      uint32_t key_inactive, cudaStream_t s) {
+    if (n <= 0) return;
+    k_loss_grad<<<(n + 255) / 256, 256, 0, s>>>(st, n, cls, ls, mask, key_inactive, bars);
+}
+
+// ---------------------------------------------------------------------------
+// rigid pass adjoint (adjoint.hpp:210-279)
+// ---------------------------------------------------------------------------
+constexpr int kAdjRigidQ = 12;  // r_bar[9], c_bar[3]
+
+__global__ void __launch_bounds__(256) k_adj_rigid_partial(Geom g, BarBuf post, RigidDev rd, const int* chunk_m0,
+                                                           const int* chunk_m1, double* partial, float* start_bar) {
+    __shared__ double red[256];
+    const int c = blockIdx.x;
+    const int m0 = chunk_m0[c], m1 = chunk_m1[c];
+    double acc[kAdjRigidQ];
+    for (int q = 0; q < kAdjRigidQ; q++) acc[q] = 0.0;
+    for (int r = m0 + threadIdx.x; r < m1; r += 256) {
+        const int body = rd.member_body[r];
+        const double* fit = rd.fit + 24 * size_t(body);
+        if (fit[22] != 0.0) {
+            for (int a = 0; a < 3; a++) start_bar[3 * r + a] = 0.f;
+            continue;
+        }
+        const int j = rd.mslot[r];
+        const double inv_dt = 1.0 / double(g.dt);
+        double xn_bar[3];
+        for (int a = 0; a < 3; a++) {
+            const double xb = post.x(a)[j], vb = post.v(a)[j];
+            xn_bar[a] = xb + vb * inv_dt;
+            start_bar[3 * r + a] = float(-vb * inv_dt);
+            post.x(a)[j] = 0.f;
+            post.v(a)[j] = 0.f;
+        }
+        const double* re = rd.rest + 3 * size_t(r);
+        for (int a = 0; a < 3; a++) {
+            const double raw = fit[3 * a] * re[0] + fit[3 * a + 1] * re[1] + fit[3 * a + 2] * re[2] + fit[9 + a];
+            const double cl = clamp_ref(raw, double(g.lo[a]), double(g.hi[a]));
+            if (raw != cl) xn_bar[a] = 0.0;
+        }
+        for (int a = 0; a < 3; a++)
+            for (int b = 0; b < 3; b++) acc[3 * a + b] += xn_bar[a] * re[b];
+        for (int a = 0; a < 3; a++) acc[9 + a] += xn_bar[a];
+    }
+    for (int q = 0; q < kAdjRigidQ; q++) {
+        red[threadIdx.x] = acc[q];
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) partial[size_t(c) * kAdjRigidQ + q] = red[0];
+        __syncthreads();
+    }
+}
+
+// abar per body: A_bar[9], c_total[3], total
+__global__ void k_adj_rigid_solve(RigidDev rd, int nchunks, const int* chunk_body, const double* partial,
+                                  double* abar) {
+    const int body = blockIdx.x * blockDim.x + threadIdx.x;
+    if (body >= rd.nbody) return;
+    const double* fit = rd.fit + 24 * size_t(body);
+    double* o = abar + 13 * size_t(body);
+    if (fit[22] != 0.0) {
+        for (int q = 0; q < 13; q++) o[q] = 0.0;
+        return;
+    }
+    double s[kAdjRigidQ];
+    for (int q = 0; q < kAdjRigidQ; q++) s[q] = 0.0;
+    for (int c = 0; c < nchunks; c++) {
+        if (chunk_body[c] != body) continue;
+        for (int q = 0; q < kAdjRigidQ; q++) s[q] += partial[size_t(c) * kAdjRigidQ + q];
+    }
+    M3<double> r_bar, A;
+    for (int k = 0; k < 9; k++) {
+        r_bar.m[k] = s[k];
+        A.m[k] = fit[12 + k];
+    }
+    V3<double> c_bar = {s[9], s[10], s[11]};
+    Svd<double> t = svd3(A);
+    M3<double> a_bar;
+    if (det(A) > 0.0) {
+        a_bar = polar_rotation_vjp(t, r_bar);
+    } else {
+        M3<double> flip = mdiag(V3<double>{1.0, 1.0, -1.0});
+        a_bar = svd_vjp(t, r_bar * t.V * flip, V3<double>{0.0, 0.0, 0.0}, transpose(r_bar) * t.U * flip, 1e-8);
+    }
+    V3<double> smr = {rd.smrest[3 * body], rd.smrest[3 * body + 1], rd.smrest[3 * body + 2]};
+    V3<double> ct = c_bar - a_bar * smr;
+    for (int k = 0; k < 9; k++) o[k] = a_bar.m[k];
+    o[9] = ct.x;
+    o[10] = ct.y;
+    o[11] = ct.z;
+    o[12] = fit[21];
+}
+
+__global__ void k_adj_rigid_apply(BarBuf post, RigidDev rd, const double* abar) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rd.nmem) return;
+    const int body = rd.member_body[r];
+    if (rd.fit[24 * size_t(body) + 22] != 0.0) return;
+    const double* o = abar + 13 * size_t(body);
+    const int j = rd.mslot[r];
+    const double* re = rd.rest + 3 * size_t(r);
+    const double m = rd.mass[r];
+    for (int a = 0; a < 3; a++) {
+        const double gv = (o[3 * a] * re[0] + o[3 * a + 1] * re[1] + o[3 * a + 2] * re[2]) * m;
+        post.x(a)[j] += float(gv + o[9 + a] * (m / o[12]));
+    }
+}
+
+void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, const int* chunk_body,
+                      const int* chunk_m0, const int* chunk_m1, double* partial, float* start_bar, double* abar,
+                      cudaStream_t s) {
+    if (rd.nbody == 0) return;
+    k_adj_rigid_partial<<<nchunks, 256, 0, s>>>(g, post, rd, chunk_m0, chunk_m1, partial, start_bar);
+    k_adj_rigid_solve<<<(rd.nbody + 31) / 32, 32, 0, s>>>(rd, nchunks, chunk_body, partial, abar);
+    k_adj_rigid_apply<<<(rd.nmem + 255) / 256, 256, 0, s>>>(post, rd, abar);
+}
+
+// ---------------------------------------------------------------------------
+// G2P adjoint (adjoint.hpp:281-365): gather + deterministic scatter of grid v_bar
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+                                                        const BlockRec* __restrict__ recs,
+                                                        const int* __restrict__ n_blocks,
+                                                        const ClassInfo* __restrict__ cls,
+                                                        const float4* __restrict__ gridv, BarBuf post,
+                                                        float* xbar_tmp, float* Fbar_tmp, RigidDev rd,
+                                                        const float* __restrict__ start_bar, float4* staging_bar,
+                                                        int cap) {
+    __shared__ ScSmem sm;
+    __shared__ float4 vt[kTile];
+    const int tid = threadIdx.x;
+    const int nb = *n_blocks;
+    const int my_c = tid & 63, my_ox = tid >> 6;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const BlockRec r = recs[b];
+        int bx, by, bz;
+        block_unlin(g, r.block, bx, by, bz);
+        load_tile(g, gridv, vt, bx, by, bz, tid, kScThreads);
+        float acc[9][4];
+#pragma unroll
+        for (int k = 0; k < 9; k++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[k][q] = 0.f;
+        for (int c0 = r.start; c0 < r.end; c0 += kScChunk) {
+            const int n = min(kScChunk, r.end - c0);
+            if (tid < 64) sm.cs[tid] = sm.ce[tid] = 0;
+            __syncthreads();
+            for (int i = tid; i < n; i += kScThreads) {
+                const int j = c0 + i;
+                const uint32_t s = perm[j];
+                sm.lc[i] = uint8_t(pre.key[s] & 63);
+                float* pay = &sm.u.pay[i * kPayStride];
+                const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
+                const ClassInfo ci = cls[pre.meta[s]];
+                StencilW sw;
+                stencil_weights(g, x, bx, by, bz, sw);
+                V3<float> vraw;
+                M3<float> cnew;
+                g2p_gather(g, vt, sw, vraw, cnew);
+                const float vn = norm(vraw);
+                const bool clamped_v = vn > g.vmax;
+                const V3<float> vuse = clamped_v ? vraw * (g.vmax / vn) : vraw;
+                M3<float> F;
+#pragma unroll
+                for (int k = 0; k < 9; k++) F.m[k] = pre.F(k)[s];
+                const M3<float> ipc = meye<float>() + cnew * g.dt;
+                const M3<float> ftr = ipc * F;
+                M3<float> fpost_bar, cin_bar;
+#pragma unroll
+                for (int k = 0; k < 9; k++) {
+                    fpost_bar.m[k] = post.F(k)[j];
+                    cin_bar.m[k] = post.C(k)[j];
+                }
+                M3<float> ftr_bar;
+                switch (ci.kind) {
+                    case MK_LIQUID:
+                    case MK_VISCOUS: ftr_bar = liquid_project_vjp(ftr, fpost_bar); break;
+                    case MK_PLASTIC: ftr_bar = box_yield_project_vjp(ftr, ci.theta_c, ci.theta_s, fpost_bar); break;
+                    case MK_NONNEWTONIAN: ftr_bar = von_mises_project_vjp(ftr, ci.sigma_y, ci.mu, fpost_bar); break;
+                    default: ftr_bar = fpost_bar; break;
+                }
+                const M3<float> fpre_bar = transpose(ipc) * ftr_bar;
+                const M3<float> c_bar = cin_bar + ftr_bar * transpose(F) * g.dt;
+                V3<float> xnb = {post.x(0)[j], post.x(1)[j], post.x(2)[j]};
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    const float xr = x[a] + vuse[a] * g.dt;
+                    const float xc = clamp_ref(xr, g.lo[a], g.hi[a]);
+                    if (xr != xc) xnb[a] = 0.f;
+                }
+                const V3<float> vub = {post.v(0)[j] + xnb.x * g.dt, post.v(1)[j] + xnb.y * g.dt,
+                                       post.v(2)[j] + xnb.z * g.dt};
+                const V3<float> vrb = clamped_v ? V3<float>{0.f, 0.f, 0.f} : vub;
+                // x_bar = x_new_bar + sum_o grad w_o s_o - k4 c_bar^T v_raw
+                V3<float> xb = xnb - tmul(c_bar, vraw) * g.k4;
+                const float kd = g.k4 * g.dx;
+#pragma unroll
+                for (int ox = 0; ox < 3; ox++) {
+#pragma unroll
+                    for (int oy = 0; oy < 3; oy++) {
+#pragma unroll
+                        for (int oz = 0; oz < 3; oz++) {
+                            const float4 gv4 = vt[(sw.l[0] + ox) * 36 + (sw.l[1] + oy) * 6 + (sw.l[2] + oz)];
+                            const V3<float> gv = {gv4.x, gv4.y, gv4.z};
+                            const V3<float> rel = {(float(ox) - sw.fx[0]) * kd, (float(oy) - sw.fx[1]) * kd,
+                                                   (float(oz) - sw.fx[2]) * kd};
+                            // k4 * c_bar * rel_phys, rel_phys = dx (o - fx)
+                            const V3<float> cr = c_bar * rel;
+                            const float sv = dot(gv, vrb) + dot(gv, cr);
+                            const float gx = sw.dw[0][ox] * sw.w[1][oy] * sw.w[2][oz];
+                            const float gy = sw.w[0][ox] * sw.dw[1][oy] * sw.w[2][oz];
+                            const float gz = sw.w[0][ox] * sw.w[1][oy] * sw.dw[2][oz];
+                            xb.x += gx * g.inv_dx * sv;
+                            xb.y += gy * g.inv_dx * sv;
+                            xb.z += gz * g.inv_dx * sv;
+                        }
+                    }
+                }
+                if (ci.rigid >= 0) {
+                    const int mr = rd.mrank[pre.id[s]];
+                    xb.x += start_bar[3 * mr];
+                    xb.y += start_bar[3 * mr + 1];
+                    xb.z += start_bar[3 * mr + 2];
+                }
+                xbar_tmp[j] = xb.x;
+                xbar_tmp[size_t(cap) + j] = xb.y;
+                xbar_tmp[2 * size_t(cap) + j] = xb.z;
+#pragma unroll
+                for (int k = 0; k < 9; k++) Fbar_tmp[size_t(k) * cap + j] = fpre_bar.m[k];
+                // scatter payload: w (v_raw_bar + k4 c_bar dx (o - fx))
+                const M3<float> bm = c_bar * kd;
+                const V3<float> f3 = {sw.fx[0], sw.fx[1], sw.fx[2]};
+                const V3<float> a = vrb - bm * f3;
+                pay[0] = sw.fx[0];
+                pay[1] = sw.fx[1];
+                pay[2] = sw.fx[2];
+                pay[3] = a.x;
+                pay[4] = a.y;
+                pay[5] = a.z;
+#pragma unroll
+                for (int k = 0; k < 9; k++) pay[6 + k] = bm.m[k];
+            }
+            __syncthreads();
+            sc_ranges(sm, n, tid, kScThreads);
+            __syncthreads();
+            sc_accumulate<3>(sm, my_c, my_ox, acc);
+            __syncthreads();
+        }
+        sc_store_cellpart<3>(sm, my_c, my_ox, acc);
+        __syncthreads();
+        sc_tile(sm, staging_bar + size_t(b) * kTile, tid, kScThreads);
+        __syncthreads();
+    }
+}
+
+void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                    int grid, const ClassInfo* cls, const float4* gridv, BarBuf post, float* xbar_tmp,
+                    float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar, cudaStream_t s) {
+    k_adj_g2p<<<grid, kScThreads, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridv, post, xbar_tmp, Fbar_tmp, rd,
+                                          start_bar, staging_bar, post.cap);
+}
+
+// ---------------------------------------------------------------------------
+// grid update adjoint (adjoint.hpp:367-412) with a deterministic CTA-level
+// reduction of the per-effector bars (18 scalars each)
+// ---------------------------------------------------------------------------
+constexpr int kEffQ = 18;  // t[3] R[9] vlin[3] w[3]
+
+__device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __restrict__ blockmap,
+                                                  const float4* __restrict__ staging, int bx, int by, int bz, int lx,
+                                                  int ly, int lz) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int d = 0; d < 8; d++) {
+        const int ddx = d >> 2, ddy = (d >> 1) & 1, ddz = d & 1;
+        if ((ddx && lx >= 2) || (ddy && ly >= 2) || (ddz && lz >= 2)) continue;
+        const int px = bx - ddx, py = by - ddy, pz = bz - ddz;
+        if (px < 0 || py < 0 || pz < 0) continue;
+        const int slot = blockmap[block_lin(g, px, py, pz)];
+        if (slot < 0) continue;
+        const float4 v = staging[size_t(slot) * kTile + (lx + 4 * ddx) * 36 + (ly + 4 * ddy) * 6 + (lz + 4 * ddz)];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(64) k_adj_grid(Geom g, const int* __restrict__ nb_list, const int* __restrict__ n_nb,
+                                                 const int* __restrict__ blockmap,
+                                                 const float4* __restrict__ staging_bar,
+                                                 const float4* __restrict__ gridv0, float4* gridbar, EffSet eff,
+                                                 double* eff_partial) {
+    __shared__ double wred[2][kEffQ];
+    __shared__ double cta_acc[kMaxEff][kEffQ];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int q = tid; q < kMaxEff * kEffQ; q += 64) (&cta_acc[0][0])[q] = 0.0;
+    __syncthreads();
+    const int n = *n_nb;
+    const int lx = tid >> 4, ly = (tid >> 2) & 3, lz = tid & 3;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+        const int nbid = nb_list[k];
+        int bx, by, bz;
+        block_unlin(g, nbid, bx, by, bz);
+        const float4 sb = gather_tile_sum(g, blockmap, staging_bar, bx, by, bz, lx, ly, lz);
+        V3<float> bar = {sb.x, sb.y, sb.z};
+        const size_t idx = size_t(nbid) * 64 + tid;
+        const float4 g0 = gridv0[idx];
+        const float m = g0.w;
+        const V3<float> v0 = {g0.x, g0.y, g0.z};
+        const bool act = m > g.mass_eps && (bar.x != 0.f || bar.y != 0.f || bar.z != 0.f);
+        const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
+        const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
+        V3<float> v1 = {v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
+        V3<float> v2 = v1;
+        V3<float> chain[kMaxEff];
+        if (act) {
+            v2 = wall_bc_dev(g, i, j, kk, v1);
+            V3<float> c = v2;
+            for (int e = 0; e < eff.n; e++) {
+                chain[e] = c;
+                c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
+            }
+        }
+        for (int e = eff.n - 1; e >= 0; e--) {
+            EffBars<float> eb;
+            eb.t = V3<float>{0.f, 0.f, 0.f};
+            eb.R = mzero<float>();
+            eb.vlin = eb.t;
+            eb.w = eb.t;
+            bool contact = false;
+            if (act) {
+                V3<float> in_bar = {0.f, 0.f, 0.f};
+                contact = effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
+                                               in_bar, eb);
+                bar = in_bar;
+            }
+            if (__syncthreads_or(contact ? 1 : 0)) {
+                float vals[kEffQ];
+                vals[0] = eb.t.x; vals[1] = eb.t.y; vals[2] = eb.t.z;
+#pragma unroll
+                for (int q = 0; q < 9; q++) vals[3 + q] = eb.R.m[q];
+                vals[12] = eb.vlin.x; vals[13] = eb.vlin.y; vals[14] = eb.vlin.z;
+                vals[15] = eb.w.x; vals[16] = eb.w.y; vals[17] = eb.w.z;
+#pragma unroll
+                for (int q = 0; q < kEffQ; q++) {
+                    double v = double(vals[q]);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                    if (lane == 0) wred[warp][q] = v;
+                }
+                __syncthreads();
+                if (tid < kEffQ) cta_acc[e][tid] += wred[0][tid] + wred[1][tid];
+                __syncthreads();
+            }
+        }
+        float pb0 = 0.f, pb1 = 0.f, pb2 = 0.f, mb = 0.f;
+        if (act) {
+            if (v2.x != v1.x) bar.x = 0.f;
+            if (v2.y != v1.y) bar.y = 0.f;
+            if (v2.z != v1.z) bar.z = 0.f;
+            const float inv = 1.0f / m;
+            pb0 = bar.x * inv;
+            pb1 = bar.y * inv;
+            pb2 = bar.z * inv;
+            mb = -dot(v0, bar) * inv;
+        }
+        gridbar[idx] = make_float4(pb0, pb1, pb2, mb);
+    }
+    __syncthreads();
+    for (int q = tid; q < kMaxEff * kEffQ; q += 64)
+        eff_partial[size_t(blockIdx.x) * kMaxEff * kEffQ + q] = (&cta_acc[0][0])[q];
+}
+
+__global__ void k_eff_final(const double* partial, int nblocks, double* out) {
+    const int q = threadIdx.x;
+    if (q >= kMaxEff * kEffQ) return;
+    double s = 0.0;
+    for (int b = 0; b < nblocks; b++) s += partial[size_t(b) * kMaxEff * kEffQ + q];
+    out[q] = s;
+}
+
+void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
+                     const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
+                     double* eff_partial, double* eff_out, cudaStream_t s) {
+    k_adj_grid<<<kEffBlocks, 64, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial);
+    k_eff_final<<<1, kMaxEff * kEffQ, 0, s>>>(eff_partial, kEffBlocks, eff_out);
+}
+
+// ---------------------------------------------------------------------------
+// P2G adjoint (adjoint.hpp:414-470)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+                                                 const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
+                                                 const ClassInfo* __restrict__ cls,
+                                                 const float4* __restrict__ gridbar,
+                                                 const float* __restrict__ xbar_tmp,
+                                                 const float* __restrict__ Fbar_tmp, BarBuf out, int* nonfinite,
+                                                 int cap) {
+    __shared__ float4 bt[kTile];
+    const int tid = threadIdx.x;
+    const int nb = *n_blocks;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const BlockRec r = recs[b];
+        int bx, by, bz;
+        block_unlin(g, r.block, bx, by, bz);
+        __syncthreads();
+        load_tile(g, gridbar, bt, bx, by, bz, tid, 128);
+        __syncthreads();
+        for (int j = r.start + tid; j < r.end; j += 128) {
+            const uint32_t s = perm[j];
+            const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
+            const V3<float> v = {pre.v(0)[s], pre.v(1)[s], pre.v(2)[s]};
+            const ClassInfo ci = cls[pre.meta[s]];
+            M3<float> F, C;
+#pragma unroll
+            for (int k = 0; k < 9; k++) {
+                F.m[k] = pre.F(k)[s];
+                C.m[k] = pre.C(k)[s];
+            }
+            const bool visc = ci.kind == MK_VISCOUS;
+            const M3<float> ipc = meye<float>() + C * g.dt;
+            const M3<float> fs = visc ? ipc * F : F;
+            bool ok;
+            Svd<float> t;
+            const M3<float> P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
+            const M3<float> smat = P * transpose(fs);
+            const float cc = g.stress_coeff * ci.vol0;
+            const M3<float> affine = C * ci.mass - smat * cc;
+            StencilW sw;
+            stencil_weights(g, x, bx, by, bz, sw);
+            const V3<float> mv = v * ci.mass;
+            V3<float> xb = {0.f, 0.f, 0.f}, vbsum = {0.f, 0.f, 0.f};
+            M3<float> ab = mzero<float>();
+            float wsum_p[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ox = 0; ox < 3; ox++) {
+#pragma unroll
+                for (int oy = 0; oy < 3; oy++) {
+#pragma unroll
+                    for (int oz = 0; oz < 3; oz++) {
+                        const float4 b4 = bt[(sw.l[0] + ox) * 36 + (sw.l[1] + oy) * 6 + (sw.l[2] + oz)];
+                        const V3<float> ob = {b4.x, b4.y, b4.z};
+                        const float mbar = b4.w;
+                        const float w = sw.w[0][ox] * sw.w[1][oy] * sw.w[2][oz];
+                        const V3<float> rel = {(float(ox) - sw.fx[0]) * g.dx, (float(oy) - sw.fx[1]) * g.dx,
+                                               (float(oz) - sw.fx[2]) * g.dx};
+                        const V3<float> contrib = mv + affine * rel;
+                        const float sv = mbar * ci.mass + dot(ob, contrib);
+                        const float gx = sw.dw[0][ox] * sw.w[1][oy] * sw.w[2][oz];
+                        const float gy = sw.w[0][ox] * sw.dw[1][oy] * sw.w[2][oz];
+                        const float gz = sw.w[0][ox] * sw.w[1][oy] * sw.dw[2][oz];
+                        xb.x += gx * g.inv_dx * sv;
+                        xb.y += gy * g.inv_dx * sv;
+                        xb.z += gz * g.inv_dx * sv;
+                        const V3<float> wob = ob * w;
+                        wsum_p[0] += wob.x;
+                        wsum_p[1] += wob.y;
+                        wsum_p[2] += wob.z;
+                        ab += outer(wob, rel);
+                    }
+                }
+            }
+            const V3<float> wp = {wsum_p[0], wsum_p[1], wsum_p[2]};
+            xb -= tmul(affine, wp);
+            vbsum = wp * ci.mass;
+            const M3<float> sm_bar = ab * (-cc);
+            const M3<float> p_bar = sm_bar * fs;
+            M3<float> fs_bar = transpose(sm_bar) * P;
+            fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
+            M3<float> Fb, Cb = ab * ci.mass;
+#pragma unroll
+            for (int k = 0; k < 9; k++) Fb.m[k] = Fbar_tmp[size_t(k) * cap + j];
+            if (visc) {
+                Fb += transpose(ipc) * fs_bar;
+                Cb += fs_bar * transpose(F) * g.dt;
+            } else {
+                Fb += fs_bar;
+            }
+            const float xo[3] = {xbar_tmp[j] + xb.x, xbar_tmp[size_t(cap) + j] + xb.y,
+                                 xbar_tmp[2 * size_t(cap) + j] + xb.z};
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                out.x(a)[s] = xo[a];
+                out.v(a)[s] = vbsum[a];
+            }
+#pragma unroll
+            for (int k = 0; k < 9; k++) {
+                out.F(k)[s] = Fb.m[k];
+                out.C(k)[s] = Cb.m[k];
+            }
+            if (!isfinite(xo[0]) || !isfinite(vbsum.x) || !isfinite(Fb.m[0])) atomicOr(nonfinite, 1);
+        }
+    }
+}
+
+void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                    int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
+                    const float* Fbar_tmp, BarBuf out, int* nonfinite, cudaStream_t s) {
+    k_adj_p2g<<<grid, 128, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out, nonfinite,
+                                   out.cap);
+}
+
+// inactive particles pass their bars through untouched
+__global__ void k_tail_bars(BarBuf post, BarBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
+    int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    uint32_t s = perm[j];
+    for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = post.f[size_t(c) * post.cap + j];
+}
+
+void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s) {
+    int m = n - n_active;
+    if (m <= 0) return;
+    k_tail_bars<<<(m + 255) / 256, 256, 0, s>>>(post, out, perm, n_active, n);
+}
+
+// emitter spawn adjoint, sequential over the substep's spawns (fixed order)
+__global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int q = 0; q < n_eff * 12; q++) em_out[q] = 0.0;
+    for (int i = 0; i < n; i++) {
+        const EmitAdjEntry e = list[i];
+        double xb[3], vb[3];
+        for (int a = 0; a < 3; a++) {
+            xb[a] = out.x(a)[e.slot];
+            vb[a] = out.v(a)[e.slot];
+            out.x(a)[e.slot] = 0.f;
+            out.v(a)[e.slot] = 0.f;
+        }
+        if (e.eff < 0) continue;
+        for (int a = 0; a < 3; a++)
+            if (e.mask[a]) xb[a] = 0.0;
+        double* o = em_out + 12 * size_t(e.eff);
+        for (int a = 0; a < 3; a++) o[a] += xb[a];
+        for (int a = 0; a < 3; a++)
+            for (int b = 0; b < 3; b++) o[3 + 3 * a + b] += xb[a] * e.local_pos[b] + vb[a] * e.local_vel[b];
+    }
+}
+
+void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s) {
+    k_adj_emit<<<1, 32, 0, s>>>(out, list, n, em_out, n_eff);
+}
+
+// ---------------------------------------------------------------------------
+// bars <-> reference (particle id) order
+// ---------------------------------------------------------------------------
+__global__ void k_bars_from_ref(BarBuf bars, PBuf st, int n, const double* xb, const double* vb, const double* Fb,
+                                const double* Cb) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    size_t id = st.id[i];
+    for (int a = 0; a < 3; a++) {
+        bars.x(a)[i] = float(xb[3 * id + a]);
+        bars.v(a)[i] = float(vb[3 * id + a]);
+    }
+    for (int k = 0; k < 9; k++) {
+        bars.F(k)[i] = float(Fb[9 * id + k]);
+        bars.C(k)[i] = float(Cb[9 * id + k]);
+    }
+}
+
+void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb, const double* Fb,
+                          const double* Cb, cudaStream_t s) {
+    if (n <= 0) return;
+    k_bars_from_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb);
+}
+
+__global__ void k_bars_to_ref(BarBuf bars, PBuf st, int n, double* xb, double* vb, double* Fb, double* Cb) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    size_t id = st.id[i];
+    for (int a = 0; a < 3; a++) {
+        xb[3 * id + a] = bars.x(a)[i];
+        vb[3 * id + a] = bars.v(a)[i];
+    }
+    for (int k = 0; k < 9; k++) {
+        Fb[9 * id + k] = bars.F(k)[i];
+        Cb[9 * id + k] = bars.C(k)[i];
+    }
+}
+
+void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* vb, double* Fb, double* Cb,
+                        cudaStream_t s) {
+    if (n <= 0) return;
+    k_bars_to_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb);
+}
+
+}  // namespace fl

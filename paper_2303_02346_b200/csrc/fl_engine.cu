@@ -1,0 +1,1359 @@
+// fl_engine.cu -- host runtime behind the C ABI (include/flume_b200.h).
+//
+// Owns the device-resident trajectory store and drives the kernels:
+//   substep()          = mpm_substep          (mpm.hpp:455-473)
+//   rollout_loss()     = rollout_loss         (grad.hpp:15-41)
+//   grad_trajectory()  = grad_trajectory      (grad.hpp:61-134) with the
+//                        CheckpointStore policy (checkpoint.hpp:11-50): snapshots
+//                        at stride multiples, each segment replayed once into an
+//                        HBM cache.  Unlike the reference there is no
+//                        capture_forward re-run: the cache already holds every
+//                        pre-state of the segment.
+//   adjoint_substep()  = adjoint_substep      (adjoint.hpp:476-548)
+// Effector kinematics (advance_effectors, mpm.hpp:418-433) and the effector
+// pose adjoint (adjoint.hpp:522-545) are tiny and open-loop, so they run on the
+// host in fp64; everything per-particle / per-node runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/flume_b200.h"
+#include "fl_kernels.h"
+
+namespace fl {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct FlumeError : std::runtime_error {
+    int code;
+    long pid = -1;
+    int body = -1;
+    long substep = -1;
+    FlumeError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            throw FlumeError(FLUME_E_CUDA, std::string("cuda: ") + cudaGetErrorString(e_) + " at " \
+                                               + __FILE__ + ":" + std::to_string(__LINE__));     \
+    } while (0)
+
+template <class T>
+struct DevArr {
+    T* p = nullptr;
+    size_t n = 0;
+    DevArr() = default;
+    DevArr(const DevArr&) = delete;
+    DevArr& operator=(const DevArr&) = delete;
+    ~DevArr() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count <= n && p) return;
+        release();
+        if (count == 0) count = 1;
+        CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void upload(const std::vector<T>& h, cudaStream_t s) {
+        alloc(h.size());
+        if (!h.empty()) CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+// one trajectory state in HBM
+struct StateBuf {
+    void* mem = nullptr;
+    PBuf p{};
+    explicit StateBuf(int cap) {
+        size_t bytes = size_t(cap) * (24 * sizeof(float) + 3 * sizeof(uint32_t));
+        CK(cudaMalloc(&mem, bytes));
+        p.cap = cap;
+        p.f = static_cast<float*>(mem);
+        p.meta = reinterpret_cast<uint32_t*>(p.f + size_t(24) * cap);
+        p.id = p.meta + cap;
+        p.key = p.id + cap;
+    }
+    ~StateBuf() { cudaFree(mem); }
+};
+using StatePtr = std::shared_ptr<StateBuf>;
+
+struct EffState {
+    V3<double> t;
+    M3<double> R;
+    V3<double> vlin;
+    V3<double> w;
+};
+
+// everything the backward of one substep needs besides its pre-state buffer
+struct Record {
+    void* mem = nullptr;
+    uint32_t* perm = nullptr;
+    BlockRec* recs = nullptr;
+    int* n_blocks = nullptr;
+    int* nb_list = nullptr;
+    int* n_nb = nullptr;
+    int* mslot = nullptr;
+    float* mstart = nullptr;
+    float* mid = nullptr;
+    double* fit = nullptr;
+    int n_active = 0;
+    long substep = 0;
+    std::vector<ActEntry> act;
+    std::vector<EmitAdjEntry> emit;
+    EffSet effk{};
+    Record(int N, int maxb, int nbtot, int nmem, int nbody) {
+        size_t off = 0;
+        auto carve = [&](size_t bytes) {
+            size_t o = off;
+            off += (bytes + 255) & ~size_t(255);
+            return o;
+        };
+        size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(16),
+               o_nbl = carve(size_t(nbtot) * 4), o_nnb = carve(16), o_ms = carve(size_t(nmem) * 4),
+               o_mst = carve(size_t(nmem) * 12), o_mid = carve(size_t(nmem) * 12),
+               o_fit = carve(size_t(nbody) * 24 * 8);
+        CK(cudaMalloc(&mem, off));
+        char* b = static_cast<char*>(mem);
+        perm = reinterpret_cast<uint32_t*>(b + o_perm);
+        recs = reinterpret_cast<BlockRec*>(b + o_recs);
+        n_blocks = reinterpret_cast<int*>(b + o_nb);
+        nb_list = reinterpret_cast<int*>(b + o_nbl);
+        n_nb = reinterpret_cast<int*>(b + o_nnb);
+        mslot = reinterpret_cast<int*>(b + o_ms);
+        mstart = reinterpret_cast<float*>(b + o_mst);
+        mid = reinterpret_cast<float*>(b + o_mid);
+        fit = reinterpret_cast<double*>(b + o_fit);
+    }
+    ~Record() { cudaFree(mem); }
+};
+using RecordPtr = std::shared_ptr<Record>;
+
+static int bits_for(uint64_t v) {
+    int b = 0;
+    while ((uint64_t(1) << b) <= v) b++;
+    return b < 1 ? 1 : b;
+}
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    flume_error_info last_err{};
+    flume_timing timing{};
+    long launches = 0;
+
+    // scene
+    flume_config cfg{};
+    Geom geom{};
+    int N = 0;
+    int maxb = 0;
+    std::vector<flume_material> mats;
+    std::vector<flume_effector_shape> eff_shapes;
+    std::vector<int> p_mat, p_body;
+    std::vector<double> p_mass, p_vol0;
+    std::vector<long> p_act;
+    std::vector<uint32_t> p_class;
+    std::vector<ClassInfo> classes;
+    // rigid
+    int nbody = 0, nmem = 0;
+    std::vector<int> rb_off, rb_id, member_body, mrank_by_id;
+    std::vector<long> rb_members;
+    std::vector<double> rb_rest, rb_mass, rb_smrest, rb_total;
+    std::vector<int> chunk_body, chunk_m0, chunk_m1;
+    // emitters by particle id
+    std::vector<int> emitter_of;
+    std::vector<flume_emitter> emitters;
+    std::map<long, std::vector<int>> pending;  // activation substep -> ids (sorted)
+
+    // device constants
+    DevArr<ClassInfo> d_cls;
+    DevArr<int> d_rb_off, d_rb_id, d_member_body, d_mrank, d_chunk_body, d_chunk_m0, d_chunk_m1, d_act;
+    DevArr<double> d_rb_rest, d_rb_mass, d_rb_smrest, d_rb_total;
+
+    // scratch
+    DevArr<uint64_t> ck_in, ck_out;
+    DevArr<uint32_t> idx_in;
+    DevArr<unsigned char> cub_tmp;
+    size_t cub_bytes = 0;
+    DevArr<int> flags, pos, starts, nbflag, nbpos, blockmap;
+    DevArr<float4> staging, gridv, gridv0, staging_bar, gridbar;
+    DevArr<unsigned long long> d_err;
+    DevArr<int> d_nonfinite;
+    DevArr<double> rig_partial, abar, eff_partial, eff_out, em_out, loss_partial, loss_out;
+    DevArr<float> start_bar, xbar_tmp, Fbar_tmp;
+    DevArr<ActEntry> d_act_list;
+    DevArr<EmitAdjEntry> d_emit_list;
+    DevArr<double> d_up[4];
+    DevArr<uint32_t> d_upmeta;
+    DevArr<uint8_t> d_upactive;
+    int grid_p2g = 0, grid_g2p = 0, grid_upd = 0;
+
+    // live state
+    StatePtr cur;
+    std::vector<uint32_t> inactive_ids;  // tail of cur's storage, sorted by id
+    int n_active = 0;
+    long substep_index = 0;
+    double time = 0;
+    std::vector<EffState> eff;
+    std::vector<StatePtr> pool;
+    std::vector<RecordPtr> rec_pool;
+    RecordPtr scratch_rec;
+
+    // -------------------------------------------------------------------
+    StatePtr get_state() {
+        if (!pool.empty()) {
+            StatePtr s = pool.back();
+            pool.pop_back();
+            return s;
+        }
+        return std::make_shared<StateBuf>(N);
+    }
+    void put_state(StatePtr s) {
+        if (s) pool.push_back(std::move(s));
+    }
+    RecordPtr get_record() {
+        if (!rec_pool.empty()) {
+            RecordPtr r = rec_pool.back();
+            rec_pool.pop_back();
+            return r;
+        }
+        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1));
+    }
+    void put_record(RecordPtr r) {
+        if (r) rec_pool.push_back(std::move(r));
+    }
+
+    RigidDev rigid_dev(Record& r) {
+        RigidDev d{};
+        d.nbody = nbody;
+        d.nmem = nmem;
+        d.off = d_rb_off.p;
+        d.mrank = d_mrank.p;
+        d.rest = d_rb_rest.p;
+        d.mass = d_rb_mass.p;
+        d.smrest = d_rb_smrest.p;
+        d.total = d_rb_total.p;
+        d.body_id = d_rb_id.p;
+        d.member_body = d_member_body.p;
+        d.mslot = r.mslot;
+        d.mstart = r.mstart;
+        d.mid = r.mid;
+        d.fit = r.fit;
+        return d;
+    }
+
+    void init(const flume_scene_desc* desc, int dev);
+    void check_error(long substep_base = 0);
+    EffSet make_effset(const std::vector<EffState>& es) const;
+    void advance_effectors(const double* action);
+    void upload(const flume_state_view* view);
+    void download(flume_state_view* view);
+    void sort_and_lists(StateBuf& st, Record& r);
+    void forward_substep(const double* action, StatePtr in, StatePtr out, Record& r, bool record_grid);
+    void substep(const double* action, int count);
+    void stage_grid(double* mass, double* vel);
+    LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<DevArr<float>>>& keep);
+    uint32_t loss_mask(const flume_loss_desc* loss, int seg, int nseg) const;
+    void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, long substep);
+    double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg);
+    void adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre, int t_slot);
+    void grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
+                         double* grad, double* loss_out, double* full_loss, double* per_seg, long* snapshots);
+    void adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* eb,
+                             double* abar_out);
+    void copy_state(StateBuf& dst, const StateBuf& src) {
+        size_t bytes = size_t(N) * (24 * sizeof(float) + 3 * sizeof(uint32_t));
+        CK(cudaMemcpyAsync(dst.mem, src.mem, bytes, cudaMemcpyDeviceToDevice, stream));
+    }
+};
+
+// ---------------------------------------------------------------------------
+void Ctx::init(const flume_scene_desc* desc, int dev) {
+    device = dev;
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    cfg = desc->config;
+    N = int(desc->n_particles);
+    if (N <= 0) throw FlumeError(FLUME_E_SCENE, "scene has no particles");
+    mats.assign(desc->materials, desc->materials + desc->n_materials);
+    eff_shapes.assign(desc->effectors, desc->effectors + desc->n_effectors);
+    if (desc->n_effectors > kMaxEff) throw FlumeError(FLUME_E_ARG, "at most 8 effectors are supported");
+
+    // geometry (types.hpp:67-95)
+    const double dx = cfg.domain[0] / cfg.grid_resolution;
+    Geom& g = geom;
+    for (int a = 0; a < 3; a++) {
+        g.nd[a] = int(std::lround(cfg.domain[a] / dx)) + 1;
+        g.NB[a] = (g.nd[a] + 3) / 4;
+        g.lo[a] = float(dx);
+        g.hi[a] = float(cfg.domain[a] - dx);
+        g.gdt[a] = float(cfg.gravity[a] * cfg.dt_substep);
+    }
+    g.nbtot = g.NB[0] * g.NB[1] * g.NB[2];
+    g.key_inactive = uint32_t(g.nbtot) << 6;
+    g.keybits = bits_for(g.key_inactive);
+    g.idbits = bits_for(uint64_t(N - 1));
+    if (g.keybits + g.idbits > 64) throw FlumeError(FLUME_E_ARG, "grid too large for 64-bit sort keys");
+    g.dx = float(dx);
+    g.inv_dx = float(1.0 / dx);
+    g.dt = float(cfg.dt_substep);
+    g.bw = cfg.boundary_width;
+    g.vmax = float(cfg.cfl_fraction * dx / cfg.dt_substep);
+    g.mass_eps = float(cfg.mass_epsilon);
+    g.eps_cells = float(cfg.contact_eps_cells);
+    g.hard = cfg.hard_contact;
+    g.k4 = float(4.0 / (dx * dx));
+    g.stress_coeff = float(cfg.dt_substep * 4.0 / (dx * dx));
+    maxb = std::min(g.nbtot, N);
+
+    // per-particle immutable fields and the class table
+    p_mat.assign(desc->material_id, desc->material_id + N);
+    p_body.assign(desc->body_id, desc->body_id + N);
+    p_mass.assign(desc->mass, desc->mass + N);
+    p_vol0.assign(desc->volume0, desc->volume0 + N);
+    p_act.assign(N, 0);
+    if (desc->activation_substep) p_act.assign(desc->activation_substep, desc->activation_substep + N);
+
+    // rigid bodies
+    nbody = desc->n_rigid;
+    rb_off.assign(1, 0);
+    mrank_by_id.assign(N, -1);
+    std::vector<int> rigid_of_id(N, -1);
+    for (int b = 0; b < nbody; b++) {
+        const flume_rigid_body& rb = desc->rigid[b];
+        if (rb.n_members < 3) throw FlumeError(FLUME_E_RIGIDITY, "rigid_shape_match: bad point lists");
+        rb_id.push_back(rb.body_id);
+        rb_total.push_back(rb.total_mass);
+        double sm[3] = {0, 0, 0};
+        for (long j = 0; j < rb.n_members; j++) {
+            long pid = rb.members[j];
+            if (pid < 0 || pid >= N) throw FlumeError(FLUME_E_ARG, "rigid member out of range");
+            mrank_by_id[pid] = int(rb_members.size());
+            rigid_of_id[pid] = b;
+            rb_members.push_back(pid);
+            member_body.push_back(b);
+            for (int a = 0; a < 3; a++) rb_rest.push_back(rb.rest_offsets[3 * j + a]);
+            rb_mass.push_back(p_mass[pid]);
+            for (int a = 0; a < 3; a++) sm[a] += p_mass[pid] * rb.rest_offsets[3 * j + a];
+        }
+        for (int a = 0; a < 3; a++) rb_smrest.push_back(sm[a]);
+        rb_off.push_back(int(rb_members.size()));
+        for (long m0 = 0; m0 < rb.n_members; m0 += kRigidChunk) {
+            chunk_body.push_back(b);
+            chunk_m0.push_back(rb_off[b] + int(m0));
+            chunk_m1.push_back(rb_off[b] + int(std::min<long>(rb.n_members, m0 + kRigidChunk)));
+        }
+    }
+    nmem = int(rb_members.size());
+
+    std::map<std::tuple<int, int, double, double, int>, uint32_t> cmap;
+    p_class.resize(N);
+    for (int i = 0; i < N; i++) {
+        if (p_mat[i] < 0 || p_mat[i] >= int(mats.size())) throw FlumeError(FLUME_E_SCENE, "bad material id");
+        auto key = std::make_tuple(p_mat[i], p_body[i], p_mass[i], p_vol0[i], rigid_of_id[i]);
+        auto it = cmap.find(key);
+        if (it == cmap.end()) {
+            const flume_material& m = mats[p_mat[i]];
+            ClassInfo ci{};
+            ci.kind = m.kind;
+            ci.body = p_body[i];
+            ci.rigid = rigid_of_id[i];
+            ci.mass = float(p_mass[i]);
+            ci.vol0 = float(p_vol0[i]);
+            ci.mu = float(m.mu);
+            ci.lambda = float(m.lambda);
+            ci.theta_c = float(m.theta_c);
+            ci.theta_s = float(m.theta_s);
+            ci.sigma_y = float(m.sigma_y);
+            it = cmap.emplace(key, uint32_t(classes.size())).first;
+            classes.push_back(ci);
+        }
+        p_class[i] = it->second;
+    }
+
+    // emitters
+    emitter_of.assign(N, -1);
+    emitters.assign(desc->emitters, desc->emitters + desc->n_emitters);
+    for (size_t k = 0; k < emitters.size(); k++) emitter_of[emitters[k].particle] = int(k);
+
+    // device constants
+    d_cls.upload(classes, stream);
+    d_rb_off.upload(rb_off, stream);
+    d_rb_id.upload(rb_id, stream);
+    d_member_body.upload(member_body, stream);
+    d_mrank.upload(mrank_by_id, stream);
+    d_chunk_body.upload(chunk_body, stream);
+    d_chunk_m0.upload(chunk_m0, stream);
+    d_chunk_m1.upload(chunk_m1, stream);
+    d_rb_rest.upload(rb_rest, stream);
+    d_rb_mass.upload(rb_mass, stream);
+    d_rb_smrest.upload(rb_smrest, stream);
+    d_rb_total.upload(rb_total, stream);
+    std::vector<int> act32(N);
+    for (int i = 0; i < N; i++) act32[i] = int(std::min<long>(p_act[i], 0x7fffffff));
+    d_act.upload(act32, stream);
+
+    // scratch
+    ck_in.alloc(N);
+    ck_out.alloc(N);
+    idx_in.alloc(N);
+    flags.alloc(N);
+    pos.alloc(N);
+    starts.alloc(maxb);
+    nbflag.alloc(g.nbtot);
+    nbpos.alloc(g.nbtot);
+    blockmap.alloc(g.nbtot);
+    staging.alloc(size_t(maxb) * kTile);
+    staging_bar.alloc(size_t(maxb) * kTile);
+    gridv.alloc(size_t(g.nbtot) * 64);
+    gridv0.alloc(size_t(g.nbtot) * 64);
+    gridbar.alloc(size_t(g.nbtot) * 64);
+    d_err.alloc(1);
+    CK(cudaMemsetAsync(d_err.p, 0xff, sizeof(unsigned long long), stream));
+    d_nonfinite.alloc(1);
+    rig_partial.alloc(std::max<size_t>(chunk_body.size(), 1) * 17);
+    abar.alloc(std::max(nbody, 1) * 13);
+    start_bar.alloc(std::max(nmem, 1) * 3);
+    eff_partial.alloc(size_t(kEffBlocks) * kMaxEff * 18);
+    loss_partial.alloc(size_t(kLossBlocks) * kMaxLossTerms);
+    d_act_list.alloc(64);
+    d_emit_list.alloc(64);
+    CK(cudaMemsetAsync(gridv.p, 0, gridv.n * sizeof(float4), stream));
+    CK(cudaMemsetAsync(gridv0.p, 0, gridv0.n * sizeof(float4), stream));
+    CK(cudaMemsetAsync(gridbar.p, 0, gridbar.n * sizeof(float4), stream));
+
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, ck_in.p, ck_out.p, idx_in.p, idx_in.p, N, 0,
+                                       g.keybits + g.idbits, stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, flags.p, pos.p, N, stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b3, nbflag.p, nbpos.p, g.nbtot, stream));
+    cub_bytes = std::max(b1, std::max(b2, b3));
+    cub_tmp.alloc(cub_bytes);
+
+    grid_p2g = p2g_occupancy_grid();
+    grid_g2p = g2p_occupancy_grid();
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid_upd = sms * 8;
+
+    // initial effector state from the shapes' defaults is set by upload()
+    eff.resize(eff_shapes.size());
+    scratch_rec = get_record();
+    cur = get_state();
+    CK(cudaStreamSynchronize(stream));
+}
+
+EffSet Ctx::make_effset(const std::vector<EffState>& es) const {
+    EffSet s{};
+    s.n = int(es.size());
+    for (size_t i = 0; i < es.size(); i++) {
+        const flume_effector_shape& sh = eff_shapes[i];
+        EffK<float>& k = s.e[i];
+        k.shape.kind = sh.shape_kind;
+        k.shape.radius = float(sh.radius);
+        k.shape.half = V3<float>{float(sh.half_extents[0]), float(sh.half_extents[1]), float(sh.half_extents[2])};
+        k.shape.seg_a = V3<float>{float(sh.seg_a[0]), float(sh.seg_a[1]), float(sh.seg_a[2])};
+        k.shape.seg_b = V3<float>{float(sh.seg_b[0]), float(sh.seg_b[1]), float(sh.seg_b[2])};
+        k.shape.normal = V3<float>{float(sh.plane_normal[0]), float(sh.plane_normal[1]), float(sh.plane_normal[2])};
+        k.shape.offset = float(sh.plane_offset);
+        k.shape.half_height = float(sh.half_height);
+        // world shape pose = compose(pose, sdf.pose) in fp64 (sdf.hpp:17-22)
+        M3<double> sR;
+        for (int q = 0; q < 9; q++) sR.m[q] = sh.shape_R[q];
+        V3<double> st = {sh.shape_t[0], sh.shape_t[1], sh.shape_t[2]};
+        V3<double> wt = es[i].t + es[i].R * st;
+        M3<double> wR = es[i].R * sR;
+        k.wt = V3<float>{float(wt.x), float(wt.y), float(wt.z)};
+        for (int q = 0; q < 9; q++) {
+            k.wR.m[q] = float(wR.m[q]);
+            k.shapeR.m[q] = float(sR.m[q]);
+        }
+        k.shapet = V3<float>{float(st.x), float(st.y), float(st.z)};
+        k.pt = V3<float>{float(es[i].t.x), float(es[i].t.y), float(es[i].t.z)};
+        k.vlin = V3<float>{float(es[i].vlin.x), float(es[i].vlin.y), float(es[i].vlin.z)};
+        k.wang = V3<float>{float(es[i].w.x), float(es[i].w.y), float(es[i].w.z)};
+        k.sticky = std::isinf(sh.friction_mu) ? 1 : 0;
+        k.mu = k.sticky ? 0.f : float(sh.friction_mu);
+    }
+    return s;
+}
+
+// mpm.hpp:418-433, fp64 on the host
+void Ctx::advance_effectors(const double* action) {
+    const double dt = cfg.dt_substep;
+    for (size_t i = 0; i < eff.size(); i++) {
+        const flume_effector_shape& sh = eff_shapes[i];
+        EffState& e = eff[i];
+        for (int a = 0; a < 3; a++)
+            if (sh.action_mask[a]) e.vlin[a] = action[a];
+        for (int a = 0; a < 3; a++)
+            if (sh.action_mask[3 + a]) e.w[a] = action[3 + a];
+        e.t = e.t + e.vlin * dt;
+        e.R = advance_rotation(e.R, e.w, dt);
+    }
+}
+
+void Ctx::check_error(long /*substep_base*/) {
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, d_err.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (h == ~0ull) return;
+    uint32_t who = uint32_t(h & 0xffffffffull);
+    uint32_t stage = uint32_t((h >> 32) & 0xf);
+    long sub = long(h >> 36);
+    unsigned long long reset = ~0ull;
+    CK(cudaMemcpy(d_err.p, &reset, sizeof(reset), cudaMemcpyHostToDevice));
+    switch (stage) {
+        case ES_P2G_ESCAPE: {
+            FlumeError e(FLUME_E_ENGINE, "p2g: particle " + std::to_string(who) + " escaped the clamped region");
+            e.pid = who;
+            e.substep = sub;
+            throw e;
+        }
+        case ES_P2G_STRESS: {
+            FlumeError e(FLUME_E_DEGENERATE, "corotated_stress: det(F) <= 0");
+            e.pid = who;
+            e.substep = sub;
+            throw e;
+        }
+        case ES_G2P_PROJECT: {
+            FlumeError e(FLUME_E_DEGENERATE, "g2p return map: det(F) <= 0 or singular value <= 0");
+            e.pid = who;
+            e.substep = sub;
+            throw e;
+        }
+        case ES_RIGID: {
+            FlumeError e(FLUME_E_RIGIDITY, "rigid_shape_match: degenerate covariance");
+            e.body = int(who);
+            e.substep = sub;
+            throw e;
+        }
+        default: throw FlumeError(FLUME_E_ENGINE, "device error");
+    }
+}
+
+// upload a SimState<3> view; canonical store order is established here
+void Ctx::upload(const flume_state_view* view) {
+    for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
+    CK(cudaMemcpyAsync(d_up[0].p, view->x, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_up[1].p, view->v, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_up[2].p, view->F, size_t(N) * 9 * 8, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_up[3].p, view->C, size_t(N) * 9 * 8, cudaMemcpyHostToDevice, stream));
+    substep_index = view->substep_index;
+    time = view->time;
+    // particles activating at or after this substep are parked in the tail; the
+    // substep that reaches their activation index brings them in (mpm.hpp:435-449)
+    std::vector<uint8_t> active(N);
+    pending.clear();
+    inactive_ids.clear();
+    n_active = 0;
+    for (int i = 0; i < N; i++) {
+        bool act = p_act[i] < substep_index || (p_act[i] <= substep_index && emitter_of[i] < 0);
+        active[i] = act ? 1 : 0;
+        if (act)
+            n_active++;
+        else {
+            inactive_ids.push_back(uint32_t(i));
+            pending[p_act[i]].push_back(i);
+        }
+    }
+    d_upmeta.upload(p_class, stream);
+    d_upactive.upload(active, stream);
+    StatePtr raw = get_state();
+    launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, stream);
+    launches++;
+    launch_make_sortkeys(geom, raw->p, N, ck_in.p, idx_in.p, stream);
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, cub_bytes, ck_in.p, ck_out.p, idx_in.p, scratch_rec->perm, N, 0,
+                                       geom.keybits + geom.idbits, stream));
+    launch_gather(raw->p, cur->p, scratch_rec->perm, N, stream);
+    launches += 2;
+    put_state(raw);
+    for (size_t i = 0; i < eff.size(); i++) {
+        const flume_effector_state& es = view->effectors[i];
+        eff[i].t = V3<double>{es.pose_t[0], es.pose_t[1], es.pose_t[2]};
+        for (int q = 0; q < 9; q++) eff[i].R.m[q] = es.pose_R[q];
+        eff[i].vlin = V3<double>{es.linear_velocity[0], es.linear_velocity[1], es.linear_velocity[2]};
+        eff[i].w = V3<double>{es.angular_velocity[0], es.angular_velocity[1], es.angular_velocity[2]};
+    }
+    unsigned long long reset = ~0ull;
+    CK(cudaMemcpyAsync(d_err.p, &reset, sizeof(reset), cudaMemcpyHostToDevice, stream));
+    // escape check of the uploaded positions happens in the first P2G
+    CK(cudaStreamSynchronize(stream));
+}
+
+void Ctx::download(flume_state_view* view) {
+    for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
+    launch_download(cur->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
+    launches++;
+    if (view->x) CK(cudaMemcpyAsync(view->x, d_up[0].p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, stream));
+    if (view->v) CK(cudaMemcpyAsync(view->v, d_up[1].p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, stream));
+    if (view->F) CK(cudaMemcpyAsync(view->F, d_up[2].p, size_t(N) * 9 * 8, cudaMemcpyDeviceToHost, stream));
+    if (view->C) CK(cudaMemcpyAsync(view->C, d_up[3].p, size_t(N) * 9 * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    view->time = time;
+    view->substep_index = substep_index;
+    if (view->effectors)
+        for (size_t i = 0; i < eff.size(); i++) {
+            flume_effector_state& es = view->effectors[i];
+            for (int a = 0; a < 3; a++) {
+                es.pose_t[a] = eff[i].t[a];
+                es.linear_velocity[a] = eff[i].vlin[a];
+                es.angular_velocity[a] = eff[i].w[a];
+            }
+            for (int q = 0; q < 9; q++) es.pose_R[q] = eff[i].R.m[q];
+        }
+}
+
+// keys -> canonical order -> particle-block list -> node-block list
+void Ctx::sort_and_lists(StateBuf& st, Record& r) {
+    Geom& g = geom;
+    launch_make_sortkeys(g, st.p, N, ck_in.p, idx_in.p, stream);
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, cub_bytes, ck_in.p, ck_out.p, idx_in.p, r.perm, N, 0,
+                                       g.keybits + g.idbits, stream));
+    const int na = r.n_active;
+    launch_block_flags(g, ck_out.p, na, flags.p, stream);
+    if (na > 0) CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, flags.p, pos.p, na, stream));
+    launch_block_scatter(flags.p, pos.p, na, starts.p, r.n_blocks, stream);
+    CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
+    CK(cudaMemsetAsync(nbflag.p, 0, size_t(g.nbtot) * sizeof(int), stream));
+    launch_block_recs(g, ck_out.p, starts.p, r.n_blocks, na, maxb, r.recs, blockmap.p, nbflag.p, stream);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag.p, nbpos.p, g.nbtot, stream));
+    launch_nb_scatter(nbflag.p, nbpos.p, g.nbtot, r.nb_list, r.n_nb, stream);
+    launches += 6;
+}
+
+void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r, bool record_grid) {
+    advance_effectors(action);
+    r.substep = substep_index;
+    r.effk = make_effset(eff);
+    // activation (mpm.hpp:435-449): ids reaching their activation substep
+    r.act.clear();
+    r.emit.clear();
+    auto it = pending.find(substep_index);
+    if (it != pending.end()) {
+        for (int id : it->second) {
+            auto pos_it = std::lower_bound(inactive_ids.begin(), inactive_ids.end(), uint32_t(id));
+            int slot = n_active + int(pos_it - inactive_ids.begin());
+            ActEntry a{};
+            a.slot = slot;
+            int em = emitter_of[id];
+            if (em >= 0) {
+                const flume_emitter& e = emitters[em];
+                V3<double> lp = {e.local_pos[0], e.local_pos[1], e.local_pos[2]};
+                V3<double> lv = {e.local_vel[0], e.local_vel[1], e.local_vel[2]};
+                V3<double> raw = lp, vel = lv;
+                if (e.effector >= 0) {
+                    const EffState& es = eff[e.effector];
+                    raw = es.R * lp + es.t;
+                    vel = es.R * lv;
+                }
+                EmitAdjEntry ea{};
+                ea.slot = slot;
+                ea.eff = e.effector;
+                a.has_xv = 1;
+                for (int d = 0; d < 3; d++) {
+                    double cl = clamp_ref(raw[d], double(geom.lo[d]), double(geom.hi[d]));
+                    a.x[d] = float(cl);
+                    a.v[d] = float(vel[d]);
+                    ea.mask[d] = (cl != raw[d]) ? 1 : 0;
+                    ea.local_pos[d] = lp[d];
+                    ea.local_vel[d] = lv[d];
+                }
+                r.emit.push_back(ea);
+            }
+            r.act.push_back(a);
+        }
+        for (int id : it->second) {
+            auto pos_it = std::lower_bound(inactive_ids.begin(), inactive_ids.end(), uint32_t(id));
+            inactive_ids.erase(pos_it);
+        }
+        n_active += int(it->second.size());
+        d_act_list.alloc(r.act.size());
+        CK(cudaMemcpyAsync(d_act_list.p, r.act.data(), r.act.size() * sizeof(ActEntry), cudaMemcpyHostToDevice,
+                           stream));
+        launch_activate(geom, in->p, d_act_list.p, int(r.act.size()), stream);
+        launches++;
+        // the activation list buffer is reused next substep: order the copy
+        CK(cudaStreamSynchronize(stream));
+    }
+    r.n_active = n_active;
+    sort_and_lists(*in, r);
+    launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
+               uint32_t(substep_index), stream);
+    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p,
+                       record_grid ? gridv0.p : nullptr, r.effk, stream);
+    RigidDev rd = rigid_dev(r);
+    if (nbody > 0) CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
+    launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridv.p, rd, d_err.p,
+               uint32_t(substep_index), stream);
+    launch_tail_copy(geom, in->p, out->p, r.perm, n_active, N, stream);
+    launches += 4;
+    if (nbody > 0) {
+        launch_rigid(geom, out->p, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p, d_chunk_m1.p,
+                     rig_partial.p, d_err.p, uint32_t(substep_index), stream);
+        launches += 3;
+    }
+    time += cfg.dt_substep;
+    substep_index++;
+}
+
+void Ctx::substep(const double* action, int count) {
+    for (int i = 0; i < count; i++) {
+        StatePtr nxt = get_state();
+        forward_substep(action, cur, nxt, *scratch_rec, false);
+        put_state(cur);
+        cur = nxt;
+    }
+    check_error();
+}
+
+// p2g + grid_update on the live state without advancing (KAT harness)
+void Ctx::stage_grid(double* mass, double* vel) {
+    Record& r = *scratch_rec;
+    r.n_active = n_active;
+    sort_and_lists(*cur, r);
+    EffSet es = make_effset(eff);
+    launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
+               uint32_t(substep_index), stream);
+    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, nullptr, es, stream);
+    std::vector<float4> h(gridv.n);
+    // nodes outside the touched blocks hold stale values: clear by list
+    std::vector<int> nbl(geom.nbtot);
+    int nn = 0;
+    CK(cudaMemcpyAsync(&nn, r.n_nb, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h.data(), gridv.p, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(nbl.data(), r.nb_list, nbl.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    check_error();
+    std::vector<char> touched(geom.nbtot, 0);
+    for (int k = 0; k < nn; k++) touched[nbl[k]] = 1;
+    const int* nd = geom.nd;
+    for (int i = 0; i < nd[0]; i++)
+        for (int j = 0; j < nd[1]; j++)
+            for (int k = 0; k < nd[2]; k++) {
+                size_t flat = (size_t(i) * nd[1] + j) * nd[2] + k;
+                int blk = block_lin(geom, i >> 2, j >> 2, k >> 2);
+                float4 v = touched[blk] ? h[node_index(geom, i, j, k)] : make_float4(0, 0, 0, 0);
+                if (mass) mass[flat] = v.w;
+                if (vel) {
+                    vel[3 * flat] = v.x;
+                    vel[3 * flat + 1] = v.y;
+                    vel[3 * flat + 2] = v.z;
+                }
+            }
+}
+
+LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<DevArr<float>>>& keep) {
+    LossSet ls{};
+    if (!loss || loss->n_terms <= 0) throw FlumeError(FLUME_E_SCENE, "scene has no loss specification");
+    if (loss->n_terms > kMaxLossTerms) throw FlumeError(FLUME_E_ARG, "too many loss terms");
+    ls.n = loss->n_terms;
+    for (int k = 0; k < ls.n; k++) {
+        const flume_loss_term& t = loss->terms[k];
+        LossTermDev& d = ls.t[k];
+        d.kind = t.kind;
+        d.body = t.body;
+        d.squared = t.squared;
+        d.weight = t.weight;
+        for (int a = 0; a < 3; a++) d.goal[a] = t.goal[a];
+        d.init = nullptr;
+        if (t.kind == FLUME_LOSS_HOLD_INITIAL) {
+            // initial positions by particle id from the current (state0) store
+            auto arr = std::make_shared<DevArr<float>>();
+            arr->alloc(size_t(N) * 3);
+            for (int q = 0; q < 1; q++) d_up[0].alloc(size_t(N) * 3);
+            launch_download(cur->p, N, d_up[0].p, nullptr, nullptr, nullptr, stream);
+            std::vector<double> hx(size_t(N) * 3);
+            CK(cudaMemcpyAsync(hx.data(), d_up[0].p, hx.size() * 8, cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            std::vector<float> fx(hx.begin(), hx.end());
+            arr->upload(fx, stream);
+            d.init = arr->p;
+            keep.push_back(arr);
+        } else if (t.kind != FLUME_LOSS_TARGET_POINT) {
+            throw FlumeError(FLUME_E_SCENE, "loss kind not supported on device");
+        }
+    }
+    return ls;
+}
+
+uint32_t Ctx::loss_mask(const flume_loss_desc* loss, int seg, int nseg) const {
+    uint32_t m = 0;
+    for (int k = 0; k < loss->n_terms; k++)
+        if (!loss->terms[k].final_only || seg == nseg - 1) m |= 1u << k;
+    return m;
+}
+
+void Ctx::eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, long /*substep*/) {
+    launch_loss(st.p, N, d_cls.p, ls, mask, loss_partial.p, out_dev, geom.key_inactive, stream);
+    launches += 2;
+}
+
+double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg) {
+    const long T = long(a->n_segments) * a->segment_length;
+    if (window <= 0) window = T;
+    std::vector<std::shared_ptr<DevArr<float>>> keep;
+    LossSet ls = make_lossset(loss, keep);
+    loss_out.alloc(a->n_segments);
+    // state0 is const: work on a copy
+    const long s0 = substep_index;
+    const double time0 = time;
+    const int na0 = n_active;
+    const std::vector<EffState> eff0 = eff;
+    const std::vector<uint32_t> inact0 = inactive_ids;
+    const auto pend0 = pending;
+    StatePtr st = get_state();
+    copy_state(*st, *cur);
+    for (long t = 0; t < T; t++) {
+        StatePtr nxt = get_state();
+        forward_substep(a->values + 6 * (t / a->segment_length), st, nxt, *scratch_rec, false);
+        put_state(st);
+        st = nxt;
+        if ((t + 1) % a->segment_length == 0) {
+            int seg = int((t + 1) / a->segment_length) - 1;
+            eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, substep_index);
+        }
+    }
+    std::vector<double> per(a->n_segments);
+    CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    put_state(st);
+    substep_index = s0;
+    time = time0;
+    n_active = na0;
+    eff = eff0;
+    inactive_ids = inact0;
+    pending = pend0;
+    check_error();
+    double total = 0;
+    for (int s = 0; s < a->n_segments; s++) {
+        if (per_seg) per_seg[s] = per[s];
+        if (long(s + 1) * a->segment_length <= window) total += per[s];
+    }
+    if (!std::isfinite(total)) throw FlumeError(FLUME_E_ENGINE, "rollout produced a non-finite loss");
+    return total;
+}
+
+// reverse one substep: bars_post (store order of state[t+1]) -> bars_pre (store order of state[t])
+void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre, int t_slot) {
+    Geom& g = geom;
+    BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
+    // rebuild this substep's forward grid (staging -> v, v0) from the pre-state
+    CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
+    launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap.p, stream);
+    launch_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p, uint32_t(r.substep),
+               stream);
+    launch_grid_update(g, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, gridv0.p, r.effk, stream);
+    launches += 3;
+    RigidDev rd = rigid_dev(r);
+    if (nbody > 0) {
+        launch_adj_rigid(g, post, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p, d_chunk_m1.p,
+                         rig_partial.p, start_bar.p, abar.p, stream);
+        launches += 3;
+    }
+    launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, gridv.p, post, xbar_tmp.p, Fbar_tmp.p,
+                   rd, start_bar.p, staging_bar.p, stream);
+    launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, gridv0.p, gridbar.p, r.effk, eff_partial.p,
+                    eff_out.p + size_t(t_slot) * kMaxEff * 18, stream);
+    launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridbar.p, xbar_tmp.p, Fbar_tmp.p, out,
+                   d_nonfinite.p + t_slot, stream);
+    launch_tail_bars(post, out, r.perm, r.n_active, N, stream);
+    launches += 5;
+    if (!r.emit.empty()) {
+        d_emit_list.alloc(r.emit.size());
+        CK(cudaMemcpyAsync(d_emit_list.p, r.emit.data(), r.emit.size() * sizeof(EmitAdjEntry),
+                           cudaMemcpyHostToDevice, stream));
+        launch_adj_emit(out, d_emit_list.p, int(r.emit.size()), em_out.p + size_t(t_slot) * kMaxEff * 12,
+                        int(eff.size()), stream);
+        launches++;
+        CK(cudaStreamSynchronize(stream));
+    }
+}
+
+void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
+                          double* grad, double* loss_out_h, double* full_loss, double* per_seg, long* snapshots) {
+    const long T = long(a->n_segments) * a->segment_length;
+    if (stride <= 0) stride = T;
+    if (window <= 0) window = T;
+    const int nseg = a->n_segments, seglen = a->segment_length;
+    std::vector<std::shared_ptr<DevArr<float>>> keep;
+    LossSet ls = make_lossset(loss, keep);
+    loss_out.alloc(nseg);
+    eff_out.alloc(size_t(T) * kMaxEff * 18);
+    em_out.alloc(size_t(T) * kMaxEff * 12);
+    d_nonfinite.alloc(T);
+    xbar_tmp.alloc(size_t(N) * 3);
+    Fbar_tmp.alloc(size_t(N) * 9);
+    CK(cudaMemsetAsync(em_out.p, 0, em_out.n * 8, stream));
+    CK(cudaMemsetAsync(d_nonfinite.p, 0, size_t(T) * sizeof(int), stream));
+
+    cudaEvent_t ev0, ev1, ev2;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreate(&ev2));
+    long launches0 = launches;
+
+    // host-side replay context per substep start
+    struct HostSnap {
+        long substep;
+        double time;
+        int n_active;
+        std::vector<EffState> eff;
+        std::vector<uint32_t> inactive;
+        std::map<long, std::vector<int>> pending;
+    };
+    const long s0 = substep_index;
+    const double time0 = time;
+    auto take_host = [&]() {
+        return HostSnap{substep_index, time, n_active, eff, inactive_ids, pending};
+    };
+    auto restore_host = [&](const HostSnap& h) {
+        substep_index = h.substep;
+        time = h.time;
+        n_active = h.n_active;
+        eff = h.eff;
+        inactive_ids = h.inactive;
+        pending = h.pending;
+    };
+    const HostSnap host0 = take_host();
+    std::vector<std::vector<EffState>> eff_pre(T), eff_post(T);
+
+    // ---------------- forward with snapshots ----------------
+    CK(cudaEventRecord(ev0, stream));
+    std::map<long, StatePtr> snaps;
+    std::map<long, HostSnap> host_snaps;
+    const long last_base = ((T - 1) / stride) * stride;  // segment replayed first in the backward
+    std::vector<StatePtr> cache_states;                   // indices [cache_base, ...]
+    std::vector<RecordPtr> cache_recs;
+    long cache_base = -1;
+
+    StatePtr st = get_state();
+    copy_state(*st, *cur);
+    snaps[0] = st;
+    host_snaps[0] = take_host();
+    for (long t = 0; t < T; t++) {
+        const bool in_last = t >= last_base;
+        if (in_last && cache_base < 0) {
+            cache_base = t;
+            cache_states.push_back(st);
+        }
+        RecordPtr rec = in_last ? get_record() : scratch_rec;
+        StatePtr nxt = get_state();
+        eff_pre[t] = eff;
+        forward_substep(a->values + 6 * (t / seglen), st, nxt, *rec, false);
+        eff_post[t] = eff;
+        if (in_last) {
+            cache_recs.push_back(rec);
+            cache_states.push_back(nxt);
+        } else if (!snaps.count(t)) {
+            put_state(st);
+        }
+        st = nxt;
+        if ((t + 1) % stride == 0) {
+            snaps[t + 1] = st;
+            host_snaps[t + 1] = take_host();
+        }
+        if ((t + 1) % seglen == 0) {
+            int seg = int((t + 1) / seglen) - 1;
+            eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, substep_index);
+        }
+    }
+    const size_t n_snap = snaps.size();
+    CK(cudaEventRecord(ev1, stream));
+    std::vector<double> per(nseg);
+    CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
+    check_error();
+    double lsum = 0, fsum = 0;
+    for (int s = 0; s < nseg; s++) {
+        fsum += per[s];
+        if (long(s + 1) * seglen <= window) lsum += per[s];
+    }
+    if (!std::isfinite(lsum)) throw FlumeError(FLUME_E_ENGINE, "grad_trajectory: non-finite forward loss");
+
+    // ---------------- backward ----------------
+    DevArr<float> barsA, barsB;
+    barsA.alloc(size_t(N) * 24);
+    barsB.alloc(size_t(N) * 24);
+    CK(cudaMemsetAsync(barsA.p, 0, barsA.n * 4, stream));
+    auto release_cache = [&]() {
+        for (auto& s : cache_states) {
+            bool is_snap = false;
+            for (auto& kv : snaps)
+                if (kv.second == s) is_snap = true;
+            if (!is_snap) put_state(s);
+        }
+        for (auto& r : cache_recs) put_record(r);
+        cache_states.clear();
+        cache_recs.clear();
+        cache_base = -1;
+    };
+    auto ensure_cached = [&](long t) {
+        if (cache_base >= 0 && t >= cache_base && t < cache_base + long(cache_recs.size())) return;
+        release_cache();
+        auto it = snaps.upper_bound(t);
+        --it;
+        long base = it->first;
+        long end = std::min(base + stride, T);
+        restore_host(host_snaps[base]);
+        StatePtr s = it->second;
+        cache_base = base;
+        cache_states.push_back(s);
+        for (long q = base; q < end; q++) {
+            RecordPtr rec = get_record();
+            StatePtr nxt = get_state();
+            forward_substep(a->values + 6 * (q / seglen), s, nxt, *rec, false);
+            cache_recs.push_back(rec);
+            cache_states.push_back(nxt);
+            s = nxt;
+        }
+    };
+    for (long t = T - 1; t >= 0; t--) {
+        if ((t + 1) % seglen == 0 && t + 1 <= window) {
+            int seg = int((t + 1) / seglen) - 1;
+            ensure_cached(t);
+            StateBuf& boundary = *cache_states[size_t(t + 1 - cache_base)];
+            launch_loss_grad(boundary.p, N, d_cls.p, ls, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
+                             geom.key_inactive, stream);
+            launches++;
+        }
+        ensure_cached(t);
+        const size_t k = size_t(t - cache_base);
+        adjoint_step(*cache_states[k], *cache_recs[k], barsA, barsB, int(t));
+        std::swap(barsA.p, barsB.p);
+        std::swap(barsA.n, barsB.n);
+    }
+    release_cache();
+    for (auto& kv : snaps) put_state(kv.second);
+    CK(cudaEventRecord(ev2, stream));
+
+    // ---------------- effector pose chain (host, fp64) ----------------
+    std::vector<double> eb(size_t(T) * kMaxEff * 18), em(size_t(T) * kMaxEff * 12);
+    std::vector<int> nonf(T);
+    CK(cudaMemcpyAsync(eb.data(), eff_out.p, eb.size() * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(em.data(), em_out.p, em.size() * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(nonf.data(), d_nonfinite.p, nonf.size() * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    check_error();
+    float fms = 0, bms = 0;
+    CK(cudaEventElapsedTime(&fms, ev0, ev1));
+    CK(cudaEventElapsedTime(&bms, ev1, ev2));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    cudaEventDestroy(ev2);
+    restore_host(host0);
+    substep_index = s0;
+    time = time0;
+
+    const size_t ne = eff.size();
+    const double dt = cfg.dt_substep;
+    std::vector<V3<double>> et(ne, V3<double>{0, 0, 0});
+    std::vector<M3<double>> eR(ne, mzero<double>());
+    for (int s = 0; s < nseg; s++)
+        for (int k2 = 0; k2 < 6; k2++) grad[6 * s + k2] = 0.0;
+    for (long t = T - 1; t >= 0; t--) {
+        const int seg = int(t / seglen);
+        double echeck = 0;
+        for (size_t e = 0; e < ne; e++) {
+            const double* b = &eb[(size_t(t) * kMaxEff + e) * 18];
+            const double* m = &em[(size_t(t) * kMaxEff + e) * 12];
+            for (int q = 0; q < 3; q++) et[e][q] += m[q];
+            for (int q = 0; q < 9; q++) eR[e].m[q] += m[3 + q];
+            V3<double> t_bar = et[e] + V3<double>{b[0], b[1], b[2]};
+            M3<double> r_bar = eR[e];
+            for (int q = 0; q < 9; q++) r_bar.m[q] += b[3 + q];
+            V3<double> vlin_bar = V3<double>{b[12], b[13], b[14]} + t_bar * dt;
+            V3<double> w_bar = {b[15], b[16], b[17]};
+            M3<double> r_pre_bar = mzero<double>();
+            advance_rotation_vjp(eff_pre[t][e].R, eff_post[t][e].w, dt, r_bar, r_pre_bar, w_bar);
+            et[e] = t_bar;
+            eR[e] = r_pre_bar;
+            const int* mask = eff_shapes[e].action_mask;
+            for (int q = 0; q < 3; q++)
+                if (mask[q]) grad[6 * seg + q] += vlin_bar[q];
+            for (int q = 0; q < 3; q++)
+                if (mask[3 + q]) grad[6 * seg + 3 + q] += w_bar[q];
+            echeck += t_bar.x;
+        }
+        if (nonf[t] || !std::isfinite(echeck)) {
+            FlumeError e(FLUME_E_ADJOINT, "non-finite adjoint at substep " + std::to_string(t));
+            e.substep = t;
+            throw e;
+        }
+    }
+    if (loss_out_h) *loss_out_h = lsum;
+    if (full_loss) *full_loss = fsum;
+    if (per_seg)
+        for (int s = 0; s < nseg; s++) per_seg[s] = per[s];
+    if (snapshots) *snapshots = long(n_snap);
+    timing.forward_ms = fms;
+    timing.backward_ms = bms;
+    timing.substeps = T;
+    timing.particle_substeps = T * long(N);
+    timing.launches = launches - launches0;
+}
+
+void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* ebars,
+                              double* abar_out) {
+    xbar_tmp.alloc(size_t(N) * 3);
+    Fbar_tmp.alloc(size_t(N) * 9);
+    eff_out.alloc(kMaxEff * 18);
+    em_out.alloc(kMaxEff * 12);
+    d_nonfinite.alloc(1);
+    CK(cudaMemsetAsync(em_out.p, 0, em_out.n * 8, stream));
+    CK(cudaMemsetAsync(d_nonfinite.p, 0, sizeof(int), stream));
+    const long s0 = substep_index;
+    const double time0 = time;
+    const int na0 = n_active;
+    const std::vector<EffState> eff0 = eff;
+    const std::vector<uint32_t> inact0 = inactive_ids;
+    const auto pend0 = pending;
+    StatePtr pre = get_state(), post = get_state();
+    copy_state(*pre, *cur);
+    RecordPtr rec = get_record();
+    forward_substep(action, pre, post, *rec, false);
+    const std::vector<EffState> eff_stage = eff;
+    check_error();
+    for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
+    CK(cudaMemcpyAsync(d_up[0].p, xb, size_t(N) * 24, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_up[1].p, vb, size_t(N) * 24, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_up[2].p, Fb, size_t(N) * 72, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_up[3].p, Cb, size_t(N) * 72, cudaMemcpyHostToDevice, stream));
+    DevArr<float> barsA, barsB;
+    barsA.alloc(size_t(N) * 24);
+    barsB.alloc(size_t(N) * 24);
+    launch_bars_from_ref(BarBuf{barsA.p, N}, post->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
+    adjoint_step(*pre, *rec, barsA, barsB, 0);
+    launch_bars_to_ref(BarBuf{barsB.p, N}, pre->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
+    CK(cudaMemcpyAsync(xb, d_up[0].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(vb, d_up[1].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(Fb, d_up[2].p, size_t(N) * 72, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(Cb, d_up[3].p, size_t(N) * 72, cudaMemcpyDeviceToHost, stream));
+    std::vector<double> ebh(kMaxEff * 18), emh(kMaxEff * 12);
+    int nonf = 0;
+    CK(cudaMemcpyAsync(ebh.data(), eff_out.p, ebh.size() * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(emh.data(), em_out.p, emh.size() * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(&nonf, d_nonfinite.p, 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    check_error();
+    put_state(pre);
+    put_state(post);
+    put_record(rec);
+    substep_index = s0;
+    time = time0;
+    n_active = na0;
+    inactive_ids = inact0;
+    pending = pend0;
+    const double dt = cfg.dt_substep;
+    double echeck = 0;
+    for (size_t e = 0; e < eff0.size(); e++) {
+        const double* b = &ebh[e * 18];
+        const double* m = &emh[e * 12];
+        V3<double> t_bar = {ebars[12 * e] + m[0], ebars[12 * e + 1] + m[1], ebars[12 * e + 2] + m[2]};
+        M3<double> r_bar;
+        for (int q = 0; q < 9; q++) r_bar.m[q] = ebars[12 * e + 3 + q] + m[3 + q] + b[3 + q];
+        t_bar = t_bar + V3<double>{b[0], b[1], b[2]};
+        V3<double> vlin_bar = V3<double>{b[12], b[13], b[14]} + t_bar * dt;
+        V3<double> w_bar = {b[15], b[16], b[17]};
+        M3<double> r_pre_bar = mzero<double>();
+        advance_rotation_vjp(eff0[e].R, eff_stage[e].w, dt, r_bar, r_pre_bar, w_bar);
+        for (int q = 0; q < 3; q++) ebars[12 * e + q] = t_bar[q];
+        for (int q = 0; q < 9; q++) ebars[12 * e + 3 + q] = r_pre_bar.m[q];
+        const int* mask = eff_shapes[e].action_mask;
+        for (int q = 0; q < 3; q++)
+            if (mask[q]) abar_out[q] += vlin_bar[q];
+        for (int q = 0; q < 3; q++)
+            if (mask[3 + q]) abar_out[3 + q] += w_bar[q];
+        echeck += t_bar.x;
+    }
+    eff = eff0;
+    if (nonf || !std::isfinite(echeck)) {
+        FlumeError e(FLUME_E_ADJOINT, "non-finite adjoint at substep " + std::to_string(s0));
+        e.substep = s0;
+        throw e;
+    }
+}
+
+}  // namespace fl
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using fl::Ctx;
+using fl::FlumeError;
+
+struct flume_ctx {
+    Ctx c;
+};
+
+namespace {
+thread_local flume_error_info g_create_err{};
+
+template <class F>
+int guard(flume_ctx* ctx, F&& f) {
+    flume_error_info* info = ctx ? &ctx->c.last_err : &g_create_err;
+    *info = flume_error_info{};
+    info->particle_id = -1;
+    info->body_id = -1;
+    info->substep = -1;
+    try {
+        f();
+        return FLUME_OK;
+    } catch (const FlumeError& e) {
+        info->code = e.code;
+        info->particle_id = e.pid;
+        info->body_id = e.body;
+        info->substep = e.substep;
+        std::snprintf(info->message, sizeof(info->message), "%s", e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        info->code = FLUME_E_OTHER;
+        std::snprintf(info->message, sizeof(info->message), "%s", e.what());
+        return FLUME_E_OTHER;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int flume_abi_version(void) { return FLUME_B200_ABI_VERSION; }
+
+int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out) {
+    if (!desc || !out) return FLUME_E_ARG;
+    *out = nullptr;
+    flume_ctx* ctx = new flume_ctx();
+    int rc = guard(nullptr, [&] { ctx->c.init(desc, device); });
+    if (rc != FLUME_OK) {
+        ctx->c.last_err = g_create_err;
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return FLUME_OK;
+}
+
+int flume_ctx_destroy(flume_ctx* ctx) {
+    if (!ctx) return FLUME_OK;
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaStream_t s = ctx->c.stream;
+    delete ctx;
+    if (s) cudaStreamDestroy(s);
+    return FLUME_OK;
+}
+
+int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact) {
+    return guard(ctx, [&] {
+        if (!deterministic)
+            throw FlumeError(FLUME_E_ARG, "only the deterministic mode exists (it is also the fast one)");
+        ctx->c.cfg.hard_contact = hard_contact;
+        ctx->c.geom.hard = hard_contact;
+    });
+}
+
+int flume_last_error(const flume_ctx* ctx, flume_error_info* info) {
+    if (!info) return FLUME_E_ARG;
+    *info = ctx ? ctx->c.last_err : g_create_err;
+    return FLUME_OK;
+}
+
+int flume_get_stream(flume_ctx* ctx, void** s) {
+    if (!ctx || !s) return FLUME_E_ARG;
+    *s = ctx->c.stream;
+    return FLUME_OK;
+}
+
+int flume_sync(flume_ctx* ctx) {
+    return guard(ctx, [&] { CK(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+int flume_last_timing(const flume_ctx* ctx, flume_timing* out) {
+    if (!ctx || !out) return FLUME_E_ARG;
+    *out = ctx->c.timing;
+    return FLUME_OK;
+}
+
+int flume_state_upload(flume_ctx* ctx, const flume_state_view* view) {
+    if (!ctx || !view) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.upload(view); });
+}
+
+int flume_state_download(flume_ctx* ctx, flume_state_view* view) {
+    if (!ctx || !view) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.download(view); });
+}
+
+int flume_store_order(flume_ctx* ctx, unsigned* keys, unsigned* ids, long* n_active) {
+    if (!ctx) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (keys) CK(cudaMemcpyAsync(keys, c.cur->p.key, size_t(c.N) * 4, cudaMemcpyDeviceToHost, c.stream));
+        if (ids) CK(cudaMemcpyAsync(ids, c.cur->p.id, size_t(c.N) * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        if (n_active) *n_active = c.n_active;
+    });
+}
+
+int flume_store_positions(flume_ctx* ctx, float* x) {
+    if (!ctx || !x) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        Ctx& c = ctx->c;
+        CK(cudaMemcpyAsync(x, c.cur->p.f, size_t(c.N) * 3 * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int flume_substep(flume_ctx* ctx, const double action[6], int count) {
+    if (!ctx || !action) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.substep(action, count); });
+}
+
+int flume_stage_grid(flume_ctx* ctx, double* mass, double* vel) {
+    if (!ctx) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.stage_grid(mass, vel); });
+}
+
+int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long window,
+                       double* loss_out, double* per_segment) {
+    if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
+    return guard(ctx, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment); });
+}
+
+int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long stride,
+                          long window, double* action_grad, double* loss_out, double* full_loss,
+                          double* per_segment, long* snapshots) {
+    if (!ctx || !actions || !action_grad) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.grad_trajectory(actions, loss, stride, window, action_grad, loss_out, full_loss, per_segment,
+                               snapshots);
+    });
+}
+
+int flume_adjoint_substep(flume_ctx* ctx, const double action[6], double* x_bar, double* v_bar, double* F_bar,
+                          double* C_bar, double* eff_bars, double* action_bar) {
+    if (!ctx || !action || !x_bar || !v_bar || !F_bar || !C_bar || !action_bar) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        std::vector<double> dummy(size_t(fl::kMaxEff) * 12, 0.0);
+        ctx->c.adjoint_substep_api(action, x_bar, v_bar, F_bar, C_bar, eff_bars ? eff_bars : dummy.data(),
+                                   action_bar);
+    });
+}
+
+}  // extern "C"

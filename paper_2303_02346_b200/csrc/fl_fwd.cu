@@ -1,0 +1,639 @@
+// fl_fwd.cu -- forward MLS-MPM substep kernels for sm_100a.
+//
+// One substep (proj/include/flume/mpm.hpp:455-473) is
+//   activate -> keys/sort -> P2G -> grid update -> G2P (+projection) -> rigid
+// with the particle store kept in canonical (cell key, id) order.  P2G and the
+// G2P-adjoint scatter are deterministic without atomics: a CTA owns one 4^3
+// particle block, accumulates each base cell's 27 node contributions in
+// registers in sorted-particle order, folds cells into the block's 6^3 node
+// tile in a fixed order and writes the tile to a per-block staging slot.  The
+// grid update then sums the (at most 8) staging tiles that cover a node in a
+// fixed order.  Every float sum therefore has a run-independent order.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "fl_kernels.h"
+#include "fl_scatter.cuh"
+
+namespace fl {
+
+// ---------------------------------------------------------------------------
+// upload / download / permutation
+// ---------------------------------------------------------------------------
+
+__global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, const double* __restrict__ v,
+                         const double* __restrict__ F, const double* __restrict__ C,
+                         const uint32_t* __restrict__ meta, const uint8_t* __restrict__ active) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int a = 0; a < 3; a++) {
+        raw.x(a)[i] = float(x[3 * size_t(i) + a]);
+        raw.v(a)[i] = float(v[3 * size_t(i) + a]);
+    }
+    for (int k = 0; k < 9; k++) {
+        raw.F(k)[i] = float(F[9 * size_t(i) + k]);
+        raw.C(k)[i] = float(C[9 * size_t(i) + k]);
+    }
+    raw.meta[i] = meta[i];
+    raw.id[i] = uint32_t(i);
+    uint32_t key = g.key_inactive;
+    if (active[i]) cell_key(g, raw.x(0)[i], raw.x(1)[i], raw.x(2)[i], key);
+    raw.key[i] = key;
+}
+
+void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
+                   const double* C, const uint32_t* meta, const uint8_t* active, cudaStream_t s) {
+    if (n <= 0) return;
+    k_upload<<<(n + 255) / 256, 256, 0, s>>>(g, raw, n, x, v, F, C, meta, active);
+}
+
+__global__ void k_make_sortkeys(PBuf st, int n, int idbits, uint64_t* ck, uint32_t* idx) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ck[i] = (uint64_t(st.key[i]) << idbits) | uint64_t(st.id[i]);
+    idx[i] = uint32_t(i);
+}
+
+void launch_make_sortkeys(const Geom& g, const PBuf& st, int n, uint64_t* ck, uint32_t* idx, cudaStream_t s) {
+    if (n <= 0) return;
+    k_make_sortkeys<<<(n + 255) / 256, 256, 0, s>>>(st, n, g.idbits, ck, idx);
+}
+
+__global__ void k_gather(PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    uint32_t s = perm[j];
+#pragma unroll
+    for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + j] = in.f[size_t(c) * in.cap + s];
+    out.meta[j] = in.meta[s];
+    out.id[j] = in.id[s];
+    out.key[j] = in.key[s];
+}
+
+void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    k_gather<<<(n + 255) / 256, 256, 0, s>>>(in, out, perm, n);
+}
+
+__global__ void k_download(PBuf st, int n, double* x, double* v, double* F, double* C) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    size_t id = st.id[i];
+    for (int a = 0; a < 3; a++) {
+        if (x) x[3 * id + a] = double(st.x(a)[i]);
+        if (v) v[3 * id + a] = double(st.v(a)[i]);
+    }
+    for (int k = 0; k < 9; k++) {
+        if (F) F[9 * id + k] = double(st.F(k)[i]);
+        if (C) C[9 * id + k] = double(st.C(k)[i]);
+    }
+}
+
+void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, cudaStream_t s) {
+    if (n <= 0) return;
+    k_download<<<(n + 255) / 256, 256, 0, s>>>(st, n, x, v, F, C);
+}
+
+// ---------------------------------------------------------------------------
+// particle-block / node-block lists from the sorted composite keys
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int ck_block(uint64_t ck, int idbits) { return int(ck >> (idbits + 6)); }
+
+__global__ void k_block_flags(const uint64_t* __restrict__ ck, int n, int idbits, int* flags) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flags[i] = (i == 0 || ck_block(ck[i], idbits) != ck_block(ck[i - 1], idbits)) ? 1 : 0;
+}
+
+void launch_block_flags(const Geom& g, const uint64_t* ck_sorted, int n_active, int* flags, cudaStream_t s) {
+    if (n_active <= 0) return;
+    k_block_flags<<<(n_active + 255) / 256, 256, 0, s>>>(ck_sorted, n_active, g.idbits, flags);
+}
+
+__global__ void k_block_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* starts,
+                                int* n_blocks) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (flags[i]) starts[pos[i]] = i;
+    if (i == n - 1) *n_blocks = pos[i] + flags[i];
+}
+
+void launch_block_scatter(const int* flags, const int* pos, int n_active, int* starts, int* n_blocks,
+                          cudaStream_t s) {
+    if (n_active <= 0) {
+        cudaMemsetAsync(n_blocks, 0, sizeof(int), s);
+        return;
+    }
+    k_block_scatter<<<(n_active + 255) / 256, 256, 0, s>>>(flags, pos, n_active, starts, n_blocks);
+}
+
+__global__ void k_block_recs(Geom g, const uint64_t* __restrict__ ck, const int* __restrict__ starts,
+                             const int* __restrict__ n_blocks, int n_active, int max_blocks, BlockRec* recs,
+                             int* blockmap, int* nbflag) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    int nb = *n_blocks;
+    if (b >= nb || b >= max_blocks) return;
+    int st = starts[b];
+    int en = (b + 1 < nb) ? starts[b + 1] : n_active;
+    int blk = ck_block(ck[st], g.idbits);
+    recs[b] = BlockRec{blk, st, en};
+    blockmap[blk] = b;
+    int bx, by, bz;
+    block_unlin(g, blk, bx, by, bz);
+    for (int d = 0; d < 8; d++) {
+        int x = bx + (d >> 2), y = by + ((d >> 1) & 1), z = bz + (d & 1);
+        if (x < g.NB[0] && y < g.NB[1] && z < g.NB[2]) nbflag[block_lin(g, x, y, z)] = 1;
+    }
+}
+
+void launch_block_recs(const Geom& g, const uint64_t* ck_sorted, const int* starts, const int* n_blocks,
+                       int n_active, int max_blocks, BlockRec* recs, int* blockmap, int* nbflag,
+                       cudaStream_t s) {
+    if (max_blocks <= 0) return;
+    k_block_recs<<<(max_blocks + 255) / 256, 256, 0, s>>>(g, ck_sorted, starts, n_blocks, n_active, max_blocks,
+                                                          recs, blockmap, nbflag);
+}
+
+__global__ void k_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= *n_blocks || b >= max_blocks) return;
+    blockmap[recs[b].block] = b;
+}
+
+void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap,
+                         cudaStream_t s) {
+    if (max_blocks <= 0) return;
+    k_blockmap_set<<<(max_blocks + 255) / 256, 256, 0, s>>>(recs, n_blocks, max_blocks, blockmap);
+}
+
+__global__ void k_nb_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* list,
+                             int* n_list) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (flags[i]) list[pos[i]] = i;
+    if (i == n - 1) *n_list = pos[i] + (flags[i] ? 1 : 0);
+}
+
+void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s) {
+    k_nb_scatter<<<(nbtot + 255) / 256, 256, 0, s>>>(flags, pos, nbtot, list, n_list);
+}
+
+// ---------------------------------------------------------------------------
+// emitter activation (mpm.hpp:435-449); positions precomputed on the host in
+// fp64 from the stage-a effector pose
+// ---------------------------------------------------------------------------
+
+__global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ActEntry e = list[i];
+    if (e.has_xv) {
+        for (int a = 0; a < 3; a++) {
+            st.x(a)[e.slot] = e.x[a];
+            st.v(a)[e.slot] = e.v[a];
+        }
+    }
+    uint32_t key;
+    cell_key(g, st.x(0)[e.slot], st.x(1)[e.slot], st.x(2)[e.slot], key);
+    st.key[e.slot] = key;
+}
+
+void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    k_activate<<<(n + 127) / 128, 128, 0, s>>>(g, st, list, n);
+}
+
+// ---------------------------------------------------------------------------
+// P2G (mpm.hpp:249-287)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kScThreads) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
+                                                    const BlockRec* __restrict__ recs,
+                                                    const int* __restrict__ n_blocks,
+                                                    const ClassInfo* __restrict__ cls, float4* staging,
+                                                    unsigned long long* err, uint32_t substep) {
+    __shared__ ScSmem sm;
+    const int tid = threadIdx.x;
+    const int nb = *n_blocks;
+    const int my_c = tid & 63, my_ox = tid >> 6;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const BlockRec r = recs[b];
+        int bx, by, bz;
+        block_unlin(g, r.block, bx, by, bz);
+        float acc[9][4];
+#pragma unroll
+        for (int k = 0; k < 9; k++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[k][q] = 0.f;
+
+        for (int c0 = r.start; c0 < r.end; c0 += kScChunk) {
+            const int n = min(kScChunk, r.end - c0);
+            if (tid < 64) sm.cs[tid] = sm.ce[tid] = 0;
+            __syncthreads();
+            for (int i = tid; i < n; i += kScThreads) {
+                const uint32_t s = perm[c0 + i];
+                const uint32_t key = st.key[s];
+                float* pay = &sm.u.pay[i * kPayStride];
+                sm.lc[i] = uint8_t(key & 63);
+                float fx[3];
+                int b0 = base_cell(st.x(0)[s], g.inv_dx, fx[0]);
+                int b1 = base_cell(st.x(1)[s], g.inv_dx, fx[1]);
+                int b2 = base_cell(st.x(2)[s], g.inv_dx, fx[2]);
+                uint32_t lc = uint32_t(((b0 - 4 * bx) << 4) | ((b1 - 4 * by) << 2) | (b2 - 4 * bz));
+                bool inside = b0 >= 4 * bx && b0 < 4 * bx + 4 && b1 >= 4 * by && b1 < 4 * by + 4 && b2 >= 4 * bz &&
+                              b2 < 4 * bz + 4 && lc == (key & 63) && b0 + 2 < g.nd[0] && b1 + 2 < g.nd[1] &&
+                              b2 + 2 < g.nd[2];
+                if (!inside) {
+                    atomicMin(err, (unsigned long long)pack_err(substep, ES_P2G_ESCAPE, st.id[s]));
+#pragma unroll
+                    for (int q = 0; q < 16; q++) pay[q] = 0.f;
+                    pay[0] = pay[1] = pay[2] = 1.f;
+                    continue;
+                }
+                const ClassInfo ci = cls[st.meta[s]];
+                M3<float> F, C;
+#pragma unroll
+                for (int k = 0; k < 9; k++) {
+                    F.m[k] = st.F(k)[s];
+                    C.m[k] = st.C(k)[s];
+                }
+                V3<float> v = {st.v(0)[s], st.v(1)[s], st.v(2)[s]};
+                M3<float> fs = (ci.kind == MK_VISCOUS) ? (meye<float>() + C * g.dt) * F : F;
+                bool ok;
+                M3<float> P = corotated_stress(fs, ci.mu, ci.lambda, ok);
+                if (!ok) atomicMin(err, (unsigned long long)pack_err(substep, ES_P2G_STRESS, st.id[s]));
+                M3<float> smat = P * transpose(fs);
+                M3<float> affine = C * ci.mass - smat * (g.stress_coeff * ci.vol0);
+                V3<float> f3 = {fx[0], fx[1], fx[2]};
+                V3<float> a = v * ci.mass - (affine * f3) * g.dx;
+                pay[0] = fx[0];
+                pay[1] = fx[1];
+                pay[2] = fx[2];
+                pay[3] = ci.mass;
+                pay[4] = a.x;
+                pay[5] = a.y;
+                pay[6] = a.z;
+#pragma unroll
+                for (int k = 0; k < 9; k++) pay[7 + k] = affine.m[k] * g.dx;
+            }
+            __syncthreads();
+            sc_ranges(sm, n, tid, kScThreads);
+            __syncthreads();
+            sc_accumulate<4>(sm, my_c, my_ox, acc);
+            __syncthreads();
+        }
+        sc_store_cellpart<4>(sm, my_c, my_ox, acc);
+        __syncthreads();
+        sc_tile(sm, staging + size_t(b) * kTile, tid, kScThreads);
+        __syncthreads();
+    }
+}
+
+void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks, int grid,
+                const ClassInfo* cls, float4* staging, unsigned long long* err, uint32_t substep, cudaStream_t s) {
+    k_p2g<<<grid, kScThreads, 0, s>>>(g, st, perm, recs, n_blocks, cls, staging, err, substep);
+}
+
+// ---------------------------------------------------------------------------
+// grid update (mpm.hpp:289-320): one thread per node of each touched node block
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __restrict__ blockmap,
+                                                 const float4* __restrict__ staging, int bx, int by, int bz, int lx,
+                                                 int ly, int lz) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int d = 0; d < 8; d++) {
+        const int ddx = d >> 2, ddy = (d >> 1) & 1, ddz = d & 1;
+        if ((ddx && lx >= 2) || (ddy && ly >= 2) || (ddz && lz >= 2)) continue;
+        const int px = bx - ddx, py = by - ddy, pz = bz - ddz;
+        if (px < 0 || py < 0 || pz < 0) continue;
+        const int slot = blockmap[block_lin(g, px, py, pz)];
+        if (slot < 0) continue;
+        const int t = (lx + 4 * ddx) * 36 + (ly + 4 * ddy) * 6 + (lz + 4 * ddz);
+        const float4 v = staging[size_t(slot) * kTile + t];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restrict__ nb_list,
+                                                     const int* __restrict__ n_nb, const int* __restrict__ blockmap,
+                                                     const float4* __restrict__ staging, float4* gridv, float4* gridv0,
+                                                     EffSet eff) {
+    const int n = *n_nb;
+    const int sub = threadIdx.x >> 6, l = threadIdx.x & 63;
+    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    for (int k = blockIdx.x * 4 + sub; k < n; k += gridDim.x * 4) {
+        const int nbid = nb_list[k];
+        int bx, by, bz;
+        block_unlin(g, nbid, bx, by, bz);
+        const float4 mp = gather_staging(g, blockmap, staging, bx, by, bz, lx, ly, lz);
+        const float m = mp.x;
+        const size_t idx = size_t(nbid) * 64 + l;
+        V3<float> v0 = {0.f, 0.f, 0.f}, v = {0.f, 0.f, 0.f};
+        if (m > g.mass_eps) {
+            const float inv = 1.0f / m;
+            v0 = V3<float>{mp.y * inv, mp.z * inv, mp.w * inv};
+            v = V3<float>{v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
+            const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
+            v = wall_bc_dev(g, i, j, kk, v);
+            const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
+            for (int e = 0; e < eff.n; e++) v = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, v);
+        }
+        gridv[idx] = make_float4(v.x, v.y, v.z, m);
+        if (gridv0) gridv0[idx] = make_float4(v0.x, v0.y, v0.z, m);
+    }
+}
+
+void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
+                        const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, cudaStream_t s) {
+    k_grid_update<<<grid, 256, 0, s>>>(g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff);
+}
+
+// ---------------------------------------------------------------------------
+// G2P (mpm.hpp:338-384) with the per-material return map
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
+                                             const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
+                                             const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
+                                             RigidDev rd, unsigned long long* err, uint32_t substep) {
+    __shared__ float4 vt[kTile];
+    const int tid = threadIdx.x;
+    const int nb = *n_blocks;
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const BlockRec r = recs[b];
+        int bx, by, bz;
+        block_unlin(g, r.block, bx, by, bz);
+        __syncthreads();
+        load_tile(g, gridv, vt, bx, by, bz, tid, 128);
+        __syncthreads();
+        for (int j = r.start + tid; j < r.end; j += 128) {
+            const uint32_t s = perm[j];
+            const V3<float> x = {in.x(0)[s], in.x(1)[s], in.x(2)[s]};
+            const uint32_t meta = in.meta[s];
+            const uint32_t pid = in.id[s];
+            const ClassInfo ci = cls[meta];
+            StencilW sw;
+            stencil_weights(g, x, bx, by, bz, sw);
+            V3<float> vraw;
+            M3<float> cnew;
+            g2p_gather(g, vt, sw, vraw, cnew);
+            V3<float> vuse = vraw;
+            const float vn = norm(vraw);
+            if (vn > g.vmax) vuse = vraw * (g.vmax / vn);
+            V3<float> xn;
+#pragma unroll
+            for (int a = 0; a < 3; a++) xn[a] = clamp_ref(x[a] + vuse[a] * g.dt, g.lo[a], g.hi[a]);
+            M3<float> F;
+#pragma unroll
+            for (int k = 0; k < 9; k++) F.m[k] = in.F(k)[s];
+            const M3<float> ftr = (meye<float>() + cnew * g.dt) * F;
+            M3<float> fnew = ftr;
+            bool ok = true;
+            switch (ci.kind) {
+                case MK_LIQUID:
+                case MK_VISCOUS: fnew = liquid_project(ftr, ok); break;
+                case MK_PLASTIC: fnew = box_yield_project(ftr, ci.theta_c, ci.theta_s, ok); break;
+                case MK_NONNEWTONIAN: fnew = von_mises_project(ftr, ci.sigma_y, ci.mu, ok); break;
+                default: break;
+            }
+            if (!ok) atomicMin(err, (unsigned long long)pack_err(substep, ES_G2P_PROJECT, pid));
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                out.x(a)[j] = xn[a];
+                out.v(a)[j] = vuse[a];
+            }
+#pragma unroll
+            for (int k = 0; k < 9; k++) {
+                out.F(k)[j] = fnew.m[k];
+                out.C(k)[j] = cnew.m[k];
+            }
+            out.meta[j] = meta;
+            out.id[j] = pid;
+            uint32_t key;
+            cell_key(g, xn.x, xn.y, xn.z, key);
+            out.key[j] = key;
+            if (ci.rigid >= 0) {
+                const int mr = rd.mrank[pid];
+                rd.mslot[mr] = j;
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    rd.mstart[3 * mr + a] = x[a];
+                    rd.mid[3 * mr + a] = xn[a];
+                }
+            }
+        }
+    }
+}
+
+void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd, unsigned long long* err,
+                uint32_t substep, cudaStream_t s) {
+    k_g2p<<<grid, 128, 0, s>>>(g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep);
+}
+
+__global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
+    int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    uint32_t s = perm[j];
+    for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + j] = in.f[size_t(c) * in.cap + s];
+    out.meta[j] = in.meta[s];
+    out.id[j] = in.id[s];
+    out.key[j] = g.key_inactive;
+}
+
+void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s) {
+    int m = n - n_active;
+    if (m <= 0) return;
+    k_tail_copy<<<(m + 255) / 256, 256, 0, s>>>(g, in, out, perm, n_active, n);
+}
+
+// ---------------------------------------------------------------------------
+// rigid shape matching (mpm.hpp:386-416, materials.hpp:163-202)
+// ---------------------------------------------------------------------------
+
+constexpr int kRigidQ = 17;  // m, m x[3], m x r^T[9], m r[3], count
+
+__global__ void __launch_bounds__(256) k_rigid_partial(PBuf out, RigidDev rd, const int* chunk_m0,
+                                                       const int* chunk_m1, double* partial) {
+    __shared__ double red[256];
+    const int c = blockIdx.x;
+    const int m0 = chunk_m0[c], m1 = chunk_m1[c];
+    double acc[kRigidQ];
+#pragma unroll
+    for (int q = 0; q < kRigidQ; q++) acc[q] = 0.0;
+    for (int r = m0 + threadIdx.x; r < m1; r += 256) {
+        const int j = rd.mslot[r];
+        if (j < 0) continue;
+        const double m = rd.mass[r];
+        const double x[3] = {double(out.x(0)[j]), double(out.x(1)[j]), double(out.x(2)[j])};
+        const double* re = rd.rest + 3 * size_t(r);
+        acc[0] += m;
+        for (int a = 0; a < 3; a++) acc[1 + a] += m * x[a];
+        for (int a = 0; a < 3; a++)
+            for (int b = 0; b < 3; b++) acc[4 + 3 * a + b] += m * x[a] * re[b];
+        for (int a = 0; a < 3; a++) acc[13 + a] += m * re[a];
+        acc[16] += 1.0;
+    }
+    for (int q = 0; q < kRigidQ; q++) {
+        red[threadIdx.x] = acc[q];
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) partial[size_t(c) * kRigidQ + q] = red[0];
+        __syncthreads();
+    }
+}
+
+// one thread per body: fit = Kabsch(A), recorded for the adjoint
+__global__ void k_rigid_solve(RigidDev rd, int nchunks, const int* chunk_body, const double* partial,
+                              unsigned long long* err, uint32_t substep) {
+    const int body = blockIdx.x * blockDim.x + threadIdx.x;
+    if (body >= rd.nbody) return;
+    double s[kRigidQ];
+    for (int q = 0; q < kRigidQ; q++) s[q] = 0.0;
+    for (int c = 0; c < nchunks; c++) {
+        if (chunk_body[c] != body) continue;
+        for (int q = 0; q < kRigidQ; q++) s[q] += partial[size_t(c) * kRigidQ + q];
+    }
+    double* fit = rd.fit + 24 * size_t(body);
+    const int nmem = rd.off[body + 1] - rd.off[body];
+    fit[22] = (double(nmem) == s[16]) ? 0.0 : 1.0;  // skip unless every member is active
+    fit[23] = 1.0;
+    if (fit[22] != 0.0) return;
+    const double total = s[0];
+    V3<double> c = {s[1] / total, s[2] / total, s[3] / total};
+    M3<double> A;
+    for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) A.m[3 * a + b] = s[4 + 3 * a + b] - c[a] * s[13 + b];
+    Svd<double> t = svd3(A);
+    double smax = t.s.x > 1e-30 ? t.s.x : 1e-30;
+    if (t.s.y < 1e-12 * smax) {
+        atomicMin(err, (unsigned long long)pack_err(substep, ES_RIGID, uint32_t(rd.body_id[body])));
+        fit[23] = 0.0;
+    }
+    M3<double> R = t.U * transpose(t.V);
+    if (det(A) < 0.0) R = t.U * mdiag(V3<double>{1.0, 1.0, -1.0}) * transpose(t.V);
+    for (int k = 0; k < 9; k++) fit[k] = R.m[k];
+    for (int a = 0; a < 3; a++) fit[9 + a] = c[a];
+    for (int k = 0; k < 9; k++) fit[12 + k] = A.m[k];
+    fit[21] = total;
+}
+
+__global__ void k_rigid_apply(Geom g, PBuf out, RigidDev rd) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rd.nmem) return;
+    const int body = rd.member_body[r];
+    const double* fit = rd.fit + 24 * size_t(body);
+    if (fit[22] != 0.0) return;
+    const int j = rd.mslot[r];
+    const double* re = rd.rest + 3 * size_t(r);
+    double xn[3];
+    for (int a = 0; a < 3; a++) {
+        double raw = fit[3 * a] * re[0] + fit[3 * a + 1] * re[1] + fit[3 * a + 2] * re[2] + fit[9 + a];
+        xn[a] = clamp_ref(raw, double(g.lo[a]), double(g.hi[a]));
+    }
+    const double inv_dt = 1.0 / double(g.dt);
+    for (int a = 0; a < 3; a++) {
+        out.x(a)[j] = float(xn[a]);
+        out.v(a)[j] = float((xn[a] - double(rd.mstart[3 * r + a])) * inv_dt);
+    }
+    uint32_t key;
+    cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key);
+    out.key[j] = key;
+}
+
+void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body, const int* chunk_m0,
+                  const int* chunk_m1, double* partial, unsigned long long* err, uint32_t substep, cudaStream_t s) {
+    if (rd.nbody == 0) return;
+    k_rigid_partial<<<nchunks, 256, 0, s>>>(out, rd, chunk_m0, chunk_m1, partial);
+    k_rigid_solve<<<(rd.nbody + 31) / 32, 32, 0, s>>>(rd, nchunks, chunk_body, partial, err, substep);
+    k_rigid_apply<<<(rd.nmem + 255) / 256, 256, 0, s>>>(g, out, rd);
+}
+
+// ---------------------------------------------------------------------------
+// target_point / hold_initial losses at segment boundaries (losses.hpp:474-551)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const ClassInfo* __restrict__ cls,
+                                                      LossSet ls, uint32_t mask, uint32_t key_inactive,
+                                                      double* partial) {
+    __shared__ double red[256];
+    double acc[kMaxLossTerms];
+    for (int k = 0; k < kMaxLossTerms; k++) acc[k] = 0.0;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        const int body = cls[st.meta[i]].body;
+        const bool active = st.key[i] != key_inactive;
+        for (int k = 0; k < ls.n; k++) {
+            if (!((mask >> k) & 1u) || ls.t[k].body != body) continue;
+            const LossTermDev& t = ls.t[k];
+            double d[3];
+            if (t.kind == LK_TARGET) {
+                if (!active) continue;
+                for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - t.goal[a];
+            } else {
+                const uint32_t id = st.id[i];
+                for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - double(t.init[3 * size_t(id) + a]);
+            }
+            const double nn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+            acc[k] += (t.kind == LK_TARGET && t.squared) ? nn * nn : nn;
+        }
+    }
+    for (int k = 0; k < ls.n; k++) {
+        red[threadIdx.x] = acc[k];
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) partial[size_t(blockIdx.x) * kMaxLossTerms + k] = red[0];
+        __syncthreads();
+    }
+}
+
+__global__ void k_loss_final(const double* partial, int nblocks, LossSet ls, uint32_t mask, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double total = 0.0;
+    for (int k = 0; k < ls.n; k++) {
+        if (!((mask >> k) & 1u)) continue;
+        double s = 0.0;
+        for (int b = 0; b < nblocks; b++) s += partial[size_t(b) * kMaxLossTerms + k];
+        total += ls.t[k].weight * s;
+    }
+    *out = total;
+}
+
+void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, double* partial,
+                 double* out, uint32_t key_inactive, cudaStream_t s) {
+    k_loss_partial<<<kLossBlocks, 256, 0, s>>>(st, n, cls, ls, mask, key_inactive, partial);
+    k_loss_final<<<1, 32, 0, s>>>(partial, kLossBlocks, ls, mask, out);
+}
+
+int p2g_occupancy_grid() {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2g, kScThreads, 0);
+    if (per < 1) per = 1;
+    return sms * per;
+}
+
+int g2p_occupancy_grid() {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_g2p, 128, 0);
+    if (per < 1) per = 1;
+    return sms * per;
+}
+
+}  // namespace fl

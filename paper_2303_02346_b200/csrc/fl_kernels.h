@@ -1,0 +1,117 @@
+// fl_kernels.h -- launch wrappers for the sm_100a kernels (host side view).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fl_layout.cuh"
+
+namespace fl {
+
+// rigid-body bookkeeping for one substep (forward record / backward input)
+struct RigidDev {
+    int nbody;
+    int nmem;                 // total members over all bodies
+    const int* off;           // [nbody+1] member offsets
+    const int* mrank;         // [N] member rank (global, off[body]+j) by particle id, -1 otherwise
+    const double* rest;       // [3*nmem] rest offsets (x0 - c0)
+    const double* mass;       // [nmem] member masses
+    const double* smrest;     // [3*nbody] sum_j m_j rest_j
+    const double* total;      // [nbody] total mass
+    const int* body_id;       // [nbody] reference body id
+    const int* member_body;   // [nmem] body index of each member
+    // per-substep arrays
+    int* mslot;               // [nmem] sorted position of the member in the post-g2p buffer (-1 inactive)
+    float* mstart;            // [3*nmem] stage-a position (rigid_body_pass start_positions)
+    float* mid;               // [3*nmem] post-g2p position
+    double* fit;              // [nbody*24]: R[9] c[3] A[9] total skip ok
+};
+
+struct ActEntry {
+    int slot;
+    int has_xv;
+    float x[3];
+    float v[3];
+};
+
+struct EmitAdjEntry {
+    int slot;
+    int eff;
+    int mask[3];  // 1 when the spawn clamp was active on that axis
+    double local_pos[3];
+    double local_vel[3];
+};
+
+constexpr int kMaxLossTerms = 8;
+enum LossKindId : int { LK_TARGET = 0, LK_HOLD = 1 };
+struct LossTermDev {
+    int kind;
+    int body;
+    int squared;
+    double weight;
+    double goal[3];
+    const float* init;  // hold_initial: [3*N] initial positions by particle id
+};
+struct LossSet {
+    int n;
+    LossTermDev t[kMaxLossTerms];
+};
+
+constexpr int kLossBlocks = 296;
+constexpr int kEffBlocks = 592;
+constexpr int kRigidChunk = 2048;
+
+// ---- forward ----
+void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
+                   const double* C, const uint32_t* meta, const uint8_t* active, cudaStream_t s);
+void launch_make_sortkeys(const Geom& g, const PBuf& st, int n, uint64_t* ck, uint32_t* idx, cudaStream_t s);
+void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
+void launch_block_flags(const Geom& g, const uint64_t* ck_sorted, int n_active, int* flags, cudaStream_t s);
+void launch_block_scatter(const int* flags, const int* pos, int n_active, int* starts, int* n_blocks, cudaStream_t s);
+void launch_block_recs(const Geom& g, const uint64_t* ck_sorted, const int* starts, const int* n_blocks,
+                       int n_active, int max_blocks, BlockRec* recs, int* blockmap, int* nbflag,
+                       cudaStream_t s);
+void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap, cudaStream_t s);
+void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s);
+void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s);
+void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                int grid, const ClassInfo* cls, float4* staging, unsigned long long* err, uint32_t substep,
+                cudaStream_t s);
+void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
+                        const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, cudaStream_t s);
+void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs,
+                const int* n_blocks, int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd,
+                unsigned long long* err, uint32_t substep, cudaStream_t s);
+void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
+void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body,
+                  const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
+                  uint32_t substep, cudaStream_t s);
+void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, cudaStream_t s);
+void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
+                 double* partial, double* out, uint32_t key_inactive, cudaStream_t s);
+
+// ---- backward ----
+void launch_loss_grad(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
+                      BarBuf bars, uint32_t key_inactive, cudaStream_t s);
+void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, const int* chunk_body,
+                      const int* chunk_m0, const int* chunk_m1, double* partial, float* start_bar,
+                      double* abar, cudaStream_t s);
+void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                    int grid, const ClassInfo* cls, const float4* gridv, BarBuf post, float* xbar_tmp,
+                    float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar, cudaStream_t s);
+void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
+                     const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
+                     double* eff_partial, double* eff_out, cudaStream_t s);
+void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                    int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
+                    const float* Fbar_tmp, BarBuf out, int* nonfinite, cudaStream_t s);
+void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
+void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
+void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb,
+                          const double* Fb, const double* Cb, cudaStream_t s);
+void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* vb, double* Fb, double* Cb,
+                        cudaStream_t s);
+
+int p2g_occupancy_grid();
+int g2p_occupancy_grid();
+
+}  // namespace fl

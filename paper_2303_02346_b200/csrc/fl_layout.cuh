@@ -1,0 +1,156 @@
+// fl_layout.cuh -- HBM data layout shared by the kernels and the host engine.
+//
+// Particles: SoA fp32 (x[3], v[3], F[9], C[9]) plus u32 class / id / cell-key
+// per slot; every trajectory state is one such buffer.  The grid is dense but
+// block-major: 4x4x4 node blocks, node (i,j,k) lives at
+//     block_lin(i>>2, j>>2, k>>2) * 64 + ((i&3)<<4 | (j&3)<<2 | (k&3)).
+// Particles are kept in canonical order: stable by (cell key, particle id),
+// where the cell key of a particle is
+//     block_lin(base>>2) << 6 | (base&3) packed like a node,   base = floor(x/dx - 0.5)
+// (the B-spline base cell of quad_weights, proj/include/flume/mpm.hpp:55-71).
+// A 4x4x4 block of base cells (a "particle block") scatters into the 6x6x6
+// node tile [4B, 4B+6): its own node block plus two planes of the next ones.
+#pragma once
+
+#include <cstdint>
+
+#include "fl_physics.cuh"
+
+namespace fl {
+
+constexpr int kMaxEff = 8;
+constexpr uint32_t kTile = 216;  // 6^3 nodes per particle-block tile
+
+struct Geom {
+    int nd[3];      // node dims (res+1 per axis, types.hpp:84-88)
+    int NB[3];      // 4^3 blocks per axis (cover nd)
+    int nbtot;      // NB0*NB1*NB2
+    uint32_t key_inactive;  // nbtot << 6, sorts after every valid key
+    int keybits;    // bits needed for key_inactive
+    int idbits;     // bits needed for particle ids
+    float dx, inv_dx, dt;
+    float lo[3], hi[3];  // clamp_to_interior bounds [dx, L-dx] (mpm.hpp:330-336)
+    int bw;              // wall band (types.hpp:61)
+    float vmax;          // cfl_fraction * dx / dt (mpm.hpp:322-328)
+    float mass_eps;
+    float gdt[3];        // gravity * dt
+    float eps_cells;
+    int hard;
+    float k4;            // 4 / dx^2
+    float stress_coeff;  // dt * 4 / dx^2 (mpm.hpp:259)
+};
+
+// one entry per distinct (material, body, mass, volume0) tuple
+struct ClassInfo {
+    int kind;
+    int body;
+    int rigid;   // rigid-body index or -1
+    float mass, vol0;
+    float mu, lambda, theta_c, theta_s, sigma_y;
+};
+
+struct EffSet {
+    int n;
+    EffK<float> e[kMaxEff];
+};
+
+struct PBuf {
+    float* f;         // [24][cap]: x0 x1 x2 v0 v1 v2 F00..F22 C00..C22
+    uint32_t* meta;   // class index
+    uint32_t* id;     // reference particle index
+    uint32_t* key;    // cell key (key_inactive for inactive)
+    int cap;
+    __host__ __device__ float* x(int a) const { return f + size_t(a) * cap; }
+    __host__ __device__ float* v(int a) const { return f + size_t(3 + a) * cap; }
+    __host__ __device__ float* F(int k) const { return f + size_t(6 + k) * cap; }
+    __host__ __device__ float* C(int k) const { return f + size_t(15 + k) * cap; }
+};
+
+// 24-float cotangent buffer with the same component order (x v F C)
+struct BarBuf {
+    float* f;
+    int cap;
+    __host__ __device__ float* x(int a) const { return f + size_t(a) * cap; }
+    __host__ __device__ float* v(int a) const { return f + size_t(3 + a) * cap; }
+    __host__ __device__ float* F(int k) const { return f + size_t(6 + k) * cap; }
+    __host__ __device__ float* C(int k) const { return f + size_t(15 + k) * cap; }
+};
+
+struct BlockRec {
+    int block;  // particle-block linear index
+    int start;  // sorted positions [start, end)
+    int end;
+};
+
+// error record: lexicographic min over (substep, stage, particle/body)
+enum ErrStage : uint32_t {
+    ES_P2G_ESCAPE = 1,
+    ES_P2G_STRESS = 2,
+    ES_G2P_PROJECT = 3,
+    ES_RIGID = 4,
+};
+
+__host__ __device__ inline uint64_t pack_err(uint32_t substep, uint32_t stage, uint32_t who) {
+    return (uint64_t(substep) << 36) | (uint64_t(stage) << 32) | uint64_t(who);
+}
+
+__host__ __device__ inline int block_lin(const Geom& g, int bx, int by, int bz) {
+    return (bx * g.NB[1] + by) * g.NB[2] + bz;
+}
+__host__ __device__ inline void block_unlin(const Geom& g, int b, int& bx, int& by, int& bz) {
+    bz = b % g.NB[2];
+    int r = b / g.NB[2];
+    by = r % g.NB[1];
+    bx = r / g.NB[1];
+}
+__host__ __device__ inline size_t node_index(const Geom& g, int i, int j, int k) {
+    return size_t(block_lin(g, i >> 2, j >> 2, k >> 2)) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3));
+}
+
+// Canonical base-cell computation.  Written with explicitly rounded fp32 ops
+// (no FMA contraction) so a CPU recomputation from the same fp32 positions is
+// bit-identical.
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+#else
+inline float mul_rn(float a, float b) { volatile float r = a * b; return r; }
+inline float sub_rn(float a, float b) { volatile float r = a - b; return r; }
+#endif
+
+__host__ __device__ inline int base_cell(float x, float inv_dx, float& fx) {
+    float xs = mul_rn(x, inv_dx);
+    float b = floorf(sub_rn(xs, 0.5f));
+    fx = sub_rn(xs, b);
+    return int(b);
+}
+
+// returns false when the stencil leaves the grid (mpm.hpp:265-269)
+__host__ __device__ inline bool cell_key(const Geom& g, float x0, float x1, float x2, uint32_t& key) {
+    float f;
+    int b0 = base_cell(x0, g.inv_dx, f), b1 = base_cell(x1, g.inv_dx, f), b2 = base_cell(x2, g.inv_dx, f);
+    bool ok = b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 + 2 < g.nd[0] && b1 + 2 < g.nd[1] && b2 + 2 < g.nd[2];
+    if (!ok) {
+        b0 = b0 < 0 ? 0 : (b0 > g.nd[0] - 3 ? g.nd[0] - 3 : b0);
+        b1 = b1 < 0 ? 0 : (b1 > g.nd[1] - 3 ? g.nd[1] - 3 : b1);
+        b2 = b2 < 0 ? 0 : (b2 > g.nd[2] - 3 ? g.nd[2] - 3 : b2);
+    }
+    key = (uint32_t(block_lin(g, b0 >> 2, b1 >> 2, b2 >> 2)) << 6) |
+          uint32_t(((b0 & 3) << 4) | ((b1 & 3) << 2) | (b2 & 3));
+    return ok;
+}
+
+// quadratic B-spline weights (mpm.hpp:63-68) and their d/dfx
+__host__ __device__ inline void bspline_w(float fx, float w[3]) {
+    float a = 1.5f - fx, b = fx - 1.0f, c = fx - 0.5f;
+    w[0] = 0.5f * a * a;
+    w[1] = 0.75f - b * b;
+    w[2] = 0.5f * c * c;
+}
+__host__ __device__ inline void bspline_dw(float fx, float dw[3]) {
+    dw[0] = fx - 1.5f;
+    dw[1] = -2.0f * (fx - 1.0f);
+    dw[2] = fx - 0.5f;
+}
+
+}  // namespace fl
