@@ -1,0 +1,362 @@
+#!/usr/bin/env python3
+"""Benchmark: MPM particle-substeps/s, forward+backward, on the 1M-particle multi-material scene.
+
+One "step" = one grad_trajectory (grad.hpp:61-134) over one segment of the c4
+scooping scene (1,027,233 particles of water + an
+elastic floater on a 128^3 grid, a three-box ladle effector), i.e. T forward
+substeps with the trajectory kept in HBM, a target-point loss, and T adjoint
+substeps producing the action gradient.  value = particles * T / device time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs one independent replica per GPU (torchrun; weak scaling).  The
+reference arm (--impl reference) times the unmodified reference engine
+(oracle/_ref, proj/include/flume compiled as-is) on this host's CPU cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MPM particle-substeps/sec fwd & fwd+bwd at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "particle-substeps/s"
+SCENE = "c4"
+HORIZON = 50  # one segment of c4 (optimizer.segment_length)
+
+# algorithmic bytes per launch unit: fp32 state, each
+# field counted once per kernel that must move it; N = active particles, A =
+# touched nodes (64 per node block)
+KERNELS = ["p2g", "grid_update", "g2p", "sort", "g2p_adjoint", "grid_adjoint", "p2g_adjoint", "rigid", "other"]
+ALG_BYTES = {
+    "p2g": (100, 16),           # read x v F C class | write m,p per node
+    "grid_update": (0, 44),     # read m,p (16) write v,m (16) + v0,m (16) - forward writes only v: use 44 avg
+    "g2p": (148, 16),           # read x F class, write x v F C | read v,m per node
+    "g2p_adjoint": (196, 32),   # read x F class + 4 bars, write x_bar F_bar | read v, write v_bar
+    "grid_adjoint": (0, 48),
+    "p2g_adjoint": (244, 16),   # read x v F C class + x_bar F_bar, write 4 bars | read m_bar,p_bar
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [s.strip() for s in out.stdout.strip().split(",")]
+                if len(f) == 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_sample(substeps: int = 4, stride: int = 2):
+    """The reference engine (oracle/_ref) on this host, single-threaded like the reference:
+    grad_trajectory over `substeps` substeps of the same scene (SURVEY.md 8(d) protocol)."""
+    from oracle import ref
+    from paper_2303_02346_b200 import scenes
+    spec = scenes.load(SCENE)
+    r = ref.RefWorld(spec)
+    init = np.array(spec["optimizer"]["init"], dtype=np.float64)
+    t0 = time.perf_counter()
+    r.grad_trajectory(init.reshape(1, 6), substeps, stride=stride)
+    dt = time.perf_counter() - t0
+    return r.n * substeps / dt, r.n, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libflume_ref.so not built"}))
+        return
+    sub = 2
+    for _ in range(args.warmup):
+        cpu_reference_sample(sub, 1)
+    rates, times, n = [], [], 0
+    for _ in range(args.steps):
+        rate, n, dt = cpu_reference_sample(sub, 1)
+        rates.append(rate)
+        times.append(dt)
+    total_t = sum(times)
+    value = n * sub * args.steps / total_t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{SCENE}_scooping grad_trajectory, {sub}-substep sample per step, stride 1",
+                       "particles": n, "grid": "128^3"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": f"grad_trajectory over {sub} substeps of {SCENE} per step (1 core, g++ -O3)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import ctypes as C
+
+    import paper_2303_02346_b200 as fl
+    from paper_2303_02346_b200 import _abi, scenes
+    from paper_2303_02346_b200.api import _dp
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world_size > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    spec = scenes.load(SCENE)
+    w = fl.build_scene(spec)
+    lib = _abi.load()
+    ws = fl.GpuWorkspace(w.scene, device=local)
+    ctx = ws.ctx
+    n = w.scene.n_particles
+    T = args.horizon
+    acts = fl.ActionTrajectory(1, T, w.init_action.reshape(1, 6))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+
+    # pinned host copies of the inputs for the end-to-end leg
+    import torch
+    pin = {k: torch.empty(getattr(w.state, k).shape, dtype=torch.float64).pin_memory()
+           for k in ("x", "v", "F", "C")}
+    for k in pin:
+        pin[k].numpy()[...] = getattr(w.state, k)
+    effs = fl.GpuWorkspace._eff_to_c(w.state.effectors)
+    view = _abi.StateView()
+    view.time, view.substep_index = 0.0, 0
+    view.x, view.v = (C.cast(pin["x"].data_ptr(), C.POINTER(C.c_double)),
+                      C.cast(pin["v"].data_ptr(), C.POINTER(C.c_double)))
+    view.F, view.C = (C.cast(pin["F"].data_ptr(), C.POINTER(C.c_double)),
+                      C.cast(pin["C"].data_ptr(), C.POINTER(C.c_double)))
+    view.effectors = effs
+    h2d = sum(pin[k].numel() * 8 for k in pin)
+    a_c = acts._c()
+    grad = np.zeros((1, 6))
+    lo, fu, snaps = C.c_double(), C.c_double(), C.c_long()
+    per = np.zeros(1)
+
+    def check(rc):
+        fl.api._raise(lib, ctx, rc)
+
+    def upload():
+        check(lib.flume_state_upload(ctx, C.byref(view)))
+
+    def step():
+        check(lib.flume_grad_trajectory(ctx, C.byref(a_c), C.byref(loss.desc), 0, 0, _dp(grad), C.byref(lo),
+                                        C.byref(fu), _dp(per), C.byref(snaps)))
+
+    def fwd_only():
+        check(lib.flume_substep(ctx, _dp(w.init_action), T))
+
+    upload()
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    check(lib.flume_sync(ctx))
+
+    # ---- timed: device time over exactly K steps (inputs resident in HBM) ----
+    check(lib.flume_profile(ctx, 1))
+    launches = 0
+    fwd_ms = bwd_ms = 0.0
+    with ClockSampler(local) as clocks:
+        check(lib.flume_timer_mark(ctx, 0))
+        for _ in range(args.steps):
+            step()
+            t = ws.last_timing()
+            launches += t.launches
+            fwd_ms += t.forward_ms
+            bwd_ms += t.backward_ms
+        check(lib.flume_timer_mark(ctx, 1))
+        ms = C.c_double()
+        check(lib.flume_timer_elapsed(ctx, 0, 1, C.byref(ms)))
+    total_ms = ms.value
+    kms = (C.c_double * 9)()
+    kcnt = (C.c_long * 9)()
+    check(lib.flume_kernel_times(ctx, kms, kcnt, 9))
+    check(lib.flume_profile(ctx, 0))
+    if dist:
+        tt = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = world_size * n * T * args.steps / (total_ms / 1e3)
+
+    # ---- forward-only rate (mpm_substep chain), same scene ----
+    upload()
+    check(lib.flume_sync(ctx))
+    check(lib.flume_timer_mark(ctx, 2))
+    for _ in range(args.steps):
+        fwd_only()
+    check(lib.flume_timer_mark(ctx, 3))
+    fms = C.c_double()
+    check(lib.flume_timer_elapsed(ctx, 2, 3, C.byref(fms)))
+    fwd_value = world_size * n * T * args.steps / (fms.value / 1e3)
+
+    # ---- end to end through the public C ABI: H2D of the state from pinned host
+    #      memory, grad_trajectory, D2H of loss + action gradient, every step ----
+    check(lib.flume_timer_mark(ctx, 4))
+    for _ in range(args.steps):
+        upload()
+        step()  # returns loss/gradient in host memory (D2H inside)
+    check(lib.flume_timer_mark(ctx, 5))
+    ems = C.c_double()
+    check(lib.flume_timer_elapsed(ctx, 4, 5, C.byref(ems)))
+    e2e_ms = ems.value
+    if dist:
+        tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = world_size * n * T * args.steps / (e2e_ms / 1e3)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel class ----
+    peak, peak_kind = peaks()
+    nb_nodes = None
+    kern = {}
+    for i, name in enumerate(KERNELS):
+        if kcnt[i]:
+            kern[name] = {"ms_total": kms[i], "launches": int(kcnt[i]), "us_per_launch": 1e3 * kms[i] / kcnt[i]}
+    dom = max((k for k in kern if k in ALG_BYTES), key=lambda k: kern[k]["ms_total"])
+    # active nodes per substep: touched node blocks x 64 (measured on the first step's lists)
+    A = int(0.155 * n * 1.6)  # fallback estimate; replaced by the measured value below
+    try:
+        keys, ids, na, _ = ws.store_order(w.state)
+        blocks = np.unique(keys[:na] >> 6)
+        nd = w.scene.node_dims
+        NB = [(d + 3) // 4 for d in nd]
+        bz = blocks % NB[2]
+        by = (blocks // NB[2]) % NB[1]
+        bx = blocks // (NB[2] * NB[1])
+        touched = set()
+        for dxx in (0, 1):
+            for dyy in (0, 1):
+                for dzz in (0, 1):
+                    touched.update(((bx + dxx) * NB[1] + by + dyy) * NB[2] + bz + dzz)
+        A = 64 * len(touched)
+    except Exception:
+        pass
+    pb, nb = ALG_BYTES[dom]
+    alg = pb * n + nb * A
+    per_launch_s = kern[dom]["ms_total"] / kern[dom]["launches"] / 1e3
+    achieved = alg / per_launch_s / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(dom)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if not args.no_cpu:
+        try:
+            rate, rn, dt = cpu_reference_sample(4, 2)
+            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"reference grad_trajectory, {SCENE} ({rn} particles), 4 substeps, stride 2, "
+                             f"{dt:.1f} s on 1 host core (g++ -O3 build of proj/include)"}
+        except Exception as e:  # keep the GPU line even if the host leg fails
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference scene JSON c4 (SURVEY.md App. A) sampled by the reference lattice+jitter rule",
+        "config": {"workload": f"{SCENE}_scooping: grad_trajectory, 1 segment x {T} substeps, stride {T} "
+                               "(forward + adjoint, trajectory kept in HBM), target_point loss",
+                   "particles": n, "grid": "128^3", "active_nodes": A, "horizon": T,
+                   "l2": "inputs larger than L2 (trajectory store ~%.1f GB per step)" % (n * 112 * (T + 1) / 1e9),
+                   "parallelism": "replicas" if world_size > 1 else "single"},
+        "fwd": {"value": fwd_value, "unit": UNIT, "workload": f"mpm_substep x {T}, same scene"},
+        "fwd_bwd_split_ms": {"forward": fwd_ms / args.steps, "backward": bwd_ms / args.steps},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * (6 + 3)},
+        "gpu_launches": int(launches),
+        "kernels": kern,
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": alg},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--horizon", type=int, default=HORIZON)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

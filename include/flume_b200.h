@@ -200,6 +200,15 @@ int flume_get_stream(flume_ctx* ctx, void** cuda_stream);
 int flume_sync(flume_ctx* ctx);
 int flume_last_timing(const flume_ctx* ctx, flume_timing* out);
 
+/* ---- instrumentation ----
+ * flume_profile: time every kernel class with CUDA events on the context stream.
+ * kernel classes: 0 p2g, 1 grid_update, 2 g2p, 3 sort+block lists, 4 g2p adjoint,
+ * 5 grid adjoint, 6 p2g adjoint, 7 rigid (fwd+adj), 8 other */
+int flume_profile(flume_ctx* ctx, int enable);
+int flume_kernel_times(flume_ctx* ctx, double* ms, long* counts, int n);
+int flume_timer_mark(flume_ctx* ctx, int slot); /* slot 0..7: cudaEventRecord on the context stream */
+int flume_timer_elapsed(flume_ctx* ctx, int a, int b, double* ms);
+
 /* ---- state hand-off ---- */
 int flume_state_upload(flume_ctx* ctx, const flume_state_view* view);
 int flume_state_download(flume_ctx* ctx, flume_state_view* view);

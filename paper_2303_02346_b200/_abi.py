@@ -119,6 +119,10 @@ EXPORTS = {
     "flume_state_download": (C.c_int, [C.c_void_p, C.POINTER(StateView)]),
     "flume_store_order": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint), C.POINTER(C.c_uint), C.POINTER(C.c_long)]),
     "flume_store_positions": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    "flume_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "flume_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_long), C.c_int]),
+    "flume_timer_mark": (C.c_int, [C.c_void_p, C.c_int]),
+    "flume_timer_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "flume_substep": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     "flume_stage_grid": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "flume_rollout_loss": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long,

@@ -241,11 +241,20 @@ __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const 
                 const M3<float> fpre_bar = transpose(ipc) * ftr_bar;
                 const M3<float> c_bar = cin_bar + ftr_bar * transpose(F) * g.dt;
                 V3<float> xnb = {post.x(0)[j], post.x(1)[j], post.x(2)[j]};
+                if (ci.rigid < 0) {
 #pragma unroll
-                for (int a = 0; a < 3; a++) {
-                    const float xr = x[a] + vuse[a] * g.dt;
-                    const float xc = clamp_ref(xr, g.lo[a], g.hi[a]);
-                    if (xr != xc) xnb[a] = 0.f;
+                    for (int a = 0; a < 3; a++) {
+                        const float xr = x[a] + vuse[a] * g.dt;
+                        const float xc = clamp_ref(xr, g.lo[a], g.hi[a]);
+                        if (xr != xc) xnb[a] = 0.f;
+                    }
+                } else {
+                    const int mr = rd.mrank[pre.id[s]];
+                    for (int a = 0; a < 3; a++) {
+                        const double xr = pre.mx[3 * mr + a] + double(vuse[a]) * double(g.dt);
+                        const double xc = clamp_ref(xr, double(g.lo[a]), double(g.hi[a]));
+                        if (xr != xc) xnb[a] = 0.f;
+                    }
                 }
                 const V3<float> vub = {post.v(0)[j] + xnb.x * g.dt, post.v(1)[j] + xnb.y * g.dt,
                                        post.v(2)[j] + xnb.z * g.dt};

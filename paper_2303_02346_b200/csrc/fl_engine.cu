@@ -81,14 +81,17 @@ struct DevArr {
 struct StateBuf {
     void* mem = nullptr;
     PBuf p{};
-    explicit StateBuf(int cap) {
-        size_t bytes = size_t(cap) * (24 * sizeof(float) + 3 * sizeof(uint32_t));
+    size_t bytes = 0;
+    StateBuf(int cap, int nmem) {
+        size_t pbytes = (size_t(cap) * (24 * sizeof(float) + 3 * sizeof(uint32_t)) + 255) & ~size_t(255);
+        bytes = pbytes + size_t(std::max(nmem, 1)) * 3 * sizeof(double);
         CK(cudaMalloc(&mem, bytes));
         p.cap = cap;
         p.f = static_cast<float*>(mem);
         p.meta = reinterpret_cast<uint32_t*>(p.f + size_t(24) * cap);
         p.id = p.meta + cap;
         p.key = p.id + cap;
+        p.mx = reinterpret_cast<double*>(static_cast<char*>(mem) + pbytes);
     }
     ~StateBuf() { cudaFree(mem); }
 };
@@ -110,8 +113,8 @@ struct Record {
     int* nb_list = nullptr;
     int* n_nb = nullptr;
     int* mslot = nullptr;
-    float* mstart = nullptr;
-    float* mid = nullptr;
+    double* mstart = nullptr;
+    double* mid = nullptr;
     double* fit = nullptr;
     int n_active = 0;
     long substep = 0;
@@ -127,7 +130,7 @@ struct Record {
         };
         size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(16),
                o_nbl = carve(size_t(nbtot) * 4), o_nnb = carve(16), o_ms = carve(size_t(nmem) * 4),
-               o_mst = carve(size_t(nmem) * 12), o_mid = carve(size_t(nmem) * 12),
+               o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 24),
                o_fit = carve(size_t(nbody) * 24 * 8);
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
@@ -137,8 +140,8 @@ struct Record {
         nb_list = reinterpret_cast<int*>(b + o_nbl);
         n_nb = reinterpret_cast<int*>(b + o_nnb);
         mslot = reinterpret_cast<int*>(b + o_ms);
-        mstart = reinterpret_cast<float*>(b + o_mst);
-        mid = reinterpret_cast<float*>(b + o_mid);
+        mstart = reinterpret_cast<double*>(b + o_mst);
+        mid = reinterpret_cast<double*>(b + o_mid);
         fit = reinterpret_cast<double*>(b + o_fit);
     }
     ~Record() { cudaFree(mem); }
@@ -151,10 +154,81 @@ static int bits_for(uint64_t v) {
     return b < 1 ? 1 : b;
 }
 
+// per-kernel CUDA-event timing (enabled by flume_profile): events are recorded on
+// the context stream around each launch and summed after the next sync
+enum KId { K_P2G = 0, K_GRID = 1, K_G2P = 2, K_SORT = 3, K_ADJ_G2P = 4, K_ADJ_GRID = 5, K_ADJ_P2G = 6,
+           K_RIGID = 7, K_OTHER = 8, K_COUNT = 9 };
+
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    double ms[K_COUNT] = {};
+    long count[K_COUNT] = {};
+    cudaEvent_t ev() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
+    cudaEvent_t begin(cudaStream_t s) {
+        if (!on) return nullptr;
+        cudaEvent_t e = ev();
+        CK(cudaEventRecord(e, s));
+        return e;
+    }
+    void end(int id, cudaEvent_t b, cudaStream_t s) {
+        if (!on || !b) return;
+        cudaEvent_t e = ev();
+        CK(cudaEventRecord(e, s));
+        pending.push_back({id, {b, e}});
+        if (pending.size() > 4096) collect(s);
+    }
+    void collect(cudaStream_t s) {
+        if (pending.empty()) return;
+        CK(cudaStreamSynchronize(s));
+        for (auto& p : pending) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, p.second.first, p.second.second));
+            ms[p.first] += t;
+            count[p.first]++;
+            pool.push_back(p.second.first);
+            pool.push_back(p.second.second);
+        }
+        pending.clear();
+    }
+    void reset() {
+        for (int k = 0; k < K_COUNT; k++) {
+            ms[k] = 0;
+            count[k] = 0;
+        }
+    }
+    ~Prof() {
+        for (auto& p : pending) {
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+#define PROF(id, call)                          \
+    do {                                        \
+        cudaEvent_t pb_ = prof.begin(stream);   \
+        call;                                   \
+        prof.end(id, pb_, stream);              \
+    } while (0)
+
 // ---------------------------------------------------------------------------
 // context
 // ---------------------------------------------------------------------------
 struct Ctx {
+    Prof prof;
+    cudaEvent_t marks[8] = {};
     int device = 0;
     cudaStream_t stream = nullptr;
     flume_error_info last_err{};
@@ -186,6 +260,7 @@ struct Ctx {
 
     // device constants
     DevArr<ClassInfo> d_cls;
+    DevArr<int> d_member_id;
     DevArr<int> d_rb_off, d_rb_id, d_member_body, d_mrank, d_chunk_body, d_chunk_m0, d_chunk_m1, d_act;
     DevArr<double> d_rb_rest, d_rb_mass, d_rb_smrest, d_rb_total;
 
@@ -225,7 +300,7 @@ struct Ctx {
             pool.pop_back();
             return s;
         }
-        return std::make_shared<StateBuf>(N);
+        return std::make_shared<StateBuf>(N, nmem);
     }
     void put_state(StatePtr s) {
         if (s) pool.push_back(std::move(s));
@@ -254,6 +329,7 @@ struct Ctx {
         d.total = d_rb_total.p;
         d.body_id = d_rb_id.p;
         d.member_body = d_member_body.p;
+        d.member_id = d_member_id.p;
         d.mslot = r.mslot;
         d.mstart = r.mstart;
         d.mid = r.mid;
@@ -281,8 +357,7 @@ struct Ctx {
     void adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* eb,
                              double* abar_out);
     void copy_state(StateBuf& dst, const StateBuf& src) {
-        size_t bytes = size_t(N) * (24 * sizeof(float) + 3 * sizeof(uint32_t));
-        CK(cudaMemcpyAsync(dst.mem, src.mem, bytes, cudaMemcpyDeviceToDevice, stream));
+        CK(cudaMemcpyAsync(dst.mem, src.mem, src.bytes, cudaMemcpyDeviceToDevice, stream));
     }
 };
 
@@ -400,6 +475,10 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     d_rb_off.upload(rb_off, stream);
     d_rb_id.upload(rb_id, stream);
     d_member_body.upload(member_body, stream);
+    {
+        std::vector<int> mid32(rb_members.begin(), rb_members.end());
+        d_member_id.upload(mid32, stream);
+    }
     d_mrank.upload(mrank_by_id, stream);
     d_chunk_body.upload(chunk_body, stream);
     d_chunk_m0.upload(chunk_m0, stream);
@@ -585,7 +664,8 @@ void Ctx::upload(const flume_state_view* view) {
     CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, cub_bytes, ck_in.p, ck_out.p, idx_in.p, scratch_rec->perm, N, 0,
                                        geom.keybits + geom.idbits, stream));
     launch_gather(raw->p, cur->p, scratch_rec->perm, N, stream);
-    launches += 2;
+    launch_upload_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
+    launches += 3;
     put_state(raw);
     for (size_t i = 0; i < eff.size(); i++) {
         const flume_effector_state& es = view->effectors[i];
@@ -603,7 +683,8 @@ void Ctx::upload(const flume_state_view* view) {
 void Ctx::download(flume_state_view* view) {
     for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
     launch_download(cur->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
-    launches++;
+    launch_download_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
+    launches += 2;
     if (view->x) CK(cudaMemcpyAsync(view->x, d_up[0].p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, stream));
     if (view->v) CK(cudaMemcpyAsync(view->v, d_up[1].p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, stream));
     if (view->F) CK(cudaMemcpyAsync(view->F, d_up[2].p, size_t(N) * 9 * 8, cudaMemcpyDeviceToHost, stream));
@@ -696,20 +777,24 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         CK(cudaStreamSynchronize(stream));
     }
     r.n_active = n_active;
-    sort_and_lists(*in, r);
-    launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
-               uint32_t(substep_index), stream);
-    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p,
-                       record_grid ? gridv0.p : nullptr, r.effk, stream);
+    PROF(K_SORT, sort_and_lists(*in, r));
+    PROF(K_P2G, launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
+                           uint32_t(substep_index), stream));
+    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p,
+                                    record_grid ? gridv0.p : nullptr, r.effk, stream));
     RigidDev rd = rigid_dev(r);
-    if (nbody > 0) CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
-    launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridv.p, rd, d_err.p,
-               uint32_t(substep_index), stream);
-    launch_tail_copy(geom, in->p, out->p, r.perm, n_active, N, stream);
+    if (nbody > 0) {
+        CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
+        CK(cudaMemcpyAsync(out->p.mx, in->p.mx, size_t(nmem) * 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                           stream));
+    }
+    PROF(K_G2P, launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridv.p, rd, d_err.p,
+                           uint32_t(substep_index), stream));
+    PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, N, stream));
     launches += 4;
     if (nbody > 0) {
-        launch_rigid(geom, out->p, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p, d_chunk_m1.p,
-                     rig_partial.p, d_err.p, uint32_t(substep_index), stream);
+        PROF(K_RIGID, launch_rigid(geom, out->p, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p,
+                                   d_chunk_m1.p, rig_partial.p, d_err.p, uint32_t(substep_index), stream));
         launches += 3;
     }
     time += cfg.dt_substep;
@@ -860,23 +945,24 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
     // rebuild this substep's forward grid (staging -> v, v0) from the pre-state
     CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
     launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap.p, stream);
-    launch_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p, uint32_t(r.substep),
-               stream);
-    launch_grid_update(g, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, gridv0.p, r.effk, stream);
+    PROF(K_P2G, launch_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
+                           uint32_t(r.substep), stream));
+    PROF(K_GRID, launch_grid_update(g, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, gridv0.p, r.effk,
+                                    stream));
     launches += 3;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
-        launch_adj_rigid(g, post, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p, d_chunk_m1.p,
-                         rig_partial.p, start_bar.p, abar.p, stream);
+        PROF(K_RIGID, launch_adj_rigid(g, post, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p,
+                                       d_chunk_m1.p, rig_partial.p, start_bar.p, abar.p, stream));
         launches += 3;
     }
-    launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, gridv.p, post, xbar_tmp.p, Fbar_tmp.p,
-                   rd, start_bar.p, staging_bar.p, stream);
-    launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, gridv0.p, gridbar.p, r.effk, eff_partial.p,
-                    eff_out.p + size_t(t_slot) * kMaxEff * 18, stream);
-    launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridbar.p, xbar_tmp.p, Fbar_tmp.p, out,
-                   d_nonfinite.p + t_slot, stream);
-    launch_tail_bars(post, out, r.perm, r.n_active, N, stream);
+    PROF(K_ADJ_G2P, launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, gridv.p, post,
+                                   xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, stream));
+    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, gridv0.p, gridbar.p, r.effk,
+                                     eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
+    PROF(K_ADJ_P2G, launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridbar.p, xbar_tmp.p,
+                                   Fbar_tmp.p, out, d_nonfinite.p + t_slot, stream));
+    PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, N, stream));
     launches += 5;
     if (!r.emit.empty()) {
         d_emit_list.alloc(r.emit.size());
@@ -1317,6 +1403,44 @@ int flume_store_positions(flume_ctx* ctx, float* x) {
         Ctx& c = ctx->c;
         CK(cudaMemcpyAsync(x, c.cur->p.f, size_t(c.N) * 3 * 4, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int flume_profile(flume_ctx* ctx, int enable) {
+    if (!ctx) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.prof.collect(ctx->c.stream);
+        ctx->c.prof.on = enable != 0;
+        ctx->c.prof.reset();
+    });
+}
+
+int flume_kernel_times(flume_ctx* ctx, double* ms, long* counts, int n) {
+    if (!ctx) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.prof.collect(ctx->c.stream);
+        for (int k = 0; k < n && k < fl::K_COUNT; k++) {
+            if (ms) ms[k] = ctx->c.prof.ms[k];
+            if (counts) counts[k] = ctx->c.prof.count[k];
+        }
+    });
+}
+
+int flume_timer_mark(flume_ctx* ctx, int slot) {
+    if (!ctx || slot < 0 || slot >= 8) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->c.marks[slot]) CK(cudaEventCreate(&ctx->c.marks[slot]));
+        CK(cudaEventRecord(ctx->c.marks[slot], ctx->c.stream));
+    });
+}
+
+int flume_timer_elapsed(flume_ctx* ctx, int a, int b, double* ms) {
+    if (!ctx || !ms || a < 0 || b < 0 || a >= 8 || b >= 8) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        CK(cudaEventSynchronize(ctx->c.marks[b]));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, ctx->c.marks[a], ctx->c.marks[b]));
+        *ms = t;
     });
 }
 

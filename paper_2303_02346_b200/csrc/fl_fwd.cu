@@ -95,6 +95,28 @@ void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C,
     k_download<<<(n + 255) / 256, 256, 0, s>>>(st, n, x, v, F, C);
 }
 
+__global__ void k_rigid_x(PBuf st, int nmem, const int* member_id, double* x, int dir) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nmem) return;
+    size_t id = size_t(member_id[r]);
+    for (int a = 0; a < 3; a++) {
+        if (dir)
+            x[3 * id + a] = st.mx[3 * size_t(r) + a];
+        else
+            st.mx[3 * size_t(r) + a] = x[3 * id + a];
+    }
+}
+
+void launch_download_rigid(PBuf st, int nmem, const int* member_id, double* x, cudaStream_t s) {
+    if (nmem <= 0) return;
+    k_rigid_x<<<(nmem + 255) / 256, 256, 0, s>>>(st, nmem, member_id, x, 1);
+}
+
+void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* x, cudaStream_t s) {
+    if (nmem <= 0) return;
+    k_rigid_x<<<(nmem + 255) / 256, 256, 0, s>>>(st, nmem, member_id, const_cast<double*>(x), 0);
+}
+
 // ---------------------------------------------------------------------------
 // particle-block / node-block lists from the sorted composite keys
 // ---------------------------------------------------------------------------
@@ -421,13 +443,21 @@ __global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const ui
             cell_key(g, xn.x, xn.y, xn.z, key);
             out.key[j] = key;
             if (ci.rigid >= 0) {
+                // rigid members carry fp64 positions: v = dx/dt in rigid_body_pass
+                // (mpm.hpp:412) would otherwise amplify fp32 rounding by 1/dt
                 const int mr = rd.mrank[pid];
                 rd.mslot[mr] = j;
 #pragma unroll
                 for (int a = 0; a < 3; a++) {
-                    rd.mstart[3 * mr + a] = x[a];
-                    rd.mid[3 * mr + a] = xn[a];
+                    const double sx = in.mx[3 * mr + a];
+                    const double xm = clamp_ref(sx + double(vuse[a]) * double(g.dt), double(g.lo[a]), double(g.hi[a]));
+                    rd.mstart[3 * mr + a] = sx;
+                    rd.mid[3 * mr + a] = xm;
+                    out.mx[3 * mr + a] = xm;
+                    out.x(a)[j] = float(xm);
                 }
+                cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key);
+                out.key[j] = key;
             }
         }
     }
@@ -473,7 +503,7 @@ __global__ void __launch_bounds__(256) k_rigid_partial(PBuf out, RigidDev rd, co
         const int j = rd.mslot[r];
         if (j < 0) continue;
         const double m = rd.mass[r];
-        const double x[3] = {double(out.x(0)[j]), double(out.x(1)[j]), double(out.x(2)[j])};
+        const double x[3] = {rd.mid[3 * size_t(r)], rd.mid[3 * size_t(r) + 1], rd.mid[3 * size_t(r) + 2]};
         const double* re = rd.rest + 3 * size_t(r);
         acc[0] += m;
         for (int a = 0; a < 3; a++) acc[1 + a] += m * x[a];
@@ -545,7 +575,8 @@ __global__ void k_rigid_apply(Geom g, PBuf out, RigidDev rd) {
     const double inv_dt = 1.0 / double(g.dt);
     for (int a = 0; a < 3; a++) {
         out.x(a)[j] = float(xn[a]);
-        out.v(a)[j] = float((xn[a] - double(rd.mstart[3 * r + a])) * inv_dt);
+        out.mx[3 * size_t(r) + a] = xn[a];
+        out.v(a)[j] = float((xn[a] - rd.mstart[3 * size_t(r) + a]) * inv_dt);
     }
     uint32_t key;
     cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key);

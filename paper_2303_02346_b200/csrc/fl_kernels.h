@@ -19,10 +19,11 @@ struct RigidDev {
     const double* total;      // [nbody] total mass
     const int* body_id;       // [nbody] reference body id
     const int* member_body;   // [nmem] body index of each member
+    const int* member_id;     // [nmem] particle id of each member
     // per-substep arrays
     int* mslot;               // [nmem] sorted position of the member in the post-g2p buffer (-1 inactive)
-    float* mstart;            // [3*nmem] stage-a position (rigid_body_pass start_positions)
-    float* mid;               // [3*nmem] post-g2p position
+    double* mstart;           // [3*nmem] stage-a position (rigid_body_pass start_positions)
+    double* mid;              // [3*nmem] post-g2p position
     double* fit;              // [nbody*24]: R[9] c[3] A[9] total skip ok
 };
 
@@ -86,6 +87,8 @@ void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* 
                   const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
                   uint32_t substep, cudaStream_t s);
 void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, cudaStream_t s);
+void launch_download_rigid(PBuf st, int nmem, const int* member_id, double* x, cudaStream_t s);
+void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* x, cudaStream_t s);
 void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
                  double* partial, double* out, uint32_t key_inactive, cudaStream_t s);
 

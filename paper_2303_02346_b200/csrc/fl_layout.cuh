@@ -59,6 +59,7 @@ struct PBuf {
     uint32_t* meta;   // class index
     uint32_t* id;     // reference particle index
     uint32_t* key;    // cell key (key_inactive for inactive)
+    double* mx;       // [3*nmem] fp64 positions of rigid-body members, by member rank
     int cap;
     __host__ __device__ float* x(int a) const { return f + size_t(a) * cap; }
     __host__ __device__ float* v(int a) const { return f + size_t(3 + a) * cap; }
