@@ -177,38 +177,43 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
 // ---------------------------------------------------------------------------
 // G2P adjoint (adjoint.hpp:281-365): gather + deterministic scatter of grid v_bar
 // ---------------------------------------------------------------------------
+template <bool HEAVY>
 __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                         const BlockRec* __restrict__ recs,
                                                         const int* __restrict__ n_blocks,
+                                                        const uint16_t* __restrict__ celltab,
                                                         const ClassInfo* __restrict__ cls,
                                                         const float4* __restrict__ gridv, BarBuf post,
                                                         float* xbar_tmp, float* Fbar_tmp, RigidDev rd,
                                                         const float* __restrict__ start_bar, float4* staging_bar,
-                                                        int cap) {
-    __shared__ ScSmem sm;
-    __shared__ float4 vt[kTile];
+                                                        int cap, int* wq) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
+    float4* vt = reinterpret_cast<float4*>(smraw + sizeof(ScSmem));
     const int tid = threadIdx.x;
-    const int nb = *n_blocks;
+    const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     const int my_c = tid & 63, my_ox = tid >> 6;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    __shared__ int sh_next;
+    for (;;) {
+        const int b = q0 + next_work(wq, &sh_next);
+        if (b >= q1) break;
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
+        __syncthreads();
         load_tile(g, gridv, vt, bx, by, bz, tid, kScThreads);
-        float acc[9][4];
-#pragma unroll
-        for (int k = 0; k < 9; k++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) acc[k][q] = 0.f;
-        for (int c0 = r.start; c0 < r.end; c0 += kScChunk) {
-            const int n = min(kScChunk, r.end - c0);
-            if (tid < 64) sm.cs[tid] = sm.ce[tid] = 0;
-            __syncthreads();
-            for (int i = tid; i < n; i += kScThreads) {
-                const int j = c0 + i;
+        sc_tile_zero(sm, tid, kScThreads);
+        const int npass = sc_load_cells(sm, celltab, b, tid);
+        const int cnt = r.end - r.start;
+        for (int pass = 0; pass < npass; pass++) {
+            const int r0 = pass * kScR;
+            for (int i = tid; i < cnt; i += kScThreads) {
+                const int j = r.start + i;
                 const uint32_t s = perm[j];
-                sm.lc[i] = uint8_t(pre.key[s] & 63);
-                float* pay = &sm.u.pay[i * kPayStride];
+                const int c = int(pre.key[s] & 63);
+                const int rank = i - int(sm.cs[c]) - r0;
+                if (rank < 0 || rank >= kScR) continue;
+                float* pay = pay_slot(sm, rank, c);
                 const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
                 const ClassInfo ci = cls[pre.meta[s]];
                 StencilW sw;
@@ -231,17 +236,23 @@ __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const 
                     cin_bar.m[k] = post.C(k)[j];
                 }
                 M3<float> ftr_bar;
-                switch (ci.kind) {
-                    case MK_LIQUID:
-                    case MK_VISCOUS: ftr_bar = liquid_project_vjp(ftr, fpost_bar); break;
-                    case MK_PLASTIC: ftr_bar = box_yield_project_vjp(ftr, ci.theta_c, ci.theta_s, fpost_bar); break;
-                    case MK_NONNEWTONIAN: ftr_bar = von_mises_project_vjp(ftr, ci.sigma_y, ci.mu, fpost_bar); break;
-                    default: ftr_bar = fpost_bar; break;
+                if constexpr (HEAVY) {
+                    switch (ci.kind) {
+                        case MK_LIQUID:
+                        case MK_VISCOUS: ftr_bar = liquid_project_vjp(ftr, fpost_bar); break;
+                        case MK_PLASTIC: ftr_bar = box_yield_project_vjp(ftr, ci.theta_c, ci.theta_s, fpost_bar); break;
+                        case MK_NONNEWTONIAN:
+                            ftr_bar = von_mises_project_vjp(ftr, ci.sigma_y, ci.mu, fpost_bar);
+                            break;
+                        default: ftr_bar = fpost_bar; break;
+                    }
+                } else {
+                    ftr_bar = liquid_project_vjp(ftr, fpost_bar);
                 }
                 const M3<float> fpre_bar = transpose(ipc) * ftr_bar;
                 const M3<float> c_bar = cin_bar + ftr_bar * transpose(F) * g.dt;
                 V3<float> xnb = {post.x(0)[j], post.x(1)[j], post.x(2)[j]};
-                if (ci.rigid < 0) {
+                if (!HEAVY || ci.rigid < 0) {
 #pragma unroll
                     for (int a = 0; a < 3; a++) {
                         const float xr = x[a] + vuse[a] * g.dt;
@@ -262,8 +273,10 @@ __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const 
                 // x_bar = x_new_bar + sum_o grad w_o s_o - k4 c_bar^T v_raw
                 V3<float> xb = xnb - tmul(c_bar, vraw) * g.k4;
                 const float kd = g.k4 * g.dx;
-#pragma unroll
+#pragma unroll 1
                 for (int ox = 0; ox < 3; ox++) {
+                    const float wox = ox == 0 ? sw.w[0][0] : (ox == 1 ? sw.w[0][1] : sw.w[0][2]);
+                    const float dox = ox == 0 ? sw.dw[0][0] : (ox == 1 ? sw.dw[0][1] : sw.dw[0][2]);
 #pragma unroll
                     for (int oy = 0; oy < 3; oy++) {
 #pragma unroll
@@ -275,16 +288,16 @@ __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const 
                             // k4 * c_bar * rel_phys, rel_phys = dx (o - fx)
                             const V3<float> cr = c_bar * rel;
                             const float sv = dot(gv, vrb) + dot(gv, cr);
-                            const float gx = sw.dw[0][ox] * sw.w[1][oy] * sw.w[2][oz];
-                            const float gy = sw.w[0][ox] * sw.dw[1][oy] * sw.w[2][oz];
-                            const float gz = sw.w[0][ox] * sw.w[1][oy] * sw.dw[2][oz];
+                            const float gx = dox * sw.w[1][oy] * sw.w[2][oz];
+                            const float gy = wox * sw.dw[1][oy] * sw.w[2][oz];
+                            const float gz = wox * sw.w[1][oy] * sw.dw[2][oz];
                             xb.x += gx * g.inv_dx * sv;
                             xb.y += gy * g.inv_dx * sv;
                             xb.z += gz * g.inv_dx * sv;
                         }
                     }
                 }
-                if (ci.rigid >= 0) {
+                if (HEAVY && ci.rigid >= 0) {
                     const int mr = rd.mrank[pre.id[s]];
                     xb.x += start_bar[3 * mr];
                     xb.y += start_bar[3 * mr + 1];
@@ -300,32 +313,41 @@ __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const 
                 const V3<float> f3 = {sw.fx[0], sw.fx[1], sw.fx[2]};
                 const V3<float> a = vrb - bm * f3;
                 pay[0] = sw.fx[0];
-                pay[1] = sw.fx[1];
-                pay[2] = sw.fx[2];
-                pay[3] = a.x;
-                pay[4] = a.y;
-                pay[5] = a.z;
+                pay[kPayPlane] = sw.fx[1];
+                pay[2 * kPayPlane] = sw.fx[2];
+                pay[3 * kPayPlane] = a.x;
+                pay[4 * kPayPlane] = a.y;
+                pay[5 * kPayPlane] = a.z;
 #pragma unroll
-                for (int k = 0; k < 9; k++) pay[6 + k] = bm.m[k];
+                for (int k = 0; k < 9; k++) pay[(6 + k) * kPayPlane] = bm.m[k];
             }
             __syncthreads();
-            sc_ranges(sm, n, tid, kScThreads);
-            __syncthreads();
-            sc_accumulate<3>(sm, my_c, my_ox, acc);
+            const int nr = min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR);
+            sc_accumulate<3>(sm, my_c, my_ox, nr);
             __syncthreads();
         }
-        sc_store_cellpart<3>(sm, my_c, my_ox, acc);
         __syncthreads();
-        sc_tile(sm, staging_bar + size_t(b) * kTile, tid, kScThreads);
-        __syncthreads();
+        sc_tile_store(sm, staging_bar + size_t(b) * kTile, tid, kScThreads);
     }
 }
 
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
-                    int grid, const ClassInfo* cls, const float4* gridv, BarBuf post, float* xbar_tmp,
-                    float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar, cudaStream_t s) {
-    k_adj_g2p<<<grid, kScThreads, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridv, post, xbar_tmp, Fbar_tmp, rd,
-                                          start_bar, staging_bar, post.cap);
+                    const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, BarBuf post,
+                    float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar,
+                    bool heavy, int* wq, cudaStream_t s) {
+    const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_adj_g2p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_adj_g2p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    if (heavy)
+        k_adj_g2p<true><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, post,
+                                                       xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
+    else
+        k_adj_g2p<false><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, post,
+                                                        xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
 }
 
 // ---------------------------------------------------------------------------
@@ -333,6 +355,7 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 // reduction of the per-effector bars (18 scalars each)
 // ---------------------------------------------------------------------------
 constexpr int kEffQ = 18;  // t[3] R[9] vlin[3] w[3]
+constexpr int kAdjGridThreads = 128;
 
 __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __restrict__ blockmap,
                                                   const float4* __restrict__ staging, int bx, int by, int bz, int lx,
@@ -355,76 +378,68 @@ __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __re
     return acc;
 }
 
-__global__ void __launch_bounds__(64) k_adj_grid(Geom g, const int* __restrict__ nb_list, const int* __restrict__ n_nb,
-                                                 const int* __restrict__ blockmap,
-                                                 const float4* __restrict__ staging_bar,
-                                                 const float4* __restrict__ gridv0, float4* gridbar, EffSet eff,
-                                                 double* eff_partial) {
-    __shared__ double wred[2][kEffQ];
-    __shared__ double cta_acc[kMaxEff][kEffQ];
+// NE = number of effectors (compile time).  Every thread accumulates the
+// effector bars of the nodes it processes in registers (fixed node order, since
+// the list partition is static), then one fixed-order CTA reduction per launch.
+template <int NE>
+__global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int* __restrict__ nb_list,
+                                                              const int* __restrict__ n_nb,
+                                                              const int* __restrict__ blockmap,
+                                                              const float4* __restrict__ staging_bar,
+                                                              const float4* __restrict__ gridv0, float4* gridbar,
+                                                              EffSet eff, double* eff_partial) {
+    __shared__ double red[kAdjGridThreads / 32][NE * kEffQ > 0 ? NE * kEffQ : 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int q = tid; q < kMaxEff * kEffQ; q += 64) (&cta_acc[0][0])[q] = 0.0;
-    __syncthreads();
+    const int sub = tid >> 6, l = tid & 63;
+    const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
+    float acc[NE > 0 ? NE : 1][kEffQ];
+#pragma unroll
+    for (int e = 0; e < (NE > 0 ? NE : 1); e++)
+#pragma unroll
+        for (int q = 0; q < kEffQ; q++) acc[e][q] = 0.f;
     const int n = *n_nb;
-    const int lx = tid >> 4, ly = (tid >> 2) & 3, lz = tid & 3;
-    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    constexpr int kPer = kAdjGridThreads / 64;
+    for (int k = blockIdx.x * kPer + sub; k < n; k += gridDim.x * kPer) {
         const int nbid = nb_list[k];
         int bx, by, bz;
         block_unlin(g, nbid, bx, by, bz);
         const float4 sb = gather_tile_sum(g, blockmap, staging_bar, bx, by, bz, lx, ly, lz);
         V3<float> bar = {sb.x, sb.y, sb.z};
-        const size_t idx = size_t(nbid) * 64 + tid;
+        const size_t idx = size_t(nbid) * 64 + l;
         const float4 g0 = gridv0[idx];
         const float m = g0.w;
         const V3<float> v0 = {g0.x, g0.y, g0.z};
-        const bool act = m > g.mass_eps && (bar.x != 0.f || bar.y != 0.f || bar.z != 0.f);
-        const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
-        const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
-        V3<float> v1 = {v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
-        V3<float> v2 = v1;
-        V3<float> chain[kMaxEff];
-        if (act) {
-            v2 = wall_bc_dev(g, i, j, kk, v1);
+        float pb0 = 0.f, pb1 = 0.f, pb2 = 0.f, mb = 0.f;
+        if (m > g.mass_eps && (bar.x != 0.f || bar.y != 0.f || bar.z != 0.f)) {
+            const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
+            const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
+            const V3<float> v1 = {v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
+            const V3<float> v2 = wall_bc_dev(g, i, j, kk, v1);
+            V3<float> chain[NE > 0 ? NE : 1];
             V3<float> c = v2;
-            for (int e = 0; e < eff.n; e++) {
+#pragma unroll
+            for (int e = 0; e < NE; e++) {
                 chain[e] = c;
                 c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
             }
-        }
-        for (int e = eff.n - 1; e >= 0; e--) {
-            EffBars<float> eb;
-            eb.t = V3<float>{0.f, 0.f, 0.f};
-            eb.R = mzero<float>();
-            eb.vlin = eb.t;
-            eb.w = eb.t;
-            bool contact = false;
-            if (act) {
+#pragma unroll
+            for (int e = NE - 1; e >= 0; e--) {
+                EffBars<float> eb;
+                eb.t = V3<float>{0.f, 0.f, 0.f};
+                eb.R = mzero<float>();
+                eb.vlin = eb.t;
+                eb.w = eb.t;
                 V3<float> in_bar = {0.f, 0.f, 0.f};
-                contact = effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
-                                               in_bar, eb);
+                if (effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
+                                         in_bar, eb)) {
+                    acc[e][0] += eb.t.x; acc[e][1] += eb.t.y; acc[e][2] += eb.t.z;
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[e][3 + q] += eb.R.m[q];
+                    acc[e][12] += eb.vlin.x; acc[e][13] += eb.vlin.y; acc[e][14] += eb.vlin.z;
+                    acc[e][15] += eb.w.x; acc[e][16] += eb.w.y; acc[e][17] += eb.w.z;
+                }
                 bar = in_bar;
             }
-            if (__syncthreads_or(contact ? 1 : 0)) {
-                float vals[kEffQ];
-                vals[0] = eb.t.x; vals[1] = eb.t.y; vals[2] = eb.t.z;
-#pragma unroll
-                for (int q = 0; q < 9; q++) vals[3 + q] = eb.R.m[q];
-                vals[12] = eb.vlin.x; vals[13] = eb.vlin.y; vals[14] = eb.vlin.z;
-                vals[15] = eb.w.x; vals[16] = eb.w.y; vals[17] = eb.w.z;
-#pragma unroll
-                for (int q = 0; q < kEffQ; q++) {
-                    double v = double(vals[q]);
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-                    if (lane == 0) wred[warp][q] = v;
-                }
-                __syncthreads();
-                if (tid < kEffQ) cta_acc[e][tid] += wred[0][tid] + wred[1][tid];
-                __syncthreads();
-            }
-        }
-        float pb0 = 0.f, pb1 = 0.f, pb2 = 0.f, mb = 0.f;
-        if (act) {
             if (v2.x != v1.x) bar.x = 0.f;
             if (v2.y != v1.y) bar.y = 0.f;
             if (v2.z != v1.z) bar.z = 0.f;
@@ -436,40 +451,74 @@ __global__ void __launch_bounds__(64) k_adj_grid(Geom g, const int* __restrict__
         }
         gridbar[idx] = make_float4(pb0, pb1, pb2, mb);
     }
+    // fixed-order CTA reduction: warp shuffle tree, then warps in index order
+#pragma unroll
+    for (int e = 0; e < NE; e++)
+#pragma unroll
+        for (int q = 0; q < kEffQ; q++) {
+            double v = double(acc[e][q]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp][e * kEffQ + q] = v;
+        }
     __syncthreads();
-    for (int q = tid; q < kMaxEff * kEffQ; q += 64)
-        eff_partial[size_t(blockIdx.x) * kMaxEff * kEffQ + q] = (&cta_acc[0][0])[q];
+    for (int q = tid; q < kMaxEff * kEffQ; q += kAdjGridThreads) {
+        double s = 0.0;
+        if (q < NE * kEffQ)
+            for (int w = 0; w < kAdjGridThreads / 32; w++) s += red[w][q];
+        eff_partial[size_t(blockIdx.x) * kMaxEff * kEffQ + q] = s;
+    }
 }
 
-__global__ void k_eff_final(const double* partial, int nblocks, double* out) {
-    const int q = threadIdx.x;
-    if (q >= kMaxEff * kEffQ) return;
-    double s = 0.0;
-    for (int b = 0; b < nblocks; b++) s += partial[size_t(b) * kMaxEff * kEffQ + q];
-    out[q] = s;
+// one warp per (effector, component): strided lane sums + fixed shuffle tree
+__global__ void k_eff_final(const double* partial, int nblocks, int nvals, double* out) {
+    const int lane = threadIdx.x & 31;
+    for (int q = threadIdx.x >> 5; q < kMaxEff * kEffQ; q += blockDim.x >> 5) {
+        double s = 0.0;
+        if (q < nvals)
+            for (int b = lane; b < nblocks; b += 32) s += partial[size_t(b) * kMaxEff * kEffQ + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) out[q] = s;
+    }
 }
 
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                      double* eff_partial, double* eff_out, cudaStream_t s) {
-    k_adj_grid<<<kEffBlocks, 64, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial);
-    k_eff_final<<<1, kMaxEff * kEffQ, 0, s>>>(eff_partial, kEffBlocks, eff_out);
+    switch (eff.n) {
+        case 0: k_adj_grid<0><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+                                                                     gridbar, eff, eff_partial); break;
+        case 1: k_adj_grid<1><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+                                                                     gridbar, eff, eff_partial); break;
+        case 2: k_adj_grid<2><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+                                                                     gridbar, eff, eff_partial); break;
+        case 3: k_adj_grid<3><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+                                                                     gridbar, eff, eff_partial); break;
+        default: k_adj_grid<kMaxEff><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar,
+                                                                            gridv0, gridbar, eff, eff_partial);
+    }
+    k_eff_final<<<1, 1024, 0, s>>>(eff_partial, kEffBlocks, eff.n * kEffQ, eff_out);
 }
 
 // ---------------------------------------------------------------------------
 // P2G adjoint (adjoint.hpp:414-470)
 // ---------------------------------------------------------------------------
+template <bool HEAVY>
 __global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                  const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                                  const ClassInfo* __restrict__ cls,
                                                  const float4* __restrict__ gridbar,
                                                  const float* __restrict__ xbar_tmp,
                                                  const float* __restrict__ Fbar_tmp, BarBuf out, int* nonfinite,
-                                                 int cap) {
+                                                 int cap, int* wq) {
     __shared__ float4 bt[kTile];
     const int tid = threadIdx.x;
-    const int nb = *n_blocks;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
+    __shared__ int sh_next;
+    for (;;) {
+        const int b = q0 + next_work(wq, &sh_next);
+        if (b >= q1) break;
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
@@ -487,12 +536,18 @@ __global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_
                 F.m[k] = pre.F(k)[s];
                 C.m[k] = pre.C(k)[s];
             }
-            const bool visc = ci.kind == MK_VISCOUS;
+            const bool visc = HEAVY && ci.kind == MK_VISCOUS;
             const M3<float> ipc = meye<float>() + C * g.dt;
             const M3<float> fs = visc ? ipc * F : F;
             bool ok;
             Svd<float> t;
-            const M3<float> P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
+            M3<float> P;
+            if constexpr (HEAVY) {
+                P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
+            } else {
+                const float jj = det(fs);
+                P = cofactor(fs) * (ci.lambda * (jj - 1.f));
+            }
             const M3<float> smat = P * transpose(fs);
             const float cc = g.stress_coeff * ci.vol0;
             const M3<float> affine = C * ci.mass - smat * cc;
@@ -536,7 +591,11 @@ __global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_
             const M3<float> sm_bar = ab * (-cc);
             const M3<float> p_bar = sm_bar * fs;
             M3<float> fs_bar = transpose(sm_bar) * P;
-            fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
+            if constexpr (HEAVY) {
+                fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
+            } else {
+                fs_bar += pressure_stress_vjp(fs, ci.lambda, p_bar);
+            }
             M3<float> Fb, Cb = ab * ci.mass;
 #pragma unroll
             for (int k = 0; k < 9; k++) Fb.m[k] = Fbar_tmp[size_t(k) * cap + j];
@@ -565,9 +624,13 @@ __global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_
 
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
-                    const float* Fbar_tmp, BarBuf out, int* nonfinite, cudaStream_t s) {
-    k_adj_p2g<<<grid, 128, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out, nonfinite,
-                                   out.cap);
+                    const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s) {
+    if (heavy)
+        k_adj_p2g<true><<<grid, 128, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
+                                             nonfinite, out.cap, wq);
+    else
+        k_adj_p2g<false><<<grid, 128, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
+                                              nonfinite, out.cap, wq);
 }
 
 // inactive particles pass their bars through untouched
@@ -653,6 +716,31 @@ void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* 
                         cudaStream_t s) {
     if (n <= 0) return;
     k_bars_to_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb);
+}
+
+int occupancy_grid_fwd(KGrid which, bool heavy);
+
+int occupancy_grid(KGrid which, bool heavy) {
+    if (which == KG_P2G || which == KG_G2P) return occupancy_grid_fwd(which, heavy);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (which == KG_ADJ_G2P) {
+        const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
+        cudaFuncSetAttribute(k_adj_g2p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_adj_g2p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (heavy)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_g2p<true>, kScThreads, smem);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_g2p<false>, kScThreads, smem);
+    } else {
+        if (heavy)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_p2g<true>, 128, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_p2g<false>, 128, 0);
+    }
+    if (per < 1) per = 1;
+    return sms * per;
 }
 
 }  // namespace fl

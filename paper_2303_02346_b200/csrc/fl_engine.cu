@@ -29,6 +29,7 @@
 
 #include "../../include/flume_b200.h"
 #include "fl_kernels.h"
+#include "fl_scatter.cuh"
 
 namespace fl {
 
@@ -116,6 +117,7 @@ struct Record {
     double* mstart = nullptr;
     double* mid = nullptr;
     double* fit = nullptr;
+    uint16_t* celltab = nullptr;
     int n_active = 0;
     long substep = 0;
     std::vector<ActEntry> act;
@@ -131,7 +133,7 @@ struct Record {
         size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(16),
                o_nbl = carve(size_t(nbtot) * 4), o_nnb = carve(16), o_ms = carve(size_t(nmem) * 4),
                o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 24),
-               o_fit = carve(size_t(nbody) * 24 * 8);
+               o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2);
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -143,6 +145,7 @@ struct Record {
         mstart = reinterpret_cast<double*>(b + o_mst);
         mid = reinterpret_cast<double*>(b + o_mid);
         fit = reinterpret_cast<double*>(b + o_fit);
+        celltab = reinterpret_cast<uint16_t*>(b + o_ct);
     }
     ~Record() { cudaFree(mem); }
 };
@@ -229,6 +232,30 @@ struct Prof {
 struct Ctx {
     Prof prof;
     cudaEvent_t marks[8] = {};
+    // light (plain-liquid) and heavy (SVD / rigid) block variants run concurrently
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    DevArr<int> wq;  // rolling work counters for dynamically scheduled kernels
+    int wq_next = 0;
+    static constexpr int kWq = 256;
+    int* take_wq() {
+        if (wq_next + 1 > kWq) {
+            CK(cudaMemsetAsync(wq.p, 0, kWq * sizeof(int), stream));
+            wq_next = 0;
+        }
+        return wq.p + wq_next++;
+    }
+    template <class Fn>
+    void dual(Fn&& fn) {
+        int* wh = take_wq();
+        int* wl = take_wq();
+        CK(cudaEventRecord(ev_fork, stream));
+        CK(cudaStreamWaitEvent(s2, ev_fork, 0));
+        fn(true, wh, s2);
+        fn(false, wl, stream);
+        CK(cudaEventRecord(ev_join, s2));
+        CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    }
     int device = 0;
     cudaStream_t stream = nullptr;
     flume_error_info last_err{};
@@ -265,22 +292,26 @@ struct Ctx {
     DevArr<double> d_rb_rest, d_rb_mass, d_rb_smrest, d_rb_total;
 
     // scratch
-    DevArr<uint64_t> ck_in, ck_out;
-    DevArr<uint32_t> idx_in;
+    DevArr<int> bzero, bstart;  // bzero = [bcount | bheavy | bfill], zeroed per sort
+    int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr;
+    DevArr<int> nbpos;
+    DevArr<uint32_t> skey, sslot, gk, gv;
     DevArr<unsigned char> cub_tmp;
     size_t cub_bytes = 0;
-    DevArr<int> flags, pos, starts, nbflag, nbpos, blockmap;
+    DevArr<int> blockmap;
     DevArr<float4> staging, gridv, gridv0, staging_bar, gridbar;
     DevArr<unsigned long long> d_err;
     DevArr<int> d_nonfinite;
     DevArr<double> rig_partial, abar, eff_partial, eff_out, em_out, loss_partial, loss_out;
-    DevArr<float> start_bar, xbar_tmp, Fbar_tmp;
+    DevArr<float> start_bar, xbar_tmp, Fbar_tmp, barsA, barsB;
+    cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
     DevArr<ActEntry> d_act_list;
     DevArr<EmitAdjEntry> d_emit_list;
     DevArr<double> d_up[4];
     DevArr<uint32_t> d_upmeta;
     DevArr<uint8_t> d_upactive;
-    int grid_p2g = 0, grid_g2p = 0, grid_upd = 0;
+    int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
+    int grid_p2g_h = 0, grid_g2p_h = 0, grid_adj_h = 0, grid_ap = 0, grid_ap_h = 0;
 
     // live state
     StatePtr cur;
@@ -366,6 +397,11 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     device = dev;
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    wq.alloc(kWq);
+    CK(cudaMemsetAsync(wq.p, 0, kWq * sizeof(int), stream));
     cfg = desc->config;
     N = int(desc->n_particles);
     if (N <= 0) throw FlumeError(FLUME_E_SCENE, "scene has no particles");
@@ -399,6 +435,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     g.k4 = float(4.0 / (dx * dx));
     g.stress_coeff = float(cfg.dt_substep * 4.0 / (dx * dx));
     maxb = std::min(g.nbtot, N);
+    g.maxb = maxb;
 
     // per-particle immutable fields and the class table
     p_mat.assign(desc->material_id, desc->material_id + N);
@@ -452,6 +489,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
             ci.kind = m.kind;
             ci.body = p_body[i];
             ci.rigid = rigid_of_id[i];
+            ci.heavy = (m.kind != MK_LIQUID || m.mu != 0.0 || rigid_of_id[i] >= 0) ? 1 : 0;
             ci.mass = float(p_mass[i]);
             ci.vol0 = float(p_vol0[i]);
             ci.mu = float(m.mu);
@@ -492,14 +530,18 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     d_act.upload(act32, stream);
 
     // scratch
-    ck_in.alloc(N);
-    ck_out.alloc(N);
-    idx_in.alloc(N);
-    flags.alloc(N);
-    pos.alloc(N);
-    starts.alloc(maxb);
-    nbflag.alloc(g.nbtot);
+    if (N >= (1 << 26)) throw FlumeError(FLUME_E_ARG, "at most 2^26-1 particles per context");
+    bzero.alloc(4 * size_t(g.nbtot + 1));
+    bcount = bzero.p;
+    bheavy = bzero.p + (g.nbtot + 1);
+    bfill = bzero.p + 2 * (g.nbtot + 1);
+    nbflag = bzero.p + 3 * (g.nbtot + 1);
     nbpos.alloc(g.nbtot);
+    bstart.alloc(g.nbtot + 1);
+    skey.alloc(N);
+    sslot.alloc(N);
+    gk.alloc(2 * size_t(N) + 2);
+    gv.alloc(2 * size_t(N) + 2);
     blockmap.alloc(g.nbtot);
     staging.alloc(size_t(maxb) * kTile);
     staging_bar.alloc(size_t(maxb) * kTile);
@@ -520,19 +562,25 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     CK(cudaMemsetAsync(gridv0.p, 0, gridv0.n * sizeof(float4), stream));
     CK(cudaMemsetAsync(gridbar.p, 0, gridbar.n * sizeof(float4), stream));
 
-    size_t b1 = 0, b2 = 0, b3 = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, ck_in.p, ck_out.p, idx_in.p, idx_in.p, N, 0,
-                                       g.keybits + g.idbits, stream));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, flags.p, pos.p, N, stream));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, b3, nbflag.p, nbpos.p, g.nbtot, stream));
-    cub_bytes = std::max(b1, std::max(b2, b3));
+    size_t b2 = 0, b3 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, bcount, bstart.p, g.nbtot + 1, stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b3, nbflag, nbpos.p, g.nbtot, stream));
+    cub_bytes = std::max(b2, b3);
     cub_tmp.alloc(cub_bytes);
 
-    grid_p2g = p2g_occupancy_grid();
-    grid_g2p = g2p_occupancy_grid();
+    grid_p2g = occupancy_grid(KG_P2G, false);
+    grid_p2g_h = occupancy_grid(KG_P2G, true);
+    grid_g2p = occupancy_grid(KG_G2P, false);
+    grid_g2p_h = occupancy_grid(KG_G2P, true);
+    grid_adj = occupancy_grid(KG_ADJ_G2P, false);
+    grid_adj_h = occupancy_grid(KG_ADJ_G2P, true);
+    grid_ap = occupancy_grid(KG_ADJ_P2G, false);
+    grid_ap_h = occupancy_grid(KG_ADJ_P2G, true);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid_upd = sms * 8;
+    grid_sort = sms * 4;
+
 
     // initial effector state from the shapes' defaults is set by upload()
     eff.resize(eff_shapes.size());
@@ -660,9 +708,8 @@ void Ctx::upload(const flume_state_view* view) {
     StatePtr raw = get_state();
     launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, stream);
     launches++;
-    launch_make_sortkeys(geom, raw->p, N, ck_in.p, idx_in.p, stream);
-    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, cub_bytes, ck_in.p, ck_out.p, idx_in.p, scratch_rec->perm, N, 0,
-                                       geom.keybits + geom.idbits, stream));
+    scratch_rec->n_active = n_active;
+    sort_and_lists(*raw, *scratch_rec);
     launch_gather(raw->p, cur->p, scratch_rec->perm, N, stream);
     launch_upload_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
     launches += 3;
@@ -704,22 +751,21 @@ void Ctx::download(flume_state_view* view) {
         }
 }
 
-// keys -> canonical order -> particle-block list -> node-block list
+// keys -> canonical order + particle-block list (fl_sort.cu)
 void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     Geom& g = geom;
-    launch_make_sortkeys(g, st.p, N, ck_in.p, idx_in.p, stream);
-    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, cub_bytes, ck_in.p, ck_out.p, idx_in.p, r.perm, N, 0,
-                                       g.keybits + g.idbits, stream));
-    const int na = r.n_active;
-    launch_block_flags(g, ck_out.p, na, flags.p, stream);
-    if (na > 0) CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, flags.p, pos.p, na, stream));
-    launch_block_scatter(flags.p, pos.p, na, starts.p, r.n_blocks, stream);
+    CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
+    CK(cudaMemsetAsync(r.n_blocks, 0, 2 * sizeof(int), stream));
     CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
-    CK(cudaMemsetAsync(nbflag.p, 0, size_t(g.nbtot) * sizeof(int), stream));
-    launch_block_recs(g, ck_out.p, starts.p, r.n_blocks, na, maxb, r.recs, blockmap.p, nbflag.p, stream);
-    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag.p, nbpos.p, g.nbtot, stream));
-    launch_nb_scatter(nbflag.p, nbpos.p, g.nbtot, r.nb_list, r.n_nb, stream);
-    launches += 6;
+    launch_sort_count(g, st.p, N, d_cls.p, bcount, bheavy, stream);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, bcount, bstart.p, g.nbtot + 1, stream));
+    launch_sort_scatter(g, st.p, N, bstart.p, bcount, bheavy, bfill, skey.p, sslot.p, r.recs, r.n_blocks, blockmap.p,
+                        nbflag, maxb, stream);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, g.nbtot, stream));
+    launch_nb_scatter(nbflag, nbpos.p, g.nbtot, r.nb_list, r.n_nb, stream);
+    launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
+                       grid_sort, stream);
+    launches += 4;
 }
 
 void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r, bool record_grid) {
@@ -778,8 +824,10 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     }
     r.n_active = n_active;
     PROF(K_SORT, sort_and_lists(*in, r));
-    PROF(K_P2G, launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
-                           uint32_t(substep_index), stream));
+    PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
+             launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
+                        staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
+         }));
     PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p,
                                     record_grid ? gridv0.p : nullptr, r.effk, stream));
     RigidDev rd = rigid_dev(r);
@@ -788,8 +836,10 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         CK(cudaMemcpyAsync(out->p.mx, in->p.mx, size_t(nmem) * 3 * sizeof(double), cudaMemcpyDeviceToDevice,
                            stream));
     }
-    PROF(K_G2P, launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridv.p, rd, d_err.p,
-                           uint32_t(substep_index), stream));
+    PROF(K_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
+             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : grid_g2p, d_cls.p, gridv.p,
+                        rd, d_err.p, uint32_t(substep_index), hv, w, s);
+         }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, N, stream));
     launches += 4;
     if (nbody > 0) {
@@ -817,20 +867,28 @@ void Ctx::stage_grid(double* mass, double* vel) {
     r.n_active = n_active;
     sort_and_lists(*cur, r);
     EffSet es = make_effset(eff);
-    launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
-               uint32_t(substep_index), stream);
+    dual([&](bool hv, int* w, cudaStream_t s) {
+        launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
+                   staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
+    });
     launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, nullptr, es, stream);
     std::vector<float4> h(gridv.n);
-    // nodes outside the touched blocks hold stale values: clear by list
-    std::vector<int> nbl(geom.nbtot);
-    int nn = 0;
-    CK(cudaMemcpyAsync(&nn, r.n_nb, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    std::vector<int> bm(geom.nbtot);
     CK(cudaMemcpyAsync(h.data(), gridv.p, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(nbl.data(), r.nb_list, nbl.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(bm.data(), blockmap.p, bm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     check_error();
+    // node blocks the grid update wrote (the rest of the dense array is stale)
     std::vector<char> touched(geom.nbtot, 0);
-    for (int k = 0; k < nn; k++) touched[nbl[k]] = 1;
+    for (int b = 0; b < geom.nbtot; b++) {
+        if (bm[b] < 0) continue;
+        int bx, by, bz;
+        block_unlin(geom, b, bx, by, bz);
+        for (int d = 0; d < 8; d++) {
+            int x = bx + (d >> 2), y = by + ((d >> 1) & 1), z = bz + (d & 1);
+            if (x < geom.NB[0] && y < geom.NB[1] && z < geom.NB[2]) touched[block_lin(geom, x, y, z)] = 1;
+        }
+    }
     const int* nd = geom.nd;
     for (int i = 0; i < nd[0]; i++)
         for (int j = 0; j < nd[1]; j++)
@@ -945,8 +1003,10 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
     // rebuild this substep's forward grid (staging -> v, v0) from the pre-state
     CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
     launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap.p, stream);
-    PROF(K_P2G, launch_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, staging.p, d_err.p,
-                           uint32_t(r.substep), stream));
+    PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
+             launch_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
+                        staging.p, d_err.p, uint32_t(r.substep), hv, w, s);
+         }));
     PROF(K_GRID, launch_grid_update(g, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, gridv0.p, r.effk,
                                     stream));
     launches += 3;
@@ -956,12 +1016,16 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
                                        d_chunk_m1.p, rig_partial.p, start_bar.p, abar.p, stream));
         launches += 3;
     }
-    PROF(K_ADJ_G2P, launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, grid_p2g, d_cls.p, gridv.p, post,
-                                   xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, stream));
+    PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
+             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
+                            gridv.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
+         }));
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, gridv0.p, gridbar.p, r.effk,
                                      eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
-    PROF(K_ADJ_P2G, launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, grid_g2p, d_cls.p, gridbar.p, xbar_tmp.p,
-                                   Fbar_tmp.p, out, d_nonfinite.p + t_slot, stream));
+    PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
+             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
+                            xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv, w, s);
+         }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, N, stream));
     launches += 5;
     if (!r.emit.empty()) {
@@ -992,10 +1056,9 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     CK(cudaMemsetAsync(em_out.p, 0, em_out.n * 8, stream));
     CK(cudaMemsetAsync(d_nonfinite.p, 0, size_t(T) * sizeof(int), stream));
 
-    cudaEvent_t ev0, ev1, ev2;
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
-    CK(cudaEventCreate(&ev2));
+    for (auto& e : tev)
+        if (!e) CK(cudaEventCreate(&e));
+    cudaEvent_t ev0 = tev[0], ev1 = tev[1], ev2 = tev[2];
     long launches0 = launches;
 
     // host-side replay context per substep start
@@ -1076,7 +1139,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     if (!std::isfinite(lsum)) throw FlumeError(FLUME_E_ENGINE, "grad_trajectory: non-finite forward loss");
 
     // ---------------- backward ----------------
-    DevArr<float> barsA, barsB;
+    
     barsA.alloc(size_t(N) * 24);
     barsB.alloc(size_t(N) * 24);
     CK(cudaMemsetAsync(barsA.p, 0, barsA.n * 4, stream));
@@ -1142,9 +1205,6 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     float fms = 0, bms = 0;
     CK(cudaEventElapsedTime(&fms, ev0, ev1));
     CK(cudaEventElapsedTime(&bms, ev1, ev2));
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    cudaEventDestroy(ev2);
     restore_host(host0);
     substep_index = s0;
     time = time0;
@@ -1223,7 +1283,7 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     CK(cudaMemcpyAsync(d_up[1].p, vb, size_t(N) * 24, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_up[2].p, Fb, size_t(N) * 72, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_up[3].p, Cb, size_t(N) * 72, cudaMemcpyHostToDevice, stream));
-    DevArr<float> barsA, barsB;
+    
     barsA.alloc(size_t(N) * 24);
     barsB.alloc(size_t(N) * 24);
     launch_bars_from_ref(BarBuf{barsA.p, N}, post->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
@@ -1339,9 +1399,14 @@ int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out) 
 int flume_ctx_destroy(flume_ctx* ctx) {
     if (!ctx) return FLUME_OK;
     cudaStreamSynchronize(ctx->c.stream);
-    cudaStream_t s = ctx->c.stream;
+    cudaStream_t s = ctx->c.stream, s2 = ctx->c.s2;
+    cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join;
+    cudaStreamSynchronize(s2);
     delete ctx;
     if (s) cudaStreamDestroy(s);
+    if (s2) cudaStreamDestroy(s2);
+    if (e1) cudaEventDestroy(e1);
+    if (e2) cudaEventDestroy(e2);
     return FLUME_OK;
 }
 

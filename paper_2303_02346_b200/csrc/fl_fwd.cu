@@ -118,88 +118,21 @@ void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* 
 }
 
 // ---------------------------------------------------------------------------
-// particle-block / node-block lists from the sorted composite keys
+// block map rebuild for the backward (the list itself comes from fl_sort.cu)
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ int ck_block(uint64_t ck, int idbits) { return int(ck >> (idbits + 6)); }
-
-__global__ void k_block_flags(const uint64_t* __restrict__ ck, int n, int idbits, int* flags) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    flags[i] = (i == 0 || ck_block(ck[i], idbits) != ck_block(ck[i - 1], idbits)) ? 1 : 0;
-}
-
-void launch_block_flags(const Geom& g, const uint64_t* ck_sorted, int n_active, int* flags, cudaStream_t s) {
-    if (n_active <= 0) return;
-    k_block_flags<<<(n_active + 255) / 256, 256, 0, s>>>(ck_sorted, n_active, g.idbits, flags);
-}
-
-__global__ void k_block_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* starts,
-                                int* n_blocks) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (flags[i]) starts[pos[i]] = i;
-    if (i == n - 1) *n_blocks = pos[i] + flags[i];
-}
-
-void launch_block_scatter(const int* flags, const int* pos, int n_active, int* starts, int* n_blocks,
-                          cudaStream_t s) {
-    if (n_active <= 0) {
-        cudaMemsetAsync(n_blocks, 0, sizeof(int), s);
-        return;
-    }
-    k_block_scatter<<<(n_active + 255) / 256, 256, 0, s>>>(flags, pos, n_active, starts, n_blocks);
-}
-
-__global__ void k_block_recs(Geom g, const uint64_t* __restrict__ ck, const int* __restrict__ starts,
-                             const int* __restrict__ n_blocks, int n_active, int max_blocks, BlockRec* recs,
-                             int* blockmap, int* nbflag) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    int nb = *n_blocks;
-    if (b >= nb || b >= max_blocks) return;
-    int st = starts[b];
-    int en = (b + 1 < nb) ? starts[b + 1] : n_active;
-    int blk = ck_block(ck[st], g.idbits);
-    recs[b] = BlockRec{blk, st, en};
-    blockmap[blk] = b;
-    int bx, by, bz;
-    block_unlin(g, blk, bx, by, bz);
-    for (int d = 0; d < 8; d++) {
-        int x = bx + (d >> 2), y = by + ((d >> 1) & 1), z = bz + (d & 1);
-        if (x < g.NB[0] && y < g.NB[1] && z < g.NB[2]) nbflag[block_lin(g, x, y, z)] = 1;
-    }
-}
-
-void launch_block_recs(const Geom& g, const uint64_t* ck_sorted, const int* starts, const int* n_blocks,
-                       int n_active, int max_blocks, BlockRec* recs, int* blockmap, int* nbflag,
-                       cudaStream_t s) {
-    if (max_blocks <= 0) return;
-    k_block_recs<<<(max_blocks + 255) / 256, 256, 0, s>>>(g, ck_sorted, starts, n_blocks, n_active, max_blocks,
-                                                          recs, blockmap, nbflag);
-}
-
 __global__ void k_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= *n_blocks || b >= max_blocks) return;
-    blockmap[recs[b].block] = b;
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nl = n_blocks[0], nh = n_blocks[1];
+    if (w >= nl + nh) return;
+    const int q = w < nl ? w : max_blocks - 1 - (w - nl);
+    blockmap[recs[q].block] = q;
 }
 
 void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap,
                          cudaStream_t s) {
     if (max_blocks <= 0) return;
     k_blockmap_set<<<(max_blocks + 255) / 256, 256, 0, s>>>(recs, n_blocks, max_blocks, blockmap);
-}
-
-__global__ void k_nb_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* list,
-                             int* n_list) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (flags[i]) list[pos[i]] = i;
-    if (i == n - 1) *n_list = pos[i] + (flags[i] ? 1 : 0);
-}
-
-void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s) {
-    k_nb_scatter<<<(nbtot + 255) / 256, 256, 0, s>>>(flags, pos, nbtot, list, n_list);
 }
 
 // ---------------------------------------------------------------------------
@@ -231,47 +164,51 @@ void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaSt
 // P2G (mpm.hpp:249-287)
 // ---------------------------------------------------------------------------
 
+template <bool HEAVY>
 __global__ void __launch_bounds__(kScThreads) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
                                                     const BlockRec* __restrict__ recs,
                                                     const int* __restrict__ n_blocks,
+                                                    const uint16_t* __restrict__ celltab,
                                                     const ClassInfo* __restrict__ cls, float4* staging,
-                                                    unsigned long long* err, uint32_t substep) {
-    __shared__ ScSmem sm;
+                                                    unsigned long long* err, uint32_t substep, int* wq) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
     const int tid = threadIdx.x;
-    const int nb = *n_blocks;
+    const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     const int my_c = tid & 63, my_ox = tid >> 6;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    __shared__ int sh_next;
+    for (;;) {
+        const int b = q0 + next_work(wq, &sh_next);
+        if (b >= q1) break;
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
-        float acc[9][4];
-#pragma unroll
-        for (int k = 0; k < 9; k++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) acc[k][q] = 0.f;
-
-        for (int c0 = r.start; c0 < r.end; c0 += kScChunk) {
-            const int n = min(kScChunk, r.end - c0);
-            if (tid < 64) sm.cs[tid] = sm.ce[tid] = 0;
-            __syncthreads();
-            for (int i = tid; i < n; i += kScThreads) {
-                const uint32_t s = perm[c0 + i];
+        __syncthreads();
+        sc_tile_zero(sm, tid, kScThreads);
+        const int npass = sc_load_cells(sm, celltab, b, tid);
+        const int cnt = r.end - r.start;
+        for (int pass = 0; pass < npass; pass++) {
+            const int r0 = pass * kScR;
+            for (int i = tid; i < cnt; i += kScThreads) {
+                const uint32_t s = perm[r.start + i];
                 const uint32_t key = st.key[s];
-                float* pay = &sm.u.pay[i * kPayStride];
-                sm.lc[i] = uint8_t(key & 63);
+                const int c = int(key & 63);
+                const int rank = i - int(sm.cs[c]) - r0;
+                if (rank < 0 || rank >= kScR) continue;
+                float* pay = pay_slot(sm, rank, c);
                 float fx[3];
                 int b0 = base_cell(st.x(0)[s], g.inv_dx, fx[0]);
                 int b1 = base_cell(st.x(1)[s], g.inv_dx, fx[1]);
                 int b2 = base_cell(st.x(2)[s], g.inv_dx, fx[2]);
                 uint32_t lc = uint32_t(((b0 - 4 * bx) << 4) | ((b1 - 4 * by) << 2) | (b2 - 4 * bz));
                 bool inside = b0 >= 4 * bx && b0 < 4 * bx + 4 && b1 >= 4 * by && b1 < 4 * by + 4 && b2 >= 4 * bz &&
-                              b2 < 4 * bz + 4 && lc == (key & 63) && b0 + 2 < g.nd[0] && b1 + 2 < g.nd[1] &&
+                              b2 < 4 * bz + 4 && lc == uint32_t(c) && b0 + 2 < g.nd[0] && b1 + 2 < g.nd[1] &&
                               b2 + 2 < g.nd[2];
                 if (!inside) {
                     atomicMin(err, (unsigned long long)pack_err(substep, ES_P2G_ESCAPE, st.id[s]));
 #pragma unroll
-                    for (int q = 0; q < 16; q++) pay[q] = 0.f;
-                    pay[0] = pay[1] = pay[2] = 1.f;
+                    for (int q = 0; q < kPayF; q++) pay[q * kPayPlane] = 0.f;
+                    pay[0] = pay[kPayPlane] = pay[2 * kPayPlane] = 1.f;
                     continue;
                 }
                 const ClassInfo ci = cls[st.meta[s]];
@@ -282,40 +219,57 @@ __global__ void __launch_bounds__(kScThreads) k_p2g(Geom g, PBuf st, const uint3
                     C.m[k] = st.C(k)[s];
                 }
                 V3<float> v = {st.v(0)[s], st.v(1)[s], st.v(2)[s]};
-                M3<float> fs = (ci.kind == MK_VISCOUS) ? (meye<float>() + C * g.dt) * F : F;
+                M3<float> fs = F;
                 bool ok;
-                M3<float> P = corotated_stress(fs, ci.mu, ci.lambda, ok);
+                M3<float> P;
+                if constexpr (HEAVY) {
+                    if (ci.kind == MK_VISCOUS) fs = (meye<float>() + C * g.dt) * F;
+                    P = corotated_stress(fs, ci.mu, ci.lambda, ok);
+                } else {  // plain liquid: mu = 0, no polar decomposition
+                    const float j = det(fs);
+                    ok = j > 0.f;
+                    P = cofactor(fs) * (ci.lambda * (j - 1.f));
+                }
                 if (!ok) atomicMin(err, (unsigned long long)pack_err(substep, ES_P2G_STRESS, st.id[s]));
                 M3<float> smat = P * transpose(fs);
                 M3<float> affine = C * ci.mass - smat * (g.stress_coeff * ci.vol0);
                 V3<float> f3 = {fx[0], fx[1], fx[2]};
                 V3<float> a = v * ci.mass - (affine * f3) * g.dx;
                 pay[0] = fx[0];
-                pay[1] = fx[1];
-                pay[2] = fx[2];
-                pay[3] = ci.mass;
-                pay[4] = a.x;
-                pay[5] = a.y;
-                pay[6] = a.z;
+                pay[kPayPlane] = fx[1];
+                pay[2 * kPayPlane] = fx[2];
+                pay[3 * kPayPlane] = ci.mass;
+                pay[4 * kPayPlane] = a.x;
+                pay[5 * kPayPlane] = a.y;
+                pay[6 * kPayPlane] = a.z;
 #pragma unroll
-                for (int k = 0; k < 9; k++) pay[7 + k] = affine.m[k] * g.dx;
+                for (int k = 0; k < 9; k++) pay[(7 + k) * kPayPlane] = affine.m[k] * g.dx;
             }
             __syncthreads();
-            sc_ranges(sm, n, tid, kScThreads);
-            __syncthreads();
-            sc_accumulate<4>(sm, my_c, my_ox, acc);
+            const int nr = min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR);
+            sc_accumulate<4>(sm, my_c, my_ox, nr);
             __syncthreads();
         }
-        sc_store_cellpart<4>(sm, my_c, my_ox, acc);
         __syncthreads();
-        sc_tile(sm, staging + size_t(b) * kTile, tid, kScThreads);
-        __syncthreads();
+        sc_tile_store(sm, staging + size_t(b) * kTile, tid, kScThreads);
     }
 }
 
-void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks, int grid,
-                const ClassInfo* cls, float4* staging, unsigned long long* err, uint32_t substep, cudaStream_t s) {
-    k_p2g<<<grid, kScThreads, 0, s>>>(g, st, perm, recs, n_blocks, cls, staging, err, substep);
+void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
+                const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
+                uint32_t substep, bool heavy, int* wq, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
+        cudaFuncSetAttribute(k_p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
+        attr = true;
+    }
+    if (heavy)
+        k_p2g<true><<<grid, kScThreads, sizeof(ScSmem), s>>>(g, st, perm, recs, n_blocks, celltab, cls, staging, err,
+                                                            substep, wq);
+    else
+        k_p2g<false><<<grid, kScThreads, sizeof(ScSmem), s>>>(g, st, perm, recs, n_blocks, celltab, cls, staging, err,
+                                                             substep, wq);
 }
 
 // ---------------------------------------------------------------------------
@@ -382,14 +336,18 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 // G2P (mpm.hpp:338-384) with the per-material return map
 // ---------------------------------------------------------------------------
 
+template <bool HEAVY>
 __global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
-                                             RigidDev rd, unsigned long long* err, uint32_t substep) {
+                                             RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {
     __shared__ float4 vt[kTile];
     const int tid = threadIdx.x;
-    const int nb = *n_blocks;
-    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
+    __shared__ int sh_next;
+    for (;;) {
+        const int b = q0 + next_work(wq, &sh_next);
+        if (b >= q1) break;
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
@@ -419,12 +377,16 @@ __global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const ui
             const M3<float> ftr = (meye<float>() + cnew * g.dt) * F;
             M3<float> fnew = ftr;
             bool ok = true;
-            switch (ci.kind) {
-                case MK_LIQUID:
-                case MK_VISCOUS: fnew = liquid_project(ftr, ok); break;
-                case MK_PLASTIC: fnew = box_yield_project(ftr, ci.theta_c, ci.theta_s, ok); break;
-                case MK_NONNEWTONIAN: fnew = von_mises_project(ftr, ci.sigma_y, ci.mu, ok); break;
-                default: break;
+            if constexpr (HEAVY) {
+                switch (ci.kind) {
+                    case MK_LIQUID:
+                    case MK_VISCOUS: fnew = liquid_project(ftr, ok); break;
+                    case MK_PLASTIC: fnew = box_yield_project(ftr, ci.theta_c, ci.theta_s, ok); break;
+                    case MK_NONNEWTONIAN: fnew = von_mises_project(ftr, ci.sigma_y, ci.mu, ok); break;
+                    default: break;
+                }
+            } else {
+                fnew = liquid_project(ftr, ok);
             }
             if (!ok) atomicMin(err, (unsigned long long)pack_err(substep, ES_G2P_PROJECT, pid));
 #pragma unroll
@@ -442,7 +404,7 @@ __global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const ui
             uint32_t key;
             cell_key(g, xn.x, xn.y, xn.z, key);
             out.key[j] = key;
-            if (ci.rigid >= 0) {
+            if (HEAVY && ci.rigid >= 0) {
                 // rigid members carry fp64 positions: v = dx/dt in rigid_body_pass
                 // (mpm.hpp:412) would otherwise amplify fp32 rounding by 1/dt
                 const int mr = rd.mrank[pid];
@@ -465,8 +427,11 @@ __global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const ui
 
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd, unsigned long long* err,
-                uint32_t substep, cudaStream_t s) {
-    k_g2p<<<grid, 128, 0, s>>>(g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep);
+                uint32_t substep, bool heavy, int* wq, cudaStream_t s) {
+    if (heavy)
+        k_g2p<true><<<grid, 128, 0, s>>>(g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
+    else
+        k_g2p<false><<<grid, 128, 0, s>>>(g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
 }
 
 __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
@@ -631,38 +596,48 @@ __global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const Clas
     }
 }
 
+// warp k sums term k over the block partials (strided lanes + fixed shuffle tree)
 __global__ void k_loss_final(const double* partial, int nblocks, LossSet ls, uint32_t mask, double* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double total = 0.0;
-    for (int k = 0; k < ls.n; k++) {
-        if (!((mask >> k) & 1u)) continue;
-        double s = 0.0;
-        for (int b = 0; b < nblocks; b++) s += partial[size_t(b) * kMaxLossTerms + k];
-        total += ls.t[k].weight * s;
+    __shared__ double term[kMaxLossTerms];
+    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+    double s = 0.0;
+    if (k < ls.n)
+        for (int b = lane; b < nblocks; b += 32) s += partial[size_t(b) * kMaxLossTerms + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) term[k] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double total = 0.0;
+        for (int q = 0; q < ls.n; q++)
+            if ((mask >> q) & 1u) total += ls.t[q].weight * term[q];
+        *out = total;
     }
-    *out = total;
 }
 
 void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, double* partial,
                  double* out, uint32_t key_inactive, cudaStream_t s) {
     k_loss_partial<<<kLossBlocks, 256, 0, s>>>(st, n, cls, ls, mask, key_inactive, partial);
-    k_loss_final<<<1, 32, 0, s>>>(partial, kLossBlocks, ls, mask, out);
+    k_loss_final<<<1, 32 * kMaxLossTerms, 0, s>>>(partial, kLossBlocks, ls, mask, out);
 }
 
-int p2g_occupancy_grid() {
+int occupancy_grid_fwd(KGrid which, bool heavy) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2g, kScThreads, 0);
-    if (per < 1) per = 1;
-    return sms * per;
-}
-
-int g2p_occupancy_grid() {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_g2p, 128, 0);
+    if (which == KG_P2G) {
+        cudaFuncSetAttribute(k_p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
+        cudaFuncSetAttribute(k_p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
+        if (heavy)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2g<true>, kScThreads, sizeof(ScSmem));
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2g<false>, kScThreads, sizeof(ScSmem));
+    } else {
+        if (heavy)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_g2p<true>, 128, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_g2p<false>, 128, 0);
+    }
     if (per < 1) per = 1;
     return sms * per;
 }

@@ -58,7 +58,7 @@ struct LossSet {
 };
 
 constexpr int kLossBlocks = 296;
-constexpr int kEffBlocks = 592;
+constexpr int kEffBlocks = 1184;
 constexpr int kRigidChunk = 2048;
 
 // ---- forward ----
@@ -66,22 +66,16 @@ void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double
                    const double* C, const uint32_t* meta, const uint8_t* active, cudaStream_t s);
 void launch_make_sortkeys(const Geom& g, const PBuf& st, int n, uint64_t* ck, uint32_t* idx, cudaStream_t s);
 void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
-void launch_block_flags(const Geom& g, const uint64_t* ck_sorted, int n_active, int* flags, cudaStream_t s);
-void launch_block_scatter(const int* flags, const int* pos, int n_active, int* starts, int* n_blocks, cudaStream_t s);
-void launch_block_recs(const Geom& g, const uint64_t* ck_sorted, const int* starts, const int* n_blocks,
-                       int n_active, int max_blocks, BlockRec* recs, int* blockmap, int* nbflag,
-                       cudaStream_t s);
 void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap, cudaStream_t s);
-void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s);
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s);
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
-                int grid, const ClassInfo* cls, float4* staging, unsigned long long* err, uint32_t substep,
-                cudaStream_t s);
+                const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
+                uint32_t substep, bool heavy, int* wq, cudaStream_t s);
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, cudaStream_t s);
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs,
                 const int* n_blocks, int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd,
-                unsigned long long* err, uint32_t substep, cudaStream_t s);
+                unsigned long long* err, uint32_t substep, bool heavy, int* wq, cudaStream_t s);
 void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
 void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body,
                   const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
@@ -99,14 +93,15 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
                       const int* chunk_m0, const int* chunk_m1, double* partial, float* start_bar,
                       double* abar, cudaStream_t s);
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
-                    int grid, const ClassInfo* cls, const float4* gridv, BarBuf post, float* xbar_tmp,
-                    float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar, cudaStream_t s);
+                    const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, BarBuf post, float* xbar_tmp,
+                    float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar, bool heavy, int* wq,
+                    cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                      double* eff_partial, double* eff_out, cudaStream_t s);
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
-                    const float* Fbar_tmp, BarBuf out, int* nonfinite, cudaStream_t s);
+                    const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s);
 void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
 void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
 void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb,
@@ -114,7 +109,17 @@ void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, 
 void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* vb, double* Fb, double* Cb,
                         cudaStream_t s);
 
-int p2g_occupancy_grid();
-int g2p_occupancy_grid();
+void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
+                       cudaStream_t s);
+void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, const int* bcount,
+                         const int* bheavy, int* bfill, uint32_t* skey, uint32_t* sslot, BlockRec* recs, int* n_blocks,
+                         int* blockmap, int* nbflag, int cap, cudaStream_t s);
+void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s);
+void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
+                        const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
+                        uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s);
+
+enum KGrid { KG_P2G = 0, KG_G2P = 1, KG_ADJ_G2P = 2, KG_ADJ_P2G = 3 };
+int occupancy_grid(KGrid which, bool heavy);  // resident CTAs per SM x SMs
 
 }  // namespace fl

@@ -25,6 +25,7 @@ struct Geom {
     int nd[3];      // node dims (res+1 per axis, types.hpp:84-88)
     int NB[3];      // 4^3 blocks per axis (cover nd)
     int nbtot;      // NB0*NB1*NB2
+    int maxb;       // particle-block list capacity: light blocks at [0, n0), heavy at [maxb - n1, maxb)
     uint32_t key_inactive;  // nbtot << 6, sorts after every valid key
     int keybits;    // bits needed for key_inactive
     int idbits;     // bits needed for particle ids
@@ -45,6 +46,7 @@ struct ClassInfo {
     int kind;
     int body;
     int rigid;   // rigid-body index or -1
+    int heavy;   // needs the SVD / rigid code paths (anything but a plain liquid)
     float mass, vol0;
     float mu, lambda, theta_c, theta_s, sigma_y;
 };

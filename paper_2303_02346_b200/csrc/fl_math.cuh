@@ -279,34 +279,46 @@ FL_HD Svd<T> svd3(const M3<T>& a) {
         jacobi_rotate(b, v, 1, 2, off);
         if (off < SvdTol<T>::stop) break;
     }
-    T sg[3];
-#pragma unroll
-    for (int j = 0; j < 3; j++) sg[j] = sqrt(b.m[j] * b.m[j] + b.m[3 + j] * b.m[3 + j] + b.m[6 + j] * b.m[6 + j]);
-    // stable descending order of three values
-    int o0 = 0, o1 = 1, o2 = 2, tmp;
-    if (sg[o1] > sg[o0]) { tmp = o0; o0 = o1; o1 = tmp; }
-    if (sg[o2] > sg[o1]) {
-        tmp = o1; o1 = o2; o2 = tmp;
-        if (sg[o1] > sg[o0]) { tmp = o0; o0 = o1; o1 = tmp; }
-    }
-    int ord[3] = {o0, o1, o2};
-    Svd<T> out;
-#pragma unroll
-    for (int jj = 0; jj < 3; jj++) {
-        int j = ord[jj];
-        T sj = sg[j];
-        (&out.s.x)[jj] = sj;
-        T inv = sj > SvdTol<T>::null_sigma ? T(1) / sj : T(0);
+    // column norms, then a stable descending sort by swapping whole columns
+    // (static indices only: no local-memory arrays)
+    T s0 = sqrt(b.m[0] * b.m[0] + b.m[3] * b.m[3] + b.m[6] * b.m[6]);
+    T s1 = sqrt(b.m[1] * b.m[1] + b.m[4] * b.m[4] + b.m[7] * b.m[7]);
+    T s2 = sqrt(b.m[2] * b.m[2] + b.m[5] * b.m[5] + b.m[8] * b.m[8]);
+    auto swap01 = [&]() {
+        T t = s0; s0 = s1; s1 = t;
 #pragma unroll
         for (int i = 0; i < 3; i++) {
-            out.V.m[3 * i + jj] = v.m[3 * i + j];
-            out.U.m[3 * i + jj] = b.m[3 * i + j] * inv;
+            t = b.m[3 * i]; b.m[3 * i] = b.m[3 * i + 1]; b.m[3 * i + 1] = t;
+            t = v.m[3 * i]; v.m[3 * i] = v.m[3 * i + 1]; v.m[3 * i + 1] = t;
         }
+    };
+    auto swap12 = [&]() {
+        T t = s1; s1 = s2; s2 = t;
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+            t = b.m[3 * i + 1]; b.m[3 * i + 1] = b.m[3 * i + 2]; b.m[3 * i + 2] = t;
+            t = v.m[3 * i + 1]; v.m[3 * i + 1] = v.m[3 * i + 2]; v.m[3 * i + 2] = t;
+        }
+    };
+    if (s1 > s0) swap01();
+    if (s2 > s1) {
+        swap12();
+        if (s1 > s0) swap01();
+    }
+    Svd<T> out;
+    out.s = V3<T>{s0, s1, s2};
+    out.V = v;
+#pragma unroll
+    for (int jj = 0; jj < 3; jj++) {
+        const T sj = jj == 0 ? s0 : (jj == 1 ? s1 : s2);
+        const T inv = sj > SvdTol<T>::null_sigma ? T(1) / sj : T(0);
+#pragma unroll
+        for (int i = 0; i < 3; i++) out.U.m[3 * i + jj] = b.m[3 * i + jj] * inv;
     }
     // rebuild null columns of U (svd.hpp:88-106)
 #pragma unroll
     for (int j = 0; j < 3; j++) {
-        if ((&out.s.x)[j] > SvdTol<T>::null_sigma) continue;
+        if (out.s[j] > SvdTol<T>::null_sigma) continue;
         for (int axis = 0; axis < 3; axis++) {
             V3<T> c = v3zero<T>();
             c[axis] = T(1);
@@ -353,7 +365,9 @@ FL_HD M3<T> svd_vjp(const Svd<T>& t, const M3<T>& u_bar, V3<T> sig_bar, const M3
     M3<T> bu = transpose(t.U) * u_bar;
     M3<T> bv = transpose(t.V) * v_bar;
     M3<T> inner = mdiag(sig_bar);
+#pragma unroll
     for (int i = 0; i < 3; i++)
+#pragma unroll
         for (int j = 0; j < 3; j++) {
             if (i == j) continue;
             T si = t.s[i], sj = t.s[j];
@@ -373,7 +387,9 @@ FL_HD M3<T> spectral_map_vjp(const Svd<T>& t, const double g[3], const double jg
     const double gap_tol = 1e-8;
     double s[3] = {double(t.s.x), double(t.s.y), double(t.s.z)};
     M3<T> p_bar = mzero<T>();
+#pragma unroll
     for (int i = 0; i < 3; i++)
+#pragma unroll
         for (int j = 0; j < 3; j++) {
             if (i == j) continue;
             double sum = s[i] + s[j];
@@ -393,7 +409,9 @@ FL_HD M3<T> spectral_map_vjp(const Svd<T>& t, const double g[3], const double jg
             p_bar.m[3 * i + j] += T(a) * q_bar.m[3 * i + j];
             p_bar.m[3 * j + i] += T(b) * q_bar.m[3 * i + j];
         }
+#pragma unroll
     for (int i = 0; i < 3; i++)
+#pragma unroll
         for (int k = 0; k < 3; k++) p_bar.m[4 * k] += T(jg[3 * i + k]) * q_bar.m[4 * i];
     return t.U * p_bar * transpose(t.V);
 }

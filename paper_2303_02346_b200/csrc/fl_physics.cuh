@@ -181,12 +181,24 @@ FL_HD M3<T> corotated_stress_vjp(const M3<T>& f, T mu, T lambda, const M3<T>& p_
     return f_bar;
 }
 
+// the lambda (J-1) cofactor(F) part of corotated_stress_vjp alone (mu = 0 liquids)
+template <class T>
+FL_HD M3<T> pressure_stress_vjp(const M3<T>& f, T lambda, const M3<T>& p_bar) {
+    T j = det(f);
+    M3<T> finv_t = transpose(inverse(f));
+    T s = lambda * (j - T(1)) * j;
+    M3<T> f_bar = finv_t * (j * lambda * (T(2) * j - T(1)) * ddot(p_bar, finv_t));
+    f_bar -= (finv_t * transpose(p_bar) * finv_t) * s;
+    return f_bar;
+}
+
 // materials.hpp:55-63
 template <class T>
 FL_HD M3<T> box_yield_project(const M3<T>& f, T theta_c, T theta_s, bool& ok) {
     ok = det(f) > T(0);
     Svd<T> t = svd3(f);
     V3<T> s;
+#pragma unroll
     for (int i = 0; i < 3; i++) s[i] = clamp_ref(t.s[i], T(1) - theta_c, T(1) + theta_s);
     return usv(t, s);
 }
@@ -195,6 +207,7 @@ template <class T>
 FL_HD M3<T> box_yield_project_vjp(const M3<T>& f, T theta_c, T theta_s, const M3<T>& out_bar) {
     Svd<T> t = svd3(f);
     double g[3], jg[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
     for (int i = 0; i < 3; i++) {
         T si = t.s[i];
         g[i] = double(clamp_ref(si, T(1) - theta_c, T(1) + theta_s));
@@ -210,12 +223,14 @@ FL_HD M3<T> von_mises_project(const M3<T>& f, T sigma_y, T mu, bool& ok) {
     Svd<T> t = svd3(f);
     ok = t.s.x > T(0) && t.s.y > T(0) && t.s.z > T(0);
     T eps[3], mean = T(0);
+#pragma unroll
     for (int i = 0; i < 3; i++) {
         eps[i] = log(t.s[i]);
         mean += eps[i];
     }
     mean /= T(3);
     T dev[3], dn2 = T(0);
+#pragma unroll
     for (int i = 0; i < 3; i++) {
         dev[i] = eps[i] - mean;
         dn2 += dev[i] * dev[i];
@@ -224,6 +239,7 @@ FL_HD M3<T> von_mises_project(const M3<T>& f, T sigma_y, T mu, bool& ok) {
     if (T(2) * mu * dn <= sigma_y) return f;
     T scale = sigma_y / (T(2) * mu * dn);
     V3<T> s;
+#pragma unroll
     for (int i = 0; i < 3; i++) s[i] = exp(mean + scale * dev[i]);
     return usv(t, s);
 }
@@ -234,12 +250,14 @@ FL_HD M3<T> von_mises_project_vjp(const M3<T>& f, T sigma_y, T mu, const M3<T>& 
     Svd<T> t = svd3(f);
     double sd[3] = {double(t.s.x), double(t.s.y), double(t.s.z)};
     double eps[3], mean = 0;
+#pragma unroll
     for (int i = 0; i < 3; i++) {
         eps[i] = log(sd[i]);
         mean += eps[i];
     }
     mean /= 3.0;
     double dev[3], dn2 = 0;
+#pragma unroll
     for (int i = 0; i < 3; i++) {
         dev[i] = eps[i] - mean;
         dn2 += dev[i] * dev[i];
@@ -248,12 +266,17 @@ FL_HD M3<T> von_mises_project_vjp(const M3<T>& f, T sigma_y, T mu, const M3<T>& 
     double g[3], jg[9];
     double muD = double(mu), syD = double(sigma_y);
     if (2 * muD * dn <= syD) {
+#pragma unroll
         for (int i = 0; i < 3; i++) g[i] = sd[i];
+#pragma unroll
         for (int k = 0; k < 9; k++) jg[k] = (k % 4 == 0) ? 1.0 : 0.0;
     } else {
         double scale = syD / (2 * muD * dn);
+#pragma unroll
         for (int i = 0; i < 3; i++) g[i] = exp(mean + scale * dev[i]);
+#pragma unroll
         for (int i = 0; i < 3; i++)
+#pragma unroll
             for (int k = 0; k < 3; k++) {
                 double m = (i == k ? 1.0 : 0.0) - 1.0 / 3.0;
                 double jeps = 1.0 / 3.0 + scale * (m - (dev[i] / dn) * (dev[k] / dn));

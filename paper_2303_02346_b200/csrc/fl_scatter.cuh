@@ -15,43 +15,66 @@
 namespace fl {
 
 constexpr int kScThreads = 192;  // 64 cells x 3 planes
-constexpr int kScChunk = 512;    // particles staged per pass
-constexpr int kPayStride = 17;   // 16 payload floats, odd stride vs. bank conflicts
+constexpr int kScR = 8;          // particle ranks per cell staged per pass (8 = ppc 2^3)
+constexpr int kCS = 68;          // rank stride = 4 (mod 32): conflict-free for 8 ranks x 4 cells and 32 cells
+constexpr int kPayF = 16;        // payload floats per particle
+constexpr int kCellTab = 66;     // per block: 64 cell starts + end (+pad), u16
 
-struct ScSmem {
-    union {
-        float pay[kScChunk * kPayStride];
-        float cellpart[64 * 27 * 4];
-    } u;
-    uint8_t lc[kScChunk];
-    int16_t cs[64], ce[64];
+// Payload staged as pay[f][rank][cell]: the payload phase (lanes = consecutive
+// particles of a cell, consecutive ranks) and the accumulate phase (lanes =
+// consecutive cells, same rank) both hit distinct banks.  The 6^3 node tile is
+// kept as four channel planes and filled by 27 ordered passes (one per
+// stencil offset): within a pass every cell adds into a different node, and
+// the pass order fixes the summation order of every node.
+struct alignas(16) ScSmem {
+    float pay[kPayF * kScR * kCS];
+    float tile[4 * kTile];
+    uint16_t cs[kCellTab];
 };
 
-__device__ __forceinline__ void sc_ranges(ScSmem& sm, int n, int tid, int nthreads) {
-    for (int i = tid; i < n; i += nthreads) {
-        const int c = sm.lc[i];
-        if (i == 0 || sm.lc[i - 1] != c) sm.cs[c] = int16_t(i);
-        if (i == n - 1 || sm.lc[i + 1] != c) sm.ce[c] = int16_t(i + 1);
-    }
+__device__ __forceinline__ float* pay_slot(ScSmem& sm, int rank, int cell) { return &sm.pay[rank * kCS + cell]; }
+constexpr int kPayPlane = kScR * kCS;  // floats between payload fields
+
+// dynamic block scheduling: a CTA grabs the next list slot from a work counter
+// (results do not depend on which CTA processes which block)
+__device__ __forceinline__ int next_work(int* counter, int* sh) {
+    __syncthreads();
+    if (threadIdx.x == 0) *sh = atomicAdd(counter, 1);
+    __syncthreads();
+    return *sh;
 }
 
-// payload layout: [0..2] fx, then (NCH==4 ? m : -), a[3], Bm[9] row-major
+__device__ __forceinline__ void sc_tile_zero(ScSmem& sm, int tid, int nthreads) {
+    for (int i = tid; i < 4 * int(kTile); i += nthreads) sm.tile[i] = 0.f;
+}
+
+// Thread (cell c, plane ox) sums the 9 nodes (ox, oy, oz) over the particles of
+// cell c staged in this pass, in rank (= particle id) order, then folds them
+// into the tile in 27 ordered passes.  Must be reached by all threads.
+// payload fields: [0..2] fx, then (NCH==4 ? m : -), a[3], Bm[9] row-major
 template <int NCH>
-__device__ __forceinline__ void sc_accumulate(const ScSmem& sm, int c, int ox, float (&acc)[9][4]) {
+__device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nrank) {
     constexpr int A0 = (NCH == 4) ? 4 : 3;
+    float acc[9][4];
+#pragma unroll
+    for (int k = 0; k < 9; k++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[k][q] = 0.f;
     const float oxf = float(ox);
-    for (int i = sm.cs[c]; i < sm.ce[c]; i++) {
-        const float* p = &sm.u.pay[i * kPayStride];
+    for (int r = 0; r < nrank; r++) {
+        const float* p = &sm.pay[r * kCS + c];
+#define PF(f) p[(f) * kPayPlane]
         float wxa[3], wy[3], wz[3];
-        bspline_w(p[0], wxa);
-        bspline_w(p[1], wy);
-        bspline_w(p[2], wz);
-        const float wx = wxa[ox];
-        const float m = (NCH == 4) ? p[3] : 0.f;
-        const float b00 = p[A0 + 3], b01 = p[A0 + 4], b02 = p[A0 + 5];
-        const float b10 = p[A0 + 6], b11 = p[A0 + 7], b12 = p[A0 + 8];
-        const float b20 = p[A0 + 9], b21 = p[A0 + 10], b22 = p[A0 + 11];
-        const float a0x = p[A0] + b00 * oxf, a0y = p[A0 + 1] + b10 * oxf, a0z = p[A0 + 2] + b20 * oxf;
+        bspline_w(PF(0), wxa);
+        bspline_w(PF(1), wy);
+        bspline_w(PF(2), wz);
+        const float wx = ox == 0 ? wxa[0] : (ox == 1 ? wxa[1] : wxa[2]);
+        const float m = (NCH == 4) ? PF(3) : 0.f;
+        const float b00 = PF(A0 + 3), b01 = PF(A0 + 4), b02 = PF(A0 + 5);
+        const float b10 = PF(A0 + 6), b11 = PF(A0 + 7), b12 = PF(A0 + 8);
+        const float b20 = PF(A0 + 9), b21 = PF(A0 + 10), b22 = PF(A0 + 11);
+        const float a0x = PF(A0) + b00 * oxf, a0y = PF(A0 + 1) + b10 * oxf, a0z = PF(A0 + 2) + b20 * oxf;
+#undef PF
 #pragma unroll
         for (int oy = 0; oy < 3; oy++) {
             const float oyf = float(oy);
@@ -76,39 +99,36 @@ __device__ __forceinline__ void sc_accumulate(const ScSmem& sm, int c, int ox, f
             }
         }
     }
-}
-
-template <int NCH>
-__device__ __forceinline__ void sc_store_cellpart(ScSmem& sm, int c, int ox, const float (&acc)[9][4]) {
+    const int cx = c >> 4, cy = (c >> 2) & 3, cz = c & 3;
 #pragma unroll
-    for (int k = 0; k < 9; k++) {
-        float* d = &sm.u.cellpart[(c * 27 + ox * 9 + k) * 4];
+    for (int px = 0; px < 3; px++) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) d[q] = (q < NCH) ? acc[k][q] : 0.f;
+        for (int k = 0; k < 9; k++) {
+            __syncthreads();
+            if (px == ox) {
+                const int t = (cx + ox) * 36 + (cy + k / 3) * 6 + (cz + k % 3);
+#pragma unroll
+                for (int q = 0; q < NCH; q++) sm.tile[q * kTile + t] += acc[k][q];
+            }
+        }
     }
 }
 
-// fold cell partials into the 6^3 tile (fixed order) and store it
-__device__ __forceinline__ void sc_tile(const ScSmem& sm, float4* out, int tid, int nthreads) {
-    for (int t = tid; t < int(kTile); t += nthreads) {
-        const int tx = t / 36, ty = (t / 6) % 6, tz = t % 6;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        const int cx0 = tx > 2 ? tx - 2 : 0, cx1 = tx < 3 ? tx : 3;
-        const int cy0 = ty > 2 ? ty - 2 : 0, cy1 = ty < 3 ? ty : 3;
-        const int cz0 = tz > 2 ? tz - 2 : 0, cz1 = tz < 3 ? tz : 3;
-        for (int cx = cx0; cx <= cx1; cx++)
-            for (int cy = cy0; cy <= cy1; cy++)
-                for (int cz = cz0; cz <= cz1; cz++) {
-                    const int c = cx * 16 + cy * 4 + cz;
-                    const int k = (tx - cx) * 9 + (ty - cy) * 3 + (tz - cz);
-                    const float* p = &sm.u.cellpart[(c * 27 + k) * 4];
-                    s0 += p[0];
-                    s1 += p[1];
-                    s2 += p[2];
-                    s3 += p[3];
-                }
-        out[t] = make_float4(s0, s1, s2, s3);
+// load the block's cell table; returns the pass count ceil(max cell count / kScR)
+__device__ __forceinline__ int sc_load_cells(ScSmem& sm, const uint16_t* __restrict__ celltab, int slot, int tid) {
+    if (tid < kCellTab) sm.cs[tid] = celltab[size_t(slot) * kCellTab + tid];
+    __syncthreads();
+    int mx = 0;
+    for (int c = 0; c < 64; c++) {
+        int n = int(sm.cs[c + 1]) - int(sm.cs[c]);
+        mx = n > mx ? n : mx;
     }
+    return (mx + kScR - 1) / kScR;
+}
+
+__device__ __forceinline__ void sc_tile_store(const ScSmem& sm, float4* out, int tid, int nthreads) {
+    for (int t = tid; t < int(kTile); t += nthreads)
+        out[t] = make_float4(sm.tile[t], sm.tile[kTile + t], sm.tile[2 * kTile + t], sm.tile[3 * kTile + t]);
 }
 
 // 6^3 node tile of a block-major float4 grid into shared memory
