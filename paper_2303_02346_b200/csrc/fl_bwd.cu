@@ -470,16 +470,20 @@ __global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int*
     }
 }
 
-// one warp per (effector, component): strided lane sums + fixed shuffle tree
-__global__ void k_eff_final(const double* partial, int nblocks, int nvals, double* out) {
-    const int lane = threadIdx.x & 31;
-    for (int q = threadIdx.x >> 5; q < kMaxEff * kEffQ; q += blockDim.x >> 5) {
-        double s = 0.0;
-        if (q < nvals)
-            for (int b = lane; b < nblocks; b += 32) s += partial[size_t(b) * kMaxEff * kEffQ + q];
+// one CTA per (effector, component): strided thread sums + fixed shuffle tree
+__global__ void __launch_bounds__(256) k_eff_final(const double* partial, int nblocks, double* out) {
+    __shared__ double wsum[8];
+    const int q = blockIdx.x, tid = threadIdx.x;
+    double s = 0.0;
+    for (int b = tid; b < nblocks; b += 256) s += partial[size_t(b) * kMaxEff * kEffQ + q];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-        if (lane == 0) out[q] = s;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((tid & 31) == 0) wsum[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; w++) t += wsum[w];
+        out[q] = t;
     }
 }
 
@@ -498,7 +502,7 @@ void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const i
         default: k_adj_grid<kMaxEff><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar,
                                                                             gridv0, gridbar, eff, eff_partial);
     }
-    k_eff_final<<<1, 1024, 0, s>>>(eff_partial, kEffBlocks, eff.n * kEffQ, eff_out);
+    if (eff.n > 0) k_eff_final<<<eff.n * kEffQ, 256, 0, s>>>(eff_partial, kEffBlocks, eff_out);
 }
 
 // ---------------------------------------------------------------------------

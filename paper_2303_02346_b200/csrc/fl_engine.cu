@@ -118,6 +118,8 @@ struct Record {
     double* mid = nullptr;
     double* fit = nullptr;
     uint16_t* celltab = nullptr;
+    float4* gridv = nullptr;   // grid velocity after contact (G2P input), dense block-major
+    float4* gridv0 = nullptr;  // (p/m, m) before gravity/walls/contact (grid-update adjoint input)
     int n_active = 0;
     long substep = 0;
     std::vector<ActEntry> act;
@@ -133,7 +135,8 @@ struct Record {
         size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(16),
                o_nbl = carve(size_t(nbtot) * 4), o_nnb = carve(16), o_ms = carve(size_t(nmem) * 4),
                o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 24),
-               o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2);
+               o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),
+               o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4));
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -146,6 +149,10 @@ struct Record {
         mid = reinterpret_cast<double*>(b + o_mid);
         fit = reinterpret_cast<double*>(b + o_fit);
         celltab = reinterpret_cast<uint16_t*>(b + o_ct);
+        gridv = reinterpret_cast<float4*>(b + o_gv);
+        gridv0 = reinterpret_cast<float4*>(b + o_gv0);
+        CK(cudaMemset(gridv, 0, size_t(nbtot) * 64 * sizeof(float4)));
+        CK(cudaMemset(gridv0, 0, size_t(nbtot) * 64 * sizeof(float4)));
     }
     ~Record() { cudaFree(mem); }
 };
@@ -299,7 +306,7 @@ struct Ctx {
     DevArr<unsigned char> cub_tmp;
     size_t cub_bytes = 0;
     DevArr<int> blockmap;
-    DevArr<float4> staging, gridv, gridv0, staging_bar, gridbar;
+    DevArr<float4> staging, staging_bar, gridbar;
     DevArr<unsigned long long> d_err;
     DevArr<int> d_nonfinite;
     DevArr<double> rig_partial, abar, eff_partial, eff_out, em_out, loss_partial, loss_out;
@@ -342,7 +349,7 @@ struct Ctx {
             rec_pool.pop_back();
             return r;
         }
-        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1));
+        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1));  // ~2 KB/node block
     }
     void put_record(RecordPtr r) {
         if (r) rec_pool.push_back(std::move(r));
@@ -545,8 +552,6 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     blockmap.alloc(g.nbtot);
     staging.alloc(size_t(maxb) * kTile);
     staging_bar.alloc(size_t(maxb) * kTile);
-    gridv.alloc(size_t(g.nbtot) * 64);
-    gridv0.alloc(size_t(g.nbtot) * 64);
     gridbar.alloc(size_t(g.nbtot) * 64);
     d_err.alloc(1);
     CK(cudaMemsetAsync(d_err.p, 0xff, sizeof(unsigned long long), stream));
@@ -558,8 +563,6 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     loss_partial.alloc(size_t(kLossBlocks) * kMaxLossTerms);
     d_act_list.alloc(64);
     d_emit_list.alloc(64);
-    CK(cudaMemsetAsync(gridv.p, 0, gridv.n * sizeof(float4), stream));
-    CK(cudaMemsetAsync(gridv0.p, 0, gridv0.n * sizeof(float4), stream));
     CK(cudaMemsetAsync(gridbar.p, 0, gridbar.n * sizeof(float4), stream));
 
     size_t b2 = 0, b3 = 0;
@@ -828,8 +831,8 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
          }));
-    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p,
-                                    record_grid ? gridv0.p : nullptr, r.effk, stream));
+    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, r.gridv, r.gridv0,
+                                    r.effk, stream));
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
         CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
@@ -837,7 +840,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                            stream));
     }
     PROF(K_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : grid_g2p, d_cls.p, gridv.p,
+             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : grid_g2p, d_cls.p, r.gridv,
                         rd, d_err.p, uint32_t(substep_index), hv, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, N, stream));
@@ -871,10 +874,10 @@ void Ctx::stage_grid(double* mass, double* vel) {
         launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
                    staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
     });
-    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, nullptr, es, stream);
-    std::vector<float4> h(gridv.n);
+    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, r.gridv, r.gridv0, es, stream);
+    std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
-    CK(cudaMemcpyAsync(h.data(), gridv.p, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(h.data(), r.gridv, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(bm.data(), blockmap.p, bm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     check_error();
@@ -1000,16 +1003,11 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
 void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre, int t_slot) {
     Geom& g = geom;
     BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
-    // rebuild this substep's forward grid (staging -> v, v0) from the pre-state
+    // the forward recorded this substep's grid (r.gridv, r.gridv0); only the
+    // particle-block map is rebuilt for the staging gathers
     CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
     launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap.p, stream);
-    PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
-                        staging.p, d_err.p, uint32_t(r.substep), hv, w, s);
-         }));
-    PROF(K_GRID, launch_grid_update(g, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, gridv.p, gridv0.p, r.effk,
-                                    stream));
-    launches += 3;
+    launches += 1;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
         PROF(K_RIGID, launch_adj_rigid(g, post, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p,
@@ -1018,9 +1016,9 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
-                            gridv.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
+                            r.gridv, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
          }));
-    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, gridv0.p, gridbar.p, r.effk,
+    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
                                      eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
