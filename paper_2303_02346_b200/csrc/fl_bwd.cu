@@ -178,7 +178,7 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
 // G2P adjoint (adjoint.hpp:281-365): gather + deterministic scatter of grid v_bar
 // ---------------------------------------------------------------------------
 template <bool HEAVY>
-__global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : 3) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                         const BlockRec* __restrict__ recs,
                                                         const int* __restrict__ n_blocks,
                                                         const uint16_t* __restrict__ celltab,
@@ -273,29 +273,46 @@ __global__ void __launch_bounds__(kScThreads) k_adj_g2p(Geom g, PBuf pre, const 
                 // x_bar = x_new_bar + sum_o grad w_o s_o - k4 c_bar^T v_raw
                 V3<float> xb = xnb - tmul(c_bar, vraw) * g.k4;
                 const float kd = g.k4 * g.dx;
-#pragma unroll 1
-                for (int ox = 0; ox < 3; ox++) {
-                    const float wox = ox == 0 ? sw.w[0][0] : (ox == 1 ? sw.w[0][1] : sw.w[0][2]);
-                    const float dox = ox == 0 ? sw.dw[0][0] : (ox == 1 ? sw.dw[0][1] : sw.dw[0][2]);
+                {
+                    // x_bar += sum_o grad w_o (gv_o . (v_raw_bar + k4 c_bar rel_o)), factored per axis:
+                    // k4 c_bar rel_o = ax[ox] + ay[oy] + az[oz]; the weight-gradient products are
+                    // accumulated per x-plane and scaled by dw_x / w_x once per plane.
+                    V3<float> ay[3], az[3];
 #pragma unroll
-                    for (int oy = 0; oy < 3; oy++) {
-#pragma unroll
-                        for (int oz = 0; oz < 3; oz++) {
-                            const float4 gv4 = vt[(sw.l[0] + ox) * 36 + (sw.l[1] + oy) * 6 + (sw.l[2] + oz)];
-                            const V3<float> gv = {gv4.x, gv4.y, gv4.z};
-                            const V3<float> rel = {(float(ox) - sw.fx[0]) * kd, (float(oy) - sw.fx[1]) * kd,
-                                                   (float(oz) - sw.fx[2]) * kd};
-                            // k4 * c_bar * rel_phys, rel_phys = dx (o - fx)
-                            const V3<float> cr = c_bar * rel;
-                            const float sv = dot(gv, vrb) + dot(gv, cr);
-                            const float gx = dox * sw.w[1][oy] * sw.w[2][oz];
-                            const float gy = wox * sw.dw[1][oy] * sw.w[2][oz];
-                            const float gz = wox * sw.w[1][oy] * sw.dw[2][oz];
-                            xb.x += gx * g.inv_dx * sv;
-                            xb.y += gy * g.inv_dx * sv;
-                            xb.z += gz * g.inv_dx * sv;
-                        }
+                    for (int o = 0; o < 3; o++) {
+                        const float ry = (float(o) - sw.fx[1]) * kd, rz = (float(o) - sw.fx[2]) * kd;
+                        ay[o] = V3<float>{c_bar.m[1] * ry, c_bar.m[4] * ry, c_bar.m[7] * ry};
+                        az[o] = V3<float>{c_bar.m[2] * rz, c_bar.m[5] * rz, c_bar.m[8] * rz};
                     }
+                    float sxx = 0.f, syy = 0.f, szz = 0.f;
+#pragma unroll 1
+                    for (int ox = 0; ox < 3; ox++) {
+                        const float wox = ox == 0 ? sw.w[0][0] : (ox == 1 ? sw.w[0][1] : sw.w[0][2]);
+                        const float dox = ox == 0 ? sw.dw[0][0] : (ox == 1 ? sw.dw[0][1] : sw.dw[0][2]);
+                        const float rx = (float(ox) - sw.fx[0]) * kd;
+                        const V3<float> ax = {vrb.x + c_bar.m[0] * rx, vrb.y + c_bar.m[3] * rx, vrb.z + c_bar.m[6] * rx};
+                        float px = 0.f, py = 0.f, pz = 0.f;
+                        const float4* row = vt + (sw.l[0] + ox) * 36 + sw.l[1] * 6 + sw.l[2];
+#pragma unroll
+                        for (int oy = 0; oy < 3; oy++) {
+                            const V3<float> axy = ax + ay[oy];
+#pragma unroll
+                            for (int oz = 0; oz < 3; oz++) {
+                                const float4 gv4 = row[oy * 6 + oz];
+                                const V3<float> u = axy + az[oz];
+                                const float sv = gv4.x * u.x + gv4.y * u.y + gv4.z * u.z;
+                                px += (sw.w[1][oy] * sw.w[2][oz]) * sv;
+                                py += (sw.dw[1][oy] * sw.w[2][oz]) * sv;
+                                pz += (sw.w[1][oy] * sw.dw[2][oz]) * sv;
+                            }
+                        }
+                        sxx += dox * px;
+                        syy += wox * py;
+                        szz += wox * pz;
+                    }
+                    xb.x += sxx * g.inv_dx;
+                    xb.y += syy * g.inv_dx;
+                    xb.z += szz * g.inv_dx;
                 }
                 if (HEAVY && ci.rigid >= 0) {
                     const int mr = rd.mrank[pre.id[s]];
@@ -367,7 +384,7 @@ __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __re
         if ((ddx && lx >= 2) || (ddy && ly >= 2) || (ddz && lz >= 2)) continue;
         const int px = bx - ddx, py = by - ddy, pz = bz - ddz;
         if (px < 0 || py < 0 || pz < 0) continue;
-        const int slot = blockmap[block_lin(g, px, py, pz)];
+        const int slot = blockmap[block_lin(g, px, py, pz)] - 1;  // map holds slot + 1
         if (slot < 0) continue;
         const float4 v = staging[size_t(slot) * kTile + (lx + 4 * ddx) * 36 + (ly + 4 * ddy) * 6 + (lz + 4 * ddz)];
         acc.x += v.x;
@@ -509,7 +526,7 @@ void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const i
 // P2G adjoint (adjoint.hpp:414-470)
 // ---------------------------------------------------------------------------
 template <bool HEAVY>
-__global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(128, HEAVY ? 3 : 5) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                  const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                                  const ClassInfo* __restrict__ cls,
                                                  const float4* __restrict__ gridbar,
@@ -561,33 +578,58 @@ __global__ void __launch_bounds__(128) k_adj_p2g(Geom g, PBuf pre, const uint32_
             V3<float> xb = {0.f, 0.f, 0.f}, vbsum = {0.f, 0.f, 0.f};
             M3<float> ab = mzero<float>();
             float wsum_p[3] = {0.f, 0.f, 0.f};
+            {
+                // contrib_o = mv + affine rel_o with rel_o = dx (o - fx) split per axis;
+                // grad-w products accumulated per x-plane; A_bar = sum_o w_o p_bar_o rel_o^T
+                // gathered column-wise (x column through the per-plane sum).
+                V3<float> ay[3], az[3];
+                float ry[3], rz[3];
 #pragma unroll
-            for (int ox = 0; ox < 3; ox++) {
-#pragma unroll
-                for (int oy = 0; oy < 3; oy++) {
-#pragma unroll
-                    for (int oz = 0; oz < 3; oz++) {
-                        const float4 b4 = bt[(sw.l[0] + ox) * 36 + (sw.l[1] + oy) * 6 + (sw.l[2] + oz)];
-                        const V3<float> ob = {b4.x, b4.y, b4.z};
-                        const float mbar = b4.w;
-                        const float w = sw.w[0][ox] * sw.w[1][oy] * sw.w[2][oz];
-                        const V3<float> rel = {(float(ox) - sw.fx[0]) * g.dx, (float(oy) - sw.fx[1]) * g.dx,
-                                               (float(oz) - sw.fx[2]) * g.dx};
-                        const V3<float> contrib = mv + affine * rel;
-                        const float sv = mbar * ci.mass + dot(ob, contrib);
-                        const float gx = sw.dw[0][ox] * sw.w[1][oy] * sw.w[2][oz];
-                        const float gy = sw.w[0][ox] * sw.dw[1][oy] * sw.w[2][oz];
-                        const float gz = sw.w[0][ox] * sw.w[1][oy] * sw.dw[2][oz];
-                        xb.x += gx * g.inv_dx * sv;
-                        xb.y += gy * g.inv_dx * sv;
-                        xb.z += gz * g.inv_dx * sv;
-                        const V3<float> wob = ob * w;
-                        wsum_p[0] += wob.x;
-                        wsum_p[1] += wob.y;
-                        wsum_p[2] += wob.z;
-                        ab += outer(wob, rel);
-                    }
+                for (int o = 0; o < 3; o++) {
+                    ry[o] = (float(o) - sw.fx[1]) * g.dx;
+                    rz[o] = (float(o) - sw.fx[2]) * g.dx;
+                    ay[o] = V3<float>{affine.m[1] * ry[o], affine.m[4] * ry[o], affine.m[7] * ry[o]};
+                    az[o] = V3<float>{affine.m[2] * rz[o], affine.m[5] * rz[o], affine.m[8] * rz[o]};
                 }
+                const float mm = ci.mass;
+                float sxx = 0.f, syy = 0.f, szz = 0.f;
+#pragma unroll 1
+                for (int ox = 0; ox < 3; ox++) {
+                    const float wox = ox == 0 ? sw.w[0][0] : (ox == 1 ? sw.w[0][1] : sw.w[0][2]);
+                    const float dox = ox == 0 ? sw.dw[0][0] : (ox == 1 ? sw.dw[0][1] : sw.dw[0][2]);
+                    const float rx = (float(ox) - sw.fx[0]) * g.dx;
+                    const V3<float> ax = {mv.x + affine.m[0] * rx, mv.y + affine.m[3] * rx, mv.z + affine.m[6] * rx};
+                    float px = 0.f, py = 0.f, pz = 0.f;
+                    V3<float> tx = {0.f, 0.f, 0.f};
+                    const float4* row = bt + (sw.l[0] + ox) * 36 + sw.l[1] * 6 + sw.l[2];
+#pragma unroll
+                    for (int oy = 0; oy < 3; oy++) {
+                        const V3<float> axy = ax + ay[oy];
+#pragma unroll
+                        for (int oz = 0; oz < 3; oz++) {
+                            const float4 b4 = row[oy * 6 + oz];
+                            const V3<float> u = axy + az[oz];
+                            const float sv = b4.w * mm + b4.x * u.x + b4.y * u.y + b4.z * u.z;
+                            const float wyz = sw.w[1][oy] * sw.w[2][oz];
+                            px += wyz * sv;
+                            py += (sw.dw[1][oy] * sw.w[2][oz]) * sv;
+                            pz += (sw.w[1][oy] * sw.dw[2][oz]) * sv;
+                            const float w = wox * wyz;
+                            const V3<float> wob = {b4.x * w, b4.y * w, b4.z * w};
+                            tx += wob;
+                            ab.m[1] += wob.x * ry[oy]; ab.m[4] += wob.y * ry[oy]; ab.m[7] += wob.z * ry[oy];
+                            ab.m[2] += wob.x * rz[oz]; ab.m[5] += wob.y * rz[oz]; ab.m[8] += wob.z * rz[oz];
+                        }
+                    }
+                    sxx += dox * px;
+                    syy += wox * py;
+                    szz += wox * pz;
+                    ab.m[0] += tx.x * rx; ab.m[3] += tx.y * rx; ab.m[6] += tx.z * rx;
+                    wsum_p[0] += tx.x;
+                    wsum_p[1] += tx.y;
+                    wsum_p[2] += tx.z;
+                }
+                xb = V3<float>{sxx * g.inv_dx, syy * g.inv_dx, szz * g.inv_dx};
             }
             const V3<float> wp = {wsum_p[0], wsum_p[1], wsum_p[2]};
             xb -= tmul(affine, wp);

@@ -300,12 +300,12 @@ struct Ctx {
 
     // scratch
     DevArr<int> bzero, bstart;  // bzero = [bcount | bheavy | bfill], zeroed per sort
-    int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr;
+    int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr, *blockmap_p = nullptr,
+        *list_cnt = nullptr;
     DevArr<int> nbpos;
     DevArr<uint32_t> skey, sslot, gk, gv;
     DevArr<unsigned char> cub_tmp;
     size_t cub_bytes = 0;
-    DevArr<int> blockmap;
     DevArr<float4> staging, staging_bar, gridbar;
     DevArr<unsigned long long> d_err;
     DevArr<int> d_nonfinite;
@@ -538,18 +538,21 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
 
     // scratch
     if (N >= (1 << 26)) throw FlumeError(FLUME_E_ARG, "at most 2^26-1 particles per context");
-    bzero.alloc(4 * size_t(g.nbtot + 1));
+    // one zero-memset per sort covers counts, heavy flags, fill cursors, node-block
+    // flags, the block map (slot + 1, 0 = none) and the list counters
+    bzero.alloc(5 * size_t(g.nbtot + 1) + 8);
     bcount = bzero.p;
     bheavy = bzero.p + (g.nbtot + 1);
     bfill = bzero.p + 2 * (g.nbtot + 1);
     nbflag = bzero.p + 3 * (g.nbtot + 1);
+    blockmap_p = bzero.p + 4 * (g.nbtot + 1);
+    list_cnt = bzero.p + 5 * (g.nbtot + 1);
     nbpos.alloc(g.nbtot);
     bstart.alloc(g.nbtot + 1);
     skey.alloc(N);
     sslot.alloc(N);
     gk.alloc(2 * size_t(N) + 2);
     gv.alloc(2 * size_t(N) + 2);
-    blockmap.alloc(g.nbtot);
     staging.alloc(size_t(maxb) * kTile);
     staging_bar.alloc(size_t(maxb) * kTile);
     gridbar.alloc(size_t(g.nbtot) * 64);
@@ -758,14 +761,12 @@ void Ctx::download(flume_state_view* view) {
 void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     Geom& g = geom;
     CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
-    CK(cudaMemsetAsync(r.n_blocks, 0, 2 * sizeof(int), stream));
-    CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
     launch_sort_count(g, st.p, N, d_cls.p, bcount, bheavy, stream);
     CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, bcount, bstart.p, g.nbtot + 1, stream));
-    launch_sort_scatter(g, st.p, N, bstart.p, bcount, bheavy, bfill, skey.p, sslot.p, r.recs, r.n_blocks, blockmap.p,
+    launch_sort_scatter(g, st.p, N, bstart.p, bcount, bheavy, bfill, skey.p, sslot.p, r.recs, list_cnt, blockmap_p,
                         nbflag, maxb, stream);
     CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, g.nbtot, stream));
-    launch_nb_scatter(nbflag, nbpos.p, g.nbtot, r.nb_list, r.n_nb, stream);
+    launch_nb_scatter(nbflag, nbpos.p, g.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
     launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
                        grid_sort, stream);
     launches += 4;
@@ -831,7 +832,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
          }));
-    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, r.gridv, r.gridv0,
+    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0,
                                     r.effk, stream));
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
@@ -874,17 +875,17 @@ void Ctx::stage_grid(double* mass, double* vel) {
         launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
                    staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
     });
-    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap.p, staging.p, r.gridv, r.gridv0, es, stream);
+    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0, es, stream);
     std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
     CK(cudaMemcpyAsync(h.data(), r.gridv, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(bm.data(), blockmap.p, bm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(bm.data(), blockmap_p, bm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     check_error();
     // node blocks the grid update wrote (the rest of the dense array is stale)
     std::vector<char> touched(geom.nbtot, 0);
     for (int b = 0; b < geom.nbtot; b++) {
-        if (bm[b] < 0) continue;
+        if (bm[b] <= 0) continue;
         int bx, by, bz;
         block_unlin(geom, b, bx, by, bz);
         for (int d = 0; d < 8; d++) {
@@ -1005,8 +1006,8 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
     BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
     // the forward recorded this substep's grid (r.gridv, r.gridv0); only the
     // particle-block map is rebuilt for the staging gathers
-    CK(cudaMemsetAsync(blockmap.p, 0xff, size_t(g.nbtot) * sizeof(int), stream));
-    launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap.p, stream);
+    CK(cudaMemsetAsync(blockmap_p, 0, size_t(g.nbtot) * sizeof(int), stream));
+    launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap_p, stream);
     launches += 1;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
@@ -1018,7 +1019,7 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
                             r.gridv, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
          }));
-    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap.p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
+    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap_p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
                                      eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,

@@ -126,7 +126,7 @@ __global__ void k_blockmap_set(const BlockRec* recs, const int* n_blocks, int ma
     const int nl = n_blocks[0], nh = n_blocks[1];
     if (w >= nl + nh) return;
     const int q = w < nl ? w : max_blocks - 1 - (w - nl);
-    blockmap[recs[q].block] = q;
+    blockmap[recs[q].block] = q + 1;
 }
 
 void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap,
@@ -286,7 +286,7 @@ __device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __res
         if ((ddx && lx >= 2) || (ddy && ly >= 2) || (ddz && lz >= 2)) continue;
         const int px = bx - ddx, py = by - ddy, pz = bz - ddz;
         if (px < 0 || py < 0 || pz < 0) continue;
-        const int slot = blockmap[block_lin(g, px, py, pz)];
+        const int slot = blockmap[block_lin(g, px, py, pz)] - 1;  // map holds slot + 1
         if (slot < 0) continue;
         const int t = (lx + 4 * ddx) * 36 + (ly + 4 * ddy) * 6 + (lz + 4 * ddz);
         const float4 v = staging[size_t(slot) * kTile + t];
@@ -337,7 +337,7 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 // ---------------------------------------------------------------------------
 
 template <bool HEAVY>
-__global__ void __launch_bounds__(128) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(128, HEAVY ? 4 : 8) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
                                              RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {

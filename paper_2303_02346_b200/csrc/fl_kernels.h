@@ -114,7 +114,8 @@ void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cl
 void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, const int* bcount,
                          const int* bheavy, int* bfill, uint32_t* skey, uint32_t* sslot, BlockRec* recs, int* n_blocks,
                          int* blockmap, int* nbflag, int cap, cudaStream_t s);
-void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s);
+void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, const int* cnt_scratch,
+                       int* n_blocks, cudaStream_t s);
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s);

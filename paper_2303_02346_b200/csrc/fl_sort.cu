@@ -60,7 +60,7 @@ __global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ b
             const bool hv = bheavy[b] != 0;
             const int q = hv ? cap - 1 - atomicAdd(&n_blocks[1], 1) : atomicAdd(&n_blocks[0], 1);
             recs[q] = BlockRec{b, bstart[b], bstart[b] + bcount[b]};
-            blockmap[b] = q;
+            blockmap[b] = q + 1;
             int bx, by, bz;  // node blocks covered by this block's tile
             block_unlin(g, b, bx, by, bz);
             for (int d = 0; d < 8; d++) {
@@ -221,16 +221,23 @@ void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart
 }
 
 // compact, id-ordered list of touched node blocks
+// compact, id-ordered list of touched node blocks; also publishes the
+// particle-block list counters (scratch -> record)
 __global__ void k_nb_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* list,
-                             int* n_list) {
+                             int* n_list, const int* __restrict__ cnt_scratch, int* n_blocks) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        n_blocks[0] = cnt_scratch[0];
+        n_blocks[1] = cnt_scratch[1];
+    }
     if (i >= n) return;
     if (flags[i]) list[pos[i]] = i;
     if (i == n - 1) *n_list = pos[i] + (flags[i] ? 1 : 0);
 }
 
-void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, cudaStream_t s) {
-    k_nb_scatter<<<(nbtot + 255) / 256, 256, 0, s>>>(flags, pos, nbtot, list, n_list);
+void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, const int* cnt_scratch,
+                       int* n_blocks, cudaStream_t s) {
+    k_nb_scatter<<<(nbtot + 255) / 256, 256, 0, s>>>(flags, pos, nbtot, list, n_list, cnt_scratch, n_blocks);
 }
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
