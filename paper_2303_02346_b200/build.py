@@ -82,6 +82,7 @@ def build_oracle() -> None:
     if not Path("/root/reference/proj/include").exists():
         return
     _run(["make", "-s", "-C", str(ROOT / "oracle")])
+    _run(["make", "-s", "-C", str(ROOT / "tests" / "cpp")])
 
 
 if __name__ == "__main__":
