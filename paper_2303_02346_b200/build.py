@@ -47,19 +47,23 @@ def _run(cmd):
     return r
 
 
-def build_library(verbose: bool = False) -> Path:
-    OBJ.mkdir(exist_ok=True)
+def build_library(verbose: bool = False, defines=(), tag: str = "") -> Path:
+    """defines/tag: A/B variants (tools/ab.py) go to _ab/<tag>/libflume_b200.so (travels to the GPU box)."""
+    obj = PKG / "_ab" / tag if tag else OBJ
+    lib = obj / "libflume_b200.so" if tag else LIB
+    obj.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     hdrs = _headers()
     jobs = []
     objs = []
     for s in CU_SRCS:
-        o = OBJ / (s + ".o")
+        o = obj / (s + ".o")
         objs.append(o)
         if _stale(o, [CSRC / s] + hdrs):
-            jobs.append([NVCC, "-std=c++17", *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
+            jobs.append([NVCC, "-std=c++17", *ARCH, *dflags, "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
                          "-c", str(CSRC / s), "-o", str(o)])
     for s in CPP_SRCS:
-        o = OBJ / (s + ".o")
+        o = obj / (s + ".o")
         objs.append(o)
         if _stale(o, [CSRC / s] + hdrs):
             jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", f"-I{JSON_INC}",
@@ -69,9 +73,9 @@ def build_library(verbose: bool = False) -> Path:
             for r in ex.map(_run, jobs):
                 if verbose:
                     sys.stdout.write(r.stdout + r.stderr)
-    if jobs or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)])
-    return LIB
+    if jobs or _stale(lib, objs):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)])
+    return lib
 
 
 def build_oracle() -> None:

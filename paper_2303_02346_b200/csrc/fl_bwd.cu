@@ -25,7 +25,7 @@ __global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, L
                             uint32_t key_inactive, BarBuf bars) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int body = cls[st.meta[i]].body;
+    const int body = cls[meta_cls(st.meta[i])].body;
     const bool active = st.key[i] != key_inactive;
     double g[3] = {0.0, 0.0, 0.0};
     bool any = false;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : 3) k_adj_g2p(Geom g, P
                                                         const int* __restrict__ n_blocks,
                                                         const uint16_t* __restrict__ celltab,
                                                         const ClassInfo* __restrict__ cls,
-                                                        const float4* __restrict__ gridv, BarBuf post,
+                                                        const float4* __restrict__ gridv, PBuf postst, BarBuf post,
                                                         float* xbar_tmp, float* Fbar_tmp, RigidDev rd,
                                                         const float* __restrict__ start_bar, float4* staging_bar,
                                                         int cap, int* wq) {
@@ -210,20 +210,36 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : 3) k_adj_g2p(Geom g, P
             for (int i = tid; i < cnt; i += kScThreads) {
                 const int j = r.start + i;
                 const uint32_t s = perm[j];
-                const int c = int(pre.key[s] & 63);
+                const int c = cell_of(sm.cs, i);
                 const int rank = i - int(sm.cs[c]) - r0;
                 if (rank < 0 || rank >= kScR) continue;
                 float* pay = pay_slot(sm, rank, c);
                 const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
-                const ClassInfo ci = cls[pre.meta[s]];
+                const ClassInfo ci = cls[meta_cls(pre.meta[s])];
                 StencilW sw;
                 stencil_weights(g, x, bx, by, bz, sw);
-                V3<float> vraw;
+                V3<float> vraw, vuse;
                 M3<float> cnew;
-                g2p_gather(g, vt, sw, vraw, cnew);
-                const float vn = norm(vraw);
-                const bool clamped_v = vn > g.vmax;
-                const V3<float> vuse = clamped_v ? vraw * (g.vmax / vn) : vraw;
+                bool clamped_v;
+                if constexpr (HEAVY) {
+                    g2p_gather(g, vt, sw, vraw, cnew);
+                    const float vn = norm(vraw);
+                    clamped_v = vn > g.vmax;
+                    vuse = clamped_v ? vraw * (g.vmax / vn) : vraw;
+                } else {
+                    // plain liquids: the forward stored C_new and the (clamped) velocity
+                    // in the post-state at this sorted position; re-gather only when the
+                    // CFL clamp fired (v_raw is then not recoverable)
+                    clamped_v = (postst.meta[j] & kMetaCfl) != 0u;
+#pragma unroll
+                    for (int k = 0; k < 9; k++) cnew.m[k] = postst.C(k)[j];
+                    vuse = V3<float>{postst.v(0)[j], postst.v(1)[j], postst.v(2)[j]};
+                    vraw = vuse;
+                    if (clamped_v) {
+                        M3<float> cdummy;
+                        g2p_gather(g, vt, sw, vraw, cdummy);
+                    }
+                }
                 M3<float> F;
 #pragma unroll
                 for (int k = 0; k < 9; k++) F.m[k] = pre.F(k)[s];
@@ -349,9 +365,9 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : 3) k_adj_g2p(Geom g, P
 }
 
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
-                    const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, BarBuf post,
-                    float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar,
-                    bool heavy, int* wq, cudaStream_t s) {
+                    const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, PBuf postst,
+                    BarBuf post, float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar,
+                    float4* staging_bar, bool heavy, int* wq, cudaStream_t s) {
     const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
     static bool attr = false;
     if (!attr) {
@@ -360,10 +376,10 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
         attr = true;
     }
     if (heavy)
-        k_adj_g2p<true><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, post,
+        k_adj_g2p<true><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
                                                        xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
     else
-        k_adj_g2p<false><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, post,
+        k_adj_g2p<false><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
                                                         xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
 }
 
@@ -550,7 +566,7 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : 5) k_adj_p2g(Geom g, PBuf pre
             const uint32_t s = perm[j];
             const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
             const V3<float> v = {pre.v(0)[s], pre.v(1)[s], pre.v(2)[s]};
-            const ClassInfo ci = cls[pre.meta[s]];
+            const ClassInfo ci = cls[meta_cls(pre.meta[s])];
             M3<float> F, C;
 #pragma unroll
             for (int k = 0; k < 9; k++) {

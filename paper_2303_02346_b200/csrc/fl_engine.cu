@@ -389,7 +389,8 @@ struct Ctx {
     uint32_t loss_mask(const flume_loss_desc* loss, int seg, int nseg) const;
     void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, long substep);
     double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg);
-    void adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre, int t_slot);
+    void adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre,
+                      int t_slot);
     void grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
                          double* grad, double* loss_out, double* full_loss, double* per_seg, long* snapshots);
     void adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* eb,
@@ -1001,7 +1002,8 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
 }
 
 // reverse one substep: bars_post (store order of state[t+1]) -> bars_pre (store order of state[t])
-void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre, int t_slot) {
+void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre,
+                       int t_slot) {
     Geom& g = geom;
     BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
     // the forward recorded this substep's grid (r.gridv, r.gridv0); only the
@@ -1017,7 +1019,7 @@ void Ctx::adjoint_step(StateBuf& pre, Record& r, DevArr<float>& bars_post, DevAr
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
-                            r.gridv, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
+                            r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
          }));
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap_p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
                                      eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
@@ -1185,7 +1187,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         }
         ensure_cached(t);
         const size_t k = size_t(t - cache_base);
-        adjoint_step(*cache_states[k], *cache_recs[k], barsA, barsB, int(t));
+        adjoint_step(*cache_states[k], *cache_states[k + 1], *cache_recs[k], barsA, barsB, int(t));
         std::swap(barsA.p, barsB.p);
         std::swap(barsA.n, barsB.n);
     }
@@ -1286,7 +1288,7 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     barsA.alloc(size_t(N) * 24);
     barsB.alloc(size_t(N) * 24);
     launch_bars_from_ref(BarBuf{barsA.p, N}, post->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
-    adjoint_step(*pre, *rec, barsA, barsB, 0);
+    adjoint_step(*pre, *post, *rec, barsA, barsB, 0);
     launch_bars_to_ref(BarBuf{barsB.p, N}, pre->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
     CK(cudaMemcpyAsync(xb, d_up[0].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(vb, d_up[1].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));

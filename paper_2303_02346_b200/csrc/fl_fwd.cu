@@ -190,9 +190,8 @@ __global__ void __launch_bounds__(kScThreads) k_p2g(Geom g, PBuf st, const uint3
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
             for (int i = tid; i < cnt; i += kScThreads) {
+                const int c = cell_of(sm.cs, i);
                 const uint32_t s = perm[r.start + i];
-                const uint32_t key = st.key[s];
-                const int c = int(key & 63);
                 const int rank = i - int(sm.cs[c]) - r0;
                 if (rank < 0 || rank >= kScR) continue;
                 float* pay = pay_slot(sm, rank, c);
@@ -211,7 +210,7 @@ __global__ void __launch_bounds__(kScThreads) k_p2g(Geom g, PBuf st, const uint3
                     pay[0] = pay[kPayPlane] = pay[2 * kPayPlane] = 1.f;
                     continue;
                 }
-                const ClassInfo ci = cls[st.meta[s]];
+                const ClassInfo ci = cls[meta_cls(st.meta[s])];
                 M3<float> F, C;
 #pragma unroll
                 for (int k = 0; k < 9; k++) {
@@ -359,7 +358,7 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : 8) k_g2p(Geom g, PBuf in, PBu
             const V3<float> x = {in.x(0)[s], in.x(1)[s], in.x(2)[s]};
             const uint32_t meta = in.meta[s];
             const uint32_t pid = in.id[s];
-            const ClassInfo ci = cls[meta];
+            const ClassInfo ci = cls[meta_cls(meta)];
             StencilW sw;
             stencil_weights(g, x, bx, by, bz, sw);
             V3<float> vraw;
@@ -399,7 +398,7 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : 8) k_g2p(Geom g, PBuf in, PBu
                 out.F(k)[j] = fnew.m[k];
                 out.C(k)[j] = cnew.m[k];
             }
-            out.meta[j] = meta;
+            out.meta[j] = meta_cls(meta) | (vn > g.vmax ? kMetaCfl : 0u);
             out.id[j] = pid;
             uint32_t key;
             cell_key(g, xn.x, xn.y, xn.z, key);
@@ -567,7 +566,7 @@ __global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const Clas
     double acc[kMaxLossTerms];
     for (int k = 0; k < kMaxLossTerms; k++) acc[k] = 0.0;
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-        const int body = cls[st.meta[i]].body;
+        const int body = cls[meta_cls(st.meta[i])].body;
         const bool active = st.key[i] != key_inactive;
         for (int k = 0; k < ls.n; k++) {
             if (!((mask >> k) & 1u) || ls.t[k].body != body) continue;

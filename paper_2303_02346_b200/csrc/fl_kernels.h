@@ -93,9 +93,9 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
                       const int* chunk_m0, const int* chunk_m1, double* partial, float* start_bar,
                       double* abar, cudaStream_t s);
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
-                    const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, BarBuf post, float* xbar_tmp,
-                    float* Fbar_tmp, RigidDev rd, const float* start_bar, float4* staging_bar, bool heavy, int* wq,
-                    cudaStream_t s);
+                    const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, PBuf postst,
+                    BarBuf post, float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar,
+                    float4* staging_bar, bool heavy, int* wq, cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                      double* eff_partial, double* eff_out, cudaStream_t s);

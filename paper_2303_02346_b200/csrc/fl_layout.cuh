@@ -41,6 +41,11 @@ struct Geom {
     float stress_coeff;  // dt * 4 / dx^2 (mpm.hpp:259)
 };
 
+// class word of a particle: class index, plus bit 31 set by G2P when the CFL
+// clamp (mpm.hpp:322-328) was active in the substep that produced the state
+constexpr uint32_t kMetaCfl = 0x80000000u;
+__host__ __device__ inline uint32_t meta_cls(uint32_t m) { return m & 0x7fffffffu; }
+
 // one entry per distinct (material, body, mass, volume0) tuple
 struct ClassInfo {
     int kind;

@@ -35,13 +35,25 @@ struct alignas(16) ScSmem {
 __device__ __forceinline__ float* pay_slot(ScSmem& sm, int rank, int cell) { return &sm.pay[rank * kCS + cell]; }
 constexpr int kPayPlane = kScR * kCS;  // floats between payload fields
 
-// dynamic block scheduling: a CTA grabs the next list slot from a work counter
-// (results do not depend on which CTA processes which block)
+// Dynamic block scheduling: a CTA grabs the next list slot from a work counter
+// (results do not depend on which CTA processes which block).  Claiming a slot
+// one block ahead was measured slower: with a few blocks per CTA the tail
+// imbalance it adds outweighs the hidden atomic latency.
 __device__ __forceinline__ int next_work(int* counter, int* sh) {
     __syncthreads();
     if (threadIdx.x == 0) *sh = atomicAdd(counter, 1);
     __syncthreads();
     return *sh;
+}
+
+// local cell (0..63) of the i-th particle of a block from its cell-start table
+// (largest c with cs[c] <= i; empty cells have cs[c] == cs[c+1])
+__device__ __forceinline__ int cell_of(const uint16_t* cs, int i) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)
+        if (int(cs[lo + step]) <= i) lo += step;
+    return lo;
 }
 
 __device__ __forceinline__ void sc_tile_zero(ScSmem& sm, int tid, int nthreads) {
