@@ -200,6 +200,23 @@ int flume_get_stream(flume_ctx* ctx, void** cuda_stream);
 int flume_sync(flume_ctx* ctx);
 int flume_last_timing(const flume_ctx* ctx, flume_timing* out);
 
+/* ---- x-slab decomposition over several ranks ----
+ * Rank r owns the 4-cell columns [sx0, sx1) along x (split by particle count at
+ * upload); neighbours exchange two halo planes per scatter and migrating
+ * particles, everything else is all-reduced.  Every call on a rank context is
+ * collective: all ranks make the same calls in the same order, concurrently.
+ * The results equal one rank's: particle states bit-identical, losses and
+ * action gradients up to the order of their final sums.
+ *   flume_group_create     n contexts in this process (one host thread per rank;
+ *                          ranks may share a device), peer copies over NVLink
+ *   flume_ctx_create_dist  one context per process (torchrun), NCCL; all ranks
+ *                          pass the id rank 0 got from flume_dist_unique_id */
+int flume_group_create(const flume_scene_desc* desc, int n_ranks, const int* devices, flume_ctx** out_ctxs);
+int flume_dist_unique_id(unsigned char uid[128]);
+int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, int n_ranks,
+                          const unsigned char uid[128], flume_ctx** out);
+int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int* sx1, long* n_active);
+
 /* ---- instrumentation ----
  * flume_profile: time every kernel class with CUDA events on the context stream.
  * kernel classes: 0 p2g, 1 grid_update, 2 g2p, 3 sort+block lists, 4 g2p adjoint,

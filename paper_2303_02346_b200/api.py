@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json as _json
+import threading
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -393,25 +394,81 @@ class SubstepRecord:
 
 
 class GpuWorkspace:
-    """Device context for one scene (MpmWorkspace analogue, mpm.hpp:223-238)."""
+    """Device context for one scene (MpmWorkspace analogue, mpm.hpp:223-238).
 
-    def __init__(self, scene: Scene, device: int = 0):
+    ranks > 1: x-slab decomposition over `ranks` contexts in this process
+    (SURVEY.md 8(e)); `devices` lists one CUDA device per rank (default: all on
+    `device`).  Every call runs on all ranks concurrently, one thread each.
+    """
+
+    def __init__(self, scene: Scene, device: int = 0, ranks: int = 1, devices: Optional[Sequence[int]] = None):
         self.lib = load()
         self.scene = scene
         self.ctx = C.c_void_p()
-        rc = self.lib.flume_ctx_create(C.byref(scene.desc), device, C.byref(self.ctx))
-        if rc != _abi.FLUME_OK:
-            _raise(self.lib, None, rc)
+        if ranks == 1 and devices is None:
+            rc = self.lib.flume_ctx_create(C.byref(scene.desc), device, C.byref(self.ctx))
+            if rc != _abi.FLUME_OK:
+                _raise(self.lib, None, rc)
+            self.ctxs = [self.ctx]
+        else:
+            devs = list(devices) if devices is not None else [device] * ranks
+            arr = (C.c_void_p * len(devs))()
+            rc = self.lib.flume_group_create(C.byref(scene.desc), len(devs), (C.c_int * len(devs))(*devs), arr)
+            if rc != _abi.FLUME_OK:
+                _raise(self.lib, None, rc)
+            self.ctxs = [C.c_void_p(arr[i]) for i in range(len(devs))]
+            self.ctx = self.ctxs[0]
         self._resident: Optional[SimState] = None
         self._ctx_time = 0.0
         self._ctx_substep = 0
+
+    @property
+    def ranks(self) -> int:
+        return len(self.ctxs)
+
+    def slab_info(self):
+        """[(rank, sx0, sx1, n_active)] -- the x-columns of 4 cells each rank owns."""
+        out = []
+        for c in self.ctxs:
+            r, n, a, b, na = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_long()
+            self.lib.flume_slab_info(c, C.byref(r), C.byref(n), C.byref(a), C.byref(b), C.byref(na))
+            out.append((r.value, a.value, b.value, na.value))
+        return out
+
+    def _collective(self, fn):
+        """fn(rank, ctx) -> status, on every rank concurrently (ctypes drops the GIL)."""
+        if len(self.ctxs) == 1:
+            self._check(fn(0, self.ctx))
+            return
+        rcs = [None] * len(self.ctxs)
+
+        def run(i):
+            rcs[i] = fn(i, self.ctxs[i])
+
+        th = [threading.Thread(target=run, args=(i,)) for i in range(len(self.ctxs))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        bad = [i for i, rc in enumerate(rcs) if rc != _abi.FLUME_OK]
+        if not bad:
+            return
+        # report the rank that failed first, not the peers it released
+        for i in bad:
+            info = _abi.ErrorInfo()
+            self.lib.flume_last_error(self.ctxs[i], C.byref(info))
+            if b"aborted by a failing rank" not in info.message:
+                _raise(self.lib, self.ctxs[i], rcs[i])
+        _raise(self.lib, self.ctxs[bad[0]], rcs[bad[0]])
 
     def close(self):
         if self.ctx:
             if self._resident is not None:
                 self._resident._pull()
-            self.lib.flume_ctx_destroy(self.ctx)
+            for c in self.ctxs:
+                self.lib.flume_ctx_destroy(c)
             self.ctx = C.c_void_p()
+            self.ctxs = []
 
     def __del__(self):
         try:
@@ -447,7 +504,8 @@ class GpuWorkspace:
             self._resident._pull()
         st._pull()
         effs = self._eff_to_c(st._eff)
-        self._check(self.lib.flume_state_upload(self.ctx, C.byref(self._view(st, effs))))
+        view = self._view(st, effs)
+        self._collective(lambda r, c: self.lib.flume_state_upload(c, C.byref(view)))
         self._resident = st
         self._ctx_time = st._time
         self._ctx_substep = st._substep
@@ -455,7 +513,15 @@ class GpuWorkspace:
     def _download(self, st: SimState):
         effs = (_abi.EffectorState * max(len(st._eff), 1))()
         v = self._view(st, effs)
-        self._check(self.lib.flume_state_download(self.ctx, C.byref(v)))
+        views, keep = [v], []
+        for _ in range(1, len(self.ctxs)):  # every rank assembles the whole state; keep rank 0's
+            sc = SimState.__new__(SimState)
+            sc._time, sc._substep = st._time, st._substep
+            sc._x, sc._v, sc._F, sc._C = (np.empty_like(a) for a in (st._x, st._v, st._F, st._C))
+            e = (_abi.EffectorState * max(len(st._eff), 1))()
+            keep.append((sc, e))
+            views.append(self._view(sc, e))
+        self._collective(lambda r, c: self.lib.flume_state_download(c, C.byref(views[r])))
         for i in range(len(st._eff)):
             e = effs[i]
             st._eff[i] = list(e.pose_t) + list(e.pose_R) + list(e.linear_velocity) + list(e.angular_velocity)
@@ -503,7 +569,7 @@ def mpm_substep(scene: Scene, state: SimState, action, ws: GpuWorkspace, count: 
     ws = _ws_for(scene, ws)
     ws._upload(state)
     a = np.ascontiguousarray(action, dtype=np.float64)
-    ws._check(ws.lib.flume_substep(ws.ctx, _dp(a), int(count)))
+    ws._collective(lambda r, c: ws.lib.flume_substep(c, _dp(a), int(count)))
     ws._ctx_time = state._time + count * scene.dt_substep
     ws._ctx_substep = state._substep + count
     state._time, state._substep = ws._ctx_time, ws._ctx_substep
@@ -517,7 +583,8 @@ def p2g_grid(scene: Scene, state: SimState, ws: GpuWorkspace):
     nd = scene.node_dims
     mass = np.zeros(nd)
     vel = np.zeros(nd + (3,))
-    ws._check(ws.lib.flume_stage_grid(ws.ctx, _dp(mass), _dp(vel)))
+    # slab ranks write disjoint node planes of the same arrays
+    ws._collective(lambda r, c: ws.lib.flume_stage_grid(c, _dp(mass), _dp(vel)))
     return mass, vel
 
 
@@ -526,11 +593,12 @@ def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss
     """grad.hpp:15-41."""
     ws = _ws_for(scene, ws)
     ws._upload(state0)
-    out = C.c_double()
-    per = np.zeros(actions.n_segments)
+    outs = [C.c_double() for _ in ws.ctxs]
+    pers = [np.zeros(actions.n_segments) for _ in ws.ctxs]
     a = actions._c()
-    ws._check(ws.lib.flume_rollout_loss(ws.ctx, C.byref(a), C.byref(loss.desc), int(window), C.byref(out),
-                                        _dp(per)))
+    ws._collective(lambda r, c: ws.lib.flume_rollout_loss(c, C.byref(a), C.byref(loss.desc), int(window),
+                                                          C.byref(outs[r]), _dp(pers[r])))
+    out, per = outs[0], pers[0]
     if per_segment is not None:
         per_segment[:] = per.tolist()
     return out.value
@@ -541,12 +609,16 @@ def grad_trajectory(scene: Scene, state0: SimState, actions: ActionTrajectory, l
     """grad.hpp:61-134 (checkpoint stride semantics of checkpoint.hpp:11-50)."""
     ws = _ws_for(scene, ws)
     ws._upload(state0)
-    g = np.zeros((actions.n_segments, 6))
-    lo, fl, snaps = C.c_double(), C.c_double(), C.c_long()
-    per = np.zeros(actions.n_segments)
+    R = len(ws.ctxs)
+    gs = [np.zeros((actions.n_segments, 6)) for _ in range(R)]
+    res = [(C.c_double(), C.c_double(), C.c_long()) for _ in range(R)]
+    pers = [np.zeros(actions.n_segments) for _ in range(R)]
     a = actions._c()
-    ws._check(ws.lib.flume_grad_trajectory(ws.ctx, C.byref(a), C.byref(loss.desc), int(stride), int(window), _dp(g),
-                                           C.byref(lo), C.byref(fl), _dp(per), C.byref(snaps)))
+    ws._collective(lambda r, c: ws.lib.flume_grad_trajectory(c, C.byref(a), C.byref(loss.desc), int(stride),
+                                                             int(window), _dp(gs[r]), C.byref(res[r][0]),
+                                                             C.byref(res[r][1]), _dp(pers[r]), C.byref(res[r][2])))
+    g, per = gs[0], pers[0]
+    lo, fl, snaps = res[0]
     t = ws.last_timing()
     return TrajectoryGrad(lo.value, fl.value, per.tolist(), g, snaps.value, t.forward_ms, t.backward_ms)
 

@@ -25,8 +25,10 @@ __global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, L
                             uint32_t key_inactive, BarBuf bars) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const uint32_t key = st.key[i];
+    if (key > key_inactive) return;  // departed slot
     const int body = cls[meta_cls(st.meta[i])].body;
-    const bool active = st.key[i] != key_inactive;
+    const bool active = key < key_inactive;
     double g[3] = {0.0, 0.0, 0.0};
     bool any = false;
     for (int k = 0; k < ls.n; k++) {
@@ -64,8 +66,28 @@ void launch_loss_grad(const PBuf& st, int n, const ClassInfo* cls, const LossSet
 // ---------------------------------------------------------------------------
 constexpr int kAdjRigidQ = 12;  // r_bar[9], c_bar[3]
 
-__global__ void __launch_bounds__(256) k_adj_rigid_partial(Geom g, BarBuf post, RigidDev rd, const int* chunk_m0,
-                                                           const int* chunk_m1, double* partial, float* start_bar) {
+// member cotangents (x_bar, v_bar of the post-rigid state) by member rank; with
+// slabs every rank contributes its own members and the array is all-reduced
+// (disjoint support: the sum is exact), so every rank solves identical fits
+__global__ void k_adj_rigid_gather(BarBuf post, RigidDev rd, double* mbar) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rd.nmem) return;
+    const int body = rd.member_body[r];
+    const int j = rd.mslot[r];
+    double* o = mbar + 6 * size_t(r);
+    for (int q = 0; q < 6; q++) o[q] = 0.0;
+    if (rd.fit[24 * size_t(body) + 22] != 0.0 || j < 0) return;
+    for (int a = 0; a < 3; a++) {
+        o[a] = post.x(a)[j];
+        o[3 + a] = post.v(a)[j];
+        post.x(a)[j] = 0.f;
+        post.v(a)[j] = 0.f;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_adj_rigid_partial(Geom g, const double* mbar, RigidDev rd,
+                                                           const int* chunk_m0, const int* chunk_m1,
+                                                           double* partial, float* start_bar) {
     __shared__ double red[256];
     const int c = blockIdx.x;
     const int m0 = chunk_m0[c], m1 = chunk_m1[c];
@@ -78,15 +100,12 @@ __global__ void __launch_bounds__(256) k_adj_rigid_partial(Geom g, BarBuf post, 
             for (int a = 0; a < 3; a++) start_bar[3 * r + a] = 0.f;
             continue;
         }
-        const int j = rd.mslot[r];
         const double inv_dt = 1.0 / double(g.dt);
         double xn_bar[3];
         for (int a = 0; a < 3; a++) {
-            const double xb = post.x(a)[j], vb = post.v(a)[j];
+            const double xb = mbar[6 * size_t(r) + a], vb = mbar[6 * size_t(r) + 3 + a];
             xn_bar[a] = xb + vb * inv_dt;
             start_bar[3 * r + a] = float(-vb * inv_dt);
-            post.x(a)[j] = 0.f;
-            post.v(a)[j] = 0.f;
         }
         const double* re = rd.rest + 3 * size_t(r);
         for (int a = 0; a < 3; a++) {
@@ -157,6 +176,7 @@ __global__ void k_adj_rigid_apply(BarBuf post, RigidDev rd, const double* abar) 
     if (rd.fit[24 * size_t(body) + 22] != 0.0) return;
     const double* o = abar + 13 * size_t(body);
     const int j = rd.mslot[r];
+    if (j < 0) return;  // member lives on another slab
     const double* re = rd.rest + 3 * size_t(r);
     const double m = rd.mass[r];
     for (int a = 0; a < 3; a++) {
@@ -165,11 +185,16 @@ __global__ void k_adj_rigid_apply(BarBuf post, RigidDev rd, const double* abar) 
     }
 }
 
-void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, const int* chunk_body,
-                      const int* chunk_m0, const int* chunk_m1, double* partial, float* start_bar, double* abar,
-                      cudaStream_t s) {
+void launch_adj_rigid_gather(BarBuf post, RigidDev rd, double* mbar, cudaStream_t s) {
     if (rd.nbody == 0) return;
-    k_adj_rigid_partial<<<nchunks, 256, 0, s>>>(g, post, rd, chunk_m0, chunk_m1, partial, start_bar);
+    k_adj_rigid_gather<<<(rd.nmem + 255) / 256, 256, 0, s>>>(post, rd, mbar);
+}
+
+void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, const int* chunk_body,
+                      const int* chunk_m0, const int* chunk_m1, const double* mbar, double* partial,
+                      float* start_bar, double* abar, cudaStream_t s) {
+    if (rd.nbody == 0) return;
+    k_adj_rigid_partial<<<nchunks, 256, 0, s>>>(g, mbar, rd, chunk_m0, chunk_m1, partial, start_bar);
     k_adj_rigid_solve<<<(rd.nbody + 31) / 32, 32, 0, s>>>(rd, nchunks, chunk_body, partial, abar);
     k_adj_rigid_apply<<<(rd.nmem + 255) / 256, 256, 0, s>>>(post, rd, abar);
 }
@@ -463,8 +488,10 @@ __global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int*
                 eb.vlin = eb.t;
                 eb.w = eb.t;
                 V3<float> in_bar = {0.f, 0.f, 0.f};
+                // ghost node column (bx == sx1): computed for this slab's gathers, counted by its owner
                 if (effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
-                                         in_bar, eb)) {
+                                         in_bar, eb) &&
+                    bx < g.sx1) {
                     acc[e][0] += eb.t.x; acc[e][1] += eb.t.y; acc[e][2] += eb.t.z;
 #pragma unroll
                     for (int q = 0; q < 9; q++) acc[e][3 + q] += eb.R.m[q];
@@ -696,17 +723,25 @@ void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 }
 
 // inactive particles pass their bars through untouched
-__global__ void k_tail_bars(BarBuf post, BarBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
+// parked particles pass their cotangents through; departed slots (sorted
+// positions [n_keep, n_stored)) get zero -- a migrated particle's cotangent is
+// returned by its new slab before the previous substep's adjoint
+__global__ void k_tail_bars(BarBuf post, BarBuf out, const uint32_t* __restrict__ perm, int n0, int n_keep,
+                            int n_stored) {
     int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    if (j >= n_stored) return;
     uint32_t s = perm[j];
-    for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = post.f[size_t(c) * post.cap + j];
+    if (j < n_keep)
+        for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = post.f[size_t(c) * post.cap + j];
+    else
+        for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = 0.f;
 }
 
-void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s) {
-    int m = n - n_active;
+void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n_keep, int n_stored,
+                      cudaStream_t s) {
+    int m = n_stored - n_active;
     if (m <= 0) return;
-    k_tail_bars<<<(m + 255) / 256, 256, 0, s>>>(post, out, perm, n_active, n);
+    k_tail_bars<<<(m + 255) / 256, 256, 0, s>>>(post, out, perm, n_active, n_keep, n_stored);
 }
 
 // emitter spawn adjoint, sequential over the substep's spawns (fixed order)

@@ -28,61 +28,21 @@
 #include <vector>
 
 #include "../../include/flume_b200.h"
+#include "fl_comm.h"
+#include "fl_host.h"
 #include "fl_kernels.h"
 #include "fl_scatter.cuh"
 
 namespace fl {
 
 // ---------------------------------------------------------------------------
-// errors
+// trajectory storage
 // ---------------------------------------------------------------------------
-struct FlumeError : std::runtime_error {
-    int code;
-    long pid = -1;
-    int body = -1;
-    long substep = -1;
-    FlumeError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-#define CK(expr)                                                                                  \
-    do {                                                                                          \
-        cudaError_t e_ = (expr);                                                                  \
-        if (e_ != cudaSuccess)                                                                    \
-            throw FlumeError(FLUME_E_CUDA, std::string("cuda: ") + cudaGetErrorString(e_) + " at " \
-                                               + __FILE__ + ":" + std::to_string(__LINE__));     \
-    } while (0)
-
-template <class T>
-struct DevArr {
-    T* p = nullptr;
-    size_t n = 0;
-    DevArr() = default;
-    DevArr(const DevArr&) = delete;
-    DevArr& operator=(const DevArr&) = delete;
-    ~DevArr() { release(); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    void alloc(size_t count) {
-        if (count <= n && p) return;
-        release();
-        if (count == 0) count = 1;
-        CK(cudaMalloc(&p, count * sizeof(T)));
-        n = count;
-    }
-    void upload(const std::vector<T>& h, cudaStream_t s) {
-        alloc(h.size());
-        if (!h.empty()) CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
-    }
-};
-
-// one trajectory state in HBM
 struct StateBuf {
     void* mem = nullptr;
     PBuf p{};
     size_t bytes = 0;
+    int n = 0;  // occupied slots (active + parked + arrivals + departed holes; N on one rank)
     StateBuf(int cap, int nmem) {
         size_t pbytes = (size_t(cap) * (24 * sizeof(float) + 3 * sizeof(uint32_t)) + 255) & ~size_t(255);
         bytes = pbytes + size_t(std::max(nmem, 1)) * 3 * sizeof(double);
@@ -116,16 +76,25 @@ struct Record {
     int* mslot = nullptr;
     double* mstart = nullptr;
     double* mid = nullptr;
+    double* mact = nullptr;
     double* fit = nullptr;
     uint16_t* celltab = nullptr;
     float4* gridv = nullptr;   // grid velocity after contact (G2P input), dense block-major
     float4* gridv0 = nullptr;  // (p/m, m) before gravity/walls/contact (grid-update adjoint input)
     int n_active = 0;
+    int n_keep = 0;    // active + parked slots of the pre-state (= N on one rank)
+    int n_stored = 0;  // all slots of the pre-state, departed holes included
+    // slab migration after this substep's G2P: slots of the departed particles
+    // (by direction, in message order) and the arrivals' base slot in the post-state
+    uint32_t* mig_src = nullptr;
+    int mig_cap = 0;
+    long n_out[2] = {0, 0}, n_in[2] = {0, 0};
+    int arr_base = 0;
     long substep = 0;
     std::vector<ActEntry> act;
     std::vector<EmitAdjEntry> emit;
     EffSet effk{};
-    Record(int N, int maxb, int nbtot, int nmem, int nbody) {
+    Record(int N, int maxb, int nbtot, int nmem, int nbody, int migcap) {
         size_t off = 0;
         auto carve = [&](size_t bytes) {
             size_t o = off;
@@ -134,9 +103,10 @@ struct Record {
         };
         size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(16),
                o_nbl = carve(size_t(nbtot) * 4), o_nnb = carve(16), o_ms = carve(size_t(nmem) * 4),
-               o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 24),
+               o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 32),
                o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),
-               o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4));
+               o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4)),
+               o_mig = carve(size_t(2) * migcap * 4);
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -147,10 +117,13 @@ struct Record {
         mslot = reinterpret_cast<int*>(b + o_ms);
         mstart = reinterpret_cast<double*>(b + o_mst);
         mid = reinterpret_cast<double*>(b + o_mid);
+        mact = mid + 3 * size_t(nmem);
         fit = reinterpret_cast<double*>(b + o_fit);
         celltab = reinterpret_cast<uint16_t*>(b + o_ct);
         gridv = reinterpret_cast<float4*>(b + o_gv);
         gridv0 = reinterpret_cast<float4*>(b + o_gv0);
+        mig_src = migcap > 0 ? reinterpret_cast<uint32_t*>(b + o_mig) : nullptr;
+        mig_cap = migcap;
         CK(cudaMemset(gridv, 0, size_t(nbtot) * 64 * sizeof(float4)));
         CK(cudaMemset(gridv0, 0, size_t(nbtot) * 64 * sizeof(float4)));
     }
@@ -331,6 +304,27 @@ struct Ctx {
     std::vector<RecordPtr> rec_pool;
     RecordPtr scratch_rec;
 
+    // x-slab decomposition; comm == nullptr on one rank
+    std::unique_ptr<Transport> comm;
+    int rank = 0, nranks = 1;
+    int n_stored = 0;  // slots of cur: active + parked + arrivals + departed holes (= N on one rank)
+    int park_base = 0;  // first parked slot of cur (= n_active on one rank)
+    int mig_cap = 0;
+    DevArr<unsigned char> halo_send[2], halo_recv[2], mig_send[2], mig_recv[2];
+    DevArr<int> mig_cnt;
+    DevArr<double> mbar;
+    std::vector<float> parked_x;  // positions of parked particles by id (ownership of their activation)
+    bool slab() const { return comm != nullptr; }
+    int n_parked() const { return int(inactive_ids.size()); }
+    void set_transport(std::unique_ptr<Transport> t);
+    void partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t>& active);
+    void halo_exchange(float4* stg, int* flags);
+    void migrate(StateBuf& out, Record& r);
+    void return_bars(Record& r, BarBuf post);
+    void allreduce(void* p, size_t n, DType t, ROp op) {
+        if (comm) comm->allreduce(p, n, t, op, stream);
+    }
+
     // -------------------------------------------------------------------
     StatePtr get_state() {
         if (!pool.empty()) {
@@ -349,7 +343,8 @@ struct Ctx {
             rec_pool.pop_back();
             return r;
         }
-        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1));  // ~2 KB/node block
+        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1),
+                                        mig_cap);  // ~2 KB/node block
     }
     void put_record(RecordPtr r) {
         if (r) rec_pool.push_back(std::move(r));
@@ -371,6 +366,7 @@ struct Ctx {
         d.mslot = r.mslot;
         d.mstart = r.mstart;
         d.mid = r.mid;
+        d.mact = r.mact;
         d.fit = r.fit;
         return d;
     }
@@ -396,6 +392,7 @@ struct Ctx {
     void adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* eb,
                              double* abar_out);
     void copy_state(StateBuf& dst, const StateBuf& src) {
+        dst.n = src.n;
         CK(cudaMemcpyAsync(dst.mem, src.mem, src.bytes, cudaMemcpyDeviceToDevice, stream));
     }
 };
@@ -429,7 +426,11 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     }
     g.nbtot = g.NB[0] * g.NB[1] * g.NB[2];
     g.key_inactive = uint32_t(g.nbtot) << 6;
-    g.keybits = bits_for(g.key_inactive);
+    g.key_departed = uint32_t(g.nbtot + 1) << 6;
+    g.keybits = bits_for(g.key_departed);
+    g.colblocks = g.NB[1] * g.NB[2];
+    g.sx0 = 0;
+    g.sx1 = g.NB[0];
     g.idbits = bits_for(uint64_t(N - 1));
     if (g.keybits + g.idbits > 64) throw FlumeError(FLUME_E_ARG, "grid too large for 64-bit sort keys");
     g.dx = float(dx);
@@ -541,15 +542,17 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     if (N >= (1 << 26)) throw FlumeError(FLUME_E_ARG, "at most 2^26-1 particles per context");
     // one zero-memset per sort covers counts, heavy flags, fill cursors, node-block
     // flags, the block map (slot + 1, 0 = none) and the list counters
-    bzero.alloc(5 * size_t(g.nbtot + 1) + 8);
+    // (counts / heavy flags / fill cursors carry two virtual blocks: parked, departed)
+    const size_t bz = size_t(g.nbtot) + 2;
+    bzero.alloc(5 * bz + 8);
     bcount = bzero.p;
-    bheavy = bzero.p + (g.nbtot + 1);
-    bfill = bzero.p + 2 * (g.nbtot + 1);
-    nbflag = bzero.p + 3 * (g.nbtot + 1);
-    blockmap_p = bzero.p + 4 * (g.nbtot + 1);
-    list_cnt = bzero.p + 5 * (g.nbtot + 1);
+    bheavy = bzero.p + bz;
+    bfill = bzero.p + 2 * bz;
+    nbflag = bzero.p + 3 * bz;
+    blockmap_p = bzero.p + 4 * bz;
+    list_cnt = bzero.p + 5 * bz;
     nbpos.alloc(g.nbtot);
-    bstart.alloc(g.nbtot + 1);
+    bstart.alloc(g.nbtot + 2);
     skey.alloc(N);
     sslot.alloc(N);
     gk.alloc(2 * size_t(N) + 2);
@@ -563,6 +566,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     rig_partial.alloc(std::max<size_t>(chunk_body.size(), 1) * 17);
     abar.alloc(std::max(nbody, 1) * 13);
     start_bar.alloc(std::max(nmem, 1) * 3);
+    mbar.alloc(std::max(nmem, 1) * 6);
     eff_partial.alloc(size_t(kEffBlocks) * kMaxEff * 18);
     loss_partial.alloc(size_t(kLossBlocks) * kMaxLossTerms);
     d_act_list.alloc(64);
@@ -570,7 +574,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     CK(cudaMemsetAsync(gridbar.p, 0, gridbar.n * sizeof(float4), stream));
 
     size_t b2 = 0, b3 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, bcount, bstart.p, g.nbtot + 1, stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, bcount, bstart.p, g.nbtot + 2, stream));
     CK(cub::DeviceScan::ExclusiveSum(nullptr, b3, nbflag, nbpos.p, g.nbtot, stream));
     cub_bytes = std::max(b2, b3);
     cub_tmp.alloc(cub_bytes);
@@ -648,6 +652,7 @@ void Ctx::advance_effectors(const double* action) {
 
 void Ctx::check_error(long /*substep_base*/) {
     unsigned long long h = 0;
+    allreduce(d_err.p, 1, DType::U64, ROp::Min);  // slabs: every rank raises the same error
     CK(cudaMemcpyAsync(&h, d_err.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     if (h == ~0ull) return;
@@ -710,14 +715,41 @@ void Ctx::upload(const flume_state_view* view) {
             pending[p_act[i]].push_back(i);
         }
     }
+    if (slab()) {
+        // split the columns by the uploaded positions (the same on every rank), keep
+        // this slab's active particles; parked ones stay replicated on all slabs
+        std::vector<uint32_t> keys(N, 0);
+        parked_x.assign(size_t(N) * 3, 0.f);
+        for (int i = 0; i < N; i++) {
+            const float p[3] = {float(view->x[3 * size_t(i)]), float(view->x[3 * size_t(i) + 1]),
+                                float(view->x[3 * size_t(i) + 2])};
+            for (int a = 0; a < 3; a++) parked_x[3 * size_t(i) + a] = p[a];
+            if (active[i]) cell_key(geom, p[0], p[1], p[2], keys[i]);
+        }
+        partition(keys, active);
+        n_active = 0;
+        for (int i = 0; i < N; i++) {
+            if (!active[i]) continue;
+            const int col = key_col(geom, keys[i]);
+            if (col < geom.sx0 || col >= geom.sx1)
+                active[i] = 2;
+            else
+                n_active++;
+        }
+    }
     d_upmeta.upload(p_class, stream);
     d_upactive.upload(active, stream);
     StatePtr raw = get_state();
     launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, stream);
     launches++;
     scratch_rec->n_active = n_active;
+    scratch_rec->n_keep = n_active + n_parked();
+    scratch_rec->n_stored = N;
     sort_and_lists(*raw, *scratch_rec);
-    launch_gather(raw->p, cur->p, scratch_rec->perm, N, stream);
+    launch_gather(raw->p, cur->p, scratch_rec->perm, scratch_rec->n_keep, stream);
+    n_stored = scratch_rec->n_keep;
+    cur->n = n_stored;
+    park_base = n_active;
     launch_upload_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
     launches += 3;
     put_state(raw);
@@ -736,7 +768,16 @@ void Ctx::upload(const flume_state_view* view) {
 
 void Ctx::download(flume_state_view* view) {
     for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
-    launch_download(cur->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
+    if (slab()) {
+        // every rank fills its own particles (rank 0 also the parked ones) into
+        // zeroed arrays; the all-reduce assembles the whole state on every rank
+        for (int k = 0; k < 4; k++) CK(cudaMemsetAsync(d_up[k].p, 0, d_up[k].n * 8, stream));
+        launch_download(cur->p, n_stored, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, rank == 0,
+                        geom.key_inactive, stream);
+        for (int k = 0; k < 4; k++) allreduce(d_up[k].p, size_t(N) * (k < 2 ? 3 : 9), DType::F64, ROp::Sum);
+    } else {
+        launch_download(cur->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, 1, geom.key_inactive, stream);
+    }
     launch_download_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
     launches += 2;
     if (view->x) CK(cudaMemcpyAsync(view->x, d_up[0].p, size_t(N) * 3 * 8, cudaMemcpyDeviceToHost, stream));
@@ -761,15 +802,140 @@ void Ctx::download(flume_state_view* view) {
 // keys -> canonical order + particle-block list (fl_sort.cu)
 void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     Geom& g = geom;
+    const int n = r.n_stored;
     CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
-    launch_sort_count(g, st.p, N, d_cls.p, bcount, bheavy, stream);
-    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, bcount, bstart.p, g.nbtot + 1, stream));
-    launch_sort_scatter(g, st.p, N, bstart.p, bcount, bheavy, bfill, skey.p, sslot.p, r.recs, list_cnt, blockmap_p,
+    launch_sort_count(g, st.p, n, d_cls.p, bcount, bheavy, stream);
+    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, bcount, bstart.p, g.nbtot + 2, stream));
+    launch_sort_scatter(g, st.p, n, bstart.p, bcount, bheavy, bfill, skey.p, sslot.p, r.recs, list_cnt, blockmap_p,
                         nbflag, maxb, stream);
     CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, g.nbtot, stream));
     launch_nb_scatter(nbflag, nbpos.p, g.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
     launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
                        grid_sort, stream);
+    launches += 4;
+}
+
+// ---------------------------------------------------------------------------
+// x-slabs: halo exchange of scatter tiles, particle migration, cotangent return
+// ---------------------------------------------------------------------------
+void Ctx::set_transport(std::unique_ptr<Transport> t) {
+    comm = std::move(t);
+    rank = comm->rank();
+    nranks = comm->size();
+    if (nranks > geom.NB[0]) throw FlumeError(FLUME_E_ARG, "more slab ranks than 4-cell columns along x");
+    // ghost particle blocks of the two neighbour columns live past the block list
+    staging.alloc((size_t(maxb) + 2 * size_t(geom.colblocks)) * kTile);
+    staging_bar.alloc((size_t(maxb) + 2 * size_t(geom.colblocks)) * kTile);
+    for (int d = 0; d < 2; d++) {
+        halo_send[d].alloc(halo_bytes(geom));
+        halo_recv[d].alloc(halo_bytes(geom));
+    }
+    // a slab can lose at most its own particles; a quarter of the scene per
+    // direction is far beyond what the CFL bound (< 1 cell per substep) allows
+    mig_cap = std::max(4096, N / 4);
+    for (int d = 0; d < 2; d++) {
+        mig_send[d].alloc(mig_bytes(mig_cap));
+        mig_recv[d].alloc(mig_bytes(mig_cap));
+    }
+    mig_cnt.alloc(2);
+    rec_pool.clear();
+    scratch_rec = get_record();
+    CK(cudaStreamSynchronize(stream));
+}
+
+// Columns [sx0, sx1) per rank, balanced by active particle count; every rank
+// computes the same split from the same uploaded state.
+void Ctx::partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t>& active) {
+    const int nc = geom.NB[0];
+    std::vector<double> w(nc, 0.0);
+    for (size_t i = 0; i < keys.size(); i++)
+        if (active[i]) w[key_col(geom, keys[i])] += 1.0;
+    double tot = 0;
+    for (double v : w) tot += v;
+    std::vector<int> cut(nranks + 1, 0);
+    cut[nranks] = nc;
+    double acc = 0;
+    int c = 0;
+    for (int r = 1; r < nranks; r++) {
+        const double want = tot * r / nranks;
+        while (c < nc && acc + w[c] <= want) acc += w[c++];
+        // at least one column per rank on both sides
+        cut[r] = std::max(cut[r - 1] + 1, std::min(c, nc - (nranks - r)));
+        while (c < cut[r]) acc += w[c++];
+    }
+    geom.sx0 = cut[rank];
+    geom.sx1 = cut[rank + 1];
+}
+
+// After a scatter into `stg` (P2G tiles or the G2P-adjoint grid cotangent):
+// send tile planes 0,1 of the bottom column down and 4,5 of the top column up,
+// install the received planes as ghost blocks.  flags != nullptr (forward):
+// also flag the owned node blocks reached only by the lower neighbour's tiles.
+void Ctx::halo_exchange(float4* stg, int* flags) {
+    Geom& g = geom;
+    const bool lo = rank > 0, hi = rank + 1 < nranks;
+    if (lo) launch_halo_pack(g, blockmap_p, stg, g.sx0, 0, halo_send[0].p, stream);
+    if (hi) launch_halo_pack(g, blockmap_p, stg, g.sx1 - 1, 4, halo_send[1].p, stream);
+    const size_t hb = halo_bytes(g);
+    const void* sb[2] = {halo_send[0].p, halo_send[1].p};
+    void* rb[2] = {halo_recv[0].p, halo_recv[1].p};
+    const size_t sz[2] = {lo ? hb : 0, hi ? hb : 0};
+    comm->neighbor_exchange(sb, sz, rb, sz, stream);
+    if (lo)
+        launch_halo_unpack(g, halo_recv[0].p, g.sx0 - 1, 4, maxb, blockmap_p, stg, flags, flags ? g.sx0 : -1,
+                           stream);
+    if (hi) launch_halo_unpack(g, halo_recv[1].p, g.sx1, 0, maxb + g.colblocks, blockmap_p, stg, nullptr, -1, stream);
+    launches += 2 * (int(lo) + int(hi));
+}
+
+// Particles whose post-G2P base cell left the slab go to the neighbour (CFL:
+// < 1 cell per substep, so never further); arrivals are appended after the
+// parked tail.  One host round trip for the message sizes.
+void Ctx::migrate(StateBuf& out, Record& r) {
+    CK(cudaMemsetAsync(mig_cnt.p, 0, 2 * sizeof(int), stream));
+    launch_mig_pack(geom, out.p, n_active, mig_send[0].p, mig_send[1].p, r.mig_src, mig_cnt.p, mig_cap, stream);
+    int h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, mig_cnt.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (h[0] > mig_cap || h[1] > mig_cap) {
+        comm->abort();
+        throw FlumeError(FLUME_E_ENGINE, "slab migration buffer overflow");
+    }
+    const long send[2] = {h[0], h[1]};
+    long recv[2] = {0, 0};
+    comm->exchange_counts(send, recv, stream);
+    const void* sb[2] = {mig_send[0].p, mig_send[1].p};
+    void* rb[2] = {mig_recv[0].p, mig_recv[1].p};
+    const size_t ss[2] = {mig_bytes(h[0]), mig_bytes(h[1])}, rs[2] = {mig_bytes(int(recv[0])), mig_bytes(int(recv[1]))};
+    comm->neighbor_exchange(sb, ss, rb, rs, stream);
+    const int base = n_active + n_parked();
+    if (base + recv[0] + recv[1] > N) throw FlumeError(FLUME_E_ENGINE, "slab store overflow");
+    launch_mig_unpack(out.p, mig_recv[0].p, int(recv[0]), base, stream);
+    launch_mig_unpack(out.p, mig_recv[1].p, int(recv[1]), base + int(recv[0]), stream);
+    launches += 3;
+    for (int d = 0; d < 2; d++) {
+        r.n_out[d] = h[d];
+        r.n_in[d] = recv[d];
+    }
+    r.arr_base = base;
+    n_active += int(recv[0] + recv[1]) - h[0] - h[1];
+    n_stored = base + int(recv[0] + recv[1]);
+}
+
+// Backward of migrate(): before the adjoint of substep r, the cotangents of the
+// particles that arrived here travel back into the departed slots of their
+// previous slab (message order = the forward's).
+void Ctx::return_bars(Record& r, BarBuf post) {
+    const size_t w = 24 * sizeof(float);
+    launch_bars_pack(post, r.arr_base, int(r.n_in[0]), mig_send[0].p, stream);
+    launch_bars_pack(post, r.arr_base + int(r.n_in[0]), int(r.n_in[1]), mig_send[1].p, stream);
+    const void* sb[2] = {mig_send[0].p, mig_send[1].p};
+    void* rb[2] = {mig_recv[0].p, mig_recv[1].p};
+    const size_t ss[2] = {size_t(r.n_in[0]) * w, size_t(r.n_in[1]) * w};
+    const size_t rs[2] = {size_t(r.n_out[0]) * w, size_t(r.n_out[1]) * w};
+    comm->neighbor_exchange(sb, ss, rb, rs, stream);
+    launch_bars_scatter(post, mig_recv[0].p, r.mig_src, int(r.n_out[0]), stream);
+    launch_bars_scatter(post, mig_recv[1].p, r.mig_src + r.mig_cap, int(r.n_out[1]), stream);
     launches += 4;
 }
 
@@ -782,12 +948,18 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     r.emit.clear();
     auto it = pending.find(substep_index);
     if (it != pending.end()) {
+        int gained = 0;
         for (int id : it->second) {
             auto pos_it = std::lower_bound(inactive_ids.begin(), inactive_ids.end(), uint32_t(id));
-            int slot = n_active + int(pos_it - inactive_ids.begin());
+            int slot = park_base + int(pos_it - inactive_ids.begin());
             ActEntry a{};
             a.slot = slot;
             int em = emitter_of[id];
+            float px[3] = {parked_x.empty() ? 0.f : parked_x[3 * size_t(id)],
+                           parked_x.empty() ? 0.f : parked_x[3 * size_t(id) + 1],
+                           parked_x.empty() ? 0.f : parked_x[3 * size_t(id) + 2]};
+            EmitAdjEntry ea{};
+            bool has_emit = false;
             if (em >= 0) {
                 const flume_emitter& e = emitters[em];
                 V3<double> lp = {e.local_pos[0], e.local_pos[1], e.local_pos[2]};
@@ -798,7 +970,6 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                     raw = es.R * lp + es.t;
                     vel = es.R * lv;
                 }
-                EmitAdjEntry ea{};
                 ea.slot = slot;
                 ea.eff = e.effector;
                 a.has_xv = 1;
@@ -806,19 +977,30 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                     double cl = clamp_ref(raw[d], double(geom.lo[d]), double(geom.hi[d]));
                     a.x[d] = float(cl);
                     a.v[d] = float(vel[d]);
+                    px[d] = a.x[d];
                     ea.mask[d] = (cl != raw[d]) ? 1 : 0;
                     ea.local_pos[d] = lp[d];
                     ea.local_vel[d] = lv[d];
                 }
-                r.emit.push_back(ea);
+                has_emit = true;
             }
+            if (slab()) {  // the slab owning the activation cell takes the particle
+                uint32_t key;
+                cell_key(geom, px[0], px[1], px[2], key);
+                const int col = key_col(geom, key);
+                a.departed = (col < geom.sx0 || col >= geom.sx1) ? 1 : 0;
+            }
+            if (has_emit && !a.departed) r.emit.push_back(ea);
+            if (!a.departed) gained++;
             r.act.push_back(a);
         }
         for (int id : it->second) {
             auto pos_it = std::lower_bound(inactive_ids.begin(), inactive_ids.end(), uint32_t(id));
             inactive_ids.erase(pos_it);
         }
-        n_active += int(it->second.size());
+        // parked slots are [n_active, n_active + parked): the activated ones are
+        // re-keyed in place and sorted in; departed ones drop out at the next sort
+        n_active += gained;
         d_act_list.alloc(r.act.size());
         CK(cudaMemcpyAsync(d_act_list.p, r.act.data(), r.act.size() * sizeof(ActEntry), cudaMemcpyHostToDevice,
                            stream));
@@ -828,16 +1010,26 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         CK(cudaStreamSynchronize(stream));
     }
     r.n_active = n_active;
+    r.n_keep = n_active + n_parked();
+    r.n_stored = n_stored;
     PROF(K_SORT, sort_and_lists(*in, r));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
          }));
+    if (slab()) {
+        halo_exchange(staging.p, nbflag);
+        // node-block list again, now with the blocks reached only by ghost tiles
+        CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
+        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
+        launches += 2;
+    }
     PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0,
                                     r.effk, stream));
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
         CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
+        CK(cudaMemsetAsync(r.mid, 0, size_t(nmem) * 4 * sizeof(double), stream));
         CK(cudaMemcpyAsync(out->p.mx, in->p.mx, size_t(nmem) * 3 * sizeof(double), cudaMemcpyDeviceToDevice,
                            stream));
     }
@@ -845,13 +1037,23 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
              launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : grid_g2p, d_cls.p, r.gridv,
                         rd, d_err.p, uint32_t(substep_index), hv, w, s);
          }));
-    PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, N, stream));
+    PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
     launches += 4;
     if (nbody > 0) {
+        // slabs: every rank contributes its members' positions (disjoint support,
+        // exact sum) so all ranks fit identical rigid transforms
+        if (slab()) allreduce(r.mid, size_t(nmem) * 4, DType::F64, ROp::Sum);
         PROF(K_RIGID, launch_rigid(geom, out->p, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p,
                                    d_chunk_m1.p, rig_partial.p, d_err.p, uint32_t(substep_index), stream));
         launches += 3;
     }
+    park_base = r.n_active;
+    if (slab()) {
+        migrate(*out, r);
+    } else {
+        n_stored = r.n_keep;
+    }
+    out->n = n_stored;
     time += cfg.dt_substep;
     substep_index++;
 }
@@ -870,12 +1072,19 @@ void Ctx::substep(const double* action, int count) {
 void Ctx::stage_grid(double* mass, double* vel) {
     Record& r = *scratch_rec;
     r.n_active = n_active;
+    r.n_keep = n_active + n_parked();
+    r.n_stored = n_stored;
     sort_and_lists(*cur, r);
     EffSet es = make_effset(eff);
     dual([&](bool hv, int* w, cudaStream_t s) {
         launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
                    staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
     });
+    if (slab()) {
+        halo_exchange(staging.p, nbflag);
+        CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
+        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
+    }
     launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0, es, stream);
     std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
@@ -895,7 +1104,9 @@ void Ctx::stage_grid(double* mass, double* vel) {
         }
     }
     const int* nd = geom.nd;
-    for (int i = 0; i < nd[0]; i++)
+    // slabs: each rank writes the node planes it owns
+    const int i0 = slab() ? 4 * geom.sx0 : 0, i1 = slab() ? std::min(nd[0], 4 * geom.sx1) : nd[0];
+    for (int i = i0; i < i1; i++)
         for (int j = 0; j < nd[1]; j++)
             for (int k = 0; k < nd[2]; k++) {
                 size_t flat = (size_t(i) * nd[1] + j) * nd[2] + k;
@@ -928,8 +1139,11 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
             // initial positions by particle id from the current (state0) store
             auto arr = std::make_shared<DevArr<float>>();
             arr->alloc(size_t(N) * 3);
-            for (int q = 0; q < 1; q++) d_up[0].alloc(size_t(N) * 3);
-            launch_download(cur->p, N, d_up[0].p, nullptr, nullptr, nullptr, stream);
+            d_up[0].alloc(size_t(N) * 3);
+            if (slab()) CK(cudaMemsetAsync(d_up[0].p, 0, size_t(N) * 3 * 8, stream));
+            launch_download(cur->p, n_stored, d_up[0].p, nullptr, nullptr, nullptr, rank == 0, geom.key_inactive,
+                            stream);
+            if (slab()) allreduce(d_up[0].p, size_t(N) * 3, DType::F64, ROp::Sum);
             std::vector<double> hx(size_t(N) * 3);
             CK(cudaMemcpyAsync(hx.data(), d_up[0].p, hx.size() * 8, cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
@@ -952,7 +1166,8 @@ uint32_t Ctx::loss_mask(const flume_loss_desc* loss, int seg, int nseg) const {
 }
 
 void Ctx::eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, long /*substep*/) {
-    launch_loss(st.p, N, d_cls.p, ls, mask, loss_partial.p, out_dev, geom.key_inactive, stream);
+    // per-slab partial; the segment losses are all-reduced once after the rollout
+    launch_loss(st.p, st.n, d_cls.p, ls, mask, loss_partial.p, out_dev, geom.key_inactive, stream);
     launches += 2;
 }
 
@@ -965,7 +1180,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     // state0 is const: work on a copy
     const long s0 = substep_index;
     const double time0 = time;
-    const int na0 = n_active;
+    const int na0 = n_active, ns0 = n_stored, pb0 = park_base;
     const std::vector<EffState> eff0 = eff;
     const std::vector<uint32_t> inact0 = inactive_ids;
     const auto pend0 = pending;
@@ -981,6 +1196,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
             eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, substep_index);
         }
     }
+    allreduce(loss_out.p, size_t(a->n_segments), DType::F64, ROp::Sum);
     std::vector<double> per(a->n_segments);
     CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
@@ -988,6 +1204,8 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     substep_index = s0;
     time = time0;
     n_active = na0;
+    n_stored = ns0;
+    park_base = pb0;
     eff = eff0;
     inactive_ids = inact0;
     pending = pend0;
@@ -1006,6 +1224,8 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                        int t_slot) {
     Geom& g = geom;
     BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
+    // slabs: cotangents of the particles that migrated in after this substep go home first
+    if (slab()) return_bars(r, post);
     // the forward recorded this substep's grid (r.gridv, r.gridv0); only the
     // particle-block map is rebuilt for the staging gathers
     CK(cudaMemsetAsync(blockmap_p, 0, size_t(g.nbtot) * sizeof(int), stream));
@@ -1013,21 +1233,24 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     launches += 1;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
+        launch_adj_rigid_gather(post, rd, mbar.p, stream);
+        if (slab()) allreduce(mbar.p, size_t(nmem) * 6, DType::F64, ROp::Sum);
         PROF(K_RIGID, launch_adj_rigid(g, post, rd, int(chunk_body.size()), d_chunk_body.p, d_chunk_m0.p,
-                                       d_chunk_m1.p, rig_partial.p, start_bar.p, abar.p, stream));
-        launches += 3;
+                                       d_chunk_m1.p, mbar.p, rig_partial.p, start_bar.p, abar.p, stream));
+        launches += 4;
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
          }));
+    if (slab()) halo_exchange(staging_bar.p, nullptr);
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap_p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
                                      eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv, w, s);
          }));
-    PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, N, stream));
+    PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
     launches += 5;
     if (!r.emit.empty()) {
         d_emit_list.alloc(r.emit.size());
@@ -1066,7 +1289,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     struct HostSnap {
         long substep;
         double time;
-        int n_active;
+        int n_active, n_stored, park_base;
         std::vector<EffState> eff;
         std::vector<uint32_t> inactive;
         std::map<long, std::vector<int>> pending;
@@ -1074,12 +1297,14 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     const long s0 = substep_index;
     const double time0 = time;
     auto take_host = [&]() {
-        return HostSnap{substep_index, time, n_active, eff, inactive_ids, pending};
+        return HostSnap{substep_index, time, n_active, n_stored, park_base, eff, inactive_ids, pending};
     };
     auto restore_host = [&](const HostSnap& h) {
         substep_index = h.substep;
         time = h.time;
         n_active = h.n_active;
+        n_stored = h.n_stored;
+        park_base = h.park_base;
         eff = h.eff;
         inactive_ids = h.inactive;
         pending = h.pending;
@@ -1128,6 +1353,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         }
     }
     const size_t n_snap = snaps.size();
+    allreduce(loss_out.p, size_t(nseg), DType::F64, ROp::Sum);
     CK(cudaEventRecord(ev1, stream));
     std::vector<double> per(nseg);
     CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
@@ -1181,7 +1407,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             int seg = int((t + 1) / seglen) - 1;
             ensure_cached(t);
             StateBuf& boundary = *cache_states[size_t(t + 1 - cache_base)];
-            launch_loss_grad(boundary.p, N, d_cls.p, ls, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
+            launch_loss_grad(boundary.p, boundary.n, d_cls.p, ls, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
                              geom.key_inactive, stream);
             launches++;
         }
@@ -1193,6 +1419,11 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     }
     release_cache();
     for (auto& kv : snaps) put_state(kv.second);
+    if (slab()) {  // per-slab effector / spawn bars and non-finite flags
+        allreduce(eff_out.p, size_t(T) * kMaxEff * 18, DType::F64, ROp::Sum);
+        allreduce(em_out.p, size_t(T) * kMaxEff * 12, DType::F64, ROp::Sum);
+        allreduce(d_nonfinite.p, size_t(T), DType::I32, ROp::Max);
+    }
     CK(cudaEventRecord(ev2, stream));
 
     // ---------------- effector pose chain (host, fp64) ----------------
@@ -1260,6 +1491,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
 
 void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* ebars,
                               double* abar_out) {
+    if (slab()) throw FlumeError(FLUME_E_ARG, "adjoint_substep: single-rank contexts only");
     xbar_tmp.alloc(size_t(N) * 3);
     Fbar_tmp.alloc(size_t(N) * 9);
     eff_out.alloc(kMaxEff * 18);
@@ -1269,7 +1501,7 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     CK(cudaMemsetAsync(d_nonfinite.p, 0, sizeof(int), stream));
     const long s0 = substep_index;
     const double time0 = time;
-    const int na0 = n_active;
+    const int na0 = n_active, ns0 = n_stored, pb0 = park_base;
     const std::vector<EffState> eff0 = eff;
     const std::vector<uint32_t> inact0 = inactive_ids;
     const auto pend0 = pending;
@@ -1307,6 +1539,8 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     substep_index = s0;
     time = time0;
     n_active = na0;
+    n_stored = ns0;
+    park_base = pb0;
     inactive_ids = inact0;
     pending = pend0;
     const double dt = cfg.dt_substep;
@@ -1365,6 +1599,10 @@ int guard(flume_ctx* ctx, F&& f) {
         f();
         return FLUME_OK;
     } catch (const FlumeError& e) {
+        // engine errors are raised identically on every slab rank (error flags and
+        // losses are all-reduced first); device failures may hit one rank only,
+        // so they release the peers waiting in the group
+        if (e.code == FLUME_E_CUDA && ctx && ctx->c.comm) ctx->c.comm->abort();
         info->code = e.code;
         info->particle_id = e.pid;
         info->body_id = e.body;
@@ -1372,6 +1610,7 @@ int guard(flume_ctx* ctx, F&& f) {
         std::snprintf(info->message, sizeof(info->message), "%s", e.what());
         return e.code;
     } catch (const std::exception& e) {
+        if (ctx && ctx->c.comm) ctx->c.comm->abort();
         info->code = FLUME_E_OTHER;
         std::snprintf(info->message, sizeof(info->message), "%s", e.what());
         return FLUME_E_OTHER;
@@ -1394,6 +1633,63 @@ int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out) 
         return rc;
     }
     *out = ctx;
+    return FLUME_OK;
+}
+
+int flume_group_create(const flume_scene_desc* desc, int n_ranks, const int* devices, flume_ctx** out) {
+    if (!desc || !out || n_ranks < 1) return FLUME_E_ARG;
+    for (int r = 0; r < n_ranks; r++) out[r] = nullptr;
+    auto grp = std::make_shared<fl::ThreadGroup>(n_ranks);
+    for (int r = 0; r < n_ranks; r++) {
+        const int dev = devices ? devices[r] : 0;
+        flume_ctx* ctx = new flume_ctx();
+        int rc = guard(nullptr, [&] {
+            ctx->c.init(desc, dev);
+            if (n_ranks > 1) ctx->c.set_transport(fl::make_thread_transport(grp, r, dev));
+        });
+        if (rc != FLUME_OK) {
+            delete ctx;
+            for (int q = 0; q < r; q++) {
+                delete out[q];
+                out[q] = nullptr;
+            }
+            return rc;
+        }
+        out[r] = ctx;
+    }
+    return FLUME_OK;
+}
+
+int flume_dist_unique_id(unsigned char uid[128]) {
+    if (!uid) return FLUME_E_ARG;
+    return guard(nullptr, [&] { fl::nccl_unique_id(uid); });
+}
+
+int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, int n_ranks,
+                          const unsigned char uid[128], flume_ctx** out) {
+    if (!desc || !out || !uid || rank < 0 || rank >= n_ranks) return FLUME_E_ARG;
+    *out = nullptr;
+    flume_ctx* ctx = new flume_ctx();
+    int rc = guard(nullptr, [&] {
+        ctx->c.init(desc, device);
+        if (n_ranks > 1) ctx->c.set_transport(fl::make_nccl_transport(uid, rank, n_ranks, device));
+    });
+    if (rc != FLUME_OK) {
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return FLUME_OK;
+}
+
+int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int* sx1, long* n_active) {
+    if (!ctx) return FLUME_E_ARG;
+    const fl::Ctx& c = ctx->c;
+    if (rank) *rank = c.rank;
+    if (n_ranks) *n_ranks = c.nranks;
+    if (sx0) *sx0 = c.geom.sx0;
+    if (sx1) *sx1 = c.geom.sx1;
+    if (n_active) *n_active = c.n_active;
     return FLUME_OK;
 }
 

@@ -37,8 +37,10 @@ __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, 
     }
     raw.meta[i] = meta[i];
     raw.id[i] = uint32_t(i);
+    // active: 0 = parked (activates later), 1 = active here, 2 = active on another slab
     uint32_t key = g.key_inactive;
     if (active[i]) cell_key(g, raw.x(0)[i], raw.x(1)[i], raw.x(2)[i], key);
+    if (active[i] == 2) key = g.key_departed;
     raw.key[i] = key;
 }
 
@@ -76,9 +78,14 @@ void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t 
     k_gather<<<(n + 255) / 256, 256, 0, s>>>(in, out, perm, n);
 }
 
-__global__ void k_download(PBuf st, int n, double* x, double* v, double* F, double* C) {
+// by particle id; departed slots are skipped, parked particles (replicated on
+// every slab) only where write_parked is set
+__global__ void k_download(PBuf st, int n, double* x, double* v, double* F, double* C, int write_parked,
+                           uint32_t key_inactive) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const uint32_t key = st.key[i];
+    if (key > key_inactive || (key == key_inactive && !write_parked)) return;
     size_t id = st.id[i];
     for (int a = 0; a < 3; a++) {
         if (x) x[3 * id + a] = double(st.x(a)[i]);
@@ -90,9 +97,10 @@ __global__ void k_download(PBuf st, int n, double* x, double* v, double* F, doub
     }
 }
 
-void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, cudaStream_t s) {
+void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, int write_parked,
+                     uint32_t key_inactive, cudaStream_t s) {
     if (n <= 0) return;
-    k_download<<<(n + 255) / 256, 256, 0, s>>>(st, n, x, v, F, C);
+    k_download<<<(n + 255) / 256, 256, 0, s>>>(st, n, x, v, F, C, write_parked, key_inactive);
 }
 
 __global__ void k_rigid_x(PBuf st, int nmem, const int* member_id, double* x, int dir) {
@@ -152,7 +160,7 @@ __global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n) {
     }
     uint32_t key;
     cell_key(g, st.x(0)[e.slot], st.x(1)[e.slot], st.x(2)[e.slot], key);
-    st.key[e.slot] = key;
+    st.key[e.slot] = e.departed ? g.key_departed : key;  // departed: activates on another slab
 }
 
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s) {
@@ -414,6 +422,7 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : 8) k_g2p(Geom g, PBuf in, PBu
                     const double xm = clamp_ref(sx + double(vuse[a]) * double(g.dt), double(g.lo[a]), double(g.hi[a]));
                     rd.mstart[3 * mr + a] = sx;
                     rd.mid[3 * mr + a] = xm;
+                    if (a == 0) rd.mact[mr] = 1.0;
                     out.mx[3 * mr + a] = xm;
                     out.x(a)[j] = float(xm);
                 }
@@ -443,6 +452,7 @@ __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restric
     out.key[j] = g.key_inactive;
 }
 
+// parked particles: sorted positions [n_active, n) (departed slots beyond n are dropped)
 void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s) {
     int m = n - n_active;
     if (m <= 0) return;
@@ -464,8 +474,7 @@ __global__ void __launch_bounds__(256) k_rigid_partial(PBuf out, RigidDev rd, co
 #pragma unroll
     for (int q = 0; q < kRigidQ; q++) acc[q] = 0.0;
     for (int r = m0 + threadIdx.x; r < m1; r += 256) {
-        const int j = rd.mslot[r];
-        if (j < 0) continue;
+        if (rd.mact[r] == 0.0) continue;  // member not active (or, with slabs, not reduced yet)
         const double m = rd.mass[r];
         const double x[3] = {rd.mid[3 * size_t(r)], rd.mid[3 * size_t(r) + 1], rd.mid[3 * size_t(r) + 2]};
         const double* re = rd.rest + 3 * size_t(r);
@@ -528,18 +537,24 @@ __global__ void k_rigid_apply(Geom g, PBuf out, RigidDev rd) {
     if (r >= rd.nmem) return;
     const int body = rd.member_body[r];
     const double* fit = rd.fit + 24 * size_t(body);
-    if (fit[22] != 0.0) return;
+    // the fp64 member positions are replicated on every slab (mid is all-reduced)
+    if (fit[22] != 0.0) {
+        if (rd.mact[r] != 0.0)
+            for (int a = 0; a < 3; a++) out.mx[3 * size_t(r) + a] = rd.mid[3 * size_t(r) + a];
+        return;
+    }
     const int j = rd.mslot[r];
     const double* re = rd.rest + 3 * size_t(r);
     double xn[3];
     for (int a = 0; a < 3; a++) {
         double raw = fit[3 * a] * re[0] + fit[3 * a + 1] * re[1] + fit[3 * a + 2] * re[2] + fit[9 + a];
         xn[a] = clamp_ref(raw, double(g.lo[a]), double(g.hi[a]));
+        out.mx[3 * size_t(r) + a] = xn[a];
     }
+    if (j < 0) return;  // member lives on another slab
     const double inv_dt = 1.0 / double(g.dt);
     for (int a = 0; a < 3; a++) {
         out.x(a)[j] = float(xn[a]);
-        out.mx[3 * size_t(r) + a] = xn[a];
         out.v(a)[j] = float((xn[a] - rd.mstart[3 * size_t(r) + a]) * inv_dt);
     }
     uint32_t key;
@@ -549,7 +564,7 @@ __global__ void k_rigid_apply(Geom g, PBuf out, RigidDev rd) {
 
 void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body, const int* chunk_m0,
                   const int* chunk_m1, double* partial, unsigned long long* err, uint32_t substep, cudaStream_t s) {
-    if (rd.nbody == 0) return;
+    if (rd.nbody == 0) return;  // (with slabs rd.mid / rd.mact were all-reduced first)
     k_rigid_partial<<<nchunks, 256, 0, s>>>(out, rd, chunk_m0, chunk_m1, partial);
     k_rigid_solve<<<(rd.nbody + 31) / 32, 32, 0, s>>>(rd, nchunks, chunk_body, partial, err, substep);
     k_rigid_apply<<<(rd.nmem + 255) / 256, 256, 0, s>>>(g, out, rd);
@@ -567,7 +582,9 @@ __global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const Clas
     for (int k = 0; k < kMaxLossTerms; k++) acc[k] = 0.0;
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
         const int body = cls[meta_cls(st.meta[i])].body;
-        const bool active = st.key[i] != key_inactive;
+        const uint32_t key = st.key[i];
+        if (key > key_inactive) continue;  // departed slot: counted on the particle's new slab
+        const bool active = key < key_inactive;
         for (int k = 0; k < ls.n; k++) {
             if (!((mask >> k) & 1u) || ls.t[k].body != body) continue;
             const LossTermDev& t = ls.t[k];

@@ -24,12 +24,14 @@ struct RigidDev {
     int* mslot;               // [nmem] sorted position of the member in the post-g2p buffer (-1 inactive)
     double* mstart;           // [3*nmem] stage-a position (rigid_body_pass start_positions)
     double* mid;              // [3*nmem] post-g2p position
+    double* mact;             // [nmem] 1 where mid holds an active member (all-reduced with mid on slabs)
     double* fit;              // [nbody*24]: R[9] c[3] A[9] total skip ok
 };
 
 struct ActEntry {
     int slot;
     int has_xv;
+    int departed;  // activates inside another rank's slab
     float x[3];
     float v[3];
 };
@@ -80,7 +82,8 @@ void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, in
 void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body,
                   const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
                   uint32_t substep, cudaStream_t s);
-void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, cudaStream_t s);
+void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, int write_parked,
+                     uint32_t key_inactive, cudaStream_t s);
 void launch_download_rigid(PBuf st, int nmem, const int* member_id, double* x, cudaStream_t s);
 void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* x, cudaStream_t s);
 void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
@@ -89,9 +92,10 @@ void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
 // ---- backward ----
 void launch_loss_grad(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
                       BarBuf bars, uint32_t key_inactive, cudaStream_t s);
+void launch_adj_rigid_gather(BarBuf post, RigidDev rd, double* mbar, cudaStream_t s);
 void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, const int* chunk_body,
-                      const int* chunk_m0, const int* chunk_m1, double* partial, float* start_bar,
-                      double* abar, cudaStream_t s);
+                      const int* chunk_m0, const int* chunk_m1, const double* mbar, double* partial,
+                      float* start_bar, double* abar, cudaStream_t s);
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, PBuf postst,
                     BarBuf post, float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar,
@@ -102,7 +106,8 @@ void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const i
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s);
-void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
+void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n_keep, int n_stored,
+                      cudaStream_t s);
 void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
 void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb,
                           const double* Fb, const double* Cb, cudaStream_t s);
@@ -119,6 +124,19 @@ void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, i
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s);
+
+// ---- x-slab decomposition (fl_slab.cu) ----
+size_t halo_bytes(const Geom& g);
+size_t mig_bytes(int n);
+void launch_halo_pack(const Geom& g, const int* blockmap, const float4* staging, int col, int plane0, void* out,
+                      cudaStream_t s);
+void launch_halo_unpack(const Geom& g, const void* in, int col, int plane0, int ghost_base, int* blockmap,
+                        float4* staging, int* nbflag, int flag_col, cudaStream_t s);
+void launch_mig_pack(const Geom& g, PBuf out, int n, void* send0, void* send1, uint32_t* src, int* cnt, int cap,
+                     cudaStream_t s);
+void launch_mig_unpack(PBuf out, const void* in, int n, int pos0, cudaStream_t s);
+void launch_bars_pack(BarBuf bars, int pos0, int n, void* out, cudaStream_t s);
+void launch_bars_scatter(BarBuf bars, const void* in, const uint32_t* src, int n, cudaStream_t s);
 
 enum KGrid { KG_P2G = 0, KG_G2P = 1, KG_ADJ_G2P = 2, KG_ADJ_P2G = 3 };
 int occupancy_grid(KGrid which, bool heavy);  // resident CTAs per SM x SMs

@@ -27,7 +27,10 @@ struct Geom {
     int nbtot;      // NB0*NB1*NB2
     int maxb;       // particle-block list capacity: light blocks at [0, n0), heavy at [maxb - n1, maxb)
     uint32_t key_inactive;  // nbtot << 6, sorts after every valid key
-    int keybits;    // bits needed for key_inactive
+    uint32_t key_departed;  // (nbtot + 1) << 6: slot left by a particle that moved to another slab
+    int keybits;    // bits needed for key_departed
+    int sx0, sx1;   // x-slab of particle-block columns owned by this rank ([0, NB0) for one rank)
+    int colblocks;  // NB1 * NB2 blocks per x column
     int idbits;     // bits needed for particle ids
     float dx, inv_dx, dt;
     float lo[3], hi[3];  // clamp_to_interior bounds [dx, L-dx] (mpm.hpp:330-336)
@@ -111,6 +114,8 @@ __host__ __device__ inline void block_unlin(const Geom& g, int b, int& bx, int& 
     by = r % g.NB[1];
     bx = r / g.NB[1];
 }
+__host__ __device__ inline int key_col(const Geom& g, uint32_t key) { return int(key >> 6) / g.colblocks; }
+
 __host__ __device__ inline size_t node_index(const Geom& g, int i, int j, int k) {
     return size_t(block_lin(g, i >> 2, j >> 2, k >> 2)) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3));
 }

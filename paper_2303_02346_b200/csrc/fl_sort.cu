@@ -2,7 +2,9 @@
 //
 // Block counting sort, device-driven (no host round trip):
 //   1. count particles per 4^3 particle block (inactive particles form a
-//      virtual block nbtot that sorts last, ordered by id)
+//      virtual block nbtot that sorts last, ordered by id; slots whose
+//      particle moved to another slab form a second one, nbtot + 1, that is
+//      listed after it and dropped by the next G2P)
 //   2. exclusive scan of the counts -> segment starts
 //   3. scatter (local cell, id, slot) into the block segments (arbitrary
 //      order inside a segment)
@@ -26,7 +28,7 @@ __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = st.key[i];
-    const int b = key == g.key_inactive ? g.nbtot : int(key >> 6);
+    const int b = key >= g.key_inactive ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
     // warp-aggregated: the store order is nearly sorted, so lanes share blocks
     const unsigned peers = __match_any_sync(__activemask(), b);
     const unsigned heavy = __ballot_sync(__activemask(), cls[meta_cls(st.meta[i])].heavy != 0) & peers;
@@ -48,8 +50,8 @@ __global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ b
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = st.key[i];
-    const bool inact = key == g.key_inactive;
-    const int b = inact ? g.nbtot : int(key >> 6);
+    const bool inact = key >= g.key_inactive;  // parked or departed
+    const int b = inact ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
     const unsigned peers = __match_any_sync(__activemask(), b);
     const int leader = __ffs(peers) - 1;
     const int lane = threadIdx.x & 31;
@@ -132,14 +134,18 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
     const int nl = n_blocks[0], nh = n_blocks[1];
     const int nb = nl + nh;
     const int tid = threadIdx.x;
-    for (int w = blockIdx.x; w <= nb; w += gridDim.x) {
+    for (int w = blockIdx.x; w <= nb + 1; w += gridDim.x) {
         // w < nb: active block (light ones, then heavy ones from the back of recs);
-        // w == nb: the inactive tail (ordered by id)
+        // w == nb: the inactive tail (ordered by id); w == nb + 1: departed slots (any order)
         const int q = w < nl ? w : cap - 1 - (w - nl);
         const bool act = w < nb;
-        const int cnt = act ? recs[q].end - recs[q].start : bcount[nbtot];
+        const int cnt = act ? recs[q].end - recs[q].start : bcount[nbtot + (w - nb)];
         if (cnt == 0) continue;
-        const int s0 = act ? recs[q].start : bstart[nbtot];
+        const int s0 = act ? recs[q].start : bstart[nbtot + (w - nb)];
+        if (w == nb + 1) {
+            for (int i = tid; i < cnt; i += kSortThreads) perm[s0 + i] = sslot[s0 + i];
+            continue;
+        }
         if (act && cnt <= kCountCap) {
             for (int i = tid; i < cnt; i += kSortThreads) {
                 ik[i] = skey[s0 + i];
@@ -211,11 +217,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
 
 void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s) {
+    if (n <= 0) return;  // (an empty slab)
     k_sort_count<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, cls, bcount, bheavy);
 }
 void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, const int* bcount,
                          const int* bheavy, int* bfill, uint32_t* skey, uint32_t* sslot, BlockRec* recs, int* n_blocks,
                          int* blockmap, int* nbflag, int cap, cudaStream_t s) {
+    if (n <= 0) return;
     k_sort_scatter<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, bstart, bcount, bheavy, bfill, skey, sslot, recs,
                                                    n_blocks, blockmap, nbflag, cap);
 }
