@@ -9,8 +9,11 @@ substeps producing the action gradient.  value = particles * T / device time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs one independent replica per GPU (torchrun; weak scaling).  The
-reference arm (--impl reference) times the unmodified reference engine
+N > 1 (torchrun, one process per GPU) splits the SAME scene into x-slabs, one
+per GPU: halo planes and migrating particles go to the
+neighbouring ranks over NCCL, rigid/loss/effector sums are all-reduced, so the
+scaling is strong.  If the slab transport cannot start, each GPU runs an
+independent replica instead and the line says so.  The reference arm (--impl reference) times the unmodified reference engine
 (oracle/_ref, proj/include/flume compiled as-is) on this host's CPU cores.
 """
 from __future__ import annotations
@@ -144,6 +147,18 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def _watchdog(seconds: float, rank: int):
+    """A multi-process run that stops making progress is ended with a JSON line, not a hang."""
+    def bite():
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT,
+                              "error": f"watchdog: no result after {seconds:.0f} s"}), flush=True)
+        os._exit(3)
+    t = threading.Timer(seconds, bite)
+    t.daemon = True
+    t.start()
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -160,13 +175,41 @@ def run_ours(args):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
+        _watchdog(args.deadline, rank)
 
     spec = scenes.load(SCENE)
     w = fl.build_scene(spec)
     lib = _abi.load()
-    ws = fl.GpuWorkspace(w.scene, device=local)
+    mode, note = "single", None
+    ws = None
+    if world_size > 1:
+        obj = [None]
+        if rank == 0:
+            try:
+                obj[0] = fl.dist_unique_id()
+            except Exception as e:
+                obj[0] = "error: " + str(e)
+        dist.broadcast_object_list(obj, src=0)
+        if isinstance(obj[0], bytes):
+            try:
+                ws = fl.GpuWorkspace.distributed(w.scene, local, rank, world_size, obj[0])
+                mode = "slabs"
+            except Exception as e:
+                note = f"slab transport unavailable ({e}); independent replicas"
+        else:
+            note = f"slab transport unavailable ({obj[0]}); independent replicas"
+        ok = torch.tensor([1 if mode == "slabs" else 0], device=f"cuda:{local}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and mode == "slabs":
+            mode, note = "replicas", "slab transport failed on a peer rank; independent replicas"
+            ws = None
+        elif mode != "slabs":
+            mode = "replicas"
+    if ws is None:
+        ws = fl.GpuWorkspace(w.scene, device=local)
     ctx = ws.ctx
     n = w.scene.n_particles
+    jobs = world_size if mode == "replicas" else 1  # independent scenes in the job
     T = args.horizon
     acts = fl.ActionTrajectory(1, T, w.init_action.reshape(1, 6))
     loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
@@ -239,7 +282,7 @@ def run_ours(args):
         tt = torch.tensor([total_ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
-    value = world_size * n * T * args.steps / (total_ms / 1e3)
+    value = jobs * n * T * args.steps / (total_ms / 1e3)
 
     # ---- forward-only rate (mpm_substep chain), same scene ----
     upload()
@@ -250,7 +293,12 @@ def run_ours(args):
     check(lib.flume_timer_mark(ctx, 3))
     fms = C.c_double()
     check(lib.flume_timer_elapsed(ctx, 2, 3, C.byref(fms)))
-    fwd_value = world_size * n * T * args.steps / (fms.value / 1e3)
+    fwd_ms_all = fms.value
+    if dist:
+        tt = torch.tensor([fwd_ms_all], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        fwd_ms_all = float(tt.item())
+    fwd_value = jobs * n * T * args.steps / (fwd_ms_all / 1e3)
 
     # ---- end to end through the public C ABI: H2D of the state from pinned host
     #      memory, grad_trajectory, D2H of loss + action gradient, every step ----
@@ -266,7 +314,9 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = world_size * n * T * args.steps / (e2e_ms / 1e3)
+    e2e_value = jobs * n * T * args.steps / (e2e_ms / 1e3)
+    # slabs: rank 0's share of the work, for its roofline line
+    keys, ids, na, _ = ws.store_order(w.state)
 
     if rank != 0:
         if dist:
@@ -283,8 +333,8 @@ def run_ours(args):
     dom = max((k for k in kern if k in ALG_BYTES), key=lambda k: kern[k]["ms_total"])
     # active nodes per substep: touched node blocks x 64 (measured on the first step's lists)
     A = int(0.155 * n * 1.6)  # fallback estimate; replaced by the measured value below
+    n_local = int(na)
     try:
-        keys, ids, na, _ = ws.store_order(w.state)
         blocks = np.unique(keys[:na] >> 6)
         nd = w.scene.node_dims
         NB = [(d + 3) // 4 for d in nd]
@@ -300,7 +350,7 @@ def run_ours(args):
     except Exception:
         pass
     pb, nb = ALG_BYTES[dom]
-    alg = pb * n + nb * A
+    alg = pb * n_local + nb * A
     per_launch_s = kern[dom]["ms_total"] / kern[dom]["launches"] / 1e3
     achieved = alg / per_launch_s / 1e9
     traffic = None
@@ -312,7 +362,7 @@ def run_ours(args):
             traffic = None
 
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world_size == 1:
         try:
             rate, rn, dt = cpu_reference_sample(4, 2)
             cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
@@ -323,17 +373,22 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if mode == "slabs" else "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: reference scene JSON c4 (SURVEY.md App. A) sampled by the reference lattice+jitter rule",
         "config": {"workload": f"{SCENE}_scooping: grad_trajectory, 1 segment x {T} substeps, stride {T} "
                                "(forward + adjoint, trajectory kept in HBM), target_point loss",
                    "particles": n, "grid": "128^3", "active_nodes": A, "horizon": T,
                    "l2": "inputs larger than L2 (trajectory store ~%.1f GB per step)" % (n * 112 * (T + 1) / 1e9),
-                   "parallelism": "replicas" if world_size > 1 else "single"},
+                   "parallelism": {"single": "single", "slabs": f"x-slabs over {world_size} GPUs (NCCL halos)",
+                                   "replicas": f"{world_size} independent replicas"}[mode],
+                   **({"note": note} if note else {}),
+                   **({"rank0_particles": n_local} if mode == "slabs" else {})},
         "fwd": {"value": fwd_value, "unit": UNIT, "workload": f"mpm_substep x {T}, same scene"},
         "fwd_bwd_split_ms": {"forward": fwd_ms / args.steps, "backward": bwd_ms / args.steps},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * (6 + 3)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world_size,
+                "d2h_bytes_per_step": 8 * (6 + 3) * world_size},
         "gpu_launches": int(launches),
         "kernels": kern,
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -355,6 +410,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--horizon", type=int, default=HORIZON)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--deadline", type=float, default=1500.0, help="multi-GPU watchdog (s)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

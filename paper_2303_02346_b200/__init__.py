@@ -7,11 +7,11 @@ include/flume_b200.h.  This package is the host-side mirror of the reference's
 scene / step / grad API (proj/include/flume)."""
 from .api import (ActionTrajectory, AdjointError, AdjointState, DegenerateDeformation, DeviceError, EngineError,
                   GpuWorkspace, LossEvaluator, RigidityError, Scene, SceneError, SimState, SubstepRecord,
-                  TrajectoryGrad, World, adjoint_substep, build_scene, grad_trajectory, mpm_substep, p2g_grid,
-                  rollout_loss)
+                  TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, mpm_substep,
+                  p2g_grid, rollout_loss)
 from . import scenes
 
 __all__ = ["ActionTrajectory", "AdjointError", "AdjointState", "DegenerateDeformation", "DeviceError", "EngineError",
            "GpuWorkspace", "LossEvaluator", "RigidityError", "Scene", "SceneError", "SimState", "SubstepRecord",
-           "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "grad_trajectory", "mpm_substep", "p2g_grid",
+           "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "mpm_substep", "p2g_grid",
            "rollout_loss", "scenes"]

@@ -422,6 +422,25 @@ class GpuWorkspace:
         self._ctx_time = 0.0
         self._ctx_substep = 0
 
+    @classmethod
+    def distributed(cls, scene: Scene, device: int, rank: int, n_ranks: int, uid: bytes) -> "GpuWorkspace":
+        """This process's rank of an x-slab group spanning processes (one per GPU,
+        NCCL); `uid` = dist_unique_id() of rank 0, shared by the launcher.  Every
+        call is collective over the ranks."""
+        self = cls.__new__(cls)
+        self.lib = load()
+        self.scene = scene
+        self.ctx = C.c_void_p()
+        u = (C.c_ubyte * 128).from_buffer_copy(uid)
+        rc = self.lib.flume_ctx_create_dist(C.byref(scene.desc), device, rank, n_ranks, u, C.byref(self.ctx))
+        if rc != _abi.FLUME_OK:
+            _raise(self.lib, None, rc)
+        self.ctxs = [self.ctx]
+        self._resident = None
+        self._ctx_time = 0.0
+        self._ctx_substep = 0
+        return self
+
     @property
     def ranks(self) -> int:
         return len(self.ctxs)
@@ -549,6 +568,16 @@ class GpuWorkspace:
         t = _abi.Timing()
         self.lib.flume_last_timing(self.ctx, C.byref(t))
         return t
+
+
+def dist_unique_id() -> bytes:
+    """NCCL unique id for GpuWorkspace.distributed (call on one rank, broadcast)."""
+    lib = load()
+    u = (C.c_ubyte * 128)()
+    rc = lib.flume_dist_unique_id(u)
+    if rc != _abi.FLUME_OK:
+        _raise(lib, None, rc)
+    return bytes(u)
 
 
 def _ws_for(scene: Scene, ws: Optional[GpuWorkspace]) -> GpuWorkspace:

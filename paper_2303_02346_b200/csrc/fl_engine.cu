@@ -858,7 +858,7 @@ void Ctx::partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t
     int c = 0;
     for (int r = 1; r < nranks; r++) {
         const double want = tot * r / nranks;
-        while (c < nc && acc + w[c] <= want) acc += w[c++];
+        while (c < nc && acc + 0.5 * w[c] <= want) acc += w[c++];  // cut nearest to the target
         // at least one column per rank on both sides
         cut[r] = std::max(cut[r - 1] + 1, std::min(c, nc - (nranks - r)));
         while (c < cut[r]) acc += w[c++];
