@@ -216,6 +216,9 @@ int flume_dist_unique_id(unsigned char uid[128]);
 int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, int n_ranks,
                           const unsigned char uid[128], flume_ctx** out);
 int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int* sx1, long* n_active);
+/* the column split every rank computes at upload: weights = active particles per
+ * 4-cell x column, cuts[n_ranks + 1] (host-only, no device needed) */
+int flume_slab_split(const double* col_weight, int n_cols, int n_ranks, int* cuts);
 
 /* ---- instrumentation ----
  * flume_profile: time every kernel class with CUDA events on the context stream.

@@ -570,6 +570,18 @@ class GpuWorkspace:
         return t
 
 
+def slab_split(col_weight, n_ranks: int) -> list:
+    """The x-column split of the slab ranks (flume_slab_split): rank r owns the
+    4-cell columns [cuts[r], cuts[r+1]).  Host-only."""
+    lib = load()
+    w = np.ascontiguousarray(col_weight, dtype=np.float64)
+    cuts = (C.c_int * (n_ranks + 1))()
+    rc = lib.flume_slab_split(_dp(w), int(w.size), int(n_ranks), cuts)
+    if rc != _abi.FLUME_OK:
+        raise ValueError("slab_split: need at least one column per rank")
+    return list(cuts)
+
+
 def dist_unique_id() -> bytes:
     """NCCL unique id for GpuWorkspace.distributed (call on one rank, broadcast)."""
     lib = load()

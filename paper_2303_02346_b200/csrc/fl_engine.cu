@@ -843,26 +843,31 @@ void Ctx::set_transport(std::unique_ptr<Transport> t) {
     CK(cudaStreamSynchronize(stream));
 }
 
-// Columns [sx0, sx1) per rank, balanced by active particle count; every rank
-// computes the same split from the same uploaded state.
-void Ctx::partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t>& active) {
-    const int nc = geom.NB[0];
-    std::vector<double> w(nc, 0.0);
-    for (size_t i = 0; i < keys.size(); i++)
-        if (active[i]) w[key_col(geom, keys[i])] += 1.0;
+// Columns [cut[r], cut[r+1]) per rank, cut nearest to equal weight, at least
+// one column each (flume_slab_split exposes it to the host tests).
+static void slab_split(const double* w, int nc, int nranks, int* cut) {
     double tot = 0;
-    for (double v : w) tot += v;
-    std::vector<int> cut(nranks + 1, 0);
+    for (int c = 0; c < nc; c++) tot += w[c];
+    cut[0] = 0;
     cut[nranks] = nc;
     double acc = 0;
     int c = 0;
     for (int r = 1; r < nranks; r++) {
         const double want = tot * r / nranks;
-        while (c < nc && acc + 0.5 * w[c] <= want) acc += w[c++];  // cut nearest to the target
-        // at least one column per rank on both sides
+        while (c < nc && acc + 0.5 * w[c] <= want) acc += w[c++];
         cut[r] = std::max(cut[r - 1] + 1, std::min(c, nc - (nranks - r)));
         while (c < cut[r]) acc += w[c++];
     }
+}
+
+// every rank computes the same split from the same uploaded state
+void Ctx::partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t>& active) {
+    const int nc = geom.NB[0];
+    std::vector<double> w(nc, 0.0);
+    for (size_t i = 0; i < keys.size(); i++)
+        if (active[i]) w[key_col(geom, keys[i])] += 1.0;
+    std::vector<int> cut(nranks + 1, 0);
+    slab_split(w.data(), nc, nranks, cut.data());
     geom.sx0 = cut[rank];
     geom.sx1 = cut[rank + 1];
 }
@@ -1679,6 +1684,12 @@ int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, in
         return rc;
     }
     *out = ctx;
+    return FLUME_OK;
+}
+
+int flume_slab_split(const double* col_weight, int n_cols, int n_ranks, int* cuts) {
+    if (!col_weight || !cuts || n_ranks < 1 || n_cols < n_ranks) return FLUME_E_ARG;
+    fl::slab_split(col_weight, n_cols, n_ranks, cuts);
     return FLUME_OK;
 }
 
