@@ -49,9 +49,19 @@ inline void check(flume_ctx* ctx, int rc) {
 // Device context for one Scene<3> (the MpmWorkspace<3> analogue).  The scene's
 // per-particle constants (material, body, mass, volume0, activation substep)
 // and effector shapes are taken from the state given at construction.
+// one rank of an x-slab group spanning processes (one per GPU, NCCL); uid from
+// flume_dist_unique_id() on rank 0, shared by the launcher.  Every gpu:: call on
+// such a workspace is collective over the ranks.
+struct SlabRank {
+    int rank = 0;
+    int n_ranks = 1;
+    const unsigned char* uid = nullptr;
+};
+
 class Workspace {
 public:
-    Workspace(const Scene<3>& scene, const SimState<3>& state, int device = 0) : scene_(&scene) {
+    Workspace(const Scene<3>& scene, const SimState<3>& state, int device = 0, const SlabRank* slab = nullptr)
+        : scene_(&scene) {
         const SimConfig<3>& c = scene.config;
         desc_.config.grid_resolution = c.grid_resolution;
         for (int a = 0; a < 3; a++) {
@@ -128,7 +138,10 @@ public:
         desc_.mass = mass_.data();
         desc_.volume0 = vol_.data();
         desc_.activation_substep = act_.data();
-        check(nullptr, flume_ctx_create(&desc_, device, &ctx_));
+        if (slab && slab->n_ranks > 1)
+            check(nullptr, flume_ctx_create_dist(&desc_, device, slab->rank, slab->n_ranks, slab->uid, &ctx_));
+        else
+            check(nullptr, flume_ctx_create(&desc_, device, &ctx_));
     }
     ~Workspace() { flume_ctx_destroy(ctx_); }
     Workspace(const Workspace&) = delete;
