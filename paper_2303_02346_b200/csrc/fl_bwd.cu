@@ -203,7 +203,7 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
 // G2P adjoint (adjoint.hpp:281-365): gather + deterministic scatter of grid v_bar
 // ---------------------------------------------------------------------------
 template <bool HEAVY>
-__global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : 3) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                         const BlockRec* __restrict__ recs,
                                                         const int* __restrict__ n_blocks,
                                                         const uint16_t* __restrict__ celltab,
@@ -569,7 +569,7 @@ void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const i
 // P2G adjoint (adjoint.hpp:414-470)
 // ---------------------------------------------------------------------------
 template <bool HEAVY>
-__global__ void __launch_bounds__(128, HEAVY ? 3 : 5) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                  const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                                  const ClassInfo* __restrict__ cls,
                                                  const float4* __restrict__ gridbar,

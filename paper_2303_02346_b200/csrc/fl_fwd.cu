@@ -173,7 +173,7 @@ void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaSt
 // ---------------------------------------------------------------------------
 
 template <bool HEAVY>
-__global__ void __launch_bounds__(kScThreads) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
                                                     const BlockRec* __restrict__ recs,
                                                     const int* __restrict__ n_blocks,
                                                     const uint16_t* __restrict__ celltab,
@@ -344,7 +344,7 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 // ---------------------------------------------------------------------------
 
 template <bool HEAVY>
-__global__ void __launch_bounds__(128, HEAVY ? 4 : 8) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
+__global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
                                              RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {

@@ -15,6 +15,20 @@
 namespace fl {
 
 constexpr int kScThreads = 192;  // 64 cells x 3 planes
+
+// resident CTAs per SM requested from ptxas for the plain-liquid variants (register caps)
+#ifndef FL_LB_P2G
+#define FL_LB_P2G 5
+#endif
+#ifndef FL_LB_G2P
+#define FL_LB_G2P 8
+#endif
+#ifndef FL_LB_ADJG2P
+#define FL_LB_ADJG2P 4
+#endif
+#ifndef FL_LB_ADJP2G
+#define FL_LB_ADJP2G 5
+#endif
 constexpr int kScR = 8;          // particle ranks per cell staged per pass (8 = ppc 2^3)
 constexpr int kCS = 68;          // rank stride = 4 (mod 32): conflict-free for 8 ranks x 4 cells and 32 cells
 constexpr int kPayF = 16;        // payload floats per particle
