@@ -436,25 +436,26 @@ __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __re
     return acc;
 }
 
-// NE = number of effectors (compile time).  Every thread accumulates the
-// effector bars of the nodes it processes in registers (fixed node order, since
-// the list partition is static), then one fixed-order CTA reduction per launch.
+// NE = number of effectors (compile time).  Effector bars: where any lane of a
+// warp touched effector e, the warp reduces the 18 components with a fixed
+// shuffle tree and lane 0 adds them to the warp's fp64 accumulator in shared
+// memory (static node order per warp, since the list partition is static), then
+// one fixed-order CTA reduction per launch.  Nothing effector-sized lives in
+// registers across nodes, which keeps the kernel at ~64 registers.
 template <int NE>
-__global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int* __restrict__ nb_list,
-                                                              const int* __restrict__ n_nb,
-                                                              const int* __restrict__ blockmap,
-                                                              const float4* __restrict__ staging_bar,
-                                                              const float4* __restrict__ gridv0, float4* gridbar,
-                                                              EffSet eff, double* eff_partial) {
-    __shared__ double red[kAdjGridThreads / 32][NE * kEffQ > 0 ? NE * kEffQ : 1];
+__global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const int* __restrict__ nb_list,
+                                                                 const int* __restrict__ n_nb,
+                                                                 const int* __restrict__ blockmap,
+                                                                 const float4* __restrict__ staging_bar,
+                                                                 const float4* __restrict__ gridv0, float4* gridbar,
+                                                                 EffSet eff, double* eff_partial) {
+    constexpr int kW = kAdjGridThreads / 32;
+    constexpr int kQ = NE * kEffQ > 0 ? NE * kEffQ : 1;
+    __shared__ double wacc[kW][kQ];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = tid >> 6, l = tid & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    float acc[NE > 0 ? NE : 1][kEffQ];
-#pragma unroll
-    for (int e = 0; e < (NE > 0 ? NE : 1); e++)
-#pragma unroll
-        for (int q = 0; q < kEffQ; q++) acc[e][q] = 0.f;
+    for (int q = lane; q < kQ; q += 32) wacc[warp][q] = 0.0;
     const int n = *n_nb;
     constexpr int kPer = kAdjGridThreads / 64;
     for (int k = blockIdx.x * kPer + sub; k < n; k += gridDim.x * kPer) {
@@ -467,8 +468,9 @@ __global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int*
         const float4 g0 = gridv0[idx];
         const float m = g0.w;
         const V3<float> v0 = {g0.x, g0.y, g0.z};
+        const bool live = m > g.mass_eps && (bar.x != 0.f || bar.y != 0.f || bar.z != 0.f);
         float pb0 = 0.f, pb1 = 0.f, pb2 = 0.f, mb = 0.f;
-        if (m > g.mass_eps && (bar.x != 0.f || bar.y != 0.f || bar.z != 0.f)) {
+        if (__any_sync(0xffffffffu, live)) {  // warp-uniform: the effector reductions need all lanes
             const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
             const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
             const V3<float> v1 = {v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
@@ -478,8 +480,10 @@ __global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int*
 #pragma unroll
             for (int e = 0; e < NE; e++) {
                 chain[e] = c;
-                c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
+                if (live) c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
             }
+            // ghost node column (bx == sx1): computed for this slab's gathers, counted by its owner
+            const bool owned = bx < g.sx1;
 #pragma unroll
             for (int e = NE - 1; e >= 0; e--) {
                 EffBars<float> eb;
@@ -488,44 +492,43 @@ __global__ void __launch_bounds__(kAdjGridThreads) k_adj_grid(Geom g, const int*
                 eb.vlin = eb.t;
                 eb.w = eb.t;
                 V3<float> in_bar = {0.f, 0.f, 0.f};
-                // ghost node column (bx == sx1): computed for this slab's gathers, counted by its owner
-                if (effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
-                                         in_bar, eb) &&
-                    bx < g.sx1) {
-                    acc[e][0] += eb.t.x; acc[e][1] += eb.t.y; acc[e][2] += eb.t.z;
+                bool hit = false;
+                if (live)
+                    hit = effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
+                                               in_bar, eb) &&
+                          owned;
+                if (__any_sync(0xffffffffu, hit)) {
+                    float vals[kEffQ] = {eb.t.x, eb.t.y, eb.t.z, eb.R.m[0], eb.R.m[1], eb.R.m[2], eb.R.m[3],
+                                         eb.R.m[4], eb.R.m[5], eb.R.m[6], eb.R.m[7], eb.R.m[8], eb.vlin.x,
+                                         eb.vlin.y, eb.vlin.z, eb.w.x, eb.w.y, eb.w.z};
 #pragma unroll
-                    for (int q = 0; q < 9; q++) acc[e][3 + q] += eb.R.m[q];
-                    acc[e][12] += eb.vlin.x; acc[e][13] += eb.vlin.y; acc[e][14] += eb.vlin.z;
-                    acc[e][15] += eb.w.x; acc[e][16] += eb.w.y; acc[e][17] += eb.w.z;
+                    for (int q = 0; q < kEffQ; q++) {
+                        float v = hit ? vals[q] : 0.f;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        if (lane == 0) wacc[warp][e * kEffQ + q] += double(v);
+                    }
                 }
-                bar = in_bar;
+                if (live) bar = in_bar;
             }
-            if (v2.x != v1.x) bar.x = 0.f;
-            if (v2.y != v1.y) bar.y = 0.f;
-            if (v2.z != v1.z) bar.z = 0.f;
-            const float inv = 1.0f / m;
-            pb0 = bar.x * inv;
-            pb1 = bar.y * inv;
-            pb2 = bar.z * inv;
-            mb = -dot(v0, bar) * inv;
+            if (live) {
+                if (v2.x != v1.x) bar.x = 0.f;
+                if (v2.y != v1.y) bar.y = 0.f;
+                if (v2.z != v1.z) bar.z = 0.f;
+                const float inv = 1.0f / m;
+                pb0 = bar.x * inv;
+                pb1 = bar.y * inv;
+                pb2 = bar.z * inv;
+                mb = -dot(v0, bar) * inv;
+            }
         }
         gridbar[idx] = make_float4(pb0, pb1, pb2, mb);
     }
-    // fixed-order CTA reduction: warp shuffle tree, then warps in index order
-#pragma unroll
-    for (int e = 0; e < NE; e++)
-#pragma unroll
-        for (int q = 0; q < kEffQ; q++) {
-            double v = double(acc[e][q]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-            if (lane == 0) red[warp][e * kEffQ + q] = v;
-        }
     __syncthreads();
     for (int q = tid; q < kMaxEff * kEffQ; q += kAdjGridThreads) {
         double s = 0.0;
         if (q < NE * kEffQ)
-            for (int w = 0; w < kAdjGridThreads / 32; w++) s += red[w][q];
+            for (int w = 0; w < kW; w++) s += wacc[w][q];
         eff_partial[size_t(blockIdx.x) * kMaxEff * kEffQ + q] = s;
     }
 }
