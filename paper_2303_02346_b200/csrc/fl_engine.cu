@@ -276,6 +276,7 @@ struct Ctx {
     int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr, *blockmap_p = nullptr,
         *list_cnt = nullptr;
     DevArr<int> nbpos;
+    DevArr<int4> tile_sum;
     DevArr<uint32_t> skey, sslot, gk, gv;
     DevArr<unsigned char> cub_tmp;
     size_t cub_bytes = 0;
@@ -552,6 +553,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     blockmap_p = bzero.p + 4 * bz;
     list_cnt = bzero.p + 5 * bz;
     nbpos.alloc(g.nbtot);
+    tile_sum.alloc(sort_list_tiles(g));
     bstart.alloc(g.nbtot + 2);
     skey.alloc(N);
     sslot.alloc(N);
@@ -805,11 +807,9 @@ void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     const int n = r.n_stored;
     CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
     launch_sort_count(g, st.p, n, d_cls.p, bcount, bheavy, stream);
-    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, bcount, bstart.p, g.nbtot + 2, stream));
-    launch_sort_scatter(g, st.p, n, bstart.p, bcount, bheavy, bfill, skey.p, sslot.p, r.recs, list_cnt, blockmap_p,
-                        nbflag, maxb, stream);
-    CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, g.nbtot, stream));
-    launch_nb_scatter(nbflag, nbpos.p, g.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
+    launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, blockmap_p, r.n_blocks,
+                      tile_sum.p, stream);
+    launch_sort_scatter(g, st.p, n, bstart.p, bfill, skey.p, sslot.p, stream);
     launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
                        grid_sort, stream);
     launches += 4;
@@ -1026,7 +1026,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         halo_exchange(staging.p, nbflag);
         // node-block list again, now with the blocks reached only by ghost tiles
         CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
-        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
+        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
         launches += 2;
     }
     PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0,
@@ -1088,7 +1088,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
     if (slab()) {
         halo_exchange(staging.p, nbflag);
         CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
-        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, list_cnt, r.n_blocks, stream);
+        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
     }
     launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0, es, stream);
     std::vector<float4> h(size_t(geom.nbtot) * 64);

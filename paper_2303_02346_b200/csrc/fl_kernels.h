@@ -116,9 +116,12 @@ void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* 
 
 void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s);
-void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, const int* bcount,
-                         const int* bheavy, int* bfill, uint32_t* skey, uint32_t* sslot, BlockRec* recs, int* n_blocks,
-                         int* blockmap, int* nbflag, int cap, cudaStream_t s);
+void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, int* bfill, uint32_t* skey,
+                         uint32_t* sslot, cudaStream_t s);
+int sort_list_tiles(const Geom& g);
+void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
+                       int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
+                       cudaStream_t s);
 void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, const int* cnt_scratch,
                        int* n_blocks, cudaStream_t s);
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,

@@ -5,7 +5,10 @@
 //      virtual block nbtot that sorts last, ordered by id; slots whose
 //      particle moved to another slab form a second one, nbtot + 1, that is
 //      listed after it and dropped by the next G2P)
-//   2. exclusive scan of the counts -> segment starts
+//   2. one CTA scans the counts -> segment starts, and in the same pass the
+//      node-block flags (from the counts of the 2x2x2 particle blocks below
+//      each node block), the node-block list and the particle-block list
+//      (plain-liquid blocks from the front, SVD/rigid blocks from the back)
 //   3. scatter (local cell, id, slot) into the block segments (arbitrary
 //      order inside a segment)
 //   4. one CTA per non-empty block sorts its segment by (local cell, id)
@@ -15,6 +18,9 @@
 // stable (key, id) sort -- the same order the CPU parity test recomputes.
 // The block count array doubles as the particle-block list for the kernels.
 #include <cuda_runtime.h>
+
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "fl_kernels.h"
 #include "fl_scatter.cuh"
@@ -39,14 +45,8 @@ __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict
     }
 }
 
-// Also builds the active particle-block list: the warp that claims a block's
-// first segment slot appends the block -- plain-liquid blocks from the front of
-// recs, SVD/rigid blocks from the back (n_blocks[0] / n_blocks[1] entries).
-// Slot assignment is run-dependent but no result depends on it.
-__global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ bstart,
-                               const int* __restrict__ bcount, const int* __restrict__ bheavy, int* bfill,
-                               uint32_t* skey, uint32_t* sslot, BlockRec* recs, int* n_blocks, int* blockmap,
-                               int* nbflag, int cap) {
+__global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ bstart, int* bfill, uint32_t* skey,
+                               uint32_t* sslot) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = st.key[i];
@@ -56,21 +56,7 @@ __global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ b
     const int leader = __ffs(peers) - 1;
     const int lane = threadIdx.x & 31;
     int base = 0;
-    if (lane == leader) {
-        base = atomicAdd(&bfill[b], __popc(peers));
-        if (base == 0 && !inact) {
-            const bool hv = bheavy[b] != 0;
-            const int q = hv ? cap - 1 - atomicAdd(&n_blocks[1], 1) : atomicAdd(&n_blocks[0], 1);
-            recs[q] = BlockRec{b, bstart[b], bstart[b] + bcount[b]};
-            blockmap[b] = q + 1;
-            int bx, by, bz;  // node blocks covered by this block's tile
-            block_unlin(g, b, bx, by, bz);
-            for (int d = 0; d < 8; d++) {
-                const int x = bx + (d >> 2), y = by + ((d >> 1) & 1), z = bz + (d & 1);
-                if (x < g.NB[0] && y < g.NB[1] && z < g.NB[2]) nbflag[block_lin(g, x, y, z)] = 1;
-            }
-        }
-    }
+    if (lane == leader) base = atomicAdd(&bfill[b], __popc(peers));
     base = __shfl_sync(peers, base, leader);
     const int p = bstart[b] + base + __popc(peers & ((1u << lane) - 1));
     skey[p] = ((inact ? 0u : (key & 63u)) << 26) | st.id[i];
@@ -220,12 +206,149 @@ void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cl
     if (n <= 0) return;  // (an empty slab)
     k_sort_count<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, cls, bcount, bheavy);
 }
-void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, const int* bcount,
-                         const int* bheavy, int* bfill, uint32_t* skey, uint32_t* sslot, BlockRec* recs, int* n_blocks,
-                         int* blockmap, int* nbflag, int cap, cudaStream_t s) {
+void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, int* bfill, uint32_t* skey,
+                         uint32_t* sslot, cudaStream_t s) {
     if (n <= 0) return;
-    k_sort_scatter<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, bstart, bcount, bheavy, bfill, skey, sslot, recs,
-                                                   n_blocks, blockmap, nbflag, cap);
+    k_sort_scatter<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, bstart, bfill, skey, sslot);
+}
+
+// ---------------------------------------------------------------------------
+// step 2: 4-channel scan over the nbtot + 2 block counts (particles, touched
+// node blocks, plain-liquid blocks, SVD/rigid blocks) in two passes of
+// 2048-block tiles: tile sums, then every tile adds its predecessors' sums
+// (<= a few hundred) and writes its outputs.  Deterministic, no atomics.
+// ---------------------------------------------------------------------------
+constexpr int kListThreads = 256;
+constexpr int kListItems = 8;  // consecutive blocks per thread
+constexpr int kListTile = kListThreads * kListItems;
+
+struct Sum4 {
+    __device__ __forceinline__ int4 operator()(const int4& a, const int4& b) const {
+        return make_int4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    }
+};
+
+// node block (x,y,z) is touched when any particle block (x-i, y-j, z-k), i,j,k in {0,1}, is occupied
+__device__ __forceinline__ int node_touched(const Geom& g, const int* __restrict__ bcount, int b) {
+    int x, y, z;
+    block_unlin(g, b, x, y, z);
+    int f = 0;
+#pragma unroll
+    for (int d = 0; d < 8; d++) {
+        const int xx = x - (d >> 2), yy = y - ((d >> 1) & 1), zz = z - (d & 1);
+        if (xx >= 0 && yy >= 0 && zz >= 0) f |= bcount[block_lin(g, xx, yy, zz)];
+    }
+    return f != 0;
+}
+
+// 1 = plain-liquid block, 2 = SVD/rigid block, 0 = empty (or a virtual block)
+__device__ __forceinline__ int block_kind(const Geom& g, const int* __restrict__ bcount,
+                                          const int* __restrict__ bheavy, int b) {
+    if (b >= g.nbtot || bcount[b] == 0) return 0;
+    return bheavy[b] != 0 ? 2 : 1;
+}
+
+__global__ void __launch_bounds__(kListThreads) k_list_sums(Geom g, const int* __restrict__ bcount,
+                                                            const int* __restrict__ bheavy, int* nbflag,
+                                                            int4* tile_sum) {
+    using Red = cub::BlockReduce<int4, kListThreads>;
+    __shared__ typename Red::TempStorage tmp;
+    const int n = g.nbtot + 2;
+    const int b0 = blockIdx.x * kListTile + threadIdx.x * kListItems;
+    int4 mine = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kListItems; k++) {
+        const int b = b0 + k;
+        if (b >= n) break;
+        mine.x += bcount[b];
+        if (b < g.nbtot) {
+            const int f = node_touched(g, bcount, b);
+            nbflag[b] = f;
+            mine.y += f;
+        }
+        const int kind = block_kind(g, bcount, bheavy, b);
+        mine.z += kind == 1;
+        mine.w += kind == 2;
+    }
+    const int4 tot = Red(tmp).Reduce(mine, Sum4());
+    if (threadIdx.x == 0) tile_sum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, const int* __restrict__ bcount,
+                                                             const int* __restrict__ bheavy,
+                                                             const int* __restrict__ nbflag,
+                                                             const int4* __restrict__ tile_sum, int* bstart,
+                                                             int* nb_list, int* n_nb, BlockRec* recs, int* blockmap,
+                                                             int* n_blocks) {
+    using Scan = cub::BlockScan<int4, kListThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int4 base;
+    const int n = g.nbtot + 2, tid = threadIdx.x;
+    if (tid < 32) {  // predecessors' tile sums: strided lanes + fixed shuffle tree
+        int4 s = make_int4(0, 0, 0, 0);
+        for (int t = tid; t < int(blockIdx.x); t += 32) s = Sum4()(s, tile_sum[t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s.x += __shfl_down_sync(0xffffffffu, s.x, o);
+            s.y += __shfl_down_sync(0xffffffffu, s.y, o);
+            s.z += __shfl_down_sync(0xffffffffu, s.z, o);
+            s.w += __shfl_down_sync(0xffffffffu, s.w, o);
+        }
+        if (tid == 0) base = s;
+    }
+    const int b0 = blockIdx.x * kListTile + tid * kListItems;
+    int cnt[kListItems], flag[kListItems], kind[kListItems];
+    int4 mine = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int k = 0; k < kListItems; k++) {
+        const int b = b0 + k;
+        cnt[k] = b < n ? bcount[b] : 0;
+        flag[k] = b < g.nbtot ? nbflag[b] : 0;
+        kind[k] = b < n ? block_kind(g, bcount, bheavy, b) : 0;
+        mine.x += cnt[k];
+        mine.y += flag[k];
+        mine.z += kind[k] == 1;
+        mine.w += kind[k] == 2;
+    }
+    int4 pre, tot;
+    Scan(tmp).ExclusiveScan(mine, pre, make_int4(0, 0, 0, 0), Sum4(), tot);
+    __syncthreads();
+    pre = Sum4()(pre, base);
+#pragma unroll
+    for (int k = 0; k < kListItems; k++) {
+        const int b = b0 + k;
+        if (b >= n) break;
+        bstart[b] = pre.x;
+        if (b < g.nbtot) {
+            if (flag[k]) nb_list[pre.y] = b;
+            int slot = 0;  // block-map convention: slot + 1, 0 = none
+            if (kind[k] == 1) slot = pre.z + 1;
+            if (kind[k] == 2) slot = cap - pre.w;  // SVD/rigid blocks fill recs from the back
+            if (slot) recs[slot - 1] = BlockRec{b, pre.x, pre.x + cnt[k]};
+            blockmap[b] = slot;
+        }
+        pre.x += cnt[k];
+        pre.y += flag[k];
+        pre.z += kind[k] == 1;
+        pre.w += kind[k] == 2;
+    }
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) {
+        const int4 all = Sum4()(base, tot);
+        *n_nb = all.y;
+        n_blocks[0] = all.z;
+        n_blocks[1] = all.w;
+    }
+}
+
+int sort_list_tiles(const Geom& g) { return (g.nbtot + 2 + kListTile - 1) / kListTile; }
+
+void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
+                       int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
+                       cudaStream_t s) {
+    const int tiles = sort_list_tiles(g);
+    k_list_sums<<<tiles, kListThreads, 0, s>>>(g, bcount, bheavy, nbflag, tile_sum);
+    k_list_write<<<tiles, kListThreads, 0, s>>>(g, cap, bcount, bheavy, nbflag, tile_sum, bstart, nb_list, n_nb,
+                                                recs, blockmap, n_blocks);
 }
 
 // compact, id-ordered list of touched node blocks
@@ -234,7 +357,7 @@ void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart
 __global__ void k_nb_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* list,
                              int* n_list, const int* __restrict__ cnt_scratch, int* n_blocks) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) {
+    if (i == 0 && cnt_scratch) {
         n_blocks[0] = cnt_scratch[0];
         n_blocks[1] = cnt_scratch[1];
     }
