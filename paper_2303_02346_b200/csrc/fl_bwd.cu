@@ -589,11 +589,13 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom 
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
+        uint32_t s_nx = r.start + tid < r.end ? perm[r.start + tid] : 0u;  // see k_g2p
         __syncthreads();
         load_tile(g, gridbar, bt, bx, by, bz, tid, 128);
         __syncthreads();
         for (int j = r.start + tid; j < r.end; j += 128) {
-            const uint32_t s = perm[j];
+            const uint32_t s = s_nx;
+            if (j + 128 < r.end) s_nx = perm[j + 128];
             const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
             const V3<float> v = {pre.v(0)[s], pre.v(1)[s], pre.v(2)[s]};
             const ClassInfo ci = cls[meta_cls(pre.meta[s])];

@@ -192,14 +192,17 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom 
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
         __syncthreads();
+        const int cnt = r.end - r.start;
+        uint32_t s_nx = tid < cnt ? perm[r.start + tid] : 0u;  // overlaps the cell-table barrier
         sc_tile_zero(sm, tid, kScThreads);
         const int npass = sc_load_cells(sm, celltab, b, tid);
-        const int cnt = r.end - r.start;
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
+            if (pass > 0) s_nx = tid < cnt ? perm[r.start + tid] : 0u;
             for (int i = tid; i < cnt; i += kScThreads) {
                 const int c = cell_of(sm.cs, i);
-                const uint32_t s = perm[r.start + i];
+                const uint32_t s = s_nx;
+                if (i + kScThreads < cnt) s_nx = perm[r.start + i + kScThreads];
                 const int rank = i - int(sm.cs[c]) - r0;
                 if (rank < 0 || rank >= kScR) continue;
                 float* pay = pay_slot(sm, rank, c);
@@ -358,11 +361,15 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
+        // the first permutation load overlaps the tile barrier; later ones run one
+        // particle ahead (the perm -> state loads are the kernel's latency chain)
+        uint32_t s_nx = r.start + tid < r.end ? perm[r.start + tid] : 0u;
         __syncthreads();
         load_tile(g, gridv, vt, bx, by, bz, tid, 128);
         __syncthreads();
         for (int j = r.start + tid; j < r.end; j += 128) {
-            const uint32_t s = perm[j];
+            const uint32_t s = s_nx;
+            if (j + 128 < r.end) s_nx = perm[j + 128];
             const V3<float> x = {in.x(0)[s], in.x(1)[s], in.x(2)[s]};
             const uint32_t meta = in.meta[s];
             const uint32_t pid = in.id[s];
