@@ -240,7 +240,10 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2
                 if (rank < 0 || rank >= kScR) continue;
                 float* pay = pay_slot(sm, rank, c);
                 const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
-                const ClassInfo ci = cls[meta_cls(pre.meta[s])];
+                const uint32_t pmeta = pre.meta[s];
+                const ClassInfo ci = cls[meta_cls(pmeta)];
+                const bool cin = !HEAVY || f_compact(ci, pmeta);  // pre-state F = c I
+                const bool cpost = !HEAVY || ci.iso;              // post-state F (and its bar) compact
                 StencilW sw;
                 stencil_weights(g, x, bx, by, bz, sw);
                 V3<float> vraw, vuse;
@@ -265,33 +268,37 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2
                         g2p_gather(g, vt, sw, vraw, cdummy);
                     }
                 }
-                M3<float> F;
-#pragma unroll
-                for (int k = 0; k < 9; k++) F.m[k] = pre.F(k)[s];
                 const M3<float> ipc = meye<float>() + cnew * g.dt;
-                const M3<float> ftr = ipc * F;
-                M3<float> fpost_bar, cin_bar;
+                M3<float> F;
+                if (cin) {
+                    F = meye<float>() * pre.F(0)[s];
+                } else {
 #pragma unroll
-                for (int k = 0; k < 9; k++) {
-                    fpost_bar.m[k] = post.F(k)[j];
-                    cin_bar.m[k] = post.C(k)[j];
+                    for (int k = 0; k < 9; k++) F.m[k] = pre.F(k)[s];
                 }
+                const M3<float> ftr = cin ? ipc * F.m[0] : ipc * F;
+                M3<float> cin_bar;
+#pragma unroll
+                for (int k = 0; k < 9; k++) cin_bar.m[k] = post.C(k)[j];
                 M3<float> ftr_bar;
-                if constexpr (HEAVY) {
+                if (cpost) {  // (viscous) liquid: only tr(F_post_bar) = dL/dc_post is stored
+                    ftr_bar = liquid_project_vjp_c(ftr, post.F(0)[j]);
+                } else {
+                    M3<float> fpost_bar;
+#pragma unroll
+                    for (int k = 0; k < 9; k++) fpost_bar.m[k] = post.F(k)[j];
                     switch (ci.kind) {
                         case MK_LIQUID:
-                        case MK_VISCOUS: ftr_bar = liquid_project_vjp(ftr, fpost_bar); break;
+                        case MK_VISCOUS: ftr_bar = liquid_project_vjp(ftr, fpost_bar); break;  // (rigid members)
                         case MK_PLASTIC: ftr_bar = box_yield_project_vjp(ftr, ci.theta_c, ci.theta_s, fpost_bar); break;
                         case MK_NONNEWTONIAN:
                             ftr_bar = von_mises_project_vjp(ftr, ci.sigma_y, ci.mu, fpost_bar);
                             break;
                         default: ftr_bar = fpost_bar; break;
                     }
-                } else {
-                    ftr_bar = liquid_project_vjp(ftr, fpost_bar);
                 }
                 const M3<float> fpre_bar = transpose(ipc) * ftr_bar;
-                const M3<float> c_bar = cin_bar + ftr_bar * transpose(F) * g.dt;
+                const M3<float> c_bar = cin ? cin_bar + ftr_bar * (F.m[0] * g.dt) : cin_bar + ftr_bar * transpose(F) * g.dt;
                 V3<float> xnb = {post.x(0)[j], post.x(1)[j], post.x(2)[j]};
                 if (!HEAVY || ci.rigid < 0) {
 #pragma unroll
@@ -364,8 +371,12 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2
                 xbar_tmp[j] = xb.x;
                 xbar_tmp[size_t(cap) + j] = xb.y;
                 xbar_tmp[2 * size_t(cap) + j] = xb.z;
+                if (cin) {  // dL/dc of the pre-state's F = c I
+                    Fbar_tmp[j] = trace(fpre_bar);
+                } else {
 #pragma unroll
-                for (int k = 0; k < 9; k++) Fbar_tmp[size_t(k) * cap + j] = fpre_bar.m[k];
+                    for (int k = 0; k < 9; k++) Fbar_tmp[size_t(k) * cap + j] = fpre_bar.m[k];
+                }
                 // scatter payload: w (v_raw_bar + k4 c_bar dx (o - fx))
                 const M3<float> bm = c_bar * kd;
                 const V3<float> f3 = {sw.fx[0], sw.fx[1], sw.fx[2]};
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2
             }
             __syncthreads();
             const int nr = min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR);
-            sc_accumulate<3>(sm, my_c, my_ox, nr);
+            sc_accumulate<3>(sm, my_c, my_ox, nr, tid, kScThreads);
             __syncthreads();
         }
         __syncthreads();
@@ -598,28 +609,36 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom 
             if (j + 128 < r.end) s_nx = perm[j + 128];
             const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
             const V3<float> v = {pre.v(0)[s], pre.v(1)[s], pre.v(2)[s]};
-            const ClassInfo ci = cls[meta_cls(pre.meta[s])];
+            const uint32_t pmeta = pre.meta[s];
+            const ClassInfo ci = cls[meta_cls(pmeta)];
+            const bool cin = !HEAVY || f_compact(ci, pmeta);     // F = c I, F_bar stored as dL/dc
+            const bool pressure = !HEAVY || (cin && ci.kind == MK_LIQUID);  // stress_mat = s(c) I
             M3<float> F, C;
 #pragma unroll
-            for (int k = 0; k < 9; k++) {
-                F.m[k] = pre.F(k)[s];
-                C.m[k] = pre.C(k)[s];
+            for (int k = 0; k < 9; k++) C.m[k] = pre.C(k)[s];
+            if (cin) {
+                F = meye<float>() * pre.F(0)[s];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; k++) F.m[k] = pre.F(k)[s];
             }
+            const float cc = g.stress_coeff * ci.vol0;
             const bool visc = HEAVY && ci.kind == MK_VISCOUS;
             const M3<float> ipc = meye<float>() + C * g.dt;
-            const M3<float> fs = visc ? ipc * F : F;
-            bool ok;
+            M3<float> fs, P, affine = C * ci.mass;
             Svd<float> t;
-            M3<float> P;
-            if constexpr (HEAVY) {
-                P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
+            if (pressure) {  // lambda (J - 1) J I with J = c^3
+                const float c = F.m[0], jj = c * c * c;
+                const float sm = ci.lambda * (jj - 1.f) * jj * cc;
+                affine.m[0] -= sm;
+                affine.m[4] -= sm;
+                affine.m[8] -= sm;
             } else {
-                const float jj = det(fs);
-                P = cofactor(fs) * (ci.lambda * (jj - 1.f));
+                fs = visc ? ipc * F : F;
+                bool ok;
+                P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
+                affine -= (P * transpose(fs)) * cc;
             }
-            const M3<float> smat = P * transpose(fs);
-            const float cc = g.stress_coeff * ci.vol0;
-            const M3<float> affine = C * ci.mass - smat * cc;
             StencilW sw;
             stencil_weights(g, x, bx, by, bz, sw);
             const V3<float> mv = v * ci.mass;
@@ -683,21 +702,27 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom 
             xb -= tmul(affine, wp);
             vbsum = wp * ci.mass;
             const M3<float> sm_bar = ab * (-cc);
-            const M3<float> p_bar = sm_bar * fs;
-            M3<float> fs_bar = transpose(sm_bar) * P;
-            if constexpr (HEAVY) {
-                fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
-            } else {
-                fs_bar += pressure_stress_vjp(fs, ci.lambda, p_bar);
-            }
             M3<float> Fb, Cb = ab * ci.mass;
-#pragma unroll
-            for (int k = 0; k < 9; k++) Fb.m[k] = Fbar_tmp[size_t(k) * cap + j];
-            if (visc) {
-                Fb += transpose(ipc) * fs_bar;
-                Cb += fs_bar * transpose(F) * g.dt;
+            float c_bar = 0.f;  // dL/dc for a compact F
+            if (pressure) {
+                // d/dc [lambda (c^6 - c^3)] tr(sm_bar) = 3 lambda c^2 (2J - 1) tr(sm_bar)
+                const float c = F.m[0], jj = c * c * c;
+                c_bar = Fbar_tmp[j] + 3.f * ci.lambda * c * c * (2.f * jj - 1.f) * trace(sm_bar);
             } else {
-                Fb += fs_bar;
+                const M3<float> p_bar = sm_bar * fs;
+                M3<float> fs_bar = transpose(sm_bar) * P;
+                fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
+                M3<float> fb_add = fs_bar;
+                if (visc) {
+                    fb_add = transpose(ipc) * fs_bar;
+                    Cb += fs_bar * transpose(F) * g.dt;
+                }
+                if (cin) {
+                    c_bar = Fbar_tmp[j] + trace(fb_add);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 9; k++) Fb.m[k] = Fbar_tmp[size_t(k) * cap + j] + fb_add.m[k];
+                }
             }
             const float xo[3] = {xbar_tmp[j] + xb.x, xbar_tmp[size_t(cap) + j] + xb.y,
                                  xbar_tmp[2 * size_t(cap) + j] + xb.z};
@@ -707,11 +732,14 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom 
                 out.v(a)[s] = vbsum[a];
             }
 #pragma unroll
-            for (int k = 0; k < 9; k++) {
-                out.F(k)[s] = Fb.m[k];
-                out.C(k)[s] = Cb.m[k];
+            for (int k = 0; k < 9; k++) out.C(k)[s] = Cb.m[k];
+            if (cin) {
+                out.F(0)[s] = c_bar;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; k++) out.F(k)[s] = Fb.m[k];
             }
-            if (!isfinite(xo[0]) || !isfinite(vbsum.x) || !isfinite(Fb.m[0])) atomicOr(nonfinite, 1);
+            if (!isfinite(xo[0]) || !isfinite(vbsum.x) || !isfinite(cin ? c_bar : Fb.m[0])) atomicOr(nonfinite, 1);
         }
     }
 }
@@ -779,11 +807,14 @@ void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out
 // ---------------------------------------------------------------------------
 // bars <-> reference (particle id) order
 // ---------------------------------------------------------------------------
+// reference-layout cotangents <-> store order; a compact F's cotangent is dL/dc = tr(F_bar)
 __global__ void k_bars_from_ref(BarBuf bars, PBuf st, int n, const double* xb, const double* vb, const double* Fb,
-                                const double* Cb) {
+                                const double* Cb, const ClassInfo* __restrict__ cls) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     size_t id = st.id[i];
+    const uint32_t meta = st.meta[i];
+    const bool cf = f_compact(cls[meta_cls(meta)], meta);
     for (int a = 0; a < 3; a++) {
         bars.x(a)[i] = float(xb[3 * id + a]);
         bars.v(a)[i] = float(vb[3 * id + a]);
@@ -792,32 +823,53 @@ __global__ void k_bars_from_ref(BarBuf bars, PBuf st, int n, const double* xb, c
         bars.F(k)[i] = float(Fb[9 * id + k]);
         bars.C(k)[i] = float(Cb[9 * id + k]);
     }
+    if (cf) bars.F(0)[i] = float(Fb[9 * id] + Fb[9 * id + 4] + Fb[9 * id + 8]);
 }
 
 void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb, const double* Fb,
-                          const double* Cb, cudaStream_t s) {
+                          const double* Cb, const ClassInfo* cls, cudaStream_t s) {
     if (n <= 0) return;
-    k_bars_from_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb);
+    k_bars_from_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb, cls);
 }
 
-__global__ void k_bars_to_ref(BarBuf bars, PBuf st, int n, double* xb, double* vb, double* Fb, double* Cb) {
+__global__ void k_bars_to_ref(BarBuf bars, PBuf st, int n, double* xb, double* vb, double* Fb, double* Cb,
+                              const ClassInfo* __restrict__ cls) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     size_t id = st.id[i];
+    const uint32_t meta = st.meta[i];
+    const bool cf = f_compact(cls[meta_cls(meta)], meta);
     for (int a = 0; a < 3; a++) {
         xb[3 * id + a] = bars.x(a)[i];
         vb[3 * id + a] = bars.v(a)[i];
     }
     for (int k = 0; k < 9; k++) {
-        Fb[9 * id + k] = bars.F(k)[i];
+        Fb[9 * id + k] = cf ? (k % 4 == 0 ? double(bars.F(0)[i]) / 3.0 : 0.0) : double(bars.F(k)[i]);
         Cb[9 * id + k] = bars.C(k)[i];
     }
 }
 
 void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* vb, double* Fb, double* Cb,
-                        cudaStream_t s) {
+                        const ClassInfo* cls, cudaStream_t s) {
     if (n <= 0) return;
-    k_bars_to_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb);
+    k_bars_to_ref<<<(n + 255) / 256, 256, 0, s>>>(bars, st, n, xb, vb, Fb, Cb, cls);
+}
+
+// adjoint_substep API: every compact F of the pre-state in full (kMetaFull), so
+// the substep's F cotangent comes out as the reference's full 3x3
+__global__ void k_expand_f(PBuf st, int n, const ClassInfo* __restrict__ cls) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t meta = st.meta[i];
+    if (!f_compact(cls[meta_cls(meta)], meta)) return;
+    const float c = st.F(0)[i];
+    for (int k = 1; k < 9; k++) st.F(k)[i] = k % 4 == 0 ? c : 0.f;
+    st.meta[i] = meta | kMetaFull;
+}
+
+void launch_expand_f(PBuf st, int n, const ClassInfo* cls, cudaStream_t s) {
+    if (n <= 0) return;
+    k_expand_f<<<(n + 255) / 256, 256, 0, s>>>(st, n, cls);
 }
 
 int occupancy_grid_fwd(KGrid which, bool heavy);

@@ -500,6 +500,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
             ci.body = p_body[i];
             ci.rigid = rigid_of_id[i];
             ci.heavy = (m.kind != MK_LIQUID || m.mu != 0.0 || rigid_of_id[i] >= 0) ? 1 : 0;
+            ci.iso = ((m.kind == MK_LIQUID || m.kind == MK_VISCOUS) && rigid_of_id[i] < 0) ? 1 : 0;
             ci.mass = float(p_mass[i]);
             ci.vol0 = float(p_vol0[i]);
             ci.mu = float(m.mu);
@@ -742,7 +743,8 @@ void Ctx::upload(const flume_state_view* view) {
     d_upmeta.upload(p_class, stream);
     d_upactive.upload(active, stream);
     StatePtr raw = get_state();
-    launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, stream);
+    launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, d_cls.p,
+                  stream);
     launches++;
     scratch_rec->n_active = n_active;
     scratch_rec->n_keep = n_active + n_parked();
@@ -775,10 +777,11 @@ void Ctx::download(flume_state_view* view) {
         // zeroed arrays; the all-reduce assembles the whole state on every rank
         for (int k = 0; k < 4; k++) CK(cudaMemsetAsync(d_up[k].p, 0, d_up[k].n * 8, stream));
         launch_download(cur->p, n_stored, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, rank == 0,
-                        geom.key_inactive, stream);
+                        geom.key_inactive, d_cls.p, stream);
         for (int k = 0; k < 4; k++) allreduce(d_up[k].p, size_t(N) * (k < 2 ? 3 : 9), DType::F64, ROp::Sum);
     } else {
-        launch_download(cur->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, 1, geom.key_inactive, stream);
+        launch_download(cur->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, 1, geom.key_inactive, d_cls.p,
+                        stream);
     }
     launch_download_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
     launches += 2;
@@ -1147,7 +1150,7 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
             d_up[0].alloc(size_t(N) * 3);
             if (slab()) CK(cudaMemsetAsync(d_up[0].p, 0, size_t(N) * 3 * 8, stream));
             launch_download(cur->p, n_stored, d_up[0].p, nullptr, nullptr, nullptr, rank == 0, geom.key_inactive,
-                            stream);
+                            d_cls.p, stream);
             if (slab()) allreduce(d_up[0].p, size_t(N) * 3, DType::F64, ROp::Sum);
             std::vector<double> hx(size_t(N) * 3);
             CK(cudaMemcpyAsync(hx.data(), d_up[0].p, hx.size() * 8, cudaMemcpyDeviceToHost, stream));
@@ -1512,6 +1515,7 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     const auto pend0 = pending;
     StatePtr pre = get_state(), post = get_state();
     copy_state(*pre, *cur);
+    launch_expand_f(pre->p, pre->n, d_cls.p, stream);  // full F cotangents out, like the reference
     RecordPtr rec = get_record();
     forward_substep(action, pre, post, *rec, false);
     const std::vector<EffState> eff_stage = eff;
@@ -1524,9 +1528,10 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     
     barsA.alloc(size_t(N) * 24);
     barsB.alloc(size_t(N) * 24);
-    launch_bars_from_ref(BarBuf{barsA.p, N}, post->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
+    launch_bars_from_ref(BarBuf{barsA.p, N}, post->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_cls.p,
+                         stream);
     adjoint_step(*pre, *post, *rec, barsA, barsB, 0);
-    launch_bars_to_ref(BarBuf{barsB.p, N}, pre->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, stream);
+    launch_bars_to_ref(BarBuf{barsB.p, N}, pre->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_cls.p, stream);
     CK(cudaMemcpyAsync(xb, d_up[0].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(vb, d_up[1].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(Fb, d_up[2].p, size_t(N) * 72, cudaMemcpyDeviceToHost, stream));

@@ -24,7 +24,8 @@ namespace fl {
 
 __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, const double* __restrict__ v,
                          const double* __restrict__ F, const double* __restrict__ C,
-                         const uint32_t* __restrict__ meta, const uint8_t* __restrict__ active) {
+                         const uint32_t* __restrict__ meta, const uint8_t* __restrict__ active,
+                         const ClassInfo* __restrict__ cls) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     for (int a = 0; a < 3; a++) {
@@ -35,7 +36,13 @@ __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, 
         raw.F(k)[i] = float(F[9 * size_t(i) + k]);
         raw.C(k)[i] = float(C[9 * size_t(i) + k]);
     }
-    raw.meta[i] = meta[i];
+    // the full F is stored; an isotropic-class particle whose F is not c I keeps
+    // it in full (kMetaFull) until its first G2P
+    bool isotropic = true;
+    for (int k = 0; k < 9; k++)
+        if (k % 4 != 0 && raw.F(k)[i] != 0.f) isotropic = false;
+    if (raw.F(4)[i] != raw.F(0)[i] || raw.F(8)[i] != raw.F(0)[i]) isotropic = false;
+    raw.meta[i] = meta[i] | ((cls[meta[i]].iso && !isotropic) ? kMetaFull : 0u);
     raw.id[i] = uint32_t(i);
     // active: 0 = parked (activates later), 1 = active here, 2 = active on another slab
     uint32_t key = g.key_inactive;
@@ -45,9 +52,10 @@ __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, 
 }
 
 void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
-                   const double* C, const uint32_t* meta, const uint8_t* active, cudaStream_t s) {
+                   const double* C, const uint32_t* meta, const uint8_t* active, const ClassInfo* cls,
+                   cudaStream_t s) {
     if (n <= 0) return;
-    k_upload<<<(n + 255) / 256, 256, 0, s>>>(g, raw, n, x, v, F, C, meta, active);
+    k_upload<<<(n + 255) / 256, 256, 0, s>>>(g, raw, n, x, v, F, C, meta, active, cls);
 }
 
 __global__ void k_make_sortkeys(PBuf st, int n, int idbits, uint64_t* ck, uint32_t* idx) {
@@ -81,26 +89,28 @@ void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t 
 // by particle id; departed slots are skipped, parked particles (replicated on
 // every slab) only where write_parked is set
 __global__ void k_download(PBuf st, int n, double* x, double* v, double* F, double* C, int write_parked,
-                           uint32_t key_inactive) {
+                           uint32_t key_inactive, const ClassInfo* __restrict__ cls) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = st.key[i];
     if (key > key_inactive || (key == key_inactive && !write_parked)) return;
     size_t id = st.id[i];
+    const uint32_t meta = st.meta[i];
+    const bool cf = f_compact(cls[meta_cls(meta)], meta);
     for (int a = 0; a < 3; a++) {
         if (x) x[3 * id + a] = double(st.x(a)[i]);
         if (v) v[3 * id + a] = double(st.v(a)[i]);
     }
     for (int k = 0; k < 9; k++) {
-        if (F) F[9 * id + k] = double(st.F(k)[i]);
+        if (F) F[9 * id + k] = cf ? (k % 4 == 0 ? double(st.F(0)[i]) : 0.0) : double(st.F(k)[i]);
         if (C) C[9 * id + k] = double(st.C(k)[i]);
     }
 }
 
 void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, int write_parked,
-                     uint32_t key_inactive, cudaStream_t s) {
+                     uint32_t key_inactive, const ClassInfo* cls, cudaStream_t s) {
     if (n <= 0) return;
-    k_download<<<(n + 255) / 256, 256, 0, s>>>(st, n, x, v, F, C, write_parked, key_inactive);
+    k_download<<<(n + 255) / 256, 256, 0, s>>>(st, n, x, v, F, C, write_parked, key_inactive, cls);
 }
 
 __global__ void k_rigid_x(PBuf st, int nmem, const int* member_id, double* x, int dir) {
@@ -221,28 +231,39 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom 
                     pay[0] = pay[kPayPlane] = pay[2 * kPayPlane] = 1.f;
                     continue;
                 }
-                const ClassInfo ci = cls[meta_cls(st.meta[s])];
-                M3<float> F, C;
+                const uint32_t meta = st.meta[s];
+                const ClassInfo ci = cls[meta_cls(meta)];
+                M3<float> C;
 #pragma unroll
-                for (int k = 0; k < 9; k++) {
-                    F.m[k] = st.F(k)[s];
-                    C.m[k] = st.C(k)[s];
-                }
+                for (int k = 0; k < 9; k++) C.m[k] = st.C(k)[s];
                 V3<float> v = {st.v(0)[s], st.v(1)[s], st.v(2)[s]};
-                M3<float> fs = F;
                 bool ok;
-                M3<float> P;
-                if constexpr (HEAVY) {
+                M3<float> affine = C * ci.mass;
+                if (!HEAVY || f_compact(ci, meta)) {
+                    const float c = st.F(0)[s];
+                    if (!HEAVY || ci.kind == MK_LIQUID) {
+                        // F = c I, mu = 0: stress_mat = P F^T = lambda (J - 1) J I, J = c^3
+                        const float j = c * c * c;
+                        ok = j > 0.f;
+                        const float sm = ci.lambda * (j - 1.f) * j * (g.stress_coeff * ci.vol0);
+                        affine.m[0] -= sm;
+                        affine.m[4] -= sm;
+                        affine.m[8] -= sm;
+                    } else {  // viscous liquid: Fs = (I + dt C) c
+                        const M3<float> fs = (meye<float>() + C * g.dt) * c;
+                        const M3<float> P = corotated_stress(fs, ci.mu, ci.lambda, ok);
+                        affine -= (P * transpose(fs)) * (g.stress_coeff * ci.vol0);
+                    }
+                } else {
+                    M3<float> F;
+#pragma unroll
+                    for (int k = 0; k < 9; k++) F.m[k] = st.F(k)[s];
+                    M3<float> fs = F;
                     if (ci.kind == MK_VISCOUS) fs = (meye<float>() + C * g.dt) * F;
-                    P = corotated_stress(fs, ci.mu, ci.lambda, ok);
-                } else {  // plain liquid: mu = 0, no polar decomposition
-                    const float j = det(fs);
-                    ok = j > 0.f;
-                    P = cofactor(fs) * (ci.lambda * (j - 1.f));
+                    const M3<float> P = corotated_stress(fs, ci.mu, ci.lambda, ok);
+                    affine -= (P * transpose(fs)) * (g.stress_coeff * ci.vol0);
                 }
                 if (!ok) atomicMin(err, (unsigned long long)pack_err(substep, ES_P2G_STRESS, st.id[s]));
-                M3<float> smat = P * transpose(fs);
-                M3<float> affine = C * ci.mass - smat * (g.stress_coeff * ci.vol0);
                 V3<float> f3 = {fx[0], fx[1], fx[2]};
                 V3<float> a = v * ci.mass - (affine * f3) * g.dx;
                 pay[0] = fx[0];
@@ -257,7 +278,7 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom 
             }
             __syncthreads();
             const int nr = min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR);
-            sc_accumulate<4>(sm, my_c, my_ox, nr);
+            sc_accumulate<4>(sm, my_c, my_ox, nr, tid, kScThreads);
             __syncthreads();
         }
         __syncthreads();
@@ -385,10 +406,16 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf
             V3<float> xn;
 #pragma unroll
             for (int a = 0; a < 3; a++) xn[a] = clamp_ref(x[a] + vuse[a] * g.dt, g.lo[a], g.hi[a]);
-            M3<float> F;
+            const bool cin = !HEAVY || f_compact(ci, meta);  // input F = c I
+            M3<float> ftr;
+            if (cin) {
+                ftr = (meye<float>() + cnew * g.dt) * in.F(0)[s];
+            } else {
+                M3<float> F;
 #pragma unroll
-            for (int k = 0; k < 9; k++) F.m[k] = in.F(k)[s];
-            const M3<float> ftr = (meye<float>() + cnew * g.dt) * F;
+                for (int k = 0; k < 9; k++) F.m[k] = in.F(k)[s];
+                ftr = (meye<float>() + cnew * g.dt) * F;
+            }
             M3<float> fnew = ftr;
             bool ok = true;
             if constexpr (HEAVY) {
@@ -409,9 +436,12 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf
                 out.v(a)[j] = vuse[a];
             }
 #pragma unroll
-            for (int k = 0; k < 9; k++) {
-                out.F(k)[j] = fnew.m[k];
-                out.C(k)[j] = cnew.m[k];
+            for (int k = 0; k < 9; k++) out.C(k)[j] = cnew.m[k];
+            if (!HEAVY || ci.iso) {  // projected to c I: compact store
+                out.F(0)[j] = fnew.m[0];
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; k++) out.F(k)[j] = fnew.m[k];
             }
             out.meta[j] = meta_cls(meta) | (vn > g.vmax ? kMetaCfl : 0u);
             out.id[j] = pid;

@@ -65,7 +65,8 @@ constexpr int kRigidChunk = 2048;
 
 // ---- forward ----
 void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
-                   const double* C, const uint32_t* meta, const uint8_t* active, cudaStream_t s);
+                   const double* C, const uint32_t* meta, const uint8_t* active, const ClassInfo* cls,
+                   cudaStream_t s);
 void launch_make_sortkeys(const Geom& g, const PBuf& st, int n, uint64_t* ck, uint32_t* idx, cudaStream_t s);
 void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
 void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap, cudaStream_t s);
@@ -83,7 +84,7 @@ void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* 
                   const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
                   uint32_t substep, cudaStream_t s);
 void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C, int write_parked,
-                     uint32_t key_inactive, cudaStream_t s);
+                     uint32_t key_inactive, const ClassInfo* cls, cudaStream_t s);
 void launch_download_rigid(PBuf st, int nmem, const int* member_id, double* x, cudaStream_t s);
 void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* x, cudaStream_t s);
 void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
@@ -110,9 +111,10 @@ void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_activ
                       cudaStream_t s);
 void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
 void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb,
-                          const double* Fb, const double* Cb, cudaStream_t s);
+                          const double* Fb, const double* Cb, const ClassInfo* cls, cudaStream_t s);
 void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* vb, double* Fb, double* Cb,
-                        cudaStream_t s);
+                        const ClassInfo* cls, cudaStream_t s);
+void launch_expand_f(PBuf st, int n, const ClassInfo* cls, cudaStream_t s);
 
 void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s);

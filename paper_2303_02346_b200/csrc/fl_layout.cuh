@@ -47,7 +47,9 @@ struct Geom {
 // class word of a particle: class index, plus bit 31 set by G2P when the CFL
 // clamp (mpm.hpp:322-328) was active in the substep that produced the state
 constexpr uint32_t kMetaCfl = 0x80000000u;
-__host__ __device__ inline uint32_t meta_cls(uint32_t m) { return m & 0x7fffffffu; }
+// bit 30: an isotropic-class particle whose F is not c*I yet (see f_compact)
+constexpr uint32_t kMetaFull = 0x40000000u;
+__host__ __device__ inline uint32_t meta_cls(uint32_t m) { return m & 0x3fffffffu; }
 
 // one entry per distinct (material, body, mass, volume0) tuple
 struct ClassInfo {
@@ -55,9 +57,22 @@ struct ClassInfo {
     int body;
     int rigid;   // rigid-body index or -1
     int heavy;   // needs the SVD / rigid code paths (anything but a plain liquid)
+    int iso;     // liquid / viscous liquid: the return map makes F = c I (materials.hpp:147-153)
     float mass, vol0;
     float mu, lambda, theta_c, theta_s, sigma_y;
 };
+
+// Compact deformation gradient.  The return map of (viscous) liquids resets F
+// to det(F)^(1/3) I every substep, so for those classes the store keeps only
+// c = F(0) (F(1..8) are not read or written) and the cotangent likewise only
+// dL/dc = tr(F_bar) -- exact, because every consumer of an isotropic F (the
+// stress, the trial F, liquid_project_vjp) depends on c alone.  This removes
+// 8 of the 24 state floats from every pass over a liquid particle.  A particle
+// uploaded with a non-isotropic F carries kMetaFull (full 3x3, heavy path)
+// until its first G2P.
+__host__ __device__ inline bool f_compact(const ClassInfo& ci, uint32_t meta) {
+    return ci.iso != 0 && (meta & kMetaFull) == 0u;
+}
 
 struct EffSet {
     int n;

@@ -293,6 +293,13 @@ FL_HD M3<T> liquid_project(const M3<T>& f, bool& ok) {
     ok = j > T(0);
     return meye<T>() * cbrt(j);
 }
+// the same with the output cotangent given compactly as dL/dc = tr(out_bar)
+template <class T>
+FL_HD M3<T> liquid_project_vjp_c(const M3<T>& f, T c_bar) {
+    T j = det(f);
+    return cofactor(f) * (c_bar * cbrt(j) / (T(3) * j));
+}
+
 template <class T>
 FL_HD M3<T> liquid_project_vjp(const M3<T>& f, const M3<T>& out_bar) {
     T j = det(f);

@@ -75,11 +75,13 @@ __device__ __forceinline__ void sc_tile_zero(ScSmem& sm, int tid, int nthreads) 
 }
 
 // Thread (cell c, plane ox) sums the 9 nodes (ox, oy, oz) over the particles of
-// cell c staged in this pass, in rank (= particle id) order, then folds them
-// into the tile in 27 ordered passes.  Must be reached by all threads.
+// cell c staged in this pass, in rank (= particle id) order; the partial sums
+// are then folded into the tile by sc_fold: they go to shared memory (reusing
+// the payload area) and every tile node gathers its <= 27 (cell, plane)
+// contributions in a fixed order.  Must be reached by all threads.
 // payload fields: [0..2] fx, then (NCH==4 ? m : -), a[3], Bm[9] row-major
 template <int NCH>
-__device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nrank) {
+__device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nrank, int tid, int nthreads) {
     constexpr int A0 = (NCH == 4) ? 4 : 3;
     float acc[9][4];
 #pragma unroll
@@ -125,18 +127,39 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
             }
         }
     }
-    const int cx = c >> 4, cy = (c >> 2) & 3, cz = c & 3;
+    // fold: partial sums -> shared memory -> per-node fixed-order gather
+    float4* part = reinterpret_cast<float4*>(sm.pay);  // [64 cells][3 planes][9 nodes]
+    __syncthreads();                                   // the payload has been read
 #pragma unroll
-    for (int px = 0; px < 3; px++) {
+    for (int k = 0; k < 9; k++) part[(c * 3 + ox) * 9 + k] = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
+    __syncthreads();
+    for (int t = tid; t < int(kTile); t += nthreads) {
+        const int X = t / 36, Y = (t / 6) % 6, Z = t % 6;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < 9; k++) {
-            __syncthreads();
-            if (px == ox) {
-                const int t = (cx + ox) * 36 + (cy + k / 3) * 6 + (cz + k % 3);
+        for (int px = 0; px < 3; px++) {
+            const int cx = X - px;
+            if (cx < 0 || cx > 3) continue;
 #pragma unroll
-                for (int q = 0; q < NCH; q++) sm.tile[q * kTile + t] += acc[k][q];
+            for (int py = 0; py < 3; py++) {
+                const int cy = Y - py;
+                if (cy < 0 || cy > 3) continue;
+#pragma unroll
+                for (int pz = 0; pz < 3; pz++) {
+                    const int cz = Z - pz;
+                    if (cz < 0 || cz > 3) continue;
+                    const float4 v = part[(((cx << 4) | (cy << 2) | cz) * 3 + px) * 9 + py * 3 + pz];
+                    s.x += v.x;
+                    s.y += v.y;
+                    s.z += v.z;
+                    s.w += v.w;
+                }
             }
         }
+        sm.tile[t] += s.x;
+        sm.tile[kTile + t] += s.y;
+        sm.tile[2 * kTile + t] += s.z;
+        sm.tile[3 * kTile + t] += s.w;
     }
 }
 

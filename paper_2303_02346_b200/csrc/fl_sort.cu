@@ -37,7 +37,9 @@ __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict
     const int b = key >= g.key_inactive ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
     // warp-aggregated: the store order is nearly sorted, so lanes share blocks
     const unsigned peers = __match_any_sync(__activemask(), b);
-    const unsigned heavy = __ballot_sync(__activemask(), cls[meta_cls(st.meta[i])].heavy != 0) & peers;
+    const uint32_t meta = st.meta[i];
+    const unsigned heavy =
+        __ballot_sync(__activemask(), cls[meta_cls(meta)].heavy != 0 || (meta & kMetaFull) != 0u) & peers;
     const int leader = __ffs(peers) - 1;
     if ((threadIdx.x & 31) == leader) {
         atomicAdd(&bcount[b], __popc(peers));
