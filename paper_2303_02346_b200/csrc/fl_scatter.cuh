@@ -211,34 +211,42 @@ __device__ __forceinline__ void stencil_weights(const Geom& g, V3<float> x, int 
     }
 }
 
-// v = sum w gv, C = (4/dx^2) sum w gv rel^T with rel = dx (o - fx)  (mpm.hpp:352-361)
+// v = sum w gv, C = (4/dx^2) sum w gv rel^T with rel = dx (o - fx)  (mpm.hpp:352-361).
+// Factored per axis around the middle node: with u = o - 1 in {-1,0,1} and
+// f = fx - 1, sum_o w gv (o - fx)_a = M_a - v f_a where M_a = sum_o w gv u_a is
+// built up z -> y -> x (~260 FMAs instead of ~430 for the 27-node product).
 __device__ __forceinline__ void g2p_gather(const Geom& g, const float4* tile, const StencilW& s, V3<float>& v,
                                            M3<float>& c) {
-    v = V3<float>{0.f, 0.f, 0.f};
-    c = mzero<float>();
-    const float kd = g.k4 * g.dx;
+    V3<float> mx = {0.f, 0.f, 0.f}, my = mx, mz = mx;
+    v = mx;
 #pragma unroll
     for (int ox = 0; ox < 3; ox++) {
-        const float rx = (float(ox) - s.fx[0]) * kd;
+        V3<float> bv = {0.f, 0.f, 0.f}, by = bv, bz = bv;
 #pragma unroll
         for (int oy = 0; oy < 3; oy++) {
-            const float ry = (float(oy) - s.fx[1]) * kd;
-            const float wxy = s.w[0][ox] * s.w[1][oy];
-#pragma unroll
-            for (int oz = 0; oz < 3; oz++) {
-                const float rz = (float(oz) - s.fx[2]) * kd;
-                const float w = wxy * s.w[2][oz];
-                const float4 gv = tile[(s.l[0] + ox) * 36 + (s.l[1] + oy) * 6 + (s.l[2] + oz)];
-                const float wx = w * gv.x, wy = w * gv.y, wz = w * gv.z;
-                v.x += wx;
-                v.y += wy;
-                v.z += wz;
-                c.m[0] += wx * rx; c.m[1] += wx * ry; c.m[2] += wx * rz;
-                c.m[3] += wy * rx; c.m[4] += wy * ry; c.m[5] += wy * rz;
-                c.m[6] += wz * rx; c.m[7] += wz * ry; c.m[8] += wz * rz;
-            }
+            const float4* row = tile + (s.l[0] + ox) * 36 + (s.l[1] + oy) * 6 + s.l[2];
+            const float4 g0 = row[0], g1 = row[1], g2 = row[2];
+            const V3<float> a = {s.w[2][0] * g0.x + s.w[2][1] * g1.x + s.w[2][2] * g2.x,
+                                 s.w[2][0] * g0.y + s.w[2][1] * g1.y + s.w[2][2] * g2.y,
+                                 s.w[2][0] * g0.z + s.w[2][1] * g1.z + s.w[2][2] * g2.z};
+            const V3<float> az = {s.w[2][2] * g2.x - s.w[2][0] * g0.x, s.w[2][2] * g2.y - s.w[2][0] * g0.y,
+                                  s.w[2][2] * g2.z - s.w[2][0] * g0.z};
+            const float wy = s.w[1][oy];
+            bv += a * wy;
+            if (oy != 1) by += a * (oy == 0 ? -wy : wy);
+            bz += az * wy;
         }
+        const float wx = s.w[0][ox];
+        v += bv * wx;
+        if (ox != 1) mx += bv * (ox == 0 ? -wx : wx);
+        my += by * wx;
+        mz += bz * wx;
     }
+    const float kd = g.k4 * g.dx;
+    const float f0 = s.fx[0] - 1.f, f1 = s.fx[1] - 1.f, f2 = s.fx[2] - 1.f;
+    c.m[0] = (mx.x - v.x * f0) * kd; c.m[1] = (my.x - v.x * f1) * kd; c.m[2] = (mz.x - v.x * f2) * kd;
+    c.m[3] = (mx.y - v.y * f0) * kd; c.m[4] = (my.y - v.y * f1) * kd; c.m[5] = (mz.y - v.y * f2) * kd;
+    c.m[6] = (mx.z - v.z * f0) * kd; c.m[7] = (my.z - v.z * f1) * kd; c.m[8] = (mz.z - v.z * f2) * kd;
 }
 
 // wall band (mpm.hpp:290-299): zero the inward component near each face
