@@ -32,7 +32,7 @@ constexpr int kScThreads = 192;  // 64 cells x 3 planes
 constexpr int kScR = 8;          // particle ranks per cell staged per pass (8 = ppc 2^3)
 constexpr int kCS = 68;          // rank stride = 4 (mod 32): conflict-free for 8 ranks x 4 cells and 32 cells
 constexpr int kPayF = 16;        // payload floats per particle
-constexpr int kCellTab = 66;     // per block: 64 cell starts + end (+pad), u16
+constexpr int kCellTab = 66;     // per block: 64 cell starts, end, largest cell count (u16)
 
 // Payload staged as pay[f][rank][cell]: the payload phase (lanes = consecutive
 // particles of a cell, consecutive ranks) and the accumulate phase (lanes =
@@ -163,16 +163,12 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
     }
 }
 
-// load the block's cell table; returns the pass count ceil(max cell count / kScR)
+// load the block's cell table (64 cell starts, end, largest cell count); returns
+// the pass count ceil(max cell count / kScR)
 __device__ __forceinline__ int sc_load_cells(ScSmem& sm, const uint16_t* __restrict__ celltab, int slot, int tid) {
     if (tid < kCellTab) sm.cs[tid] = celltab[size_t(slot) * kCellTab + tid];
     __syncthreads();
-    int mx = 0;
-    for (int c = 0; c < 64; c++) {
-        int n = int(sm.cs[c + 1]) - int(sm.cs[c]);
-        mx = n > mx ? n : mx;
-    }
-    return (mx + kScR - 1) / kScR;
+    return (int(sm.cs[65]) + kScR - 1) / kScR;
 }
 
 __device__ __forceinline__ void sc_tile_store(const ScSmem& sm, float4* out, int tid, int nthreads) {

@@ -156,7 +156,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
                 cs[2 * tid + 1] = uint16_t(ex + a);
                 fill[2 * tid] = ex;
                 fill[2 * tid + 1] = ex + a;
-                if (tid == 31) cs[64] = uint16_t(incl);
+                int mx = a > b ? a : b;  // largest cell: the scatter kernels' pass count
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int t = __shfl_xor_sync(0xffffffffu, mx, o);
+                    mx = t > mx ? t : mx;
+                }
+                if (tid == 31) {
+                    cs[64] = uint16_t(incl);
+                    cs[65] = uint16_t(mx);
+                }
             }
             __syncthreads();
             for (int i = tid; i < cnt; i += kSortThreads) {
@@ -179,7 +188,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
                     ov[j + 1] = vv;
                 }
             }
-            if (tid < kCellTab) celltab[size_t(q) * kCellTab + tid] = tid <= 64 ? cs[tid] : 0;
+            if (tid < kCellTab) celltab[size_t(q) * kCellTab + tid] = cs[tid];
             __syncthreads();
             for (int i = tid; i < cnt; i += kSortThreads) perm[s0 + i] = ov[i];
             __syncthreads();
@@ -199,6 +208,11 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
             for (int i = tid; i < cnt; i += kSortThreads) perm[s0 + i] = v[i];
             if (ct) cell_starts(k, cnt, ct, tid);
             __syncthreads();
+            if (ct && tid == 0) {
+                int mx = 0;
+                for (int c = 0; c < 64; c++) mx = max(mx, int(ct[c + 1]) - int(ct[c]));
+                ct[65] = uint16_t(mx);
+            }
         }
     }
 }
