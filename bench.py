@@ -61,47 +61,62 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region
+    (one nvidia-smi process in loop mode, -lms 50)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.samples = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
 
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                f = [s.strip() for s in out.stdout.strip().split(",")]
-                if len(f) == 6:
-                    self.samples.append(f)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _reader(self):
+        for line in self._p.stdout:
+            f = [s.strip() for s in line.strip().split(",")]
+            if len(f) == 6:
+                self.samples.append((time.perf_counter(), f))
+
+    def mark(self, which):
+        setattr(self, "t_" + which, time.perf_counter())
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
         if self._t:
-            self._t.join(timeout=6)
+            self._t.join(timeout=5)
 
     def summary(self):
-        if not self.samples:
+        """Samples that arrived inside the timed window (marks 'start'/'end'); if the
+        window was shorter than the sampling period, the ones within 0.25 s of it."""
+        t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_end", 1e30)
+        win = [f for t, f in self.samples if t0 <= t <= t1 + 0.06]
+        near = win or [f for t, f in self.samples if t0 - 0.25 <= t <= t1 + 0.25]
+        if not near:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in near if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in near if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        reasons = sorted({names[k] for s in near for k in range(4) if s[2 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(near), "samples_in_window": len(win)}
 
 
 def cpu_reference_sample(substeps: int = 4, stride: int = 2):
@@ -248,19 +263,22 @@ def run_ours(args):
         check(lib.flume_substep(ctx, _dp(w.init_action), T))
 
     upload()
-    for _ in range(args.warmup):
-        step()
-    if dist:
-        dist.barrier()
-    check(lib.flume_sync(ctx))
-
-    # ---- timed: device time over exactly K steps (inputs resident in HBM) ----
-    launches = 0
-    fwd_ms = bwd_ms = 0.0
+    # the clock sampler runs from the warm-up on; its summary keeps the samples
+    # that arrived inside the timed window
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step()
+        if dist:
+            dist.barrier()
+        check(lib.flume_sync(ctx))
+
+        # ---- timed: device time over exactly K steps (inputs resident in HBM) ----
+        launches = 0
+        fwd_ms = bwd_ms = 0.0
+        clocks.mark("start")
         check(lib.flume_timer_mark(ctx, 0))
         for _ in range(args.steps):
-            step()
+            step()  # synchronous: returns the loss and gradient in host memory
             t = ws.last_timing()
             launches += t.launches
             fwd_ms += t.forward_ms
@@ -268,6 +286,7 @@ def run_ours(args):
         check(lib.flume_timer_mark(ctx, 1))
         ms = C.c_double()
         check(lib.flume_timer_elapsed(ctx, 0, 1, C.byref(ms)))
+        clocks.mark("end")
     total_ms = ms.value
     # ---- per-kernel CUDA-event times: a separate instrumented pass of the same K steps
     #      (event bookkeeping on the host would otherwise perturb the timed region) ----
