@@ -29,7 +29,10 @@ constexpr int kScThreads = 192;  // 64 cells x 3 planes
 #ifndef FL_LB_ADJP2G
 #define FL_LB_ADJP2G 5
 #endif
-constexpr int kScR = 8;          // particle ranks per cell staged per pass (8 = ppc 2^3)
+#ifndef FL_SCR
+#define FL_SCR 8
+#endif
+constexpr int kScR = FL_SCR;     // particle ranks per cell staged per pass (8 = ppc 2^3)
 constexpr int kCS = 68;          // rank stride = 4 (mod 32): conflict-free for 8 ranks x 4 cells and 32 cells
 constexpr int kPayF = 16;        // payload floats per particle
 constexpr int kCellTab = 66;     // per block: 64 cell starts, end, largest cell count (u16)
