@@ -11,7 +11,7 @@ from pathlib import Path
 CLASS = {"k_p2g": "p2g", "k_grid_update": "grid_update", "k_g2p": "g2p", "k_adj_g2p": "g2p_adjoint",
          "k_adj_grid": "grid_adjoint", "k_eff_final": "grid_adjoint", "k_adj_p2g": "p2g_adjoint",
          "k_sort_count": "sort", "k_sort_scatter": "sort", "k_sort_blocks": "sort", "k_nb_scatter": "sort",
-         "DeviceScan": "sort"}
+         "DeviceScan": "sort", "k_list_sums": "sort", "k_list_write": "sort"}
 
 
 def main(path, out_json):
