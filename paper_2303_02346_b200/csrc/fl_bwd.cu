@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
                                                                  const int* __restrict__ blockmap,
                                                                  const float4* __restrict__ staging_bar,
                                                                  const float4* __restrict__ gridv0, float4* gridbar,
-                                                                 EffSet eff, double* eff_partial) {
+                                                                 EffSet eff, double* eff_partial,
+                                                                 const uint8_t* __restrict__ cmask) {
     constexpr int kW = kAdjGridThreads / 32;
     constexpr int kQ = NE * kEffQ > 0 ? NE * kEffQ : 1;
     __shared__ double wacc[kW][kQ];
@@ -480,6 +481,9 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
         const float m = g0.w;
         const V3<float> v0 = {g0.x, g0.y, g0.z};
         const bool live = m > g.mass_eps && (bar.x != 0.f || bar.y != 0.f || bar.z != 0.f);
+        // effectors in contact range of this node, recorded by the forward grid update:
+        // the others are pass-throughs and cost no SDF evaluation here
+        const uint32_t cm = live ? uint32_t(cmask[idx]) : 0u;
         float pb0 = 0.f, pb1 = 0.f, pb2 = 0.f, mb = 0.f;
         if (__any_sync(0xffffffffu, live)) {  // warp-uniform: the effector reductions need all lanes
             const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
 #pragma unroll
             for (int e = 0; e < NE; e++) {
                 chain[e] = c;
-                if (live) c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
+                if ((cm >> e) & 1u) c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
             }
             // ghost node column (bx == sx1): computed for this slab's gathers, counted by its owner
             const bool owned = bx < g.sx1;
@@ -502,12 +506,14 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
                 eb.R = mzero<float>();
                 eb.vlin = eb.t;
                 eb.w = eb.t;
-                V3<float> in_bar = {0.f, 0.f, 0.f};
+                V3<float> in_bar = bar;  // pass-through unless in contact
                 bool hit = false;
-                if (live)
+                if ((cm >> e) & 1u) {
+                    in_bar = V3<float>{0.f, 0.f, 0.f};
                     hit = effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
                                                in_bar, eb) &&
                           owned;
+                }
                 if (__any_sync(0xffffffffu, hit)) {
                     float vals[kEffQ] = {eb.t.x, eb.t.y, eb.t.z, eb.R.m[0], eb.R.m[1], eb.R.m[2], eb.R.m[3],
                                          eb.R.m[4], eb.R.m[5], eb.R.m[6], eb.R.m[7], eb.R.m[8], eb.vlin.x,
@@ -563,18 +569,18 @@ __global__ void __launch_bounds__(256) k_eff_final(const double* partial, int nb
 
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, double* eff_out, cudaStream_t s) {
+                     double* eff_partial, double* eff_out, const uint8_t* cmask, cudaStream_t s) {
     switch (eff.n) {
         case 0: k_adj_grid<0><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial); break;
+                                                                     gridbar, eff, eff_partial, cmask); break;
         case 1: k_adj_grid<1><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial); break;
+                                                                     gridbar, eff, eff_partial, cmask); break;
         case 2: k_adj_grid<2><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial); break;
+                                                                     gridbar, eff, eff_partial, cmask); break;
         case 3: k_adj_grid<3><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial); break;
+                                                                     gridbar, eff, eff_partial, cmask); break;
         default: k_adj_grid<kMaxEff><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar,
-                                                                            gridv0, gridbar, eff, eff_partial);
+                                                                            gridv0, gridbar, eff, eff_partial, cmask);
     }
     if (eff.n > 0) k_eff_final<<<eff.n * kEffQ, 256, 0, s>>>(eff_partial, kEffBlocks, eff_out);
 }

@@ -81,6 +81,7 @@ struct Record {
     uint16_t* celltab = nullptr;
     float4* gridv = nullptr;   // grid velocity after contact (G2P input), dense block-major
     float4* gridv0 = nullptr;  // (p/m, m) before gravity/walls/contact (grid-update adjoint input)
+    uint8_t* cmask = nullptr;  // per node: effectors within contact range (bit e)
     int n_active = 0;
     int n_keep = 0;    // active + parked slots of the pre-state (= N on one rank)
     int n_stored = 0;  // all slots of the pre-state, departed holes included
@@ -106,7 +107,7 @@ struct Record {
                o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 32),
                o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),
                o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4)),
-               o_mig = carve(size_t(2) * migcap * 4);
+               o_mig = carve(size_t(2) * migcap * 4), o_cm = carve(size_t(nbtot) * 64);
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -123,6 +124,7 @@ struct Record {
         gridv = reinterpret_cast<float4*>(b + o_gv);
         gridv0 = reinterpret_cast<float4*>(b + o_gv0);
         mig_src = migcap > 0 ? reinterpret_cast<uint32_t*>(b + o_mig) : nullptr;
+        cmask = reinterpret_cast<uint8_t*>(b + o_cm);
         mig_cap = migcap;
         CK(cudaMemset(gridv, 0, size_t(nbtot) * 64 * sizeof(float4)));
         CK(cudaMemset(gridv0, 0, size_t(nbtot) * 64 * sizeof(float4)));
@@ -1033,7 +1035,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         launches += 2;
     }
     PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0,
-                                    r.effk, stream));
+                                    r.effk, r.cmask, stream));
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
         CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
@@ -1093,7 +1095,8 @@ void Ctx::stage_grid(double* mass, double* vel) {
         CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
         launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
     }
-    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0, es, stream);
+    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0, es, r.cmask,
+                       stream);
     std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
     CK(cudaMemcpyAsync(h.data(), r.gridv, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
@@ -1253,7 +1256,8 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
          }));
     if (slab()) halo_exchange(staging_bar.p, nullptr);
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap_p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                     eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, stream));
+                                     eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, r.cmask,
+                                     stream));
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv, w, s);

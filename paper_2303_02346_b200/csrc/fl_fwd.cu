@@ -332,7 +332,7 @@ __device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __res
 __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restrict__ nb_list,
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
-                                                     EffSet eff) {
+                                                     EffSet eff, uint8_t* cmask) {
     const int n = *n_nb;
     const int sub = threadIdx.x >> 6, l = threadIdx.x & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
         const float m = mp.x;
         const size_t idx = size_t(nbid) * 64 + l;
         V3<float> v0 = {0.f, 0.f, 0.f}, v = {0.f, 0.f, 0.f};
+        uint32_t hits = 0;  // effectors within contact range of this node (the adjoint skips the rest)
         if (m > g.mass_eps) {
             const float inv = 1.0f / m;
             v0 = V3<float>{mp.y * inv, mp.z * inv, mp.w * inv};
@@ -351,16 +352,22 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
             const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
             v = wall_bc_dev(g, i, j, kk, v);
             const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
-            for (int e = 0; e < eff.n; e++) v = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, v);
+            for (int e = 0; e < eff.n; e++) {
+                bool hit;
+                v = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, v, &hit);
+                hits |= uint32_t(hit) << e;
+            }
         }
         gridv[idx] = make_float4(v.x, v.y, v.z, m);
         if (gridv0) gridv0[idx] = make_float4(v0.x, v0.y, v0.z, m);
+        if (cmask) cmask[idx] = uint8_t(hits);
     }
 }
 
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
-                        const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, cudaStream_t s) {
-    k_grid_update<<<grid, 256, 0, s>>>(g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff);
+                        const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
+                        cudaStream_t s) {
+    k_grid_update<<<grid, 256, 0, s>>>(g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask);
 }
 
 // ---------------------------------------------------------------------------

@@ -75,9 +75,11 @@ template <class T> FL_HD T contact_alpha_deriv(T d, bool hard) {
 
 // mpm.hpp:146-161
 template <class T>
-FL_HD V3<T> effector_contact(const EffK<T>& e, T inv_dx, T eps_cells, bool hard, V3<T> p, V3<T> v_in) {
+FL_HD V3<T> effector_contact(const EffK<T>& e, T inv_dx, T eps_cells, bool hard, V3<T> p, V3<T> v_in,
+                             bool* hit = nullptr) {
     SdfSample<T> s = sdf_eval(e.shape, e.wt, e.wR, p);
     T d = s.distance * inv_dx;
+    if (hit) *hit = d < eps_cells;
     if (d >= eps_cells) return v_in;
     V3<T> r = p - e.pt;
     V3<T> ve = e.vlin + cross(e.wang, r);
