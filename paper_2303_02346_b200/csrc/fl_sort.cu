@@ -235,7 +235,10 @@ void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart
 // (<= a few hundred) and writes its outputs.  Deterministic, no atomics.
 // ---------------------------------------------------------------------------
 constexpr int kListThreads = 256;
-constexpr int kListItems = 8;  // consecutive blocks per thread
+#ifndef FL_LIST_ITEMS
+#define FL_LIST_ITEMS 1
+#endif
+constexpr int kListItems = FL_LIST_ITEMS;  // consecutive blocks per thread
 constexpr int kListTile = kListThreads * kListItems;
 
 struct Sum4 {
