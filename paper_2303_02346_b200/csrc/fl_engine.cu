@@ -82,6 +82,7 @@ struct Record {
     float4* gridv = nullptr;   // grid velocity after contact (G2P input), dense block-major
     float4* gridv0 = nullptr;  // (p/m, m) before gravity/walls/contact (grid-update adjoint input)
     uint8_t* cmask = nullptr;  // per node: effectors within contact range (bit e)
+    int* blockmap = nullptr;   // particle block -> list slot + 1 (0 = none), incl. slab ghost blocks
     int n_active = 0;
     int n_keep = 0;    // active + parked slots of the pre-state (= N on one rank)
     int n_stored = 0;  // all slots of the pre-state, departed holes included
@@ -107,7 +108,7 @@ struct Record {
                o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 32),
                o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),
                o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4)),
-               o_mig = carve(size_t(2) * migcap * 4), o_cm = carve(size_t(nbtot) * 64);
+               o_mig = carve(size_t(2) * migcap * 4), o_cm = carve(size_t(nbtot) * 64), o_bm = carve(size_t(nbtot) * 4);
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -125,6 +126,7 @@ struct Record {
         gridv0 = reinterpret_cast<float4*>(b + o_gv0);
         mig_src = migcap > 0 ? reinterpret_cast<uint32_t*>(b + o_mig) : nullptr;
         cmask = reinterpret_cast<uint8_t*>(b + o_cm);
+        blockmap = reinterpret_cast<int*>(b + o_bm);
         mig_cap = migcap;
         CK(cudaMemset(gridv, 0, size_t(nbtot) * 64 * sizeof(float4)));
         CK(cudaMemset(gridv0, 0, size_t(nbtot) * 64 * sizeof(float4)));
@@ -275,8 +277,8 @@ struct Ctx {
 
     // scratch
     DevArr<int> bzero, bstart;  // bzero = [bcount | bheavy | bfill], zeroed per sort
-    int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr, *blockmap_p = nullptr,
-        *list_cnt = nullptr;
+    int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr;
+    DevArr<int> nbflag_arr;
     DevArr<int> nbpos;
     DevArr<int4> tile_sum;
     DevArr<uint32_t> skey, sslot, gk, gv;
@@ -321,7 +323,7 @@ struct Ctx {
     int n_parked() const { return int(inactive_ids.size()); }
     void set_transport(std::unique_ptr<Transport> t);
     void partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t>& active);
-    void halo_exchange(float4* stg, int* flags);
+    void halo_exchange(int* blockmap, float4* stg, int* flags);
     void migrate(StateBuf& out, Record& r);
     void return_bars(Record& r, BarBuf post);
     void allreduce(void* p, size_t n, DType t, ROp op) {
@@ -544,17 +546,16 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
 
     // scratch
     if (N >= (1 << 26)) throw FlumeError(FLUME_E_ARG, "at most 2^26-1 particles per context");
-    // one zero-memset per sort covers counts, heavy flags, fill cursors, node-block
-    // flags, the block map (slot + 1, 0 = none) and the list counters
-    // (counts / heavy flags / fill cursors carry two virtual blocks: parked, departed)
+    // one zero-memset per sort covers counts, heavy flags and fill cursors (with two
+    // virtual blocks: parked, departed); node-block flags and the block map are
+    // written in full by the list scan
     const size_t bz = size_t(g.nbtot) + 2;
-    bzero.alloc(5 * bz + 8);
+    bzero.alloc(3 * bz);
     bcount = bzero.p;
     bheavy = bzero.p + bz;
     bfill = bzero.p + 2 * bz;
-    nbflag = bzero.p + 3 * bz;
-    blockmap_p = bzero.p + 4 * bz;
-    list_cnt = bzero.p + 5 * bz;
+    nbflag_arr.alloc(g.nbtot);
+    nbflag = nbflag_arr.p;
     nbpos.alloc(g.nbtot);
     tile_sum.alloc(sort_list_tiles(g));
     bstart.alloc(g.nbtot + 2);
@@ -812,7 +813,7 @@ void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     const int n = r.n_stored;
     CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
     launch_sort_count(g, st.p, n, d_cls.p, bcount, bheavy, stream);
-    launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, blockmap_p, r.n_blocks,
+    launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, r.blockmap, r.n_blocks,
                       tile_sum.p, stream);
     launch_sort_scatter(g, st.p, n, bstart.p, bfill, skey.p, sslot.p, stream);
     launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
@@ -881,20 +882,20 @@ void Ctx::partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t
 // send tile planes 0,1 of the bottom column down and 4,5 of the top column up,
 // install the received planes as ghost blocks.  flags != nullptr (forward):
 // also flag the owned node blocks reached only by the lower neighbour's tiles.
-void Ctx::halo_exchange(float4* stg, int* flags) {
+void Ctx::halo_exchange(int* blockmap, float4* stg, int* flags) {
     Geom& g = geom;
     const bool lo = rank > 0, hi = rank + 1 < nranks;
-    if (lo) launch_halo_pack(g, blockmap_p, stg, g.sx0, 0, halo_send[0].p, stream);
-    if (hi) launch_halo_pack(g, blockmap_p, stg, g.sx1 - 1, 4, halo_send[1].p, stream);
+    if (lo) launch_halo_pack(g, blockmap, stg, g.sx0, 0, halo_send[0].p, stream);
+    if (hi) launch_halo_pack(g, blockmap, stg, g.sx1 - 1, 4, halo_send[1].p, stream);
     const size_t hb = halo_bytes(g);
     const void* sb[2] = {halo_send[0].p, halo_send[1].p};
     void* rb[2] = {halo_recv[0].p, halo_recv[1].p};
     const size_t sz[2] = {lo ? hb : 0, hi ? hb : 0};
     comm->neighbor_exchange(sb, sz, rb, sz, stream);
     if (lo)
-        launch_halo_unpack(g, halo_recv[0].p, g.sx0 - 1, 4, maxb, blockmap_p, stg, flags, flags ? g.sx0 : -1,
+        launch_halo_unpack(g, halo_recv[0].p, g.sx0 - 1, 4, maxb, blockmap, stg, flags, flags ? g.sx0 : -1,
                            stream);
-    if (hi) launch_halo_unpack(g, halo_recv[1].p, g.sx1, 0, maxb + g.colblocks, blockmap_p, stg, nullptr, -1, stream);
+    if (hi) launch_halo_unpack(g, halo_recv[1].p, g.sx1, 0, maxb + g.colblocks, blockmap, stg, nullptr, -1, stream);
     launches += 2 * (int(lo) + int(hi));
 }
 
@@ -1028,13 +1029,13 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                         staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
          }));
     if (slab()) {
-        halo_exchange(staging.p, nbflag);
+        halo_exchange(r.blockmap, staging.p, nbflag);
         // node-block list again, now with the blocks reached only by ghost tiles
         CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
         launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
         launches += 2;
     }
-    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0,
+    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0,
                                     r.effk, r.cmask, stream));
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
@@ -1091,16 +1092,16 @@ void Ctx::stage_grid(double* mass, double* vel) {
                    staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
     });
     if (slab()) {
-        halo_exchange(staging.p, nbflag);
+        halo_exchange(r.blockmap, staging.p, nbflag);
         CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
         launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
     }
-    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, blockmap_p, staging.p, r.gridv, r.gridv0, es, r.cmask,
+    launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0, es, r.cmask,
                        stream);
     std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
     CK(cudaMemcpyAsync(h.data(), r.gridv, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(bm.data(), blockmap_p, bm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(bm.data(), r.blockmap, bm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     check_error();
     // node blocks the grid update wrote (the rest of the dense array is stale)
@@ -1237,11 +1238,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
     // slabs: cotangents of the particles that migrated in after this substep go home first
     if (slab()) return_bars(r, post);
-    // the forward recorded this substep's grid (r.gridv, r.gridv0); only the
-    // particle-block map is rebuilt for the staging gathers
-    CK(cudaMemsetAsync(blockmap_p, 0, size_t(g.nbtot) * sizeof(int), stream));
-    launch_blockmap_set(r.recs, r.n_blocks, maxb, blockmap_p, stream);
-    launches += 1;
+    // the forward recorded this substep's grid (r.gridv, r.gridv0, r.cmask) and block map
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
         launch_adj_rigid_gather(post, rd, mbar.p, stream);
@@ -1254,8 +1251,8 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
          }));
-    if (slab()) halo_exchange(staging_bar.p, nullptr);
-    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, blockmap_p, staging_bar.p, r.gridv0, gridbar.p, r.effk,
+    if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
+    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
                                      eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, r.cmask,
                                      stream));
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
