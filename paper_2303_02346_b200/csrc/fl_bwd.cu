@@ -550,10 +550,16 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
     }
 }
 
-// one CTA per (effector, component): strided thread sums + fixed shuffle tree
-__global__ void __launch_bounds__(256) k_eff_final(const double* partial, int nblocks, double* out) {
+// final effector-bar sums of `count` consecutive substeps [t0, t0 + count) whose
+// CTA partials sit in a ring of kEffRing slots (deferred: one launch per ring,
+// not per substep); one CTA per (substep, effector component): strided thread
+// sums + fixed shuffle tree
+__global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nblocks, int nq, long t0, double* out) {
     __shared__ double wsum[8];
-    const int q = blockIdx.x, tid = threadIdx.x;
+    const int q = blockIdx.x % nq, tid = threadIdx.x;
+    const long t = t0 + blockIdx.x / nq;
+    const double* partial = ring + size_t(t % kEffRing) * nblocks * kMaxEff * kEffQ;
+    out += size_t(t) * kMaxEff * kEffQ;
     double s = 0.0;
     for (int b = tid; b < nblocks; b += 256) s += partial[size_t(b) * kMaxEff * kEffQ + q];
 #pragma unroll
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(256) k_eff_final(const double* partial, int nb
 
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, double* eff_out, const uint8_t* cmask, cudaStream_t s) {
+                     double* eff_partial, const uint8_t* cmask, cudaStream_t s) {
     switch (eff.n) {
         case 0: k_adj_grid<0><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
@@ -582,7 +588,11 @@ void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const i
         default: k_adj_grid<kMaxEff><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar,
                                                                             gridv0, gridbar, eff, eff_partial, cmask);
     }
-    if (eff.n > 0) k_eff_final<<<eff.n * kEffQ, 256, 0, s>>>(eff_partial, kEffBlocks, eff_out);
+}
+
+void launch_eff_final(const double* ring, int n_eff, long t0, int count, double* eff_out, cudaStream_t s) {
+    if (n_eff <= 0 || count <= 0) return;
+    k_eff_final<<<count * n_eff * kEffQ, 256, 0, s>>>(ring, kEffBlocks, n_eff * kEffQ, t0, eff_out);
 }
 
 // ---------------------------------------------------------------------------

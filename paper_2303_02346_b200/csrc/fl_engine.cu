@@ -279,6 +279,7 @@ struct Ctx {
     DevArr<int> bzero, bstart;  // bzero = [bcount | bheavy | bfill], zeroed per sort
     int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr;
     DevArr<int> nbflag_arr;
+    bool counters_clean = false;  // bzero already zeroed (by the last grid update)
     DevArr<int> nbpos;
     DevArr<int4> tile_sum;
     DevArr<uint32_t> skey, sslot, gk, gv;
@@ -326,6 +327,21 @@ struct Ctx {
     void halo_exchange(int* blockmap, float4* stg, int* flags);
     void migrate(StateBuf& out, Record& r);
     void return_bars(Record& r, BarBuf post);
+    // effector-bar final sums are deferred and batched (kEffRing substeps per launch);
+    // the backward runs t downwards, so the pending substeps are [eff_lo, eff_hi]
+    long eff_lo = -1, eff_hi = -1;
+    void eff_flush() {
+        if (eff_lo < 0) return;
+        launch_eff_final(eff_partial.p, int(eff.size()), eff_lo, int(eff_hi - eff_lo + 1), eff_out.p, stream);
+        launches++;
+        eff_lo = eff_hi = -1;
+    }
+    void eff_pending(long t) {
+        if (eff_lo >= 0 && (t != eff_lo - 1 || eff_hi - t + 1 > kEffRing)) eff_flush();
+        if (eff_lo < 0) eff_hi = t;
+        eff_lo = t;
+        if (eff_hi - eff_lo + 1 == kEffRing) eff_flush();
+    }
     void allreduce(void* p, size_t n, DType t, ROp op) {
         if (comm) comm->allreduce(p, n, t, op, stream);
     }
@@ -573,7 +589,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     abar.alloc(std::max(nbody, 1) * 13);
     start_bar.alloc(std::max(nmem, 1) * 3);
     mbar.alloc(std::max(nmem, 1) * 6);
-    eff_partial.alloc(size_t(kEffBlocks) * kMaxEff * 18);
+    eff_partial.alloc(size_t(kEffRing) * kEffBlocks * kMaxEff * 18);
     loss_partial.alloc(size_t(kLossBlocks) * kMaxLossTerms);
     d_act_list.alloc(64);
     d_emit_list.alloc(64);
@@ -811,7 +827,8 @@ void Ctx::download(flume_state_view* view) {
 void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     Geom& g = geom;
     const int n = r.n_stored;
-    CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
+    if (!counters_clean) CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
+    counters_clean = false;
     launch_sort_count(g, st.p, n, d_cls.p, bcount, bheavy, stream);
     launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, r.blockmap, r.n_blocks,
                       tile_sum.p, stream);
@@ -1036,7 +1053,8 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         launches += 2;
     }
     PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0,
-                                    r.effk, r.cmask, stream));
+                                    r.effk, r.cmask, bzero.p, int(bzero.n), stream));
+    counters_clean = true;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
         CK(cudaMemsetAsync(r.mslot, 0xff, size_t(nmem) * sizeof(int), stream));
@@ -1097,7 +1115,8 @@ void Ctx::stage_grid(double* mass, double* vel) {
         launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
     }
     launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0, es, r.cmask,
-                       stream);
+                       bzero.p, int(bzero.n), stream);
+    counters_clean = true;
     std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
     CK(cudaMemcpyAsync(h.data(), r.gridv, h.size() * sizeof(float4), cudaMemcpyDeviceToHost, stream));
@@ -1253,8 +1272,9 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
          }));
     if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                     eff_partial.p, eff_out.p + size_t(t_slot) * kMaxEff * 18, r.cmask,
+                                     eff_partial.p + size_t(t_slot % kEffRing) * kEffBlocks * kMaxEff * 18, r.cmask,
                                      stream));
+    eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv, w, s);
@@ -1428,6 +1448,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     }
     release_cache();
     for (auto& kv : snaps) put_state(kv.second);
+    eff_flush();
     if (slab()) {  // per-slab effector / spawn bars and non-finite flags
         allreduce(eff_out.p, size_t(T) * kMaxEff * 18, DType::F64, ROp::Sum);
         allreduce(em_out.p, size_t(T) * kMaxEff * 12, DType::F64, ROp::Sum);
@@ -1532,6 +1553,7 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     launch_bars_from_ref(BarBuf{barsA.p, N}, post->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_cls.p,
                          stream);
     adjoint_step(*pre, *post, *rec, barsA, barsB, 0);
+    eff_flush();
     launch_bars_to_ref(BarBuf{barsB.p, N}, pre->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_cls.p, stream);
     CK(cudaMemcpyAsync(xb, d_up[0].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(vb, d_up[1].p, size_t(N) * 24, cudaMemcpyDeviceToHost, stream));

@@ -332,7 +332,9 @@ __device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __res
 __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restrict__ nb_list,
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
-                                                     EffSet eff, uint8_t* cmask) {
+                                                     EffSet eff, uint8_t* cmask, int* clear, int n_clear) {
+    // the sort's counters are dead by now: clear them for the next substep's sort
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_clear; i += gridDim.x * blockDim.x) clear[i] = 0;
     const int n = *n_nb;
     const int sub = threadIdx.x >> 6, l = threadIdx.x & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
@@ -366,8 +368,9 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
 
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
-                        cudaStream_t s) {
-    k_grid_update<<<grid, 256, 0, s>>>(g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask);
+                        int* clear, int n_clear, cudaStream_t s) {
+    k_grid_update<<<grid, 256, 0, s>>>(g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
+                                       n_clear);
 }
 
 // ---------------------------------------------------------------------------

@@ -76,7 +76,7 @@ void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* re
                 uint32_t substep, bool heavy, int* wq, cudaStream_t s);
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
-                        cudaStream_t s);
+                        int* clear, int n_clear, cudaStream_t s);
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs,
                 const int* n_blocks, int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd,
                 unsigned long long* err, uint32_t substep, bool heavy, int* wq, cudaStream_t s);
@@ -104,7 +104,9 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     float4* staging_bar, bool heavy, int* wq, cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, double* eff_out, const uint8_t* cmask, cudaStream_t s);
+                     double* eff_partial, const uint8_t* cmask, cudaStream_t s);
+constexpr int kEffRing = 16;  // substeps whose effector-bar partials wait for one final-sum launch
+void launch_eff_final(const double* ring, int n_eff, long t0, int count, double* eff_out, cudaStream_t s);
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s);
