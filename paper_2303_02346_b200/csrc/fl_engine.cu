@@ -222,17 +222,21 @@ struct Ctx {
     DevArr<int> wq;  // rolling work counters for dynamically scheduled kernels
     int wq_next = 0;
     static constexpr int kWq = 256;
-    int* take_wq() {
-        if (wq_next + 1 > kWq) {
+    // n zeroed counters.  All n come from the same pool epoch: a counter handed out
+    // before a wrap's memset but used after it would start the next epoch dirty.
+    int* take_wq(int n = 1) {
+        if (wq_next + n > kWq) {
             CK(cudaMemsetAsync(wq.p, 0, kWq * sizeof(int), stream));
             wq_next = 0;
         }
-        return wq.p + wq_next++;
+        int* p = wq.p + wq_next;
+        wq_next += n;
+        return p;
     }
     template <class Fn>
     void dual(Fn&& fn) {
-        int* wh = take_wq();
-        int* wl = take_wq();
+        int* wh = take_wq(2);
+        int* wl = wh + 1;
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(s2, ev_fork, 0));
         fn(true, wh, s2);
