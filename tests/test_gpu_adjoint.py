@@ -103,3 +103,20 @@ def test_grad_rerun_bit_identical(ref_available):
     a = fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
     b = fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
     assert np.array_equal(a.action_grad, b.action_grad) and a.loss == b.loss
+
+
+def test_long_rollouts_rerun_identical():
+    """Many substeps in one context (work-counter pool wraps several times) give the
+    same gradients as a fresh context, call after call."""
+    spec = spec_for("c4", 32)
+    out = []
+    for fresh in (True, False, False):
+        if fresh or not out:
+            w = fl.build_scene(spec)
+            ws = fl.GpuWorkspace(w.scene)
+        acts = fl.ActionTrajectory(2, 45, np.tile(w.init_action, (2, 1)))
+        loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+        g = fl.grad_trajectory(w.scene, w.state, acts, loss, stride=30, ws=ws)
+        out.append((g.loss, np.asarray(g.action_grad).copy()))
+    for l, gr in out[1:]:
+        assert l == out[0][0] and np.array_equal(gr, out[0][1])
