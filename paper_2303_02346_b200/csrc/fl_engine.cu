@@ -1709,7 +1709,8 @@ int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, in
     flume_ctx* ctx = new flume_ctx();
     int rc = guard(nullptr, [&] {
         ctx->c.init(desc, device);
-        if (n_ranks > 1) ctx->c.set_transport(fl::make_nccl_transport(uid, rank, n_ranks, device));
+        // (a one-rank NCCL group is allowed: it runs the slab code path with a single slab)
+        ctx->c.set_transport(fl::make_nccl_transport(uid, rank, n_ranks, device));
     });
     if (rc != FLUME_OK) {
         delete ctx;

@@ -107,3 +107,22 @@ def test_slab_rollout_and_grid():
     assert np.array_equal(m1, m3) and np.array_equal(v1, v3)
     assert abs(l1 - l3) <= 1e-12 * abs(l1)
     np.testing.assert_allclose(p1, p3, rtol=1e-12)
+
+
+def test_nccl_transport_single_rank_matches_plain_context():
+    """The NCCL transport (dlopen'ed libnccl, comm init, all-reduce, count exchange)
+    on a one-rank group: the slab code path with one slab reproduces a plain context.
+    (Multi-rank NCCL needs several GPUs; the protocol itself is covered above.)"""
+    spec = spec_for("c5", 32)
+    w1 = fl.build_scene(spec)
+    ws1 = fl.GpuWorkspace(w1.scene)
+    w2 = fl.build_scene(spec)
+    ws2 = fl.GpuWorkspace.distributed(w2.scene, 0, 0, 1, fl.dist_unique_id())
+    fl.mpm_substep(w1.scene, w1.state, w1.init_action, ws1, count=10)
+    fl.mpm_substep(w2.scene, w2.state, w2.init_action, ws2, count=10)
+    for a, b in zip(_state(w1.state), _state(w2.state)):
+        assert np.array_equal(a, b)
+    acts = fl.ActionTrajectory(2, 3, np.tile(w1.init_action, (2, 1)))
+    g1 = fl.grad_trajectory(w1.scene, w1.state, acts, fl.LossEvaluator(w1.scene, w1.loss_spec, w1.state), ws=ws1)
+    g2 = fl.grad_trajectory(w2.scene, w2.state, acts, fl.LossEvaluator(w2.scene, w2.loss_spec, w2.state), ws=ws2)
+    assert g1.loss == g2.loss and np.array_equal(g1.action_grad, g2.action_grad)
