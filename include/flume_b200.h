@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define FLUME_B200_ABI_VERSION 1
+#define FLUME_B200_ABI_VERSION 2
 
 typedef enum {
     FLUME_OK = 0,
@@ -143,7 +143,13 @@ typedef struct {
 } flume_state_view;
 
 /* LossEvaluator terms supported on device (losses.hpp:474-551) */
-typedef enum { FLUME_LOSS_TARGET_POINT = 0, FLUME_LOSS_HOLD_INITIAL = 1 } flume_loss_kind;
+/* LossTerm kinds (losses.hpp:293-304, 405-441); air_sensors needs the gas solver (out of scope) */
+typedef enum {
+    FLUME_LOSS_TARGET_POINT = 0,
+    FLUME_LOSS_HOLD_INITIAL = 1,
+    FLUME_LOSS_MIXING_SPREAD = 2,      /* -sum_ij |x_i - x_j| over the body, O(N^2) on the device */
+    FLUME_LOSS_TRAJECTORY_CHAMFER = 3  /* symmetric mean nearest-neighbour distance to goal sets */
+} flume_loss_kind;
 typedef struct {
     int kind;
     int body;
@@ -151,6 +157,11 @@ typedef struct {
     int squared;
     int final_only;
     double goal[3];
+    /* trajectory_chamfer: point set s = goal_points[3*goal_step_offsets[s] .. 3*goal_step_offsets[s+1]);
+       segment seg uses set min(seg, n_goal_steps - 1) (losses.hpp:488-491) */
+    int n_goal_steps;
+    const long* goal_step_offsets; /* n_goal_steps + 1 */
+    const double* goal_points;
 } flume_loss_term;
 typedef struct {
     int n_terms;

@@ -12,6 +12,8 @@ from pathlib import Path
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("FLUME_B200_LIB", _PKG / "libflume_b200.so"))
 
+ABI_VERSION = 2  # include/flume_b200.h FLUME_B200_ABI_VERSION
+
 FLUME_OK = 0
 FLUME_E_ENGINE = 1
 FLUME_E_SCENE = 2
@@ -77,7 +79,8 @@ class StateView(C.Structure):
 
 class LossTerm(C.Structure):
     _fields_ = [("kind", C.c_int), ("body", C.c_int), ("weight", C.c_double), ("squared", C.c_int),
-                ("final_only", C.c_int), ("goal", d3)]
+                ("final_only", C.c_int), ("goal", d3), ("n_goal_steps", C.c_int),
+                ("goal_step_offsets", C.POINTER(C.c_long)), ("goal_points", C.POINTER(C.c_double))]
 
 
 class LossDesc(C.Structure):
@@ -159,7 +162,7 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.flume_abi_version() != 1:
+    if lib.flume_abi_version() != ABI_VERSION:
         raise RuntimeError("libflume_b200.so ABI mismatch")
     _lib = lib
     return lib

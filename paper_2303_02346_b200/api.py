@@ -244,9 +244,17 @@ def build_scene(spec) -> World:
                  spec if isinstance(spec, dict) else _json.loads(text))
 
 
+_LOSS_KINDS = ["target_point", "hold_initial", "mixing_spread", "trajectory_chamfer"]
+
+
 def _term_dict(t: _abi.LossTerm) -> dict:
-    return {"kind": ["target_point", "hold_initial"][t.kind], "body": t.body, "weight": t.weight,
-            "squared": bool(t.squared), "final_only": bool(t.final_only), "goal": list(t.goal)}
+    d = {"kind": _LOSS_KINDS[t.kind], "body": t.body, "weight": t.weight,
+         "squared": bool(t.squared), "final_only": bool(t.final_only), "goal": list(t.goal)}
+    if d["kind"] == "trajectory_chamfer":
+        off = np.ctypeslib.as_array(t.goal_step_offsets, (t.n_goal_steps + 1,)).copy()
+        pts = np.ctypeslib.as_array(t.goal_points, (int(off[-1]) * 3,)).reshape(-1, 3).copy()
+        d["goal_trajectory"] = [pts[off[s]:off[s + 1]] for s in range(t.n_goal_steps)]
+    return d
 
 
 def _copy_desc(d: _abi.SceneDesc):
@@ -319,8 +327,8 @@ class ActionTrajectory:
 
 
 class LossEvaluator:
-    """Device-evaluable LossEvaluator (losses.hpp:306): target_point and
-    hold_initial terms, optionally composite."""
+    """Device-evaluable LossEvaluator (losses.hpp:306): target_point, hold_initial,
+    mixing_spread and trajectory_chamfer terms, optionally composite."""
 
     def __init__(self, scene: Optional[Scene] = None, spec=None, state0: Optional[SimState] = None):
         terms = spec if isinstance(spec, list) else ([] if spec is None else self._parse(spec))
@@ -328,9 +336,19 @@ class LossEvaluator:
             raise SceneError("scene has no loss specification")
         self.terms = terms
         self._arr = (_abi.LossTerm * len(terms))()
+        self._keep = []
         for i, t in enumerate(terms):
-            k = {"target_point": 0, "hold_initial": 1}[t["kind"]]
+            k = _LOSS_KINDS.index(t["kind"])
             self._arr[i].kind = k
+            if t["kind"] == "trajectory_chamfer":
+                steps = [np.asarray(s, dtype=np.float64).reshape(-1, 3) for s in t["goal_trajectory"]]
+                off = np.zeros(len(steps) + 1, dtype=np.int64)
+                off[1:] = np.cumsum([len(s) for s in steps])
+                pts = np.ascontiguousarray(np.concatenate(steps, 0))
+                self._keep += [off, pts]
+                self._arr[i].n_goal_steps = len(steps)
+                self._arr[i].goal_step_offsets = off.ctypes.data_as(C.POINTER(C.c_long))
+                self._arr[i].goal_points = _dp(pts)
             self._arr[i].body = int(t["body"])
             self._arr[i].weight = float(t.get("weight", 1.0))
             self._arr[i].squared = int(bool(t.get("squared", False)))
@@ -343,9 +361,12 @@ class LossEvaluator:
     @staticmethod
     def _parse(spec: dict):
         def one(t):
-            return {"kind": t.get("kind", "target_point"), "body": t["body"], "weight": t.get("weight", 1.0),
-                    "squared": t.get("squared", False), "final_only": t.get("eval", "per_step") == "final",
-                    "goal": t.get("goal", [0, 0, 0])}
+            d = {"kind": t.get("kind", "target_point"), "body": t["body"], "weight": t.get("weight", 1.0),
+                 "squared": t.get("squared", False), "final_only": t.get("eval", "per_step") == "final",
+                 "goal": t.get("goal", [0, 0, 0])}
+            if "goal_trajectory" in t:
+                d["goal_trajectory"] = t["goal_trajectory"]
+            return d
         if spec.get("kind") == "composite":
             return [one(t) for t in spec["terms"]]
         return [one(spec)]

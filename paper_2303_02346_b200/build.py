@@ -24,7 +24,7 @@ LIB = PKG / "libflume_b200.so"
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
-CU_SRCS = ["fl_fwd.cu", "fl_bwd.cu", "fl_sort.cu", "fl_slab.cu", "fl_comm.cu", "fl_engine.cu"]
+CU_SRCS = ["fl_fwd.cu", "fl_bwd.cu", "fl_sort.cu", "fl_slab.cu", "fl_comm.cu", "fl_loss.cu", "fl_engine.cu"]
 CPP_SRCS = ["fl_scene.cpp"]
 
 

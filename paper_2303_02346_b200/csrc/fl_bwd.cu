@@ -32,7 +32,7 @@ __global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, L
     double g[3] = {0.0, 0.0, 0.0};
     bool any = false;
     for (int k = 0; k < ls.n; k++) {
-        if (!((mask >> k) & 1u) || ls.t[k].body != body) continue;
+        if (!((mask >> k) & 1u) || ls.t[k].body != body || ls.t[k].kind > LK_HOLD) continue;
         const LossTermDev& t = ls.t[k];
         double d[3];
         if (t.kind == LK_TARGET) {

@@ -406,9 +406,11 @@ struct Ctx {
     void forward_substep(const double* action, StatePtr in, StatePtr out, Record& r, bool record_grid);
     void substep(const double* action, int count);
     void stage_grid(double* mass, double* vel);
-    LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<DevArr<float>>>& keep);
+    LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep);
+    PointLossScratch pls;  // trajectory_chamfer / mixing_spread scratch (fl_loss.cu)
+    void point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, double* out_dev, BarBuf* bars);
     uint32_t loss_mask(const flume_loss_desc* loss, int seg, int nseg) const;
-    void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, long substep);
+    void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg);
     double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg);
     void adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre,
                       int t_slot);
@@ -712,6 +714,9 @@ void Ctx::check_error(long /*substep_base*/) {
             e.substep = sub;
             throw e;
         }
+        case ES_LOSS_EMPTY:
+            throw FlumeError(FLUME_E_ENGINE, who == 0 ? "chamfer_distance: empty point set"
+                                                      : "mixing_spread_loss: need at least 2 particles");
         default: throw FlumeError(FLUME_E_ENGINE, "device error");
     }
 }
@@ -1156,7 +1161,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
             }
 }
 
-LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<DevArr<float>>>& keep) {
+LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep) {
     LossSet ls{};
     if (!loss || loss->n_terms <= 0) throw FlumeError(FLUME_E_SCENE, "scene has no loss specification");
     if (loss->n_terms > kMaxLossTerms) throw FlumeError(FLUME_E_ARG, "too many loss terms");
@@ -1186,11 +1191,43 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
             arr->upload(fx, stream);
             d.init = arr->p;
             keep.push_back(arr);
+        } else if (t.kind == FLUME_LOSS_MIXING_SPREAD || t.kind == FLUME_LOSS_TRAJECTORY_CHAMFER) {
+            if (slab()) throw FlumeError(FLUME_E_ARG, "point-set losses run on single-rank contexts only");
+            int max_goals = 1;
+            if (t.kind == FLUME_LOSS_TRAJECTORY_CHAMFER) {
+                if (t.n_goal_steps < 1 || !t.goal_step_offsets || !t.goal_points)
+                    throw FlumeError(FLUME_E_SCENE, "trajectory_chamfer: empty goal_trajectory");
+                const long np = t.goal_step_offsets[t.n_goal_steps];
+                for (int q = 0; q < t.n_goal_steps; q++) {
+                    const long m = t.goal_step_offsets[q + 1] - t.goal_step_offsets[q];
+                    if (m <= 0) throw FlumeError(FLUME_E_ENGINE, "chamfer_distance: empty point set");
+                    max_goals = std::max<long>(max_goals, m);
+                }
+                auto arr = std::make_shared<DevArr<double>>();
+                arr->alloc(size_t(np) * 3);
+                CK(cudaMemcpyAsync(arr->p, t.goal_points, size_t(np) * 3 * 8, cudaMemcpyHostToDevice, stream));
+                d.gpts = arr->p;
+                d.goff_h = t.goal_step_offsets;
+                d.nsteps = t.n_goal_steps;
+                keep.push_back(arr);
+            }
+            d.kind = t.kind == FLUME_LOSS_MIXING_SPREAD ? LK_SPREAD : LK_CHAMFER;
+            pls.reserve(N, max_goals);
         } else if (t.kind != FLUME_LOSS_TARGET_POINT) {
             throw FlumeError(FLUME_E_SCENE, "loss kind not supported on device");
         }
     }
     return ls;
+}
+
+// trajectory_chamfer / mixing_spread terms of `mask` (losses.hpp:474-551): eval adds
+// weight * value into *out_dev (after the per-particle terms), grad adds into bars
+void Ctx::point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, double* out_dev, BarBuf* bars) {
+    for (int k = 0; k < ls.n; k++) {
+        if (!((mask >> k) & 1u) || ls.t[k].kind < LK_SPREAD) continue;
+        launch_point_loss(pls, st.p, st.n, d_cls.p, ls.t[k], seg, geom.key_inactive, out_dev, bars, d_err.p, stream);
+        launches += 5;
+    }
 }
 
 uint32_t Ctx::loss_mask(const flume_loss_desc* loss, int seg, int nseg) const {
@@ -1200,16 +1237,17 @@ uint32_t Ctx::loss_mask(const flume_loss_desc* loss, int seg, int nseg) const {
     return m;
 }
 
-void Ctx::eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, long /*substep*/) {
+void Ctx::eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg) {
     // per-slab partial; the segment losses are all-reduced once after the rollout
     launch_loss(st.p, st.n, d_cls.p, ls, mask, loss_partial.p, out_dev, geom.key_inactive, stream);
     launches += 2;
+    point_losses(st, ls, mask, seg, out_dev, nullptr);
 }
 
 double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg) {
     const long T = long(a->n_segments) * a->segment_length;
     if (window <= 0) window = T;
-    std::vector<std::shared_ptr<DevArr<float>>> keep;
+    std::vector<std::shared_ptr<void>> keep;
     LossSet ls = make_lossset(loss, keep);
     loss_out.alloc(a->n_segments);
     // state0 is const: work on a copy
@@ -1228,7 +1266,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
         st = nxt;
         if ((t + 1) % a->segment_length == 0) {
             int seg = int((t + 1) / a->segment_length) - 1;
-            eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, substep_index);
+            eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, seg);
         }
     }
     allreduce(loss_out.p, size_t(a->n_segments), DType::F64, ROp::Sum);
@@ -1302,7 +1340,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     if (stride <= 0) stride = T;
     if (window <= 0) window = T;
     const int nseg = a->n_segments, seglen = a->segment_length;
-    std::vector<std::shared_ptr<DevArr<float>>> keep;
+    std::vector<std::shared_ptr<void>> keep;
     LossSet ls = make_lossset(loss, keep);
     loss_out.alloc(nseg);
     eff_out.alloc(size_t(T) * kMaxEff * 18);
@@ -1382,7 +1420,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         }
         if ((t + 1) % seglen == 0) {
             int seg = int((t + 1) / seglen) - 1;
-            eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, substep_index);
+            eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, seg);
         }
     }
     const size_t n_snap = snaps.size();
@@ -1443,6 +1481,8 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             launch_loss_grad(boundary.p, boundary.n, d_cls.p, ls, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
                              geom.key_inactive, stream);
             launches++;
+            BarBuf bb{barsA.p, N};
+            point_losses(boundary, ls, loss_mask(loss, seg, nseg), seg, nullptr, &bb);
         }
         ensure_cached(t);
         const size_t k = size_t(t - cache_base);

@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const Clas
         if (key > key_inactive) continue;  // departed slot: counted on the particle's new slab
         const bool active = key < key_inactive;
         for (int k = 0; k < ls.n; k++) {
-            if (!((mask >> k) & 1u) || ls.t[k].body != body) continue;
+            if (!((mask >> k) & 1u) || ls.t[k].body != body || ls.t[k].kind > LK_HOLD) continue;
             const LossTermDev& t = ls.t[k];
             double d[3];
             if (t.kind == LK_TARGET) {

@@ -45,14 +45,17 @@ struct EmitAdjEntry {
 };
 
 constexpr int kMaxLossTerms = 8;
-enum LossKindId : int { LK_TARGET = 0, LK_HOLD = 1 };
+enum LossKindId : int { LK_TARGET = 0, LK_HOLD = 1, LK_SPREAD = 2, LK_CHAMFER = 3 };
 struct LossTermDev {
     int kind;
     int body;
     int squared;
     double weight;
     double goal[3];
-    const float* init;  // hold_initial: [3*N] initial positions by particle id
+    const float* init;    // hold_initial: [3*N] initial positions by particle id
+    const double* gpts;   // trajectory_chamfer: all goal points (device)
+    const long* goff_h;   // trajectory_chamfer: set offsets (HOST pointer, n_steps + 1)
+    int nsteps;
 };
 struct LossSet {
     int n;
@@ -60,6 +63,24 @@ struct LossSet {
 };
 
 constexpr int kLossBlocks = 296;
+
+// point-set losses (fl_loss.cu): scratch for the body compaction and the NN passes
+constexpr int kChamferChunks = 512;
+struct PointLossScratch {
+    int *flags = nullptr, *pos = nullptr, *idx = nullptr, *arg = nullptr, *carg = nullptr, *garg = nullptr,
+        *count = nullptr;
+    double *px = nullptr, *best = nullptr, *partial = nullptr, *cbest = nullptr, *gbest = nullptr,
+           *scal = nullptr;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0, cap_g = 0;
+    int cap_n = 0;
+    void reserve(int n_particles, int max_goals);
+    ~PointLossScratch();
+};
+// eval (bars == nullptr): adds weight * value into *out; grad: adds d/dx into bars
+void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossTermDev& t,
+                       int seg, uint32_t key_inactive, double* out, BarBuf* bars, unsigned long long* err,
+                       cudaStream_t s);
 constexpr int kEffBlocks = 1184;
 constexpr int kRigidChunk = 2048;
 

@@ -114,6 +114,7 @@ enum ErrStage : uint32_t {
     ES_P2G_STRESS = 2,
     ES_G2P_PROJECT = 3,
     ES_RIGID = 4,
+    ES_LOSS_EMPTY = 5,  // who: 0 chamfer_distance on an empty set, 1 mixing_spread with < 2 particles
 };
 
 __host__ __device__ inline uint64_t pack_err(uint32_t substep, uint32_t stage, uint32_t who) {

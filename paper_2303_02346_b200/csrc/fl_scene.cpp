@@ -250,6 +250,8 @@ struct flume_scene {
     std::vector<long> act;
     std::vector<double> x, v, F, C;
     std::vector<flume_loss_term> loss_terms;
+    std::vector<std::vector<long>> loss_goal_off;  // per term (trajectory_chamfer)
+    std::vector<std::vector<double>> loss_goal_pts;
     int n_segments = 1, segment_length = 1;
     double init[6] = {0, 0, 0, 0, 0, 0};
     std::string error;
@@ -492,6 +494,24 @@ void build(flume_scene& sc, const json& spec) {
             for (int a = 0; a < 3; a++) t.goal[a] = gl[a];
         } else if (kind == "hold_initial") {
             t.kind = FLUME_LOSS_HOLD_INITIAL;
+        } else if (kind == "mixing_spread") {
+            t.kind = FLUME_LOSS_MIXING_SPREAD;
+        } else if (kind == "trajectory_chamfer") {
+            t.kind = FLUME_LOSS_TRAJECTORY_CHAMFER;
+            std::vector<long> off{0};
+            std::vector<double> pts;
+            for (const json& jstep : jt.at("goal_trajectory")) {
+                for (const json& jp : jstep) {
+                    V p = vec3(jp, "goal point");
+                    for (int a = 0; a < 3; a++) pts.push_back(p[a]);
+                }
+                off.push_back(long(pts.size() / 3));
+            }
+            if (off.size() < 2) throw SceneErr("trajectory_chamfer: empty goal_trajectory");
+            sc.loss_goal_off.resize(sc.loss_terms.size() + 1);
+            sc.loss_goal_pts.resize(sc.loss_terms.size() + 1);
+            sc.loss_goal_off.back() = std::move(off);
+            sc.loss_goal_pts.back() = std::move(pts);
         } else {
             throw SceneErr("loss kind '" + kind + "' is outside the GPU path");
         }
@@ -580,6 +600,15 @@ int flume_scene_state_get(const flume_scene* s, flume_state_view* v) {
 
 int flume_scene_loss_get(const flume_scene* s, flume_loss_desc* l) {
     if (!s || !l) return FLUME_E_ARG;
+    // goal point sets live in the scene's own vectors; point the terms at them
+    flume_scene* ms = const_cast<flume_scene*>(s);
+    for (size_t k = 0; k < ms->loss_terms.size(); k++) {
+        flume_loss_term& t = ms->loss_terms[k];
+        if (t.kind != FLUME_LOSS_TRAJECTORY_CHAMFER || k >= ms->loss_goal_off.size()) continue;
+        t.n_goal_steps = int(ms->loss_goal_off[k].size()) - 1;
+        t.goal_step_offsets = ms->loss_goal_off[k].data();
+        t.goal_points = ms->loss_goal_pts[k].data();
+    }
     l->n_terms = int(s->loss_terms.size());
     l->terms = s->loss_terms.data();
     return FLUME_OK;
