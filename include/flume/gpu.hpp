@@ -243,6 +243,20 @@ public:
                 for (int a = 0; a < 3; a++) term.goal[a] = t.at("goal")[size_t(a)].get<double>();
             } else if (kind == "hold_initial") {
                 term.kind = FLUME_LOSS_HOLD_INITIAL;
+            } else if (kind == "mixing_spread") {
+                term.kind = FLUME_LOSS_MIXING_SPREAD;
+            } else if (kind == "trajectory_chamfer") {
+                term.kind = FLUME_LOSS_TRAJECTORY_CHAMFER;
+                std::vector<long> off{0};
+                std::vector<double> pts;
+                for (const json& step : t.at("goal_trajectory")) {
+                    for (const json& p : step)
+                        for (int a = 0; a < 3; a++) pts.push_back(p[size_t(a)].get<double>());
+                    off.push_back(long(pts.size() / 3));
+                }
+                goal_off_.push_back(std::move(off));
+                goal_pts_.push_back(std::move(pts));
+                term.n_goal_steps = int(goal_off_.back().size()) - 1;
             } else {
                 throw SceneError("loss kind '" + kind + "' is not evaluated on the device");
             }
@@ -256,12 +270,24 @@ public:
             for (const json& t : spec.at("terms")) add(t);
         else
             add(spec);
+        // goal sets in this object's vectors (stable once all terms are parsed)
+        size_t q = 0;
+        for (flume_loss_term& term : terms_)
+            if (term.kind == FLUME_LOSS_TRAJECTORY_CHAMFER) {
+                term.goal_step_offsets = goal_off_[q].data();
+                term.goal_points = goal_pts_[q].data();
+                q++;
+            }
         desc_ = flume_loss_desc{int(terms_.size()), terms_.data()};
     }
+    Loss(const Loss&) = delete;
+    Loss& operator=(const Loss&) = delete;
     const flume_loss_desc* desc() const { return &desc_; }
 
 private:
     std::vector<flume_loss_term> terms_;
+    std::vector<std::vector<long>> goal_off_;
+    std::vector<std::vector<double>> goal_pts_;
     flume_loss_desc desc_{};
 };
 
