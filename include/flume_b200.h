@@ -207,6 +207,10 @@ int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out);
 int flume_ctx_destroy(flume_ctx* ctx);
 int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact);
 int flume_last_error(const flume_ctx* ctx, flume_error_info* info);
+/* CheckpointStore placement for grad_trajectory (checkpoint.hpp:11-50): 0 = snapshots in HBM
+   (default), 1 = snapshots spilled to pinned host memory on a copy stream that overlaps the
+   forward, brought back when the backward replays their segment.  Results are identical. */
+int flume_set_checkpoint_spill(flume_ctx* ctx, int mode);
 int flume_get_stream(flume_ctx* ctx, void** cuda_stream);
 int flume_sync(flume_ctx* ctx);
 int flume_last_timing(const flume_ctx* ctx, flume_timing* out);

@@ -466,6 +466,10 @@ class GpuWorkspace:
     def ranks(self) -> int:
         return len(self.ctxs)
 
+    def set_checkpoint_spill(self, host: bool = True):
+        """grad_trajectory snapshots in pinned host memory instead of HBM (long horizons)."""
+        self._collective(lambda r, c: self.lib.flume_set_checkpoint_spill(c, int(bool(host))))
+
     def slab_info(self):
         """[(rank, sx0, sx1, n_active)] -- the x-columns of 4 cells each rank owns."""
         out = []

@@ -58,6 +58,24 @@ struct StateBuf {
 };
 using StatePtr = std::shared_ptr<StateBuf>;
 
+// a trajectory snapshot spilled to pinned host memory (CheckpointStore, checkpoint.hpp:11-50,
+// for horizons beyond HBM)
+struct HostState {
+    void* mem = nullptr;
+    size_t bytes = 0;
+    int n = 0;
+    cudaEvent_t done = nullptr;  // D2H completion on the copy stream
+    explicit HostState(size_t b) : bytes(b) {
+        CK(cudaMallocHost(&mem, b));
+        CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    }
+    ~HostState() {
+        if (mem) cudaFreeHost(mem);
+        if (done) cudaEventDestroy(done);
+    }
+};
+using HostPtr = std::shared_ptr<HostState>;
+
 struct EffState {
     V3<double> t;
     M3<double> R;
@@ -284,6 +302,39 @@ struct Ctx {
     int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr;
     DevArr<int> nbflag_arr;
     bool counters_clean = false;  // bzero already zeroed (by the last grid update)
+    // checkpoint spill: snapshots of grad_trajectory in pinned host memory (D2H on a
+    // copy stream overlapping the forward; H2D when the backward replays a segment)
+    int spill = 0;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_snap = nullptr;
+    std::vector<HostPtr> host_pool;
+    HostPtr get_host(size_t bytes) {
+        for (size_t i = 0; i < host_pool.size(); i++)
+            if (host_pool[i]->bytes == bytes) {
+                HostPtr h = host_pool[i];
+                host_pool.erase(host_pool.begin() + long(i));
+                return h;
+            }
+        return std::make_shared<HostState>(bytes);
+    }
+    HostPtr spill_state(const StateBuf& st) {
+        if (!cstream) {
+            CK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
+        }
+        HostPtr h = get_host(st.bytes);
+        CK(cudaEventRecord(ev_snap, stream));
+        CK(cudaStreamWaitEvent(cstream, ev_snap, 0));
+        CK(cudaMemcpyAsync(h->mem, st.mem, st.bytes, cudaMemcpyDeviceToHost, cstream));
+        CK(cudaEventRecord(h->done, cstream));
+        h->n = st.n;
+        return h;
+    }
+    void unspill(const HostState& h, StateBuf& dst) {
+        CK(cudaStreamWaitEvent(stream, h.done, 0));
+        CK(cudaMemcpyAsync(dst.mem, h.mem, h.bytes, cudaMemcpyHostToDevice, stream));
+        dst.n = h.n;
+    }
     DevArr<int> nbpos;
     DevArr<int4> tile_sum;
     DevArr<uint32_t> skey, sslot, gk, gv;
@@ -1392,10 +1443,33 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     std::vector<RecordPtr> cache_recs;
     long cache_base = -1;
 
+    std::map<long, HostPtr> hsnaps;  // spilled snapshots
+    // device buffers of spilled snapshots go back to the pool once their D2H finished
+    std::vector<std::pair<StatePtr, cudaEvent_t>> spilling;
+    auto retire_spilled = [&](bool all) {
+        for (size_t i = 0; i < spilling.size();) {
+            if (all || cudaEventQuery(spilling[i].second) == cudaSuccess || spilling.size() > 2) {
+                CK(cudaStreamWaitEvent(stream, spilling[i].second, 0));
+                put_state(spilling[i].first);
+                spilling.erase(spilling.begin() + long(i));
+            } else {
+                i++;
+            }
+        }
+    };
+    auto take_snapshot = [&](long at, StatePtr s) {  // s stays the input of the next substep
+        if (spill && at < last_base) {
+            HostPtr h = spill_state(*s);
+            hsnaps[at] = h;
+            spilling.push_back({s, h->done});
+        } else {
+            snaps[at] = s;
+        }
+        host_snaps[at] = take_host();
+    };
     StatePtr st = get_state();
     copy_state(*st, *cur);
-    snaps[0] = st;
-    host_snaps[0] = take_host();
+    take_snapshot(0, st);
     for (long t = 0; t < T; t++) {
         const bool in_last = t >= last_base;
         if (in_last && cache_base < 0) {
@@ -1410,20 +1484,19 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         if (in_last) {
             cache_recs.push_back(rec);
             cache_states.push_back(nxt);
-        } else if (!snaps.count(t)) {
+        } else if (!snaps.count(t) && !hsnaps.count(t)) {
             put_state(st);
         }
         st = nxt;
-        if ((t + 1) % stride == 0) {
-            snaps[t + 1] = st;
-            host_snaps[t + 1] = take_host();
-        }
+        retire_spilled(false);
+        if ((t + 1) % stride == 0) take_snapshot(t + 1, st);
         if ((t + 1) % seglen == 0) {
             int seg = int((t + 1) / seglen) - 1;
             eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, seg);
         }
     }
-    const size_t n_snap = snaps.size();
+    retire_spilled(true);
+    const size_t n_snap = snaps.size() + hsnaps.size();
     allreduce(loss_out.p, size_t(nseg), DType::F64, ROp::Sum);
     CK(cudaEventRecord(ev1, stream));
     std::vector<double> per(nseg);
@@ -1456,12 +1529,16 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     auto ensure_cached = [&](long t) {
         if (cache_base >= 0 && t >= cache_base && t < cache_base + long(cache_recs.size())) return;
         release_cache();
-        auto it = snaps.upper_bound(t);
-        --it;
-        long base = it->first;
+        const long base = (t / stride) * stride;
         long end = std::min(base + stride, T);
         restore_host(host_snaps[base]);
-        StatePtr s = it->second;
+        StatePtr s;
+        if (hsnaps.count(base)) {  // spilled: back into HBM (released with the cache)
+            s = get_state();
+            unspill(*hsnaps[base], *s);
+        } else {
+            s = snaps.at(base);
+        }
         cache_base = base;
         cache_states.push_back(s);
         for (long q = base; q < end; q++) {
@@ -1492,6 +1569,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     }
     release_cache();
     for (auto& kv : snaps) put_state(kv.second);
+    for (auto& kv : hsnaps) host_pool.push_back(kv.second);
     eff_flush();
     if (slab()) {  // per-slab effector / spawn bars and non-finite flags
         allreduce(eff_out.p, size_t(T) * kMaxEff * 18, DType::F64, ROp::Sum);
@@ -1781,11 +1859,15 @@ int flume_ctx_destroy(flume_ctx* ctx) {
     if (!ctx) return FLUME_OK;
     cudaStreamSynchronize(ctx->c.stream);
     cudaStream_t s = ctx->c.stream, s2 = ctx->c.s2;
-    cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join;
+    cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join, e3 = ctx->c.ev_snap;
+    cudaStream_t s3 = ctx->c.cstream;
     cudaStreamSynchronize(s2);
+    if (s3) cudaStreamSynchronize(s3);
     delete ctx;
     if (s) cudaStreamDestroy(s);
     if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
+    if (e3) cudaEventDestroy(e3);
     if (e1) cudaEventDestroy(e1);
     if (e2) cudaEventDestroy(e2);
     return FLUME_OK;
@@ -1798,6 +1880,11 @@ int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact) {
         ctx->c.cfg.hard_contact = hard_contact;
         ctx->c.geom.hard = hard_contact;
     });
+}
+
+int flume_set_checkpoint_spill(flume_ctx* ctx, int mode) {
+    if (!ctx || mode < 0 || mode > 1) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.spill = mode; });
 }
 
 int flume_last_error(const flume_ctx* ctx, flume_error_info* info) {

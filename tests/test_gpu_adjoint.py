@@ -120,3 +120,20 @@ def test_long_rollouts_rerun_identical():
         out.append((g.loss, np.asarray(g.action_grad).copy()))
     for l, gr in out[1:]:
         assert l == out[0][0] and np.array_equal(gr, out[0][1])
+
+
+def test_checkpoint_spill_to_host_identical():
+    """Snapshots spilled to pinned host memory give bit-identical
+    gradients and the same snapshot count as HBM snapshots."""
+    spec = spec_for("c4", 32)
+    out = []
+    for spill in (False, True, True):
+        w = fl.build_scene(spec)
+        ws = fl.GpuWorkspace(w.scene)
+        ws.set_checkpoint_spill(spill)
+        acts = fl.ActionTrajectory(3, 7, np.tile(w.init_action, (3, 1)))
+        loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+        g = fl.grad_trajectory(w.scene, w.state, acts, loss, stride=4, ws=ws)
+        out.append((g.loss, np.asarray(g.action_grad).copy(), g.snapshots))
+    for l, gr, ns in out[1:]:
+        assert l == out[0][0] and np.array_equal(gr, out[0][1]) and ns == out[0][2] == 21 // 4 + 1
