@@ -8,10 +8,11 @@ scene / step / grad API (proj/include/flume)."""
 from .api import (ActionTrajectory, AdjointError, AdjointState, DegenerateDeformation, DeviceError, EngineError,
                   GpuWorkspace, LossEvaluator, RigidityError, Scene, SceneError, SimState, SubstepRecord,
                   TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, mpm_substep,
-                  p2g_grid, rollout_loss, slab_split)
+                  p2g_grid, rollout_loss, slab_split, WorkspacePool, rollout_loss_batch,
+                  grad_trajectory_batch)
 from . import scenes
 
 __all__ = ["ActionTrajectory", "AdjointError", "AdjointState", "DegenerateDeformation", "DeviceError", "EngineError",
            "GpuWorkspace", "LossEvaluator", "RigidityError", "Scene", "SceneError", "SimState", "SubstepRecord",
            "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "mpm_substep", "p2g_grid",
-           "rollout_loss", "scenes", "slab_split"]
+           "rollout_loss", "scenes", "slab_split", "WorkspacePool", "rollout_loss_batch", "grad_trajectory_batch"]

@@ -702,3 +702,65 @@ def adjoint_substep(scene: Scene, rec: SubstepRecord, adj: AdjointState, action_
     ws._check(ws.lib.flume_adjoint_substep(ws.ctx, _dp(act), _dp(adj.x_bar), _dp(adj.v_bar), _dp(adj.F_bar),
                                            _dp(adj.C_bar), _dp(eb), _dp(ab)))
     action_bar[...] = ab
+
+
+# ---------------------------------------------------------------------------
+# populations: many independent rollouts of one scene, e.g. a
+# CMA-ES population (optimize.hpp:383-418) or DP line-search candidates
+# ---------------------------------------------------------------------------
+
+
+class WorkspacePool:
+    """K independent device contexts of one scene on one GPU.  Each context owns a
+    stream, and the calls below run one host thread per context (ctypes releases the
+    GIL), so the small scenes of a population overlap on the device instead of
+    queueing behind each other's per-substep launch latency."""
+
+    def __init__(self, scene: Scene, size: int, device: int = 0):
+        self.scene = scene
+        self.workspaces = [GpuWorkspace(scene, device=device) for _ in range(size)]
+
+    def close(self):
+        for ws in self.workspaces:
+            ws.close()
+
+    def _map(self, fn, items):
+        out = [None] * len(items)
+        errs = [None] * len(items)
+        k = len(self.workspaces)
+
+        def worker(w):
+            for i in range(w, len(items), k):
+                try:
+                    out[i] = fn(self.workspaces[w], items[i])
+                except Exception as e:  # noqa: BLE001 - re-raised below in item order
+                    errs[i] = e
+
+        th = [threading.Thread(target=worker, args=(w,)) for w in range(min(k, len(items)))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return out
+
+
+def rollout_loss_batch(scene: Scene, state0: SimState, population: Sequence[ActionTrajectory],
+                       loss: LossEvaluator, pool: WorkspacePool, window: int = 0) -> List[float]:
+    """rollout_loss (grad.hpp:15-41) for every action trajectory of a population."""
+    states = [state0.copy() for _ in pool.workspaces]
+    idx = {id(ws): i for i, ws in enumerate(pool.workspaces)}
+    return pool._map(lambda ws, a: rollout_loss(scene, states[idx[id(ws)]], a, loss, window=window, ws=ws),
+                     list(population))
+
+
+def grad_trajectory_batch(scene: Scene, state0: SimState, population: Sequence[ActionTrajectory],
+                          loss: LossEvaluator, pool: WorkspacePool, stride: int = 0,
+                          window: int = 0) -> List[TrajectoryGrad]:
+    """grad_trajectory (grad.hpp:61-134) for every action trajectory of a population."""
+    states = [state0.copy() for _ in pool.workspaces]
+    idx = {id(ws): i for i, ws in enumerate(pool.workspaces)}
+    return pool._map(lambda ws, a: grad_trajectory(scene, states[idx[id(ws)]], a, loss, stride=stride,
+                                                   window=window, ws=ws), list(population))
