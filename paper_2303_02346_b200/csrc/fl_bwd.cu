@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2
                                                         float* xbar_tmp, float* Fbar_tmp, RigidDev rd,
                                                         const float* __restrict__ start_bar, float4* staging_bar,
                                                         int cap, int* wq) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
     float4* vt = reinterpret_cast<float4*>(smraw + sizeof(ScSmem));
@@ -412,10 +413,10 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
         attr = true;
     }
     if (heavy)
-        k_adj_g2p<true><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
+        launch_k(k_adj_g2p<true>, dim3(grid), dim3(kScThreads), smem, s, g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
                                                        xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
     else
-        k_adj_g2p<false><<<grid, kScThreads, smem, s>>>(g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
+        launch_k(k_adj_g2p<false>, dim3(grid), dim3(kScThreads), smem, s, g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
                                                         xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
 }
 
@@ -461,6 +462,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
                                                                  const float4* __restrict__ gridv0, float4* gridbar,
                                                                  EffSet eff, double* eff_partial,
                                                                  const uint8_t* __restrict__ cmask) {
+    pdl_wait();
     constexpr int kW = kAdjGridThreads / 32;
     constexpr int kQ = NE * kEffQ > 0 ? NE * kEffQ : 1;
     __shared__ double wacc[kW][kQ];
@@ -555,6 +557,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const i
 // not per substep); one CTA per (substep, effector component): strided thread
 // sums + fixed shuffle tree
 __global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nblocks, int nq, long t0, double* out) {
+    pdl_wait();
     __shared__ double wsum[8];
     const int q = blockIdx.x % nq, tid = threadIdx.x;
     const long t = t0 + blockIdx.x / nq;
@@ -577,22 +580,22 @@ void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const i
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                      double* eff_partial, const uint8_t* cmask, cudaStream_t s) {
     switch (eff.n) {
-        case 0: k_adj_grid<0><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 0: launch_k(k_adj_grid<0>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        case 1: k_adj_grid<1><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 1: launch_k(k_adj_grid<1>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        case 2: k_adj_grid<2><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 2: launch_k(k_adj_grid<2>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        case 3: k_adj_grid<3><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 3: launch_k(k_adj_grid<3>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        default: k_adj_grid<kMaxEff><<<kEffBlocks, kAdjGridThreads, 0, s>>>(g, nb_list, n_nb, blockmap, staging_bar,
+        default: launch_k(k_adj_grid<kMaxEff>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar,
                                                                             gridv0, gridbar, eff, eff_partial, cmask);
     }
 }
 
 void launch_eff_final(const double* ring, int n_eff, long t0, int count, double* eff_out, cudaStream_t s) {
     if (n_eff <= 0 || count <= 0) return;
-    k_eff_final<<<count * n_eff * kEffQ, 256, 0, s>>>(ring, kEffBlocks, n_eff * kEffQ, t0, eff_out);
+    launch_k(k_eff_final, dim3(count * n_eff * kEffQ), dim3(256), 0, s, ring, kEffBlocks, n_eff * kEffQ, t0, eff_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -606,6 +609,7 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom 
                                                  const float* __restrict__ xbar_tmp,
                                                  const float* __restrict__ Fbar_tmp, BarBuf out, int* nonfinite,
                                                  int cap, int* wq) {
+    pdl_wait();
     __shared__ float4 bt[kTile];
     const int tid = threadIdx.x;
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
@@ -764,10 +768,10 @@ void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s) {
     if (heavy)
-        k_adj_p2g<true><<<grid, 128, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
+        launch_k(k_adj_p2g<true>, dim3(grid), dim3(128), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
                                              nonfinite, out.cap, wq);
     else
-        k_adj_p2g<false><<<grid, 128, 0, s>>>(g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
+        launch_k(k_adj_p2g<false>, dim3(grid), dim3(128), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
                                               nonfinite, out.cap, wq);
 }
 
@@ -777,6 +781,7 @@ void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 // returned by its new slab before the previous substep's adjoint
 __global__ void k_tail_bars(BarBuf post, BarBuf out, const uint32_t* __restrict__ perm, int n0, int n_keep,
                             int n_stored) {
+    pdl_wait();
     int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_stored) return;
     uint32_t s = perm[j];
@@ -790,7 +795,7 @@ void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_activ
                       cudaStream_t s) {
     int m = n_stored - n_active;
     if (m <= 0) return;
-    k_tail_bars<<<(m + 255) / 256, 256, 0, s>>>(post, out, perm, n_active, n_keep, n_stored);
+    launch_k(k_tail_bars, dim3((m + 255) / 256), dim3(256), 0, s, post, out, perm, n_active, n_keep, n_stored);
 }
 
 // emitter spawn adjoint, sequential over the substep's spawns (fixed order)

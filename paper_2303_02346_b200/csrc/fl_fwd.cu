@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom 
                                                     const uint16_t* __restrict__ celltab,
                                                     const ClassInfo* __restrict__ cls, float4* staging,
                                                     unsigned long long* err, uint32_t substep, int* wq) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
     const int tid = threadIdx.x;
@@ -296,10 +297,10 @@ void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* re
         attr = true;
     }
     if (heavy)
-        k_p2g<true><<<grid, kScThreads, sizeof(ScSmem), s>>>(g, st, perm, recs, n_blocks, celltab, cls, staging, err,
+        launch_k(k_p2g<true>, dim3(grid), dim3(kScThreads), sizeof(ScSmem), s, g, st, perm, recs, n_blocks, celltab, cls, staging, err,
                                                             substep, wq);
     else
-        k_p2g<false><<<grid, kScThreads, sizeof(ScSmem), s>>>(g, st, perm, recs, n_blocks, celltab, cls, staging, err,
+        launch_k(k_p2g<false>, dim3(grid), dim3(kScThreads), sizeof(ScSmem), s, g, st, perm, recs, n_blocks, celltab, cls, staging, err,
                                                              substep, wq);
 }
 
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
                                                      EffSet eff, uint8_t* cmask, int* clear, int n_clear) {
+    pdl_wait();
     // the sort's counters are dead by now: clear them for the next substep's sort
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_clear; i += gridDim.x * blockDim.x) clear[i] = 0;
     const int n = *n_nb;
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
                         int* clear, int n_clear, cudaStream_t s) {
-    k_grid_update<<<grid, 256, 0, s>>>(g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
+    launch_k(k_grid_update, dim3(grid), dim3(256), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
                                        n_clear);
 }
 
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
                                              RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {
+    pdl_wait();
     __shared__ float4 vt[kTile];
     const int tid = threadIdx.x;
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
@@ -484,12 +487,13 @@ void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const Bl
                 int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd, unsigned long long* err,
                 uint32_t substep, bool heavy, int* wq, cudaStream_t s) {
     if (heavy)
-        k_g2p<true><<<grid, 128, 0, s>>>(g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
+        launch_k(k_g2p<true>, dim3(grid), dim3(128), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
     else
-        k_g2p<false><<<grid, 128, 0, s>>>(g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
+        launch_k(k_g2p<false>, dim3(grid), dim3(128), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
 }
 
 __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
+    pdl_wait();
     int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     uint32_t s = perm[j];
@@ -503,7 +507,7 @@ __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restric
 void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s) {
     int m = n - n_active;
     if (m <= 0) return;
-    k_tail_copy<<<(m + 255) / 256, 256, 0, s>>>(g, in, out, perm, n_active, n);
+    launch_k(k_tail_copy, dim3((m + 255) / 256), dim3(256), 0, s, g, in, out, perm, n_active, n);
 }
 
 // ---------------------------------------------------------------------------

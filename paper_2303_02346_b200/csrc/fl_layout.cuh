@@ -130,6 +130,19 @@ __host__ __device__ inline void block_unlin(const Geom& g, int b, int& bx, int& 
     by = r % g.NB[1];
     bx = r / g.NB[1];
 }
+// Programmatic dependent launch (sm_90+): hot-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (launch_k, fl_kernels.h), so
+// a kernel's CTAs are scheduled while its predecessor drains; each such kernel
+// waits here, before touching memory, until the predecessor grid has completed.
+#ifndef FL_PDL
+#define FL_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && FL_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 __host__ __device__ inline int key_col(const Geom& g, uint32_t key) { return int(key >> 6) / g.colblocks; }
 
 __host__ __device__ inline size_t node_index(const Geom& g, int i, int j, int k) {

@@ -31,6 +31,7 @@ constexpr int kSortThreads = 256;
 
 __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict__ cls, int* bcount,
                              int* bheavy) {
+    pdl_wait();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = st.key[i];
@@ -49,6 +50,7 @@ __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict
 
 __global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ bstart, int* bfill, uint32_t* skey,
                                uint32_t* sslot) {
+    pdl_wait();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t key = st.key[i];
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
                                                               const uint32_t* skey, const uint32_t* sslot,
                                                               uint32_t* perm, uint16_t* celltab, uint32_t* gk,
                                                               uint32_t* gv) {
+    pdl_wait();
     __shared__ uint32_t ik[kCountCap], iv[kCountCap], ok[kCountCap], ov[kCountCap];
     __shared__ int hist[64], fill[64];
     __shared__ uint16_t cs[kCellTab];
@@ -220,12 +223,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
 void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s) {
     if (n <= 0) return;  // (an empty slab)
-    k_sort_count<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, cls, bcount, bheavy);
+    launch_k(k_sort_count, dim3((n + 255) / 256), dim3(256), 0, s, g, st, n, cls, bcount, bheavy);
 }
 void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, int* bfill, uint32_t* skey,
                          uint32_t* sslot, cudaStream_t s) {
     if (n <= 0) return;
-    k_sort_scatter<<<(n + 255) / 256, 256, 0, s>>>(g, st, n, bstart, bfill, skey, sslot);
+    launch_k(k_sort_scatter, dim3((n + 255) / 256), dim3(256), 0, s, g, st, n, bstart, bfill, skey, sslot);
 }
 
 // ---------------------------------------------------------------------------
@@ -270,6 +273,7 @@ __device__ __forceinline__ int block_kind(const Geom& g, const int* __restrict__
 __global__ void __launch_bounds__(kListThreads) k_list_sums(Geom g, const int* __restrict__ bcount,
                                                             const int* __restrict__ bheavy, int* nbflag,
                                                             int4* tile_sum) {
+    pdl_wait();
     using Red = cub::BlockReduce<int4, kListThreads>;
     __shared__ typename Red::TempStorage tmp;
     const int n = g.nbtot + 2;
@@ -299,6 +303,7 @@ __global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, co
                                                              const int4* __restrict__ tile_sum, int* bstart,
                                                              int* nb_list, int* n_nb, BlockRec* recs, int* blockmap,
                                                              int* n_blocks) {
+    pdl_wait();
     using Scan = cub::BlockScan<int4, kListThreads>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int4 base;
@@ -365,8 +370,8 @@ void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bhe
                        int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
                        cudaStream_t s) {
     const int tiles = sort_list_tiles(g);
-    k_list_sums<<<tiles, kListThreads, 0, s>>>(g, bcount, bheavy, nbflag, tile_sum);
-    k_list_write<<<tiles, kListThreads, 0, s>>>(g, cap, bcount, bheavy, nbflag, tile_sum, bstart, nb_list, n_nb,
+    launch_k(k_list_sums, dim3(tiles), dim3(kListThreads), 0, s, g, bcount, bheavy, nbflag, tile_sum);
+    launch_k(k_list_write, dim3(tiles), dim3(kListThreads), 0, s, g, cap, bcount, bheavy, nbflag, tile_sum, bstart, nb_list, n_nb,
                                                 recs, blockmap, n_blocks);
 }
 
@@ -392,7 +397,7 @@ void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, i
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s) {
-    k_sort_blocks<<<grid, kSortThreads, 0, s>>>(g.nbtot, bcount, bstart, recs, n_blocks, cap, skey, sslot, perm,
+    launch_k(k_sort_blocks, dim3(grid), dim3(kSortThreads), 0, s, g.nbtot, bcount, bstart, recs, n_blocks, cap, skey, sslot, perm,
                                                 celltab, gk, gv);
 }
 }  // namespace fl
