@@ -669,7 +669,10 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid_upd = sms * 8;
-    grid_sort = sms * 4;
+#ifndef FL_SORT_CTAS
+#define FL_SORT_CTAS 8
+#endif
+    grid_sort = sms * FL_SORT_CTAS;
 
 
     // initial effector state from the shapes' defaults is set by upload()

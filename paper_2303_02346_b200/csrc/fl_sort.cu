@@ -27,7 +27,13 @@
 
 namespace fl {
 
-constexpr int kSortThreads = 256;
+#ifndef FL_SORT_THREADS
+#define FL_SORT_THREADS 256
+#endif
+#ifndef FL_COUNT_CAP
+#define FL_COUNT_CAP 1024
+#endif
+constexpr int kSortThreads = FL_SORT_THREADS;
 
 __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict__ cls, int* bcount,
                              int* bheavy) {
@@ -105,7 +111,7 @@ __device__ void cell_starts(KP k, int cnt, uint16_t* out, int tid) {
     out[tid] = uint16_t(tid == 64 ? cnt : lo);
 }
 
-constexpr int kCountCap = 2048;  // particles per block segment sorted by the counting path
+constexpr int kCountCap = FL_COUNT_CAP;  // particles per block segment sorted by the counting path
 
 // One CTA per non-empty particle block: counting sort of the segment by local
 // cell (64 buckets), then each cell's run is insertion-sorted by particle id
