@@ -100,3 +100,25 @@ def test_rollout_loss_parity(ref_available):
     rl, rper = r.rollout_loss(acts.values, 5)
     assert abs(l - rl) <= 1e-6 * abs(rl)
     np.testing.assert_allclose(per, rper, rtol=1e-6)
+
+
+def test_store_order_oversized_blocks():
+    """Blocks holding more particles than the per-block counting sort takes (1024) go
+    through the bitonic fallback; the store order must still be canonical."""
+    w = fl.build_scene(spec_for("c1", 32))
+    x = w.state.x.copy()
+    dx = w.scene.dx
+    # squeeze every particle into 2x2x2 particle blocks around the domain centre
+    lo = np.floor(0.5 / dx / 4) * 4 * dx
+    x = lo + (x - x.min(0)) / (x.max(0) - x.min(0) + 1e-12) * (8 * dx - 1e-6)
+    w.state.x = x
+    ws = fl.GpuWorkspace(w.scene)
+    keys, ids, na, x32 = ws.store_order(w.state)
+    blocks, counts = np.unique(keys[:na] >> 6, return_counts=True)
+    assert counts.max() > 1024
+    nd = w.scene.node_dims
+    NB = tuple((d + 3) // 4 for d in nd)
+    cpu = canonical_keys_cpu(x32[:, :na], dx, nd, NB)
+    assert np.array_equal(cpu, keys[:na].astype(np.uint64))
+    comp = (keys[:na].astype(np.uint64) << np.uint64(32)) | ids[:na].astype(np.uint64)
+    assert np.all(comp[1:] > comp[:-1])
