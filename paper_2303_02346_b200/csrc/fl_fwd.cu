@@ -58,18 +58,6 @@ void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double
     k_upload<<<(n + 255) / 256, 256, 0, s>>>(g, raw, n, x, v, F, C, meta, active, cls);
 }
 
-__global__ void k_make_sortkeys(PBuf st, int n, int idbits, uint64_t* ck, uint32_t* idx) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    ck[i] = (uint64_t(st.key[i]) << idbits) | uint64_t(st.id[i]);
-    idx[i] = uint32_t(i);
-}
-
-void launch_make_sortkeys(const Geom& g, const PBuf& st, int n, uint64_t* ck, uint32_t* idx, cudaStream_t s) {
-    if (n <= 0) return;
-    k_make_sortkeys<<<(n + 255) / 256, 256, 0, s>>>(st, n, g.idbits, ck, idx);
-}
-
 __global__ void k_gather(PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
@@ -133,24 +121,6 @@ void launch_download_rigid(PBuf st, int nmem, const int* member_id, double* x, c
 void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* x, cudaStream_t s) {
     if (nmem <= 0) return;
     k_rigid_x<<<(nmem + 255) / 256, 256, 0, s>>>(st, nmem, member_id, const_cast<double*>(x), 0);
-}
-
-// ---------------------------------------------------------------------------
-// block map rebuild for the backward (the list itself comes from fl_sort.cu)
-// ---------------------------------------------------------------------------
-
-__global__ void k_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap) {
-    int w = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nl = n_blocks[0], nh = n_blocks[1];
-    if (w >= nl + nh) return;
-    const int q = w < nl ? w : max_blocks - 1 - (w - nl);
-    blockmap[recs[q].block] = q + 1;
-}
-
-void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap,
-                         cudaStream_t s) {
-    if (max_blocks <= 0) return;
-    k_blockmap_set<<<(max_blocks + 255) / 256, 256, 0, s>>>(recs, n_blocks, max_blocks, blockmap);
 }
 
 // ---------------------------------------------------------------------------

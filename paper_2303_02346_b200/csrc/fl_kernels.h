@@ -106,9 +106,7 @@ constexpr int kRigidChunk = 2048;
 void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
                    const double* C, const uint32_t* meta, const uint8_t* active, const ClassInfo* cls,
                    cudaStream_t s);
-void launch_make_sortkeys(const Geom& g, const PBuf& st, int n, uint64_t* ck, uint32_t* idx, cudaStream_t s);
 void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
-void launch_blockmap_set(const BlockRec* recs, const int* n_blocks, int max_blocks, int* blockmap, cudaStream_t s);
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s);
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
