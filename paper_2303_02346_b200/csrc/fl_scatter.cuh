@@ -40,9 +40,8 @@ constexpr int kCellTab = 66;     // per block: 64 cell starts, end, largest cell
 // Payload staged as pay[f][rank][cell]: the payload phase (lanes = consecutive
 // particles of a cell, consecutive ranks) and the accumulate phase (lanes =
 // consecutive cells, same rank) both hit distinct banks.  The 6^3 node tile is
-// kept as four channel planes and filled by 27 ordered passes (one per
-// stencil offset): within a pass every cell adds into a different node, and
-// the pass order fixes the summation order of every node.
+// kept as four channel planes; each pass adds the gathered (cell, plane)
+// partials of every node in a fixed order (sc_accumulate).
 struct alignas(16) ScSmem {
     float pay[kPayF * kScR * kCS];
     float tile[4 * kTile];
@@ -95,11 +94,13 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
     for (int r = 0; r < nrank; r++) {
         const float* p = &sm.pay[r * kCS + c];
 #define PF(f) p[(f) * kPayPlane]
-        float wxa[3], wy[3], wz[3];
-        bspline_w(PF(0), wxa);
+        float wy[3], wz[3];
         bspline_w(PF(1), wy);
         bspline_w(PF(2), wz);
-        const float wx = ox == 0 ? wxa[0] : (ox == 1 ? wxa[1] : wxa[2]);
+        // only this thread's x weight (same operations as bspline_w)
+        const float fx0 = PF(0);
+        const float tx = ox == 0 ? 1.5f - fx0 : (ox == 1 ? fx0 - 1.0f : fx0 - 0.5f);
+        const float wx = ox == 1 ? 0.75f - tx * tx : 0.5f * tx * tx;
         const float m = (NCH == 4) ? PF(3) : 0.f;
         const float b00 = PF(A0 + 3), b01 = PF(A0 + 4), b02 = PF(A0 + 5);
         const float b10 = PF(A0 + 6), b11 = PF(A0 + 7), b12 = PF(A0 + 8);
