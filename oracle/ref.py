@@ -50,6 +50,8 @@ def lib():
             "ref_emitters": (None, [C.c_void_p, L, I, D, D]),
             "ref_loss_spec": (C.c_char_p, [C.c_void_p]),
             "ref_optimizer_spec": (C.c_char_p, [C.c_void_p]),
+            "ref_snapshot_dump": (C.c_char_p, [C.c_void_p]),
+            "ref_snapshot_load": (C.c_int, [C.c_void_p, C.c_char_p]),
             "ref_get_state": (None, [C.c_void_p, D, D, D, D, D, D, I, I, L, D, L]),
             "ref_set_state": (None, [C.c_void_p, D, D, D, D, D, D, I, I, L, D, L]),
             "ref_get_effector_state": (None, [C.c_void_p, D]),
@@ -197,6 +199,15 @@ class RefWorld:
 
     def loss_spec(self):
         return json.loads(self.l.ref_loss_spec(self.h).decode())
+
+    def snapshot_dump(self) -> dict:
+        """state_to_json<3> of the live state (io.hpp:144-190)."""
+        return json.loads(self.l.ref_snapshot_dump(self.h).decode())
+
+    def snapshot_load(self, snap: dict):
+        """state_from_json<3> into the live state (io.hpp:192-240)."""
+        if self.l.ref_snapshot_load(self.h, json.dumps(snap).encode()) != 0:
+            raise RuntimeError("reference rejected the snapshot")
 
     def optimizer_spec(self):
         s = self.l.ref_optimizer_spec(self.h).decode()

@@ -214,6 +214,20 @@ const char* ref_loss_spec(void* h) {
     s = static_cast<RefWorld*>(h)->w.loss_spec.dump();
     return s.c_str();
 }
+// versioned state snapshots (io.hpp:144-240)
+const char* ref_snapshot_dump(void* h) {
+    static thread_local std::string s;
+    s = state_to_json<3>(static_cast<RefWorld*>(h)->state).dump();
+    return s.c_str();
+}
+int ref_snapshot_load(void* h, const char* text) {
+    try {
+        state_from_json<3>(json::parse(text), static_cast<RefWorld*>(h)->state);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
 const char* ref_optimizer_spec(void* h) {
     static thread_local std::string s;
     s = static_cast<RefWorld*>(h)->w.optimizer_spec.dump();

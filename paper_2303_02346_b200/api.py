@@ -764,3 +764,50 @@ def grad_trajectory_batch(scene: Scene, state0: SimState, population: Sequence[A
     idx = {id(ws): i for i, ws in enumerate(pool.workspaces)}
     return pool._map(lambda ws, a: grad_trajectory(scene, states[idx[id(ws)]], a, loss, stride=stride,
                                                    window=window, ws=ws), list(population))
+
+
+# ---------------------------------------------------------------------------
+# versioned state snapshots in the reference's JSON format (io.hpp:144-240), so
+# states move between this engine and the reference (and on-disk parity dumps)
+# ---------------------------------------------------------------------------
+
+
+def state_to_json(scene: Scene, state: SimState) -> dict:
+    """state_to_json<3> (io.hpp:144-190); pulls the state from the device if needed."""
+    state._pull()
+    parts = []
+    for i in range(scene.n_particles):
+        parts.append({"x": state._x[i].tolist(), "v": state._v[i].tolist(), "F": state._F[i].ravel().tolist(),
+                      "C": state._C[i].ravel().tolist(), "material": int(scene.material_id[i]),
+                      "body": int(scene.body_id[i]), "mass": float(scene.mass[i]),
+                      "volume0": float(scene.volume0[i]), "activation": int(scene.activation_substep[i])})
+    effs = [{"t": e[0:3].tolist(), "R": e[3:12].tolist(), "v": e[12:15].tolist(), "w": e[15:18].tolist()}
+            for e in state._eff]
+    return {"version": 1, "dim": 3, "time": state._time, "substep_index": state._substep, "particles": parts,
+            "effectors": effs}
+
+
+def state_from_json(snap: dict, scene: Scene, state: SimState) -> None:
+    """state_from_json<3> (io.hpp:192-240) into `state`.  The per-particle constants
+    (material, body, mass, volume0, activation) belong to the Scene here, so the
+    snapshot must agree with them."""
+    if snap.get("version", 0) != 1:
+        raise EngineError("snapshot: unsupported version")
+    if snap.get("dim", 0) != 3:
+        raise EngineError("snapshot: dimension mismatch")
+    parts = snap["particles"]
+    if len(parts) != scene.n_particles:
+        raise EngineError("snapshot: particle count mismatch")
+    state._pull()
+    for i, p in enumerate(parts):
+        if (p["material"] != scene.material_id[i] or p["body"] != scene.body_id[i] or p["mass"] != scene.mass[i]
+                or p["volume0"] != scene.volume0[i] or p["activation"] != scene.activation_substep[i]):
+            raise EngineError(f"snapshot: particle {i} does not belong to this scene")
+        state._x[i] = p["x"]
+        state._v[i] = p["v"]
+        state._F[i] = np.asarray(p["F"], dtype=np.float64).reshape(3, 3)
+        state._C[i] = np.asarray(p["C"], dtype=np.float64).reshape(3, 3)
+    for k, e in enumerate(snap["effectors"][:len(state._eff)]):
+        state._eff[k] = list(e["t"]) + list(e["R"]) + list(e["v"]) + list(e["w"])
+    state._time = float(snap["time"])
+    state._substep = int(snap["substep_index"])

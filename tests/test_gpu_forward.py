@@ -122,3 +122,19 @@ def test_store_order_oversized_blocks():
     assert np.array_equal(cpu, keys[:na].astype(np.uint64))
     comp = (keys[:na].astype(np.uint64) << np.uint64(32)) | ids[:na].astype(np.uint64)
     assert np.all(comp[1:] > comp[:-1])
+
+
+def test_continue_from_reference_snapshot(ref_available):
+    """A snapshot the reference wrote mid-run (io.hpp state_to_json) continues on the
+    device with the same parity as a fresh scene."""
+    spec = spec_for("c5", 32)
+    w, r = pair(spec)
+    r.substep(w.init_action, 6)
+    fl.state_from_json(r.snapshot_dump(), w.scene, w.state)
+    ws = fl.GpuWorkspace(w.scene)
+    fl.mpm_substep(w.scene, w.state, w.init_action, ws, count=5)
+    r.substep(w.init_action, 5)
+    rs = r.state()
+    e = state_errors(w.state, rs, w.scene.dx)
+    assert w.state.substep_index == rs["substep"] == 11
+    assert e["x"] <= 1e-4 and e["v"] <= 5e-4 and e["F"] <= 1e-4 and e["C"] <= 1e-3, e
