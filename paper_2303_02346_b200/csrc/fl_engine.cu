@@ -454,7 +454,7 @@ struct Ctx {
     void upload(const flume_state_view* view);
     void download(flume_state_view* view);
     void sort_and_lists(StateBuf& st, Record& r);
-    void forward_substep(const double* action, StatePtr in, StatePtr out, Record& r, bool record_grid);
+    void forward_substep(const double* action, StatePtr in, StatePtr out, Record& r);
     void substep(const double* action, int count);
     void stage_grid(double* mass, double* vel);
     LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep);
@@ -1030,7 +1030,7 @@ void Ctx::return_bars(Record& r, BarBuf post) {
     launches += 4;
 }
 
-void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r, bool record_grid) {
+void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r) {
     advance_effectors(action);
     r.substep = substep_index;
     r.effk = make_effset(eff);
@@ -1115,8 +1115,11 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
         launches += 2;
     }
-    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0,
-                                    r.effk, r.cmask, bzero.p, int(bzero.n), stream));
+    // the adjoint's inputs (v0 = p/m, contact mask) only for substeps that keep a record
+    const bool keep = &r != scratch_rec.get();
+    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv,
+                                    keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, bzero.p,
+                                    int(bzero.n), stream));
     counters_clean = true;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
@@ -1153,7 +1156,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
 void Ctx::substep(const double* action, int count) {
     for (int i = 0; i < count; i++) {
         StatePtr nxt = get_state();
-        forward_substep(action, cur, nxt, *scratch_rec, false);
+        forward_substep(action, cur, nxt, *scratch_rec);
         put_state(cur);
         cur = nxt;
     }
@@ -1315,7 +1318,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     copy_state(*st, *cur);
     for (long t = 0; t < T; t++) {
         StatePtr nxt = get_state();
-        forward_substep(a->values + 6 * (t / a->segment_length), st, nxt, *scratch_rec, false);
+        forward_substep(a->values + 6 * (t / a->segment_length), st, nxt, *scratch_rec);
         put_state(st);
         st = nxt;
         if ((t + 1) % a->segment_length == 0) {
@@ -1482,7 +1485,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         RecordPtr rec = in_last ? get_record() : scratch_rec;
         StatePtr nxt = get_state();
         eff_pre[t] = eff;
-        forward_substep(a->values + 6 * (t / seglen), st, nxt, *rec, false);
+        forward_substep(a->values + 6 * (t / seglen), st, nxt, *rec);
         eff_post[t] = eff;
         if (in_last) {
             cache_recs.push_back(rec);
@@ -1547,7 +1550,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         for (long q = base; q < end; q++) {
             RecordPtr rec = get_record();
             StatePtr nxt = get_state();
-            forward_substep(a->values + 6 * (q / seglen), s, nxt, *rec, false);
+            forward_substep(a->values + 6 * (q / seglen), s, nxt, *rec);
             cache_recs.push_back(rec);
             cache_states.push_back(nxt);
             s = nxt;
@@ -1664,7 +1667,7 @@ void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, doub
     copy_state(*pre, *cur);
     launch_expand_f(pre->p, pre->n, d_cls.p, stream);  // full F cotangents out, like the reference
     RecordPtr rec = get_record();
-    forward_substep(action, pre, post, *rec, false);
+    forward_substep(action, pre, post, *rec);
     const std::vector<EffState> eff_stage = eff;
     check_error();
     for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
