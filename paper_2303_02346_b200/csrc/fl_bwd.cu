@@ -202,8 +202,8 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
 // ---------------------------------------------------------------------------
 // G2P adjoint (adjoint.hpp:281-365): gather + deterministic scatter of grid v_bar
 // ---------------------------------------------------------------------------
-template <bool HEAVY>
-__global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+template <bool HEAVY, int MINB>
+__global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                         const BlockRec* __restrict__ recs,
                                                         const int* __restrict__ n_blocks,
                                                         const uint16_t* __restrict__ celltab,
@@ -401,23 +401,23 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 2 : FL_LB_ADJG2P) k_adj_g2
     }
 }
 
+static decltype(&k_adj_g2p<false, FL_LB_ADJG2P>) adj_g2p_kernel(int v) {
+    return v == 0 ? k_adj_g2p<false, FL_LB_ADJG2P>
+                  : (v == 1 ? k_adj_g2p<true, FL_LBH_ADJG2P> : k_adj_g2p<true, FL_LBD_ADJG2P>);
+}
+
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, PBuf postst,
                     BarBuf post, float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar,
-                    float4* staging_bar, bool heavy, int* wq, cudaStream_t s) {
+                    float4* staging_bar, int variant, int* wq, cudaStream_t s) {
     const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_adj_g2p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaFuncSetAttribute(k_adj_g2p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
+    static bool attr[3] = {false, false, false};
+    if (!attr[variant]) {
+        cudaFuncSetAttribute(adj_g2p_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr[variant] = true;
     }
-    if (heavy)
-        launch_k(k_adj_g2p<true>, dim3(grid), dim3(kScThreads), smem, s, g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
-                                                       xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
-    else
-        launch_k(k_adj_g2p<false>, dim3(grid), dim3(kScThreads), smem, s, g, pre, perm, recs, n_blocks, celltab, cls, gridv, postst, post,
-                                                        xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
+    launch_k(adj_g2p_kernel(variant), dim3(grid), dim3(kScThreads), smem, s, g, pre, perm, recs, n_blocks, celltab,
+             cls, gridv, postst, post, xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
 }
 
 // ---------------------------------------------------------------------------
@@ -601,8 +601,8 @@ void launch_eff_final(const double* ring, int n_eff, long t0, int count, double*
 // ---------------------------------------------------------------------------
 // P2G adjoint (adjoint.hpp:414-470)
 // ---------------------------------------------------------------------------
-template <bool HEAVY>
-__global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+template <bool HEAVY, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                  const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                                  const ClassInfo* __restrict__ cls,
                                                  const float4* __restrict__ gridbar,
@@ -764,15 +764,16 @@ __global__ void __launch_bounds__(128, HEAVY ? 3 : FL_LB_ADJP2G) k_adj_p2g(Geom 
     }
 }
 
+static decltype(&k_adj_p2g<false, FL_LB_ADJP2G>) adj_p2g_kernel(int v) {
+    return v == 0 ? k_adj_p2g<false, FL_LB_ADJP2G>
+                  : (v == 1 ? k_adj_p2g<true, FL_LBH_ADJP2G> : k_adj_p2g<true, FL_LBD_ADJP2G>);
+}
+
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
-                    const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s) {
-    if (heavy)
-        launch_k(k_adj_p2g<true>, dim3(grid), dim3(128), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
-                                             nonfinite, out.cap, wq);
-    else
-        launch_k(k_adj_p2g<false>, dim3(grid), dim3(128), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar, xbar_tmp, Fbar_tmp, out,
-                                              nonfinite, out.cap, wq);
+                    const float* Fbar_tmp, BarBuf out, int* nonfinite, int variant, int* wq, cudaStream_t s) {
+    launch_k(adj_p2g_kernel(variant), dim3(grid), dim3(128), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar,
+             xbar_tmp, Fbar_tmp, out, nonfinite, out.cap, wq);
 }
 
 // inactive particles pass their bars through untouched
@@ -893,26 +894,19 @@ void launch_expand_f(PBuf st, int n, const ClassInfo* cls, cudaStream_t s) {
     k_expand_f<<<(n + 255) / 256, 256, 0, s>>>(st, n, cls);
 }
 
-int occupancy_grid_fwd(KGrid which, bool heavy);
+int occupancy_grid_fwd(KGrid which, int variant);
 
-int occupancy_grid(KGrid which, bool heavy) {
-    if (which == KG_P2G || which == KG_G2P) return occupancy_grid_fwd(which, heavy);
+int occupancy_grid(KGrid which, int variant) {
+    if (which == KG_P2G || which == KG_G2P) return occupancy_grid_fwd(which, variant);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (which == KG_ADJ_G2P) {
         const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
-        cudaFuncSetAttribute(k_adj_g2p<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaFuncSetAttribute(k_adj_g2p<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (heavy)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_g2p<true>, kScThreads, smem);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_g2p<false>, kScThreads, smem);
+        cudaFuncSetAttribute(adj_g2p_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_g2p_kernel(variant), kScThreads, smem);
     } else {
-        if (heavy)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_p2g<true>, 128, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adj_p2g<false>, 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_p2g_kernel(variant), 128, 0);
     }
     if (per < 1) per = 1;
     return sms * per;

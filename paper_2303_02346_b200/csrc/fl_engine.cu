@@ -351,6 +351,7 @@ struct Ctx {
     DevArr<double> d_up[4];
     DevArr<uint32_t> d_upmeta;
     DevArr<uint8_t> d_upactive;
+    int hvar = 1;  // heavy kernel variant (occupancy_grid)
     int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
     int grid_p2g_h = 0, grid_g2p_h = 0, grid_adj_h = 0, grid_ap = 0, grid_ap_h = 0;
 
@@ -658,14 +659,21 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     cub_bytes = std::max(b2, b3);
     cub_tmp.alloc(cub_bytes);
 
-    grid_p2g = occupancy_grid(KG_P2G, false);
-    grid_p2g_h = occupancy_grid(KG_P2G, true);
-    grid_g2p = occupancy_grid(KG_G2P, false);
-    grid_g2p_h = occupancy_grid(KG_G2P, true);
-    grid_adj = occupancy_grid(KG_ADJ_G2P, false);
-    grid_adj_h = occupancy_grid(KG_ADJ_G2P, true);
-    grid_ap = occupancy_grid(KG_ADJ_P2G, false);
-    grid_ap_h = occupancy_grid(KG_ADJ_P2G, true);
+    // heavy kernels: a scene dominated by SVD/rigid particles (c3) wants them at high
+    // occupancy; a mostly-liquid one (c4) at low occupancy beside the light kernel
+    {
+        long nh = 0;
+        for (int i = 0; i < N; i++) nh += classes[p_class[i]].heavy;
+        hvar = 2 * nh >= N ? 2 : 1;
+    }
+    grid_p2g = occupancy_grid(KG_P2G, 0);
+    grid_p2g_h = occupancy_grid(KG_P2G, hvar);
+    grid_g2p = occupancy_grid(KG_G2P, 0);
+    grid_g2p_h = occupancy_grid(KG_G2P, hvar);
+    grid_adj = occupancy_grid(KG_ADJ_G2P, 0);
+    grid_adj_h = occupancy_grid(KG_ADJ_G2P, hvar);
+    grid_ap = occupancy_grid(KG_ADJ_P2G, 0);
+    grid_ap_h = occupancy_grid(KG_ADJ_P2G, hvar);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid_upd = sms * 8;
@@ -1106,7 +1114,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     PROF(K_SORT, sort_and_lists(*in, r));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
-                        staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
+                        staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     if (slab()) {
         halo_exchange(r.blockmap, staging.p, nbflag);
@@ -1130,7 +1138,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     }
     PROF(K_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : grid_g2p, d_cls.p, r.gridv,
-                        rd, d_err.p, uint32_t(substep_index), hv, w, s);
+                        rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
     launches += 4;
@@ -1173,7 +1181,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
     EffSet es = make_effset(eff);
     dual([&](bool hv, int* w, cudaStream_t s) {
         launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
-                   staging.p, d_err.p, uint32_t(substep_index), hv, w, s);
+                   staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
     });
     if (slab()) {
         halo_exchange(r.blockmap, staging.p, nbflag);
@@ -1367,7 +1375,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
-                            r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv, w, s);
+                            r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
     if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
@@ -1376,7 +1384,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
-                            xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv, w, s);
+                            xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
     launches += 5;

@@ -152,8 +152,8 @@ void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaSt
 // P2G (mpm.hpp:249-287)
 // ---------------------------------------------------------------------------
 
-template <bool HEAVY>
-__global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
+template <bool HEAVY, int MINB>
+__global__ void __launch_bounds__(kScThreads, MINB) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
                                                     const BlockRec* __restrict__ recs,
                                                     const int* __restrict__ n_blocks,
                                                     const uint16_t* __restrict__ celltab,
@@ -257,21 +257,22 @@ __global__ void __launch_bounds__(kScThreads, HEAVY ? 1 : FL_LB_P2G) k_p2g(Geom 
     }
 }
 
+// kernel variant: 0 plain liquid, 1 SVD/rigid blocks in a mostly-liquid scene (low
+// occupancy, runs beside the light kernel), 2 SVD/rigid-dominated scene
+static decltype(&k_p2g<false, FL_LB_P2G>) p2g_kernel(int v) {
+    return v == 0 ? k_p2g<false, FL_LB_P2G> : (v == 1 ? k_p2g<true, FL_LBH_P2G> : k_p2g<true, FL_LBD_P2G>);
+}
+
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
-                uint32_t substep, bool heavy, int* wq, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
-        cudaFuncSetAttribute(k_p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
-        attr = true;
+                uint32_t substep, int variant, int* wq, cudaStream_t s) {
+    static bool attr[3] = {false, false, false};
+    if (!attr[variant]) {
+        cudaFuncSetAttribute(p2g_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
+        attr[variant] = true;
     }
-    if (heavy)
-        launch_k(k_p2g<true>, dim3(grid), dim3(kScThreads), sizeof(ScSmem), s, g, st, perm, recs, n_blocks, celltab, cls, staging, err,
-                                                            substep, wq);
-    else
-        launch_k(k_p2g<false>, dim3(grid), dim3(kScThreads), sizeof(ScSmem), s, g, st, perm, recs, n_blocks, celltab, cls, staging, err,
-                                                             substep, wq);
+    launch_k(p2g_kernel(variant), dim3(grid), dim3(kScThreads), sizeof(ScSmem), s, g, st, perm, recs, n_blocks,
+             celltab, cls, staging, err, substep, wq);
 }
 
 // ---------------------------------------------------------------------------
@@ -349,8 +350,8 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 // G2P (mpm.hpp:338-384) with the per-material return map
 // ---------------------------------------------------------------------------
 
-template <bool HEAVY>
-__global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
+template <bool HEAVY, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
                                              RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {
@@ -453,13 +454,15 @@ __global__ void __launch_bounds__(128, HEAVY ? 4 : FL_LB_G2P) k_g2p(Geom g, PBuf
     }
 }
 
+static decltype(&k_g2p<false, FL_LB_G2P>) g2p_kernel(int v) {
+    return v == 0 ? k_g2p<false, FL_LB_G2P> : (v == 1 ? k_g2p<true, FL_LBH_G2P> : k_g2p<true, FL_LBD_G2P>);
+}
+
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd, unsigned long long* err,
-                uint32_t substep, bool heavy, int* wq, cudaStream_t s) {
-    if (heavy)
-        launch_k(k_g2p<true>, dim3(grid), dim3(128), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
-    else
-        launch_k(k_g2p<false>, dim3(grid), dim3(128), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err, substep, wq);
+                uint32_t substep, int variant, int* wq, cudaStream_t s) {
+    launch_k(g2p_kernel(variant), dim3(grid), dim3(128), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err,
+             substep, wq);
 }
 
 __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
@@ -658,22 +661,15 @@ void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
     k_loss_final<<<1, 32 * kMaxLossTerms, 0, s>>>(partial, kLossBlocks, ls, mask, out);
 }
 
-int occupancy_grid_fwd(KGrid which, bool heavy) {
+int occupancy_grid_fwd(KGrid which, int variant) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (which == KG_P2G) {
-        cudaFuncSetAttribute(k_p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
-        cudaFuncSetAttribute(k_p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
-        if (heavy)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2g<true>, kScThreads, sizeof(ScSmem));
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_p2g<false>, kScThreads, sizeof(ScSmem));
+        cudaFuncSetAttribute(p2g_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_kernel(variant), kScThreads, sizeof(ScSmem));
     } else {
-        if (heavy)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_g2p<true>, 128, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_g2p<false>, 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_kernel(variant), 128, 0);
     }
     if (per < 1) per = 1;
     return sms * per;

@@ -110,13 +110,13 @@ void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t 
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s);
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
-                uint32_t substep, bool heavy, int* wq, cudaStream_t s);
+                uint32_t substep, int variant, int* wq, cudaStream_t s);
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
                         int* clear, int n_clear, cudaStream_t s);
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs,
                 const int* n_blocks, int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd,
-                unsigned long long* err, uint32_t substep, bool heavy, int* wq, cudaStream_t s);
+                unsigned long long* err, uint32_t substep, int variant, int* wq, cudaStream_t s);
 void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
 void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body,
                   const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
@@ -138,7 +138,7 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, PBuf postst,
                     BarBuf post, float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar,
-                    float4* staging_bar, bool heavy, int* wq, cudaStream_t s);
+                    float4* staging_bar, int variant, int* wq, cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                      double* eff_partial, const uint8_t* cmask, cudaStream_t s);
@@ -146,7 +146,7 @@ constexpr int kEffRing = 16;  // substeps whose effector-bar partials wait for o
 void launch_eff_final(const double* ring, int n_eff, long t0, int count, double* eff_out, cudaStream_t s);
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
-                    const float* Fbar_tmp, BarBuf out, int* nonfinite, bool heavy, int* wq, cudaStream_t s);
+                    const float* Fbar_tmp, BarBuf out, int* nonfinite, int variant, int* wq, cudaStream_t s);
 void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n_keep, int n_stored,
                       cudaStream_t s);
 void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
@@ -184,6 +184,7 @@ void launch_bars_pack(BarBuf bars, int pos0, int n, void* out, cudaStream_t s);
 void launch_bars_scatter(BarBuf bars, const void* in, const uint32_t* src, int n, cudaStream_t s);
 
 enum KGrid { KG_P2G = 0, KG_G2P = 1, KG_ADJ_G2P = 2, KG_ADJ_P2G = 3 };
-int occupancy_grid(KGrid which, bool heavy);  // resident CTAs per SM x SMs
+// resident CTAs per SM x SMs; variant 0 plain liquid, 1 heavy beside light, 2 heavy-dominated scene
+int occupancy_grid(KGrid which, int variant);
 
 }  // namespace fl

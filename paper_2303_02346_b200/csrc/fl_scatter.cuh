@@ -29,6 +29,32 @@ constexpr int kScThreads = 192;  // 64 cells x 3 planes
 #ifndef FL_LB_ADJP2G
 #define FL_LB_ADJP2G 5
 #endif
+// ... and for the SVD / rigid ("heavy") variants
+#ifndef FL_LBH_P2G
+#define FL_LBH_P2G 1
+#endif
+#ifndef FL_LBH_G2P
+#define FL_LBH_G2P 4
+#endif
+#ifndef FL_LBH_ADJG2P
+#define FL_LBH_ADJG2P 2
+#endif
+#ifndef FL_LBH_ADJP2G
+#define FL_LBH_ADJP2G 3
+#endif
+// ... and for the heavy variants when SVD/rigid blocks dominate the scene (launcher variant 2)
+#ifndef FL_LBD_P2G
+#define FL_LBD_P2G 4
+#endif
+#ifndef FL_LBD_G2P
+#define FL_LBD_G2P 6
+#endif
+#ifndef FL_LBD_ADJG2P
+#define FL_LBD_ADJG2P 4
+#endif
+#ifndef FL_LBD_ADJP2G
+#define FL_LBD_ADJP2G 5
+#endif
 #ifndef FL_SCR
 #define FL_SCR 8
 #endif
