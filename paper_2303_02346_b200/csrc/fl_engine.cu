@@ -1809,6 +1809,16 @@ int flume_group_create(const flume_scene_desc* desc, int n_ranks, const int* dev
     if (!desc || !out || n_ranks < 1) return FLUME_E_ARG;
     for (int r = 0; r < n_ranks; r++) out[r] = nullptr;
     auto grp = std::make_shared<fl::ThreadGroup>(n_ranks);
+    // direct NVLink peer copies between the ranks' devices where the topology allows
+    for (int a = 0; a < n_ranks; a++)
+        for (int b = 0; b < n_ranks; b++) {
+            const int da = devices ? devices[a] : 0, db = devices ? devices[b] : 0;
+            int can = 0;
+            if (da == db || cudaDeviceCanAccessPeer(&can, da, db) != cudaSuccess || !can) continue;
+            cudaSetDevice(da);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
     for (int r = 0; r < n_ranks; r++) {
         const int dev = devices ? devices[r] : 0;
         flume_ctx* ctx = new flume_ctx();
