@@ -1765,6 +1765,8 @@ int guard(flume_ctx* ctx, F&& f) {
     info->body_id = -1;
     info->substep = -1;
     try {
+        // calls may come from any host thread: make the context's device current
+        if (ctx) CK(cudaSetDevice(ctx->c.device));
         f();
         return FLUME_OK;
     } catch (const FlumeError& e) {
@@ -1881,6 +1883,7 @@ int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int
 
 int flume_ctx_destroy(flume_ctx* ctx) {
     if (!ctx) return FLUME_OK;
+    cudaSetDevice(ctx->c.device);  // the device buffers are freed on their own device
     cudaStreamSynchronize(ctx->c.stream);
     cudaStream_t s = ctx->c.stream, s2 = ctx->c.s2;
     cudaEvent_t e1 = ctx->c.ev_fork, e2 = ctx->c.ev_join, e3 = ctx->c.ev_snap;
