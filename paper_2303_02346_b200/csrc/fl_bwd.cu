@@ -27,8 +27,9 @@ __global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, L
     if (i >= n) return;
     const uint32_t key = st.key[i];
     if (key > key_inactive) return;  // departed slot
+    if (key == key_inactive && !ls.count_parked) return;
     const int body = cls[meta_cls(st.meta[i])].body;
-    const bool active = key < key_inactive;
+    const bool active = key < key_inactive || ls.act[st.id[i]] <= ls.substep;
     double g[3] = {0.0, 0.0, 0.0};
     bool any = false;
     for (int k = 0; k < ls.n; k++) {
@@ -37,10 +38,10 @@ __global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, L
         double d[3];
         if (t.kind == LK_TARGET) {
             if (!active) continue;
-            for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - t.goal[a];
+            for (int a = 0; a < 3; a++) d[a] = double(loss_x(ls, st, i, st.id[i], a)) - t.goal[a];
         } else {
             const uint32_t id = st.id[i];
-            for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - double(t.init[3 * size_t(id) + a]);
+            for (int a = 0; a < 3; a++) d[a] = double(loss_x(ls, st, i, id, a)) - double(t.init[3 * size_t(id) + a]);
         }
         const double nn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
         if (t.kind == LK_TARGET && t.squared) {

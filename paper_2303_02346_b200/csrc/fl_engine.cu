@@ -351,6 +351,7 @@ struct Ctx {
     DevArr<double> d_up[4];
     DevArr<uint32_t> d_upmeta;
     DevArr<uint8_t> d_upactive;
+    DevArr<float> d_x0;  // [3][N] positions by particle id at upload (LossSet.x0)
     int hvar = 1;  // heavy kernel variant (occupancy_grid)
     int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
     int grid_p2g_h = 0, grid_g2p_h = 0, grid_adj_h = 0, grid_ap = 0, grid_ap_h = 0;
@@ -461,8 +462,14 @@ struct Ctx {
     LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep);
     PointLossScratch pls;  // trajectory_chamfer / mixing_spread scratch (fl_loss.cu)
     void point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, double* out_dev, BarBuf* bars);
+    // ls evaluated on a state at `substep` (activation semantics of parked particles)
+    static LossSet at_substep(const LossSet& ls, long substep) {
+        LossSet l = ls;
+        l.substep = substep;
+        return l;
+    }
     uint32_t loss_mask(const flume_loss_desc* loss, int seg, int nseg) const;
-    void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg);
+    void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg, long substep);
     double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg);
     void adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre,
                       int t_slot);
@@ -836,6 +843,10 @@ void Ctx::upload(const flume_state_view* view) {
     launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, d_cls.p,
                   stream);
     launches++;
+    // positions by id at upload: a parked particle keeps them until its activation substep,
+    // which is where a loss evaluated at that substep sees it (emission happens in place)
+    d_x0.alloc(size_t(N) * 3);
+    CK(cudaMemcpyAsync(d_x0.p, raw->p.f, size_t(N) * 3 * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     scratch_rec->n_active = n_active;
     scratch_rec->n_keep = n_active + n_parked();
     scratch_rec->n_stored = N;
@@ -1231,6 +1242,11 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
     if (!loss || loss->n_terms <= 0) throw FlumeError(FLUME_E_SCENE, "scene has no loss specification");
     if (loss->n_terms > kMaxLossTerms) throw FlumeError(FLUME_E_ARG, "too many loss terms");
     ls.n = loss->n_terms;
+    ls.act = d_act.p;
+    ls.x0 = d_x0.p;
+    ls.n_all = N;
+    ls.count_parked = rank == 0 ? 1 : 0;
+    ls.substep = substep_index;
     for (int k = 0; k < ls.n; k++) {
         const flume_loss_term& t = loss->terms[k];
         LossTermDev& d = ls.t[k];
@@ -1290,7 +1306,8 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
 void Ctx::point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, double* out_dev, BarBuf* bars) {
     for (int k = 0; k < ls.n; k++) {
         if (!((mask >> k) & 1u) || ls.t[k].kind < LK_SPREAD) continue;
-        launch_point_loss(pls, st.p, st.n, d_cls.p, ls.t[k], seg, geom.key_inactive, out_dev, bars, d_err.p, stream);
+        launch_point_loss(pls, st.p, st.n, d_cls.p, ls, ls.t[k], seg, geom.key_inactive, out_dev, bars, d_err.p,
+                          stream);
         launches += 5;
     }
 }
@@ -1302,7 +1319,8 @@ uint32_t Ctx::loss_mask(const flume_loss_desc* loss, int seg, int nseg) const {
     return m;
 }
 
-void Ctx::eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg) {
+void Ctx::eval_loss(StateBuf& st, const LossSet& ls0, uint32_t mask, double* out_dev, int seg, long substep) {
+    const LossSet ls = at_substep(ls0, substep);
     // per-slab partial; the segment losses are all-reduced once after the rollout
     launch_loss(st.p, st.n, d_cls.p, ls, mask, loss_partial.p, out_dev, geom.key_inactive, stream);
     launches += 2;
@@ -1331,7 +1349,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
         st = nxt;
         if ((t + 1) % a->segment_length == 0) {
             int seg = int((t + 1) / a->segment_length) - 1;
-            eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, seg);
+            eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, seg, substep_index);
         }
     }
     allreduce(loss_out.p, size_t(a->n_segments), DType::F64, ROp::Sum);
@@ -1506,7 +1524,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         if ((t + 1) % stride == 0) take_snapshot(t + 1, st);
         if ((t + 1) % seglen == 0) {
             int seg = int((t + 1) / seglen) - 1;
-            eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, seg);
+            eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, seg, substep_index);
         }
     }
     retire_spilled(true);
@@ -1569,11 +1587,12 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             int seg = int((t + 1) / seglen) - 1;
             ensure_cached(t);
             StateBuf& boundary = *cache_states[size_t(t + 1 - cache_base)];
-            launch_loss_grad(boundary.p, boundary.n, d_cls.p, ls, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
+            const LossSet lsb = at_substep(ls, s0 + t + 1);
+            launch_loss_grad(boundary.p, boundary.n, d_cls.p, lsb, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
                              geom.key_inactive, stream);
             launches++;
             BarBuf bb{barsA.p, N};
-            point_losses(boundary, ls, loss_mask(loss, seg, nseg), seg, nullptr, &bb);
+            point_losses(boundary, lsb, loss_mask(loss, seg, nseg), seg, nullptr, &bb);
         }
         ensure_cached(t);
         const size_t k = size_t(t - cache_base);

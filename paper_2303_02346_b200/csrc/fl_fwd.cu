@@ -608,17 +608,18 @@ __global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const Clas
         const int body = cls[meta_cls(st.meta[i])].body;
         const uint32_t key = st.key[i];
         if (key > key_inactive) continue;  // departed slot: counted on the particle's new slab
-        const bool active = key < key_inactive;
+        if (key == key_inactive && !ls.count_parked) continue;
+        const bool active = key < key_inactive || ls.act[st.id[i]] <= ls.substep;
         for (int k = 0; k < ls.n; k++) {
             if (!((mask >> k) & 1u) || ls.t[k].body != body || ls.t[k].kind > LK_HOLD) continue;
             const LossTermDev& t = ls.t[k];
             double d[3];
             if (t.kind == LK_TARGET) {
                 if (!active) continue;
-                for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - t.goal[a];
+                for (int a = 0; a < 3; a++) d[a] = double(loss_x(ls, st, i, st.id[i], a)) - t.goal[a];
             } else {
                 const uint32_t id = st.id[i];
-                for (int a = 0; a < 3; a++) d[a] = double(st.x(a)[i]) - double(t.init[3 * size_t(id) + a]);
+                for (int a = 0; a < 3; a++) d[a] = double(loss_x(ls, st, i, id, a)) - double(t.init[3 * size_t(id) + a]);
             }
             const double nn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
             acc[k] += (t.kind == LK_TARGET && t.squared) ? nn * nn : nn;

@@ -78,7 +78,20 @@ struct LossTermDev {
 struct LossSet {
     int n;
     LossTermDev t[kMaxLossTerms];
+    // a parked (not yet emitted) particle counts as active once the state's substep
+    // index reaches its activation substep (types.hpp:109), before its emission
+    const int* act;   // activation substep by particle id
+    long substep;     // substep index of the evaluated state
+    // emission rewrites a particle's slot in place at the start of its activation substep;
+    // at that substep a loss uses its parked position (SoA [3][n_all] by id), as the
+    // reference's state still holds it when the loss is evaluated
+    const float* x0;
+    int n_all;
+    int count_parked;  // slabs: parked particles are replicated, only rank 0 counts them
 };
+__host__ __device__ inline float loss_x(const LossSet& ls, const PBuf& st, int i, uint32_t id, int a) {
+    return ls.act[id] == ls.substep ? ls.x0[size_t(a) * ls.n_all + id] : st.x(a)[i];
+}
 
 constexpr int kLossBlocks = 296;
 
@@ -96,9 +109,9 @@ struct PointLossScratch {
     ~PointLossScratch();
 };
 // eval (bars == nullptr): adds weight * value into *out; grad: adds d/dx into bars
-void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossTermDev& t,
-                       int seg, uint32_t key_inactive, double* out, BarBuf* bars, unsigned long long* err,
-                       cudaStream_t s);
+void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
+                       const LossTermDev& t, int seg, uint32_t key_inactive, double* out, BarBuf* bars,
+                       unsigned long long* err, cudaStream_t s);
 constexpr int kEffBlocks = 1184;
 constexpr int kRigidChunk = 2048;
 

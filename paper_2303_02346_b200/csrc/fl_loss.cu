@@ -24,21 +24,23 @@ constexpr int kTileP = 256;   // points staged per shared-memory tile
 // body compaction
 // ---------------------------------------------------------------------------
 __global__ void k_body_flags(PBuf st, int n, const ClassInfo* __restrict__ cls, int body, uint32_t key_inactive,
-                             int* flags) {
+                             const int* __restrict__ act, long substep, int* flags) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    flags[i] = (st.key[i] < key_inactive && cls[meta_cls(st.meta[i])].body == body) ? 1 : 0;
+    const uint32_t key = st.key[i];
+    const bool active = key < key_inactive || (key == key_inactive && act[st.id[i]] <= substep);  // (one rank)
+    flags[i] = (active && cls[meta_cls(st.meta[i])].body == body) ? 1 : 0;
 }
 
 __global__ void k_body_gather(PBuf st, int n, const int* __restrict__ flags, const int* __restrict__ pos,
-                              int* idx, double* px, int* count) {
+                              LossSet ls, int* idx, double* px, int* count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (i == n - 1) *count = pos[i] + flags[i];
     if (!flags[i]) return;
     const int k = pos[i];
     idx[k] = i;
-    for (int a = 0; a < 3; a++) px[3 * size_t(k) + a] = double(st.x(a)[i]);
+    for (int a = 0; a < 3; a++) px[3 * size_t(k) + a] = double(loss_x(ls, st, i, st.id[i], a));
 }
 
 // ---------------------------------------------------------------------------
@@ -318,21 +320,21 @@ PointLossScratch::~PointLossScratch() {
 }
 
 static void compact_body(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, int body,
-                         uint32_t key_inactive, cudaStream_t s) {
+                         uint32_t key_inactive, const LossSet& ls, cudaStream_t s) {
     const int grid = (n + 255) / 256;
-    k_body_flags<<<grid, 256, 0, s>>>(st, n, cls, body, key_inactive, w.flags);
+    k_body_flags<<<grid, 256, 0, s>>>(st, n, cls, body, key_inactive, ls.act, ls.substep, w.flags);
     cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.flags, w.pos, n, s);
-    k_body_gather<<<grid, 256, 0, s>>>(st, n, w.flags, w.pos, w.idx, w.px, w.count);
+    k_body_gather<<<grid, 256, 0, s>>>(st, n, w.flags, w.pos, ls, w.idx, w.px, w.count);
 }
 
 // number of member chunks for the G -> A stage (<= kChamferChunks)
 static int chamfer_chunk(int n) { return (n + kChamferChunks - 1) / kChamferChunks; }
 
-void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossTermDev& t,
-                       int seg, uint32_t key_inactive, double* out, BarBuf* bars, unsigned long long* err,
-                       cudaStream_t s) {
+void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
+                       const LossTermDev& t, int seg, uint32_t key_inactive, double* out, BarBuf* bars,
+                       unsigned long long* err, cudaStream_t s) {
     if (n <= 0) return;
-    compact_body(w, st, n, cls, t.body, key_inactive, s);
+    compact_body(w, st, n, cls, t.body, key_inactive, ls, s);
     const int grid_a = (n + kLT - 1) / kLT;  // upper bound on the member count
     if (t.kind == LK_SPREAD) {
         if (!bars) {

@@ -78,3 +78,20 @@ def test_chamfer_rerun_bit_identical():
         g = fl.grad_trajectory(w.scene, w.state, acts, fl.LossEvaluator(w.scene, w.loss_spec, w.state), ws=ws)
         out.append((g.loss, np.asarray(g.action_grad).copy()))
     assert out[0][0] == out[1][0] and np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("kind", ["target_point", "hold_initial", "trajectory_chamfer"])
+def test_loss_on_emitter_body_at_activation_boundaries(ref_available, kind):
+    """c2's stream body emits one particle per substep; segment boundaries fall on
+    activation substeps, where the reference counts the not-yet-emitted particle as
+    active at its parked position (types.hpp:109, losses.hpp gather)."""
+    spec = spec_for("c2", 64)
+    term = {"kind": kind, "body": "stream"}
+    if kind == "target_point":
+        term["goal"] = [0.5, 0.3, 0.5]
+    if kind == "trajectory_chamfer":
+        term["goal_trajectory"] = _goal_sets(np.random.default_rng(9), 2, 40)
+    spec["loss"] = term
+    l, per, rl, rper, tg, rg = _run(spec, 3, 5)
+    np.testing.assert_allclose(per, rper, rtol=1e-6)
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
