@@ -137,3 +137,27 @@ def test_checkpoint_spill_to_host_identical():
         out.append((g.loss, np.asarray(g.action_grad).copy(), g.snapshots))
     for l, gr, ns in out[1:]:
         assert l == out[0][0] and np.array_equal(gr, out[0][1]) and ns == out[0][2] == 21 // 4 + 1
+
+
+def test_grad_through_cfl_clamp(ref_available):
+    """A blob faster than cfl * dx / dt: every G2P clamps |v| (mpm.hpp:322-328) and the
+    adjoint zeroes v_raw_bar there (adjoint.hpp:281-365)."""
+    from tests.test_gpu_kat import _free_blob
+    spec = _free_blob(v=(400.0, 50.0, 0.0))
+    spec["loss"] = {"kind": "target_point", "body": "blob", "goal": [0.8, 0.5, 0.5]}
+    spec["effectors"] = spec_for("c1", 32)["effectors"]
+    spec["action_bounds"] = spec_for("c1", 32)["action_bounds"]
+    spec["optimizer"] = {"n_segments": 1, "segment_length": 6, "init": [0.5, 0.0, 0.0, 0, 0, 0]}
+    tg, rg = _grad_both(spec, 1, 6)
+    assert abs(tg.loss - rg["loss"]) <= 1e-5 * abs(rg["loss"])
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
+
+
+@pytest.mark.parametrize("name,res", [("c1", None), ("c4", 32)])
+def test_grad_hard_contact(ref_available, name, res):
+    """hard_contact: the step contact weight instead of exp(-d) (mpm.hpp:120-128)."""
+    spec = spec_for(name, res)
+    spec["hard_contact"] = True
+    tg, rg = _grad_both(spec, 1, 8)
+    assert abs(tg.loss - rg["loss"]) <= 1e-5 * abs(rg["loss"])
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
