@@ -161,3 +161,13 @@ def test_grad_hard_contact(ref_available, name, res):
     tg, rg = _grad_both(spec, 1, 8)
     assert abs(tg.loss - rg["loss"]) <= 1e-5 * abs(rg["loss"])
     assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
+
+
+@pytest.mark.parametrize("friction", ["sticky", 0.0])
+def test_grad_effector_friction_modes(ref_available, friction):
+    """Sticky (v_rel' = 0) and frictionless effectors (mpm.hpp:79-117, 146-161)."""
+    spec = spec_for("c1", 32)
+    spec["effectors"][0]["friction"] = friction
+    tg, rg = _grad_both(spec, 1, 8)
+    assert abs(tg.loss - rg["loss"]) <= 1e-5 * abs(rg["loss"])
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
