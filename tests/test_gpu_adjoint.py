@@ -169,5 +169,26 @@ def test_grad_effector_friction_modes(ref_available, friction):
     spec = spec_for("c1", 32)
     spec["effectors"][0]["friction"] = friction
     tg, rg = _grad_both(spec, 1, 8)
+    assert np.max(np.abs(rg["grad"])) > 0
+    assert abs(tg.loss - rg["loss"]) <= 1e-5 * abs(rg["loss"])
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
+
+
+SHAPES = {
+    "sphere": {"type": "sphere", "radius": 0.09},
+    "capsule": {"type": "capsule", "radius": 0.05, "a": [0.0, -0.12, 0.0], "b": [0.0, 0.12, 0.05]},
+    "cylinder": {"type": "cylinder", "radius": 0.07, "half_height": 0.12, "axis_angle": [0.4, 0.0, 0.3]},
+    "halfspace": {"type": "halfspace", "normal": [-1.0, 0.2, 0.0], "offset": -0.02},
+}
+
+
+@pytest.mark.parametrize("shape", list(SHAPES))
+def test_grad_effector_shapes(ref_available, shape):
+    """Every SDF shape (sdf.hpp:131-339): contact forward, normal and pose VJPs."""
+    spec = spec_for("c1", 32)
+    spec["effectors"][0]["shape"] = dict(SHAPES[shape], center=[0.0, 0.0, 0.0])
+    spec["effectors"][0]["angular_velocity"] = [0.0, 0.0, 0.3]
+    tg, rg = _grad_both(spec, 1, 10)
+    assert np.max(np.abs(rg["grad"])) > 0  # the effector is in contact
     assert abs(tg.loss - rg["loss"]) <= 1e-5 * abs(rg["loss"])
     assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
