@@ -133,16 +133,17 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
         const float b20 = PF(A0 + 9), b21 = PF(A0 + 10), b22 = PF(A0 + 11);
         const float a0x = PF(A0) + b00 * oxf, a0y = PF(A0 + 1) + b10 * oxf, a0z = PF(A0 + 2) + b20 * oxf;
 #undef PF
+        // a + B o with o in {0,1,2} written out (b*0, b*1, b*2 are exact, so the sums are
+        // the same as a + b*o; IEEE rules keep the compiler from dropping the multiplies)
+#define FL_STEP(base, d, k) ((k) == 0 ? (base) : ((k) == 1 ? (base) + (d) : (base) + 2.f * (d)))
 #pragma unroll
         for (int oy = 0; oy < 3; oy++) {
-            const float oyf = float(oy);
-            const float ayx = a0x + b01 * oyf, ayy = a0y + b11 * oyf, ayz = a0z + b21 * oyf;
+            const float ayx = FL_STEP(a0x, b01, oy), ayy = FL_STEP(a0y, b11, oy), ayz = FL_STEP(a0z, b21, oy);
             const float wxy = wx * wy[oy];
 #pragma unroll
             for (int oz = 0; oz < 3; oz++) {
-                const float ozf = float(oz);
                 const float w = wxy * wz[oz];
-                const float vx = ayx + b02 * ozf, vy = ayy + b12 * ozf, vz = ayz + b22 * ozf;
+                const float vx = FL_STEP(ayx, b02, oz), vy = FL_STEP(ayy, b12, oz), vz = FL_STEP(ayz, b22, oz);
                 float* ac = acc[oy * 3 + oz];
                 if (NCH == 4) {
                     ac[0] += w * m;
@@ -157,6 +158,7 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
             }
         }
     }
+#undef FL_STEP
     // fold: partial sums -> shared memory -> per-node fixed-order gather
     float4* part = reinterpret_cast<float4*>(sm.pay);  // [64 cells][3 planes][9 nodes]
     __syncthreads();                                   // the payload has been read
