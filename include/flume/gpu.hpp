@@ -278,13 +278,42 @@ public:
                 term.goal_points = goal_pts_[q].data();
                 q++;
             }
-        desc_ = flume_loss_desc{int(terms_.size()), terms_.data()};
+        desc_ = flume_loss_desc{};
+        desc_.n_terms = int(terms_.size());
+        desc_.terms = terms_.data();
+        desc_.attraction_body = -1;
     }
     Loss(const Loss&) = delete;
     Loss& operator=(const Loss&) = delete;
     const flume_loss_desc* desc() const { return &desc_; }
 
+    // LossEvaluator::enable_attraction (losses.hpp:350-355)
+    void enable_attraction(int body, Real weight, Real radius, Real tau) {
+        desc_.attraction_body = body < 0 ? terms_.at(0).body : body;
+        desc_.attraction_weight = weight;
+        desc_.attraction_radius = radius;
+        desc_.attraction_tau = tau;
+    }
+    // LossEvaluator::per_particle (losses.hpp:367-390), evaluated on the device
+    std::vector<Real> per_particle(const SimState<3>& state, Workspace& ws) const {
+        ws.upload(state);
+        std::vector<Real> out(state.particles.size());
+        check(ws.ctx(), flume_loss_per_particle(ws.ctx(), &desc_, out.data()));
+        return out;
+    }
+    // LossEvaluator::refresh_attraction (losses.hpp:357-363)
+    void refresh_attraction(const SimState<3>& state, Workspace& ws) {
+        if (!(desc_.attraction_weight > 0)) return;
+        std::vector<Real> all = per_particle(state, ws);
+        prev_.clear();
+        for (size_t i = 0; i < state.particles.size(); i++)
+            if (state.particles[i].body_id == desc_.attraction_body) prev_.push_back(all[i]);
+        desc_.n_prev = long(prev_.size());
+        desc_.prev_losses = prev_.data();
+    }
+
 private:
+    std::vector<Real> prev_;
     std::vector<flume_loss_term> terms_;
     std::vector<std::vector<long>> goal_off_;
     std::vector<std::vector<double>> goal_pts_;

@@ -12,6 +12,7 @@
  *   flume_stage_grid                            p2g + grid_update mpm.hpp:249-320
  *   flume_adjoint_substep                       adjoint_substep  adjoint.hpp:476-548
  *   flume_rollout_loss                          rollout_loss     grad.hpp:15-41
+ *   flume_loss_per_particle                     LossEvaluator::per_particle losses.hpp:367
  *   flume_grad_trajectory                       grad_trajectory  grad.hpp:61-134
  *                                               (+ CheckpointStore checkpoint.hpp:11-50)
  *   flume_set_mode                              SimConfig::hard_contact types.hpp:65
@@ -32,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FLUME_B200_ABI_VERSION 2
+#define FLUME_B200_ABI_VERSION 3
 
 typedef enum {
     FLUME_OK = 0,
@@ -166,6 +167,16 @@ typedef struct {
 typedef struct {
     int n_terms;
     const flume_loss_term* terms;
+    /* attraction term: the optimizer's gradient-sharing surrogate, added at every segment
+       boundary (LossEvaluator::enable_attraction / refresh_attraction, losses.hpp:348-363;
+       attraction_loss, losses.hpp:168-218).  On when attraction_weight > 0 and n_prev > 0.
+       Single-rank contexts only. */
+    int attraction_body;       /* < 0: the first term's body (primary_body) */
+    double attraction_weight;
+    double attraction_radius;  /* world units (optimize_dp passes 3 dx when its config says 0) */
+    double attraction_tau;     /* <= 0: max(0.1 * median(prev_losses), 1e-9) */
+    long n_prev;               /* must equal the body's member count (else FLUME_E_ENGINE) */
+    const double* prev_losses; /* previous iterate's per_particle losses, body members in id order */
 } flume_loss_desc;
 
 /* ActionTrajectory (actions.hpp:13-39): values = n_segments*6 */
@@ -260,6 +271,11 @@ int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume
 int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long stride,
                           long window, double* action_grad, double* loss_out, double* full_loss,
                           double* per_segment, long* snapshots);
+/* LossEvaluator::per_particle (losses.hpp:367-390) of the context's state: per particle id,
+   the sum over the loss terms on its body of its unweighted distance (target_point,
+   hold_initial, nearest point of the last trajectory_chamfer goal set); feeds
+   flume_loss_desc.prev_losses of the next optimizer iterate.  Single-rank contexts. */
+int flume_loss_per_particle(flume_ctx* ctx, const flume_loss_desc* loss, double* out);
 int flume_adjoint_substep(flume_ctx* ctx, const double action[6], double* x_bar, double* v_bar, double* F_bar,
                           double* C_bar, double* eff_bars /* n_eff*12: t_bar[3], R_bar[9] */,
                           double* action_bar);

@@ -62,6 +62,8 @@ def lib():
             "ref_rollout_loss": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D, C.c_long, D, D]),
             "ref_grad_trajectory": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D, C.c_long, C.c_long, D, D, D, D, L]),
             "ref_adjoint_substep": (C.c_int, [C.c_void_p, D, D, D, D, D, D, D]),
+            "ref_set_attraction": (None, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double, D]),
+            "ref_per_particle": (C.c_int, [C.c_void_p, D, D]),
         }
         for k, (r, a) in sig.items():
             f = getattr(l, k)
@@ -196,6 +198,19 @@ class RefWorld:
         ab = np.zeros(6) if action_bar is None else np.array(action_bar, dtype=np.float64)
         self._check(self.l.ref_adjoint_substep(self.h, _p(a), _p(xb), _p(vb), _p(Fb), _p(Cb), _p(eb), _p(ab)))
         return xb, vb, Fb, Cb, eb, ab
+
+    def set_attraction(self, body, weight, radius, tau, refresh_x=None):
+        """enable_attraction + refresh_attraction(state with x = refresh_x) for later calls."""
+        rx = None if refresh_x is None else np.ascontiguousarray(refresh_x, dtype=np.float64)
+        self._att_keep = rx
+        self.l.ref_set_attraction(self.h, int(body), float(weight), float(radius), float(tau), _p(rx))
+
+    def per_particle(self, x=None):
+        """LossEvaluator::per_particle of the live state (positions replaced by x if given)."""
+        xs = None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+        out = np.zeros(self.n)
+        self._check(self.l.ref_per_particle(self.h, _p(xs), _p(out)))
+        return out
 
     def loss_spec(self):
         return json.loads(self.l.ref_loss_spec(self.h).decode())

@@ -29,7 +29,23 @@ struct RefWorld {
     World<3> w;
     SimState<3> state;  // the live state the calls mutate
     MpmWorkspace<3> ws;
+    // attraction (LossEvaluator::enable_attraction / refresh_attraction, losses.hpp:350-363)
+    bool att_on = false;
+    int att_body = -1;
+    Real att_weight = 0, att_radius = 0, att_tau = 0;
+    SimState<3> att_refresh;  // the state refresh_attraction reads
 };
+
+// the LossEvaluator a call uses: built from the live state like the reference's
+// drivers do, with the attraction term enabled and refreshed when configured
+std::unique_ptr<LossEvaluator<3>> make_le(RefWorld* rw) {
+    auto le = std::make_unique<LossEvaluator<3>>(rw->w.scene, rw->w.loss_spec, rw->state);
+    if (rw->att_on) {
+        le->enable_attraction(rw->att_body, rw->att_weight, rw->att_radius, rw->att_tau);
+        le->refresh_attraction(rw->att_refresh);
+    }
+    return le;
+}
 
 thread_local std::string g_err;
 thread_local long g_err_pid = -1;
@@ -346,9 +362,9 @@ int ref_rollout_loss(void* h, int nseg, int seglen, const double* actions, long 
     RefWorld* rw = static_cast<RefWorld*>(h);
     return guarded([&] {
         ActionTrajectory a = make_actions(nseg, seglen, actions);
-        LossEvaluator<3> le(rw->w.scene, rw->w.loss_spec, rw->state);
+        auto le = make_le(rw);
         std::vector<Real> per;
-        *loss = rollout_loss(rw->w.scene, rw->state, a, le, window, &per);
+        *loss = rollout_loss(rw->w.scene, rw->state, a, *le, window, &per);
         if (per_segment)
             for (int s = 0; s < nseg; s++) per_segment[s] = per[size_t(s)];
     });
@@ -360,8 +376,8 @@ int ref_grad_trajectory(void* h, int nseg, int seglen, const double* actions, lo
     RefWorld* rw = static_cast<RefWorld*>(h);
     return guarded([&] {
         ActionTrajectory a = make_actions(nseg, seglen, actions);
-        LossEvaluator<3> le(rw->w.scene, rw->w.loss_spec, rw->state);
-        TrajectoryGrad<3> tg = grad_trajectory(rw->w.scene, rw->state, a, le, stride, window);
+        auto le = make_le(rw);
+        TrajectoryGrad<3> tg = grad_trajectory(rw->w.scene, rw->state, a, *le, stride, window);
         for (int s = 0; s < nseg; s++)
             for (int k = 0; k < 6; k++) grad[s * 6 + k] = tg.action_grad[size_t(s)][size_t(k)];
         if (loss) *loss = tg.loss;
@@ -369,6 +385,36 @@ int ref_grad_trajectory(void* h, int nseg, int seglen, const double* actions, lo
         if (per_segment)
             for (int s = 0; s < nseg; s++) per_segment[s] = tg.per_segment[size_t(s)];
         if (snapshots) *snapshots = long(tg.snapshots);
+    });
+}
+
+// Attraction for the following rollout_loss / grad_trajectory calls: weight <= 0 turns it
+// off; refresh_x (n*3) = positions of the state refresh_attraction reads (the live state
+// with x replaced)
+void ref_set_attraction(void* h, int body, double weight, double radius, double tau, const double* refresh_x) {
+    RefWorld* rw = static_cast<RefWorld*>(h);
+    rw->att_on = weight > 0;
+    rw->att_body = body;
+    rw->att_weight = weight;
+    rw->att_radius = radius;
+    rw->att_tau = tau;
+    rw->att_refresh = rw->state;
+    if (refresh_x)
+        for (size_t i = 0; i < rw->att_refresh.particles.size(); i++)
+            for (int a = 0; a < 3; a++) rw->att_refresh.particles[i].x[a] = refresh_x[3 * i + a];
+}
+
+// LossEvaluator::per_particle (losses.hpp:367) of the live state with x replaced by xs (n*3) if given
+int ref_per_particle(void* h, const double* xs, double* out) {
+    RefWorld* rw = static_cast<RefWorld*>(h);
+    return guarded([&] {
+        LossEvaluator<3> le(rw->w.scene, rw->w.loss_spec, rw->state);
+        SimState<3> st = rw->state;
+        if (xs)
+            for (size_t i = 0; i < st.particles.size(); i++)
+                for (int a = 0; a < 3; a++) st.particles[i].x[a] = xs[3 * i + a];
+        std::vector<Real> v = le.per_particle(st);
+        for (size_t i = 0; i < v.size(); i++) out[i] = v[i];
     });
 }
 

@@ -12,7 +12,7 @@ from pathlib import Path
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("FLUME_B200_LIB", _PKG / "libflume_b200.so"))
 
-ABI_VERSION = 2  # include/flume_b200.h FLUME_B200_ABI_VERSION
+ABI_VERSION = 3  # include/flume_b200.h FLUME_B200_ABI_VERSION
 
 FLUME_OK = 0
 FLUME_E_ENGINE = 1
@@ -84,7 +84,9 @@ class LossTerm(C.Structure):
 
 
 class LossDesc(C.Structure):
-    _fields_ = [("n_terms", C.c_int), ("terms", C.POINTER(LossTerm))]
+    _fields_ = [("n_terms", C.c_int), ("terms", C.POINTER(LossTerm)), ("attraction_body", C.c_int),
+                ("attraction_weight", C.c_double), ("attraction_radius", C.c_double),
+                ("attraction_tau", C.c_double), ("n_prev", C.c_long), ("prev_losses", C.POINTER(C.c_double))]
 
 
 class Actions(C.Structure):
@@ -136,6 +138,7 @@ EXPORTS = {
     "flume_timer_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "flume_substep": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     "flume_stage_grid": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "flume_loss_per_particle": (C.c_int, [C.c_void_p, C.POINTER(LossDesc), C.POINTER(C.c_double)]),
     "flume_rollout_loss": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long,
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "flume_grad_trajectory": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long, C.c_long,

@@ -357,6 +357,38 @@ class LossEvaluator:
             for a in range(3):
                 self._arr[i].goal[a] = float(g[a])
         self.desc = _abi.LossDesc(len(terms), C.cast(self._arr, C.POINTER(_abi.LossTerm)))
+        self.desc.attraction_body = -1
+        self._prev = None
+
+    # -- the optimizer's gradient-sharing surrogate (losses.hpp:104-218, 348-363) --
+    def enable_attraction(self, body: int, weight: float, radius: float, tau: float) -> None:
+        """LossEvaluator::enable_attraction: body < 0 selects the first term's body."""
+        self.desc.attraction_body = int(body) if body >= 0 else int(self.terms[0]["body"])
+        self.desc.attraction_weight = float(weight)
+        self.desc.attraction_radius = float(radius)
+        self.desc.attraction_tau = float(tau)
+
+    def set_attraction_prev(self, prev_losses) -> None:
+        """prev_losses_ as refresh_attraction leaves it: per-particle losses of the body's
+        members in particle-id order."""
+        self._prev = np.ascontiguousarray(prev_losses, dtype=np.float64).reshape(-1)
+        self.desc.n_prev = self._prev.size
+        self.desc.prev_losses = _dp(self._prev)
+
+    def per_particle(self, state: SimState, ws: "GpuWorkspace") -> np.ndarray:
+        """LossEvaluator::per_particle (losses.hpp:367-390) of `state`, computed on the device."""
+        ws._upload(state)
+        out = np.zeros(ws.scene.n_particles)
+        ws._check(ws.lib.flume_loss_per_particle(ws.ctx, C.byref(self.desc), _dp(out)))
+        return out
+
+    def refresh_attraction(self, state: SimState, ws: "GpuWorkspace") -> None:
+        """LossEvaluator::refresh_attraction (losses.hpp:357-363)."""
+        if not self.desc.attraction_weight > 0:
+            return
+        allp = self.per_particle(state, ws)
+        body = np.asarray(ws.scene.body_id)
+        self.set_attraction_prev(allp[body == self.desc.attraction_body])
 
     @staticmethod
     def _parse(spec: dict):
@@ -655,8 +687,10 @@ def p2g_grid(scene: Scene, state: SimState, ws: GpuWorkspace):
 
 
 def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss: LossEvaluator,
-                 window: int = 0, per_segment: Optional[list] = None, ws: Optional[GpuWorkspace] = None) -> float:
-    """grad.hpp:15-41."""
+                 window: int = 0, per_segment: Optional[list] = None, ws: Optional[GpuWorkspace] = None,
+                 final_state: Optional[SimState] = None) -> float:
+    """grad.hpp:15-41.  final_state (the reference's out-pointer) receives the state after
+    the whole horizon: the deterministic forward is re-run on the device from state0."""
     ws = _ws_for(scene, ws)
     ws._upload(state0)
     outs = [C.c_double() for _ in ws.ctxs]
@@ -667,6 +701,14 @@ def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss
     out, per = outs[0], pers[0]
     if per_segment is not None:
         per_segment[:] = per.tolist()
+    if final_state is not None:
+        st = state0.copy()
+        for s in range(actions.n_segments):
+            mpm_substep(scene, st, actions.values[s], ws, count=actions.segment_length)
+        st._pull()
+        for name in ("_x", "_v", "_F", "_C", "_eff", "_time", "_substep"):
+            setattr(final_state, name, getattr(st, name))
+        final_state._ws = None
     return out.value
 
 

@@ -462,6 +462,8 @@ struct Ctx {
     LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep);
     PointLossScratch pls;  // trajectory_chamfer / mixing_spread scratch (fl_loss.cu)
     void point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, double* out_dev, BarBuf* bars);
+    void make_attraction(const flume_loss_desc* loss, LossSet& ls, std::vector<std::shared_ptr<void>>& keep);
+    void per_particle(const flume_loss_desc* loss, double* out);
     // ls evaluated on a state at `substep` (activation semantics of parked particles)
     static LossSet at_substep(const LossSet& ls, long substep) {
         LossSet l = ls;
@@ -1290,6 +1292,8 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
                 d.gpts = arr->p;
                 d.goff_h = t.goal_step_offsets;
                 d.nsteps = t.n_goal_steps;
+                d.last_g0 = int(t.goal_step_offsets[t.n_goal_steps - 1]);
+                d.last_ng = int(np - t.goal_step_offsets[t.n_goal_steps - 1]);
                 keep.push_back(arr);
             }
             d.kind = t.kind == FLUME_LOSS_MIXING_SPREAD ? LK_SPREAD : LK_CHAMFER;
@@ -1298,7 +1302,74 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
             throw FlumeError(FLUME_E_SCENE, "loss kind not supported on device");
         }
     }
+    if (loss->attraction_weight > 0 && loss->n_prev > 0) make_attraction(loss, ls, keep);
     return ls;
+}
+
+// LossEvaluator::enable_attraction + the prev_losses_ refresh_attraction stored
+// (losses.hpp:350-363); tau as attraction_tau (losses.hpp:159-166)
+void Ctx::make_attraction(const flume_loss_desc* loss, LossSet& ls, std::vector<std::shared_ptr<void>>& keep) {
+    if (slab()) throw FlumeError(FLUME_E_ARG, "the attraction term runs on single-rank contexts only");
+    if (!loss->prev_losses) throw FlumeError(FLUME_E_ARG, "attraction: prev_losses is null");
+    if (!(loss->attraction_radius > 0)) throw FlumeError(FLUME_E_ARG, "attraction: radius must be positive");
+    AttractionDev& A = ls.attr;
+    const int body = loss->attraction_body < 0 ? loss->terms[0].body : loss->attraction_body;
+    auto mrank = std::make_shared<DevArr<int>>();
+    std::vector<int> hr(size_t(N), -1);
+    int nm = 0;
+    for (int i = 0; i < N; i++)
+        if (p_body[size_t(i)] == body) hr[size_t(i)] = nm++;
+    if (long(nm) != loss->n_prev) throw FlumeError(FLUME_E_ENGINE, "attraction_loss: loss list size mismatch");
+    if (nm >= (1 << 24)) throw FlumeError(FLUME_E_ARG, "attraction: more than 2^24 members");
+    std::vector<double> tmp(loss->prev_losses, loss->prev_losses + nm);
+    double tau = loss->attraction_tau;
+    if (!(tau > 0)) {
+        std::nth_element(tmp.begin(), tmp.begin() + tmp.size() / 2, tmp.end());
+        tau = std::max(0.1 * tmp[tmp.size() / 2], 1e-9);
+    }
+    unsigned long long ncell = 1;
+    for (int a = 0; a < 3; a++) {
+        // cells floor(x / radius) over the domain plus one pad cell on each side
+        const double span = std::floor(cfg.domain[a] / loss->attraction_radius) + 3.0;
+        if (span > double(1 << 20)) throw FlumeError(FLUME_E_ARG, "attraction: radius too small for the hash");
+        A.nc[a] = int(span);
+        ncell *= (unsigned long long)A.nc[a];
+    }
+    int bits = 1;
+    while ((1ull << bits) < ncell) bits++;
+    if (bits > 40) throw FlumeError(FLUME_E_ARG, "attraction: radius too small for the hash");
+    mrank->upload(hr, stream);
+    auto prev = std::make_shared<DevArr<double>>();
+    prev->alloc(size_t(nm));
+    CK(cudaMemcpyAsync(prev->p, loss->prev_losses, size_t(nm) * 8, cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));  // the host copies above are temporaries
+    keep.push_back(mrank);
+    keep.push_back(prev);
+    A.on = 1;
+    A.n_members = nm;
+    A.weight = loss->attraction_weight;
+    A.radius = loss->attraction_radius;
+    A.tau = tau;
+    A.prev = prev->p;
+    A.mrank = mrank->p;
+    A.key_bits = bits;
+    pls.reserve_attraction(std::max(nm, 1));
+}
+
+// LossEvaluator::per_particle (losses.hpp:367-390) of the current state, by particle id
+void Ctx::per_particle(const flume_loss_desc* loss, double* out) {
+    if (slab()) throw FlumeError(FLUME_E_ARG, "per_particle runs on single-rank contexts only");
+    std::vector<std::shared_ptr<void>> keep;
+    flume_loss_desc plain = *loss;
+    plain.attraction_weight = 0;  // the surrogate is not part of per_particle
+    const LossSet ls = at_substep(make_lossset(&plain, keep), substep_index);
+    d_up[0].alloc(size_t(N));
+    CK(cudaMemsetAsync(d_up[0].p, 0, size_t(N) * 8, stream));
+    launch_per_particle(cur->p, cur->n, d_cls.p, ls, geom.key_departed, d_up[0].p, stream);
+    launches += 1;
+    CK(cudaMemcpyAsync(out, d_up[0].p, size_t(N) * 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    check_error();
 }
 
 // trajectory_chamfer / mixing_spread terms of `mask` (losses.hpp:474-551): eval adds
@@ -1309,6 +1380,11 @@ void Ctx::point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, 
         launch_point_loss(pls, st.p, st.n, d_cls.p, ls, ls.t[k], seg, geom.key_inactive, out_dev, bars, d_err.p,
                           stream);
         launches += 5;
+    }
+    // attraction: every segment boundary, independent of the terms' eval mode (losses.hpp:332-345)
+    if (ls.attr.on) {
+        launch_attraction(pls, st.p, st.n, ls, geom.key_departed, out_dev, bars, stream);
+        launches += 4;
     }
 }
 
@@ -2037,6 +2113,11 @@ int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume
                        double* loss_out, double* per_segment) {
     if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
     return guard(ctx, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment); });
+}
+
+int flume_loss_per_particle(flume_ctx* ctx, const flume_loss_desc* loss, double* out) {
+    if (!ctx || !loss || !out) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.per_particle(loss, out); });
 }
 
 int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long stride,

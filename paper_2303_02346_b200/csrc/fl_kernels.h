@@ -74,10 +74,24 @@ struct LossTermDev {
     const double* gpts;   // trajectory_chamfer: all goal points (device)
     const long* goff_h;   // trajectory_chamfer: set offsets (HOST pointer, n_steps + 1)
     int nsteps;
+    int last_g0, last_ng; // trajectory_chamfer: the last goal set (per_particle uses it)
+};
+// attraction term (losses.hpp:104-218, 348-363, 553-564): the gradient-sharing
+// surrogate over every member of one body (active or parked), neighbours within
+// `radius` found through a hashed grid with cell = radius
+struct AttractionDev {
+    int on = 0;
+    int n_members = 0;
+    double weight = 0, radius = 0, tau = 1;
+    const double* prev = nullptr;  // previous iterate's per-particle losses, member (id) order
+    const int* mrank = nullptr;    // member rank by particle id (-1: not a member)
+    int nc[3] = {0, 0, 0};         // hash cells per axis (one pad cell on each side)
+    int key_bits = 0;              // cell-index bits of the sort key
 };
 struct LossSet {
     int n;
     LossTermDev t[kMaxLossTerms];
+    AttractionDev attr;
     // a parked (not yet emitted) particle counts as active once the state's substep
     // index reaches its activation substep (types.hpp:109), before its emission
     const int* act;   // activation substep by particle id
@@ -105,9 +119,23 @@ struct PointLossScratch {
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0, cap_g = 0;
     int cap_n = 0;
+    // attraction: member positions / exp(-prev / tau) / slots, hash keys, per-member sums
+    double *apx = nullptr, *ae = nullptr, *awsum = nullptr, *asi = nullptr, *apart = nullptr;
+    int* aslot = nullptr;
+    unsigned long long *akey = nullptr, *akey_sorted = nullptr;
+    void* asort_tmp = nullptr;
+    size_t asort_bytes = 0;
+    int cap_a = 0;
     void reserve(int n_particles, int max_goals);
+    void reserve_attraction(int n_members);
     ~PointLossScratch();
 };
+// attraction term of `ls` (ls.attr.on): eval adds weight * value into *out, grad adds into bars
+void launch_attraction(PointLossScratch& w, const PBuf& st, int n, const LossSet& ls, uint32_t key_departed,
+                       double* out, BarBuf* bars, cudaStream_t s);
+// LossEvaluator::per_particle (losses.hpp:367-390) of the stored state, by particle id
+void launch_per_particle(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t key_departed,
+                         double* out, cudaStream_t s);
 // eval (bars == nullptr): adds weight * value into *out; grad: adds d/dx into bars
 void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
                        const LossTermDev& t, int seg, uint32_t key_inactive, double* out, BarBuf* bars,

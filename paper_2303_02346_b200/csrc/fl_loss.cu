@@ -4,6 +4,8 @@
 //                        body's active particles A and the segment's goal set G,
 //                        O(|A| |G|) brute force in fp64 (no hashing: exact argmins)
 //   mixing_spread        -sum_ij |x_i - x_j| over the body, O(|A|^2) in fp64
+//   attraction           the optimizer's gradient-sharing surrogate (losses.hpp:104-218):
+//                        hashed-grid neighbour sums over every member of one body
 // Both first compact the body's active particles in store order (deterministic
 // prefix sum), so every sum below has a fixed order.  The evaluation adds
 // weight * value into the segment's loss slot; the gradient adds into x_bar
@@ -11,6 +13,7 @@
 // in goal order).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "fl_kernels.h"
@@ -278,6 +281,191 @@ __global__ void __launch_bounds__(kLT) k_spread_final(const int* __restrict__ co
 }
 
 // ---------------------------------------------------------------------------
+// attraction (losses.hpp:104-218, 553-564) and per_particle (losses.hpp:367-390)
+// ---------------------------------------------------------------------------
+// A particle's position in the reference's state at this boundary: parked particles
+// keep their parked position until the substep that emits them has run
+// (mpm.hpp:435-449), while the store already holds the emitted one at that substep.
+__device__ __forceinline__ double member_x(const LossSet& ls, const PBuf& st, int i, uint32_t id, int a) {
+    return double(ls.act[id] >= ls.substep ? ls.x0[size_t(a) * ls.n_all + id] : st.x(a)[i]);
+}
+
+// |a - b| with the reference's operation order (dot(), core.hpp:104-118; no contraction)
+__device__ __forceinline__ double dist3(double dx, double dy, double dz) {
+    return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+}
+
+constexpr int kMemberBits = 24;  // sort key = cell << 24 | member rank
+
+// members in member (= particle id) order: position, exp(-prev / tau), store slot and
+// hash key (SpatialHash::build, losses.hpp:118-126: cell = floor(x / radius))
+__global__ void k_attr_gather(PBuf st, int n, LossSet ls, uint32_t key_departed, double* px, double* e, int* slot,
+                              unsigned long long* key) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || st.key[i] >= key_departed) return;
+    const uint32_t id = st.id[i];
+    const AttractionDev& A = ls.attr;
+    const int r = A.mrank[id];
+    if (r < 0) return;
+    unsigned long long c = 0;
+    for (int a = 0; a < 3; a++) {
+        const double p = member_x(ls, st, i, id, a);
+        px[3 * size_t(r) + a] = p;
+        const int q = min(max(int(floor(p / A.radius)) + 1, 0), A.nc[a] - 1);
+        c = c * (unsigned long long)A.nc[a] + (unsigned long long)q;
+    }
+    e[r] = exp(-A.prev[r] / A.tau);
+    slot[r] = i;
+    key[r] = (c << kMemberBits) | (unsigned long long)r;
+}
+
+// Thread = one member in hash order.  Neighbours are visited like SpatialHash::neighbors
+// (losses.hpp:128-147): the 27 cells with axis 0 fastest, each cell in member order.
+//   GRAD = false: wsum_i = sum_j w_ij, si_i = sum_j w_ij r_ij, CTA partials of si / wsum
+//   GRAD = true:  x_bar_i += sum_j (g_ij + g_ji) (x_i - x_j) / r_ij, where g_ij is the
+//                 reference's weight * dloss_dr of pair (i, j) seen from centre i
+//                 (losses.hpp:203-215; its grad[j] -= dir * g is the g_ji term here)
+template <bool GRAD>
+__global__ void __launch_bounds__(kLT) k_attr_pass(const unsigned long long* __restrict__ keys, int na,
+                                                   const double* __restrict__ px, const double* __restrict__ e,
+                                                   AttractionDev A, double* wsum, double* si, double* partial,
+                                                   const int* __restrict__ slot, BarBuf bars) {
+    __shared__ double red[kLT];
+    const int t = blockIdx.x * kLT + threadIdx.x;
+    double contrib = 0.0;
+    if (t < na) {
+        const unsigned long long kk = keys[t];
+        const int r = int(kk & ((1ull << kMemberBits) - 1));
+        unsigned long long c = kk >> kMemberBits;
+        const int qz = int(c % (unsigned long long)A.nc[2]);
+        c /= (unsigned long long)A.nc[2];
+        const int qy = int(c % (unsigned long long)A.nc[1]);
+        const int qx = int(c / (unsigned long long)A.nc[1]);
+        const double p0 = px[3 * size_t(r)], p1 = px[3 * size_t(r) + 1], p2 = px[3 * size_t(r) + 2];
+        const double R = A.radius;
+        double ws = 0.0, s = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+        double wr = 0.0, sr = 0.0, er = 0.0;
+        if (GRAD) {
+            wr = wsum[r];
+            sr = si[r];
+            er = e[r];
+        }
+        for (int q = 0; q < 27; q++) {
+            const int cx = qx + q % 3 - 1, cy = qy + (q / 3) % 3 - 1, cz = qz + q / 9 - 1;
+            if (cx < 0 || cy < 0 || cz < 0 || cx >= A.nc[0] || cy >= A.nc[1] || cz >= A.nc[2]) continue;
+            const unsigned long long cell =
+                ((unsigned long long)cx * A.nc[1] + (unsigned long long)cy) * A.nc[2] + (unsigned long long)cz;
+            const unsigned long long want = cell << kMemberBits;
+            int lo = 0, hi = na;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (keys[mid] < want)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            for (int u = lo; u < na; u++) {
+                const unsigned long long kj = keys[u];
+                if ((kj >> kMemberBits) != cell) break;
+                const int j = int(kj & ((1ull << kMemberBits) - 1));
+                if (j == r) continue;
+                const double dx = p0 - px[3 * size_t(j)], dy = p1 - px[3 * size_t(j) + 1],
+                             dz = p2 - px[3 * size_t(j) + 2];
+                const double d = dist3(dx, dy, dz);
+                if (d >= R) continue;
+                const double tent = 1.0 - d / R;
+                if (!GRAD) {
+                    const double w = e[j] * tent;
+                    ws += w;
+                    s = __dadd_rn(s, __dmul_rn(w, d));
+                } else {
+                    double g = 0.0;
+                    if (wr > 0.0) {  // pair (r, j) from centre r
+                        const double dwdr = -e[j] / R;
+                        const double dnum = __dadd_rn(__dmul_rn(dwdr, d), e[j] * tent);
+                        g += A.weight * (dnum / wr - sr * dwdr / (wr * wr));
+                    }
+                    const double wj = wsum[j];
+                    if (wj > 0.0) {  // pair (j, r) from centre j
+                        const double dwdr = -er / R;
+                        const double dnum = __dadd_rn(__dmul_rn(dwdr, d), er * tent);
+                        g += A.weight * (dnum / wj - si[j] * dwdr / (wj * wj));
+                    }
+                    if (d > 1e-300) {
+                        g0 += dx / d * g;
+                        g1 += dy / d * g;
+                        g2 += dz / d * g;
+                    }
+                }
+            }
+        }
+        if (!GRAD) {
+            wsum[r] = ws;  // ws == 0 also covers "no neighbours"
+            si[r] = s;
+            if (ws > 0.0) contrib = s / ws;
+        } else {
+            const int i = slot[r];
+            bars.x(0)[i] += float(g0);
+            bars.x(1)[i] += float(g1);
+            bars.x(2)[i] += float(g2);
+        }
+    }
+    if (GRAD) return;
+    red[threadIdx.x] = contrib;
+    __syncthreads();
+    for (int w = kLT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(kLT) k_attr_final(const double* __restrict__ partial, int npartial, double weight,
+                                                    double* out) {
+    __shared__ double red[kLT];
+    double s = 0.0;
+    for (int b = threadIdx.x; b < npartial; b += kLT) s += partial[b];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kLT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out += weight * red[0];
+}
+
+// per_particle: sum over the terms on the particle's body of its unweighted distance
+// (target_point, hold_initial, nearest point of the last chamfer goal set), every member
+// active or not; mixing_spread contributes nothing
+__global__ void k_per_particle(PBuf st, int n, const ClassInfo* __restrict__ cls, LossSet ls,
+                               uint32_t key_departed, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || st.key[i] >= key_departed) return;
+    const uint32_t id = st.id[i];
+    const int body = cls[meta_cls(st.meta[i])].body;
+    double p[3];
+    for (int a = 0; a < 3; a++) p[a] = member_x(ls, st, i, id, a);
+    double v = 0.0;
+    for (int k = 0; k < ls.n; k++) {
+        const LossTermDev& t = ls.t[k];
+        if (t.body != body) continue;
+        if (t.kind == LK_TARGET) {
+            v += dist3(p[0] - t.goal[0], p[1] - t.goal[1], p[2] - t.goal[2]);
+        } else if (t.kind == LK_HOLD) {
+            const float* q = t.init + 3 * size_t(id);
+            v += dist3(p[0] - double(q[0]), p[1] - double(q[1]), p[2] - double(q[2]));
+        } else if (t.kind == LK_CHAMFER) {
+            const double* g = t.gpts + 3 * size_t(t.last_g0);
+            double best = 1e300;
+            for (int q = 0; q < t.last_ng; q++)
+                best = fmin(best, dist3(p[0] - g[3 * q], p[1] - g[3 * q + 1], p[2] - g[3 * q + 2]));
+            v += best;
+        }
+    }
+    out[id] = v;
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 void PointLossScratch::reserve(int n_particles, int max_goals) {
@@ -313,10 +501,58 @@ void PointLossScratch::reserve(int n_particles, int max_goals) {
     }
 }
 
+void PointLossScratch::reserve_attraction(int n_members) {
+    if (n_members <= cap_a) return;
+    for (auto p : {(void*)apx, (void*)ae, (void*)awsum, (void*)asi, (void*)aslot, (void*)akey, (void*)akey_sorted,
+                   (void*)apart, asort_tmp})
+        cudaFree(p);
+    cudaMalloc(&apx, sizeof(double) * 3 * size_t(n_members));
+    cudaMalloc(&ae, sizeof(double) * size_t(n_members));
+    cudaMalloc(&awsum, sizeof(double) * size_t(n_members));
+    cudaMalloc(&asi, sizeof(double) * size_t(n_members));
+    cudaMalloc(&aslot, sizeof(int) * size_t(n_members));
+    cudaMalloc(&akey, sizeof(unsigned long long) * size_t(n_members));
+    cudaMalloc(&akey_sorted, sizeof(unsigned long long) * size_t(n_members));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, akey, akey_sorted, n_members, 0, 64);
+    cudaMalloc(&asort_tmp, tb);
+    asort_bytes = tb;
+    cudaMalloc(&apart, sizeof(double) * (size_t(n_members) / kLT + 2));
+    cap_a = n_members;
+}
+
 PointLossScratch::~PointLossScratch() {
     for (auto p : {(void*)flags, (void*)pos, (void*)idx, (void*)px, (void*)best, (void*)arg, (void*)partial,
-                   (void*)cbest, (void*)carg, (void*)gbest, (void*)garg, (void*)count, (void*)scal, cub_tmp})
+                   (void*)cbest, (void*)carg, (void*)gbest, (void*)garg, (void*)count, (void*)scal, cub_tmp,
+                   (void*)apx, (void*)ae, (void*)awsum, (void*)asi, (void*)aslot, (void*)akey, (void*)akey_sorted,
+                   (void*)apart, asort_tmp})
         cudaFree(p);
+}
+
+void launch_attraction(PointLossScratch& w, const PBuf& st, int n, const LossSet& ls, uint32_t key_departed,
+                       double* out, BarBuf* bars, cudaStream_t s) {
+    const AttractionDev& A = ls.attr;
+    const int na = A.n_members;
+    if (!A.on || na < 2 || n <= 0) return;  // attraction_loss: fewer than 2 points -> 0
+    k_attr_gather<<<(n + 255) / 256, 256, 0, s>>>(st, n, ls, key_departed, w.apx, w.ae, w.aslot, w.akey);
+    cub::DeviceRadixSort::SortKeys(w.asort_tmp, w.asort_bytes, w.akey, w.akey_sorted, na, 0,
+                                   kMemberBits + A.key_bits, s);
+    const int grid = (na + kLT - 1) / kLT;
+    // the gradient needs every member's sums first: pass 1 runs for eval and grad alike
+    k_attr_pass<false><<<grid, kLT, 0, s>>>(w.akey_sorted, na, w.apx, w.ae, A, w.awsum, w.asi, w.apart, w.aslot,
+                                           BarBuf{});
+    if (!bars) {
+        k_attr_final<<<1, kLT, 0, s>>>(w.apart, grid, A.weight, out);
+    } else {
+        k_attr_pass<true><<<grid, kLT, 0, s>>>(w.akey_sorted, na, w.apx, w.ae, A, w.awsum, w.asi, nullptr, w.aslot,
+                                              *bars);
+    }
+}
+
+void launch_per_particle(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t key_departed,
+                         double* out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_per_particle<<<(n + 255) / 256, 256, 0, s>>>(st, n, cls, ls, key_departed, out);
 }
 
 static void compact_body(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, int body,

@@ -609,8 +609,10 @@ int flume_scene_loss_get(const flume_scene* s, flume_loss_desc* l) {
         t.goal_step_offsets = ms->loss_goal_off[k].data();
         t.goal_points = ms->loss_goal_pts[k].data();
     }
+    *l = flume_loss_desc{};
     l->n_terms = int(s->loss_terms.size());
     l->terms = s->loss_terms.data();
+    l->attraction_body = -1;  // off until the optimizer enables it
     return FLUME_OK;
 }
 

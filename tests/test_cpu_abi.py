@@ -27,7 +27,7 @@ def header_functions():
 
 def test_library_loads_and_abi_version():
     lib = _abi.load()
-    assert lib.flume_abi_version() == 2
+    assert lib.flume_abi_version() == 3
 
 
 def test_every_declared_symbol_is_exported():

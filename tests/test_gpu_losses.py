@@ -95,3 +95,57 @@ def test_loss_on_emitter_body_at_activation_boundaries(ref_available, kind):
     l, per, rl, rper, tg, rg = _run(spec, 3, 5)
     np.testing.assert_allclose(per, rper, rtol=1e-6)
     assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
+
+
+@pytest.mark.parametrize("name,res,body,tau", [("c1", 16, "column", 0.0), ("c1", 16, "column", 0.05),
+                                               ("c2", 64, "stream", 0.0)])
+def test_attraction_parity(ref_available, name, res, body, tau):
+    """The optimizer's gradient-sharing surrogate (losses.hpp:104-218): enable_attraction,
+    refresh_attraction from a rollout's final state (optimize.hpp:157-190), then loss and
+    action gradient with the term active at every segment boundary.  c2's stream body has
+    parked emitter particles, which the term includes at their parked positions."""
+    spec = spec_for(name, res)
+    spec["loss"] = {"kind": "target_point", "body": body, "goal": [0.5, 0.3, 0.5]}
+    w, r = pair(spec)
+    ws = fl.GpuWorkspace(w.scene)
+    nseg, seglen = 3, 4
+    vals = np.tile(w.init_action, (nseg, 1))
+    acts = fl.ActionTrajectory(nseg, seglen, vals)
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    radius = 3 * w.scene.dx
+    loss.enable_attraction(-1, 1e-3, radius, tau)
+    fs = w.state.copy()
+    fl.rollout_loss(w.scene, w.state, acts, loss, final_state=fs, ws=ws)
+    assert fs.substep_index == nseg * seglen
+    # per_particle on the device == the reference's on the same positions
+    pp = loss.per_particle(fs, ws)
+    rpp = r.per_particle(fs.x)
+    np.testing.assert_allclose(pp, rpp, rtol=1e-12, atol=1e-12)
+    loss.refresh_attraction(fs, ws)
+    r.set_attraction(-1, 1e-3, radius, tau, refresh_x=fs.x)
+    body_id = int(w.loss_spec[0]["body"])
+    assert loss.desc.n_prev == int(np.sum(w.scene.body_id == body_id)) >= 2
+    per = []
+    l = fl.rollout_loss(w.scene, w.state, acts, loss, per_segment=per, ws=ws)
+    rl, rper = r.rollout_loss(vals, seglen)
+    np.testing.assert_allclose(per, rper, rtol=1e-6)
+    tg = fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
+    rg = r.grad_trajectory(vals, seglen)
+    assert abs(tg.loss - rg["loss"]) <= 1e-6 * abs(rg["loss"])
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3, (tg.action_grad, rg["grad"])
+    # the term is not negligible: switching it off changes the loss
+    r.set_attraction(-1, 0.0, radius, tau)
+    r0, _ = r.rollout_loss(vals, seglen)
+    assert abs(rl - r0) > 1e-4 * abs(rl)
+
+
+def test_attraction_size_mismatch_raises():
+    spec = spec_for("c1", 16)
+    w = fl.build_scene(spec)
+    ws = fl.GpuWorkspace(w.scene)
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    loss.enable_attraction(-1, 1.0, 3 * w.scene.dx, 0.0)
+    loss.set_attraction_prev(np.ones(5))
+    acts = fl.ActionTrajectory(1, 2, w.init_action.reshape(1, 6))
+    with pytest.raises(fl.EngineError, match="loss list size mismatch"):
+        fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws)
