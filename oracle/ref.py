@@ -64,6 +64,9 @@ def lib():
             "ref_adjoint_substep": (C.c_int, [C.c_void_p, D, D, D, D, D, D, D]),
             "ref_set_attraction": (None, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double, D]),
             "ref_per_particle": (C.c_int, [C.c_void_p, D, D]),
+            "ref_write_frame_csv": (C.c_int, [C.c_void_p, C.c_char_p, C.c_ulonglong]),
+            "ref_write_metrics": (C.c_int, [C.c_void_p, C.c_char_p, C.c_ulonglong]),
+            "ref_actions_json": (C.c_char_p, [C.c_int, C.c_int, D]),
         }
         for k, (r, a) in sig.items():
             f = getattr(l, k)
@@ -211,6 +214,17 @@ class RefWorld:
         out = np.zeros(self.n)
         self._check(self.l.ref_per_particle(self.h, _p(xs), _p(out)))
         return out
+
+    def write_frame_csv(self, path, manifest_hash):
+        self._check(self.l.ref_write_frame_csv(self.h, str(path).encode(), int(manifest_hash)))
+
+    def write_metrics(self, path, manifest_hash):
+        """MetricsWriter<3> with one row for the live state."""
+        self._check(self.l.ref_write_metrics(self.h, str(path).encode(), int(manifest_hash)))
+
+    def actions_json(self, values, seglen):
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1, 6)
+        return json.loads(self.l.ref_actions_json(v.shape[0], int(seglen), _p(v)).decode())
 
     def loss_spec(self):
         return json.loads(self.l.ref_loss_spec(self.h).decode())

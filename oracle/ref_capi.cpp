@@ -20,6 +20,7 @@
 #include <string>
 
 #include "flume/flume.hpp"
+#include "flume/io.hpp"
 
 using namespace flume;
 
@@ -386,6 +387,25 @@ int ref_grad_trajectory(void* h, int nseg, int seglen, const double* actions, lo
             for (int s = 0; s < nseg; s++) per_segment[s] = tg.per_segment[size_t(s)];
         if (snapshots) *snapshots = long(tg.snapshots);
     });
+}
+
+// run outputs (io.hpp:53-114) of the live state
+int ref_write_frame_csv(void* h, const char* path, unsigned long long hash) {
+    RefWorld* rw = static_cast<RefWorld*>(h);
+    return guarded([&] { write_frame_csv<3>(path, rw->state, hash); });
+}
+int ref_write_metrics(void* h, const char* path, unsigned long long hash) {
+    RefWorld* rw = static_cast<RefWorld*>(h);
+    return guarded([&] {
+        MetricsWriter<3> m(path, hash);
+        m.append(rw->state);
+        m.flush();
+    });
+}
+const char* ref_actions_json(int nseg, int seglen, const double* values) {
+    static thread_local std::string s;
+    s = actions_to_json(make_actions(nseg, seglen, values)).dump();
+    return s.c_str();
 }
 
 // Attraction for the following rollout_loss / grad_trajectory calls: weight <= 0 turns it

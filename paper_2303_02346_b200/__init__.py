@@ -10,10 +10,10 @@ from .api import (ActionTrajectory, AdjointError, AdjointState, DegenerateDeform
                   TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, mpm_substep,
                   p2g_grid, rollout_loss, slab_split, WorkspacePool, rollout_loss_batch,
                   grad_trajectory_batch, state_to_json, state_from_json)
-from . import scenes
+from . import frames, scenes
 
 __all__ = ["ActionTrajectory", "AdjointError", "AdjointState", "DegenerateDeformation", "DeviceError", "EngineError",
            "GpuWorkspace", "LossEvaluator", "RigidityError", "Scene", "SceneError", "SimState", "SubstepRecord",
            "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "mpm_substep", "p2g_grid",
            "rollout_loss", "scenes", "slab_split", "WorkspacePool", "rollout_loss_batch", "grad_trajectory_batch",
-           "state_to_json", "state_from_json"]
+           "state_to_json", "state_from_json", "frames"]
