@@ -13,6 +13,8 @@
 //     grad.hpp:61-134
 //   adjoint_substep(scene, rec, adj, action_bar, ws)    gpu::adjoint_substep(scene, rec, adj, action_bar, ws)
 //     adjoint.hpp:476-548
+//   grad_check(scene, state0, actions, loss, stride, eps) gpu::grad_check(scene, state0, actions, loss_spec, ws, ...)
+//     grad.hpp:190-225
 //
 // The loss is passed as the scene's loss JSON (World::loss_spec, the input of
 // LossEvaluator, losses.hpp:311) because LossEvaluator keeps its terms private;
@@ -21,6 +23,7 @@
 #pragma once
 
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -366,6 +369,35 @@ inline TrajectoryGrad<3> grad_trajectory(const Scene<3>& scene, const SimState<3
     for (int s = 0; s < actions.n_segments; s++)
         for (int k = 0; k < 6; k++) out.action_grad[size_t(s)][size_t(k)] = grad[size_t(6 * s + k)];
     return out;
+}
+
+// grad.hpp:190-225: the device adjoint gradient over the optimizable components, audited
+// by central differences of device rollouts (fp32 state: pick eps ~1e-3 for O(1) actions)
+inline GradReport grad_check(const Scene<3>& scene, const SimState<3>& state0, const ActionTrajectory& actions,
+                             const Loss& loss, Workspace& ws, long stride, Real eps, bool with_fd = true) {
+    auto start = std::chrono::steady_clock::now();
+    std::vector<int> comps = optimizable_components(state0);
+    GradReport rep;
+    TrajectoryGrad<3> tg = grad_trajectory(scene, state0, actions, loss, ws, stride);
+    rep.loss = tg.loss;
+    for (int s = 0; s < actions.n_segments; s++)
+        for (int k : comps) rep.gradient.push_back(tg.action_grad[size_t(s)][size_t(k)]);
+    if (with_fd) {
+        std::vector<Real> params;
+        for (int s = 0; s < actions.n_segments; s++)
+            for (int k : comps) params.push_back(actions.values[size_t(s)][size_t(k)]);
+        auto objective = [&](const std::vector<Real>& p) {
+            ActionTrajectory a = actions;
+            size_t idx = 0;
+            for (int s = 0; s < a.n_segments; s++)
+                for (int k : comps) a.values[size_t(s)][size_t(k)] = p[idx++];
+            return rollout_loss(scene, state0, a, loss, ws);
+        };
+        rep.fd_gradient = finite_difference_gradient(objective, params, eps);
+        rep.max_rel_error = GradReport::rel_error(rep.gradient, rep.fd_gradient);
+    }
+    rep.wall_time = std::chrono::duration<Real>(std::chrono::steady_clock::now() - start).count();
+    return rep;
 }
 
 // adjoint.hpp:476-548 (bars of the post-state in, bars of rec.pre_state out)

@@ -64,6 +64,8 @@ def lib():
             "ref_adjoint_substep": (C.c_int, [C.c_void_p, D, D, D, D, D, D, D]),
             "ref_set_attraction": (None, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double, D]),
             "ref_per_particle": (C.c_int, [C.c_void_p, D, D]),
+            "ref_grad_check": (C.c_int, [C.c_void_p, C.c_int, C.c_int, D, C.c_long, C.c_double, C.c_int, D, D, L,
+                                         D, D]),
             "ref_write_frame_csv": (C.c_int, [C.c_void_p, C.c_char_p, C.c_ulonglong]),
             "ref_write_metrics": (C.c_int, [C.c_void_p, C.c_char_p, C.c_ulonglong]),
             "ref_actions_json": (C.c_char_p, [C.c_int, C.c_int, D]),
@@ -214,6 +216,18 @@ class RefWorld:
         out = np.zeros(self.n)
         self._check(self.l.ref_per_particle(self.h, _p(xs), _p(out)))
         return out
+
+    def grad_check(self, values, seglen, stride, eps, with_fd=True):
+        """grad_check<3> (grad.hpp:190-225)."""
+        values = np.ascontiguousarray(values, dtype=np.float64).reshape(-1, 6)
+        ns = values.shape[0]
+        g, fd = np.zeros(ns * 6), np.zeros(ns * 6)
+        n, mr, lo = C.c_long(), C.c_double(), C.c_double()
+        self._check(self.l.ref_grad_check(self.h, ns, int(seglen), _p(values), int(stride), float(eps), int(with_fd),
+                                          _p(g), _p(fd), C.byref(n), C.byref(mr), C.byref(lo)))
+        k = n.value
+        return {"gradient": g[:k], "fd_gradient": fd[:k] if with_fd else np.zeros(0), "max_rel_error": mr.value,
+                "loss": lo.value}
 
     def write_frame_csv(self, path, manifest_hash):
         self._check(self.l.ref_write_frame_csv(self.h, str(path).encode(), int(manifest_hash)))

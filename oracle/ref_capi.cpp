@@ -389,6 +389,23 @@ int ref_grad_trajectory(void* h, int nseg, int seglen, const double* actions, lo
     });
 }
 
+// grad_check (grad.hpp:190-225): adjoint gradient over the optimizable components and,
+// with_fd, its central-difference audit; arrays hold up to nseg * 6 entries
+int ref_grad_check(void* h, int nseg, int seglen, const double* actions, long stride, double eps, int with_fd,
+                   double* grad, double* fd, long* n, double* max_rel, double* loss) {
+    RefWorld* rw = static_cast<RefWorld*>(h);
+    return guarded([&] {
+        ActionTrajectory a = make_actions(nseg, seglen, actions);
+        auto le = make_le(rw);
+        GradReport rep = grad_check(rw->w.scene, rw->state, a, *le, stride, eps, with_fd != 0);
+        *n = long(rep.gradient.size());
+        for (size_t i = 0; i < rep.gradient.size(); i++) grad[i] = rep.gradient[i];
+        for (size_t i = 0; i < rep.fd_gradient.size(); i++) fd[i] = rep.fd_gradient[i];
+        *max_rel = rep.max_rel_error;
+        *loss = rep.loss;
+    });
+}
+
 // run outputs (io.hpp:53-114) of the live state
 int ref_write_frame_csv(void* h, const char* path, unsigned long long hash) {
     RefWorld* rw = static_cast<RefWorld*>(h);

@@ -9,11 +9,13 @@ from .api import (ActionTrajectory, AdjointError, AdjointState, DegenerateDeform
                   GpuWorkspace, LossEvaluator, RigidityError, Scene, SceneError, SimState, SubstepRecord,
                   TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, mpm_substep,
                   p2g_grid, rollout_loss, slab_split, WorkspacePool, rollout_loss_batch,
-                  grad_trajectory_batch, state_to_json, state_from_json)
+                  grad_trajectory_batch, state_to_json, state_from_json, GradReport, grad_check,
+                  finite_difference_gradient, optimizable_components)
 from . import frames, scenes
 
 __all__ = ["ActionTrajectory", "AdjointError", "AdjointState", "DegenerateDeformation", "DeviceError", "EngineError",
            "GpuWorkspace", "LossEvaluator", "RigidityError", "Scene", "SceneError", "SimState", "SubstepRecord",
            "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "mpm_substep", "p2g_grid",
            "rollout_loss", "scenes", "slab_split", "WorkspacePool", "rollout_loss_batch", "grad_trajectory_batch",
-           "state_to_json", "state_from_json", "frames"]
+           "state_to_json", "state_from_json", "frames", "GradReport", "grad_check",
+           "finite_difference_gradient", "optimizable_components"]

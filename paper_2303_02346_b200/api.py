@@ -125,6 +125,8 @@ class Scene:
         self.activation_substep = np.ctypeslib.as_array(desc.activation_substep, (n,)).copy()
         self.materials = [desc.materials[i] for i in range(desc.n_materials)]
         self.n_effectors = desc.n_effectors
+        self.action_masks = [[bool(desc.effectors[e].action_mask[k]) for k in range(6)]
+                             for e in range(desc.n_effectors)]
 
     @property
     def node_dims(self):
@@ -688,9 +690,11 @@ def p2g_grid(scene: Scene, state: SimState, ws: GpuWorkspace):
 
 def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss: LossEvaluator,
                  window: int = 0, per_segment: Optional[list] = None, ws: Optional[GpuWorkspace] = None,
-                 final_state: Optional[SimState] = None) -> float:
+                 final_state: Optional[SimState] = None, on_substep=None) -> float:
     """grad.hpp:15-41.  final_state (the reference's out-pointer) receives the state after
-    the whole horizon: the deterministic forward is re-run on the device from state0."""
+    the whole horizon and on_substep(state) runs after every substep (metrics exports): for
+    either, the deterministic forward is re-run on the device from state0 (host copies of
+    the state happen only if the callback reads host fields)."""
     ws = _ws_for(scene, ws)
     ws._upload(state0)
     outs = [C.c_double() for _ in ws.ctxs]
@@ -701,10 +705,16 @@ def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss
     out, per = outs[0], pers[0]
     if per_segment is not None:
         per_segment[:] = per.tolist()
-    if final_state is not None:
+    if final_state is not None or on_substep is not None:
         st = state0.copy()
         for s in range(actions.n_segments):
-            mpm_substep(scene, st, actions.values[s], ws, count=actions.segment_length)
+            if on_substep is None:
+                mpm_substep(scene, st, actions.values[s], ws, count=actions.segment_length)
+                continue
+            for _ in range(actions.segment_length):  # the callback sees every substep's state
+                mpm_substep(scene, st, actions.values[s], ws)
+                on_substep(st)
+    if final_state is not None:
         st._pull()
         for name in ("_x", "_v", "_F", "_C", "_eff", "_time", "_substep"):
             setattr(final_state, name, getattr(st, name))
@@ -729,6 +739,75 @@ def grad_trajectory(scene: Scene, state0: SimState, actions: ActionTrajectory, l
     lo, fl, snaps = res[0]
     t = ws.last_timing()
     return TrajectoryGrad(lo.value, fl.value, per.tolist(), g, snaps.value, t.forward_ms, t.backward_ms)
+
+
+@dataclass
+class GradReport:
+    """grad.hpp:160-175."""
+    gradient: List[float] = field(default_factory=list)
+    fd_gradient: List[float] = field(default_factory=list)
+    max_rel_error: float = 0.0
+    wall_time: float = 0.0
+    loss: float = 0.0
+
+    @staticmethod
+    def rel_error(g, fd) -> float:
+        num = max((abs(a - b) for a, b in zip(g, fd)), default=0.0)
+        den = max((abs(b) for b in fd), default=0.0)
+        return num / (den + 1e-12)
+
+
+def finite_difference_gradient(objective, params, eps: float) -> List[float]:
+    """Central differences, two evaluations per parameter (grad.hpp:140-158)."""
+    if eps <= 0:
+        raise EngineError("finite_difference_gradient: eps must be positive")
+    grad = []
+    for i in range(len(params)):
+        p, m = list(params), list(params)
+        p[i] += eps
+        m[i] -= eps
+        fp, fm = objective(p), objective(m)
+        if not (np.isfinite(fp) and np.isfinite(fm)):
+            raise EngineError(f"finite_difference_gradient: non-finite objective at parameter {i}")
+        grad.append((fp - fm) / (2 * eps))
+    return grad
+
+
+def optimizable_components(scene: Scene) -> List[int]:
+    """Action components any effector accepts (grad.hpp:177-188)."""
+    return [k for k in range(6) if any(m[k] for m in scene.action_masks)]
+
+
+def grad_check(scene: Scene, state0: SimState, actions: ActionTrajectory, loss: LossEvaluator, stride: int,
+               eps: float, with_fd: bool = True, ws: Optional[GpuWorkspace] = None) -> GradReport:
+    """grad.hpp:190-225: the adjoint gradient over the optimizable components, audited by
+    central differences of device rollouts.  The device computes in fp32, so eps must be
+    large enough for the loss differences to clear fp32 rounding (about 1e-3 for O(1) actions)."""
+    import time as _time
+    t0 = _time.perf_counter()
+    comps = optimizable_components(scene)
+    rep = GradReport()
+    tg = grad_trajectory(scene, state0, actions, loss, stride=stride, ws=ws)
+    rep.loss = tg.loss
+    rep.gradient = [float(tg.action_grad[s][k]) for s in range(actions.n_segments) for k in comps]
+    if with_fd:
+        base = np.asarray(actions.values, dtype=np.float64).reshape(actions.n_segments, 6)
+        params = [float(base[s][k]) for s in range(actions.n_segments) for k in comps]
+
+        def objective(p):
+            v = base.copy()
+            idx = 0
+            for s in range(actions.n_segments):
+                for k in comps:
+                    v[s][k] = p[idx]
+                    idx += 1
+            return rollout_loss(scene, state0, ActionTrajectory(actions.n_segments, actions.segment_length, v), loss,
+                                ws=ws)
+
+        rep.fd_gradient = finite_difference_gradient(objective, params, eps)
+        rep.max_rel_error = GradReport.rel_error(rep.gradient, rep.fd_gradient)
+    rep.wall_time = _time.perf_counter() - t0
+    return rep
 
 
 def adjoint_substep(scene: Scene, rec: SubstepRecord, adj: AdjointState, action_bar: np.ndarray,

@@ -138,3 +138,21 @@ def test_continue_from_reference_snapshot(ref_available):
     e = state_errors(w.state, rs, w.scene.dx)
     assert w.state.substep_index == rs["substep"] == 11
     assert e["x"] <= 1e-4 and e["v"] <= 5e-4 and e["F"] <= 1e-4 and e["C"] <= 1e-3, e
+
+
+def test_rollout_loss_final_state_and_on_substep():
+    """rollout_loss's final_state / on_substep (grad.hpp:15-41): the callback sees every
+    substep's state and the final state is the one the loss was evaluated on."""
+    w = fl.build_scene(spec_for("c1", 16))
+    ws = fl.GpuWorkspace(w.scene)
+    acts = fl.ActionTrajectory(2, 3, np.tile(w.init_action, (2, 1)))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    seen = []
+    fs = w.state.copy()
+    l1 = fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws, final_state=fs,
+                         on_substep=lambda st: seen.append((st.substep_index, st.x[0].copy())))
+    assert [s for s, _ in seen] == list(range(1, 7)) and fs.substep_index == 6
+    chain = w.state.copy()
+    fl.mpm_substep(w.scene, chain, w.init_action, ws, count=6)
+    assert np.array_equal(chain.x, fs.x) and np.array_equal(seen[-1][1], fs.x[0])
+    assert fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws) == l1
