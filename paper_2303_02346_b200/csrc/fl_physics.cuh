@@ -77,10 +77,14 @@ template <class T> FL_HD T contact_alpha_deriv(T d, bool hard) {
 template <class T>
 FL_HD V3<T> effector_contact(const EffK<T>& e, T inv_dx, T eps_cells, bool hard, V3<T> p, V3<T> v_in,
                              bool* hit = nullptr) {
-    SdfSample<T> s = sdf_eval(e.shape, e.wt, e.wR, p);
-    T d = s.distance * inv_dx;
+    // sdf_eval split: the normal is only needed inside the contact band, and most
+    // nodes are far from every effector (same values as sdf_eval where it is used)
+    const V3<T> q = tmul(e.wR, p - e.wt);
+    T d = sdf_local_distance(e.shape, q) * inv_dx;
     if (hit) *hit = d < eps_cells;
     if (d >= eps_cells) return v_in;
+    SdfSample<T> s;
+    s.normal = normalized_or_x(e.wR * sdf_local_grad(e.shape, q), T(1e-30));
     V3<T> r = p - e.pt;
     V3<T> ve = e.vlin + cross(e.wang, r);
     V3<T> vrel = v_in - ve;
