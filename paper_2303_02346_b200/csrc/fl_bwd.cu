@@ -346,15 +346,18 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
 #pragma unroll
                         for (int oy = 0; oy < 3; oy++) {
                             const V3<float> axy = ax + ay[oy];
+                            float sa = 0.f, sb = 0.f;  // z-weighted and z-gradient-weighted sums
 #pragma unroll
                             for (int oz = 0; oz < 3; oz++) {
                                 const float4 gv4 = row[oy * 6 + oz];
                                 const V3<float> u = axy + az[oz];
                                 const float sv = gv4.x * u.x + gv4.y * u.y + gv4.z * u.z;
-                                px += (sw.w[1][oy] * sw.w[2][oz]) * sv;
-                                py += (sw.dw[1][oy] * sw.w[2][oz]) * sv;
-                                pz += (sw.w[1][oy] * sw.dw[2][oz]) * sv;
+                                sa += sw.w[2][oz] * sv;
+                                sb += sw.dw[2][oz] * sv;
                             }
+                            px += sw.w[1][oy] * sa;
+                            py += sw.dw[1][oy] * sa;
+                            pz += sw.w[1][oy] * sb;
                         }
                         sxx += dox * px;
                         syy += wox * py;
@@ -680,6 +683,7 @@ __global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const u
                     az[o] = V3<float>{affine.m[2] * rz[o], affine.m[5] * rz[o], affine.m[8] * rz[o]};
                 }
                 const float mm = ci.mass;
+                const float wrz[3] = {sw.w[2][0] * rz[0], sw.w[2][1] * rz[1], sw.w[2][2] * rz[2]};
                 float sxx = 0.f, syy = 0.f, szz = 0.f;
 #pragma unroll 1
                 for (int ox = 0; ox < 3; ox++) {
@@ -693,21 +697,27 @@ __global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const u
 #pragma unroll
                     for (int oy = 0; oy < 3; oy++) {
                         const V3<float> axy = ax + ay[oy];
+                        // per (x, y) column: z-weighted sums, then one scaling by the x/y weights
+                        float sa = 0.f, sb = 0.f;
+                        V3<float> tz = {0.f, 0.f, 0.f}, tzr = {0.f, 0.f, 0.f};
 #pragma unroll
                         for (int oz = 0; oz < 3; oz++) {
                             const float4 b4 = row[oy * 6 + oz];
                             const V3<float> u = axy + az[oz];
                             const float sv = b4.w * mm + b4.x * u.x + b4.y * u.y + b4.z * u.z;
-                            const float wyz = sw.w[1][oy] * sw.w[2][oz];
-                            px += wyz * sv;
-                            py += (sw.dw[1][oy] * sw.w[2][oz]) * sv;
-                            pz += (sw.w[1][oy] * sw.dw[2][oz]) * sv;
-                            const float w = wox * wyz;
-                            const V3<float> wob = {b4.x * w, b4.y * w, b4.z * w};
-                            tx += wob;
-                            ab.m[1] += wob.x * ry[oy]; ab.m[4] += wob.y * ry[oy]; ab.m[7] += wob.z * ry[oy];
-                            ab.m[2] += wob.x * rz[oz]; ab.m[5] += wob.y * rz[oz]; ab.m[8] += wob.z * rz[oz];
+                            sa += sw.w[2][oz] * sv;
+                            sb += sw.dw[2][oz] * sv;
+                            tz += V3<float>{b4.x, b4.y, b4.z} * sw.w[2][oz];
+                            tzr += V3<float>{b4.x, b4.y, b4.z} * wrz[oz];
                         }
+                        px += sw.w[1][oy] * sa;
+                        py += sw.dw[1][oy] * sa;
+                        pz += sw.w[1][oy] * sb;
+                        const float wxy = wox * sw.w[1][oy];
+                        const V3<float> wob = tz * wxy;
+                        tx += wob;
+                        ab.m[1] += wob.x * ry[oy]; ab.m[4] += wob.y * ry[oy]; ab.m[7] += wob.z * ry[oy];
+                        ab.m[2] += tzr.x * wxy; ab.m[5] += tzr.y * wxy; ab.m[8] += tzr.z * wxy;
                     }
                     sxx += dox * px;
                     syy += wox * py;
