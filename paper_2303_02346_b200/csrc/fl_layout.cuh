@@ -137,9 +137,20 @@ __host__ __device__ inline void block_unlin(const Geom& g, int b, int& bx, int& 
 #ifndef FL_PDL
 #define FL_PDL 1
 #endif
+#ifndef FL_PDL_TRIGGER
+#define FL_PDL_TRIGGER 1
+#endif
+// Every kernel starts with this: wait for the previous grid on the stream (its writes
+// are visible afterwards), then allow the next one to be scheduled.  The next grid is
+// released once all CTAs of this one have started (or exited), so its CTAs only take
+// resources this grid no longer needs, and they block in their own wait until this grid
+// has completed: launch latency and CTA rasterisation overlap the tail of this grid.
 __device__ __forceinline__ void pdl_wait() {
 #if defined(__CUDA_ARCH__) && FL_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#if FL_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
 #endif
 }
 
