@@ -31,7 +31,8 @@ def main(path, out_json):
     for (_, name), m in recs.items():
         base = re.search(r"(k_\w+|DeviceScan\w*)", name)
         base = base.group(1) if base else name[:30]
-        var = "<H>" if ("<1>" in name or "(bool)1" in name) else ("<L>" if ("<0>" in name or "(bool)0" in name) else "")
+        tm = re.search(r"k_\w+<(\(bool\))?([01])[,>]", name)  # k_x<HEAVY> / k_x<HEAVY, MINB> / k_x<(bool)H, ...>
+        var = ("<H>" if tm.group(2) == "1" else "<L>") if tm else ""
         t = m.get("gpu__time_duration.sum", 0.0)
         b = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
         k = kern[base + var]
