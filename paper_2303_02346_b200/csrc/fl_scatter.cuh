@@ -24,7 +24,7 @@ constexpr int kScThreads = 192;  // 64 cells x 3 planes
 #define FL_LB_G2P 8
 #endif
 #ifndef FL_LB_ADJG2P
-#define FL_LB_ADJG2P 4
+#define FL_LB_ADJG2P 5
 #endif
 #ifndef FL_LB_ADJP2G
 #define FL_LB_ADJP2G 5
