@@ -429,7 +429,10 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 // reduction of the per-effector bars (18 scalars each)
 // ---------------------------------------------------------------------------
 constexpr int kEffQ = 18;  // t[3] R[9] vlin[3] w[3]
-constexpr int kAdjGridThreads = 128;
+#ifndef FL_ADJGRID_THREADS
+#define FL_ADJGRID_THREADS 64
+#endif
+constexpr int kAdjGridThreads = FL_ADJGRID_THREADS;
 
 __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __restrict__ blockmap,
                                                   const float4* __restrict__ staging, int bx, int by, int bz, int lx,
@@ -459,7 +462,7 @@ __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __re
 // one fixed-order CTA reduction per launch.  Nothing effector-sized lives in
 // registers across nodes, which keeps the kernel at ~64 registers.
 template <int NE>
-__global__ void __launch_bounds__(kAdjGridThreads, 8) k_adj_grid(Geom g, const int* __restrict__ nb_list,
+__global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj_grid(Geom g, const int* __restrict__ nb_list,
                                                                  const int* __restrict__ n_nb,
                                                                  const int* __restrict__ blockmap,
                                                                  const float4* __restrict__ staging_bar,

@@ -140,7 +140,10 @@ void launch_per_particle(const PBuf& st, int n, const ClassInfo* cls, const Loss
 void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
                        const LossTermDev& t, int seg, uint32_t key_inactive, double* out, BarBuf* bars,
                        unsigned long long* err, cudaStream_t s);
-constexpr int kEffBlocks = 1184;
+#ifndef FL_EFF_BLOCKS
+#define FL_EFF_BLOCKS 3552
+#endif
+constexpr int kEffBlocks = FL_EFF_BLOCKS;  // grid of the grid adjoint = its effector-bar partials
 constexpr int kRigidChunk = 2048;
 
 // ---- forward ----
