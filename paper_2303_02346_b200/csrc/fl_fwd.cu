@@ -301,7 +301,12 @@ __device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __res
     return acc;
 }
 
-__global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restrict__ nb_list,
+#ifndef FL_GRIDUPD_THREADS
+#define FL_GRIDUPD_THREADS 256
+#endif
+constexpr int kGridUpdThreads = FL_GRIDUPD_THREADS;  // 64 nodes (one node block) per 64 threads
+
+__global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const int* __restrict__ nb_list,
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
                                                      EffSet eff, uint8_t* cmask, int* clear, int n_clear) {
@@ -311,7 +316,8 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
     const int n = *n_nb;
     const int sub = threadIdx.x >> 6, l = threadIdx.x & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    for (int k = blockIdx.x * 4 + sub; k < n; k += gridDim.x * 4) {
+    constexpr int kPer = kGridUpdThreads / 64;
+    for (int k = blockIdx.x * kPer + sub; k < n; k += gridDim.x * kPer) {
         const int nbid = nb_list[k];
         int bx, by, bz;
         block_unlin(g, nbid, bx, by, bz);
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(256) k_grid_update(Geom g, const int* __restri
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
                         int* clear, int n_clear, cudaStream_t s) {
-    launch_k(k_grid_update, dim3(grid), dim3(256), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
+    launch_k(k_grid_update, dim3(grid * (256 / kGridUpdThreads)), dim3(kGridUpdThreads), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
                                        n_clear);
 }
 
