@@ -224,10 +224,9 @@ def build_scene(spec) -> World:
         view = _abi.StateView()
         lib.flume_scene_state_get(h, C.byref(view))
         n = desc.n_particles
-        x = np.ctypeslib.as_array(view.x, (n, 3)).copy()
-        v = np.ctypeslib.as_array(view.v, (n, 3)).copy()
-        F = np.ctypeslib.as_array(view.F, (n, 9)).copy()
-        Cm = np.ctypeslib.as_array(view.C, (n, 9)).copy()
+        # (an empty scene hands out null arrays)
+        grab = lambda p, k: np.ctypeslib.as_array(p, (n, k)).copy() if n else np.zeros((0, k))  # noqa: E731
+        x, v, F, Cm = grab(view.x, 3), grab(view.v, 3), grab(view.F, 9), grab(view.C, 9)
         eff = np.zeros((desc.n_effectors, 18))
         for i in range(desc.n_effectors):
             e = view.effectors[i]
@@ -670,7 +669,10 @@ def mpm_substep(scene: Scene, state: SimState, action, ws: GpuWorkspace, count: 
     ws._upload(state)
     a = np.ascontiguousarray(action, dtype=np.float64)
     ws._collective(lambda r, c: ws.lib.flume_substep(c, _dp(a), int(count)))
-    ws._ctx_time = state._time + count * scene.dt_substep
+    t = state._time
+    for _ in range(int(count)):  # the reference accumulates time += dt per substep (mpm.hpp:471)
+        t += scene.dt_substep
+    ws._ctx_time = t
     ws._ctx_substep = state._substep + count
     state._time, state._substep = ws._ctx_time, ws._ctx_substep
     ws._mark_device_newer(state)

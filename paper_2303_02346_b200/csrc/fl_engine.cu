@@ -453,8 +453,14 @@ struct Ctx {
     void check_error(long substep_base = 0);
     EffSet make_effset(const std::vector<EffState>& es) const;
     void advance_effectors(const double* action);
+    bool empty = false;  // no particles at all (N == 0)
     void upload(const flume_state_view* view);
     void download(flume_state_view* view);
+    void set_effectors(const flume_state_view* view);
+    void download_meta(flume_state_view* view);
+    void require_particles() const {
+        if (empty) throw FlumeError(FLUME_E_SCENE, "scene has no particles");
+    }
     void sort_and_lists(StateBuf& st, Record& r);
     void forward_substep(const double* action, StatePtr in, StatePtr out, Record& r);
     void substep(const double* action, int count);
@@ -497,7 +503,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     CK(cudaMemsetAsync(wq.p, 0, kWq * sizeof(int), stream));
     cfg = desc->config;
     N = int(desc->n_particles);
-    if (N <= 0) throw FlumeError(FLUME_E_SCENE, "scene has no particles");
+    if (N < 0) throw FlumeError(FLUME_E_ARG, "negative particle count");
     mats.assign(desc->materials, desc->materials + desc->n_materials);
     eff_shapes.assign(desc->effectors, desc->effectors + desc->n_effectors);
     if (desc->n_effectors > kMaxEff) throw FlumeError(FLUME_E_ARG, "at most 8 effectors are supported");
@@ -519,6 +525,13 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     g.colblocks = g.NB[1] * g.NB[2];
     g.sx0 = 0;
     g.sx1 = g.NB[0];
+    if (N == 0) {
+        // an empty scene (no bodies): substeps only move the effectors and the clock,
+        // like the reference's particle loops over nothing (test_cli.cpp:75-84)
+        empty = true;
+        eff.resize(eff_shapes.size());
+        return;
+    }
     g.idbits = bits_for(uint64_t(N - 1));
     if (g.keybits + g.idbits > 64) throw FlumeError(FLUME_E_ARG, "grid too large for 64-bit sort keys");
     g.dx = float(dx);
@@ -794,6 +807,12 @@ void Ctx::check_error(long /*substep_base*/) {
 
 // upload a SimState<3> view; canonical store order is established here
 void Ctx::upload(const flume_state_view* view) {
+    if (empty) {
+        substep_index = view->substep_index;
+        time = view->time;
+        set_effectors(view);
+        return;
+    }
     for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
     CK(cudaMemcpyAsync(d_up[0].p, view->x, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_up[1].p, view->v, size_t(N) * 3 * 8, cudaMemcpyHostToDevice, stream));
@@ -860,6 +879,14 @@ void Ctx::upload(const flume_state_view* view) {
     launch_upload_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
     launches += 3;
     put_state(raw);
+    set_effectors(view);
+    unsigned long long reset = ~0ull;
+    CK(cudaMemcpyAsync(d_err.p, &reset, sizeof(reset), cudaMemcpyHostToDevice, stream));
+    // escape check of the uploaded positions happens in the first P2G
+    CK(cudaStreamSynchronize(stream));
+}
+
+void Ctx::set_effectors(const flume_state_view* view) {
     for (size_t i = 0; i < eff.size(); i++) {
         const flume_effector_state& es = view->effectors[i];
         eff[i].t = V3<double>{es.pose_t[0], es.pose_t[1], es.pose_t[2]};
@@ -867,13 +894,13 @@ void Ctx::upload(const flume_state_view* view) {
         eff[i].vlin = V3<double>{es.linear_velocity[0], es.linear_velocity[1], es.linear_velocity[2]};
         eff[i].w = V3<double>{es.angular_velocity[0], es.angular_velocity[1], es.angular_velocity[2]};
     }
-    unsigned long long reset = ~0ull;
-    CK(cudaMemcpyAsync(d_err.p, &reset, sizeof(reset), cudaMemcpyHostToDevice, stream));
-    // escape check of the uploaded positions happens in the first P2G
-    CK(cudaStreamSynchronize(stream));
 }
 
 void Ctx::download(flume_state_view* view) {
+    if (empty) {
+        download_meta(view);
+        return;
+    }
     for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
     if (slab()) {
         // every rank fills its own particles (rank 0 also the parked ones) into
@@ -893,6 +920,10 @@ void Ctx::download(flume_state_view* view) {
     if (view->F) CK(cudaMemcpyAsync(view->F, d_up[2].p, size_t(N) * 9 * 8, cudaMemcpyDeviceToHost, stream));
     if (view->C) CK(cudaMemcpyAsync(view->C, d_up[3].p, size_t(N) * 9 * 8, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    download_meta(view);
+}
+
+void Ctx::download_meta(flume_state_view* view) {
     view->time = time;
     view->substep_index = substep_index;
     if (view->effectors)
@@ -1175,6 +1206,14 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
 }
 
 void Ctx::substep(const double* action, int count) {
+    if (empty) {  // mpm_substep over no particles: effectors and clock only (mpm.hpp:455-473)
+        for (int i = 0; i < count; i++) {
+            advance_effectors(action);
+            time += cfg.dt_substep;
+            substep_index++;
+        }
+        return;
+    }
     for (int i = 0; i < count; i++) {
         StatePtr nxt = get_state();
         forward_substep(action, cur, nxt, *scratch_rec);
@@ -1186,6 +1225,12 @@ void Ctx::substep(const double* action, int count) {
 
 // p2g + grid_update on the live state without advancing (KAT harness)
 void Ctx::stage_grid(double* mass, double* vel) {
+    if (empty) {
+        const size_t nn = size_t(geom.nd[0]) * geom.nd[1] * geom.nd[2];
+        if (mass) std::fill(mass, mass + nn, 0.0);
+        if (vel) std::fill(vel, vel + 3 * nn, 0.0);
+        return;
+    }
     Record& r = *scratch_rec;
     r.n_active = n_active;
     r.n_keep = n_active + n_parked();
@@ -2045,6 +2090,10 @@ int flume_store_order(flume_ctx* ctx, unsigned* keys, unsigned* ids, long* n_act
     if (!ctx) return FLUME_E_ARG;
     return guard(ctx, [&] {
         Ctx& c = ctx->c;
+        if (c.empty) {
+            if (n_active) *n_active = 0;
+            return;
+        }
         if (keys) CK(cudaMemcpyAsync(keys, c.cur->p.key, size_t(c.N) * 4, cudaMemcpyDeviceToHost, c.stream));
         if (ids) CK(cudaMemcpyAsync(ids, c.cur->p.id, size_t(c.N) * 4, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
@@ -2056,6 +2105,7 @@ int flume_store_positions(flume_ctx* ctx, float* x) {
     if (!ctx || !x) return FLUME_E_ARG;
     return guard(ctx, [&] {
         Ctx& c = ctx->c;
+        if (c.empty) return;
         CK(cudaMemcpyAsync(x, c.cur->p.f, size_t(c.N) * 3 * 4, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
     });
@@ -2112,12 +2162,18 @@ int flume_stage_grid(flume_ctx* ctx, double* mass, double* vel) {
 int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long window,
                        double* loss_out, double* per_segment) {
     if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
-    return guard(ctx, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment); });
+    return guard(ctx, [&] {
+        ctx->c.require_particles();
+        *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment);
+    });
 }
 
 int flume_loss_per_particle(flume_ctx* ctx, const flume_loss_desc* loss, double* out) {
     if (!ctx || !loss || !out) return FLUME_E_ARG;
-    return guard(ctx, [&] { ctx->c.per_particle(loss, out); });
+    return guard(ctx, [&] {
+        ctx->c.require_particles();
+        ctx->c.per_particle(loss, out);
+    });
 }
 
 int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long stride,
@@ -2125,6 +2181,7 @@ int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const fl
                           double* per_segment, long* snapshots) {
     if (!ctx || !actions || !action_grad) return FLUME_E_ARG;
     return guard(ctx, [&] {
+        ctx->c.require_particles();
         ctx->c.grad_trajectory(actions, loss, stride, window, action_grad, loss_out, full_loss, per_segment,
                                snapshots);
     });
@@ -2134,6 +2191,7 @@ int flume_adjoint_substep(flume_ctx* ctx, const double action[6], double* x_bar,
                           double* C_bar, double* eff_bars, double* action_bar) {
     if (!ctx || !action || !x_bar || !v_bar || !F_bar || !C_bar || !action_bar) return FLUME_E_ARG;
     return guard(ctx, [&] {
+        ctx->c.require_particles();
         std::vector<double> dummy(size_t(fl::kMaxEff) * 12, 0.0);
         ctx->c.adjoint_substep_api(action, x_bar, v_bar, F_bar, C_bar, eff_bars ? eff_bars : dummy.data(),
                                    action_bar);

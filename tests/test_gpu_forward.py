@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import paper_2303_02346_b200 as fl
-from tests._util import canonical_keys_cpu, pair, spec_for, state_errors
+from tests._util import canonical_keys_cpu, grad_rel_error, pair, spec_for, state_errors
 
 pytestmark = pytest.mark.gpu
 
@@ -156,3 +156,61 @@ def test_rollout_loss_final_state_and_on_substep():
     fl.mpm_substep(w.scene, chain, w.init_action, ws, count=6)
     assert np.array_equal(chain.x, fs.x) and np.array_equal(seen[-1][1], fs.x[0])
     assert fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws) == l1
+
+
+def test_empty_scene_advances_effectors_and_clock(ref_available, tmp_path):
+    """A scene without bodies (test_cli.cpp:75-84): substeps move only the effectors and
+    the clock, frames have no rows, the staged grid is empty."""
+    from oracle.ref import RefWorld
+    from paper_2303_02346_b200 import frames
+    spec = {"dim": 3, "grid_resolution": 16, "domain": [1.0, 1.0, 1.0],
+            "effectors": [{"shape": {"type": "sphere", "radius": 0.1, "center": [0.0, 0.0, 0.0]},
+                           "position": [0.5, 0.5, 0.5], "action_mask": [True, True, True, False, False, True]}]}
+    w = fl.build_scene(spec)
+    assert w.scene.n_particles == 0
+    ws = fl.GpuWorkspace(w.scene)
+    act = np.array([0.2, -0.1, 0.05, 0.0, 0.0, 0.7])
+    fl.mpm_substep(w.scene, w.state, act, ws, count=7)
+    r = RefWorld(spec)
+    r.substep(act, 7)
+    rs = r.state()
+    assert w.state.substep_index == rs["substep"] == 7 and w.state.time == rs["time"]
+    np.testing.assert_array_equal(w.state.effectors, r.effector_state())
+    m, v = fl.p2g_grid(w.scene, w.state, ws)
+    assert not m.any() and not v.any()
+    frames.write_frame_csv(tmp_path / "f.csv", w.scene, w.state, 1)
+    assert (tmp_path / "f.csv").read_text().count("\n") == 2
+
+
+def test_single_particle_carried_by_sticky_effector(ref_available):
+    """test_autodiff.cpp:47-75 in 3D: one particle inside a sticky box effector moves with
+    the commanded velocity, and d|x_T - goal|^2 / da = 2 (x_T - goal) T dt."""
+    spec = {"dim": 3, "grid_resolution": 32, "domain": [1.0, 1.0, 1.0], "dt_substep": 1e-4,
+            "substeps_per_step": 10, "gravity": [0.0, 0.0, 0.0],
+            "materials": [{"name": "chip", "kind": "elastic", "mu": 10.0, "lambda": 10.0, "rho": 1.0}],
+            "bodies": [{"name": "tracer", "material": "chip",
+                        "shape": {"type": "box", "half_extents": [0.012, 0.012, 0.012], "center": [0.3, 0.4, 0.5]},
+                        "particles_per_cell_axis": 1}],
+            "effectors": [{"shape": {"type": "box", "half_extents": [0.08, 0.08, 0.08], "center": [0.0, 0.0, 0.0]},
+                           "position": [0.3, 0.4, 0.5], "friction": "sticky",
+                           "action_mask": [True, True, False, False, False, False]}],
+            "loss": {"kind": "target_point", "body": "tracer", "goal": [0.5, 0.6, 0.5], "squared": True,
+                     "eval": "final"},
+            "optimizer": {"n_segments": 1, "segment_length": 100}}
+    w, r = pair(spec)
+    assert w.scene.n_particles == 1
+    ws = fl.GpuWorkspace(w.scene)
+    T, dt = 100, 1e-4
+    a = np.array([[0.6, 0.4, 0.0, 0.0, 0.0, 0.0]])
+    acts = fl.ActionTrajectory(1, T, a)
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    fs = w.state.copy()
+    l = fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws, final_state=fs)
+    x0, xT = w.state.x[0], fs.x[0]
+    np.testing.assert_allclose(xT[:2], x0[:2] + a[0, :2] * T * dt, rtol=0, atol=2e-6)
+    tg = fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
+    expect = (xT - np.array([0.5, 0.6, 0.5])) * (2.0 * T * dt)
+    np.testing.assert_allclose(tg.action_grad[0, :2], expect[:2], rtol=2e-4)
+    rg = r.grad_trajectory(a, T)
+    assert abs(l - rg["loss"]) <= 1e-5 * abs(rg["loss"])
+    assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-4
