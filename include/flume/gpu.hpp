@@ -340,13 +340,19 @@ inline void mpm_substep(const Scene<3>& scene, SimState<3>& state, const std::ar
 // grad.hpp:15-41
 inline Real rollout_loss(const Scene<3>& scene, const SimState<3>& state0, const ActionTrajectory& actions,
                          const Loss& loss, Workspace& ws, long window_substeps = 0,
-                         std::vector<Real>* per_segment = nullptr) {
+                         std::vector<Real>* per_segment = nullptr, SimState<3>* final_state = nullptr) {
     (void)scene;
     ws.upload(state0);
     std::vector<double> buf, per(size_t(actions.n_segments));
     flume_actions av = actions_view(actions, buf);
     double out = 0;
-    check(ws.ctx(), flume_rollout_loss(ws.ctx(), &av, loss.desc(), window_substeps, &out, per.data()));
+    if (final_state) {  // the context ends on the state after the horizon
+        check(ws.ctx(), flume_rollout_loss_final(ws.ctx(), &av, loss.desc(), window_substeps, &out, per.data()));
+        *final_state = state0;
+        ws.download(*final_state);
+    } else {
+        check(ws.ctx(), flume_rollout_loss(ws.ctx(), &av, loss.desc(), window_substeps, &out, per.data()));
+    }
     if (per_segment) *per_segment = per;
     return out;
 }

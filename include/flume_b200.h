@@ -268,6 +268,11 @@ int flume_substep(flume_ctx* ctx, const double action[6], int count);
 int flume_stage_grid(flume_ctx* ctx, double* mass, double* vel); /* dense (i*ny+j)*nz+k order */
 int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long window,
                        double* loss_out, double* per_segment);
+/* rollout_loss with its final_state out-parameter (grad.hpp:15-41): the same loss, and the
+   context's state becomes the state after the whole horizon (read it with
+   flume_state_download) instead of staying at state0 */
+int flume_rollout_loss_final(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long window,
+                             double* loss_out, double* per_segment);
 int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long stride,
                           long window, double* action_grad, double* loss_out, double* full_loss,
                           double* per_segment, long* snapshots);

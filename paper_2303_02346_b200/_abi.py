@@ -138,6 +138,8 @@ EXPORTS = {
     "flume_timer_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "flume_substep": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     "flume_stage_grid": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "flume_rollout_loss_final": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "flume_loss_per_particle": (C.c_int, [C.c_void_p, C.POINTER(LossDesc), C.POINTER(C.c_double)]),
     "flume_rollout_loss": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long,
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -145,6 +145,7 @@ class SimState:
         self._time = float(time)
         self._substep = int(substep_index)
         self._ws: Optional["GpuWorkspace"] = None  # workspace holding the newer copy
+        self._ver = 0  # bumped by every host access: a workspace re-uploads a state whose version moved
 
     # host views pull the device copy first and make the host authoritative
     def _pull(self):
@@ -158,17 +159,23 @@ class SimState:
         return SimState(self._x.copy(), self._v.copy(), self._F.copy(), self._C.copy(), self._eff.copy(),
                         self._time, self._substep)
 
+    # host access hands out the arrays themselves (callers may modify them in place), so
+    # any access makes the host copy authoritative for the next upload
+    def _touch(self):
+        self._pull()
+        self._ver += 1
+
     @property
     def n_particles(self):
         return self._x.shape[0]
 
     def _prop(name):  # noqa: N805
         def get(self):
-            self._pull()
+            self._touch()
             return getattr(self, name)
 
         def set_(self, val):
-            self._pull()
+            self._touch()
             getattr(self, name)[...] = val
 
         return property(get, set_)
@@ -189,7 +196,7 @@ class SimState:
 
     @substep_index.setter
     def substep_index(self, v):
-        self._pull()
+        self._touch()
         self._substep = int(v)
 
     def active_particle_count(self, scene: Scene) -> int:
@@ -473,6 +480,7 @@ class GpuWorkspace:
             self.ctxs = [C.c_void_p(arr[i]) for i in range(len(devs))]
             self.ctx = self.ctxs[0]
         self._resident: Optional[SimState] = None
+        self._resident_ver = -1
         self._ctx_time = 0.0
         self._ctx_substep = 0
 
@@ -491,6 +499,7 @@ class GpuWorkspace:
             _raise(self.lib, None, rc)
         self.ctxs = [self.ctx]
         self._resident = None
+        self._resident_ver = -1
         self._ctx_time = 0.0
         self._ctx_substep = 0
         return self
@@ -575,7 +584,7 @@ class GpuWorkspace:
         return arr
 
     def _upload(self, st: SimState):
-        if self._resident is st:
+        if self._resident is st and self._resident_ver == st._ver:
             return
         if self._resident is not None:
             self._resident._pull()
@@ -584,6 +593,7 @@ class GpuWorkspace:
         view = self._view(st, effs)
         self._collective(lambda r, c: self.lib.flume_state_upload(c, C.byref(view)))
         self._resident = st
+        self._resident_ver = st._ver
         self._ctx_time = st._time
         self._ctx_substep = st._substep
 
@@ -608,6 +618,7 @@ class GpuWorkspace:
     def _mark_device_newer(self, st: SimState):
         st._ws = self
         self._resident = st
+        self._resident_ver = st._ver
 
     def store_order(self, st: SimState):
         """Canonical store order (cell keys, particle ids, active count) + fp32 positions."""
@@ -694,19 +705,34 @@ def rollout_loss(scene: Scene, state0: SimState, actions: ActionTrajectory, loss
                  window: int = 0, per_segment: Optional[list] = None, ws: Optional[GpuWorkspace] = None,
                  final_state: Optional[SimState] = None, on_substep=None) -> float:
     """grad.hpp:15-41.  final_state (the reference's out-pointer) receives the state after
-    the whole horizon and on_substep(state) runs after every substep (metrics exports): for
-    either, the deterministic forward is re-run on the device from state0 (host copies of
-    the state happen only if the callback reads host fields)."""
+    the whole horizon (the context continues from it: flume_rollout_loss_final), and
+    on_substep(state) runs after every substep (metrics exports; the deterministic forward is
+    re-run on the device from state0, host copies happen only if the callback reads host
+    fields)."""
     ws = _ws_for(scene, ws)
+    keep = final_state is not None and on_substep is None  # the context ends on the final state
+    if keep:
+        state0._pull()  # state0's host copy must survive the context moving on
     ws._upload(state0)
     outs = [C.c_double() for _ in ws.ctxs]
     pers = [np.zeros(actions.n_segments) for _ in ws.ctxs]
     a = actions._c()
-    ws._collective(lambda r, c: ws.lib.flume_rollout_loss(c, C.byref(a), C.byref(loss.desc), int(window),
-                                                          C.byref(outs[r]), _dp(pers[r])))
+    fn = ws.lib.flume_rollout_loss_final if keep else ws.lib.flume_rollout_loss
+    ws._collective(lambda r, c: fn(c, C.byref(a), C.byref(loss.desc), int(window), C.byref(outs[r]),
+                                   _dp(pers[r])))
     out, per = outs[0], pers[0]
     if per_segment is not None:
         per_segment[:] = per.tolist()
+    if keep:
+        ws._resident = None  # the context left state0
+        final_state._pull()
+        for name in ("_x", "_v", "_F", "_C", "_eff"):
+            setattr(final_state, name, np.empty_like(getattr(state0, name)))
+        ws._download(final_state)
+        final_state._ver += 1
+        ws._resident, ws._resident_ver = final_state, final_state._ver
+        ws._ctx_time, ws._ctx_substep = final_state._time, final_state._substep
+        return out.value
     if final_state is not None or on_substep is not None:
         st = state0.copy()
         for s in range(actions.n_segments):

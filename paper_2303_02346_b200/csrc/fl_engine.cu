@@ -478,7 +478,8 @@ struct Ctx {
     }
     uint32_t loss_mask(const flume_loss_desc* loss, int seg, int nseg) const;
     void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg, long substep);
-    double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg);
+    double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg,
+                        bool keep_final = false);
     void adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre,
                       int t_slot);
     void grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
@@ -1448,7 +1449,8 @@ void Ctx::eval_loss(StateBuf& st, const LossSet& ls0, uint32_t mask, double* out
     point_losses(st, ls, mask, seg, out_dev, nullptr);
 }
 
-double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg) {
+double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg,
+                         bool keep_final) {
     const long T = long(a->n_segments) * a->segment_length;
     if (window <= 0) window = T;
     std::vector<std::shared_ptr<void>> keep;
@@ -1477,15 +1479,20 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     std::vector<double> per(a->n_segments);
     CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    put_state(st);
-    substep_index = s0;
-    time = time0;
-    n_active = na0;
-    n_stored = ns0;
-    park_base = pb0;
-    eff = eff0;
-    inactive_ids = inact0;
-    pending = pend0;
+    if (keep_final) {  // the context continues from the final state (rollout_loss's final_state)
+        put_state(cur);
+        cur = st;
+    } else {
+        put_state(st);
+        substep_index = s0;
+        time = time0;
+        n_active = na0;
+        n_stored = ns0;
+        park_base = pb0;
+        eff = eff0;
+        inactive_ids = inact0;
+        pending = pend0;
+    }
     check_error();
     double total = 0;
     for (int s = 0; s < a->n_segments; s++) {
@@ -2165,6 +2172,15 @@ int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume
     return guard(ctx, [&] {
         ctx->c.require_particles();
         *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment);
+    });
+}
+
+int flume_rollout_loss_final(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss, long window,
+                             double* loss_out, double* per_segment) {
+    if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.require_particles();
+        *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment, true);
     });
 }
 

@@ -55,13 +55,23 @@ int main(int argc, char** argv) {
             gden = std::max(gden, std::abs(gc.action_grad[size_t(s)][size_t(k)]));
         }
     const double grel = gnum / (gden + 1e-12);
+    // rollout_loss's final_state: the state after the horizon equals the substep chain
+    SimState<3> fin_c, fin_g;
+    rollout_loss(w.scene, w.state, traj, le, 0, nullptr, &fin_c);
+    gpu::Loss fl_loss(w.loss_spec);
+    gpu::rollout_loss(w.scene, w.state, traj, fl_loss, gws, 0, nullptr, &fin_g);
+    double fdx = 0;
+    for (size_t i = 0; i < fin_c.particles.size(); i++)
+        for (int a = 0; a < 3; a++) fdx = std::max(fdx, std::abs(fin_c.particles[i].x[a] - fin_g.particles[i].x[a]));
+    fdx /= w.scene.config.dx();
+    const bool fin_ok = fin_g.substep_index == fin_c.substep_index && fdx <= 1e-4;
     // grad_check without the FD audit: the gradient over the optimizable components
     gpu::Loss gl(w.loss_spec);
     GradReport rc = grad_check(w.scene, w.state, traj, le, 2, 1e-5, false);
     GradReport rg = gpu::grad_check(w.scene, w.state, traj, gl, gws, 2, 1e-3, false);
     const double crel = rc.gradient.size() == rg.gradient.size() ? GradReport::rel_error(rg.gradient, rc.gradient) : 1.0;
     const double lrel = std::abs(gc.loss - gg.loss) / std::abs(gc.loss);
-    const bool ok = dx <= 1e-4 && dv <= 5e-4 * vmax && grel <= 1e-3 && crel <= 1e-3 && lrel <= 1e-5 && gc.snapshots == gg.snapshots;
+    const bool ok = dx <= 1e-4 && dv <= 5e-4 * vmax && grel <= 1e-3 && crel <= 1e-3 && fin_ok && lrel <= 1e-5 && gc.snapshots == gg.snapshots;
     std::printf("{\"particles\": %zu, \"substeps\": %d, \"x_err_dx\": %.3e, \"v_err_rel\": %.3e, "
                 "\"loss_rel\": %.3e, \"grad_rel\": %.3e, \"grad_check_rel\": %.3e, \"snapshots\": [%zu, %zu], "
                 "\"ok\": %s}\n",

@@ -214,3 +214,39 @@ def test_single_particle_carried_by_sticky_effector(ref_available):
     rg = r.grad_trajectory(a, T)
     assert abs(l - rg["loss"]) <= 1e-5 * abs(rg["loss"])
     assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-4
+
+
+def test_host_edits_of_a_resident_state_are_uploaded():
+    """A state the workspace already holds is re-uploaded after any host access (the
+    arrays may have been edited in place)."""
+    w = fl.build_scene(spec_for("c1", 16))
+    ws = fl.GpuWorkspace(w.scene)
+    acts = fl.ActionTrajectory(1, 3, w.init_action.reshape(1, 6))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    l0 = fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws)
+    w.state.v[:] += 0.5  # in place, through the getter
+    l1 = fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws)
+    w2 = fl.build_scene(spec_for("c1", 16))
+    v = w2.state.v
+    v += 0.5
+    w2.state.v = v
+    l2 = fl.rollout_loss(w2.scene, w2.state, acts, fl.LossEvaluator(w2.scene, w2.loss_spec, w2.state),
+                         ws=fl.GpuWorkspace(w2.scene))
+    assert l1 != l0 and l1 == l2
+
+
+def test_final_state_keeps_state0_intact():
+    w = fl.build_scene(spec_for("c1", 16))
+    ws = fl.GpuWorkspace(w.scene)
+    acts = fl.ActionTrajectory(2, 3, np.tile(w.init_action, (2, 1)))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    fl.mpm_substep(w.scene, w.state, w.init_action, ws, count=2)  # state0 now device-resident
+    s0 = w.state.copy()
+    fs = w.state.copy()
+    l = fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws, final_state=fs)
+    assert np.array_equal(w.state.x, s0.x) and w.state.substep_index == s0.substep_index
+    assert fs.substep_index == s0.substep_index + 6
+    chain = s0.copy()
+    fl.mpm_substep(w.scene, chain, w.init_action, ws, count=6)
+    assert np.array_equal(chain.x, fs.x) and np.array_equal(chain.F, fs.F)
+    assert fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws) == l
