@@ -412,6 +412,23 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # the same figures for every kernel class with algorithmic bytes (P2G / G2P are the
+    # north star's ">= 50% of HBM roofline" kernels); traffic = ncu DRAM bytes per launch
+    per_kernel = {}
+    try:
+        tr_all = json.loads(prof.read_text()) if prof.exists() else {}
+    except Exception:
+        tr_all = {}
+    for k, (pbk, nbk) in ALG_BYTES.items():
+        if k not in kern:
+            continue
+        t_s = kern[k]["ms_total"] / kern[k]["launches"] / 1e3
+        a_k = (pbk * n_local + nbk * A) / t_s / 1e9
+        tk = tr_all.get(k)
+        per_kernel[k] = {"achieved": a_k, "frac": a_k / peak, "us_per_launch": 1e6 * t_s,
+                         "alg_bytes_per_launch": pbk * n_local + nbk * A, "traffic": tk,
+                         "traffic_frac": (tk / t_s / 1e9 / peak) if tk else None}
+
     cpu = None
     if not args.no_cpu and world_size == 1:
         try:
@@ -445,6 +462,7 @@ def run_ours(args):
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_launch": alg},
+        "roofline_by_kernel": per_kernel,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }
