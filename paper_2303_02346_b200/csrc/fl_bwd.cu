@@ -814,11 +814,16 @@ void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_activ
 }
 
 // emitter spawn adjoint, sequential over the substep's spawns (fixed order)
-__global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff) {
+struct EmitBatch {
+    int n;
+    EmitAdjEntry e[kEmitInline];
+};
+
+__global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, EmitBatch inl) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int q = 0; q < n_eff * 12; q++) em_out[q] = 0.0;
     for (int i = 0; i < n; i++) {
-        const EmitAdjEntry e = list[i];
+        const EmitAdjEntry e = list ? list[i] : inl.e[i];
         double xb[3], vb[3];
         for (int a = 0; a < 3; a++) {
             xb[a] = out.x(a)[e.slot];
@@ -837,7 +842,15 @@ __global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* 
 }
 
 void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s) {
-    k_adj_emit<<<1, 32, 0, s>>>(out, list, n, em_out, n_eff);
+    k_adj_emit<<<1, 32, 0, s>>>(out, list, n, em_out, n_eff, EmitBatch{});
+}
+
+void launch_adj_emit_inline(BarBuf out, const EmitAdjEntry* host_list, int n, double* em_out, int n_eff,
+                            cudaStream_t s) {
+    EmitBatch b{};
+    b.n = n;
+    for (int i = 0; i < n; i++) b.e[i] = host_list[i];
+    k_adj_emit<<<1, 32, 0, s>>>(out, nullptr, n, em_out, n_eff, b);
 }
 
 // ---------------------------------------------------------------------------

@@ -1145,13 +1145,17 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         // parked slots are [n_active, n_active + parked): the activated ones are
         // re-keyed in place and sorted in; departed ones drop out at the next sort
         n_active += gained;
-        d_act_list.alloc(r.act.size());
-        CK(cudaMemcpyAsync(d_act_list.p, r.act.data(), r.act.size() * sizeof(ActEntry), cudaMemcpyHostToDevice,
-                           stream));
-        launch_activate(geom, in->p, d_act_list.p, int(r.act.size()), stream);
+        if (r.act.size() <= size_t(kActInline)) {
+            launch_activate_inline(geom, in->p, r.act.data(), int(r.act.size()), stream);
+        } else {
+            d_act_list.alloc(r.act.size());
+            CK(cudaMemcpyAsync(d_act_list.p, r.act.data(), r.act.size() * sizeof(ActEntry),
+                               cudaMemcpyHostToDevice, stream));
+            launch_activate(geom, in->p, d_act_list.p, int(r.act.size()), stream);
+            // the activation list buffer is reused next substep: order the copy
+            CK(cudaStreamSynchronize(stream));
+        }
         launches++;
-        // the activation list buffer is reused next substep: order the copy
-        CK(cudaStreamSynchronize(stream));
     }
     r.n_active = n_active;
     r.n_keep = n_active + n_parked();
@@ -1535,13 +1539,17 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
     launches += 5;
     if (!r.emit.empty()) {
-        d_emit_list.alloc(r.emit.size());
-        CK(cudaMemcpyAsync(d_emit_list.p, r.emit.data(), r.emit.size() * sizeof(EmitAdjEntry),
-                           cudaMemcpyHostToDevice, stream));
-        launch_adj_emit(out, d_emit_list.p, int(r.emit.size()), em_out.p + size_t(t_slot) * kMaxEff * 12,
-                        int(eff.size()), stream);
+        double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;
+        if (r.emit.size() <= size_t(kEmitInline)) {
+            launch_adj_emit_inline(out, r.emit.data(), int(r.emit.size()), eo, int(eff.size()), stream);
+        } else {
+            d_emit_list.alloc(r.emit.size());
+            CK(cudaMemcpyAsync(d_emit_list.p, r.emit.data(), r.emit.size() * sizeof(EmitAdjEntry),
+                               cudaMemcpyHostToDevice, stream));
+            launch_adj_emit(out, d_emit_list.p, int(r.emit.size()), eo, int(eff.size()), stream);
+            CK(cudaStreamSynchronize(stream));
+        }
         launches++;
-        CK(cudaStreamSynchronize(stream));
     }
 }
 

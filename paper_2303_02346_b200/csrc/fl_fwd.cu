@@ -128,10 +128,10 @@ void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* 
 // fp64 from the stage-a effector pose
 // ---------------------------------------------------------------------------
 
-__global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n) {
+__global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n, ActBatch inl) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    ActEntry e = list[i];
+    const ActEntry e = list ? list[i] : inl.e[i];
     if (e.has_xv) {
         for (int a = 0; a < 3; a++) {
             st.x(a)[e.slot] = e.x[a];
@@ -145,7 +145,15 @@ __global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n) {
 
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s) {
     if (n <= 0) return;
-    k_activate<<<(n + 127) / 128, 128, 0, s>>>(g, st, list, n);
+    k_activate<<<(n + 127) / 128, 128, 0, s>>>(g, st, list, n, ActBatch{});
+}
+
+void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, cudaStream_t s) {
+    if (n <= 0) return;
+    ActBatch b{};
+    b.n = n;
+    for (int i = 0; i < n; i++) b.e[i] = host_list[i];
+    k_activate<<<1, 128, 0, s>>>(g, st, nullptr, n, b);
 }
 
 // ---------------------------------------------------------------------------

@@ -53,6 +53,13 @@ struct ActEntry {
     float x[3];
     float v[3];
 };
+// short activation / spawn lists travel as kernel parameters: no host->device copy, so
+// no pageable-copy stream sync on the substep (an emitter adds one particle per substep)
+constexpr int kActInline = 64;
+struct ActBatch {
+    int n;
+    ActEntry e[kActInline];
+};
 
 struct EmitAdjEntry {
     int slot;
@@ -152,6 +159,7 @@ void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double
                    cudaStream_t s);
 void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s);
+void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, cudaStream_t s);
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
                 uint32_t substep, int variant, int* wq, cudaStream_t s);
@@ -194,6 +202,9 @@ void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n_keep, int n_stored,
                       cudaStream_t s);
 void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
+constexpr int kEmitInline = 32;
+void launch_adj_emit_inline(BarBuf out, const EmitAdjEntry* host_list, int n, double* em_out, int n_eff,
+                            cudaStream_t s);
 void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb,
                           const double* Fb, const double* Cb, const ClassInfo* cls, cudaStream_t s);
 void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* vb, double* Fb, double* Cb,
