@@ -36,7 +36,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "MPM particle-substeps/sec fwd & fwd+bwd at 1/2/4/8 B200; HBM GB/s vs peak"
 UNIT = "particle-substeps/s"
 SCENE = "c4"
-HORIZON = 50  # one segment of c4 (optimizer.segment_length)
+HORIZON = 500  # c4's full horizon: optimizer.n_segments (10) x segment_length (50)
 
 # algorithmic bytes per launch unit: fp32 state, each
 # field counted once per kernel that must move it; N = active particles, A =
@@ -258,7 +258,11 @@ def run_ours(args):
     n = w.scene.n_particles
     jobs = world_size if mode == "replicas" else 1  # independent scenes in the job
     T = args.horizon
-    acts = fl.ActionTrajectory(1, T, w.init_action.reshape(1, 6))
+    seglen = min(w.segment_length or T, T)
+    if T % seglen:
+        seglen = T
+    nseg = T // seglen
+    acts = fl.ActionTrajectory(nseg, seglen, np.tile(w.init_action.reshape(1, 6), (nseg, 1)))
     loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
 
     # pinned host copies of the inputs for the end-to-end leg
@@ -277,9 +281,9 @@ def run_ours(args):
     view.effectors = effs
     h2d = sum(pin[k].numel() * 8 for k in pin)
     a_c = acts._c()
-    grad = np.zeros((1, 6))
+    grad = np.zeros((nseg, 6))
     lo, fu, snaps = C.c_double(), C.c_double(), C.c_long()
-    per = np.zeros(1)
+    per = np.zeros(nseg)
 
     def check(rc):
         fl.api._raise(lib, ctx, rc)
@@ -445,8 +449,9 @@ def run_ours(args):
         "scaling": "strong" if mode == "slabs" else "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: reference scene JSON c4 (SURVEY.md App. A) sampled by the reference lattice+jitter rule",
-        "config": {"workload": f"{SCENE}_scooping: grad_trajectory, 1 segment x {T} substeps, stride {T} "
-                               "(forward + adjoint, trajectory kept in HBM), target_point loss",
+        "config": {"workload": f"{SCENE}_scooping: grad_trajectory over the full horizon, {nseg} segments x "
+                               f"{seglen} substeps, stride {T} (forward + adjoint, the whole trajectory kept in "
+                               "HBM: no checkpoint replay), target_point loss per segment",
                    "particles": n, "grid": "128^3", "active_nodes": A, "horizon": T,
                    "l2": "inputs larger than L2 (trajectory store ~%.1f GB per step)" % (n * 112 * (T + 1) / 1e9),
                    "parallelism": {"single": "single", "slabs": f"x-slabs over {world_size} GPUs (NCCL halos)",
@@ -456,7 +461,7 @@ def run_ours(args):
         "fwd": {"value": fwd_value, "unit": UNIT, "workload": f"mpm_substep x {T}, same scene"},
         "fwd_bwd_split_ms": {"forward": fwd_ms / args.steps, "backward": bwd_ms / args.steps},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world_size,
-                "d2h_bytes_per_step": 8 * (6 + 3) * world_size},
+                "d2h_bytes_per_step": 8 * (7 * nseg + 2) * world_size},  # gradient, per-segment and total losses
         "gpu_launches": int(launches),
         "kernels": kern,
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
