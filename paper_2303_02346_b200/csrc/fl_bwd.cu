@@ -234,12 +234,20 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
         const int cnt = r.end - r.start;
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
-            for (int i = tid; i < cnt; i += kScThreads) {
+            const int lim = pass == 0 ? cnt : sc_overflow_prefix(sm, r0, tid);
+            for (int it = tid; it < lim; it += kScThreads) {
+                int c, rank, i;
+                if (pass == 0) {  // every particle in sorted order; ranks beyond the pass wait
+                    i = it;
+                    c = cell_of(sm.cs, i);
+                    rank = i - int(sm.cs[c]);
+                    if (rank >= kScR) continue;
+                } else {  // the dense list of the particles left for this pass
+                    sc_overflow_item(sm, it, c, rank);
+                    i = int(sm.cs[c]) + r0 + rank;
+                }
                 const int j = r.start + i;
                 const uint32_t s = perm[j];
-                const int c = cell_of(sm.cs, i);
-                const int rank = i - int(sm.cs[c]) - r0;
-                if (rank < 0 || rank >= kScR) continue;
                 float* pay = pay_slot(sm, rank, c);
                 const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
                 const uint32_t pmeta = pre.meta[s];

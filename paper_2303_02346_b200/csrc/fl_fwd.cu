@@ -187,13 +187,20 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_p2g(Geom g, PBuf st, const
         const int npass = sc_load_cells(sm, celltab, b, tid);
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
-            if (pass > 0) s_nx = tid < cnt ? perm[r.start + tid] : 0u;
-            for (int i = tid; i < cnt; i += kScThreads) {
-                const int c = cell_of(sm.cs, i);
-                const uint32_t s = s_nx;
-                if (i + kScThreads < cnt) s_nx = perm[r.start + i + kScThreads];
-                const int rank = i - int(sm.cs[c]) - r0;
-                if (rank < 0 || rank >= kScR) continue;
+            const int lim = pass == 0 ? cnt : sc_overflow_prefix(sm, r0, tid);
+            for (int it = tid; it < lim; it += kScThreads) {
+                int c, rank;
+                uint32_t s;
+                if (pass == 0) {  // every particle in sorted order; ranks beyond the pass wait
+                    c = cell_of(sm.cs, it);
+                    s = s_nx;
+                    if (it + kScThreads < cnt) s_nx = perm[r.start + it + kScThreads];
+                    rank = it - int(sm.cs[c]);
+                    if (rank >= kScR) continue;
+                } else {  // the dense list of the particles left for this pass
+                    sc_overflow_item(sm, it, c, rank);
+                    s = perm[r.start + int(sm.cs[c]) + r0 + rank];
+                }
                 float* pay = pay_slot(sm, rank, c);
                 float fx[3];
                 int b0 = base_cell(st.x(0)[s], g.inv_dx, fx[0]);

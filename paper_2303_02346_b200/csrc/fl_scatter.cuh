@@ -72,6 +72,7 @@ struct alignas(16) ScSmem {
     float pay[kPayF * kScR * kCS];
     float tile[4 * kTile];
     uint16_t cs[kCellTab];
+    uint16_t opre[66];  // passes after the first: prefix of the particles each cell still has
 };
 
 __device__ __forceinline__ float* pay_slot(ScSmem& sm, int rank, int cell) { return &sm.pay[rank * kCS + cell]; }
@@ -193,6 +194,40 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
         sm.tile[2 * kTile + t] += s.z;
         sm.tile[3 * kTile + t] += s.w;
     }
+}
+
+// Passes after the first stage only the particles of rank >= r0 in their cell, a few per
+// block: list them densely (prefix over the cells of min(count - r0, kScR)) so whole warps
+// work on them instead of walking every particle with most lanes idle.  Returns the item
+// count; all threads.
+__device__ __forceinline__ int sc_overflow_prefix(ScSmem& sm, int r0, int tid) {
+    if (tid < 32) {
+        const int o0 = min(max(int(sm.cs[2 * tid + 1]) - int(sm.cs[2 * tid]) - r0, 0), kScR);
+        const int o1 = min(max(int(sm.cs[2 * tid + 2]) - int(sm.cs[2 * tid + 1]) - r0, 0), kScR);
+        const int s = o0 + o1;
+        int incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += t;
+        }
+        sm.opre[2 * tid] = uint16_t(incl - s);
+        sm.opre[2 * tid + 1] = uint16_t(incl - s + o0);
+        if (tid == 31) sm.opre[64] = uint16_t(incl);
+    }
+    __syncthreads();
+    return int(sm.opre[64]);
+}
+
+// item -> (cell, rank within the pass) of the dense list above
+__device__ __forceinline__ void sc_overflow_item(const ScSmem& sm, int item, int& c, int& rank) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)
+        if (lo + step < 64 && int(sm.opre[lo + step]) <= item) lo += step;
+    // skip cells with nothing left (equal prefixes): the item belongs to the last of them
+    c = lo;
+    rank = item - int(sm.opre[lo]);
 }
 
 // load the block's cell table (64 cell starts, end, largest cell count); returns
