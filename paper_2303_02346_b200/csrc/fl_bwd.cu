@@ -231,21 +231,15 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
         load_tile(g, gridv, vt, bx, by, bz, tid, kScThreads);
         sc_tile_zero(sm, tid, kScThreads);
         const int npass = sc_load_cells(sm, celltab, b, tid);
-        const int cnt = r.end - r.start;
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
-            const int lim = pass == 0 ? cnt : sc_overflow_prefix(sm, r0, tid);
+            // every pass walks the dense list of the particles it stages (measured: the
+            // sorted walk with idle lanes for ranks beyond the pass is slower here)
+            const int lim = sc_overflow_prefix(sm, r0, tid);
             for (int it = tid; it < lim; it += kScThreads) {
-                int c, rank, i;
-                if (pass == 0) {  // every particle in sorted order; ranks beyond the pass wait
-                    i = it;
-                    c = cell_of(sm.cs, i);
-                    rank = i - int(sm.cs[c]);
-                    if (rank >= kScR) continue;
-                } else {  // the dense list of the particles left for this pass
-                    sc_overflow_item(sm, it, c, rank);
-                    i = int(sm.cs[c]) + r0 + rank;
-                }
+                int c, rank;
+                sc_overflow_item(sm, it, c, rank);
+                const int i = int(sm.cs[c]) + r0 + rank;
                 const int j = r.start + i;
                 const uint32_t s = perm[j];
                 float* pay = pay_slot(sm, rank, c);

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_p2g(Geom g, PBuf st, const
             for (int it = tid; it < lim; it += kScThreads) {
                 int c, rank;
                 uint32_t s;
-                if (pass == 0) {  // every particle in sorted order; ranks beyond the pass wait
+                if (pass == 0) {  // every particle in sorted order (prefetching the permutation)
                     c = cell_of(sm.cs, it);
                     s = s_nx;
                     if (it + kScThreads < cnt) s_nx = perm[r.start + it + kScThreads];

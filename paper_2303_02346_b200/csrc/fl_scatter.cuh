@@ -196,8 +196,8 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
     }
 }
 
-// Passes after the first stage only the particles of rank >= r0 in their cell, a few per
-// block: list them densely (prefix over the cells of min(count - r0, kScR)) so whole warps
+// A pass stages the particles of rank [r0, r0 + kScR) in their cell (after the first
+// pass, a few per block): list them densely (prefix over the cells of min(count - r0, kScR)) so whole warps
 // work on them instead of walking every particle with most lanes idle.  Returns the item
 // count; all threads.
 __device__ __forceinline__ int sc_overflow_prefix(ScSmem& sm, int r0, int tid) {
