@@ -951,7 +951,7 @@ void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     launch_sort_scatter(g, st.p, n, bstart.p, bfill, skey.p, sslot.p, stream);
     launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
                        grid_sort, stream);
-    launches += 4;
+    launches += 5;  // count, list sums, list write, scatter, per-block sort
 }
 
 // ---------------------------------------------------------------------------
@@ -1190,7 +1190,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                         rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
-    launches += 4;
+    launches += 6;  // p2g light + heavy, grid update, g2p light + heavy, tail copy
     if (nbody > 0) {
         // slabs: every rank contributes its members' positions (disjoint support,
         // exact sum) so all ranks fit identical rigid transforms
@@ -1537,7 +1537,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
-    launches += 5;
+    launches += 6;  // g2p adjoint light + heavy, grid adjoint, p2g adjoint light + heavy, tail bars
     if (!r.emit.empty()) {
         double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;
         if (r.emit.size() <= size_t(kEmitInline)) {
