@@ -1190,7 +1190,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                         rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
-    launches += 6;  // p2g light + heavy, grid update, g2p light + heavy, tail copy
+    launches += 5 + (r.n_keep > n_active ? 1 : 0);  // p2g x2, grid update, g2p x2, tail copy if any
     if (nbody > 0) {
         // slabs: every rank contributes its members' positions (disjoint support,
         // exact sum) so all ranks fit identical rigid transforms
@@ -1537,7 +1537,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
-    launches += 6;  // g2p adjoint light + heavy, grid adjoint, p2g adjoint light + heavy, tail bars
+    launches += 5 + (r.n_stored > r.n_active ? 1 : 0);  // g2p adjoint x2, grid adjoint, p2g adjoint x2, tail bars
     if (!r.emit.empty()) {
         double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;
         if (r.emit.size() <= size_t(kEmitInline)) {
