@@ -291,8 +291,27 @@ def run_ours(args):
     def upload():
         check(lib.flume_state_upload(ctx, C.byref(view)))
 
+    # the whole trajectory in HBM (stride = horizon) keeps per substep the state and its
+    # permutation (~124 B per particle) and the recorded grid (two dense float4 node arrays
+    # and a contact mask, ~33 B per node of the block-major grid); where the device cannot
+    # hold it (e.g. several ranks sharing one GPU) the backward replays from checkpoints at
+    # segment boundaries (CheckpointStore stride)
+    try:
+        free_b = torch.cuda.mem_get_info(local)[0]
+    except Exception:
+        free_b = 0
+    per_rank_n = n / world_size if mode == "slabs" else n
+    sharing = max(1, -(-world_size // max(torch.cuda.device_count(), 1)))  # ranks per device
+    nb_tot = 1
+    for d in w.scene.node_dims:
+        nb_tot *= (d + 3) // 4
+    need = sharing * T * (per_rank_n * 124 + 33 * 64 * nb_tot) * 1.15
+    stride = T if (free_b == 0 or free_b > need) else seglen
+    print(f"[bench rank {rank}] free {free_b / 1e9:.1f} GB, whole-trajectory estimate {need / 1e9:.1f} GB "
+          f"-> checkpoint stride {stride}", file=sys.stderr, flush=True)
+
     def step():
-        check(lib.flume_grad_trajectory(ctx, C.byref(a_c), C.byref(loss.desc), 0, 0, _dp(grad), C.byref(lo),
+        check(lib.flume_grad_trajectory(ctx, C.byref(a_c), C.byref(loss.desc), stride, 0, _dp(grad), C.byref(lo),
                                         C.byref(fu), _dp(per), C.byref(snaps)))
 
     def fwd_only():
@@ -450,8 +469,12 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: reference scene JSON c4 (SURVEY.md App. A) sampled by the reference lattice+jitter rule",
         "config": {"workload": f"{SCENE}_scooping: grad_trajectory over the full horizon, {nseg} segments x "
-                               f"{seglen} substeps, stride {T} (forward + adjoint, the whole trajectory kept in "
-                               "HBM: no checkpoint replay), target_point loss per segment",
+                               f"{seglen} substeps, stride {stride} " + (
+                                   "(forward + adjoint, the whole trajectory kept in HBM: no checkpoint replay)"
+                                   if stride == T else
+                                   "(forward + adjoint, checkpoints at segment boundaries: the backward "
+                                   "replays each segment, the device could not hold the whole trajectory)") +
+                               ", target_point loss per segment",
                    "particles": n, "grid": "128^3", "active_nodes": A, "horizon": T,
                    "l2": "inputs larger than L2 (trajectory store ~%.1f GB per step)" % (n * 112 * (T + 1) / 1e9),
                    "parallelism": {"single": "single", "slabs": f"x-slabs over {world_size} GPUs (NCCL halos)",
