@@ -12,6 +12,7 @@
  *   flume_stage_grid                            p2g + grid_update mpm.hpp:249-320
  *   flume_adjoint_substep                       adjoint_substep  adjoint.hpp:476-548
  *   flume_rollout_loss                          rollout_loss     grad.hpp:15-41
+ *   flume_rollout_loss_final                    rollout_loss(..., final_state) grad.hpp:15-41
  *   flume_loss_per_particle                     LossEvaluator::per_particle losses.hpp:367
  *   flume_grad_trajectory                       grad_trajectory  grad.hpp:61-134
  *                                               (+ CheckpointStore checkpoint.hpp:11-50)
