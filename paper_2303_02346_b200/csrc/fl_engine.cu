@@ -253,6 +253,10 @@ struct Ctx {
     }
     template <class Fn>
     void dual(Fn&& fn) {
+        if (!classes_heavy && !upload_full) {  // no SVD/rigid particle can exist: light kernel only
+            fn(false, take_wq(1), stream);
+            return;
+        }
         int* wh = take_wq(2);
         int* wl = wh + 1;
         CK(cudaEventRecord(ev_fork, stream));
@@ -454,6 +458,9 @@ struct Ctx {
     EffSet make_effset(const std::vector<EffState>& es) const;
     void advance_effectors(const double* action);
     bool empty = false;  // no particles at all (N == 0)
+    // heavy (SVD / rigid) blocks are possible: a heavy class is present, or the last upload
+    // (or an adjoint_substep call) handed in a liquid with a full F (kMetaFull)
+    bool classes_heavy = true, upload_full = true;
     void upload(const flume_state_view* view);
     void download(flume_state_view* view);
     void set_effectors(const flume_state_view* view);
@@ -687,6 +694,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     {
         long nh = 0;
         for (int i = 0; i < N; i++) nh += classes[p_class[i]].heavy;
+        classes_heavy = nh > 0;
         hvar = 2 * nh >= N ? 2 : 1;
     }
     grid_p2g = occupancy_grid(KG_P2G, 0);
@@ -808,6 +816,15 @@ void Ctx::check_error(long /*substep_base*/) {
 
 // upload a SimState<3> view; canonical store order is established here
 void Ctx::upload(const flume_state_view* view) {
+    // the host mirror of k_upload's kMetaFull test (fp32 F of an isotropic class != c I)
+    upload_full = false;
+    for (int i = 0; i < N && !upload_full; i++) {
+        if (!classes[size_t(p_class[size_t(i)])].iso) continue;
+        const double* f = view->F + 9 * size_t(i);
+        for (int k = 0; k < 9; k++)
+            if (k % 4 != 0 && float(f[k]) != 0.f) upload_full = true;
+        if (float(f[4]) != float(f[0]) || float(f[8]) != float(f[0])) upload_full = true;
+    }
     if (empty) {
         substep_index = view->substep_index;
         time = view->time;
@@ -1813,6 +1830,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
 void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* ebars,
                               double* abar_out) {
     if (slab()) throw FlumeError(FLUME_E_ARG, "adjoint_substep: single-rank contexts only");
+    upload_full = true;  // the pre-state's liquids are expanded to a full F below (heavy blocks)
     xbar_tmp.alloc(size_t(N) * 3);
     Fbar_tmp.alloc(size_t(N) * 9);
     eff_out.alloc(kMaxEff * 18);
