@@ -1,0 +1,75 @@
+"""Size-independent properties at the BASELINE sizes (full scenes):
+c2-c5 at 1M-8M particles, where the oracle cannot follow every step in seconds.
+
+  * one forward substep of c4 at full size against the reference engine (same tolerance
+    as the small-scene parity tests)
+  * after 10 substeps: every particle finite, the staged grid mass equals the active
+    particles' mass, and the canonical store order is bit-exact (keys recomputed on the CPU
+    from the GPU's fp32 positions, strictly increasing (key, id))
+  * checkpoint strides leave the full-size gradient bit-identical, and a short full-size
+    segment's loss and action gradient match the reference
+"""
+import numpy as np
+import pytest
+
+import paper_2303_02346_b200 as fl
+from tests._util import canonical_keys_cpu, pair, spec_for, state_errors
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c4_full_one_substep_parity(ref_available):
+    w, r = pair(spec_for("c4"))
+    assert w.scene.n_particles > 1_000_000
+    ws = fl.GpuWorkspace(w.scene)
+    fl.mpm_substep(w.scene, w.state, w.init_action, ws)
+    r.substep(w.init_action)
+    e = state_errors(w.state, r.state(), w.scene.dx)
+    assert e["x"] <= 1e-5 and e["v"] <= 1e-5 and e["F"] <= 1e-5 and e["C"] <= 1e-4, e
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_full_size_invariants(name):
+    w = fl.build_scene(spec_for(name))
+    ws = fl.GpuWorkspace(w.scene)
+    fl.mpm_substep(w.scene, w.state, w.init_action, ws, count=10)
+    keys, ids, na, x32 = ws.store_order(w.state)
+    nd = w.scene.node_dims
+    NB = tuple((d + 3) // 4 for d in nd)
+    cpu = canonical_keys_cpu(x32[:, :na], w.scene.dx, nd, NB)
+    assert np.array_equal(cpu, keys[:na].astype(np.uint64))
+    comp = (keys[:na].astype(np.uint64) << np.uint64(32)) | ids[:na].astype(np.uint64)
+    assert np.all(comp[1:] > comp[:-1])
+    assert np.array_equal(np.sort(ids), np.arange(w.scene.n_particles, dtype=np.uint32))
+    for f in (w.state.x, w.state.v, w.state.F, w.state.C):
+        assert np.all(np.isfinite(f))
+    m, _ = fl.p2g_grid(w.scene, w.state, ws)
+    active = w.scene.activation_substep <= w.state.substep_index
+    pm = float(np.sum(w.scene.mass[active]))
+    assert abs(float(m.sum()) - pm) <= 1e-5 * pm, (float(m.sum()), pm)
+
+
+def test_c4_full_gradient_stride_invariance():
+    w = fl.build_scene(spec_for("c4"))
+    ws = fl.GpuWorkspace(w.scene)
+    acts = fl.ActionTrajectory(2, 10, np.tile(w.init_action, (2, 1)))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    g0 = fl.grad_trajectory(w.scene, w.state, acts, loss, stride=0, ws=ws)
+    g5 = fl.grad_trajectory(w.scene, w.state, acts, loss, stride=5, ws=ws)
+    assert g0.loss == g5.loss and np.array_equal(g0.action_grad, g5.action_grad)
+    assert np.all(np.isfinite(g0.action_grad)) and np.any(g0.action_grad != 0)
+
+
+def test_c4_full_gradient_parity(ref_available):
+    """The benchmark workload's gradient at full size over a short segment (the reference
+    needs ~3 s per substep here) against the reference's grad_trajectory."""
+    w, r = pair(spec_for("c4"))
+    ws = fl.GpuWorkspace(w.scene)
+    vals = w.init_action.reshape(1, 6)
+    acts = fl.ActionTrajectory(1, 2, vals)
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    tg = fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
+    rg = r.grad_trajectory(vals, 2, stride=1)
+    assert abs(tg.loss - rg["loss"]) <= 1e-6 * abs(rg["loss"])
+    g, rgr = np.asarray(tg.action_grad).ravel(), np.asarray(rg["grad"]).ravel()
+    assert float(np.max(np.abs(g - rgr)) / (np.max(np.abs(rgr)) + 1e-12)) <= 1e-3, (g, rgr)
