@@ -126,3 +126,14 @@ def test_nccl_transport_single_rank_matches_plain_context():
     g1 = fl.grad_trajectory(w1.scene, w1.state, acts, fl.LossEvaluator(w1.scene, w1.loss_spec, w1.state), ws=ws1)
     g2 = fl.grad_trajectory(w2.scene, w2.state, acts, fl.LossEvaluator(w2.scene, w2.loss_spec, w2.state), ws=ws2)
     assert g1.loss == g2.loss and np.array_equal(g1.action_grad, g2.action_grad)
+
+
+def test_slab_full_c5_bit_identical():
+    """The scaling target scene at full size (8M particles, 256^3): four
+    slabs give one rank's particle states bit for bit after 5 substeps."""
+    spec = spec_for("c5")
+    one, _ = _run(spec, 1, 5)
+    four, info = _run(spec, 4, 5)
+    assert len(info) == 4 and all(s[3] > 1_000_000 for s in info), info
+    for a, b in zip(one, four):
+        assert np.array_equal(a, b)
