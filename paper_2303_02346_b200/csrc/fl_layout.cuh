@@ -138,13 +138,13 @@ __host__ __device__ inline void block_unlin(const Geom& g, int b, int& bx, int& 
 #define FL_PDL 1
 #endif
 #ifndef FL_PDL_TRIGGER
-#define FL_PDL_TRIGGER 1
+#define FL_PDL_TRIGGER 0
 #endif
-// Every kernel starts with this: wait for the previous grid on the stream (its writes
-// are visible afterwards), then allow the next one to be scheduled.  The next grid is
-// released once all CTAs of this one have started (or exited), so its CTAs only take
-// resources this grid no longer needs, and they block in their own wait until this grid
-// has completed: launch latency and CTA rasterisation overlap the tail of this grid.
+// Every kernel starts with this: wait for the previous grid on the stream (its writes are
+// visible afterwards).  FL_PDL_TRIGGER = 1 would also release the next grid right away
+// (griddepcontrol.launch_dependents); measured: neutral on c4, but its early CTAs then sit
+// in their wait holding SM resources, which costs small scenes 8-16% (c1) and starves
+// concurrent contexts of a population, so the dependent launches when this grid exits.
 __device__ __forceinline__ void pdl_wait() {
 #if defined(__CUDA_ARCH__) && FL_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");
