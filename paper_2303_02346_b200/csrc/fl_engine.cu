@@ -458,6 +458,17 @@ struct Ctx {
     EffSet make_effset(const std::vector<EffState>& es) const;
     void advance_effectors(const double* action);
     bool empty = false;  // no particles at all (N == 0)
+#ifndef FL_CAP_GRID
+#define FL_CAP_GRID 1
+#endif
+    // persistent block-list kernels: no more CTAs than ~one per 256 active particles (a
+    // block holds ~8 particles per cell x 64 cells), so small scenes do not launch hundreds
+    // of CTAs that only find the work counter exhausted
+    int sm_count = 148;
+    int light_grid(int grid) const {
+        if (!FL_CAP_GRID) return grid;
+        return std::min(grid, std::max(sm_count, (n_active + 255) / 256));
+    }
     // heavy (SVD / rigid) blocks are possible: a heavy class is present, or the last upload
     // (or an adjoint_substep call) handed in a liquid with a full F (kMetaFull)
     bool classes_heavy = true, upload_full = true;
@@ -707,6 +718,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     grid_ap_h = occupancy_grid(KG_ADJ_P2G, hvar);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    sm_count = sms;
     grid_upd = sms * 8;
 #ifndef FL_SORT_CTAS
 #define FL_SORT_CTAS 8
@@ -1179,7 +1191,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     r.n_stored = n_stored;
     PROF(K_SORT, sort_and_lists(*in, r));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
+             launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     if (slab()) {
@@ -1203,7 +1215,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                            stream));
     }
     PROF(K_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : grid_g2p, d_cls.p, r.gridv,
+             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : light_grid(grid_g2p), d_cls.p, r.gridv,
                         rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
@@ -1260,7 +1272,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
     sort_and_lists(*cur, r);
     EffSet es = make_effset(eff);
     dual([&](bool hv, int* w, cudaStream_t s) {
-        launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : grid_p2g, d_cls.p,
+        launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
                    staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
     });
     if (slab()) {
@@ -1541,7 +1553,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
         launches += 4;
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : grid_adj, d_cls.p,
+             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : light_grid(grid_adj), d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
     if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
@@ -1550,7 +1562,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                                      stream));
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : grid_ap, d_cls.p, gridbar.p,
+             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : light_grid(grid_ap), d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
