@@ -587,24 +587,25 @@ __global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nbloc
 
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, const uint8_t* cmask, cudaStream_t s) {
+                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s) {
     switch (eff.n) {
-        case 0: launch_k(k_adj_grid<0>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 0: launch_k(k_adj_grid<0>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        case 1: launch_k(k_adj_grid<1>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 1: launch_k(k_adj_grid<1>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        case 2: launch_k(k_adj_grid<2>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 2: launch_k(k_adj_grid<2>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        case 3: launch_k(k_adj_grid<3>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+        case 3: launch_k(k_adj_grid<3>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
                                                                      gridbar, eff, eff_partial, cmask); break;
-        default: launch_k(k_adj_grid<kMaxEff>, dim3(kEffBlocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar,
+        default: launch_k(k_adj_grid<kMaxEff>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar,
                                                                             gridv0, gridbar, eff, eff_partial, cmask);
     }
 }
 
-void launch_eff_final(const double* ring, int n_eff, long t0, int count, double* eff_out, cudaStream_t s) {
+void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out,
+                      cudaStream_t s) {
     if (n_eff <= 0 || count <= 0) return;
-    launch_k(k_eff_final, dim3(count * n_eff * kEffQ), dim3(256), 0, s, ring, kEffBlocks, n_eff * kEffQ, t0, eff_out);
+    launch_k(k_eff_final, dim3(count * n_eff * kEffQ), dim3(256), 0, s, ring, nblocks, n_eff * kEffQ, t0, eff_out);
 }
 
 // ---------------------------------------------------------------------------

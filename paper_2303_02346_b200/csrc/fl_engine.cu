@@ -358,6 +358,7 @@ struct Ctx {
     DevArr<float> d_x0;  // [3][N] positions by particle id at upload (LossSet.x0)
     int hvar = 1;  // heavy kernel variant (occupancy_grid)
     int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
+    int eff_blocks = kEffBlocks;
     int grid_p2g_h = 0, grid_g2p_h = 0, grid_adj_h = 0, grid_ap = 0, grid_ap_h = 0;
 
     // live state
@@ -393,7 +394,8 @@ struct Ctx {
     long eff_lo = -1, eff_hi = -1;
     void eff_flush() {
         if (eff_lo < 0) return;
-        launch_eff_final(eff_partial.p, int(eff.size()), eff_lo, int(eff_hi - eff_lo + 1), eff_out.p, stream);
+        launch_eff_final(eff_partial.p, eff_blocks, int(eff.size()), eff_lo, int(eff_hi - eff_lo + 1), eff_out.p,
+                         stream);
         launches++;
         eff_lo = eff_hi = -1;
     }
@@ -688,7 +690,10 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     abar.alloc(std::max(nbody, 1) * 13);
     start_bar.alloc(std::max(nmem, 1) * 3);
     mbar.alloc(std::max(nmem, 1) * 6);
-    eff_partial.alloc(size_t(kEffRing) * kEffBlocks * kMaxEff * 18);
+    // grid adjoint: one 64-thread CTA per node block up to kEffBlocks; small scenes get fewer
+    // (every CTA writes its effector-bar partials, which the final sums then read)
+    eff_blocks = std::max(148, std::min(kEffBlocks, (N + 63) / 64));
+    eff_partial.alloc(size_t(kEffRing) * eff_blocks * kMaxEff * 18);
     loss_partial.alloc(size_t(kLossBlocks) * kMaxLossTerms);
     d_act_list.alloc(64);
     d_emit_list.alloc(64);
@@ -1558,8 +1563,8 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
          }));
     if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                     eff_partial.p + size_t(t_slot % kEffRing) * kEffBlocks * kMaxEff * 18, r.cmask,
-                                     stream));
+                                     eff_partial.p + size_t(t_slot % kEffRing) * eff_blocks * kMaxEff * 18, r.cmask,
+                                     eff_blocks, stream));
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : light_grid(grid_ap), d_cls.p, gridbar.p,

@@ -150,7 +150,7 @@ void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassIn
 #ifndef FL_EFF_BLOCKS
 #define FL_EFF_BLOCKS 3552
 #endif
-constexpr int kEffBlocks = FL_EFF_BLOCKS;  // grid of the grid adjoint = its effector-bar partials
+constexpr int kEffBlocks = FL_EFF_BLOCKS;  // largest grid of the grid adjoint = its effector-bar partials
 constexpr int kRigidChunk = 2048;
 
 // ---- forward ----
@@ -193,9 +193,10 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     float4* staging_bar, int variant, int* wq, cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, const uint8_t* cmask, cudaStream_t s);
+                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s);
 constexpr int kEffRing = 16;  // substeps whose effector-bar partials wait for one final-sum launch
-void launch_eff_final(const double* ring, int n_eff, long t0, int count, double* eff_out, cudaStream_t s);
+void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out,
+                      cudaStream_t s);
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, int variant, int* wq, cudaStream_t s);
