@@ -553,10 +553,10 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
         gridbar[idx] = make_float4(pb0, pb1, pb2, mb);
     }
     __syncthreads();
-    for (int q = tid; q < kMaxEff * kEffQ; q += kAdjGridThreads) {
+    // only the NE effectors' components: the final sums read no further (nq = n_eff * 18)
+    for (int q = tid; q < NE * kEffQ; q += kAdjGridThreads) {
         double s = 0.0;
-        if (q < NE * kEffQ)
-            for (int w = 0; w < kW; w++) s += wacc[w][q];
+        for (int w = 0; w < kW; w++) s += wacc[w][q];
         eff_partial[size_t(blockIdx.x) * kMaxEff * kEffQ + q] = s;
     }
 }
