@@ -1,19 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark: MPM particle-substeps/s, forward+backward, on the 1M-particle multi-material scene.
 
-One "step" = one grad_trajectory (grad.hpp:61-134) over one segment of the c4
-scooping scene (1,027,233 particles of water + an
-elastic floater on a 128^3 grid, a three-box ladle effector), i.e. T forward
-substeps with the trajectory kept in HBM, a target-point loss, and T adjoint
-substeps producing the action gradient.  value = particles * T / device time.
+One "step" = one grad_trajectory (grad.hpp:61-134) over the full horizon of the
+scene (10 segments x 50 substeps): T forward substeps, a target-point loss per
+segment, and T adjoint substeps producing the action gradient.
+value = active particles * T / device time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one process per GPU) splits the SAME scene into x-slabs, one
-per GPU: halo planes and migrating particles go to the
-neighbouring ranks over NCCL, rigid/loss/effector sums are all-reduced, so the
-scaling is strong.  If the slab transport cannot start, each GPU runs an
-independent replica instead and the line says so.  The reference arm (--impl reference) times the unmodified reference engine
+N = 1: the c4 scooping scene (1,027,233 particles of
+water + an elastic floater on a 128^3 grid, a three-box ladle effector), the
+1M-particle multi-material scene the north star's single-GPU target names.
+The same line carries `configs` (c1, c2, c3, c5 on one GPU, one segment each)
+and `scaling_base` (c5 on one GPU over the same full horizon as N > 1).
+N > 1 (torchrun, one process per GPU): the north star's scaling scene c5
+(8,044,544 particles, 256^3) split into x-slabs, one per GPU:
+halo planes and migrating particles go to the neighbouring ranks over NCCL,
+rigid/loss/effector sums are all-reduced, so the scaling is strong (compare
+with `scaling_base` of the N = 1 line).  If the slab transport cannot start the
+run prints an `error` line and exits non-zero (no silent fallback).
+The reference arm (--impl reference) times the unmodified reference engine
 (oracle/_ref, proj/include/flume compiled as-is) on this host's CPU cores.
 """
 from __future__ import annotations
@@ -35,7 +41,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "MPM particle-substeps/sec fwd & fwd+bwd at 1/2/4/8 B200; HBM GB/s vs peak"
 UNIT = "particle-substeps/s"
-SCENE = "c4"
+SCENE = "c4"        # N = 1
+SCENE_SCALE = "c5"  # N > 1: the 8M-particle 256^3 slab-partitioned scene
 HORIZON = 500  # c4's full horizon: optimizer.n_segments (10) x segment_length (50)
 
 # algorithmic bytes per launch unit: fp32 state, each
@@ -119,12 +126,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(near), "samples_in_window": len(win)}
 
 
-def cpu_reference_sample(substeps: int = 4, stride: int = 2):
+def cpu_reference_sample(scene: str = SCENE, substeps: int = 4, stride: int = 2):
     """The reference engine (oracle/_ref) on this host, single-threaded like the reference:
     grad_trajectory over `substeps` substeps of the same scene (SURVEY.md 8(d) protocol)."""
     from oracle import ref
     from paper_2303_02346_b200 import scenes
-    spec = scenes.load(SCENE)
+    spec = scenes.load(scene)
     r = ref.RefWorld(spec)
     init = np.array(spec["optimizer"]["init"], dtype=np.float64)
     t0 = time.perf_counter()
@@ -156,8 +163,14 @@ def run_reference(args):
     except Exception:
         avail = 64e9
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    reps = max(1, min(threads, int(avail // 3e9)))  # ~0.5 GB per c4 replica, 3 GB of headroom each
-    spec = scenes.load(SCENE)
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    scene = args.scene or (SCENE if world_size == 1 else SCENE_SCALE)  # the same workload as our arm
+    spec = scenes.load(scene)
+    # a replica holds the AoS state (224 B/particle) ~4 times over (state, capture, cache) plus
+    # the 56 B/node grid; c4 ~1.1 GB, c5 ~8.2 GB -- keep 2x headroom
+    res = spec["grid_resolution"]
+    per_rep = 2 * (4 * 224 * 1.03e6 * (res / 128) ** 3 + 56 * (res + 1) ** 3)
+    reps = max(1, min(threads, int(avail // per_rep)))
     init = np.array(spec["optimizer"]["init"], dtype=np.float64).reshape(1, 6)
     sub = 1  # one forward + adjoint substep per replica per step keeps K + W steps within minutes
     with ThreadPoolExecutor(reps) as pool:
@@ -179,11 +192,11 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{SCENE}_scooping grad_trajectory, {sub}-substep sample per step per replica, "
-                                   f"stride 1; {reps} independent replicas, one per host thread",
-                       "particles": n, "grid": "128^3", "replicas": reps},
+            "config": {"workload": f"{scenes.NAMES[scene]} grad_trajectory, {sub}-substep sample per step per "
+                                   f"replica, stride 1; {reps} independent replicas, one per host thread",
+                       "particles": n, "grid": f"{res}^3", "replicas": reps},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": reps, "kind": "reference",
-                             "sample": f"grad_trajectory over {sub} substeps of {SCENE} per replica per step "
+                             "sample": f"grad_trajectory over {sub} substeps of {scene} per replica per step "
                                        f"({reps} threads, g++ -O3 build of proj/include)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -201,6 +214,70 @@ def _watchdog(seconds: float, rank: int):
     t.start()
 
 
+def _device_ms(lib, ctx, check, fn, slot0=6):
+    """Device time of fn() on the context stream (CUDA events on that stream)."""
+    import ctypes as C
+    check(lib.flume_timer_mark(ctx, slot0))
+    fn()
+    check(lib.flume_timer_mark(ctx, slot0 + 1))
+    ms = C.c_double()
+    check(lib.flume_timer_elapsed(ctx, slot0, slot0 + 1, C.byref(ms)))
+    return ms.value
+
+
+def _stride_for(fl, w, T, seglen, n_local, device, sharing=1):
+    """The whole trajectory in HBM (stride = horizon) keeps per substep the state and its
+    permutation (~124 B per particle) and the recorded grid (two dense float4 node arrays and
+    a contact mask, ~33 B per node of the block-major grid); where the device cannot hold it
+    the backward replays from checkpoints at segment boundaries (CheckpointStore stride)."""
+    import torch
+    try:
+        free_b = torch.cuda.mem_get_info(device)[0]
+    except Exception:
+        free_b = 0
+    nb_tot = 1
+    for d in w.scene.node_dims:
+        nb_tot *= (d + 3) // 4
+    need = sharing * T * (n_local * 124 + 33 * 64 * nb_tot) * 1.15
+    return (T if (free_b == 0 or free_b > need) else seglen), free_b, need
+
+
+def scene_rates(name, steps, warmup, horizon=None, device=0):
+    """One-GPU fwd and fwd+bwd rates of a BASELINE config (device time, CUDA events): fwd+bwd =
+    grad_trajectory over `horizon` substeps (default one optimizer segment), fwd = the same
+    number of mpm_substep calls from the uploaded state (re-uploaded, untimed, every step)."""
+    import paper_2303_02346_b200 as fl
+    from paper_2303_02346_b200 import scenes
+    w = fl.build_scene(scenes.load(name))
+    ws = fl.GpuWorkspace(w.scene, device=device)
+    lib, ctx = ws.lib, ws.ctx
+    check = lambda rc: fl.api._raise(lib, ctx, rc)  # noqa: E731
+    n = int(np.sum(w.scene.activation_substep <= 0))
+    seglen = w.segment_length or 50
+    T = horizon or seglen
+    nseg = max(1, T // seglen)
+    seglen = T // nseg
+    acts = fl.ActionTrajectory(nseg, seglen, np.tile(w.init_action.reshape(1, 6), (nseg, 1)))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    stride, _, _ = _stride_for(fl, w, T, seglen, n, device)
+    for _ in range(warmup):
+        fl.grad_trajectory(w.scene, w.state, acts, loss, stride=stride, ws=ws)
+    gms = 0.0
+    for _ in range(steps):
+        g = fl.grad_trajectory(w.scene, w.state, acts, loss, stride=stride, ws=ws)
+        gms += g.forward_ms + g.backward_ms
+    fms = 0.0
+    for _ in range(steps):
+        st = w.state.copy()
+        ws._upload(st)
+        fms += _device_ms(lib, ctx, check, lambda: check(lib.flume_substep(ctx, fl.api._dp(w.init_action), T)))
+    out = {"particles": n, "grid": f"{w.scene.grid_resolution}^3", "substeps": T, "stride": stride,
+           "fwd_bwd": n * T * steps / (gms / 1e3), "fwd": n * T * steps / (fms / 1e3),
+           "fwd_bwd_ms_per_substep": gms / steps / T, "fwd_ms_per_substep": fms / steps / T}
+    ws.close()
+    return out
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -212,8 +289,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    import torch
     if world_size > 1:
-        import torch
         import torch.distributed as dist
         # (more ranks than visible GPUs only happens when the launcher is exercised on a
         # small box; the ranks then share devices)
@@ -224,10 +301,11 @@ def run_ours(args):
         dist.init_process_group("gloo")
         _watchdog(args.deadline, rank)
 
-    spec = scenes.load(SCENE)
+    scene_name = args.scene or (SCENE if world_size == 1 else SCENE_SCALE)
+    spec = scenes.load(scene_name)
     w = fl.build_scene(spec)
     lib = _abi.load()
-    mode, note = "single", None
+    mode = "single"
     ws = None
     if world_size > 1:
         obj = [None]
@@ -237,26 +315,27 @@ def run_ours(args):
             except Exception as e:
                 obj[0] = "error: " + str(e)
         dist.broadcast_object_list(obj, src=0)
+        err = None
         if isinstance(obj[0], bytes):
             try:
                 ws = fl.GpuWorkspace.distributed(w.scene, local, rank, world_size, obj[0])
                 mode = "slabs"
             except Exception as e:
-                note = f"slab transport unavailable ({e}); independent replicas"
+                err = str(e)
         else:
-            note = f"slab transport unavailable ({obj[0]}); independent replicas"
+            err = obj[0]
         ok = torch.tensor([1 if mode == "slabs" else 0])
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0 and mode == "slabs":
-            mode, note = "replicas", "slab transport failed on a peer rank; independent replicas"
-            ws = None
-        elif mode != "slabs":
-            mode = "replicas"
+        if int(ok.item()) == 0:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world_size,
+                                  "error": f"x-slab NCCL transport did not start: {err or 'failed on a peer rank'}"}),
+                      flush=True)
+            os._exit(4)
     if ws is None:
         ws = fl.GpuWorkspace(w.scene, device=local)
     ctx = ws.ctx
-    n = w.scene.n_particles
-    jobs = world_size if mode == "replicas" else 1  # independent scenes in the job
+    n = int(np.sum(w.scene.activation_substep <= 0))
     T = args.horizon
     seglen = min(w.segment_length or T, T)
     if T % seglen:
@@ -266,7 +345,6 @@ def run_ours(args):
     loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
 
     # pinned host copies of the inputs for the end-to-end leg
-    import torch
     pin = {k: torch.empty(getattr(w.state, k).shape, dtype=torch.float64).pin_memory()
            for k in ("x", "v", "F", "C")}
     for k in pin:
@@ -291,24 +369,11 @@ def run_ours(args):
     def upload():
         check(lib.flume_state_upload(ctx, C.byref(view)))
 
-    # the whole trajectory in HBM (stride = horizon) keeps per substep the state and its
-    # permutation (~124 B per particle) and the recorded grid (two dense float4 node arrays
-    # and a contact mask, ~33 B per node of the block-major grid); where the device cannot
-    # hold it (e.g. several ranks sharing one GPU) the backward replays from checkpoints at
-    # segment boundaries (CheckpointStore stride)
-    try:
-        free_b = torch.cuda.mem_get_info(local)[0]
-    except Exception:
-        free_b = 0
-    per_rank_n = n / world_size if mode == "slabs" else n
     sharing = max(1, -(-world_size // max(torch.cuda.device_count(), 1)))  # ranks per device
-    nb_tot = 1
-    for d in w.scene.node_dims:
-        nb_tot *= (d + 3) // 4
-    need = sharing * T * (per_rank_n * 124 + 33 * 64 * nb_tot) * 1.15
-    stride = T if (free_b == 0 or free_b > need) else seglen
-    print(f"[bench rank {rank}] free {free_b / 1e9:.1f} GB, whole-trajectory estimate {need / 1e9:.1f} GB "
-          f"-> checkpoint stride {stride}", file=sys.stderr, flush=True)
+    per_rank_n = n / world_size if mode == "slabs" else n
+    stride, free_b, need = _stride_for(fl, w, T, seglen, per_rank_n, local, sharing)
+    print(f"[bench rank {rank}] {scene_name}: free {free_b / 1e9:.1f} GB, whole-trajectory estimate "
+          f"{need / 1e9:.1f} GB -> checkpoint stride {stride}", file=sys.stderr, flush=True)
 
     def step():
         check(lib.flume_grad_trajectory(ctx, C.byref(a_c), C.byref(loss.desc), stride, 0, _dp(grad), C.byref(lo),
@@ -316,6 +381,13 @@ def run_ours(args):
 
     def fwd_only():
         check(lib.flume_substep(ctx, _dp(w.init_action), T))
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        tt = torch.tensor([v])
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
 
     upload()
     # the clock sampler runs from the warm-up on; its summary keeps the samples
@@ -342,7 +414,9 @@ def run_ours(args):
         ms = C.c_double()
         check(lib.flume_timer_elapsed(ctx, 0, 1, C.byref(ms)))
         clocks.mark("end")
-    total_ms = ms.value
+        if dist:
+            dist.barrier()
+    total_ms = max_over_ranks(ms.value)
     # ---- per-kernel CUDA-event times: a separate instrumented pass of the same K steps
     #      (event bookkeeping on the host would otherwise perturb the timed region) ----
     check(lib.flume_profile(ctx, 1))
@@ -352,30 +426,21 @@ def run_ours(args):
     kcnt = (C.c_long * 9)()
     check(lib.flume_kernel_times(ctx, kms, kcnt, 9))
     check(lib.flume_profile(ctx, 0))
-    if dist:
-        tt = torch.tensor([total_ms], )
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    value = jobs * n * T * args.steps / (total_ms / 1e3)
+    value = n * T * args.steps / (total_ms / 1e3)
 
-    # ---- forward-only rate (mpm_substep chain), same scene ----
-    upload()
-    check(lib.flume_sync(ctx))
-    check(lib.flume_timer_mark(ctx, 2))
+    # ---- forward-only rate (mpm_substep chain over the same horizon from the same
+    #      uploaded state: re-uploaded before every step, outside the timed events) ----
+    fwd_ms_all = 0.0
     for _ in range(args.steps):
-        fwd_only()
-    check(lib.flume_timer_mark(ctx, 3))
-    fms = C.c_double()
-    check(lib.flume_timer_elapsed(ctx, 2, 3, C.byref(fms)))
-    fwd_ms_all = fms.value
-    if dist:
-        tt = torch.tensor([fwd_ms_all], )
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        fwd_ms_all = float(tt.item())
-    fwd_value = jobs * n * T * args.steps / (fwd_ms_all / 1e3)
+        upload()
+        fwd_ms_all += _device_ms(lib, ctx, check, fwd_only, 2)
+    fwd_ms_all = max_over_ranks(fwd_ms_all)
+    fwd_value = n * T * args.steps / (fwd_ms_all / 1e3)
 
     # ---- end to end through the public C ABI: H2D of the state from pinned host
     #      memory, grad_trajectory, D2H of loss + action gradient, every step ----
+    if dist:
+        dist.barrier()
     check(lib.flume_timer_mark(ctx, 4))
     for _ in range(args.steps):
         upload()
@@ -383,12 +448,8 @@ def run_ours(args):
     check(lib.flume_timer_mark(ctx, 5))
     ems = C.c_double()
     check(lib.flume_timer_elapsed(ctx, 4, 5, C.byref(ems)))
-    e2e_ms = ems.value
-    if dist:
-        tt = torch.tensor([e2e_ms], )
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    e2e_value = jobs * n * T * args.steps / (e2e_ms / 1e3)
+    e2e_ms = max_over_ranks(ems.value)
+    e2e_value = n * T * args.steps / (e2e_ms / 1e3)
     # slabs: rank 0's share of the work, for its roofline line
     keys, ids, na, _ = ws.store_order(w.state)
 
@@ -455,33 +516,53 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu and world_size == 1:
         try:
-            rate, rn, dt = cpu_reference_sample(4, 2)
+            rate, rn, dt = cpu_reference_sample(scene_name, 4, 2)
             cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
-                   "sample": f"reference grad_trajectory, {SCENE} ({rn} particles), 4 substeps, stride 2, "
+                   "sample": f"reference grad_trajectory, {scene_name} ({rn} particles), 4 substeps, stride 2, "
                              f"{dt:.1f} s on 1 host core (g++ -O3 build of proj/include)"}
         except Exception as e:  # keep the GPU line even if the host leg fails
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
+    # ---- the other BASELINE configs on this GPU (one optimizer segment each), and the
+    #      strong-scaling base: the N > 1 workload (c5, full horizon) on one GPU ----
+    configs, scaling_base = {}, None
+    if world_size == 1 and not args.no_configs:
+        ws.close()
+        for name in ("c1", "c2", "c3", "c5"):
+            try:
+                configs[name] = scene_rates(name, 2, 1, device=local)
+            except Exception as e:
+                configs[name] = {"error": str(e)}
+        try:
+            sb = scene_rates(SCENE_SCALE, 1, 1, horizon=T, device=local)
+            scaling_base = {"scene": SCENE_SCALE, "value": sb["fwd_bwd"], "fwd": sb["fwd"], "unit": UNIT,
+                            "particles": sb["particles"], "horizon": T, "stride": sb["stride"],
+                            "note": "bench.py --gpus N>1 runs this workload as x-slabs; strong-scaling "
+                                    "efficiency(N) = value(N) / (N * this value)"}
+        except Exception as e:
+            scaling_base = {"scene": SCENE_SCALE, "error": str(e)}
+
+    grid = f"{w.scene.grid_resolution}^3"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if mode == "slabs" else "weak",
         "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: reference scene JSON c4 (SURVEY.md App. A) sampled by the reference lattice+jitter rule",
-        "config": {"workload": f"{SCENE}_scooping: grad_trajectory over the full horizon, {nseg} segments x "
-                               f"{seglen} substeps, stride {stride} " + (
+        "data": f"synthetic: reference scene JSON {scene_name} (SURVEY.md App. A) sampled by the reference "
+                "lattice+jitter rule",
+        "config": {"workload": f"{scenes.NAMES[scene_name]}: grad_trajectory over the full horizon, {nseg} "
+                               f"segments x {seglen} substeps, stride {stride} " + (
                                    "(forward + adjoint, the whole trajectory kept in HBM: no checkpoint replay)"
                                    if stride == T else
                                    "(forward + adjoint, checkpoints at segment boundaries: the backward "
                                    "replays each segment, the device could not hold the whole trajectory)") +
                                ", target_point loss per segment",
-                   "particles": n, "grid": "128^3", "active_nodes": A, "horizon": T,
+                   "particles": n, "grid": grid, "active_nodes": A, "horizon": T,
                    "l2": "inputs larger than L2 (trajectory store ~%.1f GB per step)" % (n * 112 * (T + 1) / 1e9),
-                   "parallelism": {"single": "single", "slabs": f"x-slabs over {world_size} GPUs (NCCL halos)",
-                                   "replicas": f"{world_size} independent replicas"}[mode],
-                   **({"note": note} if note else {}),
+                   "parallelism": "single" if mode == "single" else f"x-slabs over {world_size} GPUs (NCCL halos)",
                    **({"rank0_particles": n_local} if mode == "slabs" else {})},
-        "fwd": {"value": fwd_value, "unit": UNIT, "workload": f"mpm_substep x {T}, same scene"},
+        "fwd": {"value": fwd_value, "unit": UNIT,
+                "workload": f"mpm_substep x {T} from the uploaded state (re-uploaded untimed every step)"},
         "fwd_bwd_split_ms": {"forward": fwd_ms / args.steps, "backward": bwd_ms / args.steps},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world_size,
                 "d2h_bytes_per_step": 8 * (7 * nseg + 2) * world_size},  # gradient, per-segment and total losses
@@ -493,6 +574,8 @@ def run_ours(args):
         "roofline_by_kernel": per_kernel,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
+        **({"configs": configs} if configs else {}),
+        **({"scaling_base": scaling_base} if scaling_base else {}),
     }
     print(json.dumps(line))
     if dist:
@@ -507,6 +590,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--horizon", type=int, default=HORIZON)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config and scaling-base legs")
+    ap.add_argument("--scene", default=None, help="override the scene (c1..c5)")
     ap.add_argument("--deadline", type=float, default=600.0, help="multi-GPU watchdog (s)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -467,10 +467,11 @@ struct Ctx {
     // block holds ~8 particles per cell x 64 cells), so small scenes do not launch hundreds
     // of CTAs that only find the work counter exhausted
     int sm_count = 148;
-    int light_grid(int grid) const {
+    int light_grid(int grid, int active) const {
         if (!FL_CAP_GRID) return grid;
-        return std::min(grid, std::max(sm_count, (n_active + 255) / 256));
+        return std::min(grid, std::max(sm_count, (active + 255) / 256));
     }
+    int light_grid(int grid) const { return light_grid(grid, n_active); }
     // heavy (SVD / rigid) blocks are possible: a heavy class is present, or the last upload
     // (or an adjoint_substep call) handed in a liquid with a full F (kMetaFull)
     bool classes_heavy = true, upload_full = true;
@@ -690,10 +691,6 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     abar.alloc(std::max(nbody, 1) * 13);
     start_bar.alloc(std::max(nmem, 1) * 3);
     mbar.alloc(std::max(nmem, 1) * 6);
-    // grid adjoint: one 64-thread CTA per node block up to kEffBlocks; small scenes get fewer
-    // (every CTA writes its effector-bar partials, which the final sums then read)
-    eff_blocks = std::max(148, std::min(kEffBlocks, (N + 63) / 64));
-    eff_partial.alloc(size_t(kEffRing) * eff_blocks * kMaxEff * 18);
     loss_partial.alloc(size_t(kLossBlocks) * kMaxLossTerms);
     d_act_list.alloc(64);
     d_emit_list.alloc(64);
@@ -725,6 +722,12 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     sm_count = sms;
     grid_upd = sms * 8;
+    // grid adjoint: one 64-thread CTA per node block up to kEffBlocks; small scenes get fewer
+    // (every CTA writes its effector-bar partials, which the final sums then read).  Sized by
+    // the scene (grid-stride loop over the touched node blocks: never more CTAs than node
+    // blocks or ~1 per 64 particles), at least one CTA per SM.
+    eff_blocks = std::max(sm_count, std::min({kEffBlocks, g.nbtot, (N + 63) / 64}));
+    eff_partial.alloc(size_t(kEffRing) * eff_blocks * kMaxEff * 18);
 #ifndef FL_SORT_CTAS
 #define FL_SORT_CTAS 8
 #endif
@@ -789,6 +792,7 @@ void Ctx::advance_effectors(const double* action) {
 }
 
 void Ctx::check_error(long /*substep_base*/) {
+    check_launch();  // a rejected <<<>>> launch (invalid config, resources) must not pass silently
     unsigned long long h = 0;
     allreduce(d_err.p, 1, DType::U64, ROp::Min);  // slabs: every rank raises the same error
     CK(cudaMemcpyAsync(&h, d_err.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
@@ -1087,7 +1091,10 @@ void Ctx::migrate(StateBuf& out, Record& r) {
     const size_t ss[2] = {mig_bytes(h[0]), mig_bytes(h[1])}, rs[2] = {mig_bytes(int(recv[0])), mig_bytes(int(recv[1]))};
     comm->neighbor_exchange(sb, ss, rb, rs, stream);
     const int base = n_active + n_parked();
-    if (base + recv[0] + recv[1] > N) throw FlumeError(FLUME_E_ENGINE, "slab store overflow");
+    if (base + recv[0] + recv[1] > N) {
+        comm->abort();
+        throw FlumeError(FLUME_E_ENGINE, "slab store overflow");
+    }
     launch_mig_unpack(out.p, mig_recv[0].p, int(recv[0]), base, stream);
     launch_mig_unpack(out.p, mig_recv[1].p, int(recv[1]), base + int(recv[0]), stream);
     launches += 3;
@@ -1242,6 +1249,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     out->n = n_stored;
     time += cfg.dt_substep;
     substep_index++;
+    check_launch();
 }
 
 void Ctx::substep(const double* action, int count) {
@@ -1558,7 +1566,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
         launches += 4;
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : light_grid(grid_adj), d_cls.p,
+             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : light_grid(grid_adj, r.n_active), d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
     if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
@@ -1567,11 +1575,12 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                                      eff_blocks, stream));
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : light_grid(grid_ap), d_cls.p, gridbar.p,
+             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : light_grid(grid_ap, r.n_active), d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
     launches += 5 + (r.n_stored > r.n_active ? 1 : 0);  // g2p adjoint x2, grid adjoint, p2g adjoint x2, tail bars
+    check_launch();
     if (!r.emit.empty()) {
         double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;
         if (r.emit.size() <= size_t(kEmitInline)) {

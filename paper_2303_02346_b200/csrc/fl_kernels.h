@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <stdexcept>
+#include <string>
 #include <utility>
 
 #include "fl_layout.cuh"
@@ -22,7 +24,14 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     attr[0].val.programmaticStreamSerializationAllowed = FL_PDL;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+}
+
+// <<<>>> launches report through cudaGetLastError; called after each launch group
+inline void check_launch() {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
 }
 
 // rigid-body bookkeeping for one substep (forward record / backward input)
