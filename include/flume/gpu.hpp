@@ -18,7 +18,8 @@
 //
 // The loss is passed as the scene's loss JSON (World::loss_spec, the input of
 // LossEvaluator, losses.hpp:311) because LossEvaluator keeps its terms private;
-// target_point, hold_initial and composite specs are supported on the device.
+// target_point, hold_initial, chamfer, mixing_spread (with the attraction term)
+// and composite specs are evaluated on the device.
 // Errors rethrow the reference exception types (core.hpp:18-48).
 #pragma once
 
