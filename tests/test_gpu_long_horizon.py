@@ -24,9 +24,10 @@ pytestmark = pytest.mark.gpu
 # reference from an fp32-rounded initial state): one rounding moves the state by ~2e-6 dx
 # (c1, c2, c5) to 4e-6 dx (c3) over 100 substeps, and the device rounds every substep, so
 # ~100x that is the fp32 floor.  SVD materials sit higher: c3's non-Newtonian return map
-# (von Mises, a non-smooth projection) and c5's stiff solids get 5e-4 (c3's v: 1e-3).
+# (von Mises, a non-smooth projection) and c5's stiff solids get 5e-4 (c3's v: 1e-3).  c4
+# over the bench's 500 substeps: one rounding moves x by 5.0e-6 dx, so 500 x that = 2.5e-3.
 STATE_TOL = {"c1_4x25": 1e-4, "c3_fwd100": 5e-4, "c2_64_10x50": 1e-4, "c3_64_10x50": 5e-4,
-             "c5_64_10x50": 5e-4, "c4_fwd500": 1e-3}
+             "c5_64_10x50": 5e-4, "c4_fwd500": 2.5e-3}
 V_TOL = {"c3_fwd100": 1e-3, "c3_64_10x50": 1e-3}
 GRAD_TOL = {"c1_4x25": 1e-3, "c4pool_2x25": 1e-3, "c4_10x50": 1e-2, "c2_64_10x50": 1e-2, "c3_64_10x50": 1e-2,
             "c5_64_10x50": 1e-2}
