@@ -1,8 +1,9 @@
 // fl_bwd.cu -- reverse-mode MLS-MPM substep kernels for sm_100a.
 //
 // Mirrors adjoint_substep (proj/include/flume/adjoint.hpp:476-548) without the
-// reference's capture_forward re-run: the pre-state of the substep is read from
-// the trajectory store, the forward grid is rebuilt by one P2G + grid update,
+// reference's capture_forward re-run: the pre-state of the substep, its
+// permutation/block map and the forward grid (velocities after contact, p/m and
+// m before it) are all read from the substep's record in the trajectory store,
 // and then
 //   adjoint_rigid_pass   (adjoint.hpp:210-279)   k_adj_rigid_*
 //   adjoint_g2p          (adjoint.hpp:281-365)   k_adj_g2p   (gather + scatter of grid v_bar)
@@ -217,7 +218,12 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
     extern __shared__ __align__(16) unsigned char smraw[];
     ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
     float4* vt = reinterpret_cast<float4*>(smraw + sizeof(ScSmem));
+    float4* raw = reinterpret_cast<float4*>(sm.pay);  // raw TMA tile: the payload area is idle here
+    static_assert(sizeof(float) * kPayF * kScR * kCS >= sizeof(float4) * kTileRaw, "raw tile alias");
+    __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
+    TileStage ts;
+    ts.init(&bar, raw, tid);
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     const int my_c = tid & 63, my_ox = tid >> 6;
     __shared__ int sh_next;
@@ -227,10 +233,12 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
-        __syncthreads();
-        load_tile(g, gridv, vt, bx, by, bz, tid, kScThreads);
+        ts.begin(g, gridv, bx, by, bz, tid);
         sc_tile_zero(sm, tid, kScThreads);
         const int npass = sc_load_cells(sm, celltab, b, tid);
+        // repack before the first pass: its prefix barrier orders these raw reads
+        // before the payload writes into the same bytes
+        ts.end(g, gridv, vt, bx, by, bz, tid, kScThreads);
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
             // every pass walks the dense list of the particles it stages (measured: the
@@ -621,7 +629,11 @@ __global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const u
                                                  int cap, int* wq) {
     pdl_wait();
     __shared__ float4 bt[kTile];
+    __shared__ __align__(128) float4 raw[FL_TMA_TILE ? kTileRaw : 1];
+    __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
+    TileStage ts;
+    ts.init(&bar, raw, tid);
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     __shared__ int sh_next;
     for (;;) {
@@ -630,9 +642,9 @@ __global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const u
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
+        ts.begin(g, gridbar, bx, by, bz, tid);
         uint32_t s_nx = r.start + tid < r.end ? perm[r.start + tid] : 0u;  // see k_g2p
-        __syncthreads();
-        load_tile(g, gridbar, bt, bx, by, bz, tid, 128);
+        ts.end(g, gridbar, bt, bx, by, bz, tid, 128);
         __syncthreads();
         for (int j = r.start + tid; j < r.end; j += 128) {
             const uint32_t s = s_nx;

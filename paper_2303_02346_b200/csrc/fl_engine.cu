@@ -255,8 +255,10 @@ struct Ctx {
     void dual(Fn&& fn) {
         if (!classes_heavy && !upload_full) {  // no SVD/rigid particle can exist: light kernel only
             fn(false, take_wq(1), stream);
+            launches += 1;
             return;
         }
+        launches += 2;
         int* wh = take_wq(2);
         int* wl = wh + 1;
         CK(cudaEventRecord(ev_fork, stream));
@@ -1231,7 +1233,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                         rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
-    launches += 5 + (r.n_keep > n_active ? 1 : 0);  // p2g x2, grid update, g2p x2, tail copy if any
+    launches += 1 + (r.n_keep > n_active ? 1 : 0);  // grid update, tail copy if any (dual() counts p2g, g2p)
     if (nbody > 0) {
         // slabs: every rank contributes its members' positions (disjoint support,
         // exact sum) so all ranks fit identical rigid transforms
@@ -1579,7 +1581,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
-    launches += 5 + (r.n_stored > r.n_active ? 1 : 0);  // g2p adjoint x2, grid adjoint, p2g adjoint x2, tail bars
+    launches += 1 + (r.n_stored > r.n_active ? 1 : 0);  // grid adjoint, tail bars (dual() counts the rest)
     check_launch();
     if (!r.emit.empty()) {
         double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;

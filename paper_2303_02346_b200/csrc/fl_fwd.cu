@@ -378,7 +378,11 @@ __global__ void __launch_bounds__(128, MINB) k_g2p(Geom g, PBuf in, PBuf out, co
                                              RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {
     pdl_wait();
     __shared__ float4 vt[kTile];
+    __shared__ __align__(128) float4 raw[FL_TMA_TILE ? kTileRaw : 1];
+    __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
+    TileStage ts;
+    ts.init(&bar, raw, tid);
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     __shared__ int sh_next;
     for (;;) {
@@ -387,17 +391,31 @@ __global__ void __launch_bounds__(128, MINB) k_g2p(Geom g, PBuf in, PBuf out, co
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
-        // the first permutation load overlaps the tile barrier; later ones run one
-        // particle ahead (the perm -> state loads are the kernel's latency chain)
-        uint32_t s_nx = r.start + tid < r.end ? perm[r.start + tid] : 0u;
+        ts.begin(g, gridv, bx, by, bz, tid);
+        // the perm -> state loads are the kernel's latency chain: the first particle's
+        // position/class loads overlap the tile copy, and later ones run one particle
+        // ahead (the permutation two ahead)
+        const int j0 = r.start + tid;
+        uint32_t s_nx = j0 < r.end ? perm[j0] : 0u;
+        V3<float> x_nx = {0.f, 0.f, 0.f};
+        uint32_t meta_nx = 0u;
+        if (j0 < r.end) {
+            x_nx = V3<float>{in.x(0)[s_nx], in.x(1)[s_nx], in.x(2)[s_nx]};
+            meta_nx = in.meta[s_nx];
+        }
+        uint32_t s_nx2 = j0 + 128 < r.end ? perm[j0 + 128] : 0u;
+        ts.end(g, gridv, vt, bx, by, bz, tid, 128);
         __syncthreads();
-        load_tile(g, gridv, vt, bx, by, bz, tid, 128);
-        __syncthreads();
-        for (int j = r.start + tid; j < r.end; j += 128) {
+        for (int j = j0; j < r.end; j += 128) {
             const uint32_t s = s_nx;
-            if (j + 128 < r.end) s_nx = perm[j + 128];
-            const V3<float> x = {in.x(0)[s], in.x(1)[s], in.x(2)[s]};
-            const uint32_t meta = in.meta[s];
+            const V3<float> x = x_nx;
+            const uint32_t meta = meta_nx;
+            if (j + 128 < r.end) {
+                s_nx = s_nx2;
+                x_nx = V3<float>{in.x(0)[s_nx], in.x(1)[s_nx], in.x(2)[s_nx]};
+                meta_nx = in.meta[s_nx];
+                if (j + 256 < r.end) s_nx2 = perm[j + 256];
+            }
             const uint32_t pid = in.id[s];
             const ClassInfo ci = cls[meta_cls(meta)];
             StencilW sw;

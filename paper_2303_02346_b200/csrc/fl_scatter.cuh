@@ -243,7 +243,93 @@ __device__ __forceinline__ void sc_tile_store(const ScSmem& sm, float4* out, int
         out[t] = make_float4(sm.tile[t], sm.tile[kTile + t], sm.tile[2 * kTile + t], sm.tile[3 * kTile + t]);
 }
 
-// 6^3 node tile of a block-major float4 grid into shared memory
+// ---------------------------------------------------------------------------
+// TMA-staged node tiles.  The 6^3 tile of particle block (bx,by,bz) lies in the
+// 2x2x2 node blocks starting at (bx,by,bz); each node block is 64 contiguous
+// float4 (1 KB) of the block-major grid, so one elected thread moves the eight
+// of them with 1D bulk copies (cp.async.bulk, the TMA engine; SASS UBLKCP) into
+// a raw [8][64] float4 buffer and arms an mbarrier with the byte count.  The
+// other threads issue their particle loads meanwhile; after the wait every
+// thread repacks its share of the tile into the dense 6^3 layout the gather
+// loops index with immediate offsets.  Blocks past the grid edge are not
+// copied; their tile nodes read as zero.
+// ---------------------------------------------------------------------------
+constexpr int kTileRaw = 8 * 64;  // float4 per raw tile buffer
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+// valid-block mask of the tile (bit d = (dx<<2)|(dy<<1)|dz)
+__device__ __forceinline__ uint32_t tile_valid(const Geom& g, int bx, int by, int bz) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int d = 0; d < 8; d++)
+        if (bx + (d >> 2) < g.NB[0] && by + ((d >> 1) & 1) < g.NB[1] && bz + (d & 1) < g.NB[2]) m |= 1u << d;
+    return m;
+}
+
+#ifndef FL_TMA_TILE
+#define FL_TMA_TILE 1
+#endif
+#ifndef FL_TMA_LANES
+#define FL_TMA_LANES 8
+#endif
+
+// warp 0 (after a CTA barrier that ended every generic access of `raw`): lane 0 arms the
+// barrier with the byte count, then lanes 0..7 each issue one node block's bulk copy
+__device__ __forceinline__ void tile_tma_issue(const Geom& g, const float4* __restrict__ grid, float4* raw,
+                                               uint64_t* bar, int bx, int by, int bz, uint32_t valid, int lane) {
+    if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                     "r"(uint32_t(__popc(valid)) * 1024u)
+                     : "memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int d0 = 0; d0 < 8; d0 += FL_TMA_LANES) {
+        const int d = d0 + lane;
+        if (lane < FL_TMA_LANES && (valid >> d & 1u)) {
+            const float4* src = grid + size_t(block_lin(g, bx + (d >> 2), by + ((d >> 1) & 1), bz + (d & 1))) * 64;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 1024, [%2];" ::"r"(
+                    smem_u32(raw + d * 64)),
+                "l"(src), "r"(smem_u32(bar))
+                : "memory");
+        }
+    }
+}
+
+// every thread: wait for the bytes, then repack raw -> dense 6^3 tile (caller syncs after)
+__device__ __forceinline__ void tile_tma_finish(const float4* raw, float4* tile, uint64_t* bar, uint32_t& phase,
+                                                uint32_t valid, int tid, int nthreads) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    for (int t = tid; t < int(kTile); t += nthreads) {
+        const int X = t / 36, Y = (t / 6) % 6, Z = t % 6;
+        const int d = ((X >> 2) << 2) | ((Y >> 2) << 1) | (Z >> 2);
+        tile[t] = (valid >> d & 1u) ? raw[d * 64 + (((X & 3) << 4) | ((Y & 3) << 2) | (Z & 3))]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// 6^3 node tile of a block-major float4 grid into shared memory (plain loads; the
+// FL_TMA_TILE = 0 variant, kept for A/B runs)
 __device__ __forceinline__ void load_tile(const Geom& g, const float4* __restrict__ grid, float4* tile, int bx,
                                           int by, int bz, int tid, int nthreads) {
     for (int t = tid; t < int(kTile); t += nthreads) {
@@ -254,6 +340,36 @@ __device__ __forceinline__ void load_tile(const Geom& g, const float4* __restric
         tile[t] = v;
     }
 }
+
+// Tile staging used by the gather kernels: tile_begin right after the work claim (its
+// barriers ended the previous block's reads of `raw` and `tile`), tile_end before the
+// first read of `tile` (followed by a CTA barrier).
+struct TileStage {
+    uint64_t* bar;
+    float4* raw;
+    uint32_t phase;
+    uint32_t valid;
+    __device__ __forceinline__ void init(uint64_t* b, float4* r, int tid) {
+        bar = b;
+        raw = r;
+        phase = 0;
+        if (FL_TMA_TILE && tid == 0) mbar_init(bar);
+    }
+    __device__ __forceinline__ void begin(const Geom& g, const float4* __restrict__ grid, int bx, int by, int bz,
+                                          int tid) {
+        if (FL_TMA_TILE) {
+            valid = tile_valid(g, bx, by, bz);
+            if (tid < 32) tile_tma_issue(g, grid, raw, bar, bx, by, bz, valid, tid);
+        }
+    }
+    __device__ __forceinline__ void end(const Geom& g, const float4* __restrict__ grid, float4* tile, int bx, int by,
+                                        int bz, int tid, int nthreads) {
+        if (FL_TMA_TILE)
+            tile_tma_finish(raw, tile, bar, phase, valid, tid, nthreads);
+        else
+            load_tile(g, grid, tile, bx, by, bz, tid, nthreads);
+    }
+};
 
 struct StencilW {
     int l[3];        // base cell relative to the block origin, in [0,4)
