@@ -223,6 +223,11 @@ int flume_last_error(const flume_ctx* ctx, flume_error_info* info);
    (default), 1 = snapshots spilled to pinned host memory on a copy stream that overlaps the
    forward, brought back when the backward replays their segment.  Results are identical. */
 int flume_set_checkpoint_spill(flume_ctx* ctx, int mode);
+/* trajectory_chamfer nearest-neighbour search (losses.hpp:15-64): 0 = automatic (brute-force
+   scan for small member x goal sets, a uniform-grid index above 2^24 pairs), 1 = always the
+   scan, 2 = always the grid index.  Both return the reference's first-index minimum, so the
+   loss and gradient bits do not depend on the mode. */
+int flume_set_chamfer_mode(flume_ctx* ctx, int mode);
 int flume_get_stream(flume_ctx* ctx, void** cuda_stream);
 int flume_sync(flume_ctx* ctx);
 int flume_last_timing(const flume_ctx* ctx, flume_timing* out);

@@ -512,6 +512,15 @@ class GpuWorkspace:
         """grad_trajectory snapshots in pinned host memory instead of HBM (long horizons)."""
         self._collective(lambda r, c: self.lib.flume_set_checkpoint_spill(c, int(bool(host))))
 
+    CHAMFER_MODES = {"auto": 0, "scan": 1, "grid": 2}
+
+    def set_chamfer_mode(self, mode: str = "auto"):
+        """trajectory_chamfer nearest-neighbour search: "auto", "scan" (brute force) or "grid"
+        (uniform-grid index); identical results (the reference's first-index minimum)."""
+        if mode not in self.CHAMFER_MODES:
+            raise ValueError(f"chamfer mode must be one of {sorted(self.CHAMFER_MODES)}")
+        self._collective(lambda r, c: self.lib.flume_set_chamfer_mode(c, self.CHAMFER_MODES[mode]))
+
     def slab_info(self):
         """[(rank, sx0, sx1, n_active)] -- the x-columns of 4 cells each rank owns."""
         out = []

@@ -311,6 +311,7 @@ struct Ctx {
     // checkpoint spill: snapshots of grad_trajectory in pinned host memory (D2H on a
     // copy stream overlapping the forward; H2D when the backward replays a segment)
     int spill = 0;
+    int chamfer_mode = 0;  // flume_set_chamfer_mode
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_snap = nullptr;
     std::vector<HostPtr> host_pool;
@@ -1472,7 +1473,7 @@ void Ctx::point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, 
     for (int k = 0; k < ls.n; k++) {
         if (!((mask >> k) & 1u) || ls.t[k].kind < LK_SPREAD) continue;
         launch_point_loss(pls, st.p, st.n, d_cls.p, ls, ls.t[k], seg, geom.key_inactive, out_dev, bars, d_err.p,
-                          stream);
+                          chamfer_mode, stream);
         launches += 5;
     }
     // attraction: every segment boundary, independent of the terms' eval mode (losses.hpp:332-345)
@@ -2113,6 +2114,11 @@ int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact) {
 int flume_set_checkpoint_spill(flume_ctx* ctx, int mode) {
     if (!ctx || mode < 0 || mode > 1) return FLUME_E_ARG;
     return guard(ctx, [&] { ctx->c.spill = mode; });
+}
+
+int flume_set_chamfer_mode(flume_ctx* ctx, int mode) {
+    if (!ctx || mode < 0 || mode > 2) return FLUME_E_ARG;
+    return guard(ctx, [&] { ctx->c.chamfer_mode = mode; });
 }
 
 int flume_last_error(const flume_ctx* ctx, flume_error_info* info) {

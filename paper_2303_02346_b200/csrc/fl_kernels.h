@@ -127,6 +127,9 @@ constexpr int kLossBlocks = 296;
 
 // point-set losses (fl_loss.cu): scratch for the body compaction and the NN passes
 constexpr int kChamferChunks = 512;
+// trajectory_chamfer: member x goal pairs above which the nearest-neighbour passes use the
+// grid index instead of the brute-force scan (flume_set_chamfer_mode overrides)
+constexpr double kChamferBrutePairs = double(1 << 24);
 struct PointLossScratch {
     int *flags = nullptr, *pos = nullptr, *idx = nullptr, *arg = nullptr, *carg = nullptr, *garg = nullptr,
         *count = nullptr;
@@ -142,6 +145,14 @@ struct PointLossScratch {
     void* asort_tmp = nullptr;
     size_t asort_bytes = 0;
     int cap_a = 0;
+    // trajectory_chamfer at scale: uniform-grid nearest-neighbour index (fl_loss.cu nn_build)
+    unsigned long long *nn_keys = nullptr, *nn_keys_sorted = nullptr;
+    double *nn_spts = nullptr, *nn_gpart = nullptr, *nn_part = nullptr, *nn_idx = nullptr;
+    int *nn_sidx = nullptr, *nn_cstart = nullptr, *nn_cend = nullptr;
+    void* nn_sort_tmp = nullptr;
+    size_t nn_sort_bytes = 0;
+    int nn_cap = 0;
+    void reserve_nn(int n);
     void reserve(int n_particles, int max_goals);
     void reserve_attraction(int n_members);
     ~PointLossScratch();
@@ -155,7 +166,7 @@ void launch_per_particle(const PBuf& st, int n, const ClassInfo* cls, const Loss
 // eval (bars == nullptr): adds weight * value into *out; grad: adds d/dx into bars
 void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
                        const LossTermDev& t, int seg, uint32_t key_inactive, double* out, BarBuf* bars,
-                       unsigned long long* err, cudaStream_t s);
+                       unsigned long long* err, int mode, cudaStream_t s);
 #ifndef FL_EFF_BLOCKS
 #define FL_EFF_BLOCKS 3552
 #endif

@@ -1,8 +1,10 @@
 // fl_loss.cu -- point-set losses at segment boundaries on the device
 // (losses.hpp:15-100, 474-551):
 //   trajectory_chamfer   symmetric mean nearest-neighbour distance between the
-//                        body's active particles A and the segment's goal set G,
-//                        O(|A| |G|) brute force in fp64 (no hashing: exact argmins)
+//                        body's active particles A and the segment's goal set G in
+//                        fp64 with exact first-index argmins: a brute-force scan for
+//                        small |A| |G|, uniform-grid indexes (shell search) above
+//                        2^24 pairs -- both paths give identical bits
 //   mixing_spread        -sum_ij |x_i - x_j| over the body, O(|A|^2) in fp64
 //   attraction           the optimizer's gradient-sharing surrogate (losses.hpp:104-218):
 //                        hashed-grid neighbour sums over every member of one body
@@ -12,6 +14,8 @@
 // with the reference's per-particle accumulation order (A-term, then G-terms
 // in goal order).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -49,6 +53,11 @@ __global__ void k_body_gather(PBuf st, int n, const int* __restrict__ flags, con
 // ---------------------------------------------------------------------------
 // trajectory_chamfer
 // ---------------------------------------------------------------------------
+// squared distance with a fixed rounding sequence (both nearest-neighbour paths use it)
+__device__ __forceinline__ double nn_d2(double ex, double ey, double ez) {
+    return __fma_rn(ez, ez, __fma_rn(ey, ey, __dmul_rn(ex, ex)));
+}
+
 // A -> G: nearest goal of every member (first index on ties, like the reference's strict <)
 __global__ void __launch_bounds__(kLT) k_chamfer_a(const double* __restrict__ px, const int* __restrict__ count,
                                                    const double* __restrict__ g, int ng, double* best, int* arg,
@@ -70,8 +79,7 @@ __global__ void __launch_bounds__(kLT) k_chamfer_a(const double* __restrict__ px
         __syncthreads();
         if (in)
             for (int j = 0; j < m; j++) {
-                const double dx = p[0] - gs[3 * j], dy = p[1] - gs[3 * j + 1], dz = p[2] - gs[3 * j + 2];
-                const double d2 = dx * dx + dy * dy + dz * dz;
+                const double d2 = nn_d2(p[0] - gs[3 * j], p[1] - gs[3 * j + 1], p[2] - gs[3 * j + 2]);
                 if (d2 < bd) {
                     bd = d2;
                     bi = t0 + j;
@@ -113,8 +121,7 @@ __global__ void __launch_bounds__(kLT) k_chamfer_g(const double* __restrict__ px
             __syncthreads();
             if (gq < ng)
                 for (int j = 0; j < m; j++) {
-                    const double dx = q[0] - ps[3 * j], dy = q[1] - ps[3 * j + 1], dz = q[2] - ps[3 * j + 2];
-                    const double d2 = dx * dx + dy * dy + dz * dz;
+                    const double d2 = nn_d2(q[0] - ps[3 * j], q[1] - ps[3 * j + 1], q[2] - ps[3 * j + 2]);
                     if (d2 < bd) {
                         bd = d2;
                         bi = t0 + j;
@@ -143,6 +150,10 @@ __global__ void __launch_bounds__(kLT) k_chamfer_final(const int* __restrict__ c
     }
     double sg = 0.0;
     for (int gq = threadIdx.x; gq < ng; gq += kLT) {
+        if (nchunks == 0) {  // grid path: gbest / garg are final already
+            sg += gbest[gq];
+            continue;
+        }
         double bd = 1e300;
         int bi = 0;
         for (int c = 0; c < nchunks; c++) {
@@ -205,6 +216,173 @@ __global__ void k_chamfer_grad_g(const double* __restrict__ px, const int* __res
         const int k = garg[q], i = idx[k];
         for (int a = 0; a < 3; a++) bars.x(a)[i] += float((px[3 * size_t(k) + a] - g[3 * size_t(q) + a]) * s);
     }
+}
+
+// ---------------------------------------------------------------------------
+// trajectory_chamfer at scale: exact nearest neighbours through a uniform grid
+// ---------------------------------------------------------------------------
+// For |A| |G| beyond kChamferBrutePairs the two nearest-neighbour passes query a
+// uniform-grid index of the target set instead of scanning it: cells of size h over
+// the target bounding box (~1 target per cell, <= 128 per axis), targets sorted by
+// (cell, index).  A query visits Chebyshev shells r = 0, 1, ... around its (clamped)
+// cell; every target in shells > r is at least r h away, so after shell r the search
+// stops once the best squared distance is < (r h)^2.  Candidates are compared on
+// (d^2, index): the result is the first-index minimum, exactly what the brute-force
+// scan returns (losses.hpp:20-23, 38-45), so both paths give identical bits.
+constexpr int kNnMaxDim = 128;
+
+// bounding box partials: [block][lo0 lo1 lo2 hi0 hi1 hi2]
+__global__ void __launch_bounds__(kLT) k_nn_bbox(const double* __restrict__ pts, int n_static,
+                                                 const int* __restrict__ n_dev, double* partial) {
+    __shared__ double red[6][kLT];
+    const int n = n_dev ? *n_dev : n_static;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int i = blockIdx.x * kLT + threadIdx.x; i < n; i += gridDim.x * kLT)
+        for (int a = 0; a < 3; a++) {
+            const double v = pts[3 * size_t(i) + a];
+            lo[a] = fmin(lo[a], v);
+            hi[a] = fmax(hi[a], v);
+        }
+    for (int a = 0; a < 3; a++) {
+        red[a][threadIdx.x] = lo[a];
+        red[3 + a][threadIdx.x] = hi[a];
+    }
+    __syncthreads();
+    for (int w = kLT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int a = 0; a < 3; a++) {
+                red[a][threadIdx.x] = fmin(red[a][threadIdx.x], red[a][threadIdx.x + w]);
+                red[3 + a][threadIdx.x] = fmax(red[3 + a][threadIdx.x], red[3 + a][threadIdx.x + w]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) partial[6 * blockIdx.x + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// one thread: the grid of the index (idx[0..2] lo, idx[3] h, idx[4..6] dims as doubles)
+__global__ void k_nn_setup(const double* __restrict__ partial, int nblocks, int n_static, const int* __restrict__ n_dev,
+                           double* idx) {
+    const int n = n_dev ? *n_dev : n_static;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int b = 0; b < nblocks; b++)
+        for (int a = 0; a < 3; a++) {
+            lo[a] = fmin(lo[a], partial[6 * b + a]);
+            hi[a] = fmax(hi[a], partial[6 * b + 3 + a]);
+        }
+    double ext[3], emax = 0.0;
+    for (int a = 0; a < 3; a++) {
+        ext[a] = n > 0 ? hi[a] - lo[a] : 0.0;
+        emax = fmax(emax, ext[a]);
+    }
+    // ~1 target per cell over the box (flat axes count as one cell), <= kNnMaxDim per axis
+    double vol = 1.0;
+    int nflat = 0;
+    for (int a = 0; a < 3; a++) {
+        if (ext[a] > 1e-12 * (emax + 1e-300)) vol *= ext[a];
+        else nflat++;
+    }
+    double h = emax > 0.0 ? (nflat == 3 ? emax : pow(vol / double(max(n, 1)), 1.0 / double(3 - nflat))) : 1.0;
+    h = fmax(h, emax / double(kNnMaxDim - 1));
+    if (!(h > 0.0)) h = 1.0;
+    for (int a = 0; a < 3; a++) {
+        idx[a] = n > 0 ? lo[a] : 0.0;
+        idx[4 + a] = double(min(kNnMaxDim, int(floor(ext[a] / h)) + 1));
+    }
+    idx[3] = h;
+}
+
+__device__ __forceinline__ int nn_cell_axis(const double* idx, int a, double x) {
+    const int d = int(idx[4 + a]);
+    const double f = floor((x - idx[a]) / idx[3]);
+    return f < 0.0 ? 0 : (f >= double(d) ? d - 1 : int(f));
+}
+
+__global__ void k_nn_keys(const double* __restrict__ pts, int n_static, const int* __restrict__ n_dev,
+                          const double* __restrict__ idx, unsigned long long* keys, int n_cap) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = n_dev ? *n_dev : n_static;
+    if (i >= n_cap) return;
+    if (i >= n) {  // past the live count: sorts last
+        keys[i] = ~0ull;
+        return;
+    }
+    const int d1 = int(idx[5]), d2 = int(idx[6]);
+    const int c = (nn_cell_axis(idx, 0, pts[3 * size_t(i)]) * d1 + nn_cell_axis(idx, 1, pts[3 * size_t(i) + 1])) * d2 +
+                  nn_cell_axis(idx, 2, pts[3 * size_t(i) + 2]);
+    keys[i] = (static_cast<unsigned long long>(c) << 32) | static_cast<unsigned long long>(i);
+}
+
+// sorted targets (cell, index): contiguous coordinates + original index, and per-cell [start, end)
+__global__ void k_nn_cells(const unsigned long long* __restrict__ sorted, int n_static, const int* __restrict__ n_dev,
+                           const double* __restrict__ pts, double* spts, int* sidx, int* cstart, int* cend) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = n_dev ? *n_dev : n_static;
+    if (s >= n) return;
+    const unsigned long long k = sorted[s];
+    const int c = int(k >> 32), i = int(k & 0xffffffffull);
+    sidx[s] = i;
+    for (int a = 0; a < 3; a++) spts[3 * size_t(s) + a] = pts[3 * size_t(i) + a];
+    if (s == 0 || int(sorted[s - 1] >> 32) != c) cstart[c] = s;
+    if (s == n - 1 || int(sorted[s + 1] >> 32) != c) cend[c] = s + 1;
+}
+
+// nearest target of each query (first index on ties), its distance, and CTA partial sums
+__global__ void __launch_bounds__(kLT) k_nn_query(const double* __restrict__ q, int nq_static,
+                                                  const int* __restrict__ nq_dev, const double* __restrict__ idx,
+                                                  const double* __restrict__ spts, const int* __restrict__ sidx,
+                                                  const int* __restrict__ cstart, const int* __restrict__ cend,
+                                                  double* best, int* arg, double* partial) {
+    __shared__ double red[kLT];
+    const int nq = nq_dev ? *nq_dev : nq_static;
+    const int k = blockIdx.x * kLT + threadIdx.x;
+    double d = 0.0;
+    if (k < nq) {
+        const double p0 = q[3 * size_t(k)], p1 = q[3 * size_t(k) + 1], p2 = q[3 * size_t(k) + 2];
+        const int D0 = int(idx[4]), D1 = int(idx[5]), D2 = int(idx[6]);
+        const double h = idx[3];
+        const int c0 = nn_cell_axis(idx, 0, p0), c1 = nn_cell_axis(idx, 1, p1), c2 = nn_cell_axis(idx, 2, p2);
+        const int rmax = max(max(D0, D1), D2);
+        double bd = 1e300;
+        int bi = 0x7fffffff;
+        for (int r = 0; r <= rmax; r++) {
+            for (int dz = -r; dz <= r; dz++) {
+                const int z = c2 + dz;
+                if (z < 0 || z >= D2) continue;
+                for (int dy = -r; dy <= r; dy++) {
+                    const int y = c1 + dy;
+                    if (y < 0 || y >= D1) continue;
+                    const bool face = dz == -r || dz == r || dy == -r || dy == r;
+                    for (int dx = -r; dx <= r; dx += (face || r == 0) ? 1 : 2 * r) {
+                        const int x = c0 + dx;
+                        if (x < 0 || x >= D0) continue;
+                        const int c = (x * D1 + y) * D2 + z;
+                        const int e = cend[c];
+                        for (int t = cstart[c]; t < e; t++) {
+                            const double d2 = nn_d2(p0 - spts[3 * size_t(t)], p1 - spts[3 * size_t(t) + 1],
+                                                    p2 - spts[3 * size_t(t) + 2]);
+                            const int ti = sidx[t];
+                            if (d2 < bd || (d2 == bd && ti < bi)) {
+                                bd = d2;
+                                bi = ti;
+                            }
+                        }
+                    }
+                }
+            }
+            const double rh = double(r) * h;
+            if (bd < rh * rh) break;
+        }
+        d = sqrt(bd);
+        best[k] = d;
+        arg[k] = bi == 0x7fffffff ? 0 : bi;  // (no target at all: the final sum raises the empty-set error)
+    }
+    red[threadIdx.x] = d;
+    __syncthreads();
+    for (int w = kLT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -525,7 +703,8 @@ PointLossScratch::~PointLossScratch() {
     for (auto p : {(void*)flags, (void*)pos, (void*)idx, (void*)px, (void*)best, (void*)arg, (void*)partial,
                    (void*)cbest, (void*)carg, (void*)gbest, (void*)garg, (void*)count, (void*)scal, cub_tmp,
                    (void*)apx, (void*)ae, (void*)awsum, (void*)asi, (void*)aslot, (void*)akey, (void*)akey_sorted,
-                   (void*)apart, asort_tmp})
+                   (void*)apart, asort_tmp, (void*)nn_keys, (void*)nn_keys_sorted, (void*)nn_spts, (void*)nn_sidx,
+                   nn_sort_tmp, (void*)nn_gpart, (void*)nn_cstart, (void*)nn_cend, (void*)nn_part, (void*)nn_idx})
         cudaFree(p);
 }
 
@@ -566,9 +745,51 @@ static void compact_body(PointLossScratch& w, const PBuf& st, int n, const Class
 // number of member chunks for the G -> A stage (<= kChamferChunks)
 static int chamfer_chunk(int n) { return (n + kChamferChunks - 1) / kChamferChunks; }
 
+constexpr int kNnBboxBlocks = 592;
+
+void PointLossScratch::reserve_nn(int n) {
+    if (n <= nn_cap) return;
+    for (auto p : {(void*)nn_keys, (void*)nn_keys_sorted, (void*)nn_spts, (void*)nn_sidx, nn_sort_tmp,
+                   (void*)nn_gpart})
+        cudaFree(p);
+    cudaMalloc(&nn_keys, sizeof(unsigned long long) * size_t(n));
+    cudaMalloc(&nn_keys_sorted, sizeof(unsigned long long) * size_t(n));
+    cudaMalloc(&nn_spts, sizeof(double) * 3 * size_t(n));
+    cudaMalloc(&nn_sidx, sizeof(int) * size_t(n));
+    cudaMalloc(&nn_gpart, sizeof(double) * (size_t(n) / kLT + 2));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, nn_keys, nn_keys_sorted, n, 0, 53);
+    cudaMalloc(&nn_sort_tmp, tb);
+    nn_sort_bytes = tb;
+    if (!nn_cstart) {
+        const size_t cells = size_t(kNnMaxDim) * kNnMaxDim * kNnMaxDim;
+        cudaMalloc(&nn_cstart, sizeof(int) * cells);
+        cudaMalloc(&nn_cend, sizeof(int) * cells);
+        cudaMalloc(&nn_part, sizeof(double) * 6 * kNnBboxBlocks);
+        cudaMalloc(&nn_idx, sizeof(double) * 8);
+    }
+    nn_cap = n;
+}
+
+// uniform-grid index of pts[0 .. n) (n = *n_dev when given, else n_static; n <= n_cap)
+static void nn_build(PointLossScratch& w, const double* pts, int n_static, const int* n_dev, int n_cap,
+                     cudaStream_t s) {
+    w.reserve_nn(n_cap);
+    const int nb = std::max(1, std::min(kNnBboxBlocks, (n_cap + kLT - 1) / kLT));
+    k_nn_bbox<<<nb, kLT, 0, s>>>(pts, n_static, n_dev, w.nn_part);
+    k_nn_setup<<<1, 1, 0, s>>>(w.nn_part, nb, n_static, n_dev, w.nn_idx);
+    k_nn_keys<<<(n_cap + 255) / 256, 256, 0, s>>>(pts, n_static, n_dev, w.nn_idx, w.nn_keys, n_cap);
+    cub::DeviceRadixSort::SortKeys(w.nn_sort_tmp, w.nn_sort_bytes, w.nn_keys, w.nn_keys_sorted, n_cap, 0, 53, s);
+    const size_t cells = size_t(kNnMaxDim) * kNnMaxDim * kNnMaxDim;
+    cudaMemsetAsync(w.nn_cstart, 0, sizeof(int) * cells, s);
+    cudaMemsetAsync(w.nn_cend, 0, sizeof(int) * cells, s);
+    k_nn_cells<<<(n_cap + 255) / 256, 256, 0, s>>>(w.nn_keys_sorted, n_static, n_dev, pts, w.nn_spts, w.nn_sidx,
+                                                   w.nn_cstart, w.nn_cend);
+}
+
 void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls,
                        const LossTermDev& t, int seg, uint32_t key_inactive, double* out, BarBuf* bars,
-                       unsigned long long* err, cudaStream_t s) {
+                       unsigned long long* err, int mode, cudaStream_t s) {
     if (n <= 0) return;
     compact_body(w, st, n, cls, t.body, key_inactive, ls, s);
     const int grid_a = (n + kLT - 1) / kLT;  // upper bound on the member count
@@ -585,12 +806,24 @@ void launch_point_loss(PointLossScratch& w, const PBuf& st, int n, const ClassIn
     const int step = seg < t.nsteps ? seg : t.nsteps - 1;
     const int g0 = t.goff_h[step], ng = t.goff_h[step + 1] - g0;
     const double* g = t.gpts + 3 * size_t(g0);
-    const int chunk = chamfer_chunk(n);
-    const int nchunks = (n + chunk - 1) / chunk;
-    k_chamfer_a<<<grid_a, kLT, 0, s>>>(w.px, w.count, g, ng, w.best, w.arg, w.partial);
-    k_chamfer_g<<<nchunks, kLT, 0, s>>>(w.px, w.count, chunk, g, ng, w.cbest, w.carg);
-    k_chamfer_final<<<1, kLT, 0, s>>>(w.count, nchunks, ng, w.cbest, w.carg, w.partial, grid_a, t.weight, w.gbest,
-                                      w.garg, bars ? w.scal + 1 : out, w.scal, err);
+    const bool grid = mode == 2 || (mode == 0 && double(n) * double(ng) > kChamferBrutePairs);
+    if (grid) {  // exact nearest neighbours through uniform-grid indexes (A -> G, then G -> A)
+        nn_build(w, g, ng, nullptr, ng, s);
+        k_nn_query<<<grid_a, kLT, 0, s>>>(w.px, 0, w.count, w.nn_idx, w.nn_spts, w.nn_sidx, w.nn_cstart, w.nn_cend,
+                                          w.best, w.arg, w.partial);
+        nn_build(w, w.px, 0, w.count, n, s);
+        k_nn_query<<<(ng + kLT - 1) / kLT, kLT, 0, s>>>(g, ng, nullptr, w.nn_idx, w.nn_spts, w.nn_sidx, w.nn_cstart,
+                                                         w.nn_cend, w.gbest, w.garg, w.nn_gpart);
+        k_chamfer_final<<<1, kLT, 0, s>>>(w.count, 0, ng, nullptr, nullptr, w.partial, grid_a, t.weight, w.gbest,
+                                          w.garg, bars ? w.scal + 1 : out, w.scal, err);
+    } else {
+        const int chunk = chamfer_chunk(n);
+        const int nchunks = (n + chunk - 1) / chunk;
+        k_chamfer_a<<<grid_a, kLT, 0, s>>>(w.px, w.count, g, ng, w.best, w.arg, w.partial);
+        k_chamfer_g<<<nchunks, kLT, 0, s>>>(w.px, w.count, chunk, g, ng, w.cbest, w.carg);
+        k_chamfer_final<<<1, kLT, 0, s>>>(w.count, nchunks, ng, w.cbest, w.carg, w.partial, grid_a, t.weight,
+                                          w.gbest, w.garg, bars ? w.scal + 1 : out, w.scal, err);
+    }
     if (bars) {
         k_chamfer_grad_a<<<grid_a, kLT, 0, s>>>(w.px, w.idx, w.count, g, w.best, w.arg, t.weight, *bars);
         k_chamfer_grad_g<<<1, 32, 0, s>>>(w.px, w.idx, g, ng, w.gbest, w.garg, t.weight, *bars);

@@ -20,9 +20,10 @@ def _goal_sets(rng, n_steps, m):
             for _ in range(n_steps)]
 
 
-def _run(spec, nseg, seglen):
+def _run(spec, nseg, seglen, chamfer="auto"):
     w, r = pair(spec)
     ws = fl.GpuWorkspace(w.scene)
+    ws.set_chamfer_mode(chamfer)
     vals = np.tile(w.init_action, (nseg, 1))
     acts = fl.ActionTrajectory(nseg, seglen, vals)
     loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
@@ -34,12 +35,14 @@ def _run(spec, nseg, seglen):
     return l, per, rl, rper, tg, rg
 
 
+@pytest.mark.parametrize("mode", ["auto", "grid"])
 @pytest.mark.parametrize("m", [1, 37, 700])
-def test_trajectory_chamfer_parity(ref_available, m):
+def test_trajectory_chamfer_parity(ref_available, m, mode):
+    """mode "grid" forces the uniform-grid nearest-neighbour index (used above 2^24 pairs)."""
     rng = np.random.default_rng(m)
     spec = spec_for("c1", 16)
     spec["loss"] = {"kind": "trajectory_chamfer", "body": "column", "goal_trajectory": _goal_sets(rng, 2, m)}
-    l, per, rl, rper, tg, rg = _run(spec, 3, 4)  # 3 segments, 2 goal sets: the last is reused
+    l, per, rl, rper, tg, rg = _run(spec, 3, 4, chamfer=mode)  # 3 segments, 2 goal sets: the last is reused
     np.testing.assert_allclose(per, rper, rtol=1e-6)
     assert abs(l - rl) <= 1e-6 * abs(rl)
     assert abs(tg.loss - rg["loss"]) <= 1e-6 * abs(rg["loss"])
@@ -64,6 +67,59 @@ def test_composite_point_and_target(ref_available):
     l, per, rl, rper, tg, rg = _run(spec, 2, 5)
     np.testing.assert_allclose(per, rper, rtol=1e-6)
     assert grad_rel_error(tg.action_grad, rg["grad"]) <= 1e-3
+
+
+def _chamfer_run(spec, mode, nseg=2, seglen=3):
+    w = fl.build_scene(spec)
+    ws = fl.GpuWorkspace(w.scene)
+    ws.set_chamfer_mode(mode)
+    acts = fl.ActionTrajectory(nseg, seglen, np.tile(w.init_action, (nseg, 1)))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    per = []
+    l = fl.rollout_loss(w.scene, w.state, acts, loss, per_segment=per, ws=ws)
+    g = fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
+    ws.close()
+    return l, np.asarray(per), g.loss, np.asarray(g.action_grad).copy()
+
+
+@pytest.mark.parametrize("body,m", [("column", 3000), ("column", 20)])
+def test_chamfer_grid_index_equals_scan(body, m):
+    """Both nearest-neighbour paths return the first-index minimum with the same rounding,
+    so the loss, per-segment losses and action gradient are bit-identical (full c1:
+    102,400 column particles against m goals, goals clustered and spread)."""
+    rng = np.random.default_rng(11)
+    spec = spec_for("c1")
+    spec["loss"] = {"kind": "trajectory_chamfer", "body": body, "goal_trajectory": _goal_sets(rng, 2, m)}
+    a = _chamfer_run(spec, "scan")
+    b = _chamfer_run(spec, "grid")
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    assert a[2] == b[2] and np.array_equal(a[3], b[3])
+
+
+def test_chamfer_grid_full_scale():
+    """trajectory_chamfer on c4's 1M-particle pool against a 300k-point goal set (3e11 pairs:
+    grid index only), checked against exact nearest neighbours from a k-d tree on the host
+    (scipy cKDTree over the device's own state after the substep)."""
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(12)
+    spec = spec_for("c4")
+    goals = (np.array([0.5, 0.08, 0.5]) + np.array([0.3, 0.05, 0.3]) * rng.uniform(-1, 1, (300_000, 3)))
+    spec["loss"] = {"kind": "trajectory_chamfer", "body": "pool", "goal_trajectory": [goals.tolist()]}
+    w = fl.build_scene(spec)
+    ws = fl.GpuWorkspace(w.scene)
+    acts = fl.ActionTrajectory(1, 1, w.init_action.reshape(1, 6))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    l = fl.rollout_loss(w.scene, w.state, acts, loss, ws=ws)
+    st = w.state.copy()
+    fl.mpm_substep(w.scene, st, w.init_action, ws, count=1)
+    ws.close()
+    body_id = int(w.loss_spec[0]["body"])
+    pts = st.x[w.scene.body_id == body_id]
+    g = np.asarray(goals, dtype=np.float64)
+    da, _ = cKDTree(g).query(pts)
+    dg, _ = cKDTree(pts).query(g)
+    want = float(np.mean(da) + np.mean(dg))
+    assert abs(l - want) <= 1e-10 * want, (l, want)
 
 
 def test_chamfer_rerun_bit_identical():
