@@ -53,7 +53,8 @@ SCALE_HORIZON = 20
 # algorithmic bytes per launch unit: fp32 state, each
 # field counted once per kernel that must move it; N = active particles, A =
 # touched nodes (64 per node block)
-KERNELS = ["p2g", "grid_update", "g2p", "sort", "g2p_adjoint", "grid_adjoint", "p2g_adjoint", "rigid", "other"]
+KERNELS = ["p2g", "grid_update", "g2p", "sort", "g2p_adjoint", "grid_adjoint", "p2g_adjoint", "rigid", "other",
+           "slab_comm"]
 ALG_BYTES = {
     "p2g": (100, 16),           # read x v F C class | write m,p per node
     "grid_update": (0, 44),     # read m,p (16) write v,m (16) + v0,m (16) - forward writes only v: use 44 avg
@@ -427,9 +428,9 @@ def run_ours(args):
     check(lib.flume_profile(ctx, 1))
     for _ in range(args.steps):
         step()
-    kms = (C.c_double * 9)()
-    kcnt = (C.c_long * 9)()
-    check(lib.flume_kernel_times(ctx, kms, kcnt, 9))
+    kms = (C.c_double * len(KERNELS))()
+    kcnt = (C.c_long * len(KERNELS))()
+    check(lib.flume_kernel_times(ctx, kms, kcnt, len(KERNELS)))
     check(lib.flume_profile(ctx, 0))
     value = n * T * args.steps / (total_ms / 1e3)
 

@@ -248,6 +248,12 @@ int flume_dist_unique_id(unsigned char uid[128]);
 int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, int n_ranks,
                           const unsigned char uid[128], flume_ctx** out);
 int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int* sx1, long* n_active);
+/* Migrating particles travel in fixed-size messages of `capacity` slots per neighbour
+ * and substep (counts stay on the device: no host round trip per substep).  A call
+ * whose migration exceeds it is re-run from its start with 4x the capacity (same
+ * result); `retries` counts those re-runs.  Collective: every rank sets the same value. */
+int flume_slab_set_migration_capacity(flume_ctx* ctx, int capacity);
+int flume_slab_migration_stats(const flume_ctx* ctx, int* capacity, long* retries);
 /* the column split every rank computes at upload: weights = active particles per
  * 4-cell x column, cuts[n_ranks + 1] (host-only, no device needed) */
 int flume_slab_split(const double* col_weight, int n_cols, int n_ranks, int* cuts);
@@ -255,7 +261,8 @@ int flume_slab_split(const double* col_weight, int n_cols, int n_ranks, int* cut
 /* ---- instrumentation ----
  * flume_profile: time every kernel class with CUDA events on the context stream.
  * kernel classes: 0 p2g, 1 grid_update, 2 g2p, 3 sort+block lists, 4 g2p adjoint,
- * 5 grid adjoint, 6 p2g adjoint, 7 rigid (fwd+adj), 8 other */
+ * 5 grid adjoint, 6 p2g adjoint, 7 rigid (fwd+adj), 8 other, 9 slab halo / migration
+ * exchanges (pack, transport, unpack) */
 int flume_profile(flume_ctx* ctx, int enable);
 int flume_kernel_times(flume_ctx* ctx, double* ms, long* counts, int n);
 int flume_timer_mark(flume_ctx* ctx, int slot); /* slot 0..7: cudaEventRecord on the context stream */

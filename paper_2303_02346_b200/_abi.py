@@ -120,6 +120,8 @@ EXPORTS = {
     "flume_ctx_create_dist": (C.c_int, [C.POINTER(SceneDesc), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_ubyte),
                                         C.POINTER(C.c_void_p)]),
     "flume_slab_split": (C.c_int, [C.POINTER(C.c_double), C.c_int, C.c_int, C.POINTER(C.c_int)]),
+    "flume_slab_set_migration_capacity": (C.c_int, [C.c_void_p, C.c_int]),
+    "flume_slab_migration_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_long)]),
     "flume_slab_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), C.POINTER(C.c_long)]),
     "flume_set_mode": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),

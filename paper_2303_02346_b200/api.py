@@ -521,6 +521,20 @@ class GpuWorkspace:
             raise ValueError(f"chamfer mode must be one of {sorted(self.CHAMFER_MODES)}")
         self._collective(lambda r, c: self.lib.flume_set_chamfer_mode(c, self.CHAMFER_MODES[mode]))
 
+    def set_migration_capacity(self, capacity: int):
+        """Slots per neighbour and substep of the fixed-size migration messages (slab
+        workspaces); an overflowing call is re-run with 4x the capacity."""
+        self._collective(lambda r, c: self.lib.flume_slab_set_migration_capacity(c, int(capacity)))
+
+    def migration_stats(self):
+        """[(capacity, re-runs)] per rank."""
+        out = []
+        for c in self.ctxs:
+            cap, n = C.c_int(), C.c_long()
+            self.lib.flume_slab_migration_stats(c, C.byref(cap), C.byref(n))
+            out.append((cap.value, n.value))
+        return out
+
     def slab_info(self):
         """[(rank, sx0, sx1, n_active)] -- the x-columns of 4 cells each rank owns."""
         out = []

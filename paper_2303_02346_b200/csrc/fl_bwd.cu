@@ -22,10 +22,10 @@ namespace fl {
 // ---------------------------------------------------------------------------
 // loss cotangent injection at segment boundaries (losses.hpp:506-525)
 // ---------------------------------------------------------------------------
-__global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, LossSet ls, uint32_t mask,
+__global__ void k_loss_grad(PBuf st, DN nn, const ClassInfo* __restrict__ cls, LossSet ls, uint32_t mask,
                             uint32_t key_inactive, BarBuf bars) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= nn.get()) return;
     const uint32_t key = st.key[i];
     if (key > key_inactive) return;  // departed slot
     if (key == key_inactive && !ls.count_parked) return;
@@ -57,10 +57,10 @@ __global__ void k_loss_grad(PBuf st, int n, const ClassInfo* __restrict__ cls, L
         for (int a = 0; a < 3; a++) bars.x(a)[i] += float(g[a]);
 }
 
-void launch_loss_grad(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, BarBuf bars,
+void launch_loss_grad(const PBuf& st, DN n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, BarBuf bars,
                       uint32_t key_inactive, cudaStream_t s) {
-    if (n <= 0) return;
-    k_loss_grad<<<(n + 255) / 256, 256, 0, s>>>(st, n, cls, ls, mask, key_inactive, bars);
+    if (n.h <= 0) return;
+    k_loss_grad<<<(n.h + 255) / 256, 256, 0, s>>>(st, n, cls, ls, mask, key_inactive, bars);
 }
 
 // ---------------------------------------------------------------------------
@@ -809,23 +809,24 @@ void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 // parked particles pass their cotangents through; departed slots (sorted
 // positions [n_keep, n_stored)) get zero -- a migrated particle's cotangent is
 // returned by its new slab before the previous substep's adjoint
-__global__ void k_tail_bars(BarBuf post, BarBuf out, const uint32_t* __restrict__ perm, int n0, int n_keep,
-                            int n_stored) {
+__global__ void k_tail_bars(BarBuf post, BarBuf out, const uint32_t* __restrict__ perm, DN n0, DN nk, DN ns) {
     pdl_wait();
-    int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_stored) return;
-    uint32_t s = perm[j];
-    if (j < n_keep)
-        for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = post.f[size_t(c) * post.cap + j];
-    else
-        for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = 0.f;
+    const int n_keep = nk.get(), n_stored = ns.get();
+    for (int j = n0.get() + blockIdx.x * blockDim.x + threadIdx.x; j < n_stored; j += gridDim.x * blockDim.x) {
+        uint32_t s = perm[j];
+        if (j < n_keep)
+            for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = post.f[size_t(c) * post.cap + j];
+        else
+            for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + s] = 0.f;
+    }
 }
 
-void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n_keep, int n_stored,
+void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, DN n_active, DN n_keep, DN n_stored,
                       cudaStream_t s) {
-    int m = n_stored - n_active;
+    // (slabs: h is an upper bound of the tail length)
+    int m = n_stored.h - (n_active.d ? 0 : n_active.h);
     if (m <= 0) return;
-    launch_k(k_tail_bars, dim3((m + 255) / 256), dim3(256), 0, s, post, out, perm, n_active, n_keep, n_stored);
+    launch_k(k_tail_bars, dim3(gs_grid(m)), dim3(256), 0, s, post, out, perm, n_active, n_keep, n_stored);
 }
 
 // emitter spawn adjoint, sequential over the substep's spawns (fixed order)
@@ -834,11 +835,14 @@ struct EmitBatch {
     EmitAdjEntry e[kEmitInline];
 };
 
-__global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, EmitBatch inl) {
+__global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, EmitBatch inl,
+                           const int* slot_base) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int q = 0; q < n_eff * 12; q++) em_out[q] = 0.0;
+    const int base = slot_base ? *slot_base : 0;  // slabs: slots relative to the parked tail
     for (int i = 0; i < n; i++) {
-        const EmitAdjEntry e = list ? list[i] : inl.e[i];
+        EmitAdjEntry e = list ? list[i] : inl.e[i];
+        e.slot += base;
         double xb[3], vb[3];
         for (int a = 0; a < 3; a++) {
             xb[a] = out.x(a)[e.slot];
@@ -856,16 +860,17 @@ __global__ void k_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* 
     }
 }
 
-void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s) {
-    k_adj_emit<<<1, 32, 0, s>>>(out, list, n, em_out, n_eff, EmitBatch{});
+void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, const int* slot_base,
+                     cudaStream_t s) {
+    k_adj_emit<<<1, 32, 0, s>>>(out, list, n, em_out, n_eff, EmitBatch{}, slot_base);
 }
 
 void launch_adj_emit_inline(BarBuf out, const EmitAdjEntry* host_list, int n, double* em_out, int n_eff,
-                            cudaStream_t s) {
+                            const int* slot_base, cudaStream_t s) {
     EmitBatch b{};
     b.n = n;
     for (int i = 0; i < n; i++) b.e[i] = host_list[i];
-    k_adj_emit<<<1, 32, 0, s>>>(out, nullptr, n, em_out, n_eff, b);
+    k_adj_emit<<<1, 32, 0, s>>>(out, nullptr, n, em_out, n_eff, b, slot_base);
 }
 
 // ---------------------------------------------------------------------------

@@ -42,10 +42,13 @@ struct StateBuf {
     void* mem = nullptr;
     PBuf p{};
     size_t bytes = 0;
-    int n = 0;  // occupied slots (active + parked + arrivals + departed holes; N on one rank)
+    int n = 0;  // occupied slots (active + parked + arrivals + departed holes; N on one rank;
+                // an upper bound on slabs, whose exact counts are `cnt` on the device)
+    int* cnt = nullptr;  // device [StateCnt]: n_active, n_stored, park_base (slab contexts)
     StateBuf(int cap, int nmem) {
         size_t pbytes = (size_t(cap) * (24 * sizeof(float) + 3 * sizeof(uint32_t)) + 255) & ~size_t(255);
-        bytes = pbytes + size_t(std::max(nmem, 1)) * 3 * sizeof(double);
+        const size_t mbytes = (size_t(std::max(nmem, 1)) * 3 * sizeof(double) + 255) & ~size_t(255);
+        bytes = pbytes + mbytes + SC_N * sizeof(int);  // the counts travel with every copy / spill
         CK(cudaMalloc(&mem, bytes));
         p.cap = cap;
         p.f = static_cast<float*>(mem);
@@ -53,6 +56,7 @@ struct StateBuf {
         p.id = p.meta + cap;
         p.key = p.id + cap;
         p.mx = reinterpret_cast<double*>(static_cast<char*>(mem) + pbytes);
+        cnt = reinterpret_cast<int*>(static_cast<char*>(mem) + pbytes + mbytes);
     }
     ~StateBuf() { cudaFree(mem); }
 };
@@ -101,15 +105,20 @@ struct Record {
     float4* gridv0 = nullptr;  // (p/m, m) before gravity/walls/contact (grid-update adjoint input)
     uint8_t* cmask = nullptr;  // per node: effectors within contact range (bit e)
     int* blockmap = nullptr;   // particle block -> list slot + 1 (0 = none), incl. slab ghost blocks
+    // host counts: exact on one rank; upper bounds on slabs, where `dcnt` (device,
+    // [RecCnt]) holds the exact ones, the migration's message counts among them
     int n_active = 0;
     int n_keep = 0;    // active + parked slots of the pre-state (= N on one rank)
     int n_stored = 0;  // all slots of the pre-state, departed holes included
+    int* dcnt = nullptr;
+    // slabs: dcnt read back into pinned memory as the forward runs (no wait); the
+    // backward sizes the cotangent return messages from it
+    int* hcnt = nullptr;
+    cudaEvent_t hcnt_ev = nullptr;
     // slab migration after this substep's G2P: slots of the departed particles
-    // (by direction, in message order) and the arrivals' base slot in the post-state
+    // (by direction, in message order)
     uint32_t* mig_src = nullptr;
     int mig_cap = 0;
-    long n_out[2] = {0, 0}, n_in[2] = {0, 0};
-    int arr_base = 0;
     long substep = 0;
     std::vector<ActEntry> act;
     std::vector<EmitAdjEntry> emit;
@@ -126,7 +135,8 @@ struct Record {
                o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 32),
                o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),
                o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4)),
-               o_mig = carve(size_t(2) * migcap * 4), o_cm = carve(size_t(nbtot) * 64), o_bm = carve(size_t(nbtot) * 4);
+               o_mig = carve(size_t(2) * migcap * 4), o_cm = carve(size_t(nbtot) * 64), o_bm = carve(size_t(nbtot) * 4),
+               o_dc = carve(RC_N * sizeof(int));
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -145,11 +155,28 @@ struct Record {
         mig_src = migcap > 0 ? reinterpret_cast<uint32_t*>(b + o_mig) : nullptr;
         cmask = reinterpret_cast<uint8_t*>(b + o_cm);
         blockmap = reinterpret_cast<int*>(b + o_bm);
+        dcnt = reinterpret_cast<int*>(b + o_dc);
         mig_cap = migcap;
         CK(cudaMemset(gridv, 0, size_t(nbtot) * 64 * sizeof(float4)));
         CK(cudaMemset(gridv0, 0, size_t(nbtot) * 64 * sizeof(float4)));
     }
-    ~Record() { cudaFree(mem); }
+    ~Record() {
+        cudaFree(mem);
+        if (hcnt) cudaFreeHost(hcnt);
+        if (hcnt_ev) cudaEventDestroy(hcnt_ev);
+    }
+    void readback_counts(cudaStream_t s) {
+        if (!hcnt) {
+            CK(cudaMallocHost(&hcnt, RC_N * sizeof(int)));
+            CK(cudaEventCreateWithFlags(&hcnt_ev, cudaEventDisableTiming));
+        }
+        CK(cudaMemcpyAsync(hcnt, dcnt, RC_N * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(hcnt_ev, s));
+    }
+    const int* host_counts() const {  // (long complete when the backward asks)
+        CK(cudaEventSynchronize(hcnt_ev));
+        return hcnt;
+    }
 };
 using RecordPtr = std::shared_ptr<Record>;
 
@@ -162,7 +189,7 @@ static int bits_for(uint64_t v) {
 // per-kernel CUDA-event timing (enabled by flume_profile): events are recorded on
 // the context stream around each launch and summed after the next sync
 enum KId { K_P2G = 0, K_GRID = 1, K_G2P = 2, K_SORT = 3, K_ADJ_G2P = 4, K_ADJ_GRID = 5, K_ADJ_P2G = 6,
-           K_RIGID = 7, K_OTHER = 8, K_COUNT = 9 };
+           K_RIGID = 7, K_OTHER = 8, K_COMM = 9, K_COUNT = 10 };
 
 struct Prof {
     bool on = false;
@@ -382,7 +409,9 @@ struct Ctx {
     int park_base = 0;  // first parked slot of cur (= n_active on one rank)
     int mig_cap = 0;
     DevArr<unsigned char> halo_send[2], halo_recv[2], mig_send[2], mig_recv[2];
-    DevArr<int> mig_cnt;
+    DevArr<int> d_ovf;  // migration / store overflow flag (checked once per call)
+    DevArr<int> mig_bcnt;
+    void set_mig_cap(int cap);
     DevArr<double> mbar;
     std::vector<float> parked_x;  // positions of parked particles by id (ownership of their activation)
     bool slab() const { return comm != nullptr; }
@@ -392,6 +421,103 @@ struct Ctx {
     void halo_exchange(int* blockmap, float4* stg, int* flags);
     void migrate(StateBuf& out, Record& r);
     void return_bars(Record& r, BarBuf post);
+    // slab contexts keep the exact particle counts on the device (StateBuf::cnt,
+    // Record::dcnt); the host holds upper bounds between calls and the exact values
+    // after sync_counts() (one stream sync, at call boundaries)
+    void state_counts_from_host(StateBuf& st) {
+        const int h[SC_N] = {n_active, n_stored, park_base, 0};
+        CK(cudaMemcpyAsync(st.cnt, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+    void rec_counts_from_host(Record& r, int pb) {
+        int h[RC_N] = {};
+        h[RC_ACTIVE] = r.n_active;
+        h[RC_KEEP] = r.n_keep;
+        h[RC_STORED] = r.n_stored;
+        h[RC_PARK] = pb;
+        CK(cudaMemcpyAsync(r.dcnt, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+    void sync_counts() {
+        if (!slab() || !cur) return;
+        int h[SC_N] = {};
+        CK(cudaMemcpyAsync(h, cur->cnt, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        n_active = h[SC_ACTIVE];
+        n_stored = h[SC_STORED];
+        park_base = h[SC_PARK];
+        cur->n = n_stored;
+    }
+    // A slab call whose migration overflowed its fixed-size messages is re-run from the
+    // same starting point with 4x the capacity (mutates = the call advances the context:
+    // its starting state and host bookkeeping are kept for the re-run).  The canonical
+    // order makes the result independent of the capacity.
+    template <class Fn>
+    void slab_retry(bool mutates, Fn&& fn) {
+        if (!slab()) {
+            fn();
+            return;
+        }
+        for (;;) {
+            StatePtr backup;
+            const long s0 = substep_index;
+            const double t0 = time;
+            const int na0 = n_active, ns0 = n_stored, pb0 = park_base;
+            const std::vector<EffState> eff0 = eff;
+            const std::vector<uint32_t> inact0 = inactive_ids;
+            const auto pend0 = pending;
+            if (mutates) {
+                backup = get_state();
+                copy_state(*backup, *cur);
+            }
+            // an overflowed attempt lost migrants, so it may also have raised a (collective,
+            // all-reduced) engine error: the overflow decides
+            bool failed = false;
+            FlumeError err(FLUME_E_ENGINE, "");
+            try {
+                fn();
+            } catch (const FlumeError& e) {
+                if (e.code == FLUME_E_CUDA || e.code == FLUME_E_ARG) throw;
+                failed = true;
+                err = e;
+            }
+            const bool ovf = migration_overflowed();
+            if (!ovf) {
+                put_state(backup);
+                if (failed) throw err;
+                sync_counts();
+                return;
+            }
+            if (mig_cap >= N) throw FlumeError(FLUME_E_ENGINE, "slab store overflow");
+            if (mutates) {
+                put_state(cur);
+                cur = backup;
+            }
+            // (a pure call that raised midway skipped its own host restore)
+            substep_index = s0;
+            time = t0;
+            n_active = na0;
+            n_stored = ns0;
+            park_base = pb0;
+            eff = eff0;
+            inactive_ids = inact0;
+            pending = pend0;
+            set_mig_cap(4 * mig_cap);
+            mig_retries++;
+        }
+    }
+    long mig_retries = 0;
+    // after a slab call: did any rank's migration exceed the message capacity (or the
+    // store)?  Collective; resets the flag.
+    bool migration_overflowed() {
+        if (!slab()) return false;
+        allreduce(d_ovf.p, 1, DType::I32, ROp::Max);
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, d_ovf.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (h) CK(cudaMemsetAsync(d_ovf.p, 0, sizeof(int), stream));
+        return h != 0;
+    }
     // effector-bar final sums are deferred and batched (kEffRing substeps per launch);
     // the backward runs t downwards, so the pending substeps are [eff_lo, eff_hi]
     long eff_lo = -1, eff_hi = -1;
@@ -913,11 +1039,13 @@ void Ctx::upload(const flume_state_view* view) {
     scratch_rec->n_active = n_active;
     scratch_rec->n_keep = n_active + n_parked();
     scratch_rec->n_stored = N;
+    if (slab()) rec_counts_from_host(*scratch_rec, 0);
     sort_and_lists(*raw, *scratch_rec);
     launch_gather(raw->p, cur->p, scratch_rec->perm, scratch_rec->n_keep, stream);
     n_stored = scratch_rec->n_keep;
     cur->n = n_stored;
     park_base = n_active;
+    if (slab()) state_counts_from_host(*cur);
     launch_upload_rigid(cur->p, nmem, d_member_id.p, d_up[0].p, stream);
     launches += 3;
     put_state(raw);
@@ -945,6 +1073,7 @@ void Ctx::download(flume_state_view* view) {
     }
     for (int k = 0; k < 4; k++) d_up[k].alloc(size_t(N) * (k < 2 ? 3 : 9));
     if (slab()) {
+        sync_counts();
         // every rank fills its own particles (rank 0 also the parked ones) into
         // zeroed arrays; the all-reduce assembles the whole state on every rank
         for (int k = 0; k < 4; k++) CK(cudaMemsetAsync(d_up[k].p, 0, d_up[k].n * 8, stream));
@@ -983,7 +1112,7 @@ void Ctx::download_meta(flume_state_view* view) {
 // keys -> canonical order + particle-block list (fl_sort.cu)
 void Ctx::sort_and_lists(StateBuf& st, Record& r) {
     Geom& g = geom;
-    const int n = r.n_stored;
+    const DN n = dn(r.n_stored, slab() ? r.dcnt + RC_STORED : nullptr);
     if (!counters_clean) CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
     counters_clean = false;
     launch_sort_count(g, st.p, n, d_cls.p, bcount, bheavy, stream);
@@ -1010,17 +1139,24 @@ void Ctx::set_transport(std::unique_ptr<Transport> t) {
         halo_send[d].alloc(halo_bytes(geom));
         halo_recv[d].alloc(halo_bytes(geom));
     }
-    // a slab can lose at most its own particles; a quarter of the scene per
-    // direction is far beyond what the CFL bound (< 1 cell per substep) allows
-    mig_cap = std::max(4096, N / 4);
-    for (int d = 0; d < 2; d++) {
-        mig_send[d].alloc(mig_bytes(mig_cap));
-        mig_recv[d].alloc(mig_bytes(mig_cap));
-    }
-    mig_cnt.alloc(2);
-    rec_pool.clear();
-    scratch_rec = get_record();
+    // fixed-size migration messages: the CFL bound (< 1 cell per substep) lets only the
+    // particles near a slab face leave, a small fraction of a slab; a substep that sends
+    // more sets the overflow flag and the call is re-run with 4x the capacity
+    set_mig_cap(4096);
+    d_ovf.alloc(1);
+    mig_bcnt.alloc(kMigCountInts);
+    CK(cudaMemsetAsync(d_ovf.p, 0, sizeof(int), stream));
     CK(cudaStreamSynchronize(stream));
+}
+
+void Ctx::set_mig_cap(int cap) {
+    mig_cap = std::min(cap, N);
+    for (int d = 0; d < 2; d++) {
+        mig_send[d].alloc(mig_msg_bytes(mig_cap));
+        mig_recv[d].alloc(mig_msg_bytes(mig_cap));
+    }
+    rec_pool.clear();  // records carry per-capacity migration slot lists
+    scratch_rec = get_record();
 }
 
 // Columns [cut[r], cut[r+1]) per rank, cut nearest to equal weight, at least
@@ -1075,56 +1211,49 @@ void Ctx::halo_exchange(int* blockmap, float4* stg, int* flags) {
 
 // Particles whose post-G2P base cell left the slab go to the neighbour (CFL:
 // < 1 cell per substep, so never further); arrivals are appended after the
-// parked tail.  One host round trip for the message sizes.
+// parked tail.  Fixed-size messages carry their counts in a header, and one thread
+// turns the headers into the record's and the post-state's device counts: no host
+// round trip.  The host keeps upper bounds for launch sizes (tightened from the
+// device counts read back asynchronously, host_bounds()).
 void Ctx::migrate(StateBuf& out, Record& r) {
-    CK(cudaMemsetAsync(mig_cnt.p, 0, 2 * sizeof(int), stream));
-    launch_mig_pack(geom, out.p, n_active, mig_send[0].p, mig_send[1].p, r.mig_src, mig_cnt.p, mig_cap, stream);
-    int h[2] = {0, 0};
-    CK(cudaMemcpyAsync(h, mig_cnt.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    if (h[0] > mig_cap || h[1] > mig_cap) {
-        comm->abort();
-        throw FlumeError(FLUME_E_ENGINE, "slab migration buffer overflow");
-    }
-    const long send[2] = {h[0], h[1]};
-    long recv[2] = {0, 0};
-    comm->exchange_counts(send, recv, stream);
+    const bool lo = rank > 0, hi = rank + 1 < nranks;
+    launch_mig_pack(geom, out.p, dn(r.n_active, r.dcnt + RC_ACTIVE), lo ? mig_send[0].p : nullptr,
+                    hi ? mig_send[1].p : nullptr, r.mig_src, mig_cap, mig_bcnt.p, d_ovf.p, stream);
+    const size_t mb = mig_msg_bytes(mig_cap);
     const void* sb[2] = {mig_send[0].p, mig_send[1].p};
     void* rb[2] = {mig_recv[0].p, mig_recv[1].p};
-    const size_t ss[2] = {mig_bytes(h[0]), mig_bytes(h[1])}, rs[2] = {mig_bytes(int(recv[0])), mig_bytes(int(recv[1]))};
-    comm->neighbor_exchange(sb, ss, rb, rs, stream);
-    const int base = n_active + n_parked();
-    if (base + recv[0] + recv[1] > N) {
-        comm->abort();
-        throw FlumeError(FLUME_E_ENGINE, "slab store overflow");
-    }
-    launch_mig_unpack(out.p, mig_recv[0].p, int(recv[0]), base, stream);
-    launch_mig_unpack(out.p, mig_recv[1].p, int(recv[1]), base + int(recv[0]), stream);
-    launches += 3;
-    for (int d = 0; d < 2; d++) {
-        r.n_out[d] = h[d];
-        r.n_in[d] = recv[d];
-    }
-    r.arr_base = base;
-    n_active += int(recv[0] + recv[1]) - h[0] - h[1];
-    n_stored = base + int(recv[0] + recv[1]);
+    const size_t sz[2] = {lo ? mb : 0, hi ? mb : 0};
+    comm->neighbor_exchange(sb, sz, rb, sz, stream);
+    launch_mig_counts(lo ? mig_send[0].p : nullptr, hi ? mig_send[1].p : nullptr, lo ? mig_recv[0].p : nullptr,
+                      hi ? mig_recv[1].p : nullptr, r.dcnt, out.cnt, mig_cap, N, d_ovf.p, stream);
+    if (lo) launch_mig_unpack(out.p, mig_recv[0].p, r.dcnt, 0, mig_cap, stream);
+    if (hi) launch_mig_unpack(out.p, mig_recv[1].p, r.dcnt, 1, mig_cap, stream);
+    r.readback_counts(stream);
+    launches += 3 + int(lo) + int(hi);
+    // host upper bounds: every neighbour sends at most mig_cap
+    const int in_max = (int(lo) + int(hi)) * mig_cap;
+    n_active = std::min(N, n_active + in_max);
+    n_stored = std::min(N, r.n_keep + in_max);
 }
 
 // Backward of migrate(): before the adjoint of substep r, the cotangents of the
 // particles that arrived here travel back into the departed slots of their
-// previous slab (message order = the forward's).
+// previous slab (message order = the forward's; counts from the record).
 void Ctx::return_bars(Record& r, BarBuf post) {
-    const size_t w = 24 * sizeof(float);
-    launch_bars_pack(post, r.arr_base, int(r.n_in[0]), mig_send[0].p, stream);
-    launch_bars_pack(post, r.arr_base + int(r.n_in[0]), int(r.n_in[1]), mig_send[1].p, stream);
+    const bool lo = rank > 0, hi = rank + 1 < nranks;
+    if (lo) launch_bars_pack(post, r.dcnt, 0, mig_cap, mig_send[0].p, stream);
+    if (hi) launch_bars_pack(post, r.dcnt, 1, mig_cap, mig_send[1].p, stream);
+    // exact sizes: the forward's counts came back to the host while it ran
+    const int* hc = r.host_counts();
+    auto bytes = [](int n) { return size_t(16 + 24 * size_t(n)) * sizeof(float); };
     const void* sb[2] = {mig_send[0].p, mig_send[1].p};
     void* rb[2] = {mig_recv[0].p, mig_recv[1].p};
-    const size_t ss[2] = {size_t(r.n_in[0]) * w, size_t(r.n_in[1]) * w};
-    const size_t rs[2] = {size_t(r.n_out[0]) * w, size_t(r.n_out[1]) * w};
+    const size_t ss[2] = {lo ? bytes(hc[RC_RECV]) : 0, hi ? bytes(hc[RC_RECV + 1]) : 0};
+    const size_t rs[2] = {lo ? bytes(hc[RC_SENT]) : 0, hi ? bytes(hc[RC_SENT + 1]) : 0};
     comm->neighbor_exchange(sb, ss, rb, rs, stream);
-    launch_bars_scatter(post, mig_recv[0].p, r.mig_src, int(r.n_out[0]), stream);
-    launch_bars_scatter(post, mig_recv[1].p, r.mig_src + r.mig_cap, int(r.n_out[1]), stream);
-    launches += 4;
+    if (lo) launch_bars_scatter(post, mig_recv[0].p, r.mig_src, r.dcnt, 0, mig_cap, stream);
+    if (hi) launch_bars_scatter(post, mig_recv[1].p, r.mig_src + r.mig_cap, r.dcnt, 1, mig_cap, stream);
+    launches += 2 * (int(lo) + int(hi));
 }
 
 void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r) {
@@ -1135,11 +1264,15 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     r.act.clear();
     r.emit.clear();
     auto it = pending.find(substep_index);
+    // slabs: activation slots are relative to the parked tail, whose first slot only the
+    // device counts know (the record's RC_PARK)
+    const int slot0 = slab() ? 0 : park_base;
+    const int* slot_base = slab() ? r.dcnt + RC_PARK : nullptr;
+    int gained = 0;
     if (it != pending.end()) {
-        int gained = 0;
         for (int id : it->second) {
             auto pos_it = std::lower_bound(inactive_ids.begin(), inactive_ids.end(), uint32_t(id));
-            int slot = park_base + int(pos_it - inactive_ids.begin());
+            int slot = slot0 + int(pos_it - inactive_ids.begin());
             ActEntry a{};
             a.slot = slot;
             int em = emitter_of[id];
@@ -1189,28 +1322,34 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         // parked slots are [n_active, n_active + parked): the activated ones are
         // re-keyed in place and sorted in; departed ones drop out at the next sort
         n_active += gained;
+    }
+    r.n_active = n_active;
+    r.n_keep = n_active + n_parked();
+    r.n_stored = n_stored;
+    if (slab()) {  // the record's exact counts, from the pre-state's device counts
+        launch_slab_counts_pre(in->cnt, r.dcnt, gained, n_parked(), mig_send[0].p, mig_send[1].p, stream);
+        launches++;
+    }
+    if (!r.act.empty()) {
         if (r.act.size() <= size_t(kActInline)) {
-            launch_activate_inline(geom, in->p, r.act.data(), int(r.act.size()), stream);
+            launch_activate_inline(geom, in->p, r.act.data(), int(r.act.size()), slot_base, stream);
         } else {
             d_act_list.alloc(r.act.size());
             CK(cudaMemcpyAsync(d_act_list.p, r.act.data(), r.act.size() * sizeof(ActEntry),
                                cudaMemcpyHostToDevice, stream));
-            launch_activate(geom, in->p, d_act_list.p, int(r.act.size()), stream);
+            launch_activate(geom, in->p, d_act_list.p, int(r.act.size()), slot_base, stream);
             // the activation list buffer is reused next substep: order the copy
             CK(cudaStreamSynchronize(stream));
         }
         launches++;
     }
-    r.n_active = n_active;
-    r.n_keep = n_active + n_parked();
-    r.n_stored = n_stored;
     PROF(K_SORT, sort_and_lists(*in, r));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     if (slab()) {
-        halo_exchange(r.blockmap, staging.p, nbflag);
+        PROF(K_COMM, halo_exchange(r.blockmap, staging.p, nbflag));
         // node-block list again, now with the blocks reached only by ghost tiles
         CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
         launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
@@ -1233,8 +1372,9 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
              launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : light_grid(grid_g2p), d_cls.p, r.gridv,
                         rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
-    PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, n_active, r.n_keep, stream));
-    launches += 1 + (r.n_keep > n_active ? 1 : 0);  // grid update, tail copy if any (dual() counts p2g, g2p)
+    PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, dn(r.n_active, slab() ? r.dcnt + RC_ACTIVE : nullptr),
+                                   dn(r.n_keep, slab() ? r.dcnt + RC_KEEP : nullptr), n_parked(), stream));
+    launches += 1 + (n_parked() > 0 ? 1 : 0);  // grid update, tail copy if any (dual() counts p2g, g2p)
     if (nbody > 0) {
         // slabs: every rank contributes its members' positions (disjoint support,
         // exact sum) so all ranks fit identical rigid transforms
@@ -1245,7 +1385,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     }
     park_base = r.n_active;
     if (slab()) {
-        migrate(*out, r);
+        PROF(K_COMM, migrate(*out, r));
     } else {
         n_stored = r.n_keep;
     }
@@ -1282,9 +1422,11 @@ void Ctx::stage_grid(double* mass, double* vel) {
         return;
     }
     Record& r = *scratch_rec;
+    sync_counts();
     r.n_active = n_active;
     r.n_keep = n_active + n_parked();
     r.n_stored = n_stored;
+    if (slab()) rec_counts_from_host(r, park_base);
     sort_and_lists(*cur, r);
     EffSet es = make_effset(eff);
     dual([&](bool hv, int* w, cudaStream_t s) {
@@ -1358,7 +1500,10 @@ LossSet Ctx::make_lossset(const flume_loss_desc* loss, std::vector<std::shared_p
             auto arr = std::make_shared<DevArr<float>>();
             arr->alloc(size_t(N) * 3);
             d_up[0].alloc(size_t(N) * 3);
-            if (slab()) CK(cudaMemsetAsync(d_up[0].p, 0, size_t(N) * 3 * 8, stream));
+            if (slab()) {
+                sync_counts();
+                CK(cudaMemsetAsync(d_up[0].p, 0, size_t(N) * 3 * 8, stream));
+            }
             launch_download(cur->p, n_stored, d_up[0].p, nullptr, nullptr, nullptr, rank == 0, geom.key_inactive,
                             d_cls.p, stream);
             if (slab()) allreduce(d_up[0].p, size_t(N) * 3, DType::F64, ROp::Sum);
@@ -1493,7 +1638,8 @@ uint32_t Ctx::loss_mask(const flume_loss_desc* loss, int seg, int nseg) const {
 void Ctx::eval_loss(StateBuf& st, const LossSet& ls0, uint32_t mask, double* out_dev, int seg, long substep) {
     const LossSet ls = at_substep(ls0, substep);
     // per-slab partial; the segment losses are all-reduced once after the rollout
-    launch_loss(st.p, st.n, d_cls.p, ls, mask, loss_partial.p, out_dev, geom.key_inactive, stream);
+    launch_loss(st.p, dn(st.n, slab() ? st.cnt + SC_STORED : nullptr), d_cls.p, ls, mask, loss_partial.p, out_dev,
+                geom.key_inactive, stream);
     launches += 2;
     point_losses(st, ls, mask, seg, out_dev, nullptr);
 }
@@ -1558,7 +1704,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     Geom& g = geom;
     BarBuf post{bars_post.p, N}, out{bars_pre.p, N};
     // slabs: cotangents of the particles that migrated in after this substep go home first
-    if (slab()) return_bars(r, post);
+    if (slab()) PROF(K_COMM, return_bars(r, post));
     // the forward recorded this substep's grid (r.gridv, r.gridv0, r.cmask) and block map
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
@@ -1572,7 +1718,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : light_grid(grid_adj, r.n_active), d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
-    if (slab()) halo_exchange(r.blockmap, staging_bar.p, nullptr);
+    if (slab()) PROF(K_COMM, halo_exchange(r.blockmap, staging_bar.p, nullptr));
     PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
                                      eff_partial.p + size_t(t_slot % kEffRing) * eff_blocks * kMaxEff * 18, r.cmask,
                                      eff_blocks, stream));
@@ -1581,18 +1727,23 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : light_grid(grid_ap, r.n_active), d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
-    PROF(K_OTHER, launch_tail_bars(post, out, r.perm, r.n_active, r.n_keep, r.n_stored, stream));
+    const int* rc = slab() ? r.dcnt : nullptr;
+    PROF(K_OTHER, launch_tail_bars(post, out, r.perm, dn(r.n_active, rc ? rc + RC_ACTIVE : nullptr),
+                                   dn(r.n_keep, rc ? rc + RC_KEEP : nullptr), dn(r.n_stored, rc ? rc + RC_STORED : nullptr),
+                                   stream));
     launches += 1 + (r.n_stored > r.n_active ? 1 : 0);  // grid adjoint, tail bars (dual() counts the rest)
     check_launch();
     if (!r.emit.empty()) {
         double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;
         if (r.emit.size() <= size_t(kEmitInline)) {
-            launch_adj_emit_inline(out, r.emit.data(), int(r.emit.size()), eo, int(eff.size()), stream);
+            launch_adj_emit_inline(out, r.emit.data(), int(r.emit.size()), eo, int(eff.size()),
+                                   slab() ? r.dcnt + RC_PARK : nullptr, stream);
         } else {
             d_emit_list.alloc(r.emit.size());
             CK(cudaMemcpyAsync(d_emit_list.p, r.emit.data(), r.emit.size() * sizeof(EmitAdjEntry),
                                cudaMemcpyHostToDevice, stream));
-            launch_adj_emit(out, d_emit_list.p, int(r.emit.size()), eo, int(eff.size()), stream);
+            launch_adj_emit(out, d_emit_list.p, int(r.emit.size()), eo, int(eff.size()),
+                            slab() ? r.dcnt + RC_PARK : nullptr, stream);
             CK(cudaStreamSynchronize(stream));
         }
         launches++;
@@ -1770,7 +1921,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             ensure_cached(t);
             StateBuf& boundary = *cache_states[size_t(t + 1 - cache_base)];
             const LossSet lsb = at_substep(ls, s0 + t + 1);
-            launch_loss_grad(boundary.p, boundary.n, d_cls.p, lsb, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
+            launch_loss_grad(boundary.p, dn(boundary.n, slab() ? boundary.cnt + SC_STORED : nullptr), d_cls.p, lsb, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
                              geom.key_inactive, stream);
             launches++;
             BarBuf bb{barsA.p, N};
@@ -2072,6 +2223,21 @@ int flume_slab_split(const double* col_weight, int n_cols, int n_ranks, int* cut
     return FLUME_OK;
 }
 
+int flume_slab_set_migration_capacity(flume_ctx* ctx, int capacity) {
+    if (!ctx || capacity < 1) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        if (!ctx->c.slab()) throw FlumeError(FLUME_E_ARG, "not a slab context");
+        ctx->c.set_mig_cap(capacity);
+    });
+}
+
+int flume_slab_migration_stats(const flume_ctx* ctx, int* capacity, long* retries) {
+    if (!ctx) return FLUME_E_ARG;
+    if (capacity) *capacity = ctx->c.mig_cap;
+    if (retries) *retries = ctx->c.mig_retries;
+    return FLUME_OK;
+}
+
 int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int* sx1, long* n_active) {
     if (!ctx) return FLUME_E_ARG;
     const fl::Ctx& c = ctx->c;
@@ -2218,7 +2384,7 @@ int flume_timer_elapsed(flume_ctx* ctx, int a, int b, double* ms) {
 
 int flume_substep(flume_ctx* ctx, const double action[6], int count) {
     if (!ctx || !action) return FLUME_E_ARG;
-    return guard(ctx, [&] { ctx->c.substep(action, count); });
+    return guard(ctx, [&] { ctx->c.slab_retry(true, [&] { ctx->c.substep(action, count); }); });
 }
 
 int flume_stage_grid(flume_ctx* ctx, double* mass, double* vel) {
@@ -2231,7 +2397,7 @@ int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume
     if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
     return guard(ctx, [&] {
         ctx->c.require_particles();
-        *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment);
+        ctx->c.slab_retry(false, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment); });
     });
 }
 
@@ -2240,7 +2406,7 @@ int flume_rollout_loss_final(flume_ctx* ctx, const flume_actions* actions, const
     if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
     return guard(ctx, [&] {
         ctx->c.require_particles();
-        *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment, true);
+        ctx->c.slab_retry(true, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment, true); });
     });
 }
 
@@ -2258,8 +2424,10 @@ int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const fl
     if (!ctx || !actions || !action_grad) return FLUME_E_ARG;
     return guard(ctx, [&] {
         ctx->c.require_particles();
-        ctx->c.grad_trajectory(actions, loss, stride, window, action_grad, loss_out, full_loss, per_segment,
-                               snapshots);
+        ctx->c.slab_retry(false, [&] {
+            ctx->c.grad_trajectory(actions, loss, stride, window, action_grad, loss_out, full_loss, per_segment,
+                                   snapshots);
+        });
     });
 }
 

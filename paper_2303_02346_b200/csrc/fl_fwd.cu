@@ -128,32 +128,36 @@ void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* 
 // fp64 from the stage-a effector pose
 // ---------------------------------------------------------------------------
 
-__global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n, ActBatch inl) {
+// slot_base (slab contexts): the entries' slots are relative to the parked tail, whose
+// first slot the device counts hold
+__global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n, ActBatch inl, const int* slot_base) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const ActEntry e = list ? list[i] : inl.e[i];
+    const int slot = e.slot + (slot_base ? *slot_base : 0);
     if (e.has_xv) {
         for (int a = 0; a < 3; a++) {
-            st.x(a)[e.slot] = e.x[a];
-            st.v(a)[e.slot] = e.v[a];
+            st.x(a)[slot] = e.x[a];
+            st.v(a)[slot] = e.v[a];
         }
     }
     uint32_t key;
-    cell_key(g, st.x(0)[e.slot], st.x(1)[e.slot], st.x(2)[e.slot], key);
-    st.key[e.slot] = e.departed ? g.key_departed : key;  // departed: activates on another slab
+    cell_key(g, st.x(0)[slot], st.x(1)[slot], st.x(2)[slot], key);
+    st.key[slot] = e.departed ? g.key_departed : key;  // departed: activates on another slab
 }
 
-void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s) {
+void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, const int* slot_base, cudaStream_t s) {
     if (n <= 0) return;
-    k_activate<<<(n + 127) / 128, 128, 0, s>>>(g, st, list, n, ActBatch{});
+    k_activate<<<(n + 127) / 128, 128, 0, s>>>(g, st, list, n, ActBatch{}, slot_base);
 }
 
-void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, cudaStream_t s) {
+void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, const int* slot_base,
+                            cudaStream_t s) {
     if (n <= 0) return;
     ActBatch b{};
     b.n = n;
     for (int i = 0; i < n; i++) b.e[i] = host_list[i];
-    k_activate<<<1, 128, 0, s>>>(g, st, nullptr, n, b);
+    k_activate<<<1, 128, 0, s>>>(g, st, nullptr, n, b, slot_base);
 }
 
 // ---------------------------------------------------------------------------
@@ -504,10 +508,10 @@ void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const Bl
              substep, wq);
 }
 
-__global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n0, int n) {
+__global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, DN n0, DN n1) {
     pdl_wait();
-    int j = n0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    int j = n0.get() + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n1.get()) return;
     uint32_t s = perm[j];
     for (int c = 0; c < 24; c++) out.f[size_t(c) * out.cap + j] = in.f[size_t(c) * in.cap + s];
     out.meta[j] = in.meta[s];
@@ -515,11 +519,12 @@ __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restric
     out.key[j] = g.key_inactive;
 }
 
-// parked particles: sorted positions [n_active, n) (departed slots beyond n are dropped)
-void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s) {
-    int m = n - n_active;
-    if (m <= 0) return;
-    launch_k(k_tail_copy, dim3((m + 255) / 256), dim3(256), 0, s, g, in, out, perm, n_active, n);
+// parked particles: sorted positions [n_active, n) (departed slots beyond n are dropped);
+// there are n_parked of them on every rank
+void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, DN n_active, DN n, int n_parked,
+                      cudaStream_t s) {
+    if (n_parked <= 0) return;
+    launch_k(k_tail_copy, dim3((n_parked + 255) / 256), dim3(256), 0, s, g, in, out, perm, n_active, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -637,12 +642,13 @@ void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* 
 // target_point / hold_initial losses at segment boundaries (losses.hpp:474-551)
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(256) k_loss_partial(PBuf st, int n, const ClassInfo* __restrict__ cls,
+__global__ void __launch_bounds__(256) k_loss_partial(PBuf st, DN nn, const ClassInfo* __restrict__ cls,
                                                       LossSet ls, uint32_t mask, uint32_t key_inactive,
                                                       double* partial) {
     __shared__ double red[256];
     double acc[kMaxLossTerms];
     for (int k = 0; k < kMaxLossTerms; k++) acc[k] = 0.0;
+    const int n = nn.get();
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
         const int body = cls[meta_cls(st.meta[i])].body;
         const uint32_t key = st.key[i];
@@ -695,7 +701,7 @@ __global__ void k_loss_final(const double* partial, int nblocks, LossSet ls, uin
     }
 }
 
-void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, double* partial,
+void launch_loss(const PBuf& st, DN n, const ClassInfo* cls, const LossSet& ls, uint32_t mask, double* partial,
                  double* out, uint32_t key_inactive, cudaStream_t s) {
     k_loss_partial<<<kLossBlocks, 256, 0, s>>>(st, n, cls, ls, mask, key_inactive, partial);
     k_loss_final<<<1, 32 * kMaxLossTerms, 0, s>>>(partial, kLossBlocks, ls, mask, out);

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -33,6 +34,36 @@ inline void check_launch() {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
 }
+
+// A particle count a kernel needs.  On one rank the host knows every count exactly (h);
+// on x-slabs the migration changes them on the device, so the kernels read d (the state's
+// or the record's device counts) and h is only an upper bound that sizes the grid.
+struct DN {
+    int h;
+    const int* d;
+    __host__ __device__ int get() const {
+#if defined(__CUDA_ARCH__)
+        return d ? *d : h;
+#else
+        return h;
+#endif
+    }
+};
+inline DN dn(int h, const int* d = nullptr) { return DN{h, d}; }
+// device counts of a state buffer (slab contexts) and of a substep record
+enum StateCnt : int { SC_ACTIVE = 0, SC_STORED = 1, SC_PARK = 2, SC_N = 4 };
+enum RecCnt : int {
+    RC_ACTIVE = 0,   // active particles of the pre-state after this substep's activations
+    RC_KEEP = 1,     // active + parked
+    RC_STORED = 2,   // all slots of the pre-state (departed holes included)
+    RC_PARK = 3,     // first parked slot of the pre-state (activation slots are relative to it)
+    RC_SENT = 4,     // [4], [5]: particles sent down / up after G2P
+    RC_RECV = 6,     // [6], [7]: particles received from below / above
+    RC_ARR = 8,      // first arrival slot of the post-state
+    RC_N = 12
+};
+// grid for a grid-stride loop over up to n items (256 threads, at most `cap` CTAs)
+inline int gs_grid(int n, int cap = 148 * 16) { return std::max(1, std::min(cap, (n + 255) / 256)); }
 
 // rigid-body bookkeeping for one substep (forward record / backward input)
 struct RigidDev {
@@ -178,8 +209,9 @@ void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double
                    const double* C, const uint32_t* meta, const uint8_t* active, const ClassInfo* cls,
                    cudaStream_t s);
 void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
-void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, cudaStream_t s);
-void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, cudaStream_t s);
+void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, const int* slot_base, cudaStream_t s);
+void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, const int* slot_base,
+                            cudaStream_t s);
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
                 uint32_t substep, int variant, int* wq, cudaStream_t s);
@@ -189,7 +221,8 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs,
                 const int* n_blocks, int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd,
                 unsigned long long* err, uint32_t substep, int variant, int* wq, cudaStream_t s);
-void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, int n_active, int n, cudaStream_t s);
+void launch_tail_copy(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, DN n_active, DN n, int n_parked,
+                      cudaStream_t s);
 void launch_rigid(const Geom& g, PBuf out, RigidDev rd, int nchunks, const int* chunk_body,
                   const int* chunk_m0, const int* chunk_m1, double* partial, unsigned long long* err,
                   uint32_t substep, cudaStream_t s);
@@ -197,11 +230,11 @@ void launch_download(PBuf st, int n, double* x, double* v, double* F, double* C,
                      uint32_t key_inactive, const ClassInfo* cls, cudaStream_t s);
 void launch_download_rigid(PBuf st, int nmem, const int* member_id, double* x, cudaStream_t s);
 void launch_upload_rigid(PBuf st, int nmem, const int* member_id, const double* x, cudaStream_t s);
-void launch_loss(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
+void launch_loss(const PBuf& st, DN n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
                  double* partial, double* out, uint32_t key_inactive, cudaStream_t s);
 
 // ---- backward ----
-void launch_loss_grad(const PBuf& st, int n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
+void launch_loss_grad(const PBuf& st, DN n, const ClassInfo* cls, const LossSet& ls, uint32_t mask,
                       BarBuf bars, uint32_t key_inactive, cudaStream_t s);
 void launch_adj_rigid_gather(BarBuf post, RigidDev rd, double* mbar, cudaStream_t s);
 void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, const int* chunk_body,
@@ -220,11 +253,12 @@ void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int c
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, int variant, int* wq, cudaStream_t s);
-void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, int n_active, int n_keep, int n_stored,
+void launch_tail_bars(BarBuf post, BarBuf out, const uint32_t* perm, DN n_active, DN n_keep, DN n_stored,
                       cudaStream_t s);
-void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, cudaStream_t s);
+void launch_adj_emit(BarBuf out, const EmitAdjEntry* list, int n, double* em_out, int n_eff, const int* slot_base,
+                     cudaStream_t s);
 constexpr int kEmitInline = 32;
-void launch_adj_emit_inline(BarBuf out, const EmitAdjEntry* host_list, int n, double* em_out, int n_eff,
+void launch_adj_emit_inline(BarBuf out, const EmitAdjEntry* host_list, int n, double* em_out, int n_eff, const int* slot_base,
                             cudaStream_t s);
 void launch_bars_from_ref(BarBuf bars, const PBuf& st, int n, const double* xb, const double* vb,
                           const double* Fb, const double* Cb, const ClassInfo* cls, cudaStream_t s);
@@ -232,9 +266,9 @@ void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* 
                         const ClassInfo* cls, cudaStream_t s);
 void launch_expand_f(PBuf st, int n, const ClassInfo* cls, cudaStream_t s);
 
-void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
+void launch_sort_count(const Geom& g, const PBuf& st, DN n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s);
-void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, int* bfill, uint32_t* skey,
+void launch_sort_scatter(const Geom& g, const PBuf& st, DN n, const int* bstart, int* bfill, uint32_t* skey,
                          uint32_t* sslot, cudaStream_t s);
 int sort_list_tiles(const Geom& g);
 void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
@@ -248,16 +282,25 @@ void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, con
 
 // ---- x-slab decomposition (fl_slab.cu) ----
 size_t halo_bytes(const Geom& g);
-size_t mig_bytes(int n);
 void launch_halo_pack(const Geom& g, const int* blockmap, const float4* staging, int col, int plane0, void* out,
                       cudaStream_t s);
 void launch_halo_unpack(const Geom& g, const void* in, int col, int plane0, int ghost_base, int* blockmap,
                         float4* staging, int* nbflag, int flag_col, cudaStream_t s);
-void launch_mig_pack(const Geom& g, PBuf out, int n, void* send0, void* send1, uint32_t* src, int* cnt, int cap,
-                     cudaStream_t s);
-void launch_mig_unpack(PBuf out, const void* in, int n, int pos0, cudaStream_t s);
-void launch_bars_pack(BarBuf bars, int pos0, int n, void* out, cudaStream_t s);
-void launch_bars_scatter(BarBuf bars, const void* in, const uint32_t* src, int n, cudaStream_t s);
+// fixed-size migration messages: a 16-int header (the count) + cap slots of kMigW words
+size_t mig_msg_bytes(int cap);
+void launch_mig_pack(const Geom& g, PBuf out, DN n, void* send0, void* send1, uint32_t* src, int cap, int* bcnt,
+                     int* overflow, cudaStream_t s);
+constexpr int kMigCountInts = 2 * 296;  // per-CTA counts of the stable migration compaction
+// counts after the exchange: record [sent, recv, arrival base], post-state counts, overflow
+void launch_mig_counts(const void* send0, const void* send1, const void* recv0, const void* recv1, int* rec,
+                       int* post_cnt, int cap, int n_cap, int* overflow, cudaStream_t s);
+void launch_mig_unpack(PBuf out, const void* in, const int* rec, int dir, int cap, cudaStream_t s);
+// before a substep: the record's pre-state counts from the state's device counts
+void launch_slab_counts_pre(const int* state_cnt, int* rec, int gained, int n_parked, void* send0, void* send1,
+                            cudaStream_t s);
+void launch_bars_pack(BarBuf bars, const int* rec, int dir, int cap, void* out, cudaStream_t s);
+void launch_bars_scatter(BarBuf bars, const void* in, const uint32_t* src, const int* rec, int dir, int cap,
+                         cudaStream_t s);
 
 enum KGrid { KG_P2G = 0, KG_G2P = 1, KG_ADJ_G2P = 2, KG_ADJ_P2G = 3 };
 // resident CTAs per SM x SMs; variant 0 plain liquid, 1 heavy beside light, 2 heavy-dominated scene

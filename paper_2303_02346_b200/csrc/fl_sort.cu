@@ -35,11 +35,11 @@ namespace fl {
 #endif
 constexpr int kSortThreads = FL_SORT_THREADS;
 
-__global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict__ cls, int* bcount,
+__global__ void k_sort_count(Geom g, PBuf st, DN nn, const ClassInfo* __restrict__ cls, int* bcount,
                              int* bheavy) {
     pdl_wait();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= nn.get()) return;
     const uint32_t key = st.key[i];
     const int b = key >= g.key_inactive ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
     // warp-aggregated: the store order is nearly sorted, so lanes share blocks
@@ -54,11 +54,11 @@ __global__ void k_sort_count(Geom g, PBuf st, int n, const ClassInfo* __restrict
     }
 }
 
-__global__ void k_sort_scatter(Geom g, PBuf st, int n, const int* __restrict__ bstart, int* bfill, uint32_t* skey,
+__global__ void k_sort_scatter(Geom g, PBuf st, DN nn, const int* __restrict__ bstart, int* bfill, uint32_t* skey,
                                uint32_t* sslot) {
     pdl_wait();
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= nn.get()) return;
     const uint32_t key = st.key[i];
     const bool inact = key >= g.key_inactive;  // parked or departed
     const int b = inact ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
@@ -220,15 +220,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
     }
 }
 
-void launch_sort_count(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
+// n.h: the slot count (an upper bound on slabs, where the kernels read the device count)
+void launch_sort_count(const Geom& g, const PBuf& st, DN n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s) {
-    if (n <= 0) return;  // (an empty slab)
-    launch_k(k_sort_count, dim3((n + 255) / 256), dim3(256), 0, s, g, st, n, cls, bcount, bheavy);
+    if (n.h <= 0) return;  // (an empty slab)
+    launch_k(k_sort_count, dim3((n.h + 255) / 256), dim3(256), 0, s, g, st, n, cls, bcount, bheavy);
 }
-void launch_sort_scatter(const Geom& g, const PBuf& st, int n, const int* bstart, int* bfill, uint32_t* skey,
+void launch_sort_scatter(const Geom& g, const PBuf& st, DN n, const int* bstart, int* bfill, uint32_t* skey,
                          uint32_t* sslot, cudaStream_t s) {
-    if (n <= 0) return;
-    launch_k(k_sort_scatter, dim3((n + 255) / 256), dim3(256), 0, s, g, st, n, bstart, bfill, skey, sslot);
+    if (n.h <= 0) return;
+    launch_k(k_sort_scatter, dim3((n.h + 255) / 256), dim3(256), 0, s, g, st, n, bstart, bfill, skey, sslot);
 }
 
 // ---------------------------------------------------------------------------

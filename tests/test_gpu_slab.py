@@ -71,6 +71,40 @@ def test_slab_migration_happens_and_conserves():
         assert np.array_equal(a, b)
 
 
+def test_slab_migration_overflow_reruns_larger():
+    """Migration messages have a fixed capacity (counts stay on the device); a call whose
+    migrants exceed it sets the overflow flag and is re-run from its start with 4x the
+    capacity.  Forced here with 2 slots per message on the fast blob: the states are still
+    one rank's bit for bit, for a mutating call (mpm_substep) and a pure one (grad_trajectory)."""
+    spec = spec_for("c1", 32)
+    w = fl.build_scene(spec)
+    v = w.state.v
+    v[:, 0] = 100.0
+    w.state.v = v
+    ref = fl.build_scene(spec)
+    ref.state.v = v
+    ws1 = fl.GpuWorkspace(ref.scene)
+    ws3 = fl.GpuWorkspace(w.scene, ranks=3)
+    ws3._upload(w.state)
+    ws3.set_migration_capacity(2)
+    fl.mpm_substep(ref.scene, ref.state, ref.init_action, ws1, count=12)
+    fl.mpm_substep(w.scene, w.state, w.init_action, ws3, count=12)
+    stats = ws3.migration_stats()
+    assert all(n >= 1 and cap > 2 for cap, n in stats), stats
+    for a, b in zip(_state(ref.state), _state(w.state)):
+        assert np.array_equal(a, b)
+    ws3.set_migration_capacity(2)
+    acts = fl.ActionTrajectory(2, 4, np.tile(w.init_action, (2, 1)))
+    g1 = fl.grad_trajectory(ref.scene, ref.state, acts, fl.LossEvaluator(ref.scene, ref.loss_spec, ref.state),
+                            stride=2, ws=ws1)
+    g3 = fl.grad_trajectory(w.scene, w.state, acts, fl.LossEvaluator(w.scene, w.loss_spec, w.state), stride=2,
+                            ws=ws3)
+    assert ws3.migration_stats()[0][1] > stats[0][1]
+    assert abs(g1.loss - g3.loss) <= 1e-12 * abs(g1.loss)
+    gg1, gg3 = np.asarray(g1.action_grad), np.asarray(g3.action_grad)
+    assert np.max(np.abs(gg1 - gg3)) <= 1e-9 * np.max(np.abs(gg1)), (gg1, gg3)
+
+
 @pytest.mark.parametrize("name,res,nseg,seglen,stride", [("c1", 32, 2, 5, 5), ("c2", 32, 2, 4, 3),
                                                          ("c5", 32, 2, 3, 2), ("c4", 32, 1, 6, 0)])
 def test_slab_grad_trajectory_matches_one_rank(name, res, nseg, seglen, stride):
