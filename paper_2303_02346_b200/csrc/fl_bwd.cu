@@ -440,7 +440,7 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
 // ---------------------------------------------------------------------------
 constexpr int kEffQ = 18;  // t[3] R[9] vlin[3] w[3]
 #ifndef FL_ADJGRID_THREADS
-#define FL_ADJGRID_THREADS 64
+#define FL_ADJGRID_THREADS 128
 #endif
 constexpr int kAdjGridThreads = FL_ADJGRID_THREADS;
 

@@ -19,8 +19,6 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -372,8 +370,6 @@ struct Ctx {
     DevArr<int> nbpos;
     DevArr<int4> tile_sum;
     DevArr<uint32_t> skey, sslot, gk, gv;
-    DevArr<unsigned char> cub_tmp;
-    size_t cub_bytes = 0;
     DevArr<float4> staging, staging_bar, gridbar;
     DevArr<unsigned long long> d_err;
     DevArr<int> d_nonfinite;
@@ -825,11 +821,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     d_emit_list.alloc(64);
     CK(cudaMemsetAsync(gridbar.p, 0, gridbar.n * sizeof(float4), stream));
 
-    size_t b2 = 0, b3 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, bcount, bstart.p, g.nbtot + 2, stream));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, b3, nbflag, nbpos.p, g.nbtot, stream));
-    cub_bytes = std::max(b2, b3);
-    cub_tmp.alloc(cub_bytes);
+
 
     // heavy kernels: a scene dominated by SVD/rigid particles (c3) wants them at high
     // occupancy; a mostly-liquid one (c4) at low occupancy beside the light kernel
@@ -1351,8 +1343,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     if (slab()) {
         PROF(K_COMM, halo_exchange(r.blockmap, staging.p, nbflag));
         // node-block list again, now with the blocks reached only by ghost tiles
-        CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
-        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
+        launch_flag_list(nbflag, geom.nbtot, r.nb_list, r.n_nb, nbpos.p, stream);
         launches += 2;
     }
     // the adjoint's inputs (v0 = p/m, contact mask) only for substeps that keep a record
@@ -1435,8 +1426,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
     });
     if (slab()) {
         halo_exchange(r.blockmap, staging.p, nbflag);
-        CK(cub::DeviceScan::ExclusiveSum(cub_tmp.p, cub_bytes, nbflag, nbpos.p, geom.nbtot, stream));
-        launch_nb_scatter(nbflag, nbpos.p, geom.nbtot, r.nb_list, r.n_nb, nullptr, r.n_blocks, stream);
+        launch_flag_list(nbflag, geom.nbtot, r.nb_list, r.n_nb, nbpos.p, stream);
     }
     launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0, es, r.cmask,
                        bzero.p, int(bzero.n), stream);

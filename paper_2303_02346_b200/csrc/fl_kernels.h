@@ -274,8 +274,9 @@ int sort_list_tiles(const Geom& g);
 void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
                        int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
                        cudaStream_t s);
-void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, const int* cnt_scratch,
-                       int* n_blocks, cudaStream_t s);
+// id-ordered list of the nonzero flags (two-pass tile scan); tile_sum: flag_list_tiles(n) ints
+void launch_flag_list(const int* flags, int n, int* list, int* n_list, int* tile_sum, cudaStream_t s);
+int flag_list_tiles(int n);
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s);

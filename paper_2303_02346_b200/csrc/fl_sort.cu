@@ -376,25 +376,48 @@ void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bhe
                                                 recs, blockmap, n_blocks);
 }
 
-// compact, id-ordered list of touched node blocks
-// compact, id-ordered list of touched node blocks; also publishes the
-// particle-block list counters (scratch -> record)
-__global__ void k_nb_scatter(const int* __restrict__ flags, const int* __restrict__ pos, int n, int* list,
-                             int* n_list, const int* __restrict__ cnt_scratch, int* n_blocks) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0 && cnt_scratch) {
-        n_blocks[0] = cnt_scratch[0];
-        n_blocks[1] = cnt_scratch[1];
-    }
-    if (i >= n) return;
-    if (flags[i]) list[pos[i]] = i;
-    if (i == n - 1) *n_list = pos[i] + (flags[i] ? 1 : 0);
+// Slabs: the node-block list again after the halo unpack flagged the blocks reached
+// only by ghost tiles -- the same two-pass tile scan as the list pass above, over the
+// flags alone: per-tile sums, then every tile adds its predecessors' sums and writes
+// its part of the id-ordered list (deterministic, no atomics, no library scan).
+__global__ void __launch_bounds__(kListThreads) k_flag_sums(const int* __restrict__ flags, int n, int* tile_sum) {
+    using Red = cub::BlockReduce<int, kListThreads>;
+    __shared__ typename Red::TempStorage tmp;
+    const int b = blockIdx.x * kListThreads + threadIdx.x;
+    const int t = Red(tmp).Sum(b < n ? (flags[b] != 0) : 0);
+    if (threadIdx.x == 0) tile_sum[blockIdx.x] = t;
 }
 
-void launch_nb_scatter(const int* flags, const int* pos, int nbtot, int* list, int* n_list, const int* cnt_scratch,
-                       int* n_blocks, cudaStream_t s) {
-    k_nb_scatter<<<(nbtot + 255) / 256, 256, 0, s>>>(flags, pos, nbtot, list, n_list, cnt_scratch, n_blocks);
+__global__ void __launch_bounds__(kListThreads) k_flag_write(const int* __restrict__ flags, int n,
+                                                             const int* __restrict__ tile_sum, int* list,
+                                                             int* n_list) {
+    using Scan = cub::BlockScan<int, kListThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int base;
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        int s = 0;
+        for (int t = tid; t < int(blockIdx.x); t += 32) s += tile_sum[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (tid == 0) base = s;
+    }
+    const int b = blockIdx.x * kListThreads + tid;
+    const int f = b < n ? (flags[b] != 0) : 0;
+    int pre, tot;
+    Scan(tmp).ExclusiveSum(f, pre, tot);
+    __syncthreads();
+    if (f) list[base + pre] = b;
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) *n_list = base + tot;
 }
+
+void launch_flag_list(const int* flags, int n, int* list, int* n_list, int* tile_sum, cudaStream_t s) {
+    const int tiles = (n + kListThreads - 1) / kListThreads;
+    k_flag_sums<<<tiles, kListThreads, 0, s>>>(flags, n, tile_sum);
+    k_flag_write<<<tiles, kListThreads, 0, s>>>(flags, n, tile_sum, list, n_list);
+}
+int flag_list_tiles(int n) { return (n + kListThreads - 1) / kListThreads; }
+
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s) {
