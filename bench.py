@@ -15,7 +15,8 @@ The same line carries `configs` (c1, c2, c3 on one GPU, one segment each; c5 ove
 SCALE_HORIZON) and `scaling_base` (c5 on one GPU over the same horizon as N > 1).
 N > 1 (torchrun, one process per GPU): the north star's scaling scene c5
 (8,044,544 particles, 256^3) split into x-slabs, one per GPU:
-halo planes and migrating particles go to the neighbouring ranks over NCCL,
+halo planes and migrating particles go to the neighbouring ranks (CUDA IPC peer
+copies into exported device inboxes over NVLink by default, `--transport nccl` for NCCL),
 rigid/loss/effector sums are all-reduced, so the scaling is strong (compare
 with `scaling_base` of the N = 1 line).  If the slab transport cannot start the
 run prints an `error` line and exits non-zero (no silent fallback).
@@ -303,7 +304,8 @@ def run_ours(args):
         local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
         # torch.distributed is host plumbing only (id broadcast, barriers, max-over-ranks
-        # timings): gloo; the data path between the GPUs is the library's own NCCL transport
+        # timings): gloo; the data path between the GPUs is the library's own transport
+        # (CUDA IPC peer copies over NVLink, or NCCL with --transport nccl)
         dist.init_process_group("gloo")
         _watchdog(args.deadline, rank)
 
@@ -317,7 +319,7 @@ def run_ours(args):
         obj = [None]
         if rank == 0:
             try:
-                obj[0] = fl.dist_unique_id()
+                obj[0] = fl.ipc_unique_id() if args.transport == "ipc" else fl.dist_unique_id()
             except Exception as e:
                 obj[0] = "error: " + str(e)
         dist.broadcast_object_list(obj, src=0)
@@ -335,7 +337,8 @@ def run_ours(args):
         if int(ok.item()) == 0:
             if rank == 0:
                 print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world_size,
-                                  "error": f"x-slab NCCL transport did not start: {err or 'failed on a peer rank'}"}),
+                                  "error": f"x-slab {args.transport} transport did not start: "
+                                           f"{err or 'failed on a peer rank'}"}),
                       flush=True)
             os._exit(4)
     if ws is None:
@@ -568,7 +571,9 @@ def run_ours(args):
                                ", target_point loss per segment",
                    "particles": n, "grid": grid, "active_nodes": A, "horizon": T,
                    "l2": "inputs larger than L2 (trajectory store ~%.1f GB per step)" % (n * 112 * (T + 1) / 1e9),
-                   "parallelism": "single" if mode == "single" else f"x-slabs over {world_size} GPUs (NCCL halos)",
+                   "parallelism": "single" if mode == "single" else
+                   f"x-slabs over {world_size} GPUs ({'CUDA IPC' if args.transport == 'ipc' else 'NCCL'} halos "
+                   "and migration)",
                    **({"rank0_particles": n_local} if mode == "slabs" else {})},
         "fwd": {"value": fwd_value, "unit": UNIT,
                 "workload": f"mpm_substep x {T} from the uploaded state (re-uploaded untimed every step)"},
@@ -603,6 +608,8 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config and scaling-base legs")
     ap.add_argument("--scene", default=None, help="override the scene (c1..c5)")
     ap.add_argument("--deadline", type=float, default=600.0, help="multi-GPU watchdog (s)")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="x-slab data path for N > 1: CUDA IPC peer copies (default) or NCCL")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

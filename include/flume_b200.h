@@ -242,9 +242,14 @@ int flume_last_timing(const flume_ctx* ctx, flume_timing* out);
  *   flume_group_create     n contexts in this process (one host thread per rank;
  *                          ranks may share a device), peer copies over NVLink
  *   flume_ctx_create_dist  one context per process (torchrun), NCCL; all ranks
- *                          pass the id rank 0 got from flume_dist_unique_id */
+ *                          pass the id rank 0 got from flume_dist_unique_id (or
+ *                          flume_ipc_unique_id: CUDA IPC within one node) */
 int flume_group_create(const flume_scene_desc* desc, int n_ranks, const int* devices, flume_ctx** out_ctxs);
 int flume_dist_unique_id(unsigned char uid[128]);
+/* group id for the CUDA-IPC transport instead of NCCL: the processes of one node (one or
+ * several ranks per GPU) copy into each other's IPC-exported device inboxes (NVLink
+ * between GPUs), ordered by interprocess events; pass it to flume_ctx_create_dist */
+int flume_ipc_unique_id(unsigned char uid[128]);
 int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, int n_ranks,
                           const unsigned char uid[128], flume_ctx** out);
 int flume_slab_info(const flume_ctx* ctx, int* rank, int* n_ranks, int* sx0, int* sx1, long* n_active);

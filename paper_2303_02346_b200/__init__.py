@@ -7,7 +7,7 @@ include/flume_b200.h.  This package is the host-side mirror of the reference's
 scene / step / grad API (proj/include/flume)."""
 from .api import (ActionTrajectory, AdjointError, AdjointState, DegenerateDeformation, DeviceError, EngineError,
                   GpuWorkspace, LossEvaluator, RigidityError, Scene, SceneError, SimState, SubstepRecord,
-                  TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, mpm_substep,
+                  TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, ipc_unique_id, mpm_substep,
                   p2g_grid, rollout_loss, slab_split, WorkspacePool, rollout_loss_batch,
                   grad_trajectory_batch, state_to_json, state_from_json, GradReport, grad_check,
                   finite_difference_gradient, optimizable_components)
@@ -15,7 +15,7 @@ from . import frames, scenes
 
 __all__ = ["ActionTrajectory", "AdjointError", "AdjointState", "DegenerateDeformation", "DeviceError", "EngineError",
            "GpuWorkspace", "LossEvaluator", "RigidityError", "Scene", "SceneError", "SimState", "SubstepRecord",
-           "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "mpm_substep", "p2g_grid",
+           "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "ipc_unique_id", "mpm_substep", "p2g_grid",
            "rollout_loss", "scenes", "slab_split", "WorkspacePool", "rollout_loss_batch", "grad_trajectory_batch",
            "state_to_json", "state_from_json", "frames", "GradReport", "grad_check",
            "finite_difference_gradient", "optimizable_components"]

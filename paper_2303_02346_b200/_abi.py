@@ -122,6 +122,7 @@ EXPORTS = {
     "flume_slab_split": (C.c_int, [C.POINTER(C.c_double), C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "flume_slab_set_migration_capacity": (C.c_int, [C.c_void_p, C.c_int]),
     "flume_slab_migration_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_long)]),
+    "flume_ipc_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "flume_slab_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), C.POINTER(C.c_long)]),
     "flume_set_mode": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),

@@ -684,6 +684,17 @@ def dist_unique_id() -> bytes:
     return bytes(u)
 
 
+def ipc_unique_id() -> bytes:
+    """Group id for GpuWorkspace.distributed over CUDA IPC (the processes of one node,
+    one or several ranks per GPU) instead of NCCL; call on one rank and share it."""
+    lib = load()
+    u = (C.c_ubyte * 128)()
+    rc = lib.flume_ipc_unique_id(u)
+    if rc != _abi.FLUME_OK:
+        _raise(lib, None, rc)
+    return bytes(u)
+
+
 def _ws_for(scene: Scene, ws: Optional[GpuWorkspace]) -> GpuWorkspace:
     if ws is None:
         raise ValueError("a GpuWorkspace is required (MpmWorkspace analogue)")

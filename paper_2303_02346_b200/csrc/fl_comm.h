@@ -8,7 +8,7 @@
 //   * all-reduce           rigid-member positions and bars (disjoint support,
 //                          so the sum is exact), loss partials, effector bars,
 //                          error flags.
-// Two implementations:
+// Three implementations:
 //   ThreadTransport  one process, one host thread per rank (ranks may share a
 //                    device); copies are stream-ordered cudaMemcpyPeerAsync
 //                    behind cross-stream events, reductions are summed in rank
@@ -16,6 +16,9 @@
 //   NcclTransport    one process per GPU (torchrun); NCCL send/recv and
 //                    all-reduce on the context stream.  libnccl is dlopen'ed
 //                    (the copy torch already loaded when present).
+//   IpcTransport     processes of one node (one or several per GPU): peer copies
+//                    into CUDA-IPC-exported inboxes (NVLink between GPUs), ordered
+//                    by interprocess events, host barrier in POSIX shared memory.
 // All calls are collective over the group and must be issued in the same order
 // on every rank.
 #pragma once
@@ -79,6 +82,10 @@ struct ThreadGroup {
 std::unique_ptr<Transport> make_thread_transport(std::shared_ptr<ThreadGroup> g, int rank, int device);
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char uid[128], int rank, int nranks, int device);
 void nccl_unique_id(unsigned char out[128]);
+// CUDA-IPC transport between the processes of one node ("IPC:" group ids)
+bool is_ipc_unique_id(const unsigned char uid[128]);
+std::unique_ptr<Transport> make_ipc_transport(const unsigned char uid[128], int rank, int nranks, int device);
+void ipc_unique_id(unsigned char out[128]);
 
 // dtype/op reduction of `nr` stacked copies (rank order) into out (ThreadTransport)
 void launch_stack_reduce(const void* stack, size_t count, int nr, DType t, ROp op, void* out, cudaStream_t s);

@@ -2189,6 +2189,11 @@ int flume_dist_unique_id(unsigned char uid[128]) {
     return guard(nullptr, [&] { fl::nccl_unique_id(uid); });
 }
 
+int flume_ipc_unique_id(unsigned char uid[128]) {
+    if (!uid) return FLUME_E_ARG;
+    return guard(nullptr, [&] { fl::ipc_unique_id(uid); });
+}
+
 int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, int n_ranks,
                           const unsigned char uid[128], flume_ctx** out) {
     if (!desc || !out || !uid || rank < 0 || rank >= n_ranks) return FLUME_E_ARG;
@@ -2197,7 +2202,8 @@ int flume_ctx_create_dist(const flume_scene_desc* desc, int device, int rank, in
     int rc = guard(nullptr, [&] {
         ctx->c.init(desc, device);
         // (a one-rank NCCL group is allowed: it runs the slab code path with a single slab)
-        ctx->c.set_transport(fl::make_nccl_transport(uid, rank, n_ranks, device));
+        ctx->c.set_transport(fl::is_ipc_unique_id(uid) ? fl::make_ipc_transport(uid, rank, n_ranks, device)
+                                                        : fl::make_nccl_transport(uid, rank, n_ranks, device));
     });
     if (rc != FLUME_OK) {
         delete ctx;
