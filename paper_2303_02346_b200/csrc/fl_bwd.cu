@@ -204,8 +204,16 @@ void launch_adj_rigid(const Geom& g, BarBuf post, RigidDev rd, int nchunks, cons
 // ---------------------------------------------------------------------------
 // G2P adjoint (adjoint.hpp:281-365): gather + deterministic scatter of grid v_bar
 // ---------------------------------------------------------------------------
-template <bool HEAVY, int MINB>
-__global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+// NT threads: 256 stage the payload of a full block (8 particles x 64 cells) in two even
+// rounds (192 leave a third round two-thirds idle); the extra 64 idle in the accumulate
+// phase.  Measured: c4 109.9 -> 104.6 us, c3 283 -> 262 us (all three variants: with
+// 192 threads for the heavy blocks beside a liquid scene c4 keeps its 109.6 us -- those
+// few SVD blocks are the kernel's tail)
+#ifndef FL_ADJG2P_NT
+#define FL_ADJG2P_NT 256
+#endif
+template <bool HEAVY, int MINB, int NT>
+__global__ void __launch_bounds__(NT, MINB) k_adj_g2p(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                         const BlockRec* __restrict__ recs,
                                                         const int* __restrict__ n_blocks,
                                                         const uint16_t* __restrict__ celltab,
@@ -234,17 +242,17 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
         ts.begin(g, gridv, bx, by, bz, tid);
-        sc_tile_zero(sm, tid, kScThreads);
+        sc_tile_zero(sm, tid, NT);
         const int npass = sc_load_cells(sm, celltab, b, tid);
         // repack before the first pass: its prefix barrier orders these raw reads
         // before the payload writes into the same bytes
-        ts.end(g, gridv, vt, bx, by, bz, tid, kScThreads);
+        ts.end(g, gridv, vt, bx, by, bz, tid, NT);
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
             // every pass walks the dense list of the particles it stages (measured: the
             // sorted walk with idle lanes for ranks beyond the pass is slower here)
             const int lim = sc_overflow_prefix(sm, r0, tid);
-            for (int it = tid; it < lim; it += kScThreads) {
+            for (int it = tid; it < lim; it += NT) {
                 int c, rank;
                 sc_overflow_item(sm, it, c, rank);
                 const int i = int(sm.cs[c]) + r0 + rank;
@@ -406,19 +414,21 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_adj_g2p(Geom g, PBuf pre, 
                 for (int k = 0; k < 9; k++) pay[(6 + k) * kPayPlane] = bm.m[k];
             }
             __syncthreads();
-            const int nr = min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR);
-            sc_accumulate<3>(sm, my_c, my_ox, nr, tid, kScThreads);
+            const int nr = my_ox < 3 ? min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR) : 0;
+            sc_accumulate<3>(sm, my_c, my_ox, nr, tid, NT);
             __syncthreads();
         }
         __syncthreads();
-        sc_tile_store(sm, staging_bar + size_t(b) * kTile, tid, kScThreads);
+        sc_tile_store(sm, staging_bar + size_t(b) * kTile, tid, NT);
     }
 }
 
-static decltype(&k_adj_g2p<false, FL_LB_ADJG2P>) adj_g2p_kernel(int v) {
-    return v == 0 ? k_adj_g2p<false, FL_LB_ADJG2P>
-                  : (v == 1 ? k_adj_g2p<true, FL_LBH_ADJG2P> : k_adj_g2p<true, FL_LBD_ADJG2P>);
+static decltype(&k_adj_g2p<false, FL_LB_ADJG2P, FL_ADJG2P_NT>) adj_g2p_kernel(int v) {
+    return v == 0 ? k_adj_g2p<false, FL_LB_ADJG2P, FL_ADJG2P_NT>
+                  : (v == 1 ? k_adj_g2p<true, FL_LBH_ADJG2P, FL_ADJG2P_NT>
+                            : k_adj_g2p<true, FL_LBD_ADJG2P, FL_ADJG2P_NT>);
 }
+static int adj_g2p_threads(int) { return FL_ADJG2P_NT; }
 
 void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     const uint16_t* celltab, int grid, const ClassInfo* cls, const float4* gridv, PBuf postst,
@@ -430,7 +440,7 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
         cudaFuncSetAttribute(adj_g2p_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr[variant] = true;
     }
-    launch_k(adj_g2p_kernel(variant), dim3(grid), dim3(kScThreads), smem, s, g, pre, perm, recs, n_blocks, celltab,
+    launch_k(adj_g2p_kernel(variant), dim3(grid), dim3(adj_g2p_threads(variant)), smem, s, g, pre, perm, recs, n_blocks, celltab,
              cls, gridv, postst, post, xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
 }
 
@@ -951,7 +961,7 @@ int occupancy_grid(KGrid which, int variant) {
     if (which == KG_ADJ_G2P) {
         const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
         cudaFuncSetAttribute(adj_g2p_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_g2p_kernel(variant), kScThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_g2p_kernel(variant), adj_g2p_threads(variant), smem);
     } else {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_p2g_kernel(variant), 128, 0);
     }

@@ -164,8 +164,17 @@ void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, i
 // P2G (mpm.hpp:249-287)
 // ---------------------------------------------------------------------------
 
-template <bool HEAVY, int MINB>
-__global__ void __launch_bounds__(kScThreads, MINB) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
+// NT threads: 192 (64 cells x 3 planes) for the plain-liquid blocks, whose accumulate
+// phase dominates.  Variant 3: a few SVD/rigid blocks beside a liquid scene (fewer than
+// one per SM) are the kernel's tail, and their payload (a polar SVD per particle)
+// dominates, so they stage a full block in two even rounds of 256 threads (c4 76.8 ->
+// 73.1 us); with many such blocks (c5) 192 threads keep more of them in flight (256:
+// 444 -> 508 us), and SVD-dominated scenes (c3, variant 2) are even.
+#ifndef FL_P2G_NTH
+#define FL_P2G_NTH 256
+#endif
+template <bool HEAVY, int MINB, int NT>
+__global__ void __launch_bounds__(NT, MINB) k_p2g(Geom g, PBuf st, const uint32_t* __restrict__ perm,
                                                     const BlockRec* __restrict__ recs,
                                                     const int* __restrict__ n_blocks,
                                                     const uint16_t* __restrict__ celltab,
@@ -187,18 +196,18 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_p2g(Geom g, PBuf st, const
         __syncthreads();
         const int cnt = r.end - r.start;
         uint32_t s_nx = tid < cnt ? perm[r.start + tid] : 0u;  // overlaps the cell-table barrier
-        sc_tile_zero(sm, tid, kScThreads);
+        sc_tile_zero(sm, tid, NT);
         const int npass = sc_load_cells(sm, celltab, b, tid);
         for (int pass = 0; pass < npass; pass++) {
             const int r0 = pass * kScR;
             const int lim = pass == 0 ? cnt : sc_overflow_prefix(sm, r0, tid);
-            for (int it = tid; it < lim; it += kScThreads) {
+            for (int it = tid; it < lim; it += NT) {
                 int c, rank;
                 uint32_t s;
                 if (pass == 0) {  // every particle in sorted order (prefetching the permutation)
                     c = cell_of(sm.cs, it);
                     s = s_nx;
-                    if (it + kScThreads < cnt) s_nx = perm[r.start + it + kScThreads];
+                    if (it + NT < cnt) s_nx = perm[r.start + it + NT];
                     rank = it - int(sm.cs[c]);
                     if (rank >= kScR) continue;
                 } else {  // the dense list of the particles left for this pass
@@ -267,30 +276,36 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_p2g(Geom g, PBuf st, const
                 for (int k = 0; k < 9; k++) pay[(7 + k) * kPayPlane] = affine.m[k] * g.dx;
             }
             __syncthreads();
-            const int nr = min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR);
-            sc_accumulate<4>(sm, my_c, my_ox, nr, tid, kScThreads);
+            const int nr = my_ox < 3 ? min(max(int(sm.cs[my_c + 1]) - int(sm.cs[my_c]) - r0, 0), kScR) : 0;
+            sc_accumulate<4>(sm, my_c, my_ox, nr, tid, NT);
             __syncthreads();
         }
         __syncthreads();
-        sc_tile_store(sm, staging + size_t(b) * kTile, tid, kScThreads);
+        sc_tile_store(sm, staging + size_t(b) * kTile, tid, NT);
     }
 }
 
 // kernel variant: 0 plain liquid, 1 SVD/rigid blocks in a mostly-liquid scene (low
 // occupancy, runs beside the light kernel), 2 SVD/rigid-dominated scene
-static decltype(&k_p2g<false, FL_LB_P2G>) p2g_kernel(int v) {
-    return v == 0 ? k_p2g<false, FL_LB_P2G> : (v == 1 ? k_p2g<true, FL_LBH_P2G> : k_p2g<true, FL_LBD_P2G>);
+static decltype(&k_p2g<false, FL_LB_P2G, kScThreads>) p2g_kernel(int v) {
+    switch (v) {
+        case 0: return k_p2g<false, FL_LB_P2G, kScThreads>;
+        case 1: return k_p2g<true, FL_LBH_P2G, kScThreads>;
+        case 2: return k_p2g<true, FL_LBD_P2G, kScThreads>;
+        default: return k_p2g<true, FL_LBH_P2G, FL_P2G_NTH>;
+    }
 }
+static int p2g_threads(int v) { return v == 3 ? FL_P2G_NTH : kScThreads; }
 
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
                 uint32_t substep, int variant, int* wq, cudaStream_t s) {
-    static bool attr[3] = {false, false, false};
+    static bool attr[4] = {false, false, false, false};
     if (!attr[variant]) {
         cudaFuncSetAttribute(p2g_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
         attr[variant] = true;
     }
-    launch_k(p2g_kernel(variant), dim3(grid), dim3(kScThreads), sizeof(ScSmem), s, g, st, perm, recs, n_blocks,
+    launch_k(p2g_kernel(variant), dim3(grid), dim3(p2g_threads(variant)), sizeof(ScSmem), s, g, st, perm, recs, n_blocks,
              celltab, cls, staging, err, substep, wq);
 }
 
@@ -713,7 +728,7 @@ int occupancy_grid_fwd(KGrid which, int variant) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (which == KG_P2G) {
         cudaFuncSetAttribute(p2g_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_kernel(variant), kScThreads, sizeof(ScSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_kernel(variant), p2g_threads(variant), sizeof(ScSmem));
     } else {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_kernel(variant), 128, 0);
     }

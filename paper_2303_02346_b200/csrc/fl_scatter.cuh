@@ -14,7 +14,13 @@
 
 namespace fl {
 
-constexpr int kScThreads = 192;  // 64 cells x 3 planes
+// threads per scatter CTA: 64 cells x 3 planes accumulate; more threads (FL_SC_THREADS =
+// 256) only widen the payload phase (the extra ones idle in the accumulate phase)
+#ifndef FL_SC_THREADS
+#define FL_SC_THREADS 192
+#endif
+constexpr int kScThreads = FL_SC_THREADS;
+static_assert(kScThreads >= 192 && kScThreads % 64 == 0, "scatter CTA: 64 cells x 3 planes at least");
 
 // resident CTAs per SM requested from ptxas for the plain-liquid variants (register caps)
 #ifndef FL_LB_P2G
@@ -24,7 +30,7 @@ constexpr int kScThreads = 192;  // 64 cells x 3 planes
 #define FL_LB_G2P 8
 #endif
 #ifndef FL_LB_ADJG2P
-#define FL_LB_ADJG2P 5
+#define FL_LB_ADJG2P 4  // (256-thread CTAs: 64 registers)
 #endif
 #ifndef FL_LB_ADJP2G
 #define FL_LB_ADJP2G 5
@@ -50,7 +56,7 @@ constexpr int kScThreads = 192;  // 64 cells x 3 planes
 #define FL_LBD_G2P 6
 #endif
 #ifndef FL_LBD_ADJG2P
-#define FL_LBD_ADJG2P 4
+#define FL_LBD_ADJG2P 3  // (256-thread CTAs)
 #endif
 #ifndef FL_LBD_ADJP2G
 #define FL_LBD_ADJP2G 5
@@ -163,8 +169,9 @@ __device__ __forceinline__ void sc_accumulate(ScSmem& sm, int c, int ox, int nra
     // fold: partial sums -> shared memory -> per-node fixed-order gather
     float4* part = reinterpret_cast<float4*>(sm.pay);  // [64 cells][3 planes][9 nodes]
     __syncthreads();                                   // the payload has been read
+    if (ox < 3)
 #pragma unroll
-    for (int k = 0; k < 9; k++) part[(c * 3 + ox) * 9 + k] = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
+        for (int k = 0; k < 9; k++) part[(c * 3 + ox) * 9 + k] = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
     __syncthreads();
     for (int t = tid; t < int(kTile); t += nthreads) {
         const int X = t / 36, Y = (t / 6) % 6, Z = t % 6;
