@@ -425,8 +425,8 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_g2p(Geom g, PBuf pre, const ui
 
 static decltype(&k_adj_g2p<false, FL_LB_ADJG2P, FL_ADJG2P_NT>) adj_g2p_kernel(int v) {
     return v == 0 ? k_adj_g2p<false, FL_LB_ADJG2P, FL_ADJG2P_NT>
-                  : (v == 1 ? k_adj_g2p<true, FL_LBH_ADJG2P, FL_ADJG2P_NT>
-                            : k_adj_g2p<true, FL_LBD_ADJG2P, FL_ADJG2P_NT>);
+                  : (v == 2 ? k_adj_g2p<true, FL_LBD_ADJG2P, FL_ADJG2P_NT>
+                            : k_adj_g2p<true, FL_LBH_ADJG2P, FL_ADJG2P_NT>);  // (1 and 3)
 }
 static int adj_g2p_threads(int) { return FL_ADJG2P_NT; }
 
@@ -435,7 +435,7 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     BarBuf post, float* xbar_tmp, float* Fbar_tmp, RigidDev rd, const float* start_bar,
                     float4* staging_bar, int variant, int* wq, cudaStream_t s) {
     const size_t smem = sizeof(ScSmem) + kTile * sizeof(float4);
-    static bool attr[3] = {false, false, false};
+    static bool attr[4] = {false, false, false, false};
     if (!attr[variant]) {
         cudaFuncSetAttribute(adj_g2p_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr[variant] = true;
@@ -629,8 +629,14 @@ void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int c
 // ---------------------------------------------------------------------------
 // P2G adjoint (adjoint.hpp:414-470)
 // ---------------------------------------------------------------------------
-template <bool HEAVY, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
+// a few SVD/rigid P2G-adjoint blocks beside a liquid scene (variant 3) in 256-thread CTAs:
+// their stress VJP per particle makes them the dual launch's tail, and a full block then
+// takes two rounds instead of four (c4 92.8 -> 82.4 us; c5's many such blocks: variant 1)
+#ifndef FL_ADJP2G_NTH
+#define FL_ADJP2G_NTH 256
+#endif
+template <bool HEAVY, int MINB, int NT = 128>
+__global__ void __launch_bounds__(NT, MINB) k_adj_p2g(Geom g, PBuf pre, const uint32_t* __restrict__ perm,
                                                  const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                                  const ClassInfo* __restrict__ cls,
                                                  const float4* __restrict__ gridbar,
@@ -654,11 +660,11 @@ __global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const u
         block_unlin(g, r.block, bx, by, bz);
         ts.begin(g, gridbar, bx, by, bz, tid);
         uint32_t s_nx = r.start + tid < r.end ? perm[r.start + tid] : 0u;  // see k_g2p
-        ts.end(g, gridbar, bt, bx, by, bz, tid, 128);
+        ts.end(g, gridbar, bt, bx, by, bz, tid, NT);
         __syncthreads();
-        for (int j = r.start + tid; j < r.end; j += 128) {
+        for (int j = r.start + tid; j < r.end; j += NT) {
             const uint32_t s = s_nx;
-            if (j + 128 < r.end) s_nx = perm[j + 128];
+            if (j + NT < r.end) s_nx = perm[j + NT];
             const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
             const V3<float> v = {pre.v(0)[s], pre.v(1)[s], pre.v(2)[s]};
             const uint32_t pmeta = pre.meta[s];
@@ -804,14 +810,19 @@ __global__ void __launch_bounds__(128, MINB) k_adj_p2g(Geom g, PBuf pre, const u
 }
 
 static decltype(&k_adj_p2g<false, FL_LB_ADJP2G>) adj_p2g_kernel(int v) {
-    return v == 0 ? k_adj_p2g<false, FL_LB_ADJP2G>
-                  : (v == 1 ? k_adj_p2g<true, FL_LBH_ADJP2G> : k_adj_p2g<true, FL_LBD_ADJP2G>);
+    switch (v) {
+        case 0: return k_adj_p2g<false, FL_LB_ADJP2G>;
+        case 1: return k_adj_p2g<true, FL_LBH_ADJP2G>;
+        case 2: return k_adj_p2g<true, FL_LBD_ADJP2G>;
+        default: return k_adj_p2g<true, FL_LBF_ADJP2G, FL_ADJP2G_NTH>;
+    }
 }
+static int adj_p2g_threads(int v) { return v == 3 ? FL_ADJP2G_NTH : 128; }
 
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, int variant, int* wq, cudaStream_t s) {
-    launch_k(adj_p2g_kernel(variant), dim3(grid), dim3(128), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar,
+    launch_k(adj_p2g_kernel(variant), dim3(grid), dim3(adj_p2g_threads(variant)), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar,
              xbar_tmp, Fbar_tmp, out, nonfinite, out.cap, wq);
 }
 
@@ -963,7 +974,7 @@ int occupancy_grid(KGrid which, int variant) {
         cudaFuncSetAttribute(adj_g2p_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_g2p_kernel(variant), adj_g2p_threads(variant), smem);
     } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_p2g_kernel(variant), 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adj_p2g_kernel(variant), adj_p2g_threads(variant), 0);
     }
     if (per < 1) per = 1;
     return sms * per;

@@ -382,8 +382,7 @@ struct Ctx {
     DevArr<uint32_t> d_upmeta;
     DevArr<uint8_t> d_upactive;
     DevArr<float> d_x0;  // [3][N] positions by particle id at upload (LossSet.x0)
-    int hvar = 1;  // heavy kernel variant (occupancy_grid)
-    int pvar = 1;  // P2G's heavy variant (3: few SVD blocks, 256 threads)
+    int hvar = 1;  // heavy kernel variant (occupancy_grid): 1 beside liquid, 2 dominant, 3 few beside liquid
     int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
     int eff_blocks = kEffBlocks;
     int grid_p2g_h = 0, grid_g2p_h = 0, grid_adj_h = 0, grid_ap = 0, grid_ap_h = 0;
@@ -831,13 +830,14 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
         for (int i = 0; i < N; i++) nh += classes[p_class[i]].heavy;
         classes_heavy = nh > 0;
         hvar = 2 * nh >= N ? 2 : 1;
-        // P2G: fewer SVD/rigid blocks than SMs beside a liquid scene -> the 256-thread variant
+        // fewer SVD/rigid blocks than SMs beside a liquid scene (c4's floater): they are the
+        // dual launches' tail -> variant 3, 256-thread CTAs (a full block in fewer rounds)
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        pvar = (hvar == 1 && nh < long(nsm) * 512) ? 3 : hvar;
+        if (hvar == 1 && nh < long(nsm) * 512) hvar = 3;
     }
     grid_p2g = occupancy_grid(KG_P2G, 0);
-    grid_p2g_h = occupancy_grid(KG_P2G, pvar);
+    grid_p2g_h = occupancy_grid(KG_P2G, hvar);
     grid_g2p = occupancy_grid(KG_G2P, 0);
     grid_g2p_h = occupancy_grid(KG_G2P, hvar);
     grid_adj = occupancy_grid(KG_ADJ_G2P, 0);
@@ -1343,7 +1343,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     PROF(K_SORT, sort_and_lists(*in, r));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
-                        staging.p, d_err.p, uint32_t(substep_index), hv ? pvar : 0, w, s);
+                        staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     if (slab()) {
         PROF(K_COMM, halo_exchange(r.blockmap, staging.p, nbflag));
@@ -1427,7 +1427,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
     EffSet es = make_effset(eff);
     dual([&](bool hv, int* w, cudaStream_t s) {
         launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
-                   staging.p, d_err.p, uint32_t(substep_index), hv ? pvar : 0, w, s);
+                   staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
     });
     if (slab()) {
         halo_exchange(r.blockmap, staging.p, nbflag);

@@ -390,8 +390,14 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 // G2P (mpm.hpp:338-384) with the per-material return map
 // ---------------------------------------------------------------------------
 
-template <bool HEAVY, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
+// a few SVD/rigid G2P blocks beside a liquid scene (variant 3) in 256-thread CTAs: a full
+// block in two rounds instead of four (c4 42.7 -> 40.1 us; with many such blocks, c5,
+// 128 threads keep more of them in flight: variant 1)
+#ifndef FL_G2P_NTH
+#define FL_G2P_NTH 256
+#endif
+template <bool HEAVY, int MINB, int NT = 128>
+__global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
                                              RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {
@@ -422,18 +428,18 @@ __global__ void __launch_bounds__(128, MINB) k_g2p(Geom g, PBuf in, PBuf out, co
             x_nx = V3<float>{in.x(0)[s_nx], in.x(1)[s_nx], in.x(2)[s_nx]};
             meta_nx = in.meta[s_nx];
         }
-        uint32_t s_nx2 = j0 + 128 < r.end ? perm[j0 + 128] : 0u;
-        ts.end(g, gridv, vt, bx, by, bz, tid, 128);
+        uint32_t s_nx2 = j0 + NT < r.end ? perm[j0 + NT] : 0u;
+        ts.end(g, gridv, vt, bx, by, bz, tid, NT);
         __syncthreads();
-        for (int j = j0; j < r.end; j += 128) {
+        for (int j = j0; j < r.end; j += NT) {
             const uint32_t s = s_nx;
             const V3<float> x = x_nx;
             const uint32_t meta = meta_nx;
-            if (j + 128 < r.end) {
+            if (j + NT < r.end) {
                 s_nx = s_nx2;
                 x_nx = V3<float>{in.x(0)[s_nx], in.x(1)[s_nx], in.x(2)[s_nx]};
                 meta_nx = in.meta[s_nx];
-                if (j + 256 < r.end) s_nx2 = perm[j + 256];
+                if (j + 2 * NT < r.end) s_nx2 = perm[j + 2 * NT];
             }
             const uint32_t pid = in.id[s];
             const ClassInfo ci = cls[meta_cls(meta)];
@@ -513,13 +519,19 @@ __global__ void __launch_bounds__(128, MINB) k_g2p(Geom g, PBuf in, PBuf out, co
 }
 
 static decltype(&k_g2p<false, FL_LB_G2P>) g2p_kernel(int v) {
-    return v == 0 ? k_g2p<false, FL_LB_G2P> : (v == 1 ? k_g2p<true, FL_LBH_G2P> : k_g2p<true, FL_LBD_G2P>);
+    switch (v) {
+        case 0: return k_g2p<false, FL_LB_G2P>;
+        case 1: return k_g2p<true, FL_LBH_G2P>;
+        case 2: return k_g2p<true, FL_LBD_G2P>;
+        default: return k_g2p<true, FL_LBF_G2P, FL_G2P_NTH>;
+    }
 }
+static int g2p_threads(int v) { return v == 3 ? FL_G2P_NTH : 128; }
 
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd, unsigned long long* err,
                 uint32_t substep, int variant, int* wq, cudaStream_t s) {
-    launch_k(g2p_kernel(variant), dim3(grid), dim3(128), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err,
+    launch_k(g2p_kernel(variant), dim3(grid), dim3(g2p_threads(variant)), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err,
              substep, wq);
 }
 
@@ -730,7 +742,7 @@ int occupancy_grid_fwd(KGrid which, int variant) {
         cudaFuncSetAttribute(p2g_kernel(variant), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ScSmem)));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p2g_kernel(variant), p2g_threads(variant), sizeof(ScSmem));
     } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_kernel(variant), 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, g2p_kernel(variant), g2p_threads(variant), 0);
     }
     if (per < 1) per = 1;
     return sms * per;

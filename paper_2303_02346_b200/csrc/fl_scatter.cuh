@@ -48,6 +48,14 @@ static_assert(kScThreads >= 192 && kScThreads % 64 == 0, "scatter CTA: 64 cells 
 #ifndef FL_LBH_ADJP2G
 #define FL_LBH_ADJP2G 3
 #endif
+// ... and for a few SVD/rigid blocks (fewer than the SMs) beside a liquid scene (variant 3):
+// 256-thread CTAs for the thread-per-particle kernels, 128 registers
+#ifndef FL_LBF_G2P
+#define FL_LBF_G2P 2
+#endif
+#ifndef FL_LBF_ADJP2G
+#define FL_LBF_ADJP2G 2
+#endif
 // ... and for the heavy variants when SVD/rigid blocks dominate the scene (launcher variant 2)
 #ifndef FL_LBD_P2G
 #define FL_LBD_P2G 4
