@@ -629,6 +629,192 @@ void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int c
 // ---------------------------------------------------------------------------
 // P2G adjoint (adjoint.hpp:414-470)
 // ---------------------------------------------------------------------------
+// pre-state / partial sources of adj_p2g_particle
+struct AdjP2gGlobal {
+    const PBuf& pre;
+    const float* __restrict__ xbar_tmp;
+    const float* __restrict__ Fbar_tmp;
+    uint32_t s;
+    int j, cap;
+    __device__ float x(int a) const { return pre.x(a)[s]; }
+    __device__ float v(int a) const { return pre.v(a)[s]; }
+    __device__ uint32_t meta() const { return pre.meta[s]; }
+    __device__ float C(int k) const { return pre.C(k)[s]; }
+    __device__ float F(int k) const { return pre.F(k)[s]; }
+    __device__ float xbar(int a) const { return xbar_tmp[size_t(a) * cap + j]; }
+    __device__ float fbar(int k) const { return Fbar_tmp[size_t(k) * cap + j]; }
+};
+// plain-liquid staging: 21 fields per particle, [field][particle] in shared memory
+constexpr int kAp2gF = 21;  // x3 v3 meta C9 c xbar3 cbar
+#ifndef FL_ADJP2G_STAGE
+#define FL_ADJP2G_STAGE 1
+#endif
+struct AdjP2gStaged {
+    const float* sp;  // [kAp2gF][n]
+    int k, n;
+    __device__ float f(int q) const { return sp[q * n + k]; }
+    __device__ float x(int a) const { return f(a); }
+    __device__ float v(int a) const { return f(3 + a); }
+    __device__ uint32_t meta() const { return __float_as_uint(f(6)); }
+    __device__ float C(int q) const { return f(7 + q); }
+    __device__ float F(int) const { return f(16); }  // (compact: c)
+    __device__ float xbar(int a) const { return f(17 + a); }
+    __device__ float fbar(int) const { return f(20); }
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+// the P2G adjoint of one particle (adjoint.hpp:414-470): stress recompute + VJP, gather of
+// (p_bar, m_bar) from the block's tile `bt`, bars written at storage slot s.  Src supplies
+// the pre-state fields and the G2P adjoint's x_bar / F_bar partials (global memory through
+// the permutation, or the CTA's cp.async staging).
+template <bool HEAVY, class Src>
+__device__ __forceinline__ void adj_p2g_particle(const Geom& g, const Src& src, uint32_t s,
+                                                 const ClassInfo* __restrict__ cls, const float4* bt, int bx, int by,
+                                                 int bz, BarBuf out, int* nonfinite) {
+        const V3<float> x = {src.x(0), src.x(1), src.x(2)};
+        const V3<float> v = {src.v(0), src.v(1), src.v(2)};
+        const uint32_t pmeta = src.meta();
+        const ClassInfo ci = cls[meta_cls(pmeta)];
+        const bool cin = !HEAVY || f_compact(ci, pmeta);     // F = c I, F_bar stored as dL/dc
+        const bool pressure = !HEAVY || (cin && ci.kind == MK_LIQUID);  // stress_mat = s(c) I
+        M3<float> F, C;
+#pragma unroll
+        for (int k = 0; k < 9; k++) C.m[k] = src.C(k);
+        if (cin) {
+            F = meye<float>() * src.F(0);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 9; k++) F.m[k] = src.F(k);
+        }
+        const float cc = g.stress_coeff * ci.vol0;
+        const bool visc = HEAVY && ci.kind == MK_VISCOUS;
+        const M3<float> ipc = meye<float>() + C * g.dt;
+        M3<float> fs, P, affine = C * ci.mass;
+        Svd<float> t;
+        if (pressure) {  // lambda (J - 1) J I with J = c^3
+            const float c = F.m[0], jj = c * c * c;
+            const float sm = ci.lambda * (jj - 1.f) * jj * cc;
+            affine.m[0] -= sm;
+            affine.m[4] -= sm;
+            affine.m[8] -= sm;
+        } else {
+            fs = visc ? ipc * F : F;
+            bool ok;
+            P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
+            affine -= (P * transpose(fs)) * cc;
+        }
+        StencilW sw;
+        stencil_weights(g, x, bx, by, bz, sw);
+        const V3<float> mv = v * ci.mass;
+        V3<float> xb = {0.f, 0.f, 0.f}, vbsum = {0.f, 0.f, 0.f};
+        M3<float> ab = mzero<float>();
+        float wsum_p[3] = {0.f, 0.f, 0.f};
+        {
+            // contrib_o = mv + affine rel_o with rel_o = dx (o - fx) split per axis;
+            // grad-w products accumulated per x-plane; A_bar = sum_o w_o p_bar_o rel_o^T
+            // gathered column-wise (x column through the per-plane sum).
+            V3<float> ay[3], az[3];
+            float ry[3], rz[3];
+#pragma unroll
+            for (int o = 0; o < 3; o++) {
+                ry[o] = (float(o) - sw.fx[1]) * g.dx;
+                rz[o] = (float(o) - sw.fx[2]) * g.dx;
+                ay[o] = V3<float>{affine.m[1] * ry[o], affine.m[4] * ry[o], affine.m[7] * ry[o]};
+                az[o] = V3<float>{affine.m[2] * rz[o], affine.m[5] * rz[o], affine.m[8] * rz[o]};
+            }
+            const float mm = ci.mass;
+            const float wrz[3] = {sw.w[2][0] * rz[0], sw.w[2][1] * rz[1], sw.w[2][2] * rz[2]};
+            float sxx = 0.f, syy = 0.f, szz = 0.f;
+#pragma unroll 1
+            for (int ox = 0; ox < 3; ox++) {
+                const float wox = ox == 0 ? sw.w[0][0] : (ox == 1 ? sw.w[0][1] : sw.w[0][2]);
+                const float dox = ox == 0 ? sw.dw[0][0] : (ox == 1 ? sw.dw[0][1] : sw.dw[0][2]);
+                const float rx = (float(ox) - sw.fx[0]) * g.dx;
+                const V3<float> ax = {mv.x + affine.m[0] * rx, mv.y + affine.m[3] * rx, mv.z + affine.m[6] * rx};
+                float px = 0.f, py = 0.f, pz = 0.f;
+                V3<float> tx = {0.f, 0.f, 0.f};
+                const float4* row = bt + (sw.l[0] + ox) * 36 + sw.l[1] * 6 + sw.l[2];
+#pragma unroll
+                for (int oy = 0; oy < 3; oy++) {
+                    const V3<float> axy = ax + ay[oy];
+                    // per (x, y) column: z-weighted sums, then one scaling by the x/y weights
+                    float sa = 0.f, sb = 0.f;
+                    V3<float> tz = {0.f, 0.f, 0.f}, tzr = {0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int oz = 0; oz < 3; oz++) {
+                        const float4 b4 = row[oy * 6 + oz];
+                        const V3<float> u = axy + az[oz];
+                        const float sv = b4.w * mm + b4.x * u.x + b4.y * u.y + b4.z * u.z;
+                        sa += sw.w[2][oz] * sv;
+                        sb += sw.dw[2][oz] * sv;
+                        tz += V3<float>{b4.x, b4.y, b4.z} * sw.w[2][oz];
+                        tzr += V3<float>{b4.x, b4.y, b4.z} * wrz[oz];
+                    }
+                    px += sw.w[1][oy] * sa;
+                    py += sw.dw[1][oy] * sa;
+                    pz += sw.w[1][oy] * sb;
+                    const float wxy = wox * sw.w[1][oy];
+                    const V3<float> wob = tz * wxy;
+                    tx += wob;
+                    ab.m[1] += wob.x * ry[oy]; ab.m[4] += wob.y * ry[oy]; ab.m[7] += wob.z * ry[oy];
+                    ab.m[2] += tzr.x * wxy; ab.m[5] += tzr.y * wxy; ab.m[8] += tzr.z * wxy;
+                }
+                sxx += dox * px;
+                syy += wox * py;
+                szz += wox * pz;
+                ab.m[0] += tx.x * rx; ab.m[3] += tx.y * rx; ab.m[6] += tx.z * rx;
+                wsum_p[0] += tx.x;
+                wsum_p[1] += tx.y;
+                wsum_p[2] += tx.z;
+            }
+            xb = V3<float>{sxx * g.inv_dx, syy * g.inv_dx, szz * g.inv_dx};
+        }
+        const V3<float> wp = {wsum_p[0], wsum_p[1], wsum_p[2]};
+        xb -= tmul(affine, wp);
+        vbsum = wp * ci.mass;
+        const M3<float> sm_bar = ab * (-cc);
+        M3<float> Fb, Cb = ab * ci.mass;
+        float c_bar = 0.f;  // dL/dc for a compact F
+        if (pressure) {
+            // d/dc [lambda (c^6 - c^3)] tr(sm_bar) = 3 lambda c^2 (2J - 1) tr(sm_bar)
+            const float c = F.m[0], jj = c * c * c;
+            c_bar = src.fbar(0) + 3.f * ci.lambda * c * c * (2.f * jj - 1.f) * trace(sm_bar);
+        } else {
+            const M3<float> p_bar = sm_bar * fs;
+            M3<float> fs_bar = transpose(sm_bar) * P;
+            fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
+            M3<float> fb_add = fs_bar;
+            if (visc) {
+                fb_add = transpose(ipc) * fs_bar;
+                Cb += fs_bar * transpose(F) * g.dt;
+            }
+            if (cin) {
+                c_bar = src.fbar(0) + trace(fb_add);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; k++) Fb.m[k] = src.fbar(k) + fb_add.m[k];
+            }
+        }
+        const float xo[3] = {src.xbar(0) + xb.x, src.xbar(1) + xb.y, src.xbar(2) + xb.z};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            out.x(a)[s] = xo[a];
+            out.v(a)[s] = vbsum[a];
+        }
+#pragma unroll
+        for (int k = 0; k < 9; k++) out.C(k)[s] = Cb.m[k];
+        if (cin) {
+            out.F(0)[s] = c_bar;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 9; k++) out.F(k)[s] = Fb.m[k];
+        }
+        if (!isfinite(xo[0]) || !isfinite(vbsum.x) || !isfinite(cin ? c_bar : Fb.m[0])) atomicOr(nonfinite, 1);
+}
+
 // a few SVD/rigid P2G-adjoint blocks beside a liquid scene (variant 3) in 256-thread CTAs:
 // their stress VJP per particle makes them the dual launch's tail, and a full block then
 // takes two rounds instead of four (c4 92.8 -> 82.4 us; c5's many such blocks: variant 1)
@@ -647,6 +833,9 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_p2g(Geom g, PBuf pre, const ui
     __shared__ float4 bt[kTile];
     __shared__ __align__(128) float4 raw[FL_TMA_TILE ? kTileRaw : 1];
     __shared__ __align__(8) uint64_t bar;
+    constexpr int kStageBuf = (!HEAVY && FL_ADJP2G_STAGE) ? 2 * NT : 1;
+    __shared__ __align__(16) float sp[kAp2gF * kStageBuf];
+    __shared__ uint32_t ps[kStageBuf];
     const int tid = threadIdx.x;
     TileStage ts;
     ts.init(&bar, raw, tid);
@@ -659,155 +848,50 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_p2g(Geom g, PBuf pre, const ui
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
         ts.begin(g, gridbar, bx, by, bz, tid);
-        uint32_t s_nx = r.start + tid < r.end ? perm[r.start + tid] : 0u;  // see k_g2p
+        uint32_t s_nx = (HEAVY || !FL_ADJP2G_STAGE) && r.start + tid < r.end ? perm[r.start + tid] : 0u;  // see k_g2p
         ts.end(g, gridbar, bt, bx, by, bz, tid, NT);
         __syncthreads();
-        for (int j = r.start + tid; j < r.end; j += NT) {
-            const uint32_t s = s_nx;
-            if (j + NT < r.end) s_nx = perm[j + NT];
-            const V3<float> x = {pre.x(0)[s], pre.x(1)[s], pre.x(2)[s]};
-            const V3<float> v = {pre.v(0)[s], pre.v(1)[s], pre.v(2)[s]};
-            const uint32_t pmeta = pre.meta[s];
-            const ClassInfo ci = cls[meta_cls(pmeta)];
-            const bool cin = !HEAVY || f_compact(ci, pmeta);     // F = c I, F_bar stored as dL/dc
-            const bool pressure = !HEAVY || (cin && ci.kind == MK_LIQUID);  // stress_mat = s(c) I
-            M3<float> F, C;
+        if constexpr (!HEAVY && FL_ADJP2G_STAGE) {
+            // plain liquids: chunks of kStage particles -- every thread issues cp.async
+            // copies of its particles' 21 fields (independent loads, no register round trip,
+            // no perm -> state dependency per use), then the chunk computes from shared memory
+            constexpr int kStage = 2 * NT;
+            for (int c0 = r.start; c0 < r.end; c0 += kStage) {
+                const int cn = min(kStage, r.end - c0);
+                __syncthreads();  // the previous chunk's reads are done
+                for (int k = tid; k < cn; k += NT) {
+                    const int j = c0 + k;
+                    const uint32_t s = perm[j];
+                    ps[k] = s;
 #pragma unroll
-            for (int k = 0; k < 9; k++) C.m[k] = pre.C(k)[s];
-            if (cin) {
-                F = meye<float>() * pre.F(0)[s];
-            } else {
-#pragma unroll
-                for (int k = 0; k < 9; k++) F.m[k] = pre.F(k)[s];
-            }
-            const float cc = g.stress_coeff * ci.vol0;
-            const bool visc = HEAVY && ci.kind == MK_VISCOUS;
-            const M3<float> ipc = meye<float>() + C * g.dt;
-            M3<float> fs, P, affine = C * ci.mass;
-            Svd<float> t;
-            if (pressure) {  // lambda (J - 1) J I with J = c^3
-                const float c = F.m[0], jj = c * c * c;
-                const float sm = ci.lambda * (jj - 1.f) * jj * cc;
-                affine.m[0] -= sm;
-                affine.m[4] -= sm;
-                affine.m[8] -= sm;
-            } else {
-                fs = visc ? ipc * F : F;
-                bool ok;
-                P = corotated_stress_svd(fs, ci.mu, ci.lambda, ok, t);
-                affine -= (P * transpose(fs)) * cc;
-            }
-            StencilW sw;
-            stencil_weights(g, x, bx, by, bz, sw);
-            const V3<float> mv = v * ci.mass;
-            V3<float> xb = {0.f, 0.f, 0.f}, vbsum = {0.f, 0.f, 0.f};
-            M3<float> ab = mzero<float>();
-            float wsum_p[3] = {0.f, 0.f, 0.f};
-            {
-                // contrib_o = mv + affine rel_o with rel_o = dx (o - fx) split per axis;
-                // grad-w products accumulated per x-plane; A_bar = sum_o w_o p_bar_o rel_o^T
-                // gathered column-wise (x column through the per-plane sum).
-                V3<float> ay[3], az[3];
-                float ry[3], rz[3];
-#pragma unroll
-                for (int o = 0; o < 3; o++) {
-                    ry[o] = (float(o) - sw.fx[1]) * g.dx;
-                    rz[o] = (float(o) - sw.fx[2]) * g.dx;
-                    ay[o] = V3<float>{affine.m[1] * ry[o], affine.m[4] * ry[o], affine.m[7] * ry[o]};
-                    az[o] = V3<float>{affine.m[2] * rz[o], affine.m[5] * rz[o], affine.m[8] * rz[o]};
-                }
-                const float mm = ci.mass;
-                const float wrz[3] = {sw.w[2][0] * rz[0], sw.w[2][1] * rz[1], sw.w[2][2] * rz[2]};
-                float sxx = 0.f, syy = 0.f, szz = 0.f;
-#pragma unroll 1
-                for (int ox = 0; ox < 3; ox++) {
-                    const float wox = ox == 0 ? sw.w[0][0] : (ox == 1 ? sw.w[0][1] : sw.w[0][2]);
-                    const float dox = ox == 0 ? sw.dw[0][0] : (ox == 1 ? sw.dw[0][1] : sw.dw[0][2]);
-                    const float rx = (float(ox) - sw.fx[0]) * g.dx;
-                    const V3<float> ax = {mv.x + affine.m[0] * rx, mv.y + affine.m[3] * rx, mv.z + affine.m[6] * rx};
-                    float px = 0.f, py = 0.f, pz = 0.f;
-                    V3<float> tx = {0.f, 0.f, 0.f};
-                    const float4* row = bt + (sw.l[0] + ox) * 36 + sw.l[1] * 6 + sw.l[2];
-#pragma unroll
-                    for (int oy = 0; oy < 3; oy++) {
-                        const V3<float> axy = ax + ay[oy];
-                        // per (x, y) column: z-weighted sums, then one scaling by the x/y weights
-                        float sa = 0.f, sb = 0.f;
-                        V3<float> tz = {0.f, 0.f, 0.f}, tzr = {0.f, 0.f, 0.f};
-#pragma unroll
-                        for (int oz = 0; oz < 3; oz++) {
-                            const float4 b4 = row[oy * 6 + oz];
-                            const V3<float> u = axy + az[oz];
-                            const float sv = b4.w * mm + b4.x * u.x + b4.y * u.y + b4.z * u.z;
-                            sa += sw.w[2][oz] * sv;
-                            sb += sw.dw[2][oz] * sv;
-                            tz += V3<float>{b4.x, b4.y, b4.z} * sw.w[2][oz];
-                            tzr += V3<float>{b4.x, b4.y, b4.z} * wrz[oz];
-                        }
-                        px += sw.w[1][oy] * sa;
-                        py += sw.dw[1][oy] * sa;
-                        pz += sw.w[1][oy] * sb;
-                        const float wxy = wox * sw.w[1][oy];
-                        const V3<float> wob = tz * wxy;
-                        tx += wob;
-                        ab.m[1] += wob.x * ry[oy]; ab.m[4] += wob.y * ry[oy]; ab.m[7] += wob.z * ry[oy];
-                        ab.m[2] += tzr.x * wxy; ab.m[5] += tzr.y * wxy; ab.m[8] += tzr.z * wxy;
+                    for (int a = 0; a < 3; a++) {
+                        cp_async4(&sp[a * kStage + k], pre.x(a) + s);
+                        cp_async4(&sp[(3 + a) * kStage + k], pre.v(a) + s);
+                        cp_async4(&sp[(17 + a) * kStage + k], xbar_tmp + size_t(a) * cap + j);
                     }
-                    sxx += dox * px;
-                    syy += wox * py;
-                    szz += wox * pz;
-                    ab.m[0] += tx.x * rx; ab.m[3] += tx.y * rx; ab.m[6] += tx.z * rx;
-                    wsum_p[0] += tx.x;
-                    wsum_p[1] += tx.y;
-                    wsum_p[2] += tx.z;
+                    cp_async4(&sp[6 * kStage + k], pre.meta + s);
+#pragma unroll
+                    for (int q = 0; q < 9; q++) cp_async4(&sp[(7 + q) * kStage + k], pre.C(q) + s);
+                    cp_async4(&sp[16 * kStage + k], pre.F(0) + s);
+                    cp_async4(&sp[20 * kStage + k], Fbar_tmp + j);
                 }
-                xb = V3<float>{sxx * g.inv_dx, syy * g.inv_dx, szz * g.inv_dx};
+                asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+                __syncthreads();
+                for (int k = tid; k < cn; k += NT)
+                    adj_p2g_particle<HEAVY>(g, AdjP2gStaged{sp, k, kStage}, ps[k], cls, bt, bx, by, bz, out,
+                                            nonfinite);
             }
-            const V3<float> wp = {wsum_p[0], wsum_p[1], wsum_p[2]};
-            xb -= tmul(affine, wp);
-            vbsum = wp * ci.mass;
-            const M3<float> sm_bar = ab * (-cc);
-            M3<float> Fb, Cb = ab * ci.mass;
-            float c_bar = 0.f;  // dL/dc for a compact F
-            if (pressure) {
-                // d/dc [lambda (c^6 - c^3)] tr(sm_bar) = 3 lambda c^2 (2J - 1) tr(sm_bar)
-                const float c = F.m[0], jj = c * c * c;
-                c_bar = Fbar_tmp[j] + 3.f * ci.lambda * c * c * (2.f * jj - 1.f) * trace(sm_bar);
-            } else {
-                const M3<float> p_bar = sm_bar * fs;
-                M3<float> fs_bar = transpose(sm_bar) * P;
-                fs_bar += corotated_stress_vjp(fs, ci.mu, ci.lambda, p_bar, t);
-                M3<float> fb_add = fs_bar;
-                if (visc) {
-                    fb_add = transpose(ipc) * fs_bar;
-                    Cb += fs_bar * transpose(F) * g.dt;
-                }
-                if (cin) {
-                    c_bar = Fbar_tmp[j] + trace(fb_add);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 9; k++) Fb.m[k] = Fbar_tmp[size_t(k) * cap + j] + fb_add.m[k];
-                }
+        } else {
+            for (int j = r.start + tid; j < r.end; j += NT) {
+                const uint32_t s = s_nx;
+                if (j + NT < r.end) s_nx = perm[j + NT];
+                adj_p2g_particle<HEAVY>(g, AdjP2gGlobal{pre, xbar_tmp, Fbar_tmp, s, j, cap}, s, cls, bt, bx, by, bz,
+                                        out, nonfinite);
             }
-            const float xo[3] = {xbar_tmp[j] + xb.x, xbar_tmp[size_t(cap) + j] + xb.y,
-                                 xbar_tmp[2 * size_t(cap) + j] + xb.z};
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-                out.x(a)[s] = xo[a];
-                out.v(a)[s] = vbsum[a];
-            }
-#pragma unroll
-            for (int k = 0; k < 9; k++) out.C(k)[s] = Cb.m[k];
-            if (cin) {
-                out.F(0)[s] = c_bar;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 9; k++) out.F(k)[s] = Fb.m[k];
-            }
-            if (!isfinite(xo[0]) || !isfinite(vbsum.x) || !isfinite(cin ? c_bar : Fb.m[0])) atomicOr(nonfinite, 1);
         }
     }
 }
+
 
 static decltype(&k_adj_p2g<false, FL_LB_ADJP2G>) adj_p2g_kernel(int v) {
     switch (v) {

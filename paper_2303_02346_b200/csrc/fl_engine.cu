@@ -588,6 +588,9 @@ struct Ctx {
 #ifndef FL_CAP_GRID
 #define FL_CAP_GRID 1
 #endif
+#ifndef FL_CAP_HEAVY
+#define FL_CAP_HEAVY 1
+#endif
     // persistent block-list kernels: no more CTAs than ~one per 256 active particles (a
     // block holds ~8 particles per cell x 64 cells), so small scenes do not launch hundreds
     // of CTAs that only find the work counter exhausted
@@ -597,6 +600,17 @@ struct Ctx {
         return std::min(grid, std::max(sm_count, (active + 255) / 256));
     }
     int light_grid(int grid) const { return light_grid(grid, n_active); }
+    // heavy (SVD / rigid) kernels: persistent CTAs beyond the heavy blocks only hold SM
+    // resources the concurrent light kernel needs (a CTA of the 256-thread variant takes
+    // half an SM's registers), so the grid follows the heavy particle count (~2 blocks
+    // per 512 particles, partial blocks at the bodies' faces); the work counter keeps any
+    // underestimate correct.  Not after an upload that handed in full liquid F (those
+    // particles take the heavy path for a substep).
+    long n_heavy = 0;
+    int heavy_grid(int grid) const {
+        if (upload_full || !FL_CAP_HEAVY) return grid;
+        return std::min(grid, int(std::max<long>(sm_count / 4, 2 * ((n_heavy + 511) / 512) + 16)));
+    }
     // heavy (SVD / rigid) blocks are possible: a heavy class is present, or the last upload
     // (or an adjoint_substep call) handed in a liquid with a full F (kMetaFull)
     bool classes_heavy = true, upload_full = true;
@@ -829,6 +843,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
         long nh = 0;
         for (int i = 0; i < N; i++) nh += classes[p_class[i]].heavy;
         classes_heavy = nh > 0;
+        n_heavy = nh;
         hvar = 2 * nh >= N ? 2 : 1;
         // fewer SVD/rigid blocks than SMs beside a liquid scene (c4's floater): they are the
         // dual launches' tail -> variant 3, 256-thread CTAs (a full block in fewer rounds)
@@ -1342,7 +1357,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
     }
     PROF(K_SORT, sort_and_lists(*in, r));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
+             launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_p2g_h) : light_grid(grid_p2g), d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     if (slab()) {
@@ -1365,7 +1380,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
                            stream));
     }
     PROF(K_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? grid_g2p_h : light_grid(grid_g2p), d_cls.p, r.gridv,
+             launch_g2p(geom, in->p, out->p, r.perm, r.recs, r.n_blocks, hv ? heavy_grid(grid_g2p_h) : light_grid(grid_g2p), d_cls.p, r.gridv,
                         rd, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     PROF(K_OTHER, launch_tail_copy(geom, in->p, out->p, r.perm, dn(r.n_active, slab() ? r.dcnt + RC_ACTIVE : nullptr),
@@ -1426,7 +1441,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
     sort_and_lists(*cur, r);
     EffSet es = make_effset(eff);
     dual([&](bool hv, int* w, cudaStream_t s) {
-        launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_p2g_h : light_grid(grid_p2g), d_cls.p,
+        launch_p2g(geom, cur->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_p2g_h) : light_grid(grid_p2g), d_cls.p,
                    staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
     });
     if (slab()) {
@@ -1710,7 +1725,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
         launches += 4;
     }
     PROF(K_ADJ_G2P, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? grid_adj_h : light_grid(grid_adj, r.n_active), d_cls.p,
+             launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_adj_h) : light_grid(grid_adj, r.n_active), d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
     if (slab()) PROF(K_COMM, halo_exchange(r.blockmap, staging_bar.p, nullptr));
@@ -1719,7 +1734,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
                                      eff_blocks, stream));
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
-             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? grid_ap_h : light_grid(grid_ap, r.n_active), d_cls.p, gridbar.p,
+             launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? heavy_grid(grid_ap_h) : light_grid(grid_ap, r.n_active), d_cls.p, gridbar.p,
                             xbar_tmp.p, Fbar_tmp.p, out, d_nonfinite.p + t_slot, hv ? hvar : 0, w, s);
          }));
     const int* rc = slab() ? r.dcnt : nullptr;
