@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
                                                                  const float4* __restrict__ staging_bar,
                                                                  const float4* __restrict__ gridv0, float4* gridbar,
                                                                  EffSet eff, double* eff_partial,
-                                                                 const uint8_t* __restrict__ cmask) {
+                                                                 const uint8_t* __restrict__ cmask, GridCols cols) {
     pdl_wait();
     constexpr int kW = kAdjGridThreads / 32;
     constexpr int kQ = NE * kEffQ > 0 ? NE * kEffQ : 1;
@@ -503,6 +503,10 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
         const int nbid = nb_list[k];
         int bx, by, bz;
         block_unlin(g, nbid, bx, by, bz);
+        if (cols.cmode) {  // (uniform per node block: both warps skip together)
+            const bool edge = bx == cols.c0 || bx == cols.c1;
+            if (edge != (cols.cmode == 2)) continue;
+        }
         const float4 sb = gather_tile_sum(g, blockmap, staging_bar, bx, by, bz, lx, ly, lz);
         V3<float> bar = {sb.x, sb.y, sb.z};
         const size_t idx = size_t(nbid) * 64 + l;
@@ -605,18 +609,21 @@ __global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nbloc
 
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s) {
+                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s, int cmode, int c0,
+                     int c1) {
+    const GridCols cols{cmode, c0, c1};
+    const dim3 gr(nblocks), bl(kAdjGridThreads);
     switch (eff.n) {
-        case 0: launch_k(k_adj_grid<0>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial, cmask); break;
-        case 1: launch_k(k_adj_grid<1>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial, cmask); break;
-        case 2: launch_k(k_adj_grid<2>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial, cmask); break;
-        case 3: launch_k(k_adj_grid<3>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                                                                     gridbar, eff, eff_partial, cmask); break;
-        default: launch_k(k_adj_grid<kMaxEff>, dim3(nblocks), dim3(kAdjGridThreads), 0, s, g, nb_list, n_nb, blockmap, staging_bar,
-                                                                            gridv0, gridbar, eff, eff_partial, cmask);
+        case 0: launch_k(k_adj_grid<0>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        case 1: launch_k(k_adj_grid<1>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        case 2: launch_k(k_adj_grid<2>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        case 3: launch_k(k_adj_grid<3>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        default: launch_k(k_adj_grid<kMaxEff>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar,
+                          eff, eff_partial, cmask, cols);
     }
 }
 

@@ -385,6 +385,9 @@ struct Ctx {
     int hvar = 1;  // heavy kernel variant (occupancy_grid): 1 beside liquid, 2 dominant, 3 few beside liquid
     int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
     int eff_blocks = kEffBlocks;
+    // effector-bar partial rows per substep: one per grid-adjoint CTA, twice on slabs
+    // (interior and edge launches)
+    int eff_rows() const { return slab() ? 2 * eff_blocks : eff_blocks; }
     int grid_p2g_h = 0, grid_g2p_h = 0, grid_adj_h = 0, grid_ap = 0, grid_ap_h = 0;
 
     // live state
@@ -414,7 +417,9 @@ struct Ctx {
     int n_parked() const { return int(inactive_ids.size()); }
     void set_transport(std::unique_ptr<Transport> t);
     void partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t>& active);
-    void halo_exchange(int* blockmap, float4* stg, int* flags);
+    void halo_exchange(int* blockmap, float4* stg, int* flags, cudaStream_t st = nullptr);
+    cudaStream_t s_comm = nullptr;  // slabs: halo exchange overlapping the interior grid update
+    cudaEvent_t ev_halo_fork = nullptr, ev_halo_join = nullptr;
     void migrate(StateBuf& out, Record& r);
     void return_bars(Record& r, BarBuf post);
     // slab contexts keep the exact particle counts on the device (StateBuf::cnt,
@@ -519,7 +524,7 @@ struct Ctx {
     long eff_lo = -1, eff_hi = -1;
     void eff_flush() {
         if (eff_lo < 0) return;
-        launch_eff_final(eff_partial.p, eff_blocks, int(eff.size()), eff_lo, int(eff_hi - eff_lo + 1), eff_out.p,
+        launch_eff_final(eff_partial.p, eff_rows(), int(eff.size()), eff_lo, int(eff_hi - eff_lo + 1), eff_out.p,
                          stream);
         launches++;
         eff_lo = eff_hi = -1;
@@ -868,7 +873,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     // the scene (grid-stride loop over the touched node blocks: never more CTAs than node
     // blocks or ~1 per 64 particles), at least one CTA per SM.
     eff_blocks = std::max(sm_count, std::min({kEffBlocks, g.nbtot, (N + 63) / 64}));
-    eff_partial.alloc(size_t(kEffRing) * eff_blocks * kMaxEff * 18);
+    eff_partial.alloc(size_t(kEffRing) * 2 * eff_blocks * kMaxEff * 18);  // (slabs: interior + edge rows)
 #ifndef FL_SORT_CTAS
 #define FL_SORT_CTAS 8
 #endif
@@ -1157,6 +1162,11 @@ void Ctx::set_transport(std::unique_ptr<Transport> t) {
     set_mig_cap(4096);
     d_ovf.alloc(1);
     mig_bcnt.alloc(kMigCountInts);
+    if (!s_comm) {
+        CK(cudaStreamCreateWithFlags(&s_comm, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_halo_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_halo_join, cudaEventDisableTiming));
+    }
     CK(cudaMemsetAsync(d_ovf.p, 0, sizeof(int), stream));
     CK(cudaStreamSynchronize(stream));
 }
@@ -1204,20 +1214,20 @@ void Ctx::partition(const std::vector<uint32_t>& keys, const std::vector<uint8_t
 // send tile planes 0,1 of the bottom column down and 4,5 of the top column up,
 // install the received planes as ghost blocks.  flags != nullptr (forward):
 // also flag the owned node blocks reached only by the lower neighbour's tiles.
-void Ctx::halo_exchange(int* blockmap, float4* stg, int* flags) {
+void Ctx::halo_exchange(int* blockmap, float4* stg, int* flags, cudaStream_t st) {
     Geom& g = geom;
+    if (!st) st = stream;
     const bool lo = rank > 0, hi = rank + 1 < nranks;
-    if (lo) launch_halo_pack(g, blockmap, stg, g.sx0, 0, halo_send[0].p, stream);
-    if (hi) launch_halo_pack(g, blockmap, stg, g.sx1 - 1, 4, halo_send[1].p, stream);
+    if (lo) launch_halo_pack(g, blockmap, stg, g.sx0, 0, halo_send[0].p, st);
+    if (hi) launch_halo_pack(g, blockmap, stg, g.sx1 - 1, 4, halo_send[1].p, st);
     const size_t hb = halo_bytes(g);
     const void* sb[2] = {halo_send[0].p, halo_send[1].p};
     void* rb[2] = {halo_recv[0].p, halo_recv[1].p};
     const size_t sz[2] = {lo ? hb : 0, hi ? hb : 0};
-    comm->neighbor_exchange(sb, sz, rb, sz, stream);
+    comm->neighbor_exchange(sb, sz, rb, sz, st);
     if (lo)
-        launch_halo_unpack(g, halo_recv[0].p, g.sx0 - 1, 4, maxb, blockmap, stg, flags, flags ? g.sx0 : -1,
-                           stream);
-    if (hi) launch_halo_unpack(g, halo_recv[1].p, g.sx1, 0, maxb + g.colblocks, blockmap, stg, nullptr, -1, stream);
+        launch_halo_unpack(g, halo_recv[0].p, g.sx0 - 1, 4, maxb, blockmap, stg, flags, flags ? g.sx0 : -1, st);
+    if (hi) launch_halo_unpack(g, halo_recv[1].p, g.sx1, 0, maxb + g.colblocks, blockmap, stg, nullptr, -1, st);
     launches += 2 * (int(lo) + int(hi));
 }
 
@@ -1360,17 +1370,31 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_p2g_h) : light_grid(grid_p2g), d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
-    if (slab()) {
-        PROF(K_COMM, halo_exchange(r.blockmap, staging.p, nbflag));
-        // node-block list again, now with the blocks reached only by ghost tiles
-        launch_flag_list(nbflag, geom.nbtot, r.nb_list, r.n_nb, nbpos.p, stream);
-        launches += 2;
-    }
     // the adjoint's inputs (v0 = p/m, contact mask) only for substeps that keep a record
     const bool keep = &r != scratch_rec.get();
-    PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv,
-                                    keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, bzero.p,
-                                    int(bzero.n), stream));
+    if (slab()) {
+        // the halo planes travel on the comm stream while the interior node columns update
+        // (they read no ghost tile); then the node-block list gains the blocks reached only
+        // by ghost tiles and the two edge columns update
+        const int c0 = rank > 0 ? geom.sx0 : -1, c1 = rank + 1 < nranks ? geom.sx1 : -1;
+        CK(cudaEventRecord(ev_halo_fork, stream));
+        CK(cudaStreamWaitEvent(s_comm, ev_halo_fork, 0));
+        halo_exchange(r.blockmap, staging.p, nbflag, s_comm);
+        CK(cudaEventRecord(ev_halo_join, s_comm));
+        PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv,
+                                        keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, bzero.p,
+                                        int(bzero.n), stream, 1, c0, c1));
+        PROF(K_COMM, CK(cudaStreamWaitEvent(stream, ev_halo_join, 0)));
+        launch_flag_list(nbflag, geom.nbtot, r.nb_list, r.n_nb, nbpos.p, stream);
+        PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv,
+                                        keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, nullptr, 0,
+                                        stream, 2, c0, c1));
+        launches += 3;
+    } else {
+        PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv,
+                                        keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, bzero.p,
+                                        int(bzero.n), stream));
+    }
     counters_clean = true;
     RigidDev rd = rigid_dev(r);
     if (nbody > 0) {
@@ -1728,10 +1752,26 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_adj_h) : light_grid(grid_adj, r.n_active), d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
-    if (slab()) PROF(K_COMM, halo_exchange(r.blockmap, staging_bar.p, nullptr));
-    PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                     eff_partial.p + size_t(t_slot % kEffRing) * eff_blocks * kMaxEff * 18, r.cmask,
-                                     eff_blocks, stream));
+    double* ep = eff_partial.p + size_t(t_slot % kEffRing) * eff_rows() * kMaxEff * 18;
+    if (slab()) {
+        // as in the forward: the halo planes of the v_bar tiles travel while the interior node
+        // columns run their adjoint; the edge columns' effector-bar partials take the second
+        // half of the substep's rows
+        const int c0 = rank > 0 ? geom.sx0 : -1, c1 = rank + 1 < nranks ? geom.sx1 : -1;
+        CK(cudaEventRecord(ev_halo_fork, stream));
+        CK(cudaStreamWaitEvent(s_comm, ev_halo_fork, 0));
+        halo_exchange(r.blockmap, staging_bar.p, nullptr, s_comm);
+        CK(cudaEventRecord(ev_halo_join, s_comm));
+        PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
+                                         ep, r.cmask, eff_blocks, stream, 1, c0, c1));
+        PROF(K_COMM, CK(cudaStreamWaitEvent(stream, ev_halo_join, 0)));
+        PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
+                                         ep + size_t(eff_blocks) * kMaxEff * 18, r.cmask, eff_blocks, stream, 2, c0, c1));
+        launches++;
+    } else {
+        PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
+                                         ep, r.cmask, eff_blocks, stream));
+    }
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_adj_p2g(g, pre.p, r.perm, r.recs, r.n_blocks, hv ? heavy_grid(grid_ap_h) : light_grid(grid_ap, r.n_active), d_cls.p, gridbar.p,

@@ -343,7 +343,8 @@ constexpr int kGridUpdThreads = FL_GRIDUPD_THREADS;  // 64 nodes (one node block
 __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const int* __restrict__ nb_list,
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
-                                                     EffSet eff, uint8_t* cmask, int* clear, int n_clear) {
+                                                     EffSet eff, uint8_t* cmask, int* clear, int n_clear,
+                                                     GridCols cols) {
     pdl_wait();
     // the sort's counters are dead by now: clear them for the next substep's sort
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_clear; i += gridDim.x * blockDim.x) clear[i] = 0;
@@ -355,6 +356,10 @@ __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const i
         const int nbid = nb_list[k];
         int bx, by, bz;
         block_unlin(g, nbid, bx, by, bz);
+        if (cols.cmode) {
+            const bool edge = bx == cols.c0 || bx == cols.c1;
+            if (edge != (cols.cmode == 2)) continue;
+        }
         const float4 mp = gather_staging(g, blockmap, staging, bx, by, bz, lx, ly, lz);
         const float m = mp.x;
         const size_t idx = size_t(nbid) * 64 + l;
@@ -381,9 +386,9 @@ __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const i
 
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
-                        int* clear, int n_clear, cudaStream_t s) {
+                        int* clear, int n_clear, cudaStream_t s, int cmode, int c0, int c1) {
     launch_k(k_grid_update, dim3(grid * (256 / kGridUpdThreads)), dim3(kGridUpdThreads), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
-                                       n_clear);
+                                       n_clear, GridCols{cmode, c0, c1});
 }
 
 // ---------------------------------------------------------------------------

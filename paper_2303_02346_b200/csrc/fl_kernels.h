@@ -65,6 +65,13 @@ enum RecCnt : int {
 // grid for a grid-stride loop over up to n items (256 threads, at most `cap` CTAs)
 inline int gs_grid(int n, int cap = 148 * 16) { return std::max(1, std::min(cap, (n + 255) / 256)); }
 
+// node-column filter of the grid update and its adjoint (slab halo overlap): cmode 0 every
+// listed node block, 1 all but node columns c0/c1 (the interior, updated while the halo
+// planes travel), 2 only those columns
+struct GridCols {
+    int cmode, c0, c1;
+};
+
 // rigid-body bookkeeping for one substep (forward record / backward input)
 struct RigidDev {
     int nbody;
@@ -215,9 +222,10 @@ void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, i
 void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                 const uint16_t* celltab, int grid, const ClassInfo* cls, float4* staging, unsigned long long* err,
                 uint32_t substep, int variant, int* wq, cudaStream_t s);
+// cmode (slab halo overlap): 0 every listed node block, 1 all but node columns c0/c1, 2 only those
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
-                        int* clear, int n_clear, cudaStream_t s);
+                        int* clear, int n_clear, cudaStream_t s, int cmode = 0, int c0 = -1, int c1 = -1);
 void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const BlockRec* recs,
                 const int* n_blocks, int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd,
                 unsigned long long* err, uint32_t substep, int variant, int* wq, cudaStream_t s);
@@ -246,7 +254,8 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     float4* staging_bar, int variant, int* wq, cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s);
+                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s, int cmode = 0,
+                     int c0 = -1, int c1 = -1);
 constexpr int kEffRing = 16;  // substeps whose effector-bar partials wait for one final-sum launch
 void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out,
                       cudaStream_t s);
