@@ -223,6 +223,11 @@ int flume_last_error(const flume_ctx* ctx, flume_error_info* info);
    (default), 1 = snapshots spilled to pinned host memory on a copy stream that overlaps the
    forward, brought back when the backward replays their segment.  Results are identical. */
 int flume_set_checkpoint_spill(flume_ctx* ctx, int mode);
+/* The file tier (NVMe; PAPER.md's offload): snapshots other than the last segment's go to an
+   anonymous file in `dir` (D2H into pinned staging buffers on a copy stream, written by a
+   worker thread; read back -- the next older one prefetched -- when the backward replays).
+   Results identical to the other tiers.  flume_set_checkpoint_spill(ctx, 0 / 1) switches back. */
+int flume_set_checkpoint_spill_dir(flume_ctx* ctx, const char* dir);
 /* trajectory_chamfer nearest-neighbour search (losses.hpp:15-64): 0 = automatic (brute-force
    scan for small member x goal sets, a uniform-grid index above 2^24 pairs), 1 = always the
    scan, 2 = always the grid index.  Both return the reference's first-index minimum, so the

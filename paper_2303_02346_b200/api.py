@@ -512,6 +512,12 @@ class GpuWorkspace:
         """grad_trajectory snapshots in pinned host memory instead of HBM (long horizons)."""
         self._collective(lambda r, c: self.lib.flume_set_checkpoint_spill(c, int(bool(host))))
 
+    def set_checkpoint_spill_dir(self, directory: str):
+        """grad_trajectory snapshots in a file under `directory` (local NVMe), read back when
+        the backward replays their segment; results identical."""
+        d = str(directory).encode()
+        self._collective(lambda r, c: self.lib.flume_set_checkpoint_spill_dir(c, d))
+
     CHAMFER_MODES = {"auto": 0, "scan": 1, "grid": 2}
 
     def set_chamfer_mode(self, mode: str = "auto"):

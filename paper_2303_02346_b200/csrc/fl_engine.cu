@@ -30,6 +30,7 @@
 #include "fl_host.h"
 #include "fl_kernels.h"
 #include "fl_scatter.cuh"
+#include "fl_spill.h"
 
 namespace fl {
 
@@ -335,7 +336,9 @@ struct Ctx {
     bool counters_clean = false;  // bzero already zeroed (by the last grid update)
     // checkpoint spill: snapshots of grad_trajectory in pinned host memory (D2H on a
     // copy stream overlapping the forward; H2D when the backward replays a segment)
-    int spill = 0;
+    int spill = 0;  // 0 HBM, 1 pinned host memory, 2 a file in spill_dir (FileSpill)
+    std::string spill_dir;
+    std::unique_ptr<FileSpill> fspill;
     int chamfer_mode = 0;  // flume_set_chamfer_mode
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_snap = nullptr;
@@ -1858,9 +1861,20 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     std::vector<RecordPtr> cache_recs;
     long cache_base = -1;
 
-    std::map<long, HostPtr> hsnaps;  // spilled snapshots
+    std::map<long, HostPtr> hsnaps;  // snapshots spilled to pinned host memory
+    struct FileSnap {
+        off_t off;
+        size_t bytes;
+        int n;
+    };
+    std::map<long, FileSnap> fsnaps;  // snapshots spilled to the file tier
+    if (spill == 2) {
+        if (!fspill || fspill->slot_bytes() != cur->bytes) fspill.reset(new FileSpill(spill_dir, cur->bytes));
+        fspill->reset();
+    }
     // device buffers of spilled snapshots go back to the pool once their D2H finished
     std::vector<std::pair<StatePtr, cudaEvent_t>> spilling;
+    std::vector<cudaEvent_t> own_events;  // (file tier: per-snapshot D2H events)
     auto retire_spilled = [&](bool all) {
         for (size_t i = 0; i < spilling.size();) {
             if (all || cudaEventQuery(spilling[i].second) == cudaSuccess || spilling.size() > 2) {
@@ -1873,7 +1887,20 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         }
     };
     auto take_snapshot = [&](long at, StatePtr s) {  // s stays the input of the next substep
-        if (spill && at < last_base) {
+        if (spill == 2 && at < last_base) {
+            if (!cstream) {
+                CK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
+            }
+            CK(cudaEventRecord(ev_snap, stream));
+            CK(cudaStreamWaitEvent(cstream, ev_snap, 0));
+            fsnaps[at] = FileSnap{fspill->put(s->mem, s->bytes, cstream), s->bytes, s->n};
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, cstream));
+            own_events.push_back(e);
+            spilling.push_back({s, e});
+        } else if (spill == 1 && at < last_base) {
             HostPtr h = spill_state(*s);
             hsnaps[at] = h;
             spilling.push_back({s, h->done});
@@ -1899,7 +1926,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         if (in_last) {
             cache_recs.push_back(rec);
             cache_states.push_back(nxt);
-        } else if (!snaps.count(t) && !hsnaps.count(t)) {
+        } else if (!snaps.count(t) && !hsnaps.count(t) && !fsnaps.count(t)) {
             put_state(st);
         }
         st = nxt;
@@ -1911,7 +1938,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         }
     }
     retire_spilled(true);
-    const size_t n_snap = snaps.size() + hsnaps.size();
+    const size_t n_snap = snaps.size() + hsnaps.size() + fsnaps.size();
     allreduce(loss_out.p, size_t(nseg), DType::F64, ROp::Sum);
     CK(cudaEventRecord(ev1, stream));
     std::vector<double> per(nseg);
@@ -1951,6 +1978,12 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         if (hsnaps.count(base)) {  // spilled: back into HBM (released with the cache)
             s = get_state();
             unspill(*hsnaps[base], *s);
+        } else if (fsnaps.count(base)) {  // file tier: read back, and start reading the next older one
+            const FileSnap& f = fsnaps[base];
+            s = get_state();
+            fspill->get(f.off, s->mem, f.bytes, stream);
+            s->n = f.n;
+            if (fsnaps.count(base - stride)) fspill->prefetch(fsnaps[base - stride].off, fsnaps[base - stride].bytes);
         } else {
             s = snaps.at(base);
         }
@@ -1986,6 +2019,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     release_cache();
     for (auto& kv : snaps) put_state(kv.second);
     for (auto& kv : hsnaps) host_pool.push_back(kv.second);
+    for (cudaEvent_t e : own_events) cudaEventDestroy(e);
     eff_flush();
     if (slab()) {  // per-slab effector / spawn bars and non-finite flags
         allreduce(eff_out.p, size_t(T) * kMaxEff * 18, DType::F64, ROp::Sum);
@@ -2336,6 +2370,15 @@ int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact) {
 int flume_set_checkpoint_spill(flume_ctx* ctx, int mode) {
     if (!ctx || mode < 0 || mode > 1) return FLUME_E_ARG;
     return guard(ctx, [&] { ctx->c.spill = mode; });
+}
+
+int flume_set_checkpoint_spill_dir(flume_ctx* ctx, const char* dir) {
+    if (!ctx || !dir || !*dir) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.spill_dir = dir;
+        ctx->c.fspill.reset();
+        ctx->c.spill = 2;
+    });
 }
 
 int flume_set_chamfer_mode(flume_ctx* ctx, int mode) {
