@@ -35,42 +35,71 @@ namespace fl {
 #endif
 constexpr int kSortThreads = FL_SORT_THREADS;
 
+// Both passes handle kSortItems particles per thread (CTA-strided, so a warp still covers
+// consecutive slots for the warp aggregation): the loads of all items are issued before
+// the first atomic, which turns one dependent load -> atomic -> store chain per particle
+// into kSortItems overlapped ones.
+#ifndef FL_SORT_ITEMS
+#define FL_SORT_ITEMS 4
+#endif
+constexpr int kSortItems = FL_SORT_ITEMS;
+
 __global__ void k_sort_count(Geom g, PBuf st, DN nn, const ClassInfo* __restrict__ cls, int* bcount,
                              int* bheavy) {
     pdl_wait();
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nn.get()) return;
-    const uint32_t key = st.key[i];
-    const int b = key >= g.key_inactive ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
-    // warp-aggregated: the store order is nearly sorted, so lanes share blocks
-    const unsigned peers = __match_any_sync(__activemask(), b);
-    const uint32_t meta = st.meta[i];
-    const unsigned heavy =
-        __ballot_sync(__activemask(), cls[meta_cls(meta)].heavy != 0 || (meta & kMetaFull) != 0u) & peers;
-    const int leader = __ffs(peers) - 1;
-    if ((threadIdx.x & 31) == leader) {
-        atomicAdd(&bcount[b], __popc(peers));
-        if (heavy) atomicOr(&bheavy[b], 1);
+    const int n = nn.get();
+    const int i0 = blockIdx.x * blockDim.x * kSortItems + threadIdx.x;
+    uint32_t key[kSortItems], meta[kSortItems];
+#pragma unroll
+    for (int q = 0; q < kSortItems; q++) {
+        const int i = i0 + q * blockDim.x;
+        key[q] = i < n ? st.key[i] : 0u;
+        meta[q] = i < n ? st.meta[i] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kSortItems; q++) {
+        if (i0 + q * int(blockDim.x) >= n) break;
+        const int b = key[q] >= g.key_inactive ? g.nbtot + int((key[q] - g.key_inactive) >> 6) : int(key[q] >> 6);
+        // warp-aggregated: the store order is nearly sorted, so lanes share blocks
+        const unsigned peers = __match_any_sync(__activemask(), b);
+        const unsigned heavy =
+            __ballot_sync(__activemask(), cls[meta_cls(meta[q])].heavy != 0 || (meta[q] & kMetaFull) != 0u) & peers;
+        const int leader = __ffs(peers) - 1;
+        if ((threadIdx.x & 31) == leader) {
+            atomicAdd(&bcount[b], __popc(peers));
+            if (heavy) atomicOr(&bheavy[b], 1);
+        }
     }
 }
 
 __global__ void k_sort_scatter(Geom g, PBuf st, DN nn, const int* __restrict__ bstart, int* bfill, uint32_t* skey,
                                uint32_t* sslot) {
     pdl_wait();
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nn.get()) return;
-    const uint32_t key = st.key[i];
-    const bool inact = key >= g.key_inactive;  // parked or departed
-    const int b = inact ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
-    const unsigned peers = __match_any_sync(__activemask(), b);
-    const int leader = __ffs(peers) - 1;
+    const int n = nn.get();
+    const int i0 = blockIdx.x * blockDim.x * kSortItems + threadIdx.x;
+    uint32_t key[kSortItems], id[kSortItems];
+#pragma unroll
+    for (int q = 0; q < kSortItems; q++) {
+        const int i = i0 + q * blockDim.x;
+        key[q] = i < n ? st.key[i] : 0u;
+        id[q] = i < n ? st.id[i] : 0u;
+    }
     const int lane = threadIdx.x & 31;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(&bfill[b], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    const int p = bstart[b] + base + __popc(peers & ((1u << lane) - 1));
-    skey[p] = ((inact ? 0u : (key & 63u)) << 26) | st.id[i];
-    sslot[p] = uint32_t(i);
+#pragma unroll
+    for (int q = 0; q < kSortItems; q++) {
+        const int i = i0 + q * blockDim.x;
+        if (i >= n) break;
+        const bool inact = key[q] >= g.key_inactive;  // parked or departed
+        const int b = inact ? g.nbtot + int((key[q] - g.key_inactive) >> 6) : int(key[q] >> 6);
+        const unsigned peers = __match_any_sync(__activemask(), b);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&bfill[b], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const int p = bstart[b] + base + __popc(peers & ((1u << lane) - 1));
+        skey[p] = ((inact ? 0u : (key[q] & 63u)) << 26) | id[q];
+        sslot[p] = uint32_t(i);
+    }
 }
 
 template <class KP, class VP>
@@ -224,12 +253,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
 void launch_sort_count(const Geom& g, const PBuf& st, DN n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s) {
     if (n.h <= 0) return;  // (an empty slab)
-    launch_k(k_sort_count, dim3((n.h + 255) / 256), dim3(256), 0, s, g, st, n, cls, bcount, bheavy);
+    launch_k(k_sort_count, dim3((n.h + 256 * kSortItems - 1) / (256 * kSortItems)), dim3(256), 0, s, g, st, n, cls,
+             bcount, bheavy);
 }
 void launch_sort_scatter(const Geom& g, const PBuf& st, DN n, const int* bstart, int* bfill, uint32_t* skey,
                          uint32_t* sslot, cudaStream_t s) {
     if (n.h <= 0) return;
-    launch_k(k_sort_scatter, dim3((n.h + 255) / 256), dim3(256), 0, s, g, st, n, bstart, bfill, skey, sslot);
+    launch_k(k_sort_scatter, dim3((n.h + 256 * kSortItems - 1) / (256 * kSortItems)), dim3(256), 0, s, g, st, n,
+             bstart, bfill, skey, sslot);
 }
 
 // ---------------------------------------------------------------------------
