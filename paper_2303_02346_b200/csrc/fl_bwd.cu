@@ -481,7 +481,7 @@ __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __re
 // memory (static node order per warp, since the list partition is static), then
 // one fixed-order CTA reduction per launch.  Nothing effector-sized lives in
 // registers across nodes, which keeps the kernel at ~64 registers.
-template <int NE>
+template <int NE, bool FILTER>  // (the column filter only in slab contexts)
 __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj_grid(Geom g, const int* __restrict__ nb_list,
                                                                  const int* __restrict__ n_nb,
                                                                  const int* __restrict__ blockmap,
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
         const int nbid = nb_list[k];
         int bx, by, bz;
         block_unlin(g, nbid, bx, by, bz);
-        if (cols.cmode) {  // (uniform per node block: both warps skip together)
+        if (FILTER) {  // (uniform per node block: both warps skip together)
             const bool edge = bx == cols.c0 || bx == cols.c1;
             if (edge != (cols.cmode == 2)) continue;
         }
@@ -607,24 +607,37 @@ __global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nbloc
     }
 }
 
+template <bool F>
+static void launch_adj_grid_t(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
+                              const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
+                              double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s,
+                              const GridCols& cols) {
+    const dim3 gr(nblocks), bl(kAdjGridThreads);
+    switch (eff.n) {
+        case 0: launch_k(k_adj_grid<0, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        case 1: launch_k(k_adj_grid<1, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        case 2: launch_k(k_adj_grid<2, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        case 3: launch_k(k_adj_grid<3, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
+                         eff_partial, cmask, cols); break;
+        default: launch_k(k_adj_grid<kMaxEff, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
+                          gridbar, eff, eff_partial, cmask, cols);
+    }
+}
+
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                      double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s, int cmode, int c0,
                      int c1) {
     const GridCols cols{cmode, c0, c1};
-    const dim3 gr(nblocks), bl(kAdjGridThreads);
-    switch (eff.n) {
-        case 0: launch_k(k_adj_grid<0>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        case 1: launch_k(k_adj_grid<1>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        case 2: launch_k(k_adj_grid<2>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        case 3: launch_k(k_adj_grid<3>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        default: launch_k(k_adj_grid<kMaxEff>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar,
-                          eff, eff_partial, cmask, cols);
-    }
+    if (cmode)
+        launch_adj_grid_t<true>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial, cmask,
+                                nblocks, s, cols);
+    else
+        launch_adj_grid_t<false>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial, cmask,
+                                 nblocks, s, cols);
 }
 
 void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out,

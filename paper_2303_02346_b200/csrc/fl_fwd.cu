@@ -340,6 +340,7 @@ __device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __res
 #endif
 constexpr int kGridUpdThreads = FL_GRIDUPD_THREADS;  // 64 nodes (one node block) per 64 threads
 
+template <bool FILTER>  // (the column filter only in slab contexts: it costs the plain path ~2 us)
 __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const int* __restrict__ nb_list,
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const i
         const int nbid = nb_list[k];
         int bx, by, bz;
         block_unlin(g, nbid, bx, by, bz);
-        if (cols.cmode) {
+        if (FILTER) {
             const bool edge = bx == cols.c0 || bx == cols.c1;
             if (edge != (cols.cmode == 2)) continue;
         }
@@ -387,8 +388,9 @@ __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const i
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
                         int* clear, int n_clear, cudaStream_t s, int cmode, int c0, int c1) {
-    launch_k(k_grid_update, dim3(grid * (256 / kGridUpdThreads)), dim3(kGridUpdThreads), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear,
-                                       n_clear, GridCols{cmode, c0, c1});
+    launch_k(cmode ? k_grid_update<true> : k_grid_update<false>, dim3(grid * (256 / kGridUpdThreads)),
+             dim3(kGridUpdThreads), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear, n_clear,
+             GridCols{cmode, c0, c1});
 }
 
 // ---------------------------------------------------------------------------
