@@ -40,6 +40,10 @@ def spec_of(name: str) -> dict:
         return spec
     if name == "c3_fwd100":
         return scenes.load("c3")
+    if name == "c2_fwd100":
+        return scenes.load("c2")
+    if name == "c5_2x10":
+        return scenes.load("c5")
     if name.endswith("_64_10x50"):
         return scenes.scaled(name[:2], 64)
     raise KeyError(name)

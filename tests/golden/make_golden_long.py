@@ -13,6 +13,9 @@ These pin the CUDA path at the benchmark horizons of SURVEY.md 8(c)/8(d):
                soft band), 2 x 25 substeps
   c4_fwd500    full c4 state after the bench's 500 forward substeps (id sample)
   c3_fwd100    full c3 (1,024,000 non-Newtonian particles) state after 100 substeps (id sample)
+  c2_fwd100    full c2 (1,057,280 particles: liquid, viscous liquid, emitter) after 100 substeps
+  c5_2x10      full c5 (8,044,544 particles, 256^3, every material + the rigid brick): the
+               scaling workload -- state after 20 substeps, loss and gradient over 2 x 10
   elastic512   the 3D gradcheck scene (test_autodiff.cpp:113-151) over acceptance_main.cpp:71-100's
                8 x 64 substeps (the stride-invariance criterion's workload)
   c{2,3,5}_64_10x50  the scene at grid 64 (c5: 125,696 particles with every material kind and
@@ -102,6 +105,10 @@ def case(name):
         return grad_case(scenes.load("c4"), 0, 0, 0, substeps_state=500)
     if name == "c3_fwd100":
         return grad_case(scenes.load("c3"), 0, 0, 0, substeps_state=100)
+    if name == "c2_fwd100":  # full latte art: liquid + viscous liquid, the emitter active
+        return grad_case(scenes.load("c2"), 0, 0, 0, substeps_state=100)
+    if name == "c5_2x10":  # the scaling workload (8M particles, 256^3), its stable window
+        return grad_case(scenes.load("c5"), 2, 10, 10, substeps_state=20)
     if name == "elastic512":
         from tests._long import elastic512_actions
         from tests.golden.make_golden import GRADCHECK_3D
@@ -116,7 +123,7 @@ def case(name):
 
 
 CASES = ["c1_4x25", "elastic512", "c4_10x50", "c4pool_2x25", "c4_fwd500", "c3_fwd100", "c2_64_10x50", "c3_64_10x50",
-         "c5_64_10x50"]
+         "c5_64_10x50", "c2_fwd100", "c5_2x10"]
 
 
 def main(argv):
