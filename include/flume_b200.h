@@ -233,6 +233,12 @@ int flume_set_checkpoint_spill_dir(flume_ctx* ctx, const char* dir);
    scan, 2 = always the grid index.  Both return the reference's first-index minimum, so the
    loss and gradient bits do not depend on the mode. */
 int flume_set_chamfer_mode(flume_ctx* ctx, int mode);
+/* Particle sort between substeps: 1 (default) = incremental when the state came out of the
+   previous substep on this context (only the blocks a particle entered, left or moved
+   inside are re-sorted; the rest keep their order), 0 = always the full block counting
+   sort.  Identical order, so identical results.  flume_sort_stats counts both kinds. */
+int flume_set_incremental_sort(flume_ctx* ctx, int on);
+int flume_sort_stats(const flume_ctx* ctx, long* incremental, long* full);
 int flume_get_stream(flume_ctx* ctx, void** cuda_stream);
 int flume_sync(flume_ctx* ctx);
 int flume_last_timing(const flume_ctx* ctx, flume_timing* out);

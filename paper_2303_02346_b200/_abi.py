@@ -129,6 +129,8 @@ EXPORTS = {
     "flume_last_error": (C.c_int, [C.c_void_p, C.POINTER(ErrorInfo)]),
     "flume_set_checkpoint_spill": (C.c_int, [C.c_void_p, C.c_int]),
     "flume_set_chamfer_mode": (C.c_int, [C.c_void_p, C.c_int]),
+    "flume_set_incremental_sort": (C.c_int, [C.c_void_p, C.c_int]),
+    "flume_sort_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     "flume_set_checkpoint_spill_dir": (C.c_int, [C.c_void_p, C.c_char_p]),
     "flume_get_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "flume_sync": (C.c_int, [C.c_void_p]),

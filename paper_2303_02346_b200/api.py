@@ -527,6 +527,20 @@ class GpuWorkspace:
             raise ValueError(f"chamfer mode must be one of {sorted(self.CHAMFER_MODES)}")
         self._collective(lambda r, c: self.lib.flume_set_chamfer_mode(c, self.CHAMFER_MODES[mode]))
 
+    def set_incremental_sort(self, on: bool = True):
+        """Sort only the blocks whose particles changed cell since the previous substep
+        (default) or always run the full block sort; identical order and results."""
+        self._collective(lambda r, c: self.lib.flume_set_incremental_sort(c, 1 if on else 0))
+
+    def sort_stats(self):
+        """[(incremental sorts, full sorts)] per rank."""
+        out = []
+        for c in self.ctxs:
+            a, b = C.c_long(), C.c_long()
+            self.lib.flume_sort_stats(c, C.byref(a), C.byref(b))
+            out.append((a.value, b.value))
+        return out
+
     def set_migration_capacity(self, capacity: int):
         """Slots per neighbour and substep of the fixed-size migration messages (slab
         workspaces); an overflowing call is re-run with 4x the capacity."""

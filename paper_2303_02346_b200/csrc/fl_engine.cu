@@ -119,6 +119,7 @@ struct Record {
     uint32_t* mig_src = nullptr;
     int mig_cap = 0;
     long substep = 0;
+    bool scratch = false;  // a scratch record (forward only): no adjoint inputs kept
     std::vector<ActEntry> act;
     std::vector<EmitAdjEntry> emit;
     EffSet effk{};
@@ -333,7 +334,26 @@ struct Ctx {
     DevArr<int> bzero, bstart;  // bzero = [bcount | bheavy | bfill], zeroed per sort
     int *bcount = nullptr, *bheavy = nullptr, *bfill = nullptr, *nbflag = nullptr;
     DevArr<int> nbflag_arr;
-    bool counters_clean = false;  // bzero already zeroed (by the last grid update)
+    bool counters_clean = false;  // what the grid update clears is zero (all of bzero, or bfill when counts are kept)
+    // incremental sort (fl_sort.cu): the block counts persist from sort to sort, okey[okey_cur]
+    // holds the last sort's keys by sorted position, and chain_rec is the record whose sort
+    // order chain_out (the G2P output of that substep) is stored in
+    bool inc_sort = true;  // flume_set_incremental_sort
+    DevArr<uint32_t> okey[2];
+    int okey_cur = 0;
+    DevArr<int> isort_blk, rold;  // isort_blk = [dirty | acnt | afill | mover count], zero between sorts
+    DevArr<uint32_t> mov;
+    const Record* chain_rec = nullptr;
+    const StateBuf* chain_out = nullptr;
+    long n_inc_sorts = 0, n_full_sorts = 0;
+    bool keep_counts() const { return inc_sort && !comm && uint64_t(geom.key_departed) < 0x80000000ull; }
+    void chain_break() {
+        chain_rec = nullptr;
+        chain_out = nullptr;
+    }
+    // what the grid update clears for the next sort
+    int* clear_ptr() { return keep_counts() ? bfill : bzero.p; }
+    int clear_n() const { return keep_counts() ? geom.nbtot + 2 : int(bzero.n); }
     // checkpoint spill: snapshots of grad_trajectory in pinned host memory (D2H on a
     // copy stream overlapping the forward; H2D when the backward replays a segment)
     int spill = 0;  // 0 HBM, 1 pinned host memory, 2 a file in spill_dir (FileSpill)
@@ -402,7 +422,17 @@ struct Ctx {
     std::vector<EffState> eff;
     std::vector<StatePtr> pool;
     std::vector<RecordPtr> rec_pool;
-    RecordPtr scratch_rec;
+    RecordPtr scratch_rec, scratch_alt;  // alternating, so a chained sort reads the previous tables
+    Record& next_scratch() {
+        std::swap(scratch_rec, scratch_alt);
+        return *scratch_rec;
+    }
+    void new_scratch() {
+        scratch_rec = get_record();
+        scratch_alt = get_record();
+        scratch_rec->scratch = scratch_alt->scratch = true;
+        chain_break();
+    }
 
     // x-slab decomposition; comm == nullptr on one rank
     std::unique_ptr<Transport> comm;
@@ -552,6 +582,7 @@ struct Ctx {
         return std::make_shared<StateBuf>(N, nmem);
     }
     void put_state(StatePtr s) {
+        if (s.get() == chain_out) chain_break();  // about to be reused for something else
         if (s) pool.push_back(std::move(s));
     }
     RecordPtr get_record() {
@@ -629,7 +660,7 @@ struct Ctx {
     void require_particles() const {
         if (empty) throw FlumeError(FLUME_E_SCENE, "scene has no particles");
     }
-    void sort_and_lists(StateBuf& st, Record& r);
+    void sort_and_lists(StateBuf& st, Record& r, const Record* prev = nullptr);
     void forward_substep(const double* action, StatePtr in, StatePtr out, Record& r);
     void substep(const double* action, int count);
     void stage_grid(double* mass, double* vel);
@@ -819,6 +850,11 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     bcount = bzero.p;
     bheavy = bzero.p + bz;
     bfill = bzero.p + 2 * bz;
+    isort_blk.alloc(3 * bz + 1);
+    CK(cudaMemsetAsync(isort_blk.p, 0, isort_blk.n * sizeof(int), stream));
+    mov.alloc(N);
+    rold.alloc(maxb);
+    for (int k = 0; k < 2; k++) okey[k].alloc(N);
     nbflag_arr.alloc(g.nbtot);
     nbflag = nbflag_arr.p;
     nbpos.alloc(g.nbtot);
@@ -885,7 +921,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
 
     // initial effector state from the shapes' defaults is set by upload()
     eff.resize(eff_shapes.size());
-    scratch_rec = get_record();
+    new_scratch();
     cur = get_state();
     CK(cudaStreamSynchronize(stream));
 }
@@ -1063,6 +1099,9 @@ void Ctx::upload(const flume_state_view* view) {
     sort_and_lists(*raw, *scratch_rec);
     launch_gather(raw->p, cur->p, scratch_rec->perm, scratch_rec->n_keep, stream);
     n_stored = scratch_rec->n_keep;
+    // cur is stored in this sort's order: the first substep can sort incrementally
+    chain_rec = keep_counts() ? scratch_rec.get() : nullptr;
+    chain_out = chain_rec ? cur.get() : nullptr;
     cur->n = n_stored;
     park_base = n_active;
     if (slab()) state_counts_from_host(*cur);
@@ -1130,17 +1169,41 @@ void Ctx::download_meta(flume_state_view* view) {
 }
 
 // keys -> canonical order + particle-block list (fl_sort.cu)
-void Ctx::sort_and_lists(StateBuf& st, Record& r) {
+// prev: the record of the substep that produced st (st is stored in its sort order) --
+// the incremental sort; nullptr: the full sort
+void Ctx::sort_and_lists(StateBuf& st, Record& r, const Record* prev) {
     Geom& g = geom;
     const DN n = dn(r.n_stored, slab() ? r.dcnt + RC_STORED : nullptr);
-    if (!counters_clean) CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
+    const bool keep = keep_counts();
+    const size_t bz = size_t(g.nbtot) + 2;
+    if (prev) {
+        const IncSort is{prev->recs, prev->blockmap, prev->celltab, okey[okey_cur].p, okey[okey_cur ^ 1].p,
+                         isort_blk.p, isort_blk.p + bz, isort_blk.p + 2 * bz, isort_blk.p + 3 * bz, mov.p, rold.p};
+        launch_isort_diff(g, st.p, r.n_stored, d_cls.p, bcount, bheavy, is, upload_full, stream);
+        launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, r.blockmap,
+                          r.n_blocks, tile_sum.p, &is, stream);
+        launch_isort_place(g, st.p, d_cls.p, bcount, bstart.p, r.recs, r.n_blocks, maxb, is, sslot.p, r.perm,
+                           r.celltab, gk.p, gv.p, grid_sort, 2 * sm_count, stream);
+        okey_cur ^= 1;
+        counters_clean = false;
+        n_inc_sorts++;
+        launches += 5;  // diff, list sums, list write, arrivals, per-block sort
+        return;
+    }
+    // the grid update clears bfill (counts kept) or all three arrays
+    if (!counters_clean)
+        CK(cudaMemsetAsync(bzero.p, 0, bzero.n * sizeof(int), stream));
+    else if (keep)
+        CK(cudaMemsetAsync(bzero.p, 0, 2 * bz * sizeof(int), stream));
     counters_clean = false;
     launch_sort_count(g, st.p, n, d_cls.p, bcount, bheavy, stream);
     launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, r.blockmap, r.n_blocks,
-                      tile_sum.p, stream);
-    launch_sort_scatter(g, st.p, n, bstart.p, bfill, skey.p, sslot.p, stream);
+                      tile_sum.p, nullptr, stream);
+    launch_sort_scatter(g, st.p, n, bstart.p, bfill, skey.p, sslot.p, keep ? d_cls.p : nullptr, stream);
     launch_sort_blocks(g, bcount, bstart.p, r.recs, r.n_blocks, maxb, skey.p, sslot.p, r.perm, r.celltab, gk.p, gv.p,
-                       grid_sort, stream);
+                       keep ? okey[okey_cur ^ 1].p : nullptr, grid_sort, stream);
+    if (keep) okey_cur ^= 1;
+    n_full_sorts++;
     launches += 5;  // count, list sums, list write, scatter, per-block sort
 }
 
@@ -1149,6 +1212,8 @@ void Ctx::sort_and_lists(StateBuf& st, Record& r) {
 // ---------------------------------------------------------------------------
 void Ctx::set_transport(std::unique_ptr<Transport> t) {
     comm = std::move(t);
+    counters_clean = false;  // the sort counts were kept on one rank: clear them all
+    chain_break();
     rank = comm->rank();
     nranks = comm->size();
     if (nranks > geom.NB[0]) throw FlumeError(FLUME_E_ARG, "more slab ranks than 4-cell columns along x");
@@ -1181,7 +1246,7 @@ void Ctx::set_mig_cap(int cap) {
         mig_recv[d].alloc(mig_msg_bytes(mig_cap));
     }
     rec_pool.clear();  // records carry per-capacity migration slot lists
-    scratch_rec = get_record();
+    new_scratch();
 }
 
 // Columns [cut[r], cut[r+1]) per rank, cut nearest to equal weight, at least
@@ -1368,13 +1433,16 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         }
         launches++;
     }
-    PROF(K_SORT, sort_and_lists(*in, r));
+    const Record* prev = (keep_counts() && r.act.empty() && chain_rec && chain_rec != &r && chain_out == in.get())
+                             ? chain_rec
+                             : nullptr;
+    PROF(K_SORT, sort_and_lists(*in, r, prev));
     PROF(K_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
              launch_p2g(geom, in->p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_p2g_h) : light_grid(grid_p2g), d_cls.p,
                         staging.p, d_err.p, uint32_t(substep_index), hv ? hvar : 0, w, s);
          }));
     // the adjoint's inputs (v0 = p/m, contact mask) only for substeps that keep a record
-    const bool keep = &r != scratch_rec.get();
+    const bool keep = !r.scratch;
     if (slab()) {
         // the halo planes travel on the comm stream while the interior node columns update
         // (they read no ghost tile); then the node-block list gains the blocks reached only
@@ -1395,8 +1463,8 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         launches += 3;
     } else {
         PROF(K_GRID, launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv,
-                                        keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, bzero.p,
-                                        int(bzero.n), stream));
+                                        keep ? r.gridv0 : nullptr, r.effk, keep ? r.cmask : nullptr, clear_ptr(),
+                                        clear_n(), stream));
     }
     counters_clean = true;
     RigidDev rd = rigid_dev(r);
@@ -1422,6 +1490,12 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
         launches += 3;
     }
     park_base = r.n_active;
+    if (keep_counts()) {  // out is stored in r's sort order
+        chain_rec = &r;
+        chain_out = out.get();
+    } else {
+        chain_break();
+    }
     if (slab()) {
         PROF(K_COMM, migrate(*out, r));
     } else {
@@ -1444,7 +1518,7 @@ void Ctx::substep(const double* action, int count) {
     }
     for (int i = 0; i < count; i++) {
         StatePtr nxt = get_state();
-        forward_substep(action, cur, nxt, *scratch_rec);
+        forward_substep(action, cur, nxt, next_scratch());
         put_state(cur);
         cur = nxt;
     }
@@ -1460,6 +1534,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
         return;
     }
     Record& r = *scratch_rec;
+    chain_break();  // this sort replaces the chained tables
     sync_counts();
     r.n_active = n_active;
     r.n_keep = n_active + n_parked();
@@ -1476,7 +1551,7 @@ void Ctx::stage_grid(double* mass, double* vel) {
         launch_flag_list(nbflag, geom.nbtot, r.nb_list, r.n_nb, nbpos.p, stream);
     }
     launch_grid_update(geom, r.nb_list, r.n_nb, grid_upd, r.blockmap, staging.p, r.gridv, r.gridv0, es, r.cmask,
-                       bzero.p, int(bzero.n), stream);
+                       clear_ptr(), clear_n(), stream);
     counters_clean = true;
     std::vector<float4> h(size_t(geom.nbtot) * 64);
     std::vector<int> bm(geom.nbtot);
@@ -1699,7 +1774,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     copy_state(*st, *cur);
     for (long t = 0; t < T; t++) {
         StatePtr nxt = get_state();
-        forward_substep(a->values + 6 * (t / a->segment_length), st, nxt, *scratch_rec);
+        forward_substep(a->values + 6 * (t / a->segment_length), st, nxt, next_scratch());
         put_state(st);
         st = nxt;
         if ((t + 1) % a->segment_length == 0) {
@@ -1918,6 +1993,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             cache_base = t;
             cache_states.push_back(st);
         }
+        if (!in_last) next_scratch();
         RecordPtr rec = in_last ? get_record() : scratch_rec;
         StatePtr nxt = get_state();
         eff_pre[t] = eff;
@@ -2384,6 +2460,22 @@ int flume_set_checkpoint_spill_dir(flume_ctx* ctx, const char* dir) {
 int flume_set_chamfer_mode(flume_ctx* ctx, int mode) {
     if (!ctx || mode < 0 || mode > 2) return FLUME_E_ARG;
     return guard(ctx, [&] { ctx->c.chamfer_mode = mode; });
+}
+
+int flume_set_incremental_sort(flume_ctx* ctx, int on) {
+    if (!ctx || on < 0 || on > 1) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.inc_sort = on != 0;
+        ctx->c.chain_break();
+        ctx->c.counters_clean = false;  // the counts' clearing rule changes with the mode
+    });
+}
+
+int flume_sort_stats(const flume_ctx* ctx, long* incremental, long* full) {
+    if (!ctx) return FLUME_E_ARG;
+    if (incremental) *incremental = ctx->c.n_inc_sorts;
+    if (full) *full = ctx->c.n_full_sorts;
+    return FLUME_OK;
 }
 
 int flume_last_error(const flume_ctx* ctx, flume_error_info* info) {

@@ -639,13 +639,13 @@ __global__ void k_rigid_apply(Geom g, PBuf out, RigidDev rd) {
     if (r >= rd.nmem) return;
     const int body = rd.member_body[r];
     const double* fit = rd.fit + 24 * size_t(body);
+    const int j = rd.mslot[r];
     // the fp64 member positions are replicated on every slab (mid is all-reduced)
     if (fit[22] != 0.0) {
         if (rd.mact[r] != 0.0)
             for (int a = 0; a < 3; a++) out.mx[3 * size_t(r) + a] = rd.mid[3 * size_t(r) + a];
         return;
     }
-    const int j = rd.mslot[r];
     const double* re = rd.rest + 3 * size_t(r);
     double xn[3];
     for (int a = 0; a < 3; a++) {

@@ -275,20 +275,44 @@ void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* 
                         const ClassInfo* cls, cudaStream_t s);
 void launch_expand_f(PBuf st, int n, const ClassInfo* cls, cudaStream_t s);
 
+// incremental sort (fl_sort.cu header): the previous substep's sort tables + context scratch
+struct IncSort {
+    const BlockRec* orecs;     // previous record: block list
+    const int* oblockmap;      // previous record: block map
+    const uint16_t* octab;     // previous record: cell tables
+    const uint32_t* okey_in;   // [n] the previous sort's key at every sorted position (bit 31: SVD/rigid)
+    uint32_t* okey_out;        // [n] this sort's
+    int* dirty;                // [nbtot + 2] blocks a particle entered, left or moved inside (zero between sorts)
+    int* acnt;                 // [nbtot + 2] arrivals per block (zero between sorts)
+    int* afill;                // [nbtot + 2] their fill cursors (zero between sorts)
+    int* nmov;                 // movers between blocks (zero between sorts)
+    uint32_t* mov;             // [n] their slots
+    int* rold;                 // [maxb] per list slot: previous list slot of a clean block, -1 = dirty
+};
+
 void launch_sort_count(const Geom& g, const PBuf& st, DN n, const ClassInfo* cls, int* bcount, int* bheavy,
                        cudaStream_t s);
+// cls_bit != nullptr: slot words carry the class bit (for the okey output of launch_sort_blocks)
 void launch_sort_scatter(const Geom& g, const PBuf& st, DN n, const int* bstart, int* bfill, uint32_t* skey,
-                         uint32_t* sslot, cudaStream_t s);
+                         uint32_t* sslot, const ClassInfo* cls_bit, cudaStream_t s);
 int sort_list_tiles(const Geom& g);
 void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
                        int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
-                       cudaStream_t s);
+                       const IncSort* inc, cudaStream_t s);
+// meta: the class bit can change (a liquid uploaded with a full F, kMetaFull, loses it in
+// G2P): compare it too; otherwise the key alone (the class bit is the particle's own)
+void launch_isort_diff(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
+                       const IncSort& is, bool meta, cudaStream_t s);
+void launch_isort_place(const Geom& g, const PBuf& st, const ClassInfo* cls, const int* bcount, const int* bstart,
+                        const BlockRec* recs, const int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
+                        uint32_t* perm, uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, int arrive_grid,
+                        cudaStream_t s);
 // id-ordered list of the nonzero flags (two-pass tile scan); tile_sum: flag_list_tiles(n) ints
 void launch_flag_list(const int* flags, int n, int* list, int* n_list, int* tile_sum, cudaStream_t s);
 int flag_list_tiles(int n);
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
-                        uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s);
+                        uint16_t* celltab, uint32_t* gk, uint32_t* gv, uint32_t* okey, int grid, cudaStream_t s);
 
 // ---- x-slab decomposition (fl_slab.cu) ----
 size_t halo_bytes(const Geom& g);

@@ -156,6 +156,13 @@ __device__ __forceinline__ void pdl_wait() {
 
 __host__ __device__ inline int key_col(const Geom& g, uint32_t key) { return int(key >> 6) / g.colblocks; }
 
+// sort block of a key: its particle block, or the virtual parked / departed blocks nbtot, nbtot + 1
+__host__ __device__ inline int key_block(const Geom& g, uint32_t key) {
+    return key >= g.key_inactive ? g.nbtot + int((key - g.key_inactive) >> 6) : int(key >> 6);
+}
+// bit 31 of a sorted key word (okey) / sort slot word: the particle takes the SVD/rigid path
+constexpr uint32_t kHeavyBit = 0x80000000u;
+
 __host__ __device__ inline size_t node_index(const Geom& g, int i, int j, int k) {
     return size_t(block_lin(g, i >> 2, j >> 2, k >> 2)) * 64 + (((i & 3) << 4) | ((j & 3) << 2) | (k & 3));
 }

@@ -17,6 +17,26 @@
 // The resulting permutation is unique, so it is bit-identical to any other
 // stable (key, id) sort -- the same order the CPU parity test recomputes.
 // The block count array doubles as the particle-block list for the kernels.
+//
+// Incremental sort (one rank, substeps chained by forward_substep).  G2P writes state t+1
+// in the sorted order of substep t and a particle moves ~0.003 cells per substep, so
+// nearly every key is unchanged.  Each sort also writes `okey`, the key at every sorted
+// position (bit 31: an SVD/rigid particle), and keeps the block counts.  The next sort:
+//   1. diff: key (+ class bit) against okey; a changed particle marks its old and new
+//      block dirty, and one that changed block updates both counts, the heavy counts
+//      and the arrival count and joins the mover list.  The class bit only changes for a
+//      liquid uploaded with a full F (kMetaFull, dropped by its first G2P); otherwise the
+//      key alone is compared (8 bytes per particle).  (Doing this in G2P instead, where
+//      the keys are written, cost G2P more than the kernel: c4 +3.7 us, spills.)
+//   2. the list scan as above (new segment starts); for every listed block it also
+//      records the previous list slot of a clean block (rold) and clears the dirty flags
+//   3. movers are placed at the ends of their new blocks' segments
+//   4. one CTA per block: a clean block copies its old segment in order (perm = the old
+//      sorted positions, cell table and okey copied); a dirty block collects the
+//      stayers of its old segment and its arrivals and sorts them as in step 4 above
+// Counts and the permutation are the full sort's by construction (bit-identical,
+// tested against it); activation substeps, slabs and the first substep after any
+// other state write use the full sort.
 #include <cuda_runtime.h>
 
 #include <cub/block/block_reduce.cuh>
@@ -44,6 +64,10 @@ constexpr int kSortThreads = FL_SORT_THREADS;
 #endif
 constexpr int kSortItems = FL_SORT_ITEMS;
 
+__device__ __forceinline__ uint32_t heavy_bit(const ClassInfo* __restrict__ cls, uint32_t meta) {
+    return (cls[meta_cls(meta)].heavy != 0 || (meta & kMetaFull) != 0u) ? kHeavyBit : 0u;
+}
+
 __global__ void k_sort_count(Geom g, PBuf st, DN nn, const ClassInfo* __restrict__ cls, int* bcount,
                              int* bheavy) {
     pdl_wait();
@@ -67,22 +91,24 @@ __global__ void k_sort_count(Geom g, PBuf st, DN nn, const ClassInfo* __restrict
         const int leader = __ffs(peers) - 1;
         if ((threadIdx.x & 31) == leader) {
             atomicAdd(&bcount[b], __popc(peers));
-            if (heavy) atomicOr(&bheavy[b], 1);
+            if (heavy) atomicAdd(&bheavy[b], __popc(heavy));  // a count: the incremental sort updates it
         }
     }
 }
 
+// cls != nullptr: the slot word carries the class bit (kHeavyBit) for the okey output
 __global__ void k_sort_scatter(Geom g, PBuf st, DN nn, const int* __restrict__ bstart, int* bfill, uint32_t* skey,
-                               uint32_t* sslot) {
+                               uint32_t* sslot, const ClassInfo* __restrict__ cls) {
     pdl_wait();
     const int n = nn.get();
     const int i0 = blockIdx.x * blockDim.x * kSortItems + threadIdx.x;
-    uint32_t key[kSortItems], id[kSortItems];
+    uint32_t key[kSortItems], id[kSortItems], hb[kSortItems];
 #pragma unroll
     for (int q = 0; q < kSortItems; q++) {
         const int i = i0 + q * blockDim.x;
         key[q] = i < n ? st.key[i] : 0u;
         id[q] = i < n ? st.id[i] : 0u;
+        hb[q] = (cls && i < n) ? heavy_bit(cls, st.meta[i]) : 0u;
     }
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -98,7 +124,7 @@ __global__ void k_sort_scatter(Geom g, PBuf st, DN nn, const int* __restrict__ b
         base = __shfl_sync(peers, base, leader);
         const int p = bstart[b] + base + __popc(peers & ((1u << lane) - 1));
         skey[p] = ((inact ? 0u : (key[q] & 63u)) << 26) | id[q];
-        sslot[p] = uint32_t(i);
+        sslot[p] = uint32_t(i) | hb[q];
     }
 }
 
@@ -142,21 +168,102 @@ __device__ void cell_starts(KP k, int cnt, uint16_t* out, int tid) {
 
 constexpr int kCountCap = FL_COUNT_CAP;  // particles per block segment sorted by the counting path
 
-// One CTA per non-empty particle block: counting sort of the segment by local
-// cell (64 buckets), then every particle ranks itself inside its cell's run by
-// particle id (runs are ~8 long; measured 12% faster than a per-cell insertion sort).  The inactive tail and oversized segments use the
-// bitonic network instead.
-__global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const int* __restrict__ bcount,
+struct SegSmem {
+    uint32_t ik[kCountCap], iv[kCountCap], ok[kCountCap], ov[kCountCap];
+    int hist[64], fill[64];
+    uint16_t cs[kCellTab];
+    int n;
+};
+
+// Sorts the cnt (key, slot word) pairs in sm.ik / sm.iv (key = local cell << 26 | id,
+// slot word = slot | class bit) into the segment at s0: counting sort by cell, then every
+// particle ranks itself inside its cell's run by particle id (runs are ~8 long; measured
+// 12% faster than a per-cell insertion sort).  Writes perm, the cell table ct and, when
+// okey is given, the sorted keys (block word = block << 6).  The caller loaded ik / iv.
+__device__ void seg_count_sort(SegSmem& sm, int cnt, int s0, uint32_t bword, uint32_t* perm, uint16_t* ct,
+                               uint32_t* okey) {
+    const int tid = threadIdx.x;
+    if (tid < 64) sm.hist[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < cnt; i += kSortThreads) atomicAdd(&sm.hist[sm.ik[i] >> 26], 1);
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of 64 counts by one warp
+        int a = sm.hist[2 * tid], b = sm.hist[2 * tid + 1];
+        int s = a + b, incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += t;
+        }
+        const int ex = incl - s;
+        sm.cs[2 * tid] = uint16_t(ex);
+        sm.cs[2 * tid + 1] = uint16_t(ex + a);
+        sm.fill[2 * tid] = ex;
+        sm.fill[2 * tid + 1] = ex + a;
+        int mx = a > b ? a : b;  // largest cell: the scatter kernels' pass count
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int t = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = t > mx ? t : mx;
+        }
+        if (tid == 31) {
+            sm.cs[64] = uint16_t(incl);
+            sm.cs[65] = uint16_t(mx);
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < cnt; i += kSortThreads) {
+        const int p = atomicAdd(&sm.fill[sm.ik[i] >> 26], 1);
+        sm.ok[p] = sm.ik[i];
+        sm.ov[p] = sm.iv[i];
+    }
+    __syncthreads();
+    // each particle's place inside its cell run = the number of run members with a
+    // smaller key (keys are unique: they carry the particle id); all threads busy
+    for (int i = tid; i < cnt; i += kSortThreads) {
+        const uint32_t kk = sm.ok[i];
+        const int c = int(kk >> 26);
+        const int a = sm.cs[c], e = sm.cs[c + 1];
+        int rnk = 0;
+        for (int j = a; j < e; j++) rnk += sm.ok[j] < kk ? 1 : 0;
+        perm[s0 + a + rnk] = sm.ov[i] & ~kHeavyBit;
+        if (okey) okey[s0 + a + rnk] = (bword | uint32_t(c)) | (sm.ov[i] & kHeavyBit);
+    }
+    if (tid < kCellTab) ct[tid] = sm.cs[tid];
+    __syncthreads();
+}
+
+// The same for a segment above the shared capacity (or the inactive tail, ct == nullptr,
+// ordered by id): bitonic network on the global scratch copy k / v (loaded by the caller,
+// padded to a power of two with 0xffffffff keys).
+__device__ void seg_bitonic_sort(uint32_t* k, uint32_t* v, int cnt, int np, int s0, uint32_t bword, uint32_t* perm,
+                                 uint16_t* ct, uint32_t* okey) {
+    const int tid = threadIdx.x;
+    bitonic(k, v, np, tid, kSortThreads);
+    for (int i = tid; i < cnt; i += kSortThreads) {
+        perm[s0 + i] = v[i] & ~kHeavyBit;
+        if (okey) okey[s0 + i] = (ct ? (bword | (k[i] >> 26)) : bword) | (v[i] & kHeavyBit);
+    }
+    if (ct) cell_starts(k, cnt, ct, tid);
+    __syncthreads();
+    if (ct && tid == 0) {
+        int mx = 0;
+        for (int c = 0; c < 64; c++) mx = max(mx, int(ct[c + 1]) - int(ct[c]));
+        ct[65] = uint16_t(mx);
+    }
+}
+
+// One CTA per non-empty particle block (full sort).  okey != nullptr: also write the
+// sorted keys for the next substep's incremental sort.
+__global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int* __restrict__ bcount,
                                                               const int* __restrict__ bstart,
                                                               const BlockRec* __restrict__ recs,
                                                               const int* __restrict__ n_blocks, int cap,
                                                               const uint32_t* skey, const uint32_t* sslot,
                                                               uint32_t* perm, uint16_t* celltab, uint32_t* gk,
-                                                              uint32_t* gv) {
+                                                              uint32_t* gv, uint32_t* okey) {
     pdl_wait();
-    __shared__ uint32_t ik[kCountCap], iv[kCountCap], ok[kCountCap], ov[kCountCap];
-    __shared__ int hist[64], fill[64];
-    __shared__ uint16_t cs[kCellTab];
+    __shared__ SegSmem sm;
     const int nl = n_blocks[0], nh = n_blocks[1];
     const int nb = nl + nh;
     const int tid = threadIdx.x;
@@ -165,68 +272,24 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
         // w == nb: the inactive tail (ordered by id); w == nb + 1: departed slots (any order)
         const int q = w < nl ? w : cap - 1 - (w - nl);
         const bool act = w < nb;
-        const int cnt = act ? recs[q].end - recs[q].start : bcount[nbtot + (w - nb)];
+        const int cnt = act ? recs[q].end - recs[q].start : bcount[g.nbtot + (w - nb)];
         if (cnt == 0) continue;
-        const int s0 = act ? recs[q].start : bstart[nbtot + (w - nb)];
+        const int s0 = act ? recs[q].start : bstart[g.nbtot + (w - nb)];
         if (w == nb + 1) {
-            for (int i = tid; i < cnt; i += kSortThreads) perm[s0 + i] = sslot[s0 + i];
+            for (int i = tid; i < cnt; i += kSortThreads) {
+                perm[s0 + i] = sslot[s0 + i] & ~kHeavyBit;
+                if (okey) okey[s0 + i] = g.key_departed | (sslot[s0 + i] & kHeavyBit);
+            }
             continue;
         }
+        const uint32_t bword = act ? uint32_t(recs[q].block) << 6 : g.key_inactive;
         if (act && cnt <= kCountCap) {
             for (int i = tid; i < cnt; i += kSortThreads) {
-                ik[i] = skey[s0 + i];
-                iv[i] = sslot[s0 + i];
+                sm.ik[i] = skey[s0 + i];
+                sm.iv[i] = sslot[s0 + i];
             }
-            if (tid < 64) hist[tid] = 0;
-            __syncthreads();
-            for (int i = tid; i < cnt; i += kSortThreads) atomicAdd(&hist[ik[i] >> 26], 1);
-            __syncthreads();
-            if (tid < 32) {  // exclusive scan of 64 counts by one warp
-                int a = hist[2 * tid], b = hist[2 * tid + 1];
-                int s = a + b, incl = s;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (tid >= o) incl += t;
-                }
-                const int ex = incl - s;
-                cs[2 * tid] = uint16_t(ex);
-                cs[2 * tid + 1] = uint16_t(ex + a);
-                fill[2 * tid] = ex;
-                fill[2 * tid + 1] = ex + a;
-                int mx = a > b ? a : b;  // largest cell: the scatter kernels' pass count
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const int t = __shfl_xor_sync(0xffffffffu, mx, o);
-                    mx = t > mx ? t : mx;
-                }
-                if (tid == 31) {
-                    cs[64] = uint16_t(incl);
-                    cs[65] = uint16_t(mx);
-                }
-            }
-            __syncthreads();
-            for (int i = tid; i < cnt; i += kSortThreads) {
-                const int p = atomicAdd(&fill[ik[i] >> 26], 1);
-                ok[p] = ik[i];
-                ov[p] = iv[i];
-            }
-            __syncthreads();
-            // each particle's place inside its cell run = the number of run members with a
-            // smaller key (keys are unique: they carry the particle id); all threads busy
-            for (int i = tid; i < cnt; i += kSortThreads) {
-                const uint32_t kk = ok[i];
-                const int c = int(kk >> 26);
-                const int a = cs[c], e = cs[c + 1];
-                int rnk = 0;
-                for (int j = a; j < e; j++) rnk += ok[j] < kk ? 1 : 0;
-                perm[s0 + a + rnk] = ov[i];
-            }
-            if (tid < kCellTab) celltab[size_t(q) * kCellTab + tid] = cs[tid];
-            __syncthreads();
+            seg_count_sort(sm, cnt, s0, bword, perm, celltab + size_t(q) * kCellTab, okey);
         } else {
-            // inactive tail or oversized block: bitonic network on a global scratch copy
-            uint16_t* ct = act ? celltab + size_t(q) * kCellTab : nullptr;
             int np = 1;
             while (np < cnt) np <<= 1;
             uint32_t* k = gk + size_t(s0) * 2;
@@ -236,15 +299,145 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(int nbtot, const i
                 v[i] = i < cnt ? sslot[s0 + i] : 0u;
             }
             __syncthreads();
-            bitonic(k, v, np, tid, kSortThreads);
-            for (int i = tid; i < cnt; i += kSortThreads) perm[s0 + i] = v[i];
-            if (ct) cell_starts(k, cnt, ct, tid);
-            __syncthreads();
-            if (ct && tid == 0) {
-                int mx = 0;
-                for (int c = 0; c < 64; c++) mx = max(mx, int(ct[c + 1]) - int(ct[c]));
-                ct[65] = uint16_t(mx);
+            seg_bitonic_sort(k, v, cnt, np, s0, bword, perm, act ? celltab + size_t(q) * kCellTab : nullptr, okey);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// incremental sort (see the header)
+// ---------------------------------------------------------------------------
+template <bool META>
+__global__ void k_isort_diff(Geom g, PBuf st, int n, const ClassInfo* __restrict__ cls,
+                             const uint32_t* __restrict__ okey, int* bcount, int* bheavy, int* acnt, int* dirty,
+                             int* nmov, uint32_t* mov) {
+    pdl_wait();
+    const int i0 = blockIdx.x * blockDim.x * kSortItems + threadIdx.x;
+    uint32_t key[kSortItems], meta[kSortItems], ok[kSortItems];
+#pragma unroll
+    for (int q = 0; q < kSortItems; q++) {
+        const int i = i0 + q * blockDim.x;
+        key[q] = i < n ? st.key[i] : 0u;
+        if (META) meta[q] = i < n ? st.meta[i] : 0u;
+        ok[q] = i < n ? okey[i] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kSortItems; q++) {
+        const int i = i0 + q * blockDim.x;
+        if (i >= n) break;
+        const uint32_t nk = key[q] | (META ? heavy_bit(cls, meta[q]) : (ok[q] & kHeavyBit));
+        if (nk == ok[q]) continue;
+        const int ob = key_block(g, ok[q] & ~kHeavyBit), nb = key_block(g, key[q]);
+        const int oh = int(ok[q] >> 31), nh = int(nk >> 31);
+        dirty[ob] = 1;
+        dirty[nb] = 1;
+        if (ob != nb) {
+            atomicSub(&bcount[ob], 1);
+            atomicAdd(&bcount[nb], 1);
+            if (oh) atomicSub(&bheavy[ob], 1);
+            if (nh) atomicAdd(&bheavy[nb], 1);
+            atomicAdd(&acnt[nb], 1);
+            mov[atomicAdd(nmov, 1)] = uint32_t(i);
+        } else if (oh != nh) {
+            atomicAdd(&bheavy[nb], nh - oh);
+        }
+    }
+}
+
+// movers go to the end of their new block's segment (any order: the block sort orders them)
+__global__ void k_isort_arrive(Geom g, PBuf st, const int* __restrict__ nmov, const uint32_t* __restrict__ mov,
+                               const int* __restrict__ bcount, const int* __restrict__ bstart,
+                               const int* __restrict__ acnt, int* afill, uint32_t* sslot) {
+    pdl_wait();
+    const int m = *nmov;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const uint32_t p = mov[i];
+        const int b = key_block(g, st.key[p]);
+        sslot[bstart[b] + bcount[b] - acnt[b] + atomicAdd(&afill[b], 1)] = p;
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, const ClassInfo* __restrict__ cls,
+                                                               const int* __restrict__ bcount,
+                                                               const int* __restrict__ bstart,
+                                                               const BlockRec* __restrict__ recs,
+                                                               const int* __restrict__ n_blocks, int cap, IncSort is,
+                                                               const uint32_t* sslot, uint32_t* perm,
+                                                               uint16_t* celltab, uint32_t* gk, uint32_t* gv) {
+    pdl_wait();
+    __shared__ SegSmem sm;
+    const int nl = n_blocks[0], nh = n_blocks[1];
+    const int nb = nl + nh;
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && tid == 0) *is.nmov = 0;  // the arrival pass has read it
+    for (int w = blockIdx.x; w <= nb; w += gridDim.x) {
+        if (w == nb) {  // the inactive tail: unchanged without activation
+            const int s0 = bstart[g.nbtot], cnt = bcount[g.nbtot];
+            for (int i = tid; i < cnt; i += kSortThreads) {
+                perm[s0 + i] = uint32_t(s0 + i);
+                is.okey_out[s0 + i] = is.okey_in[s0 + i];
             }
+            continue;
+        }
+        const int q = w < nl ? w : cap - 1 - (w - nl);
+        const BlockRec r = recs[q];
+        const int cnt = r.end - r.start, s0 = r.start;
+        uint16_t* ct = celltab + size_t(q) * kCellTab;
+        const int oq = is.rold[q];
+        if (oq >= 0) {  // clean: the old segment, in order
+            const int os0 = is.orecs[oq].start;
+            for (int i = tid; i < cnt; i += kSortThreads) {
+                perm[s0 + i] = uint32_t(os0 + i);
+                is.okey_out[s0 + i] = is.okey_in[os0 + i];
+            }
+            if (tid < kCellTab) ct[tid] = is.octab[size_t(oq) * kCellTab + tid];
+            continue;
+        }
+        // dirty: the stayers of the old segment + the arrivals, sorted
+        const int obm = is.oblockmap[r.block];
+        const int os0 = obm > 0 ? is.orecs[obm - 1].start : 0, oe = obm > 0 ? is.orecs[obm - 1].end : 0;
+        const int na = is.acnt[r.block];
+        const int a0 = s0 + cnt - na;
+        const bool fits = cnt <= kCountCap;
+        int np = 1;
+        while (np < cnt) np <<= 1;
+        uint32_t* k = gk + size_t(s0) * 2;
+        uint32_t* v = gv + size_t(s0) * 2;
+        if (tid == 0) sm.n = 0;
+        __syncthreads();
+        for (int i = tid; i < (oe - os0) + na; i += kSortThreads) {
+            const uint32_t p = i < oe - os0 ? uint32_t(os0 + i) : sslot[a0 + (i - (oe - os0))];
+            const uint32_t key = st.key[p];
+            if (i < oe - os0 && key_block(g, key) != r.block) continue;  // left the block
+            const uint32_t kk = ((key & 63u) << 26) | st.id[p];
+            const uint32_t vv = p | heavy_bit(cls, st.meta[p]);
+            const int j = atomicAdd(&sm.n, 1);
+            if (fits) {
+                sm.ik[j] = kk;
+                sm.iv[j] = vv;
+            } else {
+                k[j] = kk;
+                v[j] = vv;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (sm.n != cnt) __trap();  // the counts and the members disagree: cannot happen
+            if (na) {
+                is.acnt[r.block] = 0;
+                is.afill[r.block] = 0;
+            }
+        }
+        const uint32_t bword = uint32_t(r.block) << 6;
+        if (fits) {
+            seg_count_sort(sm, cnt, s0, bword, perm, ct, is.okey_out);
+        } else {
+            for (int i = cnt + tid; i < np; i += kSortThreads) {
+                k[i] = 0xffffffffu;
+                v[i] = 0u;
+            }
+            __syncthreads();
+            seg_bitonic_sort(k, v, cnt, np, s0, bword, perm, ct, is.okey_out);
         }
     }
 }
@@ -257,17 +450,36 @@ void launch_sort_count(const Geom& g, const PBuf& st, DN n, const ClassInfo* cls
              bcount, bheavy);
 }
 void launch_sort_scatter(const Geom& g, const PBuf& st, DN n, const int* bstart, int* bfill, uint32_t* skey,
-                         uint32_t* sslot, cudaStream_t s) {
+                         uint32_t* sslot, const ClassInfo* cls_bit, cudaStream_t s) {
     if (n.h <= 0) return;
     launch_k(k_sort_scatter, dim3((n.h + 256 * kSortItems - 1) / (256 * kSortItems)), dim3(256), 0, s, g, st, n,
-             bstart, bfill, skey, sslot);
+             bstart, bfill, skey, sslot, cls_bit);
+}
+
+void launch_isort_diff(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
+                       const IncSort& is, bool meta, cudaStream_t s) {
+    if (n <= 0) return;
+    launch_k(meta ? k_isort_diff<true> : k_isort_diff<false>, dim3((n + 256 * kSortItems - 1) / (256 * kSortItems)),
+             dim3(256), 0, s, g, st, n, cls, (const uint32_t*)is.okey_in, bcount, bheavy, is.acnt, is.dirty, is.nmov,
+             is.mov);
+}
+void launch_isort_place(const Geom& g, const PBuf& st, const ClassInfo* cls, const int* bcount, const int* bstart,
+                        const BlockRec* recs, const int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
+                        uint32_t* perm, uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, int arrive_grid,
+                        cudaStream_t s) {
+    launch_k(k_isort_arrive, dim3(arrive_grid), dim3(256), 0, s, g, st, (const int*)is.nmov, (const uint32_t*)is.mov,
+             bcount, bstart, (const int*)is.acnt, is.afill, sslot);
+    launch_k(k_isort_blocks, dim3(grid), dim3(kSortThreads), 0, s, g, st, cls, bcount, bstart, recs, n_blocks, cap, is,
+             (const uint32_t*)sslot, perm, celltab, gk, gv);
 }
 
 // ---------------------------------------------------------------------------
 // step 2: 4-channel scan over the nbtot + 2 block counts (particles, touched
 // node blocks, plain-liquid blocks, SVD/rigid blocks) in two passes of
-// 2048-block tiles: tile sums, then every tile adds its predecessors' sums
-// (<= a few hundred) and writes its outputs.  Deterministic, no atomics.
+// 256-block tiles: tile sums, then every tile adds its predecessors' sums
+// (<= a few hundred) and writes its outputs.  Deterministic, no atomics.  (A one-pass
+// decoupled look-back scan was measured slower on c4: 256-block tiles +2 us, 1024-block
+// tiles +4 us per sort -- the look-back chain costs more than the kernel boundary.)
 // ---------------------------------------------------------------------------
 constexpr int kListThreads = 256;
 #ifndef FL_LIST_ITEMS
@@ -334,7 +546,8 @@ __global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, co
                                                              const int* __restrict__ nbflag,
                                                              const int4* __restrict__ tile_sum, int* bstart,
                                                              int* nb_list, int* n_nb, BlockRec* recs, int* blockmap,
-                                                             int* n_blocks) {
+                                                             int* n_blocks, const int* __restrict__ oblockmap,
+                                                             int* rold, int* dirty) {
     pdl_wait();
     using Scan = cub::BlockScan<int4, kListThreads>;
     __shared__ typename Scan::TempStorage tmp;
@@ -382,7 +595,10 @@ __global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, co
             if (kind[k] == 2) slot = cap - pre.w;  // SVD/rigid blocks fill recs from the back
             if (slot) recs[slot - 1] = BlockRec{b, pre.x, pre.x + cnt[k]};
             blockmap[b] = slot;
+            // incremental sort: a clean block copies its old segment (its previous list slot)
+            if (rold && slot) rold[slot - 1] = dirty[b] ? -1 : oblockmap[b] - 1;
         }
+        if (dirty) dirty[b] = 0;
         pre.x += cnt[k];
         pre.y += flag[k];
         pre.z += kind[k] == 1;
@@ -400,11 +616,12 @@ int sort_list_tiles(const Geom& g) { return (g.nbtot + 2 + kListTile - 1) / kLis
 
 void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
                        int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
-                       cudaStream_t s) {
+                       const IncSort* inc, cudaStream_t s) {
     const int tiles = sort_list_tiles(g);
     launch_k(k_list_sums, dim3(tiles), dim3(kListThreads), 0, s, g, bcount, bheavy, nbflag, tile_sum);
-    launch_k(k_list_write, dim3(tiles), dim3(kListThreads), 0, s, g, cap, bcount, bheavy, nbflag, tile_sum, bstart, nb_list, n_nb,
-                                                recs, blockmap, n_blocks);
+    launch_k(k_list_write, dim3(tiles), dim3(kListThreads), 0, s, g, cap, bcount, bheavy, nbflag, tile_sum, bstart,
+             nb_list, n_nb, recs, blockmap, n_blocks, inc ? inc->oblockmap : nullptr, inc ? inc->rold : nullptr,
+             inc ? inc->dirty : nullptr);
 }
 
 // Slabs: the node-block list again after the halo unpack flagged the blocks reached
@@ -451,8 +668,8 @@ int flag_list_tiles(int n) { return (n + kListThreads - 1) / kListThreads; }
 
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
                         const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
-                        uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, cudaStream_t s) {
-    launch_k(k_sort_blocks, dim3(grid), dim3(kSortThreads), 0, s, g.nbtot, bcount, bstart, recs, n_blocks, cap, skey, sslot, perm,
-                                                celltab, gk, gv);
+                        uint16_t* celltab, uint32_t* gk, uint32_t* gv, uint32_t* okey, int grid, cudaStream_t s) {
+    launch_k(k_sort_blocks, dim3(grid), dim3(kSortThreads), 0, s, g, bcount, bstart, recs, n_blocks, cap, skey, sslot,
+             perm, celltab, gk, gv, okey);
 }
 }  // namespace fl
