@@ -216,6 +216,24 @@ int flume_scene_optimizer_get(const flume_scene* s, int* n_segments, int* segmen
 
 /* ---- context ---- */
 int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out);
+/* ---- replica contexts (a CMA-ES population, optimize.hpp:383-418) ----
+ * n_replicas copies of one scene side by side in one grid (one empty 4-cell column between
+ * them; positions stay replica-local), so every kernel launch of a substep covers the whole
+ * population.  Particle i of replica r is r * n_particles + i and effector e is
+ * r * n_effectors + e in every state view (flume_state_upload / download take the
+ * concatenated arrays); body b is r * body_stride + b.  flume_substep takes n_replicas x 6
+ * action values.  Each replica's state evolves bit-identically to a single context's.
+ * Forward rollouts only: grad_trajectory, adjoint_substep, stage_grid and
+ * loss_per_particle return FLUME_E_ARG. */
+int flume_ctx_create_replicas(const flume_scene_desc* desc, int n_replicas, int device, flume_ctx** out);
+/* rollout_loss (grad.hpp:15-41) of every replica: actions->values = n_segments x n_replicas x 6
+ * (segment-major), `loss` is the scene's own description (applied to each replica's bodies);
+ * loss_out[n_replicas], per_segment[n_replicas x n_segments] (may be NULL).  keep_final != 0:
+ * the context continues from the final states (flume_rollout_loss_final). */
+int flume_replicas_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss,
+                                long window, int keep_final, double* loss_out, double* per_segment);
+int flume_replicas_info(const flume_ctx* ctx, int* n_replicas, long* particles_per_replica,
+                        int* effectors_per_replica, int* body_stride);
 int flume_ctx_destroy(flume_ctx* ctx);
 int flume_set_mode(flume_ctx* ctx, int deterministic, int hard_contact);
 int flume_last_error(const flume_ctx* ctx, flume_error_info* info);

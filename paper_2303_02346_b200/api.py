@@ -959,6 +959,94 @@ def rollout_loss_batch(scene: Scene, state0: SimState, population: Sequence[Acti
                      list(population))
 
 
+class ReplicaWorkspace(GpuWorkspace):
+    """One device context holding `n_replicas` copies of a scene side by side in one grid
+    (flume_ctx_create_replicas, the CMA-ES population of
+    optimize.hpp:383-418): every kernel launch of a substep covers the whole population, so
+    small scenes fill the GPU.  Positions stay replica-local and each replica's state
+    evolves bit-identically to a single context's.  Forward rollouts only."""
+
+    def __init__(self, scene: Scene, n_replicas: int, device: int = 0):
+        self.lib = load()
+        self.scene = scene
+        self.n_replicas = int(n_replicas)
+        self.ctx = C.c_void_p()
+        rc = self.lib.flume_ctx_create_replicas(C.byref(scene.desc), self.n_replicas, device, C.byref(self.ctx))
+        if rc != _abi.FLUME_OK:
+            _raise(self.lib, None, rc)
+        self.ctxs = [self.ctx]
+        self._resident = None
+        self._resident_ver = -1
+        self._ctx_time = 0.0
+        self._ctx_substep = 0
+
+    def replicate(self, states) -> SimState:
+        """The population state: one SimState per replica (or one, repeated), concatenated by
+        particle id and effector index.  One repeated state is cached, so a population
+        evaluated again from the same initial state (every CMA-ES generation) stays resident."""
+        if isinstance(states, SimState):
+            c = getattr(self, "_rep_cache", None)
+            if c is not None and c[0] is states and c[1] == states._ver and c[2]._ws is None:
+                return c[2]
+            pop = self.replicate([states] * self.n_replicas)
+            self._rep_cache = (states, states._ver, pop)
+            return pop
+        if len(states) != self.n_replicas:
+            raise ValueError(f"need {self.n_replicas} states")
+        for s in states:
+            s._pull()
+        t0, k0 = states[0]._time, states[0]._substep
+        if any(s._time != t0 or s._substep != k0 for s in states):
+            raise ValueError("replicas advance in lockstep: every state must be at the same substep")
+        cat = lambda name: np.concatenate([getattr(s, name) for s in states])  # noqa: E731
+        return SimState(cat("_x"), cat("_v"), cat("_F"), cat("_C"), cat("_eff"), t0, k0)
+
+    def split(self, pop: SimState) -> List[SimState]:
+        """Per-replica SimStates of a population state."""
+        pop._pull()
+        n1 = pop.n_particles // self.n_replicas
+        e1 = pop._eff.shape[0] // self.n_replicas
+        return [SimState(pop._x[r * n1:(r + 1) * n1].copy(), pop._v[r * n1:(r + 1) * n1].copy(),
+                         pop._F[r * n1:(r + 1) * n1].copy(), pop._C[r * n1:(r + 1) * n1].copy(),
+                         pop._eff[r * e1:(r + 1) * e1].copy(), pop._time, pop._substep)
+                for r in range(self.n_replicas)]
+
+
+def rollout_loss_replicas(scene: Scene, state0, population: Sequence[ActionTrajectory], loss: LossEvaluator,
+                          ws: ReplicaWorkspace, window: int = 0, per_segment: Optional[list] = None,
+                          final_states: Optional[list] = None) -> List[float]:
+    """rollout_loss (grad.hpp:15-41) of a whole population in one replica context: one kernel
+    launch per stage covers every candidate.  state0: the common initial SimState (or one per
+    replica); per_segment / final_states (lists) receive each replica's per-segment losses
+    and final state."""
+    ws = _ws_for(scene, ws)
+    pop = list(population)
+    R = ws.n_replicas
+    if len(pop) != R:
+        raise ValueError(f"the replica context holds {R} candidates, got {len(pop)}")
+    nseg, seglen = pop[0].n_segments, pop[0].segment_length
+    if any(a.n_segments != nseg or a.segment_length != seglen for a in pop):
+        raise ValueError("every candidate needs the same segment layout")
+    st = ws.replicate(state0)
+    ws._upload(st)
+    vals = np.ascontiguousarray(np.stack([a.values for a in pop], axis=1))  # (n_segments, R, 6)
+    a = _abi.Actions()
+    a.n_segments, a.segment_length, a.values = nseg, seglen, _dp(vals)
+    out = np.zeros(R)
+    per = np.zeros(R * nseg)
+    keep = final_states is not None
+    ws._check(ws.lib.flume_replicas_rollout_loss(ws.ctx, C.byref(a), C.byref(loss.desc), int(window), int(keep),
+                                                 _dp(out), _dp(per)))
+    if per_segment is not None:
+        per_segment[:] = [per[r * nseg:(r + 1) * nseg].copy() for r in range(R)]
+    if keep:
+        ws._resident = None
+        ws._rep_cache = None  # st now holds the final states
+        ws._download(st)
+        final_states[:] = ws.split(st)
+    return out.tolist()
+
+
 def grad_trajectory_batch(scene: Scene, state0: SimState, population: Sequence[ActionTrajectory],
                           loss: LossEvaluator, pool: WorkspacePool, stride: int = 0,
                           window: int = 0) -> List[TrajectoryGrad]:

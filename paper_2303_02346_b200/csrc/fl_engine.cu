@@ -619,7 +619,26 @@ struct Ctx {
         return d;
     }
 
-    void init(const flume_scene_desc* desc, int dev);
+    void init(const flume_scene_desc* desc, int dev, int n_replicas = 1);
+    // replica contexts (the CMA-ES population of optimize.hpp:383-418): n_rep
+    // copies of one scene in one grid (Geom::rstride), every kernel launch covering all of them.
+    // Particle i of replica r is id r * n1 + i, effector e is r * e1 + e, body b is
+    // r * body_stride + b; actions are n_rep x 6 per substep.
+    int nrep = 1, n1 = 0, e1 = 0, body_stride = 0;
+    int act_stride() const { return 6 * nrep; }
+    void require_single(const char* what) const {
+        if (nrep > 1) throw FlumeError(FLUME_E_ARG, std::string(what) + ": not available on a replica context");
+    }
+    // replica contexts: the effector set travels in device memory (a ring of per-substep
+    // copies from pinned memory; a slot is reused once its copy has run)
+    static constexpr int kEffRingRep = 64;
+    EffK<float>* h_effring = nullptr;
+    DevArr<EffK<float>> d_effring;
+    std::vector<cudaEvent_t> effring_ev;
+    int effring_i = 0;
+    void fill_effk(size_t i, const EffState& e, EffK<float>& k) const;
+    EffSet replica_effset();
+    EffSet effset_now() { return nrep > 1 ? replica_effset() : make_effset(eff); }
     void check_error(long substep_base = 0);
     EffSet make_effset(const std::vector<EffState>& es) const;
     void advance_effectors(const double* action);
@@ -677,8 +696,9 @@ struct Ctx {
     }
     uint32_t loss_mask(const flume_loss_desc* loss, int seg, int nseg) const;
     void eval_loss(StateBuf& st, const LossSet& ls, uint32_t mask, double* out_dev, int seg, long substep);
+    // rep_total (replica contexts): the n_rep losses; per_seg then holds n_rep x n_segments
     double rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg,
-                        bool keep_final = false);
+                        bool keep_final = false, double* rep_total = nullptr);
     void adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float>& bars_post, DevArr<float>& bars_pre,
                       int t_slot);
     void grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
@@ -692,7 +712,7 @@ struct Ctx {
 };
 
 // ---------------------------------------------------------------------------
-void Ctx::init(const flume_scene_desc* desc, int dev) {
+void Ctx::init(const flume_scene_desc* desc, int dev, int n_replicas) {
     device = dev;
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -704,9 +724,12 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     cfg = desc->config;
     N = int(desc->n_particles);
     if (N < 0) throw FlumeError(FLUME_E_ARG, "negative particle count");
+    nrep = n_replicas;
+    n1 = N / nrep;
+    e1 = desc->n_effectors / nrep;
     mats.assign(desc->materials, desc->materials + desc->n_materials);
     eff_shapes.assign(desc->effectors, desc->effectors + desc->n_effectors);
-    if (desc->n_effectors > kMaxEff) throw FlumeError(FLUME_E_ARG, "at most 8 effectors are supported");
+    if (e1 > kMaxEff) throw FlumeError(FLUME_E_ARG, "at most 8 effectors are supported");
 
     // geometry (types.hpp:67-95)
     const double dx = cfg.domain[0] / cfg.grid_resolution;
@@ -717,6 +740,11 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
         g.lo[a] = float(dx);
         g.hi[a] = float(cfg.domain[a] - dx);
         g.gdt[a] = float(cfg.gravity[a] * cfg.dt_substep);
+    }
+    g.rstride = 0;
+    if (nrep > 1) {  // replicas side by side along x, one empty block column between them
+        g.rstride = g.NB[0] + 1;
+        g.NB[0] = nrep * g.rstride - 1;
     }
     g.nbtot = g.NB[0] * g.NB[1] * g.NB[2];
     g.key_inactive = uint32_t(g.nbtot) << 6;
@@ -787,11 +815,12 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
     }
     nmem = int(rb_members.size());
 
-    std::map<std::tuple<int, int, double, double, int>, uint32_t> cmap;
+    std::map<std::tuple<int, int, double, double, int, int>, uint32_t> cmap;
     p_class.resize(N);
     for (int i = 0; i < N; i++) {
         if (p_mat[i] < 0 || p_mat[i] >= int(mats.size())) throw FlumeError(FLUME_E_SCENE, "bad material id");
-        auto key = std::make_tuple(p_mat[i], p_body[i], p_mass[i], p_vol0[i], rigid_of_id[i]);
+        const int rep = i / std::max(n1, 1);
+        auto key = std::make_tuple(p_mat[i], p_body[i], p_mass[i], p_vol0[i], rigid_of_id[i], rep);
         auto it = cmap.find(key);
         if (it == cmap.end()) {
             const flume_material& m = mats[p_mat[i]];
@@ -808,6 +837,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
             ci.theta_c = float(m.theta_c);
             ci.theta_s = float(m.theta_s);
             ci.sigma_y = float(m.sigma_y);
+            ci.rep = rep;
             it = cmap.emplace(key, uint32_t(classes.size())).first;
             classes.push_back(ci);
         }
@@ -929,36 +959,60 @@ void Ctx::init(const flume_scene_desc* desc, int dev) {
 EffSet Ctx::make_effset(const std::vector<EffState>& es) const {
     EffSet s{};
     s.n = int(es.size());
-    for (size_t i = 0; i < es.size(); i++) {
-        const flume_effector_shape& sh = eff_shapes[i];
-        EffK<float>& k = s.e[i];
-        k.shape.kind = sh.shape_kind;
-        k.shape.radius = float(sh.radius);
-        k.shape.half = V3<float>{float(sh.half_extents[0]), float(sh.half_extents[1]), float(sh.half_extents[2])};
-        k.shape.seg_a = V3<float>{float(sh.seg_a[0]), float(sh.seg_a[1]), float(sh.seg_a[2])};
-        k.shape.seg_b = V3<float>{float(sh.seg_b[0]), float(sh.seg_b[1]), float(sh.seg_b[2])};
-        k.shape.normal = V3<float>{float(sh.plane_normal[0]), float(sh.plane_normal[1]), float(sh.plane_normal[2])};
-        k.shape.offset = float(sh.plane_offset);
-        k.shape.half_height = float(sh.half_height);
-        // world shape pose = compose(pose, sdf.pose) in fp64 (sdf.hpp:17-22)
-        M3<double> sR;
-        for (int q = 0; q < 9; q++) sR.m[q] = sh.shape_R[q];
-        V3<double> st = {sh.shape_t[0], sh.shape_t[1], sh.shape_t[2]};
-        V3<double> wt = es[i].t + es[i].R * st;
-        M3<double> wR = es[i].R * sR;
-        k.wt = V3<float>{float(wt.x), float(wt.y), float(wt.z)};
-        for (int q = 0; q < 9; q++) {
-            k.wR.m[q] = float(wR.m[q]);
-            k.shapeR.m[q] = float(sR.m[q]);
-        }
-        k.shapet = V3<float>{float(st.x), float(st.y), float(st.z)};
-        k.pt = V3<float>{float(es[i].t.x), float(es[i].t.y), float(es[i].t.z)};
-        k.vlin = V3<float>{float(es[i].vlin.x), float(es[i].vlin.y), float(es[i].vlin.z)};
-        k.wang = V3<float>{float(es[i].w.x), float(es[i].w.y), float(es[i].w.z)};
-        k.sticky = std::isinf(sh.friction_mu) ? 1 : 0;
-        k.mu = k.sticky ? 0.f : float(sh.friction_mu);
-    }
+    for (size_t i = 0; i < es.size(); i++) fill_effk(i, es[i], s.e[i]);
     return s;
+}
+
+EffSet Ctx::replica_effset() {
+    const size_t ne = eff.size();
+    if (!h_effring) {
+        CK(cudaMallocHost(&h_effring, size_t(kEffRingRep) * ne * sizeof(EffK<float>)));
+        d_effring.alloc(size_t(kEffRingRep) * ne);
+        effring_ev.assign(kEffRingRep, nullptr);
+    }
+    const int slot = effring_i;
+    effring_i = (effring_i + 1) % kEffRingRep;
+    if (effring_ev[slot]) CK(cudaEventSynchronize(effring_ev[slot]));  // its last copy has run
+    else CK(cudaEventCreateWithFlags(&effring_ev[slot], cudaEventDisableTiming));
+    EffK<float>* h = h_effring + size_t(slot) * ne;
+    for (size_t i = 0; i < ne; i++) fill_effk(i, eff[i], h[i]);
+    EffK<float>* d = d_effring.p + size_t(slot) * ne;
+    CK(cudaMemcpyAsync(d, h, ne * sizeof(EffK<float>), cudaMemcpyHostToDevice, stream));
+    CK(cudaEventRecord(effring_ev[slot], stream));
+    EffSet s{};
+    s.n = int(ne);
+    s.per_rep = e1;
+    s.ext = d;
+    return s;
+}
+
+void Ctx::fill_effk(size_t i, const EffState& e, EffK<float>& k) const {
+    const flume_effector_shape& sh = eff_shapes[i];
+    k.shape.kind = sh.shape_kind;
+    k.shape.radius = float(sh.radius);
+    k.shape.half = V3<float>{float(sh.half_extents[0]), float(sh.half_extents[1]), float(sh.half_extents[2])};
+    k.shape.seg_a = V3<float>{float(sh.seg_a[0]), float(sh.seg_a[1]), float(sh.seg_a[2])};
+    k.shape.seg_b = V3<float>{float(sh.seg_b[0]), float(sh.seg_b[1]), float(sh.seg_b[2])};
+    k.shape.normal = V3<float>{float(sh.plane_normal[0]), float(sh.plane_normal[1]), float(sh.plane_normal[2])};
+    k.shape.offset = float(sh.plane_offset);
+    k.shape.half_height = float(sh.half_height);
+    // world shape pose = compose(pose, sdf.pose) in fp64 (sdf.hpp:17-22)
+    M3<double> sR;
+    for (int q = 0; q < 9; q++) sR.m[q] = sh.shape_R[q];
+    V3<double> st = {sh.shape_t[0], sh.shape_t[1], sh.shape_t[2]};
+    V3<double> wt = e.t + e.R * st;
+    M3<double> wR = e.R * sR;
+    k.wt = V3<float>{float(wt.x), float(wt.y), float(wt.z)};
+    for (int q = 0; q < 9; q++) {
+        k.wR.m[q] = float(wR.m[q]);
+        k.shapeR.m[q] = float(sR.m[q]);
+    }
+    k.shapet = V3<float>{float(st.x), float(st.y), float(st.z)};
+    k.pt = V3<float>{float(e.t.x), float(e.t.y), float(e.t.z)};
+    k.vlin = V3<float>{float(e.vlin.x), float(e.vlin.y), float(e.vlin.z)};
+    k.wang = V3<float>{float(e.w.x), float(e.w.y), float(e.w.z)};
+    k.sticky = std::isinf(sh.friction_mu) ? 1 : 0;
+    k.mu = k.sticky ? 0.f : float(sh.friction_mu);
 }
 
 // mpm.hpp:418-433, fp64 on the host
@@ -967,10 +1021,11 @@ void Ctx::advance_effectors(const double* action) {
     for (size_t i = 0; i < eff.size(); i++) {
         const flume_effector_shape& sh = eff_shapes[i];
         EffState& e = eff[i];
+        const double* act = action + 6 * (nrep > 1 ? int(i) / e1 : 0);  // replicas: their own actions
         for (int a = 0; a < 3; a++)
-            if (sh.action_mask[a]) e.vlin[a] = action[a];
+            if (sh.action_mask[a]) e.vlin[a] = act[a];
         for (int a = 0; a < 3; a++)
-            if (sh.action_mask[3 + a]) e.w[a] = action[3 + a];
+            if (sh.action_mask[3 + a]) e.w[a] = act[3 + a];
         e.t = e.t + e.vlin * dt;
         e.R = advance_rotation(e.R, e.w, dt);
     }
@@ -1349,7 +1404,7 @@ void Ctx::return_bars(Record& r, BarBuf post) {
 void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r) {
     advance_effectors(action);
     r.substep = substep_index;
-    r.effk = make_effset(eff);
+    r.effk = effset_now();
     // activation (mpm.hpp:435-449): ids reaching their activation substep
     r.act.clear();
     r.emit.clear();
@@ -1365,6 +1420,7 @@ void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Recor
             int slot = slot0 + int(pos_it - inactive_ids.begin());
             ActEntry a{};
             a.slot = slot;
+            a.rep = nrep > 1 ? id / n1 : 0;
             int em = emitter_of[id];
             float px[3] = {parked_x.empty() ? 0.f : parked_x[3 * size_t(id)],
                            parked_x.empty() ? 0.f : parked_x[3 * size_t(id) + 1],
@@ -1527,6 +1583,7 @@ void Ctx::substep(const double* action, int count) {
 
 // p2g + grid_update on the live state without advancing (KAT harness)
 void Ctx::stage_grid(double* mass, double* vel) {
+    require_single("stage_grid");
     if (empty) {
         const size_t nn = size_t(geom.nd[0]) * geom.nd[1] * geom.nd[2];
         if (mass) std::fill(mass, mass + nn, 0.0);
@@ -1710,6 +1767,7 @@ void Ctx::make_attraction(const flume_loss_desc* loss, LossSet& ls, std::vector<
 
 // LossEvaluator::per_particle (losses.hpp:367-390) of the current state, by particle id
 void Ctx::per_particle(const flume_loss_desc* loss, double* out) {
+    require_single("loss_per_particle");
     if (slab()) throw FlumeError(FLUME_E_ARG, "per_particle runs on single-rank contexts only");
     std::vector<std::shared_ptr<void>> keep;
     flume_loss_desc plain = *loss;
@@ -1757,12 +1815,27 @@ void Ctx::eval_loss(StateBuf& st, const LossSet& ls0, uint32_t mask, double* out
 }
 
 double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, long window, double* per_seg,
-                         bool keep_final) {
+                         bool keep_final, double* rep_total) {
     const long T = long(a->n_segments) * a->segment_length;
     if (window <= 0) window = T;
     std::vector<std::shared_ptr<void>> keep;
-    LossSet ls = make_lossset(loss, keep);
-    loss_out.alloc(a->n_segments);
+    // one loss set per replica: the scene's terms on that replica's bodies
+    std::vector<LossSet> lss;
+    for (int r = 0; r < nrep; r++) {
+        if (r == 0) {
+            lss.push_back(make_lossset(loss, keep));
+            continue;
+        }
+        if (loss && loss->attraction_weight > 0 && loss->n_prev > 0)
+            throw FlumeError(FLUME_E_ARG, "rollout_loss: the attraction term is not available on a replica context");
+        flume_loss_desc dr = *loss;
+        std::vector<flume_loss_term> terms(loss->terms, loss->terms + loss->n_terms);
+        for (auto& t : terms) t.body += r * body_stride;
+        dr.terms = terms.data();
+        lss.push_back(make_lossset(&dr, keep));
+    }
+    const int nseg = a->n_segments;
+    loss_out.alloc(size_t(nrep) * nseg);
     // state0 is const: work on a copy
     const long s0 = substep_index;
     const double time0 = time;
@@ -1774,16 +1847,18 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     copy_state(*st, *cur);
     for (long t = 0; t < T; t++) {
         StatePtr nxt = get_state();
-        forward_substep(a->values + 6 * (t / a->segment_length), st, nxt, next_scratch());
+        forward_substep(a->values + act_stride() * (t / a->segment_length), st, nxt, next_scratch());
         put_state(st);
         st = nxt;
         if ((t + 1) % a->segment_length == 0) {
             int seg = int((t + 1) / a->segment_length) - 1;
-            eval_loss(*st, ls, loss_mask(loss, seg, a->n_segments), loss_out.p + seg, seg, substep_index);
+            for (int r = 0; r < nrep; r++)
+                eval_loss(*st, lss[size_t(r)], loss_mask(loss, seg, nseg), loss_out.p + size_t(r) * nseg + seg, seg,
+                          substep_index);
         }
     }
     allreduce(loss_out.p, size_t(a->n_segments), DType::F64, ROp::Sum);
-    std::vector<double> per(a->n_segments);
+    std::vector<double> per(size_t(nrep) * nseg);
     CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     if (keep_final) {  // the context continues from the final state (rollout_loss's final_state)
@@ -1801,13 +1876,19 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
         pending = pend0;
     }
     check_error();
-    double total = 0;
-    for (int s = 0; s < a->n_segments; s++) {
-        if (per_seg) per_seg[s] = per[s];
-        if (long(s + 1) * a->segment_length <= window) total += per[s];
+    double total0 = 0;
+    for (int r = nrep - 1; r >= 0; r--) {
+        double total = 0;
+        for (int s = 0; s < nseg; s++) {
+            const double v = per[size_t(r) * nseg + s];
+            if (per_seg) per_seg[size_t(r) * nseg + s] = v;
+            if (long(s + 1) * a->segment_length <= window) total += v;
+        }
+        if (!std::isfinite(total)) throw FlumeError(FLUME_E_ENGINE, "rollout produced a non-finite loss");
+        if (rep_total) rep_total[r] = total;
+        total0 = total;
     }
-    if (!std::isfinite(total)) throw FlumeError(FLUME_E_ENGINE, "rollout produced a non-finite loss");
-    return total;
+    return total0;
 }
 
 // reverse one substep: bars_post (store order of state[t+1]) -> bars_pre (store order of state[t])
@@ -1880,6 +1961,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
 
 void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
                           double* grad, double* loss_out_h, double* full_loss, double* per_seg, long* snapshots) {
+    require_single("grad_trajectory");
     const long T = long(a->n_segments) * a->segment_length;
     if (stride <= 0) stride = T;
     if (window <= 0) window = T;
@@ -2169,6 +2251,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
 
 void Ctx::adjoint_substep_api(const double* action, double* xb, double* vb, double* Fb, double* Cb, double* ebars,
                               double* abar_out) {
+    require_single("adjoint_substep");
     if (slab()) throw FlumeError(FLUME_E_ARG, "adjoint_substep: single-rank contexts only");
     upload_full = true;  // the pre-state's liquids are expanded to a full F below (heavy blocks)
     xbar_tmp.alloc(size_t(N) * 3);
@@ -2320,6 +2403,103 @@ int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out) 
     return FLUME_OK;
 }
 
+// n copies of a scene description for a replica context: particle i of replica r is
+// r * n1 + i, effector e is r * e1 + e, body b is r * body_stride + b
+struct ReplicaDesc {
+    flume_scene_desc d{};
+    std::vector<flume_effector_shape> eff;
+    std::vector<flume_rigid_body> rig;
+    std::vector<std::vector<long>> members;
+    std::vector<flume_emitter> emi;
+    std::vector<int> mat, body;
+    std::vector<double> mass, vol;
+    std::vector<long> act;
+    int body_stride = 1;
+    ReplicaDesc(const flume_scene_desc* s, int R) {
+        const long n1 = s->n_particles;
+        const int e1 = s->n_effectors;
+        for (long i = 0; i < n1; i++) body_stride = std::max(body_stride, s->body_id[i] + 1);
+        for (int b = 0; b < s->n_rigid; b++) body_stride = std::max(body_stride, s->rigid[b].body_id + 1);
+        d = *s;
+        for (int r = 0; r < R; r++) {
+            eff.insert(eff.end(), s->effectors, s->effectors + e1);
+            for (long i = 0; i < n1; i++) {
+                mat.push_back(s->material_id[i]);
+                body.push_back(s->body_id[i] < 0 ? s->body_id[i] : s->body_id[i] + r * body_stride);
+                mass.push_back(s->mass[i]);
+                vol.push_back(s->volume0[i]);
+                act.push_back(s->activation_substep ? s->activation_substep[i] : 0);
+            }
+            for (int b = 0; b < s->n_rigid; b++) {
+                flume_rigid_body rb = s->rigid[b];
+                std::vector<long> m(rb.members, rb.members + rb.n_members);
+                for (long& p : m) p += r * n1;
+                members.push_back(std::move(m));
+                rb.body_id += r * body_stride;
+                rig.push_back(rb);
+            }
+            for (long k = 0; k < s->n_emitters; k++) {
+                flume_emitter em = s->emitters[k];
+                em.particle += r * n1;
+                if (em.effector >= 0) em.effector += r * e1;
+                emi.push_back(em);
+            }
+        }
+        for (size_t b = 0; b < rig.size(); b++) rig[b].members = members[b].data();
+        d.n_effectors = R * e1;
+        d.effectors = eff.data();
+        d.n_rigid = int(rig.size());
+        d.rigid = rig.data();
+        d.n_emitters = long(emi.size());
+        d.emitters = emi.data();
+        d.n_particles = R * n1;
+        d.material_id = mat.data();
+        d.body_id = body.data();
+        d.mass = mass.data();
+        d.volume0 = vol.data();
+        d.activation_substep = act.data();
+    }
+};
+
+int flume_ctx_create_replicas(const flume_scene_desc* desc, int n_replicas, int device, flume_ctx** out) {
+    if (!desc || !out || n_replicas < 1 || desc->n_particles <= 0) return FLUME_E_ARG;
+    *out = nullptr;
+    flume_ctx* ctx = new flume_ctx();
+    int rc = guard(nullptr, [&] {
+        if (long(n_replicas) * desc->n_particles >= (1L << 26))
+            throw FlumeError(FLUME_E_ARG, "at most 2^26-1 particles per context");
+        ReplicaDesc rd(desc, n_replicas);
+        ctx->c.body_stride = rd.body_stride;
+        ctx->c.init(&rd.d, device, n_replicas);
+    });
+    if (rc != FLUME_OK) {
+        ctx->c.last_err = g_create_err;
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return FLUME_OK;
+}
+
+int flume_replicas_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss,
+                                long window, int keep_final, double* loss_out, double* per_segment) {
+    if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.require_particles();
+        ctx->c.rollout_loss(actions, loss, window, per_segment, keep_final != 0, loss_out);
+    });
+}
+
+int flume_replicas_info(const flume_ctx* ctx, int* n_replicas, long* particles_per_replica,
+                        int* effectors_per_replica, int* body_stride) {
+    if (!ctx) return FLUME_E_ARG;
+    if (n_replicas) *n_replicas = ctx->c.nrep;
+    if (particles_per_replica) *particles_per_replica = ctx->c.n1;
+    if (effectors_per_replica) *effectors_per_replica = ctx->c.e1;
+    if (body_stride) *body_stride = ctx->c.body_stride;
+    return FLUME_OK;
+}
+
 int flume_group_create(const flume_scene_desc* desc, int n_ranks, const int* devices, flume_ctx** out) {
     if (!desc || !out || n_ranks < 1) return FLUME_E_ARG;
     for (int r = 0; r < n_ranks; r++) out[r] = nullptr;
@@ -2424,6 +2604,9 @@ int flume_ctx_destroy(flume_ctx* ctx) {
     cudaStream_t s3 = ctx->c.cstream;
     cudaStreamSynchronize(s2);
     if (s3) cudaStreamSynchronize(s3);
+    if (ctx->c.h_effring) cudaFreeHost(ctx->c.h_effring);
+    for (cudaEvent_t e : ctx->c.effring_ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
     if (s) cudaStreamDestroy(s);
     if (s2) cudaStreamDestroy(s2);

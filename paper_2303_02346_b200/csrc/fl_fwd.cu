@@ -46,7 +46,7 @@ __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, 
     raw.id[i] = uint32_t(i);
     // active: 0 = parked (activates later), 1 = active here, 2 = active on another slab
     uint32_t key = g.key_inactive;
-    if (active[i]) cell_key(g, raw.x(0)[i], raw.x(1)[i], raw.x(2)[i], key);
+    if (active[i]) cell_key(g, raw.x(0)[i], raw.x(1)[i], raw.x(2)[i], key, cls[meta[i]].rep);
     if (active[i] == 2) key = g.key_departed;
     raw.key[i] = key;
 }
@@ -142,7 +142,7 @@ __global__ void k_activate(Geom g, PBuf st, const ActEntry* list, int n, ActBatc
         }
     }
     uint32_t key;
-    cell_key(g, st.x(0)[slot], st.x(1)[slot], st.x(2)[slot], key);
+    cell_key(g, st.x(0)[slot], st.x(1)[slot], st.x(2)[slot], key, e.rep);
     st.key[slot] = e.departed ? g.key_departed : key;  // departed: activates on another slab
 }
 
@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(NT, MINB) k_p2g(Geom g, PBuf st, const uint32_
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
+        bx -= rep_of_col(g, bx) * g.rstride;  // replica-local column (positions are local)
         __syncthreads();
         const int cnt = r.end - r.start;
         uint32_t s_nx = tid < cnt ? perm[r.start + tid] : 0u;  // overlaps the cell-table barrier
@@ -340,7 +341,9 @@ __device__ __forceinline__ float4 gather_staging(const Geom& g, const int* __res
 #endif
 constexpr int kGridUpdThreads = FL_GRIDUPD_THREADS;  // 64 nodes (one node block) per 64 threads
 
-template <bool FILTER>  // (the column filter only in slab contexts: it costs the plain path ~2 us)
+// FILTER: the column filter, slab contexts only (it costs the plain path ~2 us); REP: replica
+// contexts (local node coordinates, the replica's effectors from device memory; also ~2 us)
+template <bool FILTER, bool REP>
 __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const int* __restrict__ nb_list,
                                                      const int* __restrict__ n_nb, const int* __restrict__ blockmap,
                                                      const float4* __restrict__ staging, float4* gridv, float4* gridv0,
@@ -370,13 +373,23 @@ __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const i
             const float inv = 1.0f / m;
             v0 = V3<float>{mp.y * inv, mp.z * inv, mp.w * inv};
             v = V3<float>{v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
-            const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
+            const int rep = REP ? rep_of_col(g, bx) : 0;  // replicas: local node, the replica's effectors
+            const int i = 4 * (bx - rep * g.rstride) + lx, j = 4 * by + ly, kk = 4 * bz + lz;
             v = wall_bc_dev(g, i, j, kk, v);
             const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
-            for (int e = 0; e < eff.n; e++) {
-                bool hit;
-                v = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, v, &hit);
-                hits |= uint32_t(hit) << e;
+            if (REP) {
+                const EffK<float>* er = eff.ext + rep * eff.per_rep;
+                for (int e = 0; e < eff.per_rep; e++) {
+                    bool hit;
+                    v = effector_contact(er[e], g.inv_dx, g.eps_cells, g.hard != 0, p, v, &hit);
+                    hits |= uint32_t(hit) << e;
+                }
+            } else {
+                for (int e = 0; e < eff.n; e++) {
+                    bool hit;
+                    v = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, v, &hit);
+                    hits |= uint32_t(hit) << e;
+                }
             }
         }
         gridv[idx] = make_float4(v.x, v.y, v.z, m);
@@ -388,7 +401,8 @@ __global__ void __launch_bounds__(kGridUpdThreads) k_grid_update(Geom g, const i
 void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int grid, const int* blockmap,
                         const float4* staging, float4* gridv, float4* gridv0, const EffSet& eff, uint8_t* cmask,
                         int* clear, int n_clear, cudaStream_t s, int cmode, int c0, int c1) {
-    launch_k(cmode ? k_grid_update<true> : k_grid_update<false>, dim3(grid * (256 / kGridUpdThreads)),
+    launch_k(eff.ext ? k_grid_update<false, true> : cmode ? k_grid_update<true, false> : k_grid_update<false, false>,
+             dim3(grid * (256 / kGridUpdThreads)),
              dim3(kGridUpdThreads), 0, s, g, nb_list, n_nb, blockmap, staging, gridv, gridv0, eff, cmask, clear, n_clear,
              GridCols{cmode, c0, c1});
 }
@@ -423,6 +437,7 @@ __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, con
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
+        const int rep = rep_of_col(g, bx);  // replica contexts (0 otherwise)
         ts.begin(g, gridv, bx, by, bz, tid);
         // the perm -> state loads are the kernel's latency chain: the first particle's
         // position/class loads overlap the tile copy, and later ones run one particle
@@ -451,7 +466,7 @@ __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, con
             const uint32_t pid = in.id[s];
             const ClassInfo ci = cls[meta_cls(meta)];
             StencilW sw;
-            stencil_weights(g, x, bx, by, bz, sw);
+            stencil_weights(g, x, bx - rep * g.rstride, by, bz, sw);
             V3<float> vraw;
             M3<float> cnew;
             g2p_gather(g, vt, sw, vraw, cnew);
@@ -501,7 +516,7 @@ __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, con
             out.meta[j] = meta_cls(meta) | (vn > g.vmax ? kMetaCfl : 0u);
             out.id[j] = pid;
             uint32_t key;
-            cell_key(g, xn.x, xn.y, xn.z, key);
+            cell_key(g, xn.x, xn.y, xn.z, key, rep);
             out.key[j] = key;
             if (HEAVY && ci.rigid >= 0) {
                 // rigid members carry fp64 positions: v = dx/dt in rigid_body_pass
@@ -518,7 +533,7 @@ __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, con
                     out.mx[3 * mr + a] = xm;
                     out.x(a)[j] = float(xm);
                 }
-                cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key);
+                cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key, rep);
                 out.key[j] = key;
             }
         }
@@ -660,7 +675,7 @@ __global__ void k_rigid_apply(Geom g, PBuf out, RigidDev rd) {
         out.v(a)[j] = float((xn[a] - rd.mstart[3 * size_t(r) + a]) * inv_dt);
     }
     uint32_t key;
-    cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key);
+    cell_key(g, out.x(0)[j], out.x(1)[j], out.x(2)[j], key, rep_of_col(g, key_col(g, out.key[j])));
     out.key[j] = key;
 }
 

@@ -97,6 +97,7 @@ struct ActEntry {
     int slot;
     int has_xv;
     int departed;  // activates inside another rank's slab
+    int rep;       // replica (replica contexts)
     float x[3];
     float v[3];
 };

@@ -31,6 +31,10 @@ struct Geom {
     int keybits;    // bits needed for key_departed
     int sx0, sx1;   // x-slab of particle-block columns owned by this rank ([0, NB0) for one rank)
     int colblocks;  // NB1 * NB2 blocks per x column
+    // replica contexts (a population of one scene side by side in one grid): particle-block
+    // x columns per replica including one empty gap column; nd is one replica's node grid and
+    // positions stay replica-local.  0: one scene.
+    int rstride;
     int idbits;     // bits needed for particle ids
     float dx, inv_dx, dt;
     float lo[3], hi[3];  // clamp_to_interior bounds [dx, L-dx] (mpm.hpp:330-336)
@@ -60,6 +64,7 @@ struct ClassInfo {
     int iso;     // liquid / viscous liquid: the return map makes F = c I (materials.hpp:147-153)
     float mass, vol0;
     float mu, lambda, theta_c, theta_s, sigma_y;
+    int rep;     // replica of the class's particles (replica contexts; 0 otherwise)
 };
 
 // Compact deformation gradient.  The return map of (viscous) liquids resets F
@@ -77,6 +82,9 @@ __host__ __device__ inline bool f_compact(const ClassInfo& ci, uint32_t meta) {
 struct EffSet {
     int n;
     EffK<float> e[kMaxEff];
+    // replica contexts: per_rep effectors per replica, all n of them in device memory (ext)
+    int per_rep;
+    const EffK<float>* ext;
 };
 
 struct PBuf {
@@ -185,8 +193,12 @@ __host__ __device__ inline int base_cell(float x, float inv_dx, float& fx) {
     return int(b);
 }
 
-// returns false when the stencil leaves the grid (mpm.hpp:265-269)
-__host__ __device__ inline bool cell_key(const Geom& g, float x0, float x1, float x2, uint32_t& key) {
+// replica of a particle-block x column (replica contexts)
+__host__ __device__ inline int rep_of_col(const Geom& g, int bx) { return g.rstride ? bx / g.rstride : 0; }
+
+// returns false when the stencil leaves the grid (mpm.hpp:265-269); rep: the particle's
+// replica (its blocks start at x column rep * rstride)
+__host__ __device__ inline bool cell_key(const Geom& g, float x0, float x1, float x2, uint32_t& key, int rep = 0) {
     float f;
     int b0 = base_cell(x0, g.inv_dx, f), b1 = base_cell(x1, g.inv_dx, f), b2 = base_cell(x2, g.inv_dx, f);
     bool ok = b0 >= 0 && b1 >= 0 && b2 >= 0 && b0 + 2 < g.nd[0] && b1 + 2 < g.nd[1] && b2 + 2 < g.nd[2];
@@ -195,7 +207,7 @@ __host__ __device__ inline bool cell_key(const Geom& g, float x0, float x1, floa
         b1 = b1 < 0 ? 0 : (b1 > g.nd[1] - 3 ? g.nd[1] - 3 : b1);
         b2 = b2 < 0 ? 0 : (b2 > g.nd[2] - 3 ? g.nd[2] - 3 : b2);
     }
-    key = (uint32_t(block_lin(g, b0 >> 2, b1 >> 2, b2 >> 2)) << 6) |
+    key = (uint32_t(block_lin(g, (b0 >> 2) + rep * g.rstride, b1 >> 2, b2 >> 2)) << 6) |
           uint32_t(((b0 & 3) << 4) | ((b1 & 3) << 2) | (b2 & 3));
     return ok;
 }

@@ -1,0 +1,64 @@
+"""Replica contexts: a population of one scene in one grid, every kernel
+launch covering all candidates (flume_ctx_create_replicas).  Each replica must evolve exactly
+like a single context given that replica's actions: final states bit-identical, losses equal
+up to the order of the fp64 loss sums (the replicas' particles sit at other store slots).
+
+  c1        one liquid + a box effector, full size, 4 candidates
+  c2 @ 64   emitters attached to an effector (activation per replica), 3 candidates
+  c5 @ 32   every material kind + the rigid brick + a sphere effector, 4 candidates
+"""
+import numpy as np
+import pytest
+
+import paper_2303_02346_b200 as fl
+from tests._util import spec_for
+
+pytestmark = pytest.mark.gpu
+
+
+def _population(w, R, nseg, seed=0):
+    rng = np.random.default_rng(seed)
+    base = np.asarray(w.init_action, dtype=np.float64)
+    out = []
+    for r in range(R):
+        vals = np.tile(base, (nseg, 1)) + (0.0 if r == 0 else 0.3) * rng.standard_normal((nseg, 6))
+        out.append(fl.ActionTrajectory(nseg, 0, vals))
+    return out
+
+
+@pytest.mark.parametrize("name,res,R,nseg,seglen", [("c1", None, 4, 2, 10), ("c2", 64, 3, 2, 10),
+                                                    ("c5", 32, 4, 2, 5)])
+def test_replicas_match_single_contexts(name, res, R, nseg, seglen):
+    w = fl.build_scene(spec_for(name, res))
+    pop = _population(w, R, nseg)
+    for a in pop:
+        a.segment_length = seglen
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    rws = fl.ReplicaWorkspace(w.scene, R)
+    per_r, fin_r = [], []
+    losses = fl.rollout_loss_replicas(w.scene, w.state, pop, loss, rws, per_segment=per_r, final_states=fin_r)
+    rws.close()
+    ws = fl.GpuWorkspace(w.scene)
+    for r in range(R):
+        per, fin = [], w.state.copy()
+        l1 = fl.rollout_loss(w.scene, w.state.copy(), pop[r], loss, per_segment=per, ws=ws, final_state=fin)
+        assert abs(losses[r] - l1) <= 1e-12 * abs(l1), (r, losses[r], l1)
+        np.testing.assert_allclose(per_r[r], per, rtol=1e-12, atol=0)
+        f = fin_r[r]
+        for got, want in ((f.x, fin.x), (f.v, fin.v), (f.F, fin.F), (f.C, fin.C)):
+            assert np.array_equal(got, want), r
+        assert np.array_equal(f._eff, fin._eff)
+        assert f.substep_index == fin.substep_index == nseg * seglen
+    ws.close()
+    # the candidates differ: the population is not R copies of one rollout
+    assert len({round(l, 9) for l in losses}) > 1
+
+
+def test_replica_context_is_forward_only():
+    w = fl.build_scene(spec_for("c1", 32))
+    rws = fl.ReplicaWorkspace(w.scene, 2)
+    acts = fl.ActionTrajectory(1, 2, w.init_action.reshape(1, 6))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    with pytest.raises(ValueError):
+        fl.grad_trajectory(w.scene, rws.replicate(w.state), acts, loss, ws=rws)
+    rws.close()
