@@ -9,6 +9,8 @@ reference produced (tests/golden/long/, tests/golden/make_golden_long.py).
       zero gradient over a few substeps)
   c3  full scene (1M non-Newtonian particles), state after 100 substeps
   c2/c3/c5 at grid 64 (c5: every material kind + the rigid brick), 10 x 50 substeps
+  c2 full (latte art, emitter active), state after 100 substeps
+  c5 full (8M particles, 256^3, the scaling workload), 2 x 10 substeps: state, loss, gradient
   3D 512-substep checkpoint-stride invariance (proj/tests/acceptance_main.cpp:71-100)
 """
 import numpy as np
@@ -26,11 +28,17 @@ pytestmark = pytest.mark.gpu
 # ~100x that is the fp32 floor.  SVD materials sit higher: c3's non-Newtonian return map
 # (von Mises, a non-smooth projection) and c5's stiff solids get 5e-4 (c3's v: 1e-3).  c4
 # over the bench's 500 substeps: one rounding moves x by 5.0e-6 dx, so 500 x that = 2.5e-3.
+# c2 (full latte art, emitter active) over 100 substeps: one rounding moves x by 3.8e-6 dx, so
+# 5e-4.  c5 at its full 256^3 (the scaling workload, 20 substeps): positions, F, loss and
+# gradient sit at 6e-5 / 8e-6 / 2e-9 / 3e-6, but the stiff elastic and jelly bodies' velocities
+# (and C) carry fp32 F's strain floor amplified by 256^3's 16x stress
+# coefficient: v 9.2e-4, C 9.0e-3 of their maxima on particles at 2 % of the peak speed.
 STATE_TOL = {"c1_4x25": 1e-4, "c3_fwd100": 5e-4, "c2_64_10x50": 1e-4, "c3_64_10x50": 5e-4,
-             "c5_64_10x50": 5e-4, "c4_fwd500": 2.5e-3}
-V_TOL = {"c3_fwd100": 1e-3, "c3_64_10x50": 1e-3}
+             "c5_64_10x50": 5e-4, "c4_fwd500": 2.5e-3, "c2_fwd100": 5e-4, "c5_2x10": 1e-4}
+V_TOL = {"c3_fwd100": 1e-3, "c3_64_10x50": 1e-3, "c5_2x10": 2e-3}
+C_TOL = {"c5_2x10": 2e-2}
 GRAD_TOL = {"c1_4x25": 1e-3, "c4pool_2x25": 1e-3, "c4_10x50": 1e-2, "c2_64_10x50": 1e-2, "c3_64_10x50": 1e-2,
-            "c5_64_10x50": 1e-2}
+            "c5_64_10x50": 1e-2, "c5_2x10": 1e-3}
 
 
 def _need(name):
@@ -45,7 +53,7 @@ def test_state_long_horizon(name):
     tol = STATE_TOL[name]
     for k in ("x", "v", "F"):
         assert e[k] <= (V_TOL.get(name, tol) if k == "v" else tol), (k, e)
-    assert e["C"] <= 10 * tol, e  # C = (4/dx^2) sum w v rel^T amplifies v's fp32 rounding
+    assert e["C"] <= C_TOL.get(name, 10 * tol), e  # C = (4/dx^2) sum w v rel^T amplifies v's fp32 rounding
     assert e["centroid"] <= tol, e
     if name in GRAD_TOL:
         assert e["loss"] <= 1e-5, e
