@@ -223,8 +223,8 @@ int flume_ctx_create(const flume_scene_desc* desc, int device, flume_ctx** out);
  * r * n_effectors + e in every state view (flume_state_upload / download take the
  * concatenated arrays); body b is r * body_stride + b.  flume_substep takes n_replicas x 6
  * action values.  Each replica's state evolves bit-identically to a single context's.
- * Forward rollouts only: grad_trajectory, adjoint_substep, stage_grid and
- * loss_per_particle return FLUME_E_ARG. */
+ * adjoint_substep, stage_grid and loss_per_particle return FLUME_E_ARG, and so do the single
+ * rollout / gradient entry points (use the flume_replicas_* ones). */
 int flume_ctx_create_replicas(const flume_scene_desc* desc, int n_replicas, int device, flume_ctx** out);
 /* rollout_loss (grad.hpp:15-41) of every replica: actions->values = n_segments x n_replicas x 6
  * (segment-major), `loss` is the scene's own description (applied to each replica's bodies);
@@ -232,6 +232,13 @@ int flume_ctx_create_replicas(const flume_scene_desc* desc, int n_replicas, int 
  * the context continues from the final states (flume_rollout_loss_final). */
 int flume_replicas_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss,
                                 long window, int keep_final, double* loss_out, double* per_segment);
+/* grad_trajectory (grad.hpp:61-134) of every replica (a population of independent
+ * gradient-based optimizations, optimize.hpp:180-239): action_grad[n_replicas x n_segments x 6],
+ * loss_out / full_loss[n_replicas], per_segment[n_replicas x n_segments]; actions and loss as
+ * in flume_replicas_rollout_loss. */
+int flume_replicas_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss,
+                                   long stride, long window, double* action_grad, double* loss_out,
+                                   double* full_loss, double* per_segment, long* snapshots);
 int flume_replicas_info(const flume_ctx* ctx, int* n_replicas, long* particles_per_replica,
                         int* effectors_per_replica, int* body_stride);
 int flume_ctx_destroy(flume_ctx* ctx);

@@ -9,7 +9,7 @@ from .api import (ActionTrajectory, AdjointError, AdjointState, DegenerateDeform
                   GpuWorkspace, LossEvaluator, RigidityError, Scene, SceneError, SimState, SubstepRecord,
                   TrajectoryGrad, World, adjoint_substep, build_scene, dist_unique_id, grad_trajectory, ipc_unique_id, mpm_substep,
                   p2g_grid, rollout_loss, slab_split, WorkspacePool, rollout_loss_batch, ReplicaWorkspace,
-                  rollout_loss_replicas,
+                  rollout_loss_replicas, grad_trajectory_replicas,
                   grad_trajectory_batch, state_to_json, state_from_json, GradReport, grad_check,
                   finite_difference_gradient, optimizable_components)
 from . import frames, scenes
@@ -18,6 +18,6 @@ __all__ = ["ActionTrajectory", "AdjointError", "AdjointState", "DegenerateDeform
            "GpuWorkspace", "LossEvaluator", "RigidityError", "Scene", "SceneError", "SimState", "SubstepRecord",
            "TrajectoryGrad", "World", "adjoint_substep", "build_scene", "dist_unique_id", "grad_trajectory", "ipc_unique_id", "mpm_substep", "p2g_grid",
            "rollout_loss", "scenes", "slab_split", "WorkspacePool", "rollout_loss_batch", "grad_trajectory_batch",
-           "ReplicaWorkspace", "rollout_loss_replicas",
+           "ReplicaWorkspace", "rollout_loss_replicas", "grad_trajectory_replicas",
            "state_to_json", "state_from_json", "frames", "GradReport", "grad_check",
            "finite_difference_gradient", "optimizable_components"]

@@ -133,6 +133,10 @@ EXPORTS = {
     "flume_ctx_create_replicas": (C.c_int, [C.POINTER(SceneDesc), C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "flume_replicas_rollout_loss": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long,
                                               C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "flume_replicas_grad_trajectory": (C.c_int, [C.c_void_p, C.POINTER(Actions), C.POINTER(LossDesc), C.c_long,
+                                                 C.c_long, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_long)]),
     "flume_replicas_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_long), C.POINTER(C.c_int),
                                       C.POINTER(C.c_int)]),
     "flume_sort_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_long), C.POINTER(C.c_long)]),

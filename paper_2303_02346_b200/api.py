@@ -1020,18 +1020,10 @@ def rollout_loss_replicas(scene: Scene, state0, population: Sequence[ActionTraje
     replica); per_segment / final_states (lists) receive each replica's per-segment losses
     and final state."""
     ws = _ws_for(scene, ws)
-    pop = list(population)
-    R = ws.n_replicas
-    if len(pop) != R:
-        raise ValueError(f"the replica context holds {R} candidates, got {len(pop)}")
-    nseg, seglen = pop[0].n_segments, pop[0].segment_length
-    if any(a.n_segments != nseg or a.segment_length != seglen for a in pop):
-        raise ValueError("every candidate needs the same segment layout")
     st = ws.replicate(state0)
     ws._upload(st)
-    vals = np.ascontiguousarray(np.stack([a.values for a in pop], axis=1))  # (n_segments, R, 6)
-    a = _abi.Actions()
-    a.n_segments, a.segment_length, a.values = nseg, seglen, _dp(vals)
+    a, vals, nseg = _replica_actions(ws, population)
+    R = ws.n_replicas
     out = np.zeros(R)
     per = np.zeros(R * nseg)
     keep = final_states is not None
@@ -1045,6 +1037,40 @@ def rollout_loss_replicas(scene: Scene, state0, population: Sequence[ActionTraje
         ws._download(st)
         final_states[:] = ws.split(st)
     return out.tolist()
+
+
+def _replica_actions(ws, population):
+    pop = list(population)
+    R = ws.n_replicas
+    if len(pop) != R:
+        raise ValueError(f"the replica context holds {R} candidates, got {len(pop)}")
+    nseg, seglen = pop[0].n_segments, pop[0].segment_length
+    if any(a.n_segments != nseg or a.segment_length != seglen for a in pop):
+        raise ValueError("every candidate needs the same segment layout")
+    vals = np.ascontiguousarray(np.stack([a.values for a in pop], axis=1))  # (n_segments, R, 6)
+    a = _abi.Actions()
+    a.n_segments, a.segment_length, a.values = nseg, seglen, _dp(vals)
+    return a, vals, nseg
+
+
+def grad_trajectory_replicas(scene: Scene, state0, population: Sequence[ActionTrajectory], loss: LossEvaluator,
+                             ws: ReplicaWorkspace, stride: int = 0, window: int = 0) -> List[TrajectoryGrad]:
+    """grad_trajectory (grad.hpp:61-134) of every candidate in one replica context -- a
+    population of independent gradient-based optimizations (optimize.hpp:180-239), every
+    kernel launch of the forward and the backward covering all of them."""
+    ws = _ws_for(scene, ws)
+    st = ws.replicate(state0)
+    ws._upload(st)
+    a, vals, nseg = _replica_actions(ws, population)
+    R = ws.n_replicas
+    g = np.zeros((R, nseg, 6))
+    lo, fu, per = np.zeros(R), np.zeros(R), np.zeros(R * nseg)
+    snaps = C.c_long()
+    ws._check(ws.lib.flume_replicas_grad_trajectory(ws.ctx, C.byref(a), C.byref(loss.desc), int(stride), int(window),
+                                                    _dp(g), _dp(lo), _dp(fu), _dp(per), C.byref(snaps)))
+    t = ws.last_timing()
+    return [TrajectoryGrad(float(lo[r]), float(fu[r]), per[r * nseg:(r + 1) * nseg].tolist(), g[r].copy(),
+                           snaps.value, t.forward_ms, t.backward_ms) for r in range(R)]
 
 
 def grad_trajectory_batch(scene: Scene, state0: SimState, population: Sequence[ActionTrajectory],

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_g2p(Geom g, PBuf pre, const ui
                 const bool cin = !HEAVY || f_compact(ci, pmeta);  // pre-state F = c I
                 const bool cpost = !HEAVY || ci.iso;              // post-state F (and its bar) compact
                 StencilW sw;
-                stencil_weights(g, x, bx, by, bz, sw);
+                stencil_weights(g, x, bx - rep_of_col(g, bx) * g.rstride, by, bz, sw);  // replica-local
                 V3<float> vraw, vuse;
                 M3<float> cnew;
                 bool clamped_v;
@@ -481,22 +481,29 @@ __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __re
 // memory (static node order per warp, since the list partition is static), then
 // one fixed-order CTA reduction per launch.  Nothing effector-sized lives in
 // registers across nodes, which keeps the kernel at ~64 registers.
-template <int NE, bool FILTER>  // (the column filter only in slab contexts)
+// REP (replica contexts): NE effectors per replica, read from eff.ext; the bars of replica
+// rep's effector e accumulate in slot rep * NE + e (of eff.n), so the shared accumulators
+// are dynamic (kW x eff.n x 18 doubles) and the partial rows `pstride` doubles long.
+template <int NE, bool FILTER, bool REP>  // (the column filter only in slab contexts)
 __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj_grid(Geom g, const int* __restrict__ nb_list,
                                                                  const int* __restrict__ n_nb,
                                                                  const int* __restrict__ blockmap,
                                                                  const float4* __restrict__ staging_bar,
                                                                  const float4* __restrict__ gridv0, float4* gridbar,
                                                                  EffSet eff, double* eff_partial,
-                                                                 const uint8_t* __restrict__ cmask, GridCols cols) {
+                                                                 const uint8_t* __restrict__ cmask, GridCols cols,
+                                                                 int pstride) {
     pdl_wait();
     constexpr int kW = kAdjGridThreads / 32;
-    constexpr int kQ = NE * kEffQ > 0 ? NE * kEffQ : 1;
-    __shared__ double wacc[kW][kQ];
+    constexpr int kQs = NE * kEffQ > 0 ? NE * kEffQ : 1;
+    __shared__ double wacc_s[REP ? 1 : kW * kQs];
+    extern __shared__ double wacc_d[];
+    const int kQ = REP ? eff.n * kEffQ : kQs;
+    double* wacc = REP ? wacc_d : wacc_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = tid >> 6, l = tid & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    for (int q = lane; q < kQ; q += 32) wacc[warp][q] = 0.0;
+    for (int q = lane; q < kQ; q += 32) wacc[warp * kQ + q] = 0.0;
     const int n = *n_nb;
     constexpr int kPer = kAdjGridThreads / 64;
     for (int k = blockIdx.x * kPer + sub; k < n; k += gridDim.x * kPer) {
@@ -519,7 +526,9 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
         const uint32_t cm = live ? uint32_t(cmask[idx]) : 0u;
         float pb0 = 0.f, pb1 = 0.f, pb2 = 0.f, mb = 0.f;
         if (__any_sync(0xffffffffu, live)) {  // warp-uniform: the effector reductions need all lanes
-            const int i = 4 * bx + lx, j = 4 * by + ly, kk = 4 * bz + lz;
+            const int rep = REP ? rep_of_col(g, bx) : 0;
+            const EffK<float>* ek = REP ? eff.ext + rep * NE : eff.e;
+            const int i = 4 * (bx - rep * g.rstride) + lx, j = 4 * by + ly, kk = 4 * bz + lz;
             const V3<float> p = {float(i) * g.dx, float(j) * g.dx, float(kk) * g.dx};
             const V3<float> v1 = {v0.x + g.gdt[0], v0.y + g.gdt[1], v0.z + g.gdt[2]};
             const V3<float> v2 = wall_bc_dev(g, i, j, kk, v1);
@@ -528,7 +537,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
 #pragma unroll
             for (int e = 0; e < NE; e++) {
                 chain[e] = c;
-                if ((cm >> e) & 1u) c = effector_contact(eff.e[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
+                if ((cm >> e) & 1u) c = effector_contact(ek[e], g.inv_dx, g.eps_cells, g.hard != 0, p, c);
             }
             // ghost node column (bx == sx1): computed for this slab's gathers, counted by its owner
             const bool owned = bx < g.sx1;
@@ -543,7 +552,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
                 bool hit = false;
                 if ((cm >> e) & 1u) {
                     in_bar = V3<float>{0.f, 0.f, 0.f};
-                    hit = effector_contact_vjp(eff.e[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
+                    hit = effector_contact_vjp(ek[e], g.dx, g.inv_dx, g.eps_cells, g.hard != 0, p, chain[e], bar,
                                                in_bar, eb) &&
                           owned;
                 }
@@ -556,7 +565,7 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
                         float v = hit ? vals[q] : 0.f;
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                        if (lane == 0) wacc[warp][e * kEffQ + q] += double(v);
+                        if (lane == 0) wacc[warp * kQ + (rep * NE + e) * kEffQ + q] += double(v);
                     }
                 }
                 if (live) bar = in_bar;
@@ -575,11 +584,11 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
         gridbar[idx] = make_float4(pb0, pb1, pb2, mb);
     }
     __syncthreads();
-    // only the NE effectors' components: the final sums read no further (nq = n_eff * 18)
-    for (int q = tid; q < NE * kEffQ; q += kAdjGridThreads) {
+    // only the effectors' components: the final sums read no further (nq = n_eff * 18)
+    for (int q = tid; q < (REP ? kQ : NE * kEffQ); q += kAdjGridThreads) {
         double s = 0.0;
-        for (int w = 0; w < kW; w++) s += wacc[w][q];
-        eff_partial[size_t(blockIdx.x) * kMaxEff * kEffQ + q] = s;
+        for (int w = 0; w < kW; w++) s += wacc[w * kQ + q];
+        eff_partial[size_t(blockIdx.x) * pstride + q] = s;
     }
 }
 
@@ -587,15 +596,17 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
 // CTA partials sit in a ring of kEffRing slots (deferred: one launch per ring,
 // not per substep); one CTA per (substep, effector component): strided thread
 // sums + fixed shuffle tree
-__global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nblocks, int nq, long t0, double* out) {
+// pstride: doubles per partial row / per substep of out (effector slots x 18)
+__global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nblocks, int nq, long t0, double* out,
+                                                   int pstride) {
     pdl_wait();
     __shared__ double wsum[8];
     const int q = blockIdx.x % nq, tid = threadIdx.x;
     const long t = t0 + blockIdx.x / nq;
-    const double* partial = ring + size_t(t % kEffRing) * nblocks * kMaxEff * kEffQ;
-    out += size_t(t) * kMaxEff * kEffQ;
+    const double* partial = ring + size_t(t % kEffRing) * nblocks * pstride;
+    out += size_t(t) * pstride;
     double s = 0.0;
-    for (int b = tid; b < nblocks; b += 256) s += partial[size_t(b) * kMaxEff * kEffQ + q];
+    for (int b = tid; b < nblocks; b += 256) s += partial[size_t(b) * pstride + q];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if ((tid & 31) == 0) wsum[tid >> 5] = s;
@@ -607,43 +618,53 @@ __global__ void __launch_bounds__(256) k_eff_final(const double* ring, int nbloc
     }
 }
 
-template <bool F>
+template <bool F, bool R>
 static void launch_adj_grid_t(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                               const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
                               double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s,
-                              const GridCols& cols) {
+                              const GridCols& cols, int pstride) {
     const dim3 gr(nblocks), bl(kAdjGridThreads);
-    switch (eff.n) {
-        case 0: launch_k(k_adj_grid<0, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        case 1: launch_k(k_adj_grid<1, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        case 2: launch_k(k_adj_grid<2, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        case 3: launch_k(k_adj_grid<3, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff,
-                         eff_partial, cmask, cols); break;
-        default: launch_k(k_adj_grid<kMaxEff, F>, gr, bl, 0, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0,
-                          gridbar, eff, eff_partial, cmask, cols);
+    const int ne = R ? eff.per_rep : eff.n;
+    const size_t smem = R ? size_t(kAdjGridThreads / 32) * eff.n * kEffQ * sizeof(double) : 0;
+#define FL_ADJGRID_CASE(NE)                                                                                        \
+    {                                                                                                              \
+        auto k = k_adj_grid<NE, F, R>;                                                                             \
+        if (R) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                   \
+        launch_k(k, gr, bl, smem, s, g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial,   \
+                 cmask, cols, pstride);                                                                            \
     }
+    switch (ne) {
+        case 0: FL_ADJGRID_CASE(0) break;
+        case 1: FL_ADJGRID_CASE(1) break;
+        case 2: FL_ADJGRID_CASE(2) break;
+        case 3: FL_ADJGRID_CASE(3) break;
+        default: FL_ADJGRID_CASE(kMaxEff)
+    }
+#undef FL_ADJGRID_CASE
 }
 
+// pstride: doubles per CTA partial row (effector slots x 18)
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s, int cmode, int c0,
-                     int c1) {
+                     double* eff_partial, const uint8_t* cmask, int nblocks, int pstride, cudaStream_t s, int cmode,
+                     int c0, int c1) {
     const GridCols cols{cmode, c0, c1};
-    if (cmode)
-        launch_adj_grid_t<true>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial, cmask,
-                                nblocks, s, cols);
+    if (eff.ext)
+        launch_adj_grid_t<false, true>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial,
+                                       cmask, nblocks, s, cols, pstride);
+    else if (cmode)
+        launch_adj_grid_t<true, false>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial,
+                                       cmask, nblocks, s, cols, pstride);
     else
-        launch_adj_grid_t<false>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial, cmask,
-                                 nblocks, s, cols);
+        launch_adj_grid_t<false, false>(g, nb_list, n_nb, blockmap, staging_bar, gridv0, gridbar, eff, eff_partial,
+                                        cmask, nblocks, s, cols, pstride);
 }
 
-void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out,
+void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out, int pstride,
                       cudaStream_t s) {
     if (n_eff <= 0 || count <= 0) return;
-    launch_k(k_eff_final, dim3(count * n_eff * kEffQ), dim3(256), 0, s, ring, nblocks, n_eff * kEffQ, t0, eff_out);
+    launch_k(k_eff_final, dim3(count * n_eff * kEffQ), dim3(256), 0, s, ring, nblocks, n_eff * kEffQ, t0, eff_out,
+             pstride);
 }
 
 // ---------------------------------------------------------------------------
@@ -868,6 +889,7 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_p2g(Geom g, PBuf pre, const ui
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
         ts.begin(g, gridbar, bx, by, bz, tid);
+        const int bxl = bx - rep_of_col(g, bx) * g.rstride;  // replica-local column (the weights)
         uint32_t s_nx = (HEAVY || !FL_ADJP2G_STAGE) && r.start + tid < r.end ? perm[r.start + tid] : 0u;  // see k_g2p
         ts.end(g, gridbar, bt, bx, by, bz, tid, NT);
         __syncthreads();
@@ -898,14 +920,14 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_p2g(Geom g, PBuf pre, const ui
                 asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
                 __syncthreads();
                 for (int k = tid; k < cn; k += NT)
-                    adj_p2g_particle<HEAVY>(g, AdjP2gStaged{sp, k, kStage}, ps[k], cls, bt, bx, by, bz, out,
+                    adj_p2g_particle<HEAVY>(g, AdjP2gStaged{sp, k, kStage}, ps[k], cls, bt, bxl, by, bz, out,
                                             nonfinite);
             }
         } else {
             for (int j = r.start + tid; j < r.end; j += NT) {
                 const uint32_t s = s_nx;
                 if (j + NT < r.end) s_nx = perm[j + NT];
-                adj_p2g_particle<HEAVY>(g, AdjP2gGlobal{pre, xbar_tmp, Fbar_tmp, s, j, cap}, s, cls, bt, bx, by, bz,
+                adj_p2g_particle<HEAVY>(g, AdjP2gGlobal{pre, xbar_tmp, Fbar_tmp, s, j, cap}, s, cls, bt, bxl, by, bz,
                                         out, nonfinite);
             }
         }

@@ -104,6 +104,7 @@ struct Record {
     float4* gridv0 = nullptr;  // (p/m, m) before gravity/walls/contact (grid-update adjoint input)
     uint8_t* cmask = nullptr;  // per node: effectors within contact range (bit e)
     int* blockmap = nullptr;   // particle block -> list slot + 1 (0 = none), incl. slab ghost blocks
+    EffK<float>* effx = nullptr;  // replica contexts: this substep's effector set (EffSet::ext)
     // host counts: exact on one rank; upper bounds on slabs, where `dcnt` (device,
     // [RecCnt]) holds the exact ones, the migration's message counts among them
     int n_active = 0;
@@ -123,7 +124,7 @@ struct Record {
     std::vector<ActEntry> act;
     std::vector<EmitAdjEntry> emit;
     EffSet effk{};
-    Record(int N, int maxb, int nbtot, int nmem, int nbody, int migcap) {
+    Record(int N, int maxb, int nbtot, int nmem, int nbody, int migcap, int neffx = 0) {
         size_t off = 0;
         auto carve = [&](size_t bytes) {
             size_t o = off;
@@ -136,7 +137,7 @@ struct Record {
                o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),
                o_gv = carve(size_t(nbtot) * 64 * sizeof(float4)), o_gv0 = carve(size_t(nbtot) * 64 * sizeof(float4)),
                o_mig = carve(size_t(2) * migcap * 4), o_cm = carve(size_t(nbtot) * 64), o_bm = carve(size_t(nbtot) * 4),
-               o_dc = carve(RC_N * sizeof(int));
+               o_dc = carve(RC_N * sizeof(int)), o_ex = carve(size_t(neffx) * sizeof(EffK<float>));
         CK(cudaMalloc(&mem, off));
         char* b = static_cast<char*>(mem);
         perm = reinterpret_cast<uint32_t*>(b + o_perm);
@@ -156,6 +157,7 @@ struct Record {
         cmask = reinterpret_cast<uint8_t*>(b + o_cm);
         blockmap = reinterpret_cast<int*>(b + o_bm);
         dcnt = reinterpret_cast<int*>(b + o_dc);
+        effx = neffx > 0 ? reinterpret_cast<EffK<float>*>(b + o_ex) : nullptr;
         mig_cap = migcap;
         CK(cudaMemset(gridv, 0, size_t(nbtot) * 64 * sizeof(float4)));
         CK(cudaMemset(gridv0, 0, size_t(nbtot) * 64 * sizeof(float4)));
@@ -558,7 +560,7 @@ struct Ctx {
     void eff_flush() {
         if (eff_lo < 0) return;
         launch_eff_final(eff_partial.p, eff_rows(), int(eff.size()), eff_lo, int(eff_hi - eff_lo + 1), eff_out.p,
-                         stream);
+                         eslots() * 18, stream);
         launches++;
         eff_lo = eff_hi = -1;
     }
@@ -591,8 +593,8 @@ struct Ctx {
             rec_pool.pop_back();
             return r;
         }
-        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1),
-                                        mig_cap);  // ~2 KB/node block
+        return std::make_shared<Record>(N, maxb, geom.nbtot, std::max(nmem, 1), std::max(nbody, 1), mig_cap,
+                                        nrep > 1 ? int(eff_shapes.size()) : 0);  // ~2 KB/node block
     }
     void put_record(RecordPtr r) {
         if (r) rec_pool.push_back(std::move(r));
@@ -629,16 +631,16 @@ struct Ctx {
     void require_single(const char* what) const {
         if (nrep > 1) throw FlumeError(FLUME_E_ARG, std::string(what) + ": not available on a replica context");
     }
-    // replica contexts: the effector set travels in device memory (a ring of per-substep
-    // copies from pinned memory; a slot is reused once its copy has run)
+    // replica contexts: the effector set travels in device memory, in the substep's record
+    // (the grid update and, later, its adjoint read it), copied from a ring of pinned
+    // staging slots (a slot is reused once its copy has run)
     static constexpr int kEffRingRep = 64;
     EffK<float>* h_effring = nullptr;
-    DevArr<EffK<float>> d_effring;
     std::vector<cudaEvent_t> effring_ev;
     int effring_i = 0;
     void fill_effk(size_t i, const EffState& e, EffK<float>& k) const;
-    EffSet replica_effset();
-    EffSet effset_now() { return nrep > 1 ? replica_effset() : make_effset(eff); }
+    EffSet replica_effset(Record& r);
+    EffSet effset_now(Record& r) { return nrep > 1 ? replica_effset(r) : make_effset(eff); }
     void check_error(long substep_base = 0);
     EffSet make_effset(const std::vector<EffState>& es) const;
     void advance_effectors(const double* action);
@@ -684,6 +686,23 @@ struct Ctx {
     void substep(const double* action, int count);
     void stage_grid(double* mass, double* vel);
     LossSet make_lossset(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep);
+    // one loss set per replica: the scene's terms on that replica's bodies
+    std::vector<LossSet> replica_lossets(const flume_loss_desc* loss, std::vector<std::shared_ptr<void>>& keep) {
+        std::vector<LossSet> lss;
+        lss.push_back(make_lossset(loss, keep));
+        for (int r = 1; r < nrep; r++) {
+            if (loss->attraction_weight > 0 && loss->n_prev > 0)
+                throw FlumeError(FLUME_E_ARG, "the attraction term is not available on a replica context");
+            flume_loss_desc dr = *loss;
+            std::vector<flume_loss_term> terms(loss->terms, loss->terms + loss->n_terms);
+            for (auto& t : terms) t.body += r * body_stride;
+            dr.terms = terms.data();
+            lss.push_back(make_lossset(&dr, keep));
+        }
+        return lss;
+    }
+    // effector-bar slots per substep (partials, final sums, spawn bars): at least kMaxEff
+    int eslots() const { return std::max<int>(kMaxEff, int(eff_shapes.size())); }
     PointLossScratch pls;  // trajectory_chamfer / mixing_spread scratch (fl_loss.cu)
     void point_losses(StateBuf& st, const LossSet& ls, uint32_t mask, int seg, double* out_dev, BarBuf* bars);
     void make_attraction(const flume_loss_desc* loss, LossSet& ls, std::vector<std::shared_ptr<void>>& keep);
@@ -942,7 +961,8 @@ void Ctx::init(const flume_scene_desc* desc, int dev, int n_replicas) {
     // the scene (grid-stride loop over the touched node blocks: never more CTAs than node
     // blocks or ~1 per 64 particles), at least one CTA per SM.
     eff_blocks = std::max(sm_count, std::min({kEffBlocks, g.nbtot, (N + 63) / 64}));
-    eff_partial.alloc(size_t(kEffRing) * 2 * eff_blocks * kMaxEff * 18);  // (slabs: interior + edge rows)
+    if (nrep > 1) eff_blocks = std::min(eff_blocks, 4 * sm_count);  // rows of every replica's effectors
+    eff_partial.alloc(size_t(kEffRing) * 2 * eff_blocks * eslots() * 18);  // (slabs: interior + edge rows)
 #ifndef FL_SORT_CTAS
 #define FL_SORT_CTAS 8
 #endif
@@ -963,11 +983,10 @@ EffSet Ctx::make_effset(const std::vector<EffState>& es) const {
     return s;
 }
 
-EffSet Ctx::replica_effset() {
+EffSet Ctx::replica_effset(Record& r) {
     const size_t ne = eff.size();
     if (!h_effring) {
         CK(cudaMallocHost(&h_effring, size_t(kEffRingRep) * ne * sizeof(EffK<float>)));
-        d_effring.alloc(size_t(kEffRingRep) * ne);
         effring_ev.assign(kEffRingRep, nullptr);
     }
     const int slot = effring_i;
@@ -976,7 +995,7 @@ EffSet Ctx::replica_effset() {
     else CK(cudaEventCreateWithFlags(&effring_ev[slot], cudaEventDisableTiming));
     EffK<float>* h = h_effring + size_t(slot) * ne;
     for (size_t i = 0; i < ne; i++) fill_effk(i, eff[i], h[i]);
-    EffK<float>* d = d_effring.p + size_t(slot) * ne;
+    EffK<float>* d = r.effx;
     CK(cudaMemcpyAsync(d, h, ne * sizeof(EffK<float>), cudaMemcpyHostToDevice, stream));
     CK(cudaEventRecord(effring_ev[slot], stream));
     EffSet s{};
@@ -1404,7 +1423,7 @@ void Ctx::return_bars(Record& r, BarBuf post) {
 void Ctx::forward_substep(const double* action, StatePtr in, StatePtr out, Record& r) {
     advance_effectors(action);
     r.substep = substep_index;
-    r.effk = effset_now();
+    r.effk = effset_now(r);
     // activation (mpm.hpp:435-449): ids reaching their activation substep
     r.act.clear();
     r.emit.clear();
@@ -1819,21 +1838,7 @@ double Ctx::rollout_loss(const flume_actions* a, const flume_loss_desc* loss, lo
     const long T = long(a->n_segments) * a->segment_length;
     if (window <= 0) window = T;
     std::vector<std::shared_ptr<void>> keep;
-    // one loss set per replica: the scene's terms on that replica's bodies
-    std::vector<LossSet> lss;
-    for (int r = 0; r < nrep; r++) {
-        if (r == 0) {
-            lss.push_back(make_lossset(loss, keep));
-            continue;
-        }
-        if (loss && loss->attraction_weight > 0 && loss->n_prev > 0)
-            throw FlumeError(FLUME_E_ARG, "rollout_loss: the attraction term is not available on a replica context");
-        flume_loss_desc dr = *loss;
-        std::vector<flume_loss_term> terms(loss->terms, loss->terms + loss->n_terms);
-        for (auto& t : terms) t.body += r * body_stride;
-        dr.terms = terms.data();
-        lss.push_back(make_lossset(&dr, keep));
-    }
+    std::vector<LossSet> lss = replica_lossets(loss, keep);
     const int nseg = a->n_segments;
     loss_out.alloc(size_t(nrep) * nseg);
     // state0 is const: work on a copy
@@ -1911,7 +1916,8 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
              launch_adj_g2p(g, pre.p, r.perm, r.recs, r.n_blocks, r.celltab, hv ? heavy_grid(grid_adj_h) : light_grid(grid_adj, r.n_active), d_cls.p,
                             r.gridv, post_st.p, post, xbar_tmp.p, Fbar_tmp.p, rd, start_bar.p, staging_bar.p, hv ? hvar : 0, w, s);
          }));
-    double* ep = eff_partial.p + size_t(t_slot % kEffRing) * eff_rows() * kMaxEff * 18;
+    const int es = eslots();
+    double* ep = eff_partial.p + size_t(t_slot % kEffRing) * eff_rows() * es * 18;
     if (slab()) {
         // as in the forward: the halo planes of the v_bar tiles travel while the interior node
         // columns run their adjoint; the edge columns' effector-bar partials take the second
@@ -1922,14 +1928,15 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
         halo_exchange(r.blockmap, staging_bar.p, nullptr, s_comm);
         CK(cudaEventRecord(ev_halo_join, s_comm));
         PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                         ep, r.cmask, eff_blocks, stream, 1, c0, c1));
+                                         ep, r.cmask, eff_blocks, es * 18, stream, 1, c0, c1));
         PROF(K_COMM, CK(cudaStreamWaitEvent(stream, ev_halo_join, 0)));
         PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                         ep + size_t(eff_blocks) * kMaxEff * 18, r.cmask, eff_blocks, stream, 2, c0, c1));
+                                         ep + size_t(eff_blocks) * es * 18, r.cmask, eff_blocks, es * 18, stream, 2, c0,
+                                         c1));
         launches++;
     } else {
         PROF(K_ADJ_GRID, launch_adj_grid(g, r.nb_list, r.n_nb, r.blockmap, staging_bar.p, r.gridv0, gridbar.p, r.effk,
-                                         ep, r.cmask, eff_blocks, stream));
+                                         ep, r.cmask, eff_blocks, es * 18, stream));
     }
     eff_pending(t_slot);
     PROF(K_ADJ_P2G, dual([&](bool hv, int* w, cudaStream_t s) {
@@ -1943,7 +1950,7 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
     launches += 1 + (r.n_stored > r.n_active ? 1 : 0);  // grid adjoint, tail bars (dual() counts the rest)
     check_launch();
     if (!r.emit.empty()) {
-        double* eo = em_out.p + size_t(t_slot) * kMaxEff * 12;
+        double* eo = em_out.p + size_t(t_slot) * es * 12;
         if (r.emit.size() <= size_t(kEmitInline)) {
             launch_adj_emit_inline(out, r.emit.data(), int(r.emit.size()), eo, int(eff.size()),
                                    slab() ? r.dcnt + RC_PARK : nullptr, stream);
@@ -1961,16 +1968,18 @@ void Ctx::adjoint_step(StateBuf& pre, StateBuf& post_st, Record& r, DevArr<float
 
 void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, long stride, long window,
                           double* grad, double* loss_out_h, double* full_loss, double* per_seg, long* snapshots) {
-    require_single("grad_trajectory");
+    // replica contexts: grad = n_rep x n_segments x 6, loss_out_h / full_loss n_rep,
+    // per_seg n_rep x n_segments
     const long T = long(a->n_segments) * a->segment_length;
     if (stride <= 0) stride = T;
     if (window <= 0) window = T;
     const int nseg = a->n_segments, seglen = a->segment_length;
     std::vector<std::shared_ptr<void>> keep;
-    LossSet ls = make_lossset(loss, keep);
-    loss_out.alloc(nseg);
-    eff_out.alloc(size_t(T) * kMaxEff * 18);
-    em_out.alloc(size_t(T) * kMaxEff * 12);
+    const std::vector<LossSet> lss = replica_lossets(loss, keep);
+    loss_out.alloc(size_t(nrep) * nseg);
+    const int es = eslots();
+    eff_out.alloc(size_t(T) * es * 18);
+    em_out.alloc(size_t(T) * es * 12);
     d_nonfinite.alloc(T);
     xbar_tmp.alloc(size_t(N) * 3);
     Fbar_tmp.alloc(size_t(N) * 9);
@@ -2079,7 +2088,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         RecordPtr rec = in_last ? get_record() : scratch_rec;
         StatePtr nxt = get_state();
         eff_pre[t] = eff;
-        forward_substep(a->values + 6 * (t / seglen), st, nxt, *rec);
+        forward_substep(a->values + act_stride() * (t / seglen), st, nxt, *rec);
         eff_post[t] = eff;
         if (in_last) {
             cache_recs.push_back(rec);
@@ -2092,22 +2101,26 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         if ((t + 1) % stride == 0) take_snapshot(t + 1, st);
         if ((t + 1) % seglen == 0) {
             int seg = int((t + 1) / seglen) - 1;
-            eval_loss(*st, ls, loss_mask(loss, seg, nseg), loss_out.p + seg, seg, substep_index);
+            for (int rp = 0; rp < nrep; rp++)
+                eval_loss(*st, lss[size_t(rp)], loss_mask(loss, seg, nseg), loss_out.p + size_t(rp) * nseg + seg, seg,
+                          substep_index);
         }
     }
     retire_spilled(true);
     const size_t n_snap = snaps.size() + hsnaps.size() + fsnaps.size();
     allreduce(loss_out.p, size_t(nseg), DType::F64, ROp::Sum);
     CK(cudaEventRecord(ev1, stream));
-    std::vector<double> per(nseg);
+    std::vector<double> per(size_t(nrep) * nseg);
     CK(cudaMemcpyAsync(per.data(), loss_out.p, per.size() * 8, cudaMemcpyDeviceToHost, stream));
     check_error();
-    double lsum = 0, fsum = 0;
-    for (int s = 0; s < nseg; s++) {
-        fsum += per[s];
-        if (long(s + 1) * seglen <= window) lsum += per[s];
+    std::vector<double> lsum(nrep, 0.0), fsum(nrep, 0.0);
+    for (int rp = 0; rp < nrep; rp++) {
+        for (int s = 0; s < nseg; s++) {
+            fsum[rp] += per[size_t(rp) * nseg + s];
+            if (long(s + 1) * seglen <= window) lsum[rp] += per[size_t(rp) * nseg + s];
+        }
+        if (!std::isfinite(lsum[rp])) throw FlumeError(FLUME_E_ENGINE, "grad_trajectory: non-finite forward loss");
     }
-    if (!std::isfinite(lsum)) throw FlumeError(FLUME_E_ENGINE, "grad_trajectory: non-finite forward loss");
 
     // ---------------- backward ----------------
     
@@ -2150,7 +2163,7 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
         for (long q = base; q < end; q++) {
             RecordPtr rec = get_record();
             StatePtr nxt = get_state();
-            forward_substep(a->values + 6 * (q / seglen), s, nxt, *rec);
+            forward_substep(a->values + act_stride() * (q / seglen), s, nxt, *rec);
             cache_recs.push_back(rec);
             cache_states.push_back(nxt);
             s = nxt;
@@ -2161,12 +2174,14 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             int seg = int((t + 1) / seglen) - 1;
             ensure_cached(t);
             StateBuf& boundary = *cache_states[size_t(t + 1 - cache_base)];
-            const LossSet lsb = at_substep(ls, s0 + t + 1);
-            launch_loss_grad(boundary.p, dn(boundary.n, slab() ? boundary.cnt + SC_STORED : nullptr), d_cls.p, lsb, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N},
-                             geom.key_inactive, stream);
-            launches++;
-            BarBuf bb{barsA.p, N};
-            point_losses(boundary, lsb, loss_mask(loss, seg, nseg), seg, nullptr, &bb);
+            for (int rp = 0; rp < nrep; rp++) {  // (replicas: disjoint particles, one pass each)
+                const LossSet lsb = at_substep(lss[size_t(rp)], s0 + t + 1);
+                launch_loss_grad(boundary.p, dn(boundary.n, slab() ? boundary.cnt + SC_STORED : nullptr), d_cls.p,
+                                 lsb, loss_mask(loss, seg, nseg), BarBuf{barsA.p, N}, geom.key_inactive, stream);
+                launches++;
+                BarBuf bb{barsA.p, N};
+                point_losses(boundary, lsb, loss_mask(loss, seg, nseg), seg, nullptr, &bb);
+            }
         }
         ensure_cached(t);
         const size_t k = size_t(t - cache_base);
@@ -2180,14 +2195,14 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     for (cudaEvent_t e : own_events) cudaEventDestroy(e);
     eff_flush();
     if (slab()) {  // per-slab effector / spawn bars and non-finite flags
-        allreduce(eff_out.p, size_t(T) * kMaxEff * 18, DType::F64, ROp::Sum);
-        allreduce(em_out.p, size_t(T) * kMaxEff * 12, DType::F64, ROp::Sum);
+        allreduce(eff_out.p, size_t(T) * es * 18, DType::F64, ROp::Sum);
+        allreduce(em_out.p, size_t(T) * es * 12, DType::F64, ROp::Sum);
         allreduce(d_nonfinite.p, size_t(T), DType::I32, ROp::Max);
     }
     CK(cudaEventRecord(ev2, stream));
 
     // ---------------- effector pose chain (host, fp64) ----------------
-    std::vector<double> eb(size_t(T) * kMaxEff * 18), em(size_t(T) * kMaxEff * 12);
+    std::vector<double> eb(size_t(T) * es * 18), em(size_t(T) * es * 12);
     std::vector<int> nonf(T);
     CK(cudaMemcpyAsync(eb.data(), eff_out.p, eb.size() * 8, cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(em.data(), em_out.p, em.size() * 8, cudaMemcpyDeviceToHost, stream));
@@ -2205,14 +2220,15 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
     const double dt = cfg.dt_substep;
     std::vector<V3<double>> et(ne, V3<double>{0, 0, 0});
     std::vector<M3<double>> eR(ne, mzero<double>());
-    for (int s = 0; s < nseg; s++)
+    for (int s = 0; s < nrep * nseg; s++)
         for (int k2 = 0; k2 < 6; k2++) grad[6 * s + k2] = 0.0;
     for (long t = T - 1; t >= 0; t--) {
         const int seg = int(t / seglen);
         double echeck = 0;
         for (size_t e = 0; e < ne; e++) {
-            const double* b = &eb[(size_t(t) * kMaxEff + e) * 18];
-            const double* m = &em[(size_t(t) * kMaxEff + e) * 12];
+            const double* b = &eb[(size_t(t) * es + e) * 18];
+            const double* m = &em[(size_t(t) * es + e) * 12];
+            double* gs = grad + 6 * (size_t(nrep > 1 ? e / e1 : 0) * nseg + seg);  // replica-major
             for (int q = 0; q < 3; q++) et[e][q] += m[q];
             for (int q = 0; q < 9; q++) eR[e].m[q] += m[3 + q];
             V3<double> t_bar = et[e] + V3<double>{b[0], b[1], b[2]};
@@ -2226,9 +2242,9 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             eR[e] = r_pre_bar;
             const int* mask = eff_shapes[e].action_mask;
             for (int q = 0; q < 3; q++)
-                if (mask[q]) grad[6 * seg + q] += vlin_bar[q];
+                if (mask[q]) gs[q] += vlin_bar[q];
             for (int q = 0; q < 3; q++)
-                if (mask[3 + q]) grad[6 * seg + 3 + q] += w_bar[q];
+                if (mask[3 + q]) gs[3 + q] += w_bar[q];
             echeck += t_bar.x;
         }
         if (nonf[t] || !std::isfinite(echeck)) {
@@ -2237,10 +2253,12 @@ void Ctx::grad_trajectory(const flume_actions* a, const flume_loss_desc* loss, l
             throw e;
         }
     }
-    if (loss_out_h) *loss_out_h = lsum;
-    if (full_loss) *full_loss = fsum;
+    for (int rp = 0; rp < nrep; rp++) {
+        if (loss_out_h) loss_out_h[rp] = lsum[size_t(rp)];
+        if (full_loss) full_loss[rp] = fsum[size_t(rp)];
+    }
     if (per_seg)
-        for (int s = 0; s < nseg; s++) per_seg[s] = per[s];
+        for (size_t s = 0; s < per.size(); s++) per_seg[s] = per[s];
     if (snapshots) *snapshots = long(n_snap);
     timing.forward_ms = fms;
     timing.backward_ms = bms;
@@ -2771,6 +2789,7 @@ int flume_rollout_loss(flume_ctx* ctx, const flume_actions* actions, const flume
     if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
     return guard(ctx, [&] {
         ctx->c.require_particles();
+        ctx->c.require_single("flume_rollout_loss (flume_replicas_rollout_loss)");
         ctx->c.slab_retry(false, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment); });
     });
 }
@@ -2780,6 +2799,7 @@ int flume_rollout_loss_final(flume_ctx* ctx, const flume_actions* actions, const
     if (!ctx || !actions || !loss_out) return FLUME_E_ARG;
     return guard(ctx, [&] {
         ctx->c.require_particles();
+        ctx->c.require_single("flume_rollout_loss (flume_replicas_rollout_loss)");
         ctx->c.slab_retry(true, [&] { *loss_out = ctx->c.rollout_loss(actions, loss, window, per_segment, true); });
     });
 }
@@ -2798,10 +2818,22 @@ int flume_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const fl
     if (!ctx || !actions || !action_grad) return FLUME_E_ARG;
     return guard(ctx, [&] {
         ctx->c.require_particles();
+        ctx->c.require_single("flume_grad_trajectory (flume_replicas_grad_trajectory)");
         ctx->c.slab_retry(false, [&] {
             ctx->c.grad_trajectory(actions, loss, stride, window, action_grad, loss_out, full_loss, per_segment,
                                    snapshots);
         });
+    });
+}
+
+int flume_replicas_grad_trajectory(flume_ctx* ctx, const flume_actions* actions, const flume_loss_desc* loss,
+                                   long stride, long window, double* action_grad, double* loss_out,
+                                   double* full_loss, double* per_segment, long* snapshots) {
+    if (!ctx || !actions || !action_grad) return FLUME_E_ARG;
+    return guard(ctx, [&] {
+        ctx->c.require_particles();
+        ctx->c.grad_trajectory(actions, loss, stride, window, action_grad, loss_out, full_loss, per_segment,
+                               snapshots);
     });
 }
 

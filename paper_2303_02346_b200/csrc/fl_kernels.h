@@ -255,10 +255,10 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     float4* staging_bar, int variant, int* wq, cudaStream_t s);
 void launch_adj_grid(const Geom& g, const int* nb_list, const int* n_nb, const int* blockmap,
                      const float4* staging_bar, const float4* gridv0, float4* gridbar, const EffSet& eff,
-                     double* eff_partial, const uint8_t* cmask, int nblocks, cudaStream_t s, int cmode = 0,
-                     int c0 = -1, int c1 = -1);
+                     double* eff_partial, const uint8_t* cmask, int nblocks, int pstride, cudaStream_t s,
+                     int cmode = 0, int c0 = -1, int c1 = -1);
 constexpr int kEffRing = 16;  // substeps whose effector-bar partials wait for one final-sum launch
-void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out,
+void launch_eff_final(const double* ring, int nblocks, int n_eff, long t0, int count, double* eff_out, int pstride,
                       cudaStream_t s);
 void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRec* recs, const int* n_blocks,
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,

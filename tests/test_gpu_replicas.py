@@ -1,7 +1,8 @@
 """Replica contexts: a population of one scene in one grid, every kernel
 launch covering all candidates (flume_ctx_create_replicas).  Each replica must evolve exactly
 like a single context given that replica's actions: final states bit-identical, losses equal
-up to the order of the fp64 loss sums (the replicas' particles sit at other store slots).
+up to the order of the fp64 loss sums (the replicas' particles sit at other store slots), and
+gradients (grad_trajectory_replicas) up to the order of the fp64 effector-bar sums.
 
   c1        one liquid + a box effector, full size, 4 candidates
   c2 @ 64   emitters attached to an effector (activation per replica), 3 candidates
@@ -54,11 +55,39 @@ def test_replicas_match_single_contexts(name, res, R, nseg, seglen):
     assert len({round(l, 9) for l in losses}) > 1
 
 
-def test_replica_context_is_forward_only():
+@pytest.mark.parametrize("name,res,R,nseg,seglen,stride", [("c1", None, 3, 2, 10, 5), ("c5", 32, 3, 2, 5, 5),
+                                                           ("c2", 64, 2, 2, 10, 10)])
+def test_replica_gradients_match_single_contexts(name, res, R, nseg, seglen, stride):
+    """grad_trajectory of a population in one replica context (records, checkpoint replays,
+    effector bars of every replica's effectors) against single contexts: the particle
+    cotangents are the same per block; only the fp64 effector-bar sums run in another order."""
+    w = fl.build_scene(spec_for(name, res))
+    pop = _population(w, R, nseg, seed=1)
+    for a in pop:
+        a.segment_length = seglen
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    rws = fl.ReplicaWorkspace(w.scene, R)
+    gr = fl.grad_trajectory_replicas(w.scene, w.state, pop, loss, rws, stride=stride)
+    rws.close()
+    ws = fl.GpuWorkspace(w.scene)
+    for r in range(R):
+        g1 = fl.grad_trajectory(w.scene, w.state, pop[r], loss, stride=stride, ws=ws)
+        assert abs(gr[r].loss - g1.loss) <= 1e-12 * abs(g1.loss), (r, gr[r].loss, g1.loss)
+        np.testing.assert_allclose(gr[r].per_segment, g1.per_segment, rtol=1e-12, atol=0)
+        scale = np.abs(g1.action_grad).max()
+        assert scale > 0
+        assert np.abs(gr[r].action_grad - g1.action_grad).max() <= 1e-9 * scale, (r, gr[r].action_grad, g1.action_grad)
+        assert gr[r].snapshots == g1.snapshots
+    ws.close()
+
+
+def test_replica_context_rejects_single_scene_calls():
     w = fl.build_scene(spec_for("c1", 32))
     rws = fl.ReplicaWorkspace(w.scene, 2)
     acts = fl.ActionTrajectory(1, 2, w.init_action.reshape(1, 6))
     loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
     with pytest.raises(ValueError):
         fl.grad_trajectory(w.scene, rws.replicate(w.state), acts, loss, ws=rws)
+    with pytest.raises(ValueError):
+        fl.rollout_loss(w.scene, rws.replicate(w.state), acts, loss, ws=rws)
     rws.close()

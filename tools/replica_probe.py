@@ -1,7 +1,8 @@
 """Population throughput: R candidate rollouts of one scene -- one after
 another on one context, on a pool of concurrent contexts, and in one replica context
-(every launch covering all R).  Prints one JSON line per R with candidates/s and
-particle-substeps/s of each mode (wall clock around synchronous calls, after a warm-up)."""
+(every launch covering all R) -- and R gradients (grad_trajectory, one after another vs one
+replica context).  Prints one JSON line per R with candidates/s and particle-substeps/s of
+each mode (wall clock around synchronous calls, after a warm-up)."""
 import json
 import sys
 import time
@@ -41,10 +42,14 @@ for R in Rs:
     pl = timed(lambda: fl.rollout_loss_batch(w.scene, w.state, P, loss, pool))
     rws = fl.ReplicaWorkspace(w.scene, R)
     rep = timed(lambda: fl.rollout_loss_replicas(w.scene, w.state, P, loss, rws))
+    gseq = timed(lambda: [fl.grad_trajectory(w.scene, w.state, a, loss, ws=ws) for a in P], reps=2)
+    grep_ = timed(lambda: fl.grad_trajectory_replicas(w.scene, w.state, P, loss, rws), reps=2)
     rws.close()
     ps = R * n * nseg * seglen
     print(json.dumps({"scene": name, "replicas": R, "particles": n, "horizon": nseg * seglen,
                       "sequential_s": seq, "pool4_s": pl, "replica_s": rep,
                       "candidates_per_s": {"sequential": R / seq, "pool4": R / pl, "replica": R / rep},
-                      "particle_substeps_per_s": {"sequential": ps / seq, "pool4": ps / pl, "replica": ps / rep}}),
+                      "particle_substeps_per_s": {"sequential": ps / seq, "pool4": ps / pl, "replica": ps / rep},
+                      "grad_s": {"sequential": gseq, "replica": grep_},
+                      "grad_candidates_per_s": {"sequential": R / gseq, "replica": R / grep_}}),
           flush=True)
