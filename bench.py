@@ -285,6 +285,39 @@ def scene_rates(name, steps, warmup, horizon=None, device=0):
     return out
 
 
+def population_rates(name, R, steps, warmup, device=0):
+    """A population of R candidates of a BASELINE config in one replica context (SURVEY.md
+    8(f)3): fwd+bwd = grad_trajectory_replicas over one optimizer segment, fwd = the same
+    substeps of all R (device time, CUDA events); rates count all R candidates' particles."""
+    import paper_2303_02346_b200 as fl
+    from paper_2303_02346_b200 import scenes
+    w = fl.build_scene(scenes.load(name))
+    rws = fl.ReplicaWorkspace(w.scene, R, device=device)
+    lib, ctx = rws.lib, rws.ctx
+    check = lambda rc: fl.api._raise(lib, ctx, rc)  # noqa: E731
+    n = int(np.sum(w.scene.activation_substep <= 0))
+    T = w.segment_length or 50
+    rng = np.random.default_rng(0)
+    pop = [fl.ActionTrajectory(1, T, w.init_action.reshape(1, 6) + 0.1 * rng.standard_normal((1, 6)))
+           for _ in range(R)]
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    for _ in range(warmup):
+        fl.grad_trajectory_replicas(w.scene, w.state, pop, loss, rws)
+    gms = 0.0
+    for _ in range(steps):
+        g = fl.grad_trajectory_replicas(w.scene, w.state, pop, loss, rws)
+        gms += g[0].forward_ms + g[0].backward_ms
+    acts = np.ascontiguousarray(np.concatenate([a.values[0] for a in pop]))
+    fms = 0.0
+    for _ in range(steps):
+        rws._upload(rws.replicate(w.state))
+        fms += _device_ms(lib, ctx, check, lambda: check(lib.flume_substep(ctx, fl.api._dp(acts), T)))
+    out = {"replicas": R, "particles": R * n, "substeps": T, "fwd_bwd": R * n * T * steps / (gms / 1e3),
+           "fwd": R * n * T * steps / (fms / 1e3), "context": "one replica context: every launch covers all R"}
+    rws.close()
+    return out
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -543,6 +576,10 @@ def run_ours(args):
                                             device=local)
             except Exception as e:
                 configs[name] = {"error": str(e)}
+        try:  # a CMA-ES-sized population of the small scene in one replica context
+            configs["c1x16"] = population_rates("c1", 16, 2, 1, device=local)
+        except Exception as e:
+            configs["c1x16"] = {"error": str(e)}
         try:
             sb = scene_rates(SCENE_SCALE, 2, 1, horizon=SCALE_HORIZON, device=local)
             scaling_base = {"scene": SCENE_SCALE, "value": sb["fwd_bwd"], "fwd": sb["fwd"], "unit": UNIT,
