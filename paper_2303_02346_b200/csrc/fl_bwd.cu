@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_g2p(Geom g, PBuf pre, const ui
                                                         const float4* __restrict__ gridv, PBuf postst, BarBuf post,
                                                         float* xbar_tmp, float* Fbar_tmp, RigidDev rd,
                                                         const float* __restrict__ start_bar, float4* staging_bar,
-                                                        int cap, int* wq) {
-    pdl_wait();
+                                                        int cap, int* wq, int role) {
+    const DualScope dual_scope(role);
     extern __shared__ __align__(16) unsigned char smraw[];
     ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
     float4* vt = reinterpret_cast<float4*>(smraw + sizeof(ScSmem));
@@ -441,7 +441,7 @@ void launch_adj_g2p(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
         attr[variant] = true;
     }
     launch_k(adj_g2p_kernel(variant), dim3(grid), dim3(adj_g2p_threads(variant)), smem, s, g, pre, perm, recs, n_blocks, celltab,
-             cls, gridv, postst, post, xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq);
+             cls, gridv, postst, post, xbar_tmp, Fbar_tmp, rd, start_bar, staging_bar, post.cap, wq, dual_role());
 }
 
 // ---------------------------------------------------------------------------
@@ -869,8 +869,8 @@ __global__ void __launch_bounds__(NT, MINB) k_adj_p2g(Geom g, PBuf pre, const ui
                                                  const float4* __restrict__ gridbar,
                                                  const float* __restrict__ xbar_tmp,
                                                  const float* __restrict__ Fbar_tmp, BarBuf out, int* nonfinite,
-                                                 int cap, int* wq) {
-    pdl_wait();
+                                                 int cap, int* wq, int role) {
+    const DualScope dual_scope(role);
     __shared__ float4 bt[kTile];
     __shared__ __align__(128) float4 raw[FL_TMA_TILE ? kTileRaw : 1];
     __shared__ __align__(8) uint64_t bar;
@@ -949,7 +949,7 @@ void launch_adj_p2g(const Geom& g, PBuf pre, const uint32_t* perm, const BlockRe
                     int grid, const ClassInfo* cls, const float4* gridbar, const float* xbar_tmp,
                     const float* Fbar_tmp, BarBuf out, int* nonfinite, int variant, int* wq, cudaStream_t s) {
     launch_k(adj_p2g_kernel(variant), dim3(grid), dim3(adj_p2g_threads(variant)), 0, s, g, pre, perm, recs, n_blocks, cls, gridbar,
-             xbar_tmp, Fbar_tmp, out, nonfinite, out.cap, wq);
+             xbar_tmp, Fbar_tmp, out, nonfinite, out.cap, wq, dual_role());
 }
 
 // inactive particles pass their bars through untouched

@@ -280,6 +280,12 @@ struct Ctx {
         wq_next += n;
         return p;
     }
+    // The SVD/rigid ("heavy") and plain-liquid ("light") variants of a scatter/gather kernel.
+    // dual_mode 1 (default): one stream, the heavy grid first, releasing the light grid as
+    // soon as its CTAs are resident (DualScope, fl_layout.cuh), so the few long heavy blocks
+    // run beside the light ones.  dual_mode 0 (rounds 1-2): the heavy grid on a second stream
+    // -- but the light grid, launched early by programmatic serialization, filled every SM
+    // first and the heavy grid mostly ran after it (c4 grad_trajectory 175.9 -> 162.4 ms).
     template <class Fn>
     void dual(Fn&& fn) {
         if (!classes_heavy && !upload_full) {  // no SVD/rigid particle can exist: light kernel only
@@ -290,6 +296,14 @@ struct Ctx {
         launches += 2;
         int* wh = take_wq(2);
         int* wl = wh + 1;
+        if (dual_mode == 1) {
+            dual_role() = 1;
+            fn(true, wh, stream);
+            dual_role() = 2;
+            fn(false, wl, stream);
+            dual_role() = 0;
+            return;
+        }
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(s2, ev_fork, 0));
         fn(true, wh, s2);
@@ -297,6 +311,7 @@ struct Ctx {
         CK(cudaEventRecord(ev_join, s2));
         CK(cudaStreamWaitEvent(stream, ev_join, 0));
     }
+    int dual_mode = 1;
     int device = 0;
     cudaStream_t stream = nullptr;
     flume_error_info last_err{};
@@ -736,6 +751,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev, int n_replicas) {
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    if (const char* dm = getenv("FL_DUAL_MODE")) dual_mode = atoi(dm);  // A/B experiments (tools/dual_probe.py)
     CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     wq.alloc(kWq);

@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(NT, MINB) k_p2g(Geom g, PBuf st, const uint32_
                                                     const int* __restrict__ n_blocks,
                                                     const uint16_t* __restrict__ celltab,
                                                     const ClassInfo* __restrict__ cls, float4* staging,
-                                                    unsigned long long* err, uint32_t substep, int* wq) {
-    pdl_wait();
+                                                    unsigned long long* err, uint32_t substep, int* wq, int role) {
+    const DualScope dual_scope(role);
     extern __shared__ __align__(16) unsigned char smraw[];
     ScSmem& sm = *reinterpret_cast<ScSmem*>(smraw);
     const int tid = threadIdx.x;
@@ -307,7 +307,7 @@ void launch_p2g(const Geom& g, PBuf st, const uint32_t* perm, const BlockRec* re
         attr[variant] = true;
     }
     launch_k(p2g_kernel(variant), dim3(grid), dim3(p2g_threads(variant)), sizeof(ScSmem), s, g, st, perm, recs, n_blocks,
-             celltab, cls, staging, err, substep, wq);
+             celltab, cls, staging, err, substep, wq, dual_role());
 }
 
 // ---------------------------------------------------------------------------
@@ -421,8 +421,9 @@ template <bool HEAVY, int MINB, int NT = 128>
 __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
                                              const BlockRec* __restrict__ recs, const int* __restrict__ n_blocks,
                                              const ClassInfo* __restrict__ cls, const float4* __restrict__ gridv,
-                                             RigidDev rd, unsigned long long* err, uint32_t substep, int* wq) {
-    pdl_wait();
+                                             RigidDev rd, unsigned long long* err, uint32_t substep, int* wq,
+                                             int role) {
+    const DualScope dual_scope(role);
     __shared__ float4 vt[kTile];
     __shared__ __align__(128) float4 raw[FL_TMA_TILE ? kTileRaw : 1];
     __shared__ __align__(8) uint64_t bar;
@@ -554,7 +555,7 @@ void launch_g2p(const Geom& g, PBuf in, PBuf out, const uint32_t* perm, const Bl
                 int grid, const ClassInfo* cls, const float4* gridv, RigidDev rd, unsigned long long* err,
                 uint32_t substep, int variant, int* wq, cudaStream_t s) {
     launch_k(g2p_kernel(variant), dim3(grid), dim3(g2p_threads(variant)), 0, s, g, in, out, perm, recs, n_blocks, cls, gridv, rd, err,
-             substep, wq);
+             substep, wq, dual_role());
 }
 
 __global__ void k_tail_copy(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm, DN n0, DN n1) {

@@ -12,6 +12,12 @@
 
 namespace fl {
 
+// role of the next dual-variant launch of this host thread (DualScope, fl_layout.cuh)
+inline int& dual_role() {
+    static thread_local int role = 0;
+    return role;
+}
+
 // hot-path launch with programmatic stream serialization (see pdl_wait)
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {

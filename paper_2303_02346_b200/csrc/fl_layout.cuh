@@ -162,6 +162,28 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 
+// The SVD/rigid and plain-liquid variants of a scatter/gather kernel ("dual" launches) run
+// back to back on one stream: the heavy grid (role 1) waits for its predecessor as usual and
+// then releases its dependent at once (griddepcontrol.launch_dependents), so the light grid
+// (role 2) is placed beside the heavy CTAs already resident instead of filling every SM
+// first.  The light grid reads only what the heavy grid's predecessor wrote (complete: the
+// heavy grid waited for it before releasing), so it skips the start wait and waits for the
+// heavy grid at its end instead -- the next kernel then sees both.  Role 0: a plain launch.
+struct DualScope {
+    int role;
+    __device__ __forceinline__ explicit DualScope(int r) : role(r) {
+        if (role != 2) pdl_wait();
+#if defined(__CUDA_ARCH__) && FL_PDL
+        if (role == 1) asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
+    }
+    __device__ __forceinline__ ~DualScope() {
+#if defined(__CUDA_ARCH__) && FL_PDL
+        if (role == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+    }
+};
+
 __host__ __device__ inline int key_col(const Geom& g, uint32_t key) { return int(key >> 6) / g.colblocks; }
 
 // sort block of a key: its particle block, or the virtual parked / departed blocks nbtot, nbtot + 1
