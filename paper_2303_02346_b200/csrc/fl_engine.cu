@@ -131,7 +131,7 @@ struct Record {
             off += (bytes + 255) & ~size_t(255);
             return o;
         };
-        size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(16),
+        size_t o_perm = carve(size_t(N) * 4), o_recs = carve(size_t(maxb) * sizeof(BlockRec)), o_nb = carve(size_t(work_order_ints(maxb)) * 4),
                o_nbl = carve(size_t(nbtot) * 4), o_nnb = carve(16), o_ms = carve(size_t(nmem) * 4),
                o_mst = carve(size_t(nmem) * 24), o_mid = carve(size_t(nmem) * 32),
                o_fit = carve(size_t(nbody) * 24 * 8), o_ct = carve(size_t(maxb) * kCellTab * 2),

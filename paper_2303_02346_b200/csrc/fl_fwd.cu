@@ -188,8 +188,9 @@ __global__ void __launch_bounds__(NT, MINB) k_p2g(Geom g, PBuf st, const uint32_
     const int my_c = tid & 63, my_ox = tid >> 6;
     __shared__ int sh_next;
     for (;;) {
-        const int b = q0 + next_work(wq, &sh_next);
-        if (b >= q1) break;
+        const int k = next_work(wq, &sh_next);
+        if (k >= q1 - q0) break;
+        const int b = work_block(n_blocks, g.maxb, HEAVY ? 1 : 0, k);  // costliest blocks first
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
@@ -433,8 +434,9 @@ __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, con
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     __shared__ int sh_next;
     for (;;) {
-        const int b = q0 + next_work(wq, &sh_next);
-        if (b >= q1) break;
+        const int k = next_work(wq, &sh_next);
+        if (k >= q1 - q0) break;
+        const int b = work_block(n_blocks, g.maxb, HEAVY ? 1 : 0, k);  // costliest blocks first
         const BlockRec r = recs[b];
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);

@@ -311,14 +311,14 @@ void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bhe
 void launch_isort_diff(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,
                        const IncSort& is, bool meta, cudaStream_t s);
 void launch_isort_place(const Geom& g, const PBuf& st, const ClassInfo* cls, const int* bcount, const int* bstart,
-                        const BlockRec* recs, const int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
+                        const BlockRec* recs, int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
                         uint32_t* perm, uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, int arrive_grid,
                         cudaStream_t s);
 // id-ordered list of the nonzero flags (two-pass tile scan); tile_sum: flag_list_tiles(n) ints
 void launch_flag_list(const int* flags, int n, int* list, int* n_list, int* tile_sum, cudaStream_t s);
 int flag_list_tiles(int n);
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
-                        const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
+                        int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, uint32_t* okey, int grid, cudaStream_t s);
 
 // ---- x-slab decomposition (fl_slab.cu) ----

@@ -103,6 +103,34 @@ __device__ __forceinline__ int next_work(int* counter, int* sh) {
     return *sh;
 }
 
+// Work order of the persistent block-list kernels: costliest blocks first (longest-processing-
+// time first), so a kernel's tail is made of short blocks.  The per-block sort files every
+// listed block under (kind, cost class); the record's n_blocks array holds
+//   [0] light blocks, [1] SVD/rigid blocks, [4 + kind * 4 + class] blocks per class,
+//   [16 + (kind * 4 + class) * maxb + i] their list slots (any order inside a class).
+// Class 0: cells over kScR particles (a second staging pass); 1: >= 384 particles; 2: >= 192;
+// 3: the rest.  Which CTA takes which block does not change any result.
+constexpr int kWorkClasses = 4;
+__host__ __device__ constexpr int work_order_ints(int maxb) { return 16 + 2 * kWorkClasses * maxb; }
+__device__ __forceinline__ int work_class(int cnt, int maxcell) {
+    return maxcell > FL_SCR ? 0 : (cnt >= 384 ? 1 : (cnt >= 192 ? 2 : 3));
+}
+__device__ __forceinline__ void work_file(int* nb, int maxb, int kind, int q, int cnt, int maxcell) {
+    const int c = kind * kWorkClasses + work_class(cnt, maxcell);
+    nb[16 + c * maxb + atomicAdd(&nb[4 + c], 1)] = q;
+}
+// list slot of the k-th block of `kind` in work order (k < that kind's block count)
+__device__ __forceinline__ int work_block(const int* __restrict__ nb, int maxb, int kind, int k) {
+    const int* c = nb + 4 + kind * kWorkClasses;
+#pragma unroll
+    for (int i = 0; i < kWorkClasses - 1; i++) {
+        const int ci = c[i];
+        if (k < ci) return nb[16 + (kind * kWorkClasses + i) * maxb + k];
+        k -= ci;
+    }
+    return nb[16 + (kind * kWorkClasses + kWorkClasses - 1) * maxb + k];
+}
+
 // local cell (0..63) of the i-th particle of a block from its cell-start table
 // (largest c with cs[c] <= i; empty cells have cs[c] == cs[c+1])
 __device__ __forceinline__ int cell_of(const uint16_t* cs, int i) {

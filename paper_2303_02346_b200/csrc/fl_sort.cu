@@ -257,9 +257,8 @@ __device__ void seg_bitonic_sort(uint32_t* k, uint32_t* v, int cnt, int np, int 
 // sorted keys for the next substep's incremental sort.
 __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int* __restrict__ bcount,
                                                               const int* __restrict__ bstart,
-                                                              const BlockRec* __restrict__ recs,
-                                                              const int* __restrict__ n_blocks, int cap,
-                                                              const uint32_t* skey, const uint32_t* sslot,
+                                                              const BlockRec* __restrict__ recs, int* n_blocks,
+                                                              int cap, const uint32_t* skey, const uint32_t* sslot,
                                                               uint32_t* perm, uint16_t* celltab, uint32_t* gk,
                                                               uint32_t* gv, uint32_t* okey) {
     pdl_wait();
@@ -289,6 +288,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int*
                 sm.iv[i] = sslot[s0 + i];
             }
             seg_count_sort(sm, cnt, s0, bword, perm, celltab + size_t(q) * kCellTab, okey);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, sm.cs[65]);
         } else {
             int np = 1;
             while (np < cnt) np <<= 1;
@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int*
             }
             __syncthreads();
             seg_bitonic_sort(k, v, cnt, np, s0, bword, perm, act ? celltab + size_t(q) * kCellTab : nullptr, okey);
+            if (act && tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, celltab[size_t(q) * kCellTab + 65]);
         }
     }
 }
@@ -360,8 +361,8 @@ __global__ void k_isort_arrive(Geom g, PBuf st, const int* __restrict__ nmov, co
 __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, const ClassInfo* __restrict__ cls,
                                                                const int* __restrict__ bcount,
                                                                const int* __restrict__ bstart,
-                                                               const BlockRec* __restrict__ recs,
-                                                               const int* __restrict__ n_blocks, int cap, IncSort is,
+                                                               const BlockRec* __restrict__ recs, int* n_blocks,
+                                                               int cap, IncSort is,
                                                                const uint32_t* sslot, uint32_t* perm,
                                                                uint16_t* celltab, uint32_t* gk, uint32_t* gv) {
     pdl_wait();
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
                 is.okey_out[s0 + i] = is.okey_in[os0 + i];
             }
             if (tid < kCellTab) ct[tid] = is.octab[size_t(oq) * kCellTab + tid];
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, is.octab[size_t(oq) * kCellTab + 65]);
             continue;
         }
         // dirty: the stayers of the old segment + the arrivals, sorted
@@ -431,6 +433,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
         const uint32_t bword = uint32_t(r.block) << 6;
         if (fits) {
             seg_count_sort(sm, cnt, s0, bword, perm, ct, is.okey_out);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, sm.cs[65]);
         } else {
             for (int i = cnt + tid; i < np; i += kSortThreads) {
                 k[i] = 0xffffffffu;
@@ -438,6 +441,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
             }
             __syncthreads();
             seg_bitonic_sort(k, v, cnt, np, s0, bword, perm, ct, is.okey_out);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, ct[65]);
         }
     }
 }
@@ -464,7 +468,7 @@ void launch_isort_diff(const Geom& g, const PBuf& st, int n, const ClassInfo* cl
              is.mov);
 }
 void launch_isort_place(const Geom& g, const PBuf& st, const ClassInfo* cls, const int* bcount, const int* bstart,
-                        const BlockRec* recs, const int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
+                        const BlockRec* recs, int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
                         uint32_t* perm, uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, int arrive_grid,
                         cudaStream_t s) {
     launch_k(k_isort_arrive, dim3(arrive_grid), dim3(256), 0, s, g, st, (const int*)is.nmov, (const uint32_t*)is.mov,
@@ -565,6 +569,7 @@ __global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, co
         }
         if (tid == 0) base = s;
     }
+    if (blockIdx.x == 0 && tid < 2 * kWorkClasses) n_blocks[4 + tid] = 0;  // work-order class counts
     const int b0 = blockIdx.x * kListTile + tid * kListItems;
     int cnt[kListItems], flag[kListItems], kind[kListItems];
     int4 mine = make_int4(0, 0, 0, 0);
@@ -667,7 +672,7 @@ void launch_flag_list(const int* flags, int n, int* list, int* n_list, int* tile
 int flag_list_tiles(int n) { return (n + kListThreads - 1) / kListThreads; }
 
 void launch_sort_blocks(const Geom& g, const int* bcount, const int* bstart, const BlockRec* recs,
-                        const int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
+                        int* n_blocks, int cap, const uint32_t* skey, const uint32_t* sslot, uint32_t* perm,
                         uint16_t* celltab, uint32_t* gk, uint32_t* gv, uint32_t* okey, int grid, cudaStream_t s) {
     launch_k(k_sort_blocks, dim3(grid), dim3(kSortThreads), 0, s, g, bcount, bstart, recs, n_blocks, cap, skey, sslot,
              perm, celltab, gk, gv, okey);
