@@ -11,7 +11,8 @@ from pathlib import Path
 CLASS = {"k_p2g": "p2g", "k_grid_update": "grid_update", "k_g2p": "g2p", "k_adj_g2p": "g2p_adjoint",
          "k_adj_grid": "grid_adjoint", "k_eff_final": "grid_adjoint", "k_adj_p2g": "p2g_adjoint",
          "k_sort_count": "sort", "k_sort_scatter": "sort", "k_sort_blocks": "sort", "k_nb_scatter": "sort",
-         "DeviceScan": "sort", "k_list_sums": "sort", "k_list_write": "sort"}
+         "DeviceScan": "sort", "k_list_sums": "sort", "k_list_write": "sort", "k_isort_diff": "sort",
+         "k_isort_arrive": "sort", "k_isort_blocks": "sort"}
 
 
 def main(path, out_json):
@@ -54,6 +55,8 @@ def main(path, out_json):
         print(f"| {name} | {n} | {t / n / 1e3:.1f} | {b / n / 1e6:.2f} | {b / max(t, 1):.0f} |")
     for cls, key in main_k.items():
         n = next((v[0] for k, v in kern.items() if k.startswith(key)), 0)
+        if cls == "sort":  # full and incremental sorts
+            n += next((v[0] for k, v in kern.items() if k.startswith("k_isort_blocks")), 0)
         if n and cls in per:
             traffic[cls] = per[cls][2] / n
     Path(out_json).write_text(json.dumps({k: round(v) for k, v in traffic.items()}, indent=1))
