@@ -421,6 +421,14 @@ struct Ctx {
     DevArr<double> d_up[4];
     DevArr<uint32_t> d_upmeta;
     DevArr<uint8_t> d_upactive;
+    DevArr<int> d_anyfull;
+    // the upload's active / parked split, kept for the substep index it was made at
+    long up_substep = -1;
+    bool up_active_dev = false;
+    std::vector<uint8_t> up_active;
+    std::vector<uint32_t> up_inactive;
+    std::map<long, std::vector<int>> up_pending;
+    int up_n_active = 0;
     DevArr<float> d_x0;  // [3][N] positions by particle id at upload (LossSet.x0)
     int hvar = 1;  // heavy kernel variant (occupancy_grid): 1 beside liquid, 2 dominant, 3 few beside liquid
     int grid_p2g = 0, grid_g2p = 0, grid_upd = 0, grid_sort = 0, grid_adj = 0;
@@ -1112,15 +1120,9 @@ void Ctx::check_error(long /*substep_base*/) {
 
 // upload a SimState<3> view; canonical store order is established here
 void Ctx::upload(const flume_state_view* view) {
-    // the host mirror of k_upload's kMetaFull test (fp32 F of an isotropic class != c I)
+    // upload_full (a liquid handed in with a full F, kMetaFull) is k_upload's device flag,
+    // read back with the upload's final synchronisation
     upload_full = false;
-    for (int i = 0; i < N && !upload_full; i++) {
-        if (!classes[size_t(p_class[size_t(i)])].iso) continue;
-        const double* f = view->F + 9 * size_t(i);
-        for (int k = 0; k < 9; k++)
-            if (k % 4 != 0 && float(f[k]) != 0.f) upload_full = true;
-        if (float(f[4]) != float(f[0]) || float(f[8]) != float(f[0])) upload_full = true;
-    }
     if (empty) {
         substep_index = view->substep_index;
         time = view->time;
@@ -1135,21 +1137,30 @@ void Ctx::upload(const flume_state_view* view) {
     substep_index = view->substep_index;
     time = view->time;
     // particles activating at or after this substep are parked in the tail; the
-    // substep that reaches their activation index brings them in (mpm.hpp:435-449)
-    std::vector<uint8_t> active(N);
-    pending.clear();
-    inactive_ids.clear();
-    n_active = 0;
-    for (int i = 0; i < N; i++) {
-        bool act = p_act[i] < substep_index || (p_act[i] <= substep_index && emitter_of[i] < 0);
-        active[i] = act ? 1 : 0;
-        if (act)
-            n_active++;
-        else {
-            inactive_ids.push_back(uint32_t(i));
-            pending[p_act[i]].push_back(i);
+    // substep that reaches their activation index brings them in (mpm.hpp:435-449).
+    // The split depends on the substep index alone: kept from the last upload at the same one.
+    std::vector<uint8_t>& active = up_active;
+    if (up_substep != substep_index || slab()) {
+        active.assign(N, 0);
+        up_pending.clear();
+        up_inactive.clear();
+        up_n_active = 0;
+        for (int i = 0; i < N; i++) {
+            bool act = p_act[i] < substep_index || (p_act[i] <= substep_index && emitter_of[i] < 0);
+            active[i] = act ? 1 : 0;
+            if (act)
+                up_n_active++;
+            else {
+                up_inactive.push_back(uint32_t(i));
+                up_pending[p_act[i]].push_back(i);
+            }
         }
+        up_substep = slab() ? -1 : substep_index;
+        up_active_dev = false;
     }
+    pending = up_pending;
+    inactive_ids = up_inactive;
+    n_active = up_n_active;
     if (slab()) {
         // split the columns by the uploaded positions (the same on every rank), keep
         // this slab's active particles; parked ones stay replicated on all slabs
@@ -1172,11 +1183,16 @@ void Ctx::upload(const flume_state_view* view) {
                 n_active++;
         }
     }
-    d_upmeta.upload(p_class, stream);
-    d_upactive.upload(active, stream);
+    if (!d_upmeta.p) d_upmeta.upload(p_class, stream);  // (fixed per context)
+    if (!up_active_dev || slab()) {
+        d_upactive.upload(active, stream);
+        up_active_dev = true;
+    }
+    d_anyfull.alloc(1);
+    CK(cudaMemsetAsync(d_anyfull.p, 0, sizeof(int), stream));
     StatePtr raw = get_state();
     launch_upload(geom, raw->p, N, d_up[0].p, d_up[1].p, d_up[2].p, d_up[3].p, d_upmeta.p, d_upactive.p, d_cls.p,
-                  stream);
+                  d_anyfull.p, stream);
     launches++;
     // positions by id at upload: a parked particle keeps them until its activation substep,
     // which is where a loss evaluated at that substep sees it (emission happens in place)
@@ -1201,8 +1217,11 @@ void Ctx::upload(const flume_state_view* view) {
     set_effectors(view);
     unsigned long long reset = ~0ull;
     CK(cudaMemcpyAsync(d_err.p, &reset, sizeof(reset), cudaMemcpyHostToDevice, stream));
+    int anyfull = 0;
+    CK(cudaMemcpyAsync(&anyfull, d_anyfull.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
     // escape check of the uploaded positions happens in the first P2G
     CK(cudaStreamSynchronize(stream));
+    upload_full = anyfull != 0;
 }
 
 void Ctx::set_effectors(const flume_state_view* view) {

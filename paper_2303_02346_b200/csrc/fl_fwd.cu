@@ -25,7 +25,7 @@ namespace fl {
 __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, const double* __restrict__ v,
                          const double* __restrict__ F, const double* __restrict__ C,
                          const uint32_t* __restrict__ meta, const uint8_t* __restrict__ active,
-                         const ClassInfo* __restrict__ cls) {
+                         const ClassInfo* __restrict__ cls, int* any_full) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     for (int a = 0; a < 3; a++) {
@@ -42,7 +42,9 @@ __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, 
     for (int k = 0; k < 9; k++)
         if (k % 4 != 0 && raw.F(k)[i] != 0.f) isotropic = false;
     if (raw.F(4)[i] != raw.F(0)[i] || raw.F(8)[i] != raw.F(0)[i]) isotropic = false;
-    raw.meta[i] = meta[i] | ((cls[meta[i]].iso && !isotropic) ? kMetaFull : 0u);
+    const bool full = cls[meta[i]].iso && !isotropic;
+    raw.meta[i] = meta[i] | (full ? kMetaFull : 0u);
+    if (full) *any_full = 1;  // (the host reads it after the upload: heavy paths possible)
     raw.id[i] = uint32_t(i);
     // active: 0 = parked (activates later), 1 = active here, 2 = active on another slab
     uint32_t key = g.key_inactive;
@@ -53,9 +55,9 @@ __global__ void k_upload(Geom g, PBuf raw, int n, const double* __restrict__ x, 
 
 void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
                    const double* C, const uint32_t* meta, const uint8_t* active, const ClassInfo* cls,
-                   cudaStream_t s) {
+                   int* any_full, cudaStream_t s) {
     if (n <= 0) return;
-    k_upload<<<(n + 255) / 256, 256, 0, s>>>(g, raw, n, x, v, F, C, meta, active, cls);
+    k_upload<<<(n + 255) / 256, 256, 0, s>>>(g, raw, n, x, v, F, C, meta, active, cls, any_full);
 }
 
 __global__ void k_gather(PBuf in, PBuf out, const uint32_t* __restrict__ perm, int n) {

@@ -221,7 +221,7 @@ constexpr int kRigidChunk = 2048;
 // ---- forward ----
 void launch_upload(const Geom& g, PBuf raw, int n, const double* x, const double* v, const double* F,
                    const double* C, const uint32_t* meta, const uint8_t* active, const ClassInfo* cls,
-                   cudaStream_t s);
+                   int* any_full, cudaStream_t s);
 void launch_gather(PBuf in, PBuf out, const uint32_t* perm, int n, cudaStream_t s);
 void launch_activate(const Geom& g, PBuf st, const ActEntry* list, int n, const int* slot_base, cudaStream_t s);
 void launch_activate_inline(const Geom& g, PBuf st, const ActEntry* host_list, int n, const int* slot_base,
