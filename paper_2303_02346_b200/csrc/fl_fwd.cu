@@ -189,11 +189,14 @@ __global__ void __launch_bounds__(NT, MINB) k_p2g(Geom g, PBuf st, const uint32_
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     const int my_c = tid & 63, my_ox = tid >> 6;
     __shared__ int sh_next;
+    __shared__ int s_wc[kWorkClasses];
+    work_counts_load(n_blocks, HEAVY ? 1 : 0, s_wc, tid);
     for (;;) {
         const int k = next_work(wq, &sh_next);
         if (k >= q1 - q0) break;
-        const int b = work_block(n_blocks, g.maxb, HEAVY ? 1 : 0, k);  // costliest blocks first
-        const BlockRec r = recs[b];
+        const int4 we = work_entry(n_blocks, g.maxb, HEAVY ? 1 : 0, k, s_wc);  // costliest blocks first
+        const int b = we.x;
+        const BlockRec r{we.y, we.z, we.w};
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
         bx -= rep_of_col(g, bx) * g.rstride;  // replica-local column (positions are local)
@@ -435,11 +438,14 @@ __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, con
     ts.init(&bar, raw, tid);
     const int q0 = HEAVY ? g.maxb - n_blocks[1] : 0, q1 = HEAVY ? g.maxb : n_blocks[0];
     __shared__ int sh_next;
+    __shared__ int s_wc[kWorkClasses];
+    work_counts_load(n_blocks, HEAVY ? 1 : 0, s_wc, tid);
     for (;;) {
         const int k = next_work(wq, &sh_next);
         if (k >= q1 - q0) break;
-        const int b = work_block(n_blocks, g.maxb, HEAVY ? 1 : 0, k);  // costliest blocks first
-        const BlockRec r = recs[b];
+        const int4 we = work_entry(n_blocks, g.maxb, HEAVY ? 1 : 0, k, s_wc);  // costliest blocks first
+        const int b = we.x;
+        const BlockRec r{we.y, we.z, we.w};
         int bx, by, bz;
         block_unlin(g, r.block, bx, by, bz);
         const int rep = rep_of_col(g, bx);  // replica contexts (0 otherwise)

@@ -107,28 +107,35 @@ __device__ __forceinline__ int next_work(int* counter, int* sh) {
 // time first), so a kernel's tail is made of short blocks.  The per-block sort files every
 // listed block under (kind, cost class); the record's n_blocks array holds
 //   [0] light blocks, [1] SVD/rigid blocks, [4 + kind * 4 + class] blocks per class,
-//   [16 + (kind * 4 + class) * maxb + i] their list slots (any order inside a class).
+//   from int 16 on, int4 entries [(kind * 4 + class) * maxb + i] = {list slot, block, start,
+//   end} (any order inside a class): a kernel gets its next block in one load.
 // Class 0: cells over kScR particles (a second staging pass); 1: >= 384 particles; 2: >= 192;
 // 3: the rest.  Which CTA takes which block does not change any result.
 constexpr int kWorkClasses = 4;
-__host__ __device__ constexpr int work_order_ints(int maxb) { return 16 + 2 * kWorkClasses * maxb; }
+__host__ __device__ constexpr int work_order_ints(int maxb) { return 16 + 4 * 2 * kWorkClasses * maxb; }
 __device__ __forceinline__ int work_class(int cnt, int maxcell) {
     return maxcell > FL_SCR ? 0 : (cnt >= 384 ? 1 : (cnt >= 192 ? 2 : 3));
 }
-__device__ __forceinline__ void work_file(int* nb, int maxb, int kind, int q, int cnt, int maxcell) {
-    const int c = kind * kWorkClasses + work_class(cnt, maxcell);
-    nb[16 + c * maxb + atomicAdd(&nb[4 + c], 1)] = q;
+__device__ __forceinline__ void work_file(int* nb, int maxb, int kind, int q, const BlockRec& r, int maxcell) {
+    const int c = kind * kWorkClasses + work_class(r.end - r.start, maxcell);
+    reinterpret_cast<int4*>(nb + 16)[size_t(c) * maxb + atomicAdd(&nb[4 + c], 1)] =
+        make_int4(q, r.block, r.start, r.end);
 }
-// list slot of the k-th block of `kind` in work order (k < that kind's block count)
-__device__ __forceinline__ int work_block(const int* __restrict__ nb, int maxb, int kind, int k) {
-    const int* c = nb + 4 + kind * kWorkClasses;
+// the k-th block of `kind` in work order (k < that kind's block count); wc: the kind's
+// class counts (shared memory)
+__device__ __forceinline__ int4 work_entry(const int* __restrict__ nb, int maxb, int kind, int k, const int* wc) {
+    int i = 0;
 #pragma unroll
-    for (int i = 0; i < kWorkClasses - 1; i++) {
-        const int ci = c[i];
-        if (k < ci) return nb[16 + (kind * kWorkClasses + i) * maxb + k];
-        k -= ci;
+    for (; i < kWorkClasses - 1; i++) {
+        if (k < wc[i]) break;
+        k -= wc[i];
     }
-    return nb[16 + (kind * kWorkClasses + kWorkClasses - 1) * maxb + k];
+    return reinterpret_cast<const int4*>(nb + 16)[size_t(kind * kWorkClasses + i) * maxb + k];
+}
+// every CTA of a persistent block-list kernel: its kind's class counts into shared memory
+// (visible after the first next_work barrier)
+__device__ __forceinline__ void work_counts_load(const int* __restrict__ nb, int kind, int* wc, int tid) {
+    if (tid < kWorkClasses) wc[tid] = nb[4 + kind * kWorkClasses + tid];
 }
 
 // local cell (0..63) of the i-th particle of a block from its cell-start table

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int*
                 sm.iv[i] = sslot[s0 + i];
             }
             seg_count_sort(sm, cnt, s0, bword, perm, celltab + size_t(q) * kCellTab, okey);
-            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, sm.cs[65]);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, recs[q], sm.cs[65]);
         } else {
             int np = 1;
             while (np < cnt) np <<= 1;
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int*
             }
             __syncthreads();
             seg_bitonic_sort(k, v, cnt, np, s0, bword, perm, act ? celltab + size_t(q) * kCellTab : nullptr, okey);
-            if (act && tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, celltab[size_t(q) * kCellTab + 65]);
+            if (act && tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, recs[q], celltab[size_t(q) * kCellTab + 65]);
         }
     }
 }
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
                 is.okey_out[s0 + i] = is.okey_in[os0 + i];
             }
             if (tid < kCellTab) ct[tid] = is.octab[size_t(oq) * kCellTab + tid];
-            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, is.octab[size_t(oq) * kCellTab + 65]);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, r, is.octab[size_t(oq) * kCellTab + 65]);
             continue;
         }
         // dirty: the stayers of the old segment + the arrivals, sorted
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
         const uint32_t bword = uint32_t(r.block) << 6;
         if (fits) {
             seg_count_sort(sm, cnt, s0, bword, perm, ct, is.okey_out);
-            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, sm.cs[65]);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, r, sm.cs[65]);
         } else {
             for (int i = cnt + tid; i < np; i += kSortThreads) {
                 k[i] = 0xffffffffu;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
             }
             __syncthreads();
             seg_bitonic_sort(k, v, cnt, np, s0, bword, perm, ct, is.okey_out);
-            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, cnt, ct[65]);
+            if (tid == 0) work_file(n_blocks, cap, w < nl ? 0 : 1, q, r, ct[65]);
         }
     }
 }
