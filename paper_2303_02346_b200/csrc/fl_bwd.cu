@@ -461,16 +461,21 @@ constexpr int kAdjGridThreads = FL_ADJGRID_THREADS;
 __device__ __forceinline__ float4 gather_tile_sum(const Geom& g, const int* __restrict__ blockmap,
                                                   const float4* __restrict__ staging, int bx, int by, int bz, int lx,
                                                   int ly, int lz) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    // the block-map loads first (independent), then the tile loads and the fixed-order sum
+    int slot[8];
 #pragma unroll
     for (int d = 0; d < 8; d++) {
         const int ddx = d >> 2, ddy = (d >> 1) & 1, ddz = d & 1;
-        if ((ddx && lx >= 2) || (ddy && ly >= 2) || (ddz && lz >= 2)) continue;
         const int px = bx - ddx, py = by - ddy, pz = bz - ddz;
-        if (px < 0 || py < 0 || pz < 0) continue;
-        const int slot = blockmap[block_lin(g, px, py, pz)] - 1;  // map holds slot + 1
-        if (slot < 0) continue;
-        const float4 v = staging[size_t(slot) * kTile + (lx + 4 * ddx) * 36 + (ly + 4 * ddy) * 6 + (lz + 4 * ddz)];
+        const bool in = !((ddx && lx >= 2) || (ddy && ly >= 2) || (ddz && lz >= 2)) && px >= 0 && py >= 0 && pz >= 0;
+        slot[d] = in ? blockmap[block_lin(g, px, py, pz)] - 1 : -1;  // map holds slot + 1
+    }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int d = 0; d < 8; d++) {
+        if (slot[d] < 0) continue;
+        const int ddx = d >> 2, ddy = (d >> 1) & 1, ddz = d & 1;
+        const float4 v = staging[size_t(slot[d]) * kTile + (lx + 4 * ddx) * 36 + (ly + 4 * ddy) * 6 + (lz + 4 * ddz)];
         acc.x += v.x;
         acc.y += v.y;
         acc.z += v.z;
