@@ -731,8 +731,11 @@ def _ws_for(scene: Scene, ws: Optional[GpuWorkspace]) -> GpuWorkspace:
 def mpm_substep(scene: Scene, state: SimState, action, ws: GpuWorkspace, count: int = 1) -> None:
     """mpm.hpp:455-473 (count > 1 chains substeps without host round trips)."""
     ws = _ws_for(scene, ws)
+    a = np.ascontiguousarray(action, dtype=np.float64).ravel()
+    need = 6 * getattr(ws, "n_replicas", 1)  # a replica context takes one Action6 per replica
+    if a.size != need:
+        raise ValueError(f"mpm_substep: {need} action values expected, got {a.size}")
     ws._upload(state)
-    a = np.ascontiguousarray(action, dtype=np.float64)
     ws._collective(lambda r, c: ws.lib.flume_substep(c, _dp(a), int(count)))
     t = state._time
     for _ in range(int(count)):  # the reference accumulates time += dt per substep (mpm.hpp:471)
