@@ -91,3 +91,25 @@ def test_replica_context_rejects_single_scene_calls():
     with pytest.raises(ValueError):
         fl.rollout_loss(w.scene, rws.replicate(w.state), acts, loss, ws=rws)
     rws.close()
+
+
+def test_replicas_full_size_c4():
+    """Two candidates of the benchmark scene (2 x 1,027,233 particles, 128^3 each) in one
+    replica context: final states bit-identical to single contexts after 20 substeps."""
+    w = fl.build_scene(spec_for("c4"))
+    pop = _population(w, 2, 1, seed=3)
+    for a in pop:
+        a.segment_length = 20
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    rws = fl.ReplicaWorkspace(w.scene, 2)
+    fin_r = []
+    losses = fl.rollout_loss_replicas(w.scene, w.state, pop, loss, rws, final_states=fin_r)
+    rws.close()
+    ws = fl.GpuWorkspace(w.scene)
+    for r in range(2):
+        fin = w.state.copy()
+        l1 = fl.rollout_loss(w.scene, w.state.copy(), pop[r], loss, ws=ws, final_state=fin)
+        assert abs(losses[r] - l1) <= 1e-12 * abs(l1)
+        for got, want in ((fin_r[r].x, fin.x), (fin_r[r].v, fin.v), (fin_r[r].F, fin.F), (fin_r[r].C, fin.C)):
+            assert np.array_equal(got, want), r
+    ws.close()
