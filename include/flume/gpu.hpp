@@ -62,10 +62,38 @@ struct SlabRank {
     const unsigned char* uid = nullptr;
 };
 
+// A replica context: `n` copies of the scene in one device context, every kernel launch
+// covering all of them (flume_ctx_create_replicas; the CMA-ES population of
+// optimize.hpp:383-418).  Use with rollout_loss_replicas.
+struct Replicas {
+    int n = 1;
+};
+
 class Workspace {
 public:
     Workspace(const Scene<3>& scene, const SimState<3>& state, int device = 0, const SlabRank* slab = nullptr)
         : scene_(&scene) {
+        build_desc(scene, state);
+        if (slab && slab->n_ranks > 1)
+            check(nullptr, flume_ctx_create_dist(&desc_, device, slab->rank, slab->n_ranks, slab->uid, &ctx_));
+        else
+            check(nullptr, flume_ctx_create(&desc_, device, &ctx_));
+    }
+    Workspace(const Scene<3>& scene, const SimState<3>& state, Replicas rep, int device = 0)
+        : scene_(&scene), n_rep_(rep.n) {
+        build_desc(scene, state);
+        check(nullptr, flume_ctx_create_replicas(&desc_, rep.n, device, &ctx_));
+    }
+    ~Workspace() { flume_ctx_destroy(ctx_); }
+    Workspace(const Workspace&) = delete;
+    Workspace& operator=(const Workspace&) = delete;
+
+    flume_ctx* ctx() const { return ctx_; }
+    const Scene<3>& scene() const { return *scene_; }
+    int replicas() const { return n_rep_; }
+
+private:
+    void build_desc(const Scene<3>& scene, const SimState<3>& state) {
         const SimConfig<3>& c = scene.config;
         desc_.config.grid_resolution = c.grid_resolution;
         for (int a = 0; a < 3; a++) {
@@ -142,27 +170,19 @@ public:
         desc_.mass = mass_.data();
         desc_.volume0 = vol_.data();
         desc_.activation_substep = act_.data();
-        if (slab && slab->n_ranks > 1)
-            check(nullptr, flume_ctx_create_dist(&desc_, device, slab->rank, slab->n_ranks, slab->uid, &ctx_));
-        else
-            check(nullptr, flume_ctx_create(&desc_, device, &ctx_));
     }
-    ~Workspace() { flume_ctx_destroy(ctx_); }
-    Workspace(const Workspace&) = delete;
-    Workspace& operator=(const Workspace&) = delete;
 
-    flume_ctx* ctx() const { return ctx_; }
-    const Scene<3>& scene() const { return *scene_; }
-
-    // SimState<3> (AoS, double) <-> the ABI's particle arrays (reference order)
+public:
+    // SimState<3> (AoS, double) <-> the ABI's particle arrays (reference order); a replica
+    // context gets the state repeated for every replica (the population's common start)
     void upload(const SimState<3>& st) {
-        const size_t n = st.particles.size();
+        const size_t n1 = st.particles.size(), n = n1 * size_t(n_rep_);
         x_.resize(3 * n);
         v_.resize(3 * n);
         F_.resize(9 * n);
         C_.resize(9 * n);
         for (size_t i = 0; i < n; i++) {
-            const Particle<3>& p = st.particles[i];
+            const Particle<3>& p = st.particles[i % n1];
             for (int a = 0; a < 3; a++) {
                 x_[3 * i + a] = p.x[a];
                 v_[3 * i + a] = p.v[a];
@@ -173,9 +193,10 @@ public:
                     C_[9 * i + 3 * r + q] = p.C[r][q];
                 }
         }
-        effst_.resize(st.effectors.size());
-        for (size_t k = 0; k < st.effectors.size(); k++) {
-            const Effector<3>& e = st.effectors[k];
+        const size_t ne1 = st.effectors.size();
+        effst_.resize(ne1 * size_t(n_rep_));
+        for (size_t k = 0; k < effst_.size(); k++) {
+            const Effector<3>& e = st.effectors[k % ne1];
             for (int a = 0; a < 3; a++) {
                 effst_[k].pose_t[a] = e.pose.t[a];
                 effst_[k].linear_velocity[a] = e.linear_velocity[a];
@@ -219,6 +240,7 @@ public:
 
 private:
     const Scene<3>* scene_;
+    int n_rep_ = 1;
     flume_ctx* ctx_ = nullptr;
     flume_scene_desc desc_{};
     std::vector<flume_material> mats_;
@@ -355,6 +377,31 @@ inline Real rollout_loss(const Scene<3>& scene, const SimState<3>& state0, const
         check(ws.ctx(), flume_rollout_loss(ws.ctx(), &av, loss.desc(), window_substeps, &out, per.data()));
     }
     if (per_segment) *per_segment = per;
+    return out;
+}
+
+// rollout_loss of every candidate of a population in a replica context (Workspace(...,
+// Replicas{n})): one kernel launch per stage for all of them; each replica's loss is the
+// single-context one up to the order of its fp64 sums
+inline std::vector<Real> rollout_loss_replicas(const Scene<3>& scene, const SimState<3>& state0,
+                                               const std::vector<ActionTrajectory>& population, const Loss& loss,
+                                               Workspace& ws, long window_substeps = 0) {
+    (void)scene;
+    const int R = ws.replicas();
+    if (int(population.size()) != R) throw EngineError("rollout_loss_replicas: one trajectory per replica");
+    const int nseg = population.front().n_segments, seglen = population.front().segment_length;
+    std::vector<double> vals(size_t(nseg) * R * 6);
+    for (int r = 0; r < R; r++) {
+        const ActionTrajectory& a = population[size_t(r)];
+        if (a.n_segments != nseg || a.segment_length != seglen)
+            throw EngineError("rollout_loss_replicas: every candidate needs the same segment layout");
+        for (int s = 0; s < nseg; s++)
+            for (int k = 0; k < 6; k++) vals[(size_t(s) * R + r) * 6 + k] = a.values[size_t(s)][size_t(k)];
+    }
+    ws.upload(state0);
+    flume_actions av{nseg, seglen, vals.data()};
+    std::vector<Real> out(static_cast<size_t>(R), 0.0);
+    check(ws.ctx(), flume_replicas_rollout_loss(ws.ctx(), &av, loss.desc(), window_substeps, 0, out.data(), nullptr));
     return out;
 }
 

@@ -71,11 +71,21 @@ int main(int argc, char** argv) {
     GradReport rg = gpu::grad_check(w.scene, w.state, traj, gl, gws, 2, 1e-3, false);
     const double crel = rc.gradient.size() == rg.gradient.size() ? GradReport::rel_error(rg.gradient, rc.gradient) : 1.0;
     const double lrel = std::abs(gc.loss - gg.loss) / std::abs(gc.loss);
-    const bool ok = dx <= 1e-4 && dv <= 5e-4 * vmax && grel <= 1e-3 && crel <= 1e-3 && fin_ok && lrel <= 1e-5 && gc.snapshots == gg.snapshots;
+    // a two-candidate population in one replica context against single-context rollouts
+    ActionTrajectory traj2 = traj;
+    for (auto& v : traj2.values)
+        for (auto& c : v) c *= 0.5;
+    gpu::Workspace rws(w.scene, w.state, gpu::Replicas{2}, 0);
+    const std::vector<Real> pl = gpu::rollout_loss_replicas(w.scene, w.state, {traj, traj2}, fl_loss, rws);
+    const Real l0 = gpu::rollout_loss(w.scene, w.state, traj, fl_loss, gws);
+    const Real l1 = gpu::rollout_loss(w.scene, w.state, traj2, fl_loss, gws);
+    const double prel = std::max(std::abs(pl[0] - l0) / std::abs(l0), std::abs(pl[1] - l1) / std::abs(l1));
+    const bool ok = dx <= 1e-4 && dv <= 5e-4 * vmax && grel <= 1e-3 && crel <= 1e-3 && fin_ok && lrel <= 1e-5 &&
+                    gc.snapshots == gg.snapshots && prel <= 1e-12;
     std::printf("{\"particles\": %zu, \"substeps\": %d, \"x_err_dx\": %.3e, \"v_err_rel\": %.3e, "
                 "\"loss_rel\": %.3e, \"grad_rel\": %.3e, \"grad_check_rel\": %.3e, \"snapshots\": [%zu, %zu], "
-                "\"ok\": %s}\n",
-                cpu.particles.size(), steps, dx, dv / vmax, lrel, grel, crel, gc.snapshots, gg.snapshots,
+                "\"replica_loss_rel\": %.3e, \"ok\": %s}\n",
+                cpu.particles.size(), steps, dx, dv / vmax, lrel, grel, crel, gc.snapshots, gg.snapshots, prel,
                 ok ? "true" : "false");
     return ok ? 0 : 1;
 }

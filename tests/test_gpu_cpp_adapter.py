@@ -1,7 +1,9 @@
 """The C++ drop-in adapter (include/flume/gpu.hpp) used from a program written
 against the reference's own API (tests/cpp/shim_parity.cpp, built by
 tests/cpp/Makefile against proj/include): flume::mpm_substep vs
-flume::gpu::mpm_substep and the two grad_trajectory calls agree."""
+flume::gpu::mpm_substep and the two grad_trajectory calls agree, and a two-candidate population
+in a replica context (gpu::Workspace(..., gpu::Replicas{2}), gpu::rollout_loss_replicas) gives
+the single-context losses."""
 import json
 import subprocess
 from pathlib import Path
