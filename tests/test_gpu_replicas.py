@@ -113,3 +113,21 @@ def test_replicas_full_size_c4():
         for got, want in ((fin_r[r].x, fin.x), (fin_r[r].v, fin.v), (fin_r[r].F, fin.F), (fin_r[r].C, fin.C)):
             assert np.array_equal(got, want), r
     ws.close()
+
+
+def test_replica_launches_do_not_scale_with_the_population():
+    """One launch per kernel stage covers every candidate: a 4-candidate gradient issues the
+    single context's launches plus only the per-replica loss evaluations at segment ends."""
+    w = fl.build_scene(spec_for("c1", 32))
+    acts = fl.ActionTrajectory(2, 5, np.tile(w.init_action, (2, 1)))
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    ws = fl.GpuWorkspace(w.scene)
+    fl.grad_trajectory(w.scene, w.state, acts, loss, ws=ws)
+    single = ws.last_timing().launches
+    ws.close()
+    R = 4
+    rws = fl.ReplicaWorkspace(w.scene, R)
+    fl.grad_trajectory_replicas(w.scene, w.state, [acts] * R, loss, rws)
+    rep = rws.last_timing().launches
+    rws.close()
+    assert single <= rep <= single + 4 * (R - 1) * acts.n_segments, (single, rep)
