@@ -967,6 +967,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev, int n_replicas) {
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         if (hvar == 1 && nh < long(nsm) * 512) hvar = 3;
+        if (const char* hv = getenv("FL_HVAR")) hvar = atoi(hv);  // A/B experiments
     }
     grid_p2g = occupancy_grid(KG_P2G, 0);
     grid_p2g_h = occupancy_grid(KG_P2G, hvar);
