@@ -312,10 +312,16 @@ int flume_timer_elapsed(flume_ctx* ctx, int a, int b, double* ms);
 /* ---- state hand-off ---- */
 int flume_state_upload(flume_ctx* ctx, const flume_state_view* view);
 int flume_state_download(flume_ctx* ctx, flume_state_view* view);
-/* canonical store order: cell keys, particle ids and active count (n entries each) */
+/* the store as it is: cell keys, particle ids and active count (n entries each).  The slots
+   are in the last sort's order, the keys those of the stored positions (after a substep they
+   may no longer be sorted: the next substep sorts them) */
 int flume_store_order(flume_ctx* ctx, unsigned* keys, unsigned* ids, long* n_active);
 /* fp32 positions in store order (for the bit-exact key/order check) */
 int flume_store_positions(flume_ctx* ctx, float* x);
+/* the canonical (cell key, id) order of the current store as the next substep's sort
+   produces it (incremental when possible): keys, ids and fp32 positions ([3][N], SoA) of the
+   first n_keep slots in sorted order.  One-rank contexts. */
+int flume_store_sorted(flume_ctx* ctx, unsigned* keys, unsigned* ids, float* x, long* n_active);
 
 /* ---- hot path ---- */
 int flume_substep(flume_ctx* ctx, const double action[6], int count);

@@ -147,6 +147,8 @@ EXPORTS = {
     "flume_state_upload": (C.c_int, [C.c_void_p, C.POINTER(StateView)]),
     "flume_state_download": (C.c_int, [C.c_void_p, C.POINTER(StateView)]),
     "flume_store_order": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint), C.POINTER(C.c_uint), C.POINTER(C.c_long)]),
+    "flume_store_sorted": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint), C.POINTER(C.c_uint), C.POINTER(C.c_float),
+                                     C.POINTER(C.c_long)]),
     "flume_store_positions": (C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
     "flume_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "flume_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_long), C.c_int]),

@@ -497,6 +497,7 @@ class GpuWorkspace:
         rc = self.lib.flume_ctx_create_dist(C.byref(scene.desc), device, rank, n_ranks, u, C.byref(self.ctx))
         if rc != _abi.FLUME_OK:
             _raise(self.lib, None, rc)
+        self._dist = True
         self.ctxs = [self.ctx]
         self._resident = None
         self._resident_ver = -1
@@ -664,16 +665,22 @@ class GpuWorkspace:
         self._resident_ver = st._ver
 
     def store_order(self, st: SimState):
-        """Canonical store order (cell keys, particle ids, active count) + fp32 positions."""
+        """Canonical store order (cell keys, particle ids, active count) + fp32 positions: the
+        order the next substep's sort puts the state in (one rank; slab ranks: the store as
+        it is)."""
         self._upload(st)
-        n = self.scene.n_particles
+        n = self.scene.n_particles * getattr(self, "n_replicas", 1)
         keys = np.zeros(n, np.uint32)
         ids = np.zeros(n, np.uint32)
         na = C.c_long()
-        self._check(self.lib.flume_store_order(self.ctx, keys.ctypes.data_as(C.POINTER(C.c_uint)),
-                                               ids.ctypes.data_as(C.POINTER(C.c_uint)), C.byref(na)))
         xs = np.zeros(3 * n, np.float32)
-        self._check(self.lib.flume_store_positions(self.ctx, xs.ctypes.data_as(C.POINTER(C.c_float))))
+        kp, ip = keys.ctypes.data_as(C.POINTER(C.c_uint)), ids.ctypes.data_as(C.POINTER(C.c_uint))
+        xp = xs.ctypes.data_as(C.POINTER(C.c_float))
+        if len(self.ctxs) == 1 and not getattr(self, "_dist", False):
+            self._check(self.lib.flume_store_sorted(self.ctx, kp, ip, xp, C.byref(na)))
+        else:
+            self._check(self.lib.flume_store_order(self.ctx, kp, ip, C.byref(na)))
+            self._check(self.lib.flume_store_positions(self.ctx, xp))
         return keys, ids, na.value, xs.reshape(3, n)
 
     def last_timing(self):

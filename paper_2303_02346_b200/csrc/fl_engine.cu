@@ -2762,6 +2762,40 @@ int flume_store_order(flume_ctx* ctx, unsigned* keys, unsigned* ids, long* n_act
     });
 }
 
+int flume_store_sorted(flume_ctx* ctx, unsigned* keys, unsigned* ids, float* x, long* n_active) {
+    if (!ctx) return FLUME_E_ARG;
+    using namespace fl;
+    return guard(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (c.empty) {
+            if (n_active) *n_active = 0;
+            return;
+        }
+        if (c.slab()) throw FlumeError(FLUME_E_ARG, "flume_store_sorted: one-rank contexts only");
+        // the sort the next substep would start with (incremental when the chain holds), then
+        // the store gathered through its permutation; the chain is consumed
+        Record& r = c.next_scratch();
+        r.n_active = c.n_active;
+        r.n_keep = c.n_active + c.n_parked();
+        r.n_stored = c.n_stored;
+        const Record* prev = (c.keep_counts() && c.chain_rec && c.chain_rec != &r && c.chain_out == c.cur.get())
+                                 ? c.chain_rec
+                                 : nullptr;
+        c.sort_and_lists(*c.cur, r, prev);
+        StatePtr t = c.get_state();
+        launch_gather(c.cur->p, t->p, r.perm, r.n_keep, c.stream);
+        if (keys) CK(cudaMemcpyAsync(keys, t->p.key, size_t(r.n_keep) * 4, cudaMemcpyDeviceToHost, c.stream));
+        if (ids) CK(cudaMemcpyAsync(ids, t->p.id, size_t(r.n_keep) * 4, cudaMemcpyDeviceToHost, c.stream));
+        for (int a = 0; a < 3 && x; a++)
+            CK(cudaMemcpyAsync(x + size_t(a) * c.N, t->p.x(a), size_t(r.n_keep) * 4, cudaMemcpyDeviceToHost,
+                               c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        c.put_state(t);
+        c.chain_break();
+        if (n_active) *n_active = c.n_active;
+    });
+}
+
 int flume_store_positions(flume_ctx* ctx, float* x) {
     if (!ctx || !x) return FLUME_E_ARG;
     return guard(ctx, [&] {

@@ -131,3 +131,23 @@ def test_replica_launches_do_not_scale_with_the_population():
     rep = rws.last_timing().launches
     rws.close()
     assert single <= rep <= single + 4 * (R - 1) * acts.n_segments, (single, rep)
+
+
+def test_replica_gradients_full_size_c4():
+    """Gradients of two benchmark-scene candidates (2 x 1M particles) in one replica context
+    against single contexts, 2 segments x 10 substeps with a checkpoint replay."""
+    w = fl.build_scene(spec_for("c4"))
+    pop = _population(w, 2, 2, seed=5)
+    for a in pop:
+        a.segment_length = 10
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    rws = fl.ReplicaWorkspace(w.scene, 2)
+    gr = fl.grad_trajectory_replicas(w.scene, w.state, pop, loss, rws, stride=10)
+    rws.close()
+    ws = fl.GpuWorkspace(w.scene)
+    for r in range(2):
+        g1 = fl.grad_trajectory(w.scene, w.state, pop[r], loss, stride=10, ws=ws)
+        assert abs(gr[r].loss - g1.loss) <= 1e-12 * abs(g1.loss)
+        scale = max(np.abs(g1.action_grad).max(), 1e-30)
+        assert np.abs(gr[r].action_grad - g1.action_grad).max() <= 1e-9 * scale
+    ws.close()

@@ -28,8 +28,8 @@ def _forward(spec, n, inc, x=None):
     ws = fl.GpuWorkspace(w.scene)
     ws.set_incremental_sort(inc)
     fl.mpm_substep(w.scene, w.state, w.init_action, ws, count=n)
-    keys, ids, na, x32 = ws.store_order(w.state)
     stats = ws.sort_stats()[0]
+    keys, ids, na, x32 = ws.store_order(w.state)  # (the next substep's sort: one more)
     state = [np.array(a, copy=True) for a in (w.state.x, w.state.v, w.state.F, w.state.C)]
     ws.close()
     return w, (keys, ids, na, x32), stats, state
@@ -98,3 +98,15 @@ def test_incremental_sort_oversized_blocks():
     for a, b in zip(sta, stb):
         assert np.array_equal(a, b)
     assert sa == (4, 1)
+
+
+def test_incremental_sort_benchmark_horizon():
+    """c4 over the bench's whole 500-substep horizon, where ~1,800 of ~2,800 blocks are dirty
+    per substep late on (tools/dirty_probe.py): the same bits as the full sort."""
+    spec = spec_for("c4")
+    wa, oa, sa, sta = _forward(spec, 500, True)
+    wb, ob, sb, stb = _forward(spec, 500, False)
+    _check_same(oa, ob, wa)
+    for a, b in zip(sta, stb):
+        assert np.array_equal(a, b)
+    assert sa == (500, 1) and sb == (0, 501)
