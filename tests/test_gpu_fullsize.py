@@ -3,7 +3,7 @@ c2-c5 at 1M-8M particles, where the oracle cannot follow every step in seconds.
 
   * one forward substep of c4 at full size against the reference engine (same tolerance
     as the small-scene parity tests)
-  * after 10 substeps: every particle finite, the staged grid mass equals the active
+  * after 200 substeps (c5: 20): every particle finite, the staged grid mass equals the active
     particles' mass, and the canonical store order is bit-exact (keys recomputed on the CPU
     from the GPU's fp32 positions, strictly increasing (key, id))
   * checkpoint strides leave the full-size gradient bit-identical, and a short full-size
@@ -30,11 +30,13 @@ def test_c4_full_one_substep_parity(ref_available):
     assert e["x"] <= 1e-5 and e["v"] <= 1e-5 and e["F"] <= 1e-5 and e["C"] <= 1e-4, e
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_full_size_invariants(name):
+@pytest.mark.parametrize("name,substeps", [("c2", 200), ("c3", 200), ("c4", 200), ("c5", 20)])
+def test_full_size_invariants(name, substeps):
+    """After `substeps` (past the first cell crossings: c4 has ~7,000 per substep by 200;
+    c5 stays in its stable window) the store sorted by the next substep's sort is canonical."""
     w = fl.build_scene(spec_for(name))
     ws = fl.GpuWorkspace(w.scene)
-    fl.mpm_substep(w.scene, w.state, w.init_action, ws, count=10)
+    fl.mpm_substep(w.scene, w.state, w.init_action, ws, count=substeps)
     keys, ids, na, x32 = ws.store_order(w.state)
     nd = w.scene.node_dims
     NB = tuple((d + 3) // 4 for d in nd)
