@@ -48,7 +48,7 @@ def _check_same(a, b, w):
     assert np.all(comp[1:] > comp[:-1])
 
 
-@pytest.mark.parametrize("name,res,n", [("c1", None, 30), ("c2", 64, 40), ("c3", 64, 30), ("c5", 64, 30),
+@pytest.mark.parametrize("name,res,n", [("c1", None, 200), ("c2", 64, 100), ("c3", 64, 100), ("c5", 64, 100),
                                         ("c4", None, 20)])
 def test_incremental_sort_matches_full(name, res, n):
     spec = spec_for(name, res)
