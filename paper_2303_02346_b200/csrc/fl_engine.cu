@@ -358,8 +358,8 @@ struct Ctx {
     bool inc_sort = true;  // flume_set_incremental_sort
     DevArr<uint32_t> okey[2];
     int okey_cur = 0;
-    DevArr<int> isort_blk, rold;  // isort_blk = [dirty | acnt | afill | mover count], zero between sorts
-    DevArr<uint32_t> mov;
+    DevArr<int> isort_blk, rold;  // isort_blk = [dirty | acnt | overflow count | its copy], zero between sorts
+    DevArr<uint32_t> mov, inbox;
     const Record* chain_rec = nullptr;
     const StateBuf* chain_out = nullptr;
     long n_inc_sorts = 0, n_full_sorts = 0;
@@ -923,8 +923,9 @@ void Ctx::init(const flume_scene_desc* desc, int dev, int n_replicas) {
     bcount = bzero.p;
     bheavy = bzero.p + bz;
     bfill = bzero.p + 2 * bz;
-    isort_blk.alloc(3 * bz + 1);
+    isort_blk.alloc(2 * bz + 2);
     CK(cudaMemsetAsync(isort_blk.p, 0, isort_blk.n * sizeof(int), stream));
+    inbox.alloc(bz * kInbox);
     mov.alloc(N);
     rold.alloc(maxb);
     for (int k = 0; k < 2; k++) okey[k].alloc(N);
@@ -1288,7 +1289,8 @@ void Ctx::sort_and_lists(StateBuf& st, Record& r, const Record* prev) {
     const size_t bz = size_t(g.nbtot) + 2;
     if (prev) {
         const IncSort is{prev->recs, prev->blockmap, prev->celltab, okey[okey_cur].p, okey[okey_cur ^ 1].p,
-                         isort_blk.p, isort_blk.p + bz, isort_blk.p + 2 * bz, isort_blk.p + 3 * bz, mov.p, rold.p};
+                         isort_blk.p, isort_blk.p + bz, inbox.p, isort_blk.p + 2 * bz, isort_blk.p + 2 * bz + 1,
+                         mov.p, rold.p};
         launch_isort_diff(g, st.p, r.n_stored, d_cls.p, bcount, bheavy, is, upload_full, stream);
         launch_sort_lists(g, maxb, bcount, bheavy, bstart.p, nbflag, r.nb_list, r.n_nb, r.recs, r.blockmap,
                           r.n_blocks, tile_sum.p, &is, stream);
@@ -1297,7 +1299,7 @@ void Ctx::sort_and_lists(StateBuf& st, Record& r, const Record* prev) {
         okey_cur ^= 1;
         counters_clean = false;
         n_inc_sorts++;
-        launches += 5;  // diff, list sums, list write, arrivals, per-block sort
+        launches += 4;  // diff, list sums, list write, per-block sort
         return;
     }
     // the grid update clears bfill (counts kept) or all three arrays

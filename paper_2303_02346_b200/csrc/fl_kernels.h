@@ -282,6 +282,10 @@ void launch_bars_to_ref(BarBuf bars, const PBuf& st, int n, double* xb, double* 
                         const ClassInfo* cls, cudaStream_t s);
 void launch_expand_f(PBuf st, int n, const ClassInfo* cls, cudaStream_t s);
 
+#ifndef FL_INBOX
+#define FL_INBOX 16
+#endif
+constexpr int kInbox = FL_INBOX;  // arrivals per block kept in its inbox (more go to the overflow list)
 // incremental sort (fl_sort.cu header): the previous substep's sort tables + context scratch
 struct IncSort {
     const BlockRec* orecs;     // previous record: block list
@@ -291,8 +295,9 @@ struct IncSort {
     uint32_t* okey_out;        // [n] this sort's
     int* dirty;                // [nbtot + 2] blocks a particle entered, left or moved inside (zero between sorts)
     int* acnt;                 // [nbtot + 2] arrivals per block (zero between sorts)
-    int* afill;                // [nbtot + 2] their fill cursors (zero between sorts)
-    int* nmov;                 // movers between blocks (zero between sorts)
+    uint32_t* inbox;           // [nbtot + 2][kInbox] the first kInbox arrivals' slots per block
+    int* nmov;                 // arrivals beyond a block's inbox (zero between sorts) ...
+    int* novf;                 // ... their count for the per-block sort (the list pass moves it here)
     uint32_t* mov;             // [n] their slots
     int* rold;                 // [maxb] per list slot: previous list slot of a clean block, -1 = dirty
 };
@@ -306,6 +311,7 @@ int sort_list_tiles(const Geom& g);
 void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bheavy, int* bstart, int* nbflag,
                        int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
                        const IncSort* inc, cudaStream_t s);
+// (launch_isort_place: the per-block sort; the arrivals sit in the blocks' inboxes)
 // meta: the class bit can change (a liquid uploaded with a full F, kMetaFull, loses it in
 // G2P): compare it too; otherwise the key alone (the class bit is the particle's own)
 void launch_isort_diff(const Geom& g, const PBuf& st, int n, const ClassInfo* cls, int* bcount, int* bheavy,

@@ -30,7 +30,8 @@
 //      the keys are written, cost G2P more than the kernel: c4 +3.7 us, spills.)
 //   2. the list scan as above (new segment starts); for every listed block it also
 //      records the previous list slot of a clean block (rold) and clears the dirty flags
-//   3. movers are placed at the ends of their new blocks' segments
+//   3. (the diff filed each arrival in its new block's inbox, kInbox slots, the rest in an
+//      overflow list that only blocks with more arrivals scan)
 //   4. one CTA per block: a clean block copies its old segment in order (perm = the old
 //      sorted positions, cell table and okey copied); a dirty block collects the
 //      stayers of its old segment and its arrivals and sorts them as in step 4 above
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_blocks(Geom g, const int*
 template <bool META>
 __global__ void k_isort_diff(Geom g, PBuf st, int n, const ClassInfo* __restrict__ cls,
                              const uint32_t* __restrict__ okey, int* bcount, int* bheavy, int* acnt, int* dirty,
-                             int* nmov, uint32_t* mov) {
+                             uint32_t* inbox, int* nmov, uint32_t* mov) {
     pdl_wait();
     const int i0 = blockIdx.x * blockDim.x * kSortItems + threadIdx.x;
     uint32_t key[kSortItems], meta[kSortItems], ok[kSortItems];
@@ -337,24 +338,14 @@ __global__ void k_isort_diff(Geom g, PBuf st, int n, const ClassInfo* __restrict
             atomicAdd(&bcount[nb], 1);
             if (oh) atomicSub(&bheavy[ob], 1);
             if (nh) atomicAdd(&bheavy[nb], 1);
-            atomicAdd(&acnt[nb], 1);
-            mov[atomicAdd(nmov, 1)] = uint32_t(i);
+            const int pos = atomicAdd(&acnt[nb], 1);
+            if (pos < kInbox)
+                inbox[size_t(nb) * kInbox + pos] = uint32_t(i);
+            else
+                mov[atomicAdd(nmov, 1)] = uint32_t(i);
         } else if (oh != nh) {
             atomicAdd(&bheavy[nb], nh - oh);
         }
-    }
-}
-
-// movers go to the end of their new block's segment (any order: the block sort orders them)
-__global__ void k_isort_arrive(Geom g, PBuf st, const int* __restrict__ nmov, const uint32_t* __restrict__ mov,
-                               const int* __restrict__ bcount, const int* __restrict__ bstart,
-                               const int* __restrict__ acnt, int* afill, uint32_t* sslot) {
-    pdl_wait();
-    const int m = *nmov;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-        const uint32_t p = mov[i];
-        const int b = key_block(g, st.key[p]);
-        sslot[bstart[b] + bcount[b] - acnt[b] + atomicAdd(&afill[b], 1)] = p;
     }
 }
 
@@ -370,7 +361,6 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
     const int nl = n_blocks[0], nh = n_blocks[1];
     const int nb = nl + nh;
     const int tid = threadIdx.x;
-    if (blockIdx.x == 0 && tid == 0) *is.nmov = 0;  // the arrival pass has read it
     for (int w = blockIdx.x; w <= nb; w += gridDim.x) {
         if (w == nb) {  // the inactive tail: unchanged without activation
             const int s0 = bstart[g.nbtot], cnt = bcount[g.nbtot];
@@ -399,7 +389,8 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
         const int obm = is.oblockmap[r.block];
         const int os0 = obm > 0 ? is.orecs[obm - 1].start : 0, oe = obm > 0 ? is.orecs[obm - 1].end : 0;
         const int na = is.acnt[r.block];
-        const int a0 = s0 + cnt - na;
+        const int nin = min(na, kInbox);
+        const int nov = na > kInbox ? *is.novf : 0;  // more arrivals than the inbox: scan the overflow list
         const bool fits = cnt <= kCountCap;
         int np = 1;
         while (np < cnt) np <<= 1;
@@ -407,10 +398,14 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
         uint32_t* v = gv + size_t(s0) * 2;
         if (tid == 0) sm.n = 0;
         __syncthreads();
-        for (int i = tid; i < (oe - os0) + na; i += kSortThreads) {
-            const uint32_t p = i < oe - os0 ? uint32_t(os0 + i) : sslot[a0 + (i - (oe - os0))];
+        const int nold = oe - os0;
+        for (int i = tid; i < nold + nin + nov; i += kSortThreads) {
+            const uint32_t p = i < nold ? uint32_t(os0 + i)
+                                        : (i < nold + nin ? is.inbox[size_t(r.block) * kInbox + (i - nold)]
+                                                          : is.mov[i - nold - nin]);
             const uint32_t key = st.key[p];
-            if (i < oe - os0 && key_block(g, key) != r.block) continue;  // left the block
+            if (i < nold && key_block(g, key) != r.block) continue;       // left the block
+            if (i >= nold + nin && key_block(g, key) != r.block) continue;  // another block's overflow
             const uint32_t kk = ((key & 63u) << 26) | st.id[p];
             const uint32_t vv = p | heavy_bit(cls, st.meta[p]);
             const int j = atomicAdd(&sm.n, 1);
@@ -425,10 +420,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
         __syncthreads();
         if (tid == 0) {
             if (sm.n != cnt) __trap();  // the counts and the members disagree: cannot happen
-            if (na) {
-                is.acnt[r.block] = 0;
-                is.afill[r.block] = 0;
-            }
+            if (na) is.acnt[r.block] = 0;
         }
         const uint32_t bword = uint32_t(r.block) << 6;
         if (fits) {
@@ -464,15 +456,15 @@ void launch_isort_diff(const Geom& g, const PBuf& st, int n, const ClassInfo* cl
                        const IncSort& is, bool meta, cudaStream_t s) {
     if (n <= 0) return;
     launch_k(meta ? k_isort_diff<true> : k_isort_diff<false>, dim3((n + 256 * kSortItems - 1) / (256 * kSortItems)),
-             dim3(256), 0, s, g, st, n, cls, (const uint32_t*)is.okey_in, bcount, bheavy, is.acnt, is.dirty, is.nmov,
-             is.mov);
+             dim3(256), 0, s, g, st, n, cls, (const uint32_t*)is.okey_in, bcount, bheavy, is.acnt, is.dirty, is.inbox,
+             is.nmov, is.mov);
 }
 void launch_isort_place(const Geom& g, const PBuf& st, const ClassInfo* cls, const int* bcount, const int* bstart,
                         const BlockRec* recs, int* n_blocks, int cap, const IncSort& is, uint32_t* sslot,
                         uint32_t* perm, uint16_t* celltab, uint32_t* gk, uint32_t* gv, int grid, int arrive_grid,
                         cudaStream_t s) {
-    launch_k(k_isort_arrive, dim3(arrive_grid), dim3(256), 0, s, g, st, (const int*)is.nmov, (const uint32_t*)is.mov,
-             bcount, bstart, (const int*)is.acnt, is.afill, sslot);
+    (void)sslot;
+    (void)arrive_grid;
     launch_k(k_isort_blocks, dim3(grid), dim3(kSortThreads), 0, s, g, st, cls, bcount, bstart, recs, n_blocks, cap, is,
              (const uint32_t*)sslot, perm, celltab, gk, gv);
 }
@@ -520,8 +512,12 @@ __device__ __forceinline__ int block_kind(const Geom& g, const int* __restrict__
 
 __global__ void __launch_bounds__(kListThreads) k_list_sums(Geom g, const int* __restrict__ bcount,
                                                             const int* __restrict__ bheavy, int* nbflag,
-                                                            int4* tile_sum) {
+                                                            int4* tile_sum, int* nmov, int* novf) {
     pdl_wait();
+    if (nmov && blockIdx.x == 0 && threadIdx.x == 0) {  // incremental sort: the diff is complete
+        *novf = *nmov;
+        *nmov = 0;
+    }
     using Red = cub::BlockReduce<int4, kListThreads>;
     __shared__ typename Red::TempStorage tmp;
     const int n = g.nbtot + 2;
@@ -623,7 +619,8 @@ void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bhe
                        int* nb_list, int* n_nb, BlockRec* recs, int* blockmap, int* n_blocks, int4* tile_sum,
                        const IncSort* inc, cudaStream_t s) {
     const int tiles = sort_list_tiles(g);
-    launch_k(k_list_sums, dim3(tiles), dim3(kListThreads), 0, s, g, bcount, bheavy, nbflag, tile_sum);
+    launch_k(k_list_sums, dim3(tiles), dim3(kListThreads), 0, s, g, bcount, bheavy, nbflag, tile_sum,
+             inc ? inc->nmov : nullptr, inc ? inc->novf : nullptr);
     launch_k(k_list_write, dim3(tiles), dim3(kListThreads), 0, s, g, cap, bcount, bheavy, nbflag, tile_sum, bstart,
              nb_list, n_nb, recs, blockmap, n_blocks, inc ? inc->oblockmap : nullptr, inc ? inc->rold : nullptr,
              inc ? inc->dirty : nullptr);
