@@ -234,9 +234,10 @@ def _device_ms(lib, ctx, check, fn, slot0=6):
 
 def _stride_for(fl, w, T, seglen, n_local, device, sharing=1):
     """The whole trajectory in HBM (stride = horizon) keeps per substep the state and its
-    permutation (~124 B per particle) and the recorded grid (two dense float4 node arrays and
-    a contact mask, ~33 B per node of the block-major grid); where the device cannot hold it
-    the backward replays from checkpoints at segment boundaries (CheckpointStore stride)."""
+    permutation (~124 B per particle), the recorded grid (two dense float4 node arrays and
+    a contact mask, ~33 B per node of the block-major grid) and the block lists with their
+    work order (~128 B per block); where the device cannot hold it the backward replays from
+    checkpoints at segment boundaries (CheckpointStore stride)."""
     import torch
     try:
         free_b = torch.cuda.mem_get_info(device)[0]
@@ -245,7 +246,7 @@ def _stride_for(fl, w, T, seglen, n_local, device, sharing=1):
     nb_tot = 1
     for d in w.scene.node_dims:
         nb_tot *= (d + 3) // 4
-    need = sharing * T * (n_local * 124 + 33 * 64 * nb_tot) * 1.15
+    need = sharing * T * (n_local * 124 + (33 * 64 + 128) * nb_tot) * 1.15
     return (T if (free_b == 0 or free_b > need) else seglen), free_b, need
 
 
