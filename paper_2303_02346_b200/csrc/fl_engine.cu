@@ -358,7 +358,8 @@ struct Ctx {
     bool inc_sort = true;  // flume_set_incremental_sort
     DevArr<uint32_t> okey[2];
     int okey_cur = 0;
-    DevArr<int> isort_blk, rold;  // isort_blk = [dirty | acnt | overflow count | its copy], zero between sorts
+    DevArr<int> isort_blk;  // [dirty | acnt | overflow count | its copy], zero between sorts
+    DevArr<int4> rold;
     DevArr<uint32_t> mov, inbox;
     const Record* chain_rec = nullptr;
     const StateBuf* chain_out = nullptr;

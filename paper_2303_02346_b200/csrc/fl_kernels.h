@@ -299,7 +299,7 @@ struct IncSort {
     int* nmov;                 // arrivals beyond a block's inbox (zero between sorts) ...
     int* novf;                 // ... their count for the per-block sort (the list pass moves it here)
     uint32_t* mov;             // [n] their slots
-    int* rold;                 // [maxb] per list slot: previous list slot of a clean block, -1 = dirty
+    int4* rold;                // [maxb] per list slot: {clean, previous list slot or -1, its start, its end}
 };
 
 void launch_sort_count(const Geom& g, const PBuf& st, DN n, const ClassInfo* cls, int* bcount, int* bheavy,

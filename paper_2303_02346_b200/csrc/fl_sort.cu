@@ -29,7 +29,7 @@
 //      key alone is compared (8 bytes per particle).  (Doing this in G2P instead, where
 //      the keys are written, cost G2P more than the kernel: c4 +3.7 us, spills.)
 //   2. the list scan as above (new segment starts); for every listed block it also
-//      records the previous list slot of a clean block (rold) and clears the dirty flags
+//      records each block's previous list slot and segment (rold) and clears the dirty flags
 //   3. (the diff filed each arrival in its new block's inbox, kInbox slots, the rest in an
 //      overflow list that only blocks with more arrivals scan)
 //   4. one CTA per block: a clean block copies its old segment in order (perm = the old
@@ -374,9 +374,10 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
         const BlockRec r = recs[q];
         const int cnt = r.end - r.start, s0 = r.start;
         uint16_t* ct = celltab + size_t(q) * kCellTab;
-        const int oq = is.rold[q];
-        if (oq >= 0) {  // clean: the old segment, in order
-            const int os0 = is.orecs[oq].start;
+        const int4 ro = is.rold[q];  // {clean, old list slot, old start, old end}
+        const int oq = ro.y;
+        if (ro.x) {  // clean: the old segment, in order
+            const int os0 = ro.z;
             for (int i = tid; i < cnt; i += kSortThreads) {
                 perm[s0 + i] = uint32_t(os0 + i);
                 is.okey_out[s0 + i] = is.okey_in[os0 + i];
@@ -386,8 +387,7 @@ __global__ void __launch_bounds__(kSortThreads) k_isort_blocks(Geom g, PBuf st, 
             continue;
         }
         // dirty: the stayers of the old segment + the arrivals, sorted
-        const int obm = is.oblockmap[r.block];
-        const int os0 = obm > 0 ? is.orecs[obm - 1].start : 0, oe = obm > 0 ? is.orecs[obm - 1].end : 0;
+        const int os0 = oq >= 0 ? ro.z : 0, oe = oq >= 0 ? ro.w : 0;
         const int na = is.acnt[r.block];
         const int nin = min(na, kInbox);
         const int nov = na > kInbox ? *is.novf : 0;  // more arrivals than the inbox: scan the overflow list
@@ -547,7 +547,8 @@ __global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, co
                                                              const int4* __restrict__ tile_sum, int* bstart,
                                                              int* nb_list, int* n_nb, BlockRec* recs, int* blockmap,
                                                              int* n_blocks, const int* __restrict__ oblockmap,
-                                                             int* rold, int* dirty) {
+                                                             const BlockRec* __restrict__ orecs, int4* rold,
+                                                             int* dirty) {
     pdl_wait();
     using Scan = cub::BlockScan<int4, kListThreads>;
     __shared__ typename Scan::TempStorage tmp;
@@ -597,7 +598,11 @@ __global__ void __launch_bounds__(kListThreads) k_list_write(Geom g, int cap, co
             if (slot) recs[slot - 1] = BlockRec{b, pre.x, pre.x + cnt[k]};
             blockmap[b] = slot;
             // incremental sort: a clean block copies its old segment (its previous list slot)
-            if (rold && slot) rold[slot - 1] = dirty[b] ? -1 : oblockmap[b] - 1;
+            if (rold && slot) {
+                const int oq = oblockmap[b] - 1;
+                const BlockRec o = oq >= 0 ? orecs[oq] : BlockRec{0, 0, 0};
+                rold[slot - 1] = make_int4(dirty[b] ? 0 : 1, oq, o.start, o.end);
+            }
         }
         if (dirty) dirty[b] = 0;
         pre.x += cnt[k];
@@ -622,7 +627,8 @@ void launch_sort_lists(const Geom& g, int cap, const int* bcount, const int* bhe
     launch_k(k_list_sums, dim3(tiles), dim3(kListThreads), 0, s, g, bcount, bheavy, nbflag, tile_sum,
              inc ? inc->nmov : nullptr, inc ? inc->novf : nullptr);
     launch_k(k_list_write, dim3(tiles), dim3(kListThreads), 0, s, g, cap, bcount, bheavy, nbflag, tile_sum, bstart,
-             nb_list, n_nb, recs, blockmap, n_blocks, inc ? inc->oblockmap : nullptr, inc ? inc->rold : nullptr,
+             nb_list, n_nb, recs, blockmap, n_blocks, inc ? inc->oblockmap : nullptr, inc ? inc->orecs : nullptr,
+             inc ? inc->rold : nullptr,
              inc ? inc->dirty : nullptr);
 }
 
