@@ -512,8 +512,14 @@ __global__ void __launch_bounds__(kAdjGridThreads, 1024 / kAdjGridThreads) k_adj
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = tid >> 6, l = tid & 63;
     const int lx = l >> 4, ly = (l >> 2) & 3, lz = l & 3;
-    for (int q = lane; q < kQ; q += 32) wacc[warp * kQ + q] = 0.0;
     const int n = *n_nb;
+    constexpr int kPer0 = kAdjGridThreads / 64;
+    if (int(blockIdx.x) * kPer0 >= n) {  // no node block for this CTA: its partial row is zero
+        for (int q = tid; q < (REP ? kQ : NE * kEffQ); q += kAdjGridThreads)
+            eff_partial[size_t(blockIdx.x) * pstride + q] = 0.0;
+        return;
+    }
+    for (int q = lane; q < kQ; q += 32) wacc[warp * kQ + q] = 0.0;
     constexpr int kPer = kAdjGridThreads / 64;
     for (int k = blockIdx.x * kPer + sub; k < n; k += gridDim.x * kPer) {
         const int nbid = nb_list[k];
