@@ -960,9 +960,25 @@ class WorkspacePool:
         return out
 
 
+def _replica_groups(population, R):
+    """The population in groups of a replica context's size (the last one padded with its last
+    candidate) and each group's real count."""
+    pop = list(population)
+    for i in range(0, len(pop), R):
+        grp = pop[i:i + R]
+        yield grp + [grp[-1]] * (R - len(grp)), len(grp)
+
+
 def rollout_loss_batch(scene: Scene, state0: SimState, population: Sequence[ActionTrajectory],
-                       loss: LossEvaluator, pool: WorkspacePool, window: int = 0) -> List[float]:
-    """rollout_loss (grad.hpp:15-41) for every action trajectory of a population."""
+                       loss: LossEvaluator, pool, window: int = 0) -> List[float]:
+    """rollout_loss (grad.hpp:15-41) for every action trajectory of a population, on a
+    WorkspacePool (concurrent contexts) or a ReplicaWorkspace (one launch per stage for a
+    group of its size; any population size)."""
+    if getattr(pool, "n_replicas", None):
+        out = []
+        for grp, n in _replica_groups(population, pool.n_replicas):
+            out += rollout_loss_replicas(scene, state0, grp, loss, pool, window=window)[:n]
+        return out
     states = [state0.copy() for _ in pool.workspaces]
     idx = {id(ws): i for i, ws in enumerate(pool.workspaces)}
     return pool._map(lambda ws, a: rollout_loss(scene, states[idx[id(ws)]], a, loss, window=window, ws=ws),
@@ -974,7 +990,9 @@ class ReplicaWorkspace(GpuWorkspace):
     (flume_ctx_create_replicas, the CMA-ES population of
     optimize.hpp:383-418): every kernel launch of a substep covers the whole population, so
     small scenes fill the GPU.  Positions stay replica-local and each replica's state
-    evolves bit-identically to a single context's.  Forward rollouts only."""
+    evolves bit-identically to a single context's.  rollout_loss_replicas /
+    grad_trajectory_replicas, or rollout_loss_batch / grad_trajectory_batch for populations
+    of any size."""
 
     def __init__(self, scene: Scene, n_replicas: int, device: int = 0):
         self.lib = load()
@@ -1084,9 +1102,15 @@ def grad_trajectory_replicas(scene: Scene, state0, population: Sequence[ActionTr
 
 
 def grad_trajectory_batch(scene: Scene, state0: SimState, population: Sequence[ActionTrajectory],
-                          loss: LossEvaluator, pool: WorkspacePool, stride: int = 0,
+                          loss: LossEvaluator, pool, stride: int = 0,
                           window: int = 0) -> List[TrajectoryGrad]:
-    """grad_trajectory (grad.hpp:61-134) for every action trajectory of a population."""
+    """grad_trajectory (grad.hpp:61-134) for every action trajectory of a population (a
+    WorkspacePool or a ReplicaWorkspace, as rollout_loss_batch)."""
+    if getattr(pool, "n_replicas", None):
+        out = []
+        for grp, n in _replica_groups(population, pool.n_replicas):
+            out += grad_trajectory_replicas(scene, state0, grp, loss, pool, stride=stride, window=window)[:n]
+        return out
     states = [state0.copy() for _ in pool.workspaces]
     idx = {id(ws): i for i, ws in enumerate(pool.workspaces)}
     return pool._map(lambda ws, a: grad_trajectory(scene, states[idx[id(ws)]], a, loss, stride=stride,

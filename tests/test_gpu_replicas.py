@@ -151,3 +151,25 @@ def test_replica_gradients_full_size_c4():
         scale = max(np.abs(g1.action_grad).max(), 1e-30)
         assert np.abs(gr[r].action_grad - g1.action_grad).max() <= 1e-9 * scale
     ws.close()
+
+
+def test_batch_api_on_a_replica_workspace():
+    """rollout_loss_batch / grad_trajectory_batch take a ReplicaWorkspace like a pool: a
+    population of 5 runs as groups of 2 (the last padded) with the single-context results."""
+    w = fl.build_scene(spec_for("c1", 32))
+    pop = _population(w, 5, 2, seed=7)
+    for a in pop:
+        a.segment_length = 4
+    loss = fl.LossEvaluator(w.scene, w.loss_spec, w.state)
+    rws = fl.ReplicaWorkspace(w.scene, 2)
+    lb = fl.rollout_loss_batch(w.scene, w.state, pop, loss, rws)
+    gb = fl.grad_trajectory_batch(w.scene, w.state, pop, loss, rws, stride=4)
+    rws.close()
+    ws = fl.GpuWorkspace(w.scene)
+    assert len(lb) == len(gb) == 5
+    for r in range(5):
+        l1 = fl.rollout_loss(w.scene, w.state, pop[r], loss, ws=ws)
+        g1 = fl.grad_trajectory(w.scene, w.state, pop[r], loss, stride=4, ws=ws)
+        assert abs(lb[r] - l1) <= 1e-12 * abs(l1) and abs(gb[r].loss - g1.loss) <= 1e-12 * abs(g1.loss)
+        assert np.abs(gb[r].action_grad - g1.action_grad).max() <= 1e-9 * max(np.abs(g1.action_grad).max(), 1e-30)
+    ws.close()
