@@ -27,7 +27,7 @@ static_assert(kScThreads >= 192 && kScThreads % 64 == 0, "scatter CTA: 64 cells 
 #define FL_LB_P2G 5
 #endif
 #ifndef FL_LB_G2P
-#define FL_LB_G2P 8
+#define FL_LB_G2P 7  // (8 capped it at 64 registers with spills; round-2 end: G2P 42.5 -> 40.6 us on c4)
 #endif
 #ifndef FL_LB_ADJG2P
 #define FL_LB_ADJG2P 4  // (256-thread CTAs: 64 registers)
