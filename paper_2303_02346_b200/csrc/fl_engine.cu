@@ -991,7 +991,7 @@ void Ctx::init(const flume_scene_desc* desc, int dev, int n_replicas) {
     if (nrep > 1) eff_blocks = std::min(eff_blocks, 4 * sm_count);  // rows of every replica's effectors
     eff_partial.alloc(size_t(kEffRing) * 2 * eff_blocks * eslots() * 18);  // (slabs: interior + edge rows)
 #ifndef FL_SORT_CTAS
-#define FL_SORT_CTAS 8
+#define FL_SORT_CTAS 16  // per-block sort CTAs per SM (round-2 end: 8 -> 16, c4 sort 29.2 -> 27.5 us)
 #endif
     grid_sort = sms * FL_SORT_CTAS;
 
