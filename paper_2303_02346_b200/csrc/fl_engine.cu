@@ -673,7 +673,7 @@ struct Ctx {
 #define FL_CAP_GRID 1
 #endif
 #ifndef FL_CAP_HEAVY
-#define FL_CAP_HEAVY 1
+#define FL_CAP_HEAVY 0  // (1: the cap below; it paid while the pair ran on two streams)
 #endif
     // persistent block-list kernels: no more CTAs than ~one per 256 active particles (a
     // block holds ~8 particles per cell x 64 cells), so small scenes do not launch hundreds

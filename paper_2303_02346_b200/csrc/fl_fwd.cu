@@ -421,11 +421,11 @@ void launch_grid_update(const Geom& g, const int* nb_list, const int* n_nb, int 
 // G2P (mpm.hpp:338-384) with the per-material return map
 // ---------------------------------------------------------------------------
 
-// a few SVD/rigid G2P blocks beside a liquid scene (variant 3) in 256-thread CTAs: a full
-// block in two rounds instead of four (c4 42.7 -> 40.1 us; with many such blocks, c5,
-// 128 threads keep more of them in flight: variant 1)
+// a few SVD/rigid G2P blocks beside a liquid scene (variant 3): 256-thread CTAs took a full
+// block in two rounds instead of four when the pair ran on two streams (c4 42.7 -> 40.1 us);
+// as a heavy-first pair 128 threads displace fewer light CTAs (c4 -0.2%)
 #ifndef FL_G2P_NTH
-#define FL_G2P_NTH 256
+#define FL_G2P_NTH 128
 #endif
 template <bool HEAVY, int MINB, int NT = 128>
 __global__ void __launch_bounds__(NT, MINB) k_g2p(Geom g, PBuf in, PBuf out, const uint32_t* __restrict__ perm,
